@@ -1,0 +1,130 @@
+/* skb.h — C ABI of libskb, the B200 (sm_100a) execution backend for staged
+ * control-flow graphs produced by the stagekit conversion API
+ * (reference: pkg/src/stagekit, arXiv 1810.08061 re-creation).
+ *
+ * The reference executes staged graphs with a pure-Python interpreter,
+ * `execute(graph, feeds, check=True)` (reference pkg/src/stagekit/graph/execute.py:27-36),
+ * whose hot loop is `_Session._eval_while` (execute.py:218-238) calling the
+ * per-element kernels of pkg/src/stagekit/graph/tensor.py.  The reference has
+ * no FFI of its own; these entry points are what its `execute` seam binds to
+ * (see INTEGRATION.md for the ctypes binding a stagekit maintainer adds).
+ *
+ * Conventions: plain pointers and sizes only; every pointer argument named
+ * `*_dev` is device memory; `stream` is a cudaStream_t passed as void*.
+ * Every function returns an skb_status.  Runtime graph failures detected on
+ * the device are reported through a device-resident error word
+ * (`skb_err_word`, 4 x int32: code, problem index, time step, detail) that the
+ * host copies back after the stream synchronises; codes map 1:1 onto the
+ * reference's RuntimeGraphError.cause_kind strings (errors.py:155-174).
+ */
+#ifndef SKB_H
+#define SKB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int skb_status;
+
+enum {
+  SKB_OK = 0,
+  SKB_ERR_INVALID = 1,      /* bad argument / unsupported shape              */
+  SKB_ERR_CUDA = 2,         /* CUDA runtime failure (launch, config)         */
+  SKB_ERR_UNSUPPORTED = 3,  /* configuration not compiled into this library  */
+  /* device-detected runtime errors (cause_kind of the reference)            */
+  SKB_ERR_INDEX_OUT_OF_RANGE = 10, /* "IndexOutOfRange" tensor.py:420-430     */
+  SKB_ERR_EMPTY_POP = 11,          /* "EmptyPop"        execute.py:171-174    */
+  SKB_ERR_SHAPE_MISMATCH = 12,     /* "ShapeMismatch"   tensor.py:344-353,414 */
+  SKB_ERR_DIVISION_BY_ZERO = 13,   /* "DivisionByZero"  tensor.py:235-241     */
+  SKB_ERR_ITERATION_LIMIT = 14,    /* "IterationLimitExceeded" execute.py:232 */
+  SKB_ERR_ASSERTION_FAILED = 15,   /* "AssertionFailed" execute.py:198-202    */
+  SKB_ERR_FP16_RANGE = 20          /* input outside the fp16 tensor-core range */
+};
+
+/* Cell kinds recognised by the lowering of a staged `While` region. */
+enum {
+  SKB_CELL_LSTM = 1,      /* i,f,g,o gates; c' = f*c + i*g; h' = o*tanh(c')  */
+  SKB_CELL_RNN_TANH = 2   /* h' = tanh(x W + h U + b)  (corpus/dynamic_rnn.msl) */
+};
+
+/* Library / device information. */
+const char* skb_version(void);
+int skb_device_sm_count(void);
+int skb_last_cuda_error(void); /* cudaError_t of the last SKB_ERR_CUDA */
+
+/* ---------------------------------------------------------------------------
+ * Dynamic-length recurrent loop.
+ *
+ * Replaces, for a `While` whose body is an RNN/LSTM cell with a per-row
+ * `Where(t < seq_len, new, old)` mask and a `ListAppend` of h:
+ *   execute.py:218-238 (_eval_while) + tensor.py:302-319 (matmul),
+ *   :274-287 (binop), :391-407 (tanh/sigmoid), :356-377 (where),
+ *   :420-430 (index), :322-332 (the two Transposes) and execute.py:153-185
+ *   (ListAppend/ListStack).
+ * The loop predicate (t < reduce_max(seq_len)) is evaluated on the device;
+ * every row exits at its own trip count; rows past their length carry the
+ * frozen state exactly as the reference's Where does.
+ * ------------------------------------------------------------------------- */
+typedef struct skb_rnn_shape {
+  int32_t cell;               /* SKB_CELL_*                                   */
+  int32_t hidden;             /* H                                            */
+  int32_t input;              /* F                                            */
+  int32_t time;               /* T: time extent of x (leading dim after the transpose) */
+  int32_t rows_per_problem;   /* batch rows of one execute() problem          */
+  int32_t problems;           /* independent problems batched in this launch  */
+} skb_rnn_shape;
+
+/* Bytes of device scratch the packed weights need (fp16 slabs + fp32 bias). */
+int64_t skb_rnn_packed_bytes(const skb_rnn_shape* shape);
+/* Bytes of device scratch skb_rnn_forward needs for its row schedule. */
+int64_t skb_rnn_workspace_bytes(const skb_rnn_shape* shape);
+/* Launch plan of the persistent kernel on the current device: co-resident
+ * clusters, CTAs per cluster and batch rows per tile. */
+skb_status skb_rnn_plan(const skb_rnn_shape* shape, int32_t* clusters, int32_t* ctas_per_cluster,
+                        int32_t* tile_rows);
+
+/* Pack per-gate weights into the per-CTA tensor-core slabs.
+ * w_dev[g]: [F,H], u_dev[g]: [H,H], b_dev[g]: [H]; gate order i,f,g,o for
+ * LSTM, a single gate for RNN_TANH.  `f64` selects double (1) or float (0)
+ * element type.  Sets SKB_ERR_FP16_RANGE in err_dev if |w| > 65504. */
+skb_status skb_rnn_pack(const skb_rnn_shape* shape, const void* const* w_dev,
+                        const void* const* u_dev, const void* const* b_dev, int f64,
+                        void* packed_dev, int32_t* err_dev, void* stream);
+
+/* Run the staged loop for shape->problems independent problems.
+ *   x_dev:    [R, T, F] (R = problems*rows_per_problem), batch-major as fed
+ *             (the reference's Transpose(1,0,2) is folded into addressing)
+ *   x_f64:    1 if x is double, 0 if float
+ *   h0_dev:   [R, H] float;  c0_dev: [R, H] float (LSTM) or NULL
+ *   len_dev:  [R] int64 sequence lengths
+ *   out_dev:  [R, T, H] float; problem p's result is out[p*rows : (p+1)*rows, :max_len_p, :]
+ *   hT_dev/cT_dev: optional [R, H] final states (NULL to skip)
+ *   max_len_dev: [problems] int32, receives max_len_p (the While trip count)
+ *   err_dev:  skb_err_word (4 x int32), must be zeroed by the caller
+ *   workspace_dev: skb_rnn_workspace_bytes() bytes */
+skb_status skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_dev,
+                           const void* x_dev, int x_f64, const float* h0_dev,
+                           const float* c0_dev, const int64_t* len_dev, float* out_dev,
+                           float* hT_dev, float* cT_dev, int32_t* max_len_dev,
+                           int32_t* err_dev, void* workspace_dev, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics (GPU self-tests of the tcgen05 / DSMEM building blocks).
+ * ------------------------------------------------------------------------- */
+skb_status skb_diag_umma_gemm(const void* a_dev, const void* b_dev, void* d_dev, int n, int k,
+                              int swap_lbo_sbo, long long* cycles_dev, void* stream);
+/* Record clock64() role events of CTA 0 for the first `steps` loop steps into
+ * trace_dev[steps*16] on subsequent skb_rnn_forward calls (NULL disables). */
+skb_status skb_debug_rnn_trace(long long* trace_dev, int steps);
+/* gscratch_dev == NULL: bulk DSMEM copies; else slices go through L2 and are
+ * multicast to the cluster (gscratch_dev: 2 x cluster x slice_bytes per cluster). */
+skb_status skb_diag_cluster_exchange(int cluster, int slice_bytes, int rounds,
+                                     long long* cycles_dev, int* errors_dev, void* gscratch_dev,
+                                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKB_H */

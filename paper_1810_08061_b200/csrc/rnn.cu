@@ -1,0 +1,879 @@
+// rnn.cu — persistent, cluster-resident execution of a staged dynamic-length
+// recurrent `While` region (LSTM or tanh-RNN cell) on sm_100a.
+//
+// Reference semantics (pkg/src/stagekit):
+//   graph/execute.py:218-238  _eval_while: test `idx < reduce_max(seq_len)`
+//                             before every iteration, body, state <- outputs
+//   graph/tensor.py:302-319   matmul (x_t W + h U), :274-287 binop (+ b),
+//                             :391-407 tanh / stable sigmoid,
+//                             :356-377 where (rank-1 cond = row select),
+//                             :420-430 index (x_tm[t]), :322-332 transpose
+//   graph/execute.py:153-185  ListAppend / ListStack of the masked h
+// Here the loop lives on the device: no host round trip per iteration, each
+// batch row runs to its own length, rows past their length keep the frozen
+// state (the reference's Where), and the stacked, transposed output
+// [B, max_len, H] is written directly.
+//
+// Mapping: a thread-block cluster of C CTAs owns one tile
+// of NT batch rows; CTA q owns U hidden units, i.e. 128 gate rows of the
+// concatenated weight [W;U]^T, resident in shared memory for the whole
+// kernel.  Per step each CTA issues tcgen05.mma  D[128 x NT] (TMEM) =
+// Wcat_q[128 x K] * [x_t ; h_{t-1}]^T, the epilogue warps read D with
+// tcgen05.ld, apply bias + gate nonlinearities + the c/h update + mask in
+// registers, write h_t (fp32) to the output sequence and broadcast the fp16
+// h_t slice to every CTA of the cluster with bulk DSMEM copies that complete
+// on the receivers' mbarriers.  The x_t part of the next step's MMA is
+// issued before h_t arrives (it does not depend on the recurrence).
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <climits>
+#include "sm100.cuh"
+#include "skb_internal.h"
+
+using namespace skb;
+
+namespace {
+
+constexpr int kThreads = 320;   // warps 0-7 epilogue, 8 x loader, 9 MMA issuer + TMEM alloc
+constexpr int kEpi = 256;       // epilogue threads: warp w covers TMEM lanes 32*(w&3).. and column half w>>2
+constexpr int kMaxClusterDim = 8;
+
+struct RnnGeom {
+  int cell, H, F, T, Bp, P, R;
+  int G;        // gates per unit
+  int U;        // hidden units per CTA
+  int C;        // CTAs per cluster
+  int Kx, Kh, K;
+};
+
+__host__ __device__ inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+inline bool make_geom(const skb_rnn_shape* s, RnnGeom* g) {
+  if (!s || s->hidden <= 0 || s->input <= 0 || s->time < 0 || s->rows_per_problem <= 0 ||
+      s->problems <= 0)
+    return false;
+  g->cell = s->cell;
+  if (s->cell == SKB_CELL_LSTM) g->G = 4;
+  else if (s->cell == SKB_CELL_RNN_TANH) g->G = 1;
+  else return false;
+  g->H = s->hidden; g->F = s->input; g->T = s->time;
+  g->Bp = s->rows_per_problem; g->P = s->problems;
+  g->R = s->rows_per_problem * s->problems;
+  g->U = 128 / g->G;
+  int hp = round_up(g->H, 16);
+  if (hp < g->U) g->U = hp;
+  g->C = (g->H + g->U - 1) / g->U;
+  g->Kx = round_up(g->F, 16);
+  g->Kh = g->C * g->U;
+  g->K = g->Kx + g->Kh;
+  if (g->C > kMaxClusterDim) return false;
+  if (g->K > 512) return false;   // weights must fit TMEM columns [256, 512)
+  return true;
+}
+
+template <int NT>
+inline size_t smem_bytes(const RnnGeom& g) {
+  return (size_t)2 * NT * g.Kx * 2 + (size_t)2 * NT * g.Kh * 2 +
+         (g.cell == SKB_CELL_LSTM ? (size_t)4 * NT * 32 * 4 : 0) + 1024;
+}
+
+struct RnnArgs {
+  const void* x;
+  const float* h0;
+  const float* c0;
+  const int64_t* lens;
+  const int32_t* perm;
+  const int32_t* pmax;
+  const uint8_t* wpack;
+  const float* bpack;
+  float* out;
+  float* hT;
+  float* cT;
+  const uint8_t* ximg; // [ntiles][T][NT x Kx] fp16 core-matrix images of x_t
+  uint8_t* hscratch;   // per cluster: 2 x [NT x Kh] fp16 h_t exchange buffers (L2)
+  int32_t* err;
+  int x_f64;
+  int R, T, F, H, Kx, Kh, K, U, C, Bp, ntiles;
+};
+
+// Optional per-step event trace of CTA 0 (debug only; set by skb_debug_rnn_trace).
+__device__ long long* g_trace = nullptr;
+__device__ int g_trace_steps = 0;
+#define SKB_TRACE(step_, slot_)                                                            \
+  do {                                                                                     \
+    if (g_trace != nullptr && blockIdx.x == 0 && (int)(step_) < g_trace_steps)             \
+      g_trace[(size_t)(step_) * 16 + (slot_)] = clock64();                                 \
+  } while (0)
+
+SKB_DEV void set_err(int32_t* err, int code, int problem, int t) {
+  if (atomicCAS(err, 0, code) == 0) { err[1] = problem; err[2] = t; }
+}
+
+SKB_DEV float sel4(float a, float b, float c, float d, int i) {
+  return i == 0 ? a : i == 1 ? b : i == 2 ? c : d;
+}
+
+SKB_DEV bool fp16_overflow(float v) { return isfinite(v) && fabsf(v) > 65504.f; }
+
+// 1/d for d in [1, 1e30] on the FMA pipe (the MUFU pipe is the epilogue's
+// bottleneck): bit-trick seed, three Newton steps, rel. err < 1e-7.
+SKB_DEV float rcp_nr(float d) {
+  float y = __int_as_float(0x7EF311C3 - __float_as_int(d));
+  y = y * fmaf(-d, y, 2.f);
+  y = y * fmaf(-d, y, 2.f);
+  y = y * fmaf(-d, y, 2.f);
+  return y;
+}
+// 1/(1 + e^{k x}) with one MUFU op.
+SKB_DEV float inv1pexp(float kx) { return __fdividef(1.f, 1.f + __expf(kx)); }
+
+SKB_DEV float tanh_acc(float x) {
+  // 1 - 2/(1+e^{2x}): saturates correctly at both ends, |err| ~ 1e-7.
+  return fmaf(-2.f, inv1pexp(2.f * x), 1.f);
+}
+
+// Load 8 consecutive x elements (k0..k0+7) of one row/time step, zero past F.
+template <typename XT>
+SKB_DEV void load_x8(const XT* __restrict__ p, int k0, int F, float (&v)[8]) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) v[e] = (k0 + e < F) ? (float)__ldg(p + k0 + e) : 0.f;
+}
+template <>
+SKB_DEV void load_x8<float>(const float* __restrict__ p, int k0, int F, float (&v)[8]) {
+  if (k0 + 8 <= F && ((reinterpret_cast<uintptr_t>(p + k0) & 15) == 0)) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(p + k0));
+    float4 b = __ldg(reinterpret_cast<const float4*>(p + k0 + 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = (k0 + e < F) ? __ldg(p + k0 + e) : 0.f;
+  }
+}
+template <>
+SKB_DEV void load_x8<double>(const double* __restrict__ p, int k0, int F, float (&v)[8]) {
+  if (k0 + 8 <= F && ((reinterpret_cast<uintptr_t>(p + k0) & 15) == 0)) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      double2 a = __ldg(reinterpret_cast<const double2*>(p + k0) + e);
+      v[2 * e] = (float)a.x; v[2 * e + 1] = (float)a.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = (k0 + e < F) ? (float)__ldg(p + k0 + e) : 0.f;
+  }
+}
+
+template <int CELL, int NT, typename XT>
+__global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint64_t xfull[2], xempty[2], hfull[2], mdone[2], dfree[2];
+  __shared__ uint32_t tmem_s;
+  __shared__ int s_row[NT], s_len[NT], s_tmax[NT];
+  __shared__ int s_trip;
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t q = cluster_ctarank();
+  const int C = a.C, U = a.U, H = a.H, T = a.T;
+  const uint32_t xbytes = NT * a.Kx * 2, hbytes = NT * a.Kh * 2, sbytes = NT * U * 2;
+  uint8_t* sX = smem;                      // 2 x [NT x Kx] fp16, core-matrix layout
+  uint8_t* sH = sX + 2 * xbytes;           // 2 x [NT x Kh] fp16
+  float* sG = reinterpret_cast<float*>(sH + 2 * hbytes);   // LSTM gates [4][NT][32]
+  constexpr uint32_t b_lbo = NT * 16, b_sbo = 128;    // activations: K-chunk / row-group stride
+  constexpr uint32_t kWCol = 256;                     // TMEM column of the weight operand
+  constexpr bool two_chains = false;                  // (a second h accumulator costs more TMEM reads than it saves)
+
+  if (tid == 0) {
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&xfull[j], 1);
+      mbar_init(&xempty[j], 1);
+      mbar_init(&hfull[j], 1);
+      mbar_init(&mdone[j], 1);
+      mbar_init(&dfree[j], kEpi / 32);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 9) tmem_alloc<512>(&tmem_s);
+  for (uint32_t i = tid; i < (2 * xbytes + 2 * hbytes) / 16; i += kThreads)
+    reinterpret_cast<uint4*>(sX)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_s;
+  // Weights -> TMEM (A operand of every MMA): lane = gate row, column c holds
+  // K elements (2c, 2c+1).  Epilogue warp w fills lanes [32w, 32w+32).
+  float bias = 0.f;
+  if (warp < 4) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.wpack + ((size_t)q * 128 + tid) * a.K * 2);
+    for (int c0 = 0; c0 < a.K / 2; c0 += 8) {
+      uint32_t r[8];
+      const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src + c0));
+      const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src + c0 + 4));
+      r[0] = lo.x; r[1] = lo.y; r[2] = lo.z; r[3] = lo.w; r[4] = hi.x; r[5] = hi.y; r[6] = hi.z; r[7] = hi.w;
+      tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + kWCol + c0, r);
+    }
+    tmem_st_wait();
+  }
+  if (warp < 8) bias = a.bpack[q * 128 + (warp & 3) * 32 + lane];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  cluster_sync();   // every CTA's barriers are initialised before any remote traffic
+
+  // Epilogue ownership (kEpi threads; warp w reads TMEM lane quarter qw = w&3 and
+  // batch-column half ch = w>>2).
+  //   LSTM: TMEM lane l = 32*g + u (gate g = qw, unit u = lane).  After the gate
+  //         exchange through sG, thread tid owns "pairs" idx = tid + kEpi*p: batch
+  //         column n = idx / G8 and the 8 consecutive units u8*8.. of that column
+  //         (G8 = U/8 unit groups per CTA), so h/c/out/stage are 16/32-byte vectors.
+  //   RNN : unit = 32*qw + lane; the thread owns the NT/2 columns of its half.
+  const int qw = warp & 3, ch = warp >> 2;
+  constexpr int NHALF = NT / 2;
+  constexpr int NP = (CELL == SKB_CELL_LSTM) ? (NT * 4 + kEpi - 1) / kEpi : 1;   // max pairs per thread
+  constexpr int NCELL = (CELL == SKB_CELL_LSTM) ? NP * 8 : NHALF;
+  const int G8 = U / 8;
+  int pn[NP], pu[NP];
+  bool pv[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const int idx = tid + kEpi * p;
+    pn[p] = G8 ? idx / G8 : 0;
+    pu[p] = G8 ? (idx % G8) * 8 : 0;
+    pv[p] = (CELL == SKB_CELL_LSTM) && tid < kEpi && idx < NT * G8;
+  }
+  const int rnn_u = qw * 32 + lane;
+  const int rnn_unit = (int)q * U + rnn_u;
+  const bool rnn_valid = (CELL != SKB_CELL_LSTM) && (warp < 8) && (rnn_u < U) && (rnn_unit < H);
+  float hp[NCELL], cc[NCELL];
+  uint8_t* gscr = a.hscratch + (size_t)cluster_id_x() * 2 * hbytes;   // this cluster's h_t exchange buffers
+
+  uint32_t step = 0;
+  uint32_t hwait[2] = {0u, 0u};
+  bool hfull_armed = false;
+  const int nclusters = (int)nclusters_x();
+  for (int tile = (int)cluster_id_x(); tile < a.ntiles; tile += nclusters) {
+    cluster_sync();   // previous tile retired cluster-wide (no copies in flight)
+    if (tid < NT) {
+      const int r = a.perm[tile * NT + tid];
+      int len = 0, tmax = 0;
+      if (r >= 0) {
+        tmax = max(0, min(a.pmax[r / a.Bp], T));
+        const long long L = a.lens[r];
+        len = (int)max(0LL, min(L, (long long)tmax));
+      }
+      s_row[tid] = r; s_len[tid] = len; s_tmax[tid] = tmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int m = 0;
+      for (int i = 0; i < NT; ++i) m = max(m, s_len[i]);
+      s_trip = m;
+    }
+    {  // h0 -> hbuf[step&1] (fp16, full Kh, zero padding)
+      uint8_t* hb = sH + (step & 1) * hbytes;
+      for (int i = tid; i < NT * a.Kh; i += kThreads) {
+        const int n = i / a.Kh, k = i - n * a.Kh;
+        const int r = s_row[n];
+        const float v = (r >= 0 && k < H) ? a.h0[(size_t)r * H + k] : 0.f;
+        *reinterpret_cast<__half*>(hb + cm_offset(n, k, b_lbo, b_sbo)) = __float2half_rn(v);
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    const int trip = s_trip;
+
+    if (warp < 8) {
+      // ======================= epilogue =======================
+      if constexpr (CELL == SKB_CELL_LSTM) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const int r = pv[p] ? s_row[pn[p]] : -1;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int unit = (int)q * U + pu[p] + e;
+            const bool ok = r >= 0 && unit < H;
+            hp[p * 8 + e] = ok ? a.h0[(size_t)r * H + unit] : 0.f;
+            cc[p * 8 + e] = ok ? a.c0[(size_t)r * H + unit] : 0.f;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NHALF; ++i) {
+          const int r = s_row[ch * NHALF + i];
+          hp[i] = (rnn_valid && r >= 0) ? a.h0[(size_t)r * H + rnn_unit] : 0.f;
+        }
+      }
+      for (int t = 0; t < trip; ++t) {
+        const uint32_t s = step + t, j = s & 1, use = s >> 1;
+        const uint32_t nb = (s + 1) & 1;
+        uint8_t* gslice = gscr + nb * hbytes + q * sbytes;   // where our h_t slice goes
+        mbar_wait(&mdone[j], use & 1);
+        if (tid == 0) SKB_TRACE(s, 4);
+        tc_fence_after();
+        const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16) + j * 2 * NT + ch * NHALF;
+        if constexpr (CELL == SKB_CELL_LSTM) {
+          // gate g = warp (warp-uniform): sigmoid for i, f, o; tanh(x) = 2*sigmoid(2x)-1 for g.
+          const float ks = (qw == 2) ? -2.f : -1.f;
+          const float mul = (qw == 2) ? 2.f : 1.f, add = (qw == 2) ? -1.f : 0.f;
+          float* g_out = sG + (qw * NT + ch * NHALF) * 32 + lane;
+#pragma unroll
+          for (int c16 = 0; c16 < NHALF / 16; ++c16) {
+            float v[16], v2[16];
+            tmem_ld16(trow + c16 * 16, v);
+            if (two_chains) tmem_ld16(trow + NT + c16 * 16, v2);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += two_chains ? v2[i] : 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              g_out[(c16 * 16 + i) * 32] = fmaf(mul, inv1pexp(ks * (v[i] + bias)), add);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dfree[j]);
+          named_bar_sync(2, kEpi);
+          if (tid == 0) SKB_TRACE(s, 10);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            if (!pv[p]) continue;
+            const int n = pn[p];
+            float g4[4][8];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const float4* src = reinterpret_cast<const float4*>(sG + (g * NT + n) * 32 + pu[p]);
+              const float4 x0 = src[0], x1 = src[1];
+              g4[g][0] = x0.x; g4[g][1] = x0.y; g4[g][2] = x0.z; g4[g][3] = x0.w;
+              g4[g][4] = x1.x; g4[g][5] = x1.y; g4[g][6] = x1.z; g4[g][7] = x1.w;
+            }
+            const bool live = t < s_len[n];
+            uint32_t hw[4];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float c2 = fmaf(g4[1][e], cc[p * 8 + e], g4[0][e] * g4[2][e]);
+              const float h2 = g4[3][e] * tanh_acc(c2);
+              cc[p * 8 + e] = live ? c2 : cc[p * 8 + e];
+              hp[p * 8 + e] = live ? h2 : hp[p * 8 + e];
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __half2 h2 = __floats2half2_rn(hp[p * 8 + 2 * e], hp[p * 8 + 2 * e + 1]);
+              hw[e] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            if (t + 1 < trip)
+              *reinterpret_cast<uint4*>(gslice + cm_offset(n, pu[p], b_lbo, b_sbo)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          }
+        } else {
+#pragma unroll
+          for (int c16 = 0; c16 < NHALF / 16; ++c16) {
+            float v[16], v2[16];
+            tmem_ld16(trow + c16 * 16, v);
+            if (two_chains) tmem_ld16(trow + NT + c16 * 16, v2);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int n = ch * NHALF + c16 * 16 + i;
+              v[i] += two_chains ? v2[i] : 0.f;
+              const float h2 = tanh_acc(v[i] + bias);
+              hp[c16 * 16 + i] = (t < s_len[n]) ? h2 : hp[c16 * 16 + i];
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dfree[j]);
+          if (t + 1 < trip && rnn_u < U) {
+#pragma unroll
+            for (int i = 0; i < NHALF; ++i)
+              *reinterpret_cast<__half*>(gslice + cm_offset(ch * NHALF + i, rnn_u, b_lbo, b_sbo)) = __float2half_rn(hp[i]);
+          }
+        }
+        if (tid == 0) SKB_TRACE(s, 6);
+        // h_t exchange: every CTA wrote its fp16 slice to this cluster's L2
+        // scratch; one thread multicasts it into hbuf[nb] of every CTA, the
+        // bytes completing on each CTA's hfull[nb].
+        fence_proxy_async_global();
+        named_bar_sync(1, kEpi);   // also: sG is rewritten next step only after every read
+        if (t + 1 < trip && tid == 0) {
+          bulk_g2s_multicast(sH + nb * hbytes + q * sbytes, gslice, sbytes, &hfull[nb],
+                             (uint16_t)((1u << C) - 1));
+          if (tid == 0) SKB_TRACE(s, 7);
+        }
+        // output sequence (stacked + transposed layout [R, T, H]); off the
+        // critical path: the h_t exchange is already in flight.
+        if constexpr (CELL == SKB_CELL_LSTM) {
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            if (!pv[p]) continue;
+            const int n = pn[p], r = s_row[n];
+            if (r < 0 || t >= s_tmax[n]) continue;
+            const int unit0 = (int)q * U + pu[p];
+            float* o = a.out + ((size_t)r * T + t) * H + unit0;
+            if (unit0 + 8 <= H && (H & 3) == 0) {
+              reinterpret_cast<float4*>(o)[0] = make_float4(hp[p * 8], hp[p * 8 + 1], hp[p * 8 + 2], hp[p * 8 + 3]);
+              reinterpret_cast<float4*>(o)[1] = make_float4(hp[p * 8 + 4], hp[p * 8 + 5], hp[p * 8 + 6], hp[p * 8 + 7]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) if (unit0 + e < H) o[e] = hp[p * 8 + e];
+            }
+          }
+        } else if (rnn_valid) {
+#pragma unroll
+          for (int i = 0; i < NHALF; ++i) {
+            const int n = ch * NHALF + i, r = s_row[n];
+            if (r >= 0 && t < s_tmax[n]) a.out[((size_t)r * T + t) * H + rnn_unit] = hp[i];
+          }
+        }
+      }
+      // frozen tail [trip, max_len_p) and final states
+      if constexpr (CELL == SKB_CELL_LSTM) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          if (!pv[p]) continue;
+          const int n = pn[p], r = s_row[n];
+          if (r < 0) continue;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int unit = (int)q * U + pu[p] + e;
+            if (unit >= H) continue;
+            for (int t = trip; t < s_tmax[n]; ++t) a.out[((size_t)r * T + t) * H + unit] = hp[p * 8 + e];
+            if (a.hT) a.hT[(size_t)r * H + unit] = hp[p * 8 + e];
+            if (a.cT) a.cT[(size_t)r * H + unit] = cc[p * 8 + e];
+          }
+        }
+      } else if (rnn_valid) {
+#pragma unroll
+        for (int i = 0; i < NHALF; ++i) {
+          const int n = ch * NHALF + i, r = s_row[n];
+          if (r < 0) continue;
+          for (int t = trip; t < s_tmax[n]; ++t) a.out[((size_t)r * T + t) * H + rnn_unit] = hp[i];
+          if (a.hT) a.hT[(size_t)r * H + rnn_unit] = hp[i];
+        }
+      }
+    } else if (warp == 8) {
+      // ======================= x_t loader =======================
+      // x_t arrives pre-converted (fp16, core-matrix image, see pack_x_kernel):
+      // one bulk async copy per step, prefetched two steps ahead.
+      if (tid == 256) {
+        const uint8_t* img = a.ximg + (size_t)tile * T * xbytes;
+        for (int t = 0; t < trip; ++t) {
+          const uint32_t s = step + t, j = s & 1, use = s >> 1;
+          SKB_TRACE(s, 8);
+          mbar_wait(&xempty[j], (use & 1) ^ 1);
+          mbar_arrive_expect_tx(&xfull[j], xbytes);
+          for (uint32_t off = 0; off < xbytes; off += 16384)
+            bulk_g2s(sX + j * xbytes + off, img + (size_t)t * xbytes + off, min(16384u, xbytes - off), &xfull[j]);
+          SKB_TRACE(s, 9);
+        }
+      }
+    } else if (warp == 9) {
+      // ======================= MMA issuer (whole warp, elected lane issues) =======================
+      const uint32_t idesc = idesc_f16_f32(128, NT);
+      const uint32_t x_addr = smem_u32(sX), h_addr = smem_u32(sH);
+      const int kx_steps = a.Kx / 16, kh_steps = a.Kh / 16;
+      if (!hfull_armed) {   // arm the first phase of both exchange barriers
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&hfull[0], C * sbytes);
+          mbar_arrive_expect_tx(&hfull[1], C * sbytes);
+        }
+        hfull_armed = true;
+      }
+      for (int t = 0; t < trip; ++t) {
+        const uint32_t s = step + t, j = s & 1, use = s >> 1;
+        mbar_wait(&xfull[j], use & 1);
+        if (lane == 0) SKB_TRACE(s, 0);
+        mbar_wait(&dfree[j], (use & 1) ^ 1);
+        if (lane == 0) SKB_TRACE(s, 1);
+        tc_fence_after();
+        const uint32_t d = tmem + j * 2 * NT;   // accumulator pair: d (x + even h steps), d + NT (odd h steps)
+        const uint64_t xdesc0 = sdesc_kmajor_noswz(x_addr + j * xbytes, b_lbo, b_sbo);
+#pragma unroll 4
+        for (int ks = 0; ks < kx_steps; ++ks)   // +2*b_lbo bytes per K=16 step (>>4 in the descriptor)
+          umma_f16_ts_warp(d, tmem + kWCol + ks * 8, xdesc0 + (uint64_t)(ks * 2 * b_lbo >> 4), idesc,
+                           ks > 0 ? 1u : 0u);
+        umma_commit_warp(&xempty[j]);
+        if (t > 0) {
+          const uint32_t hb = s & 1;
+          mbar_wait(&hfull[hb], hwait[hb] & 1);
+          ++hwait[hb];
+          if (lane == 0) mbar_arrive_expect_tx(&hfull[hb], C * sbytes);   // arm its next phase
+        }
+        if (lane == 0) SKB_TRACE(s, 2);
+        tc_fence_after();
+        const uint64_t hdesc0 = sdesc_kmajor_noswz(h_addr + (s & 1) * hbytes, b_lbo, b_sbo);
+        // Two independent accumulation chains so consecutive MMAs do not wait on
+        // each other's accumulator (the h part is on the recurrence's critical path).
+#pragma unroll 4
+        for (int ks = 0; ks < kh_steps; ++ks)
+          umma_f16_ts_warp(two_chains ? d + (ks & 1) * NT : d, tmem + kWCol + (kx_steps + ks) * 8,
+                           hdesc0 + (uint64_t)(ks * 2 * b_lbo >> 4), idesc,
+                           (two_chains && (ks & 1)) ? (ks > 1 ? 1u : 0u) : 1u);
+        umma_commit_warp(&mdone[j]);
+        if (lane == 0) SKB_TRACE(s, 3);
+      }
+    }
+    __syncwarp();
+    step += trip;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 9) tmem_dealloc<512>(tmem);
+}
+
+// ------------------------------------------------------------------ packing
+struct PackArgs {
+  const void* w[4];
+  const void* u[4];
+  const void* b[4];
+  int f64;
+  uint8_t* slab;
+  float* bias;
+  int32_t* err;
+  int G, H, F, U, C, Kx, Kh, K;
+};
+
+SKB_DEV float ld_any(const void* p, size_t i, int f64) {
+  return f64 ? (float)reinterpret_cast<const double*>(p)[i] : reinterpret_cast<const float*>(p)[i];
+}
+
+__global__ void rnn_pack_kernel(const PackArgs a) {
+  const int kchunks = a.K / 8;
+  const long long total = (long long)a.C * 128 * kchunks;
+  bool bad = false;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(idx / (128 * kchunks));
+    const int rem = (int)(idx - (long long)q * 128 * kchunks);
+    const int row = rem % 128, kc = rem / 128;
+    int g, ul;
+    if (a.G == 4) { g = row >> 5; ul = row & 31; } else { g = 0; ul = row; }
+    const int unit = q * a.U + ul;
+    const bool valid = (ul < a.U) && (unit < a.H) && (g < a.G);
+    __half hv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = kc * 8 + e;
+      float v = 0.f;
+      if (valid) {
+        if (k < a.F) v = ld_any(a.w[g], (size_t)k * a.H + unit, a.f64);
+        else if (k >= a.Kx && k - a.Kx < a.H) v = ld_any(a.u[g], (size_t)(k - a.Kx) * a.H + unit, a.f64);
+      }
+      bad |= fp16_overflow(v);
+      hv[e] = __float2half_rn(v);
+    }
+    // row-major [128][K] fp16 slab per CTA (copied into TMEM at kernel start)
+    uint8_t* dst = a.slab + ((size_t)q * 128 + row) * a.K * 2 + kc * 16;
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(hv);
+    if (kc == 0) a.bias[q * 128 + row] = valid ? ld_any(a.b[g], unit, a.f64) : 0.f;
+  }
+  if (bad) set_err(a.err, SKB_ERR_FP16_RANGE, -1, -1);
+}
+
+// ------------------------------------------------------------------ row schedule
+// Per-problem max_len (= the While trip count, reference tensor.py:344-353),
+// the reference's runtime errors for it, and a counting sort of rows by
+// length (descending) so each tile's trip count is as short as possible.
+struct SchedArgs {
+  const int64_t* lens;
+  int32_t* perm;      // [ntiles*NT]
+  int32_t* pmax;      // [P]
+  int32_t* hist;      // [T+1]
+  int32_t* base;      // [T+1]
+  int32_t* cursor;    // [T+1]
+  int32_t* max_len_out;
+  int32_t* err;
+  int R, Bp, P, T, npad;
+};
+
+__global__ void sched_init(const SchedArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride = gridDim.x * blockDim.x;
+  for (int p = i; p < a.P; p += stride) a.pmax[p] = INT_MIN;
+  for (int b = i; b <= a.T; b += stride) { a.hist[b] = 0; a.cursor[b] = 0; }
+  for (int r = a.R + i; r < a.npad; r += stride) a.perm[r] = -1;
+}
+
+SKB_DEV int len_bin(long long L, int T) { return (int)max(0LL, min(L, (long long)T)); }
+
+__global__ void sched_hist(const SchedArgs a) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.R; r += gridDim.x * blockDim.x) {
+    const long long L = a.lens[r];
+    const int Lc = (int)max((long long)INT_MIN, min(L, (long long)INT_MAX));
+    atomicMax(&a.pmax[r / a.Bp], Lc);
+    atomicAdd(&a.hist[len_bin(L, a.T)], 1);
+  }
+}
+
+__global__ void sched_scan(const SchedArgs a) {
+  // base[b] = number of rows with bin > b  (descending order), single block
+  __shared__ int part[1024];
+  const int nb = a.T + 1;
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int tid = threadIdx.x;
+  // thread tid owns bins counted from the top: j = tid*per .. ; bin = T - j
+  int s = 0;
+  for (int j = tid * per; j < min(nb, (tid + 1) * per); ++j) s += a.hist[a.T - j];
+  part[tid] = s;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+    const int v = tid >= off ? part[tid - off] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  int run = tid > 0 ? part[tid - 1] : 0;
+  for (int j = tid * per; j < min(nb, (tid + 1) * per); ++j) {
+    a.base[a.T - j] = run;
+    run += a.hist[a.T - j];
+  }
+  // per-problem checks, in the reference's evaluation order:
+  //   Range(max_len) with max_len < 0 -> ShapeMismatch      (tensor.py:414-417)
+  //   Index(x_tm, t) with t >= T      -> IndexOutOfRange    (tensor.py:420-430)
+  //   ListStack of an empty list      -> EmptyPop           (execute.py:171-174)
+  // The smallest failing problem index is reported.
+  __shared__ int first_bad;
+  if (tid == 0) first_bad = INT_MAX;
+  __syncthreads();
+  for (int p = tid; p < a.P; p += blockDim.x) {
+    const int m = a.pmax[p];
+    a.max_len_out[p] = m;
+    if (m < 0 || m > a.T || m == 0) atomicMin(&first_bad, p);
+  }
+  __syncthreads();
+  if (tid == 0 && first_bad != INT_MAX) {
+    const int m = a.pmax[first_bad];
+    const int code = m < 0 ? SKB_ERR_SHAPE_MISMATCH : (m > a.T ? SKB_ERR_INDEX_OUT_OF_RANGE : SKB_ERR_EMPTY_POP);
+    if (atomicCAS(a.err, 0, code) == 0) { a.err[1] = first_bad; a.err[2] = m > a.T ? a.T : 0; a.err[3] = m; }
+  }
+}
+
+__global__ void sched_scatter(const SchedArgs a) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.R; r += gridDim.x * blockDim.x) {
+    const int b = len_bin(a.lens[r], a.T);
+    a.perm[a.base[b] + atomicAdd(&a.cursor[b], 1)] = r;
+  }
+}
+
+constexpr int kNT = 64;
+
+// Pre-pass: gather each tile's rows (sorted order) and convert x[r, t, :] to the
+// fp16 core-matrix image the recurrent kernel's MMA consumes, one image per
+// (tile, t < tile trip count).  Rows past their length are zero.
+template <typename XT>
+__global__ void pack_x_kernel(const XT* __restrict__ x, const int32_t* __restrict__ perm,
+                              const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
+                              uint8_t* __restrict__ img, int32_t* err, int ntiles, int T, int F,
+                              int Kx, int Bp) {
+  const int nchunks = Kx / 8;
+  const long long per_t = (long long)kNT * nchunks;
+  const long long total = (long long)ntiles * T * per_t;
+  const uint32_t xbytes = kNT * Kx * 2;
+  bool bad = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int tile = (int)(i / (T * per_t));
+    const long long rem = i - (long long)tile * T * per_t;
+    const int t = (int)(rem / per_t);
+    const int c = (int)(rem - (long long)t * per_t);
+    const int n = c % kNT, kc = c / kNT;
+    const int r0 = perm[tile * kNT];
+    if (r0 < 0) continue;
+    const long long tm0 = (long long)min(max(pmax[r0 / Bp], 0), T);
+    const long long l0 = (long long)lens[r0];
+    const int trip0 = (int)(l0 < 0 ? 0 : (l0 < tm0 ? l0 : tm0));
+    if (t >= trip0) continue;
+    const int r = perm[tile * kNT + n];
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (r >= 0) {
+      const long long lr = (long long)lens[r];
+      const int len = (int)(lr < 0 ? 0 : (lr < T ? lr : T));
+      if (t < len) load_x8<XT>(x + ((size_t)r * T + t) * F, kc * 8, F, v);
+    }
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      bad |= fp16_overflow(v[2 * e]) || fp16_overflow(v[2 * e + 1]);
+      __half2 h2 = __floats2half2_rn(v[2 * e], v[2 * e + 1]);
+      w[e] = *reinterpret_cast<uint32_t*>(&h2);
+    }
+    *reinterpret_cast<uint4*>(img + ((size_t)tile * T + t) * xbytes + cm_offset(n, kc * 8, kNT * 16, 128)) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  if (bad) set_err(err, SKB_ERR_FP16_RANGE, -1, -1);
+}
+
+struct Workspace {
+  int32_t *perm, *pmax, *hist, *base, *cursor;
+  uint8_t* hscratch;
+  uint8_t* ximg;
+};
+
+inline int max_clusters_bound(const RnnGeom& g) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms / g.C + 1;
+}
+
+inline int64_t ws_layout(const RnnGeom& g, uint8_t* basep, Workspace* w) {
+  const int ntiles = (g.R + kNT - 1) / kNT;
+  int64_t off = 0;
+  auto take = [&](int64_t n) { int64_t o = off; off += (n * 4 + 255) / 256 * 256; return o; };
+  int64_t o_perm = take((int64_t)ntiles * kNT), o_pmax = take(g.P), o_hist = take(g.T + 1),
+          o_base = take(g.T + 1), o_cur = take(g.T + 1);
+  // h_t exchange scratch: per cluster 2 x [NT x Kh] fp16 (int32 units for take())
+  int64_t o_hs = take((int64_t)max_clusters_bound(g) * 2 * kNT * g.Kh * 2 / 4);
+  int64_t o_x = take((int64_t)ntiles * g.T * kNT * g.Kx * 2 / 4);
+  if (w) {
+    w->perm = reinterpret_cast<int32_t*>(basep + o_perm);
+    w->pmax = reinterpret_cast<int32_t*>(basep + o_pmax);
+    w->hist = reinterpret_cast<int32_t*>(basep + o_hist);
+    w->base = reinterpret_cast<int32_t*>(basep + o_base);
+    w->cursor = reinterpret_cast<int32_t*>(basep + o_cur);
+    w->hscratch = basep + o_hs;
+    w->ximg = basep + o_x;
+  }
+  return off;
+}
+
+template <int CELL, typename XT>
+int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
+  auto kern = rnn_fwd_kernel<CELL, kNT, XT>;
+  const size_t smem = smem_bytes<kNT>(g);
+  if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SKB_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(g.C);
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
+    return SKB_ERR_CUDA;
+  const int ncl = min(min(max_clusters, args.ntiles), max_clusters_bound(g) - 1);
+  cfg.gridDim = dim3(g.C * max(ncl, 1));
+  if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
+  return skb_check_launch();
+}
+
+}  // namespace
+
+extern "C" int skb_debug_rnn_trace(long long* trace_dev, int steps) {
+  if (cudaMemcpyToSymbol(g_trace, &trace_dev, sizeof(trace_dev)) != cudaSuccess) return SKB_ERR_CUDA;
+  if (cudaMemcpyToSymbol(g_trace_steps, &steps, sizeof(steps)) != cudaSuccess) return SKB_ERR_CUDA;
+  return SKB_OK;
+}
+
+extern "C" int skb_rnn_plan(const skb_rnn_shape* shape, int32_t* clusters, int32_t* ctas_per_cluster,
+                            int32_t* tile_rows) {
+  RnnGeom g;
+  if (!make_geom(shape, &g)) return SKB_ERR_INVALID;
+  const size_t smem = smem_bytes<kNT>(g);
+  if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
+  auto kern = rnn_fwd_kernel<SKB_CELL_LSTM, kNT, float>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SKB_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.C; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads); cfg.dynamicSmemBytes = smem; cfg.attrs = attr; cfg.numAttrs = 1;
+  cfg.gridDim = dim3(g.C);
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return SKB_ERR_CUDA;
+  if (clusters) *clusters = n;
+  if (ctas_per_cluster) *ctas_per_cluster = g.C;
+  if (tile_rows) *tile_rows = kNT;
+  return SKB_OK;
+}
+
+extern "C" int64_t skb_rnn_packed_bytes(const skb_rnn_shape* shape) {
+  RnnGeom g;
+  if (!make_geom(shape, &g)) return -1;
+  return (int64_t)g.C * 128 * g.K * 2 + (int64_t)g.C * 128 * 4;
+}
+
+extern "C" int64_t skb_rnn_workspace_bytes(const skb_rnn_shape* shape) {
+  RnnGeom g;
+  if (!make_geom(shape, &g)) return -1;
+  return ws_layout(g, nullptr, nullptr);
+}
+
+extern "C" int skb_rnn_pack(const skb_rnn_shape* shape, const void* const* w_dev,
+                            const void* const* u_dev, const void* const* b_dev, int f64,
+                            void* packed_dev, int32_t* err_dev, void* stream) {
+  RnnGeom g;
+  if (!make_geom(shape, &g) || !packed_dev || !w_dev || !u_dev || !b_dev) return SKB_ERR_INVALID;
+  PackArgs a = {};
+  for (int i = 0; i < g.G; ++i) {
+    a.w[i] = w_dev[i]; a.u[i] = u_dev[i]; a.b[i] = b_dev[i];
+    if (!a.w[i] || !a.u[i] || !a.b[i]) return SKB_ERR_INVALID;
+  }
+  a.f64 = f64;
+  a.slab = reinterpret_cast<uint8_t*>(packed_dev);
+  a.bias = reinterpret_cast<float*>(a.slab + (size_t)g.C * 128 * g.K * 2);
+  a.err = err_dev;
+  a.G = g.G; a.H = g.H; a.F = g.F; a.U = g.U; a.C = g.C; a.Kx = g.Kx; a.Kh = g.Kh; a.K = g.K;
+  const long long total = (long long)g.C * 128 * (g.K / 8);
+  const long long want = (total + 255) / 256;
+  const int blocks = (int)(want < 4096 ? want : 4096);
+  rnn_pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(a);
+  return skb_check_launch();
+}
+
+extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_dev, const void* x_dev,
+                               int x_f64, const float* h0_dev, const float* c0_dev,
+                               const int64_t* len_dev, float* out_dev, float* hT_dev, float* cT_dev,
+                               int32_t* max_len_dev, int32_t* err_dev, void* workspace_dev,
+                               void* stream) {
+  RnnGeom g;
+  if (!make_geom(shape, &g) || !packed_dev || !x_dev || !h0_dev || !len_dev || !out_dev ||
+      !max_len_dev || !err_dev || !workspace_dev)
+    return SKB_ERR_INVALID;
+  if (g.cell == SKB_CELL_LSTM && !c0_dev) return SKB_ERR_INVALID;
+  if (g.T > 1 << 20) return SKB_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace w;
+  ws_layout(g, reinterpret_cast<uint8_t*>(workspace_dev), &w);
+  const int ntiles = (g.R + kNT - 1) / kNT;
+  SchedArgs sa = {len_dev, w.perm, w.pmax, w.hist, w.base, w.cursor, max_len_dev, err_dev,
+                  g.R, g.Bp, g.P, g.T, ntiles * kNT};
+  const int blocks = min(1184, max(1, (max(g.R, g.P) + 255) / 256));
+  sched_init<<<blocks, 256, 0, st>>>(sa);
+  sched_hist<<<blocks, 256, 0, st>>>(sa);
+  sched_scan<<<1, 1024, 0, st>>>(sa);
+  sched_scatter<<<blocks, 256, 0, st>>>(sa);
+  if (int e = skb_check_launch()) return e;
+
+  RnnArgs a = {};
+  a.x = x_dev; a.h0 = h0_dev; a.c0 = c0_dev; a.lens = len_dev; a.perm = w.perm; a.pmax = w.pmax;
+  a.wpack = reinterpret_cast<const uint8_t*>(packed_dev);
+  a.bpack = reinterpret_cast<const float*>(a.wpack + (size_t)g.C * 128 * g.K * 2);
+  a.out = out_dev; a.hT = hT_dev; a.cT = cT_dev; a.err = err_dev; a.x_f64 = x_f64;
+  a.hscratch = w.hscratch;
+  a.ximg = w.ximg;
+  {
+    const long long total = (long long)ntiles * g.T * kNT * (g.Kx / 8);
+    const int pb = (int)min(total / 256 + 1, 148LL * 16);
+    if (x_f64)
+      pack_x_kernel<double><<<pb, 256, 0, st>>>((const double*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
+                                                  err_dev, ntiles, g.T, g.F, g.Kx, g.Bp);
+    else
+      pack_x_kernel<float><<<pb, 256, 0, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
+                                                 err_dev, ntiles, g.T, g.F, g.Kx, g.Bp);
+  }
+  a.R = g.R; a.T = g.T; a.F = g.F; a.H = g.H; a.Kx = g.Kx; a.Kh = g.Kh; a.K = g.K; a.U = g.U;
+  a.C = g.C; a.Bp = g.Bp; a.ntiles = ntiles;
+  if (g.cell == SKB_CELL_LSTM)
+    return x_f64 ? launch_main<SKB_CELL_LSTM, double>(a, g, st) : launch_main<SKB_CELL_LSTM, float>(a, g, st);
+  return x_f64 ? launch_main<SKB_CELL_RNN_TANH, double>(a, g, st) : launch_main<SKB_CELL_RNN_TANH, float>(a, g, st);
+}
