@@ -1,0 +1,143 @@
+"""Golden-fixture case table and deterministic feed generation (TEST
+INFRASTRUCTURE ONLY).
+
+`gen_golden.py` (run where /root/reference exists) traces each program with
+the reference's own `trace_module`, executes it with the reference's own
+`execute`, and writes tests/golden/<case>.json holding the traced graph (skb
+wire format), the feed specification and the reference's outputs (or its
+failure `cause_kind`).  Feeds are regenerated from the spec with numpy's
+PCG64 streams, identically on every machine, so fixtures stay small.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+GOLDEN = os.path.join(REPO, "tests", "golden")
+PROGRAMS = os.path.join(HERE, "programs")
+
+LSTM_PARAMS = ["input_data", "h0", "c0", "sequence_len"] + \
+    [f"{k}{g}" for g in "ifgo" for k in ("w", "u", "b")]
+RNN_PARAMS = ["input_data", "initial_state", "sequence_len", "w_x", "w_h", "b"]
+
+
+def lstm_case(name, B, T, F, H, lens, seed, program="lstm.msl", entry="dynamic_lstm", wscale=0.1,
+              xscale=1.0, note=""):
+    return {"name": name, "program": program, "entry": entry, "cell": "lstm",
+            "dims": {"B": B, "T": T, "F": F, "H": H}, "lens": lens, "seed": seed,
+            "wscale": wscale, "xscale": xscale, "note": note}
+
+
+def rnn_case(name, B, T, F, H, lens, seed, program="corpus:dynamic_rnn.msl", entry="dynamic_rnn",
+             wscale=1.0, xscale=1.0, note=""):
+    return {"name": name, "program": program, "entry": entry, "cell": "rnn",
+            "dims": {"B": B, "T": T, "F": F, "H": H}, "lens": lens, "seed": seed,
+            "wscale": wscale, "xscale": xscale, "note": note}
+
+
+# Parity cases: edge cases the reference's own tests and semantics pin
+# (SURVEY §8(c)), small enough for the pure-Python reference executor.
+CASES = [
+    rnn_case("rnn_corpus_2x3x4", 2, 3, 4, 4, [3, 1], 101,
+             note="corpus/dynamic_rnn.msl shapes and lengths (manifest.json:45-58)"),
+    rnn_case("rnn_accept_2x5x4", 2, 5, 4, 4, [3, 1], 1234,
+             note="acceptance criterion 3 shapes (test_acceptance.py:72-110), T longer than max_len"),
+    rnn_case("rnn_handwritten_2x3x4", 2, 3, 4, 4, [3, 1], 7, program="handwritten",
+             note="graph built by dispatch.while_stmt directly (tests/helpers.py:40-80)"),
+    rnn_case("rnn_32x16x64", 32, 16, 64, 64, "random", 11),
+    rnn_case("rnn_limit_ok", 3, 6, 4, 4, [4, 2, 1], 5, program="rnn_limited.msl",
+             note="max_iterations=4 directive, trip count 4: no failure"),
+    rnn_case("rnn_limit_hit", 3, 6, 4, 4, [5, 2, 1], 5, program="rnn_limited.msl",
+             note="max_iterations=4 with trip count 5 -> IterationLimitExceeded"),
+    lstm_case("lstm_4x8x8", 4, 8, 8, 8, [8, 3, 1, 6], 21, note="SURVEY §8(c) C1 pin shape"),
+    lstm_case("lstm_zero_len_rows", 3, 5, 8, 8, [5, 0, 2], 22, note="a row of length 0 keeps h0"),
+    lstm_case("lstm_all_full", 4, 4, 8, 8, [4, 4, 4, 4], 23),
+    lstm_case("lstm_ragged_12x20", 5, 6, 12, 20, [6, 1, 3, 6, 2], 24, note="F != H, H not a multiple of 16"),
+    lstm_case("lstm_32x16x64", 32, 16, 64, 64, "random", 25),
+    lstm_case("lstm_4x6x256", 4, 6, 256, 256, [6, 2, 5, 1], 26, note="C1 widths (H=F=256): full 8-CTA cluster"),
+    lstm_case("lstm_final_states", 3, 5, 8, 16, [5, 2, 3], 27, program="lstm_final.msl",
+              entry="dynamic_lstm_states", note="returns [stacked (time-major), h_T, c_T]"),
+    lstm_case("lstm_len_gt_T", 3, 4, 8, 8, [2, 6, 1], 28, note="len > T -> IndexOutOfRange"),
+    lstm_case("lstm_all_zero", 3, 4, 8, 8, [0, 0, 0], 29, note="max_len 0 -> EmptyPop"),
+    lstm_case("lstm_negative", 3, 4, 8, 8, [-1, -3, -2], 30, note="max_len < 0 -> ShapeMismatch (Range)"),
+    lstm_case("lstm_mixed_negative", 3, 4, 8, 8, [-2, 3, 0], 31, note="negative row is frozen at h0"),
+    lstm_case("lstm_large_inputs", 3, 5, 8, 8, [5, 4, 2], 32, xscale=100.0, wscale=0.5,
+              note="saturating gates"),
+]
+
+
+def case_by_name(name):
+    for c in CASES:
+        if c["name"] == name:
+            return c
+    raise KeyError(name)
+
+
+def param_names(case):
+    return LSTM_PARAMS if case["cell"] == "lstm" else RNN_PARAMS
+
+
+def make_feeds(case) -> dict:
+    """Deterministic numpy feeds for a case (float64 / int64)."""
+    d = case["dims"]
+    B, T, F, H = d["B"], d["T"], d["F"], d["H"]
+    rng = np.random.default_rng(case["seed"])
+    xs, ws = case["xscale"], case["wscale"]
+    feeds = {"input_data": rng.uniform(-xs, xs, (B, T, F))}
+    if case["lens"] == "random":
+        lens = rng.integers(1, T + 1, B)
+    else:
+        lens = np.asarray(case["lens"])
+    if case["cell"] == "lstm":
+        feeds["h0"] = rng.uniform(-0.1, 0.1, (B, H))
+        feeds["c0"] = rng.uniform(-0.1, 0.1, (B, H))
+        feeds["sequence_len"] = lens.astype(np.int64)
+        for g in "ifgo":
+            feeds["w" + g] = rng.uniform(-ws, ws, (F, H))
+            feeds["u" + g] = rng.uniform(-ws, ws, (H, H))
+            feeds["b" + g] = rng.uniform(-ws, ws, (H,))
+    else:
+        feeds["initial_state"] = rng.uniform(-1, 1, (B, H))
+        feeds["sequence_len"] = lens.astype(np.int64)
+        feeds["w_x"] = rng.uniform(-ws, ws, (F, H)) / np.sqrt(max(F, 1))
+        feeds["w_h"] = rng.uniform(-ws, ws, (H, H)) / np.sqrt(max(H, 1))
+        feeds["b"] = rng.uniform(-ws, ws, (H,))
+    return feeds
+
+
+def oracle_args(case, feeds):
+    """(cell, x, h0, c0, lens, W, U, b) for oracle.rnn_program."""
+    if case["cell"] == "lstm":
+        return (1, feeds["input_data"], feeds["h0"], feeds["c0"], feeds["sequence_len"],
+                [feeds["w" + g] for g in "ifgo"], [feeds["u" + g] for g in "ifgo"],
+                [feeds["b" + g] for g in "ifgo"])
+    return (2, feeds["input_data"], feeds["initial_state"], None, feeds["sequence_len"],
+            [feeds["w_x"]], [feeds["w_h"]], [feeds["b"]])
+
+
+def golden_path(name):
+    return os.path.join(GOLDEN, f"{name}.json")
+
+
+def load_golden(name) -> dict:
+    with open(golden_path(name)) as f:
+        return json.load(f)
+
+
+def load_graph_fixture(name="graph_lstm_c1"):
+    """(graph, case) of a graph-only fixture (traced program at benchmark size)."""
+    import sys
+    sys.path.insert(0, REPO)
+    from paper_1810_08061_b200 import ir
+    with open(os.path.join(GOLDEN, f"{name}.json")) as f:
+        doc = json.load(f)
+    return ir.from_json(doc["graph"]), doc["case"]
+
+
+def golden_names():
+    return [c["name"] for c in CASES if os.path.exists(golden_path(c["name"]))]

@@ -1,0 +1,342 @@
+"""`execute(graph, feeds)` — drop-in replacement for the reference CPU graph
+executor (reference pkg/src/stagekit/graph/execute.py:27-36) on the B200.
+
+Same signature and result shape: ``ExecutionResult(outputs, print_log)``;
+same feed binding errors (MissingFeed / DtypeMismatch / ShapeMismatch,
+execute.py:39-65); same runtime failures with the failing node's span and the
+reference ``cause_kind`` (IndexOutOfRange, EmptyPop, ShapeMismatch,
+IterationLimitExceeded).  ``execute_many`` runs many independent feed sets of
+one graph in a single device launch (throughput mode).
+
+The graph is lowered once per graph object (``lowering.py``) and cached; the
+packed weights are cached per weight-feed identity.  Everything numeric runs
+in libskb kernels; PyTorch only allocates device memory and moves bytes.
+"""
+
+from __future__ import annotations
+
+import threading
+import weakref
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import errors as E
+from .errors import IterationLimitExceeded, LoweringError, RuntimeGraphError
+from .lowering import CELL_LSTM, RnnProgram, lower_rnn_program
+from .validate import shapes_compatible, validate
+from .values import DeviceTensor, as_numpy, infer_dtype, shape_of
+
+
+@dataclass
+class ExecutionResult:
+    """reference execute.py:21-24"""
+    outputs: list
+    print_log: list = field(default_factory=list)
+
+
+class PrecisionRangeError(E.SkbError):
+    """A value exceeds the fp16 range of the tensor-core path (|v| > 65504)."""
+
+
+_plans: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_plans_lock = threading.Lock()
+
+
+def lower(graph) -> RnnProgram:
+    """Lowered program for `graph` (cached per graph object)."""
+    with _plans_lock:
+        plan = _plans.get(graph)
+    if plan is None:
+        plan = lower_rnn_program(graph)
+        with _plans_lock:
+            _plans[graph] = plan
+    return plan
+
+
+# ------------------------------------------------------------------ feeds
+def bind_feeds(graph, feeds: dict) -> dict:
+    """Check every main-frame parameter against its feed (reference
+    execute.py:39-65): missing -> MissingFeed, dtype -> DtypeMismatch,
+    incompatible declared shape -> ShapeMismatch."""
+    out = {}
+    for param in graph.main.params:
+        name = param.attrs.get("name")
+        if name not in feeds:
+            raise RuntimeGraphError(f"missing feed for parameter {name!r}", param.origin, E.MISSING_FEED)
+        value = feeds[name]
+        spec = param.out_types[0]
+        if spec.dtype == "tree":
+            raise LoweringError("tree-valued parameters have no device lowering yet")
+        dtype = infer_dtype(value)
+        if dtype != spec.dtype:
+            raise RuntimeGraphError(f"feed {name!r} has dtype {dtype}, parameter wants {spec.dtype}",
+                                    param.origin, E.DTYPE_MISMATCH)
+        shape = shape_of(value)
+        if spec.shape is not None and not shapes_compatible(tuple(spec.shape), shape):
+            raise RuntimeGraphError(f"feed {name!r} has shape {list(shape)}, parameter wants "
+                                    f"{_render(spec)}", param.origin, E.SHAPE_MISMATCH)
+        out[name] = value
+    return out
+
+
+def _render(spec) -> str:
+    return spec.render() if hasattr(spec, "render") else str(spec)
+
+
+def _source_value(src, feeds):
+    return feeds[src.name] if src.kind == "param" else src.value
+
+
+# ------------------------------------------------------------------ device plumbing
+def _torch():
+    import torch
+    return torch
+
+
+def _to_device(v, dtype, device, stream=None):
+    """Feed -> contiguous device tensor of `dtype` (zero-copy when it already is)."""
+    torch = _torch()
+    if isinstance(v, torch.Tensor):
+        t = v
+    elif isinstance(v, DeviceTensor):
+        t = v.tensor
+    else:
+        arr = np.ascontiguousarray(as_numpy(v))
+        t = torch.from_numpy(arr)
+    if t.device != device or t.dtype != dtype or not t.is_contiguous():
+        t = t.to(device=device, dtype=dtype, non_blocking=True).contiguous()
+    return t
+
+
+class _WeightCache:
+    """Packed tensor-core weight slabs, keyed by the identity of the weight
+    feeds (the objects are kept alive so identities stay valid)."""
+
+    def __init__(self, capacity: int = 8):
+        self.capacity = capacity
+        self.entries: list = []   # (key, keepalive, packed)
+        self.lock = threading.Lock()
+
+    def get(self, key):
+        with self.lock:
+            for k, keep, packed in self.entries:
+                if k == key:
+                    return packed
+        return None
+
+    def put(self, key, keep, packed):
+        with self.lock:
+            self.entries.append((key, keep, packed))
+            if len(self.entries) > self.capacity:
+                self.entries.pop(0)
+
+
+_weights = _WeightCache()
+
+
+class RnnExecutable:
+    """A lowered recurrent program bound to one weight set and problem shape:
+    owns the packed weights and device scratch so repeated launches allocate
+    nothing.  ``run`` is the device-resident hot path (inputs already in HBM)."""
+
+    def __init__(self, prog: RnnProgram, weights: list, B: int, T: int, F: int, H: int, P: int,
+                 device=None, stream=None):
+        from . import runtime as rt
+        torch = _torch()
+        self.rt = rt
+        self.lib = rt.lib()
+        self.prog = prog
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.B, self.T, self.F, self.H, self.P = B, T, F, H, P
+        self.shape = rt.RnnShape(prog.cell, H, F, T, B, P)
+        nb = self.lib.skb_rnn_packed_bytes(self.shape)
+        nw = self.lib.skb_rnn_workspace_bytes(self.shape)
+        if nb < 0 or nw < 0:
+            raise LoweringError(f"recurrent kernel does not support H={H}, F={F} (needs F+H <= 512 "
+                                f"after padding and H <= 256)")
+        self.packed = self._get_packed(weights, nb, stream)
+        self.ws = torch.empty(int(nw), dtype=torch.uint8, device=self.device)
+        self.err = torch.zeros(4, dtype=torch.int32, device=self.device)
+        self.max_len = torch.zeros(P, dtype=torch.int32, device=self.device)
+
+    def _get_packed(self, weights, nbytes, stream):
+        torch = _torch()
+        key = (self.prog.cell, self.H, self.F, tuple(id(w) for trip in weights for w in trip))
+        packed = _weights.get(key)
+        if packed is not None:
+            return packed
+        dev = [[_to_device(w, torch.float64, self.device) for w in trip] for trip in weights]
+        ws_ = [t[0] for t in dev] + [dev[0][0]] * (4 - len(dev))
+        us_ = [t[1] for t in dev] + [dev[0][1]] * (4 - len(dev))
+        bs_ = []
+        for t in dev:
+            b = t[2]
+            if b.dim() == 0:
+                b = b.expand(self.H).contiguous()
+            bs_.append(b.reshape(-1))
+        bs_ += [bs_[0]] * (4 - len(bs_))
+        P4 = self.rt._P4
+        packed = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        err = torch.zeros(4, dtype=torch.int32, device=self.device)
+        st = self.rt.stream_handle(stream)
+        self.rt.check(self.lib.skb_rnn_pack(
+            self.shape, P4(*[t.data_ptr() for t in ws_]), P4(*[t.data_ptr() for t in us_]),
+            P4(*[t.data_ptr() for t in bs_]), 1, self.rt.ptr(packed), self.rt.ptr(err), st), "skb_rnn_pack")
+        if int(err[0].item()) == E.SKB_ERR_FP16_RANGE:
+            raise PrecisionRangeError("a weight exceeds the fp16 range (|w| > 65504) of the tensor-core path")
+        _weights.put(key, weights, packed)
+        return packed
+
+    def run(self, x, h0, c0, lens, out, hT=None, cT=None, stream=None):
+        """Launch on device buffers (x: [R,T,F] f32/f64, h0/c0: [R,H] f32,
+        lens: [R] i64, out: [R,T,H] f32).  Asynchronous; returns nothing."""
+        torch = _torch()
+        rt = self.rt
+        self.err.zero_()
+        st = rt.stream_handle(stream)
+        rt.check(self.lib.skb_rnn_forward(
+            self.shape, rt.ptr(self.packed), rt.ptr(x), 1 if x.dtype == torch.float64 else 0,
+            rt.ptr(h0), rt.ptr(c0), rt.ptr(lens), rt.ptr(out), rt.ptr(hT), rt.ptr(cT),
+            rt.ptr(self.max_len), rt.ptr(self.err), rt.ptr(self.ws), st), "skb_rnn_forward")
+
+
+# ------------------------------------------------------------------ errors
+def classify(prog: RnnProgram, max_len: int, T: int):
+    """The reference's failure for a problem whose trip count is `max_len`,
+    in its evaluation order (Range, While limit, Index, ListStack)."""
+    if max_len < 0 and prog.range_node is not None:
+        return RuntimeGraphError(f"range of negative length {max_len}", prog.range_node.origin,
+                                 E.SHAPE_MISMATCH)
+    limit = prog.max_iterations
+    if limit is not None and max_len > limit and limit <= T:
+        return IterationLimitExceeded(f"loop exceeded max_iterations={limit}", prog.while_node.origin)
+    if max_len > T:
+        return RuntimeGraphError(f"index {T} out of range for leading dim {T}", prog.index_node.origin,
+                                 E.INDEX_OUT_OF_RANGE)
+    if max_len <= 0 and prog.stack_node is not None:
+        return RuntimeGraphError("stack of an empty list", prog.stack_node.origin, E.EMPTY_POP)
+    return None
+
+
+# ------------------------------------------------------------------ public API
+def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=None) -> ExecutionResult:
+    """Drop-in for the reference ``execute(graph, feeds, check=True)``."""
+    return execute_many(graph, [feeds or {}], check=check, stream=stream)[0]
+
+
+def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
+                 return_exceptions: bool = False) -> list:
+    """Run `graph` on P independent feed sets in one device launch.
+
+    Weight feeds must be the same objects (or equal) across the feed sets.
+    Raises the first problem's error unless ``return_exceptions`` (then the
+    failing entries of the returned list are the exception objects)."""
+    torch = _torch()
+    from . import runtime as rt
+    rt.lib()
+    if check:
+        validate(graph)
+    prog = lower(graph)
+    bound = [bind_feeds(graph, f or {}) for f in feeds_list]
+    P = len(bound)
+    if P == 0:
+        return []
+    f0 = bound[0]
+    xs = [_source_value(prog.x, b) for b in bound]
+    xshape = shape_of(xs[0])
+    if len(xshape) != 3:
+        raise RuntimeGraphError(f"x must be rank 3, got {list(xshape)}", prog.x.node.origin if prog.x.node else None,
+                                E.SHAPE_MISMATCH)
+    Bsz, T, F = xshape
+    for x in xs[1:]:
+        if shape_of(x) != xshape:
+            raise LoweringError("execute_many needs feed sets of one shape")
+    weights = [tuple(_source_value(s, f0) for s in trip) for trip in prog.gates]
+    for b in bound[1:]:
+        for trip_src, trip in zip(prog.gates, weights):
+            for s, w in zip(trip_src, trip):
+                v = _source_value(s, b)
+                if v is not w and not np.array_equal(as_numpy(v), as_numpy(w)):
+                    raise LoweringError("execute_many needs one weight set shared by all feed sets")
+    H = shape_of(weights[0][1])[0]
+    if Bsz == 0:
+        err = RuntimeGraphError("reduce_max of empty tensor", prog.reduce_node.origin, E.SHAPE_MISMATCH)
+        if return_exceptions:
+            return [err] * P
+        raise err
+    device = torch.device("cuda", torch.cuda.current_device())
+    exe = _executable(prog, weights, Bsz, T, F, H, P, device, stream)
+    R = Bsz * P
+
+    def cat(src, dtype):
+        vals = [_source_value(src, b) for b in bound]
+        if P == 1:
+            return _to_device(vals[0], dtype, device, stream)
+        if all(isinstance(v, torch.Tensor) and v.is_cuda for v in vals):
+            return torch.cat([v.to(dtype) for v in vals]).contiguous()
+        host = np.concatenate([np.ascontiguousarray(as_numpy(v)) for v in vals])
+        return _to_device(host, dtype, device, stream)
+
+    x32 = (isinstance(xs[0], torch.Tensor) and xs[0].dtype == torch.float32) or \
+          (isinstance(xs[0], np.ndarray) and xs[0].dtype == np.float32)
+    x_dtype = torch.float32 if x32 else torch.float64
+    x = cat(prog.x, x_dtype)
+    h0 = cat(prog.h0, torch.float32).reshape(R, H)
+    c0 = cat(prog.c0, torch.float32).reshape(R, H) if prog.cell == CELL_LSTM else None
+    lens = cat(prog.lens, torch.int64).reshape(R)
+    out = torch.empty((R, T, H), dtype=torch.float32, device=device)
+    want = {o.kind for o in prog.outputs}
+    hT = torch.empty((R, H), dtype=torch.float32, device=device) if "h_final" in want else None
+    cT = torch.empty((R, H), dtype=torch.float32, device=device) if "c_final" in want else None
+    if T > 0:
+        exe.run(x, h0, c0, lens, out, hT, cT, stream=stream)
+        status = exe.err.to("cpu")
+        max_len = exe.max_len.to("cpu").numpy()
+    else:
+        status = torch.zeros(4, dtype=torch.int32)
+        lv = as_numpy(lens.to("cpu")).reshape(P, Bsz)
+        max_len = lv.max(axis=1)
+    if int(status[0]) == E.SKB_ERR_FP16_RANGE:
+        raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
+    results = []
+    for p in range(P):
+        m = int(max_len[p])
+        err = classify(prog, m, T)
+        if err is not None:
+            if not return_exceptions:
+                raise err
+            results.append(err)
+            continue
+        rows = slice(p * Bsz, (p + 1) * Bsz)
+        outs = []
+        for o in prog.outputs:
+            if o.kind == "seq_bm":
+                outs.append(DeviceTensor("f64", out[rows, :m, :]))
+            elif o.kind == "seq_tm":
+                outs.append(DeviceTensor("f64", out[rows, :m, :].permute(1, 0, 2)))
+            elif o.kind == "h_final":
+                outs.append(DeviceTensor("f64", hT[rows]))
+            else:
+                outs.append(DeviceTensor("f64", cT[rows]))
+        results.append(ExecutionResult(outs, []))
+    return results
+
+
+_exes: dict = {}
+_exes_lock = threading.Lock()
+
+
+def _executable(prog, weights, B, T, F, H, P, device, stream) -> RnnExecutable:
+    key = (id(prog), B, T, F, H, P, tuple(id(w) for trip in weights for w in trip))
+    with _exes_lock:
+        hit = _exes.get(key)
+        if hit is not None and hit[0] is prog:
+            return hit[1]
+    exe = RnnExecutable(prog, weights, B, T, F, H, P, device, stream)
+    with _exes_lock:
+        if len(_exes) > 16:
+            _exes.clear()
+        _exes[key] = (prog, exe, weights)
+    return exe

@@ -1,0 +1,102 @@
+"""ctypes binding of libskb.so (include/skb.h) and device plumbing.
+
+PyTorch is used only for device allocation, streams and host<->device
+copies; every computation on the hot path is a libskb kernel.  The library is
+loaded from the package directory (built in-tree by ``build.py``); when it is
+missing, or no CUDA device is visible, ``lib()`` raises
+``BackendUnavailable`` — the executor never falls back to a CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import BackendUnavailable, DeviceError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libskb.so")
+
+SKB_OK = 0
+SKB_ERR_INVALID = 1
+SKB_ERR_CUDA = 2
+SKB_ERR_UNSUPPORTED = 3
+
+
+class RnnShape(ctypes.Structure):
+    """struct skb_rnn_shape (include/skb.h)"""
+    _fields_ = [("cell", ctypes.c_int32), ("hidden", ctypes.c_int32), ("input", ctypes.c_int32),
+                ("time", ctypes.c_int32), ("rows_per_problem", ctypes.c_int32),
+                ("problems", ctypes.c_int32)]
+
+
+_VP = ctypes.c_void_p
+_P4 = ctypes.c_void_p * 4
+
+# name -> (restype, argtypes): the complete exported surface of include/skb.h
+SIGNATURES = {
+    "skb_version": (ctypes.c_char_p, []),
+    "skb_device_sm_count": (ctypes.c_int, []),
+    "skb_last_cuda_error": (ctypes.c_int, []),
+    "skb_rnn_packed_bytes": (ctypes.c_int64, [ctypes.POINTER(RnnShape)]),
+    "skb_rnn_workspace_bytes": (ctypes.c_int64, [ctypes.POINTER(RnnShape)]),
+    "skb_rnn_plan": (ctypes.c_int, [ctypes.POINTER(RnnShape), ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
+    "skb_rnn_pack": (ctypes.c_int, [ctypes.POINTER(RnnShape), _P4, _P4, _P4, ctypes.c_int, _VP, _VP, _VP]),
+    "skb_rnn_forward": (ctypes.c_int, [ctypes.POINTER(RnnShape), _VP, _VP, ctypes.c_int, _VP, _VP, _VP,
+                                        _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "skb_debug_rnn_trace": (ctypes.c_int, [_VP, ctypes.c_int]),
+    "skb_diag_umma_gemm": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP]),
+    "skb_diag_cluster_exchange": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP, _VP, _VP]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libskb.so and bind every entry point (no CUDA device needed)."""
+    if not os.path.exists(path):
+        raise BackendUnavailable(
+            f"{path} is missing: build it with `python -m paper_1810_08061_b200.build`")
+    handle = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    return handle
+
+
+def lib() -> ctypes.CDLL:
+    """The bound library, after checking a CUDA device is present."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            import torch
+            if not torch.cuda.is_available():
+                raise BackendUnavailable("no CUDA device visible: the skb executor runs only on a B200 "
+                                         "(there is no CPU fallback)")
+            _lib = load_library()
+        return _lib
+
+
+def check(status: int, what: str):
+    if status == SKB_OK:
+        return
+    if status == SKB_ERR_CUDA:
+        code = lib().skb_last_cuda_error()
+        raise DeviceError(f"{what}: CUDA error {code}")
+    if status == SKB_ERR_UNSUPPORTED:
+        raise DeviceError(f"{what}: configuration not supported by this build of libskb")
+    raise DeviceError(f"{what}: invalid argument (status {status})")
+
+
+def ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def stream_handle(stream=None) -> ctypes.c_void_p:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)

@@ -1,0 +1,136 @@
+"""Parity of the B200 executor with the reference CPU executor.
+
+Every golden fixture (tests/golden/*.json, produced by oracle/gen_golden.py
+from the reference's own trace_module + execute) is replayed through
+``paper_1810_08061_b200.execute``: identical output shapes, trip counts and
+failure kinds (bit-exact), float outputs within the fp16-tensor-core bound
+
+    |gpu - ref| <= TOL * max(1, |gpu|, |ref|),   TOL = 3e-3
+
+(the reference's own allclose form, tensor.py:433-449; gate GEMMs take fp16
+operands with fp32 accumulation, cell state and activations are fp32).
+At the full C1 size, parity is checked against the float64 oracle on sampled
+problems, plus size-independent properties (frozen rows, batching
+invariance, device-feed zero-copy path)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import fixtures
+
+pytestmark = pytest.mark.gpu
+TOL = 3e-3
+
+
+def _run(doc, feeds=None):
+    from paper_1810_08061_b200 import execute, ir
+    g = ir.from_json(doc["graph"])
+    return g, execute(g, feeds or fixtures.make_feeds(doc["case"]))
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in fixtures.CASES])
+def test_golden_parity(name):
+    from paper_1810_08061_b200 import RuntimeGraphError, max_rel_error
+    doc = fixtures.load_golden(name)
+    exp = doc["expected"]
+    if "error" in exp:
+        with pytest.raises(RuntimeGraphError) as info:
+            _run(doc)
+        assert info.value.cause_kind == exp["error"]
+        span = info.value.span
+        assert [span.file, span.start_line, span.start_col] == exp["span"]
+        return
+    _, res = _run(doc)
+    assert res.print_log == exp["print_log"]
+    assert len(res.outputs) == len(exp["outputs"])
+    for got, ref in zip(res.outputs, exp["outputs"]):
+        assert got.dtype == ref["dtype"]
+        assert list(got.shape) == ref["shape"]
+        refa = np.asarray(ref["data"], dtype=np.float64).reshape(ref["shape"])
+        err = max_rel_error(got.array, refa)
+        assert err <= TOL, f"{name}: max rel err {err:.2e}"
+
+
+def test_golden_frozen_rows_bit_exact():
+    """Rows past their length repeat their last state exactly (reference Where)."""
+    doc = fixtures.load_golden("lstm_zero_len_rows")
+    feeds = fixtures.make_feeds(doc["case"])
+    _, res = _run(doc, feeds)
+    out = res.outputs[0].array
+    lens = feeds["sequence_len"]
+    for b, L in enumerate(lens):
+        tail = out[b, max(L, 1) - 1:] if L > 0 else out[b]
+        ref = out[b, L - 1] if L > 0 else np.asarray(feeds["h0"][b], dtype=np.float32).astype(np.float64)
+        assert np.array_equal(tail, np.broadcast_to(ref, tail.shape))
+
+
+def _c1_problems(P, seed=0, B=32, T=64, F=256, H=256):
+    rng = np.random.default_rng(seed)
+    shared = {}
+    for g in "ifgo":
+        shared["w" + g] = rng.uniform(-0.1, 0.1, (F, H))
+        shared["u" + g] = rng.uniform(-0.1, 0.1, (H, H))
+        shared["b" + g] = rng.uniform(-0.1, 0.1, (H,))
+    feeds = []
+    for p in range(P):
+        f = dict(shared)
+        f["input_data"] = rng.uniform(-1, 1, (B, T, F))
+        f["h0"] = rng.uniform(-0.1, 0.1, (B, H))
+        f["c0"] = rng.uniform(-0.1, 0.1, (B, H))
+        f["sequence_len"] = rng.integers(1, T + 1, B).astype(np.int64)
+        feeds.append(f)
+    return feeds
+
+
+@pytest.fixture(scope="module")
+def c1_graph():
+    """The LSTM program traced by the reference at C1 shapes (B=32, T=64, F=H=256)."""
+    g, _ = fixtures.load_graph_fixture("graph_lstm_c1")
+    return g
+
+
+def test_c1_full_size_against_oracle(c1_graph):
+    """C1 (B=32, T=64, F=H=256, random lengths) for 96 problems in one launch;
+    sampled problems checked against the float64 oracle."""
+    from paper_1810_08061_b200 import execute_many, max_rel_error
+    feeds = _c1_problems(96, seed=1)
+    res = execute_many(c1_graph, feeds)
+    for p in (0, 17, 95):
+        f = feeds[p]
+        ref, m = oracle.rnn_program(1, f["input_data"], f["h0"], f["c0"], f["sequence_len"],
+                                    [f["w" + g] for g in "ifgo"], [f["u" + g] for g in "ifgo"],
+                                    [f["b" + g] for g in "ifgo"])
+        got = res[p].outputs[0]
+        assert got.shape == (32, m, 256)
+        assert max_rel_error(got.array, ref) <= TOL
+
+
+def test_batching_invariance_bit_exact(c1_graph):
+    """A problem's result does not depend on which other problems share its launch."""
+    from paper_1810_08061_b200 import execute, execute_many
+    feeds = _c1_problems(5, seed=2)
+    many = execute_many(c1_graph, feeds)
+    one = execute(c1_graph, feeds[3])
+    assert np.array_equal(many[3].outputs[0].array, one.outputs[0].array)
+
+
+def test_device_feeds_zero_copy(c1_graph):
+    import torch
+    from paper_1810_08061_b200 import execute
+    f = _c1_problems(1, seed=3)[0]
+    host = execute(c1_graph, f).outputs[0].array
+    dev = {k: torch.tensor(v, device="cuda") for k, v in f.items()}
+    dev["input_data"] = dev["input_data"].float()
+    res = execute(c1_graph, dev).outputs[0]
+    assert res.tensor.is_cuda
+    assert np.allclose(res.array, host, rtol=0, atol=1e-6)
+
+
+def test_errors_per_problem(c1_graph):
+    from paper_1810_08061_b200 import RuntimeGraphError, execute_many
+    feeds = _c1_problems(3, seed=4)
+    feeds[1] = dict(feeds[1], sequence_len=np.full(32, 70, dtype=np.int64))   # > T
+    res = execute_many(c1_graph, feeds, return_exceptions=True)
+    assert isinstance(res[1], RuntimeGraphError) and res[1].cause_kind == "IndexOutOfRange"
+    assert not isinstance(res[0], Exception) and not isinstance(res[2], Exception)
