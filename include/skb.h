@@ -115,9 +115,17 @@ skb_status skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_dev,
  * ------------------------------------------------------------------------- */
 skb_status skb_diag_umma_gemm(const void* a_dev, const void* b_dev, void* d_dev, int n, int k,
                               int swap_lbo_sbo, long long* cycles_dev, void* stream);
+/* Kernel-only timing: for the next `max_launches` skb_rnn_forward calls the
+ * persistent recurrent kernel is bracketed by CUDA events on its stream;
+ * skb_profile_read returns how many were recorded and their durations (ms). */
+skb_status skb_profile_begin(int max_launches);
+int skb_profile_read(float* ms_out, int n);
+skb_status skb_profile_end(void);
 /* Record clock64() role events of CTA 0 for the first `steps` loop steps into
  * trace_dev[steps*16] on subsequent skb_rnn_forward calls (NULL disables). */
 skb_status skb_debug_rnn_trace(long long* trace_dev, int steps);
+/* Per-tile events of CTA 0 (setup start, loop start, loop end, trip count). */
+skb_status skb_debug_rnn_tile_trace(long long* trace_dev, int tiles);
 /* gscratch_dev == NULL: bulk DSMEM copies; else slices go through L2 and are
  * multicast to the cluster (gscratch_dev: 2 x cluster x slice_bytes per cluster). */
 skb_status skb_diag_cluster_exchange(int cluster, int slice_bytes, int rounds,

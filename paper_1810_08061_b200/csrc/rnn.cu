@@ -99,6 +99,13 @@ struct RnnArgs {
 // Optional per-step event trace of CTA 0 (debug only; set by skb_debug_rnn_trace).
 __device__ long long* g_trace = nullptr;
 __device__ int g_trace_steps = 0;
+__device__ long long* g_ttrace = nullptr;   // per-tile events of CTA 0: [tile_iter][4]
+__device__ int g_ttrace_n = 0;
+#define SKB_TTRACE(it_, slot_)                                                             \
+  do {                                                                                     \
+    if (g_ttrace != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && (it_) < g_ttrace_n)  \
+      g_ttrace[(size_t)(it_) * 4 + (slot_)] = clock64();                                   \
+  } while (0)
 #define SKB_TRACE(step_, slot_)                                                            \
   do {                                                                                     \
     if (g_trace != nullptr && blockIdx.x == 0 && (int)(step_) < g_trace_steps)             \
@@ -252,7 +259,9 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
   uint32_t hwait[2] = {0u, 0u};
   bool hfull_armed = false;
   const int nclusters = (int)nclusters_x();
-  for (int tile = (int)cluster_id_x(); tile < a.ntiles; tile += nclusters) {
+  int tile_iter = 0;
+  for (int tile = (int)cluster_id_x(); tile < a.ntiles; tile += nclusters, ++tile_iter) {
+    SKB_TTRACE(tile_iter, 0);
     cluster_sync();   // previous tile retired cluster-wide (no copies in flight)
     if (tid < NT) {
       const int r = a.perm[tile * NT + tid];
@@ -270,18 +279,44 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
       for (int i = 0; i < NT; ++i) m = max(m, s_len[i]);
       s_trip = m;
     }
-    {  // h0 -> hbuf[step&1] (fp16, full Kh, zero padding)
+    {  // h0 -> hbuf[step&1] (fp16, full Kh, zero padding); 8-element chunks, batched loads
       uint8_t* hb = sH + (step & 1) * hbytes;
-      for (int i = tid; i < NT * a.Kh; i += kThreads) {
-        const int n = i / a.Kh, k = i - n * a.Kh;
-        const int r = s_row[n];
-        const float v = (r >= 0 && k < H) ? a.h0[(size_t)r * H + k] : 0.f;
-        *reinterpret_cast<__half*>(hb + cm_offset(n, k, b_lbo, b_sbo)) = __float2half_rn(v);
+      const int kch = a.Kh / 8;
+      constexpr int kB = 4;
+      for (int i0 = tid; i0 < NT * kch; i0 += kThreads * kB) {
+        float v[kB][8];
+#pragma unroll
+        for (int m = 0; m < kB; ++m) {
+          const int i = i0 + m * kThreads;
+          const int n = i / kch, kc = i - n * kch;
+          const int r = (i < NT * kch) ? s_row[n] : -1;
+          if (r >= 0) load_x8<float>(a.h0 + (size_t)r * H, kc * 8, H, v[m]);
+          else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[m][e] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < kB; ++m) {
+          const int i = i0 + m * kThreads;
+          if (i >= NT * kch) continue;
+          const int n = i / kch, kc = i - n * kch;
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __half2 h2 = __floats2half2_rn(v[m][2 * e], v[m][2 * e + 1]);
+            w[e] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          *reinterpret_cast<uint4*>(hb + cm_offset(n, kc * 8, b_lbo, b_sbo)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
       }
     }
     fence_proxy_async_smem();
     __syncthreads();
     const int trip = s_trip;
+    SKB_TTRACE(tile_iter, 1);
+    if (threadIdx.x == 0 && g_ttrace != nullptr && blockIdx.x == 0 && tile_iter < g_ttrace_n)
+      g_ttrace[(size_t)tile_iter * 4 + 3] = trip;
 
     if (warp < 8) {
       // ======================= epilogue =======================
@@ -289,13 +324,17 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           const int r = pv[p] ? s_row[pn[p]] : -1;
+          const int unit0 = (int)q * U + pu[p];
+          float hv[8], cv[8];
+          if (r >= 0) {
+            load_x8<float>(a.h0 + (size_t)r * H, unit0, H, hv);
+            load_x8<float>(a.c0 + (size_t)r * H, unit0, H, cv);
+          } else {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int unit = (int)q * U + pu[p] + e;
-            const bool ok = r >= 0 && unit < H;
-            hp[p * 8 + e] = ok ? a.h0[(size_t)r * H + unit] : 0.f;
-            cc[p * 8 + e] = ok ? a.c0[(size_t)r * H + unit] : 0.f;
+            for (int e = 0; e < 8; ++e) hv[e] = cv[e] = 0.f;
           }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) { hp[p * 8 + e] = hv[e]; cc[p * 8 + e] = cv[e]; }
         }
       } else {
 #pragma unroll
@@ -406,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
           for (int p = 0; p < NP; ++p) {
             if (!pv[p]) continue;
             const int n = pn[p], r = s_row[n];
-            if (r < 0 || t >= s_tmax[n]) continue;
+            if (r < 0 || t >= s_len[n]) continue;   // frozen steps: rnn_fill_frozen_kernel
             const int unit0 = (int)q * U + pu[p];
             float* o = a.out + ((size_t)r * T + t) * H + unit0;
             if (unit0 + 8 <= H && (H & 3) == 0) {
@@ -421,11 +460,13 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
 #pragma unroll
           for (int i = 0; i < NHALF; ++i) {
             const int n = ch * NHALF + i, r = s_row[n];
-            if (r >= 0 && t < s_tmax[n]) a.out[((size_t)r * T + t) * H + rnn_unit] = hp[i];
+            if (r >= 0 && t < s_len[n]) a.out[((size_t)r * T + t) * H + rnn_unit] = hp[i];
           }
         }
       }
-      // frozen tail [trip, max_len_p) and final states
+      SKB_TTRACE(tile_iter, 2);
+      // final states (the frozen tail [len, max_len_p) of the output sequence is
+      // written by rnn_fill_frozen_kernel from hT, off the recurrence)
       if constexpr (CELL == SKB_CELL_LSTM) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -436,18 +477,15 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
           for (int e = 0; e < 8; ++e) {
             const int unit = (int)q * U + pu[p] + e;
             if (unit >= H) continue;
-            for (int t = trip; t < s_tmax[n]; ++t) a.out[((size_t)r * T + t) * H + unit] = hp[p * 8 + e];
-            if (a.hT) a.hT[(size_t)r * H + unit] = hp[p * 8 + e];
+            a.hT[(size_t)r * H + unit] = hp[p * 8 + e];
             if (a.cT) a.cT[(size_t)r * H + unit] = cc[p * 8 + e];
           }
         }
       } else if (rnn_valid) {
 #pragma unroll
         for (int i = 0; i < NHALF; ++i) {
-          const int n = ch * NHALF + i, r = s_row[n];
-          if (r < 0) continue;
-          for (int t = trip; t < s_tmax[n]; ++t) a.out[((size_t)r * T + t) * H + rnn_unit] = hp[i];
-          if (a.hT) a.hT[(size_t)r * H + rnn_unit] = hp[i];
+          const int r = s_row[ch * NHALF + i];
+          if (r >= 0) a.hT[(size_t)r * H + rnn_unit] = hp[i];
         }
       }
     } else if (warp == 8) {
@@ -708,6 +746,7 @@ struct Workspace {
   int32_t *perm, *pmax, *hist, *base, *cursor;
   uint8_t* hscratch;
   uint8_t* ximg;
+  float* hT;
 };
 
 inline int max_clusters_bound(const RnnGeom& g) {
@@ -725,6 +764,7 @@ inline int64_t ws_layout(const RnnGeom& g, uint8_t* basep, Workspace* w) {
   // h_t exchange scratch: per cluster 2 x [NT x Kh] fp16 (int32 units for take())
   int64_t o_hs = take((int64_t)max_clusters_bound(g) * 2 * kNT * g.Kh * 2 / 4);
   int64_t o_x = take((int64_t)ntiles * g.T * kNT * g.Kx * 2 / 4);
+  int64_t o_hT = take((int64_t)g.R * g.H);
   if (w) {
     w->perm = reinterpret_cast<int32_t*>(basep + o_perm);
     w->pmax = reinterpret_cast<int32_t*>(basep + o_pmax);
@@ -733,9 +773,53 @@ inline int64_t ws_layout(const RnnGeom& g, uint8_t* basep, Workspace* w) {
     w->cursor = reinterpret_cast<int32_t*>(basep + o_cur);
     w->hscratch = basep + o_hs;
     w->ximg = basep + o_x;
+    w->hT = reinterpret_cast<float*>(basep + o_hT);
   }
   return off;
 }
+
+// Rows past their length carry the frozen state (the reference's Where):
+// out[r, t, :] = hT[r, :] for len_r <= t < max_len_p.  Pure store stream.
+__global__ void rnn_fill_frozen_kernel(float* __restrict__ out, const float* __restrict__ hT,
+                                       const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
+                                       int R, int T, int H, int Bp) {
+  const int h4 = H / 4;
+  const long long total = (long long)R * T * h4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ((long long)T * h4));
+    const int rem = (int)(i - (long long)r * T * h4);
+    const int t = rem / h4, j = rem - t * h4;
+    const int tmax = min(max(pmax[r / Bp], 0), T);
+    const long long L = lens[r];
+    const int len = (int)(L < 0 ? 0 : (L < tmax ? L : tmax));
+    if (t < len || t >= tmax) continue;
+    reinterpret_cast<float4*>(out + ((size_t)r * T + t) * H)[j] = reinterpret_cast<const float4*>(hT + (size_t)r * H)[j];
+  }
+}
+
+__global__ void rnn_fill_frozen_scalar_kernel(float* __restrict__ out, const float* __restrict__ hT,
+                                              const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
+                                              int R, int T, int H, int Bp) {
+  const long long total = (long long)R * T * H;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ((long long)T * H));
+    const int rem = (int)(i - (long long)r * T * H);
+    const int t = rem / H, j = rem - t * H;
+    const int tmax = min(max(pmax[r / Bp], 0), T);
+    const long long L = lens[r];
+    const int len = (int)(L < 0 ? 0 : (L < tmax ? L : tmax));
+    if (t < len || t >= tmax) continue;
+    out[((size_t)r * T + t) * H + j] = hT[(size_t)r * H + j];
+  }
+}
+
+// Kernel-only timing of the persistent recurrent kernel (bench.py's roofline):
+// when armed, each launch is bracketed by a pair of CUDA events on its stream.
+constexpr int kProfMax = 256;
+cudaEvent_t g_prof_ev[2 * kProfMax];
+int g_prof_cap = 0, g_prof_n = 0;
 
 template <int CELL, typename XT>
 int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
@@ -761,11 +845,49 @@ int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
     return SKB_ERR_CUDA;
   const int ncl = min(min(max_clusters, args.ntiles), max_clusters_bound(g) - 1);
   cfg.gridDim = dim3(g.C * max(ncl, 1));
+  const bool prof = g_prof_n < g_prof_cap;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], stream);
   if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n++ + 1], stream);
   return skb_check_launch();
 }
 
 }  // namespace
+
+extern "C" int skb_profile_begin(int max_launches) {
+  if (max_launches < 0 || max_launches > kProfMax) return SKB_ERR_INVALID;
+  for (int i = g_prof_cap; i < max_launches; ++i) {
+    if (cudaEventCreate(&g_prof_ev[2 * i]) != cudaSuccess) return SKB_ERR_CUDA;
+    if (cudaEventCreate(&g_prof_ev[2 * i + 1]) != cudaSuccess) return SKB_ERR_CUDA;
+  }
+  if (max_launches > g_prof_cap) g_prof_cap = max_launches;
+  g_prof_n = 0;
+  return SKB_OK;
+}
+
+extern "C" int skb_profile_read(float* ms_out, int n) {
+  int m = g_prof_n < n ? g_prof_n : n;
+  for (int i = 0; i < m; ++i) {
+    if (cudaEventSynchronize(g_prof_ev[2 * i + 1]) != cudaSuccess) return -1;
+    if (cudaEventElapsedTime(&ms_out[i], g_prof_ev[2 * i], g_prof_ev[2 * i + 1]) != cudaSuccess) return -1;
+  }
+  g_prof_cap = g_prof_cap;  // events are kept for reuse
+  return m;
+}
+
+extern "C" int skb_profile_end(void) {
+  g_prof_n = 0;
+  const int cap = g_prof_cap;
+  g_prof_cap = 0;
+  for (int i = 0; i < cap; ++i) { cudaEventDestroy(g_prof_ev[2 * i]); cudaEventDestroy(g_prof_ev[2 * i + 1]); }
+  return SKB_OK;
+}
+
+extern "C" int skb_debug_rnn_tile_trace(long long* trace_dev, int tiles) {
+  if (cudaMemcpyToSymbol(g_ttrace, &trace_dev, sizeof(trace_dev)) != cudaSuccess) return SKB_ERR_CUDA;
+  if (cudaMemcpyToSymbol(g_ttrace_n, &tiles, sizeof(tiles)) != cudaSuccess) return SKB_ERR_CUDA;
+  return SKB_OK;
+}
 
 extern "C" int skb_debug_rnn_trace(long long* trace_dev, int steps) {
   if (cudaMemcpyToSymbol(g_trace, &trace_dev, sizeof(trace_dev)) != cudaSuccess) return SKB_ERR_CUDA;
@@ -858,7 +980,7 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   a.x = x_dev; a.h0 = h0_dev; a.c0 = c0_dev; a.lens = len_dev; a.perm = w.perm; a.pmax = w.pmax;
   a.wpack = reinterpret_cast<const uint8_t*>(packed_dev);
   a.bpack = reinterpret_cast<const float*>(a.wpack + (size_t)g.C * 128 * g.K * 2);
-  a.out = out_dev; a.hT = hT_dev; a.cT = cT_dev; a.err = err_dev; a.x_f64 = x_f64;
+  a.out = out_dev; a.hT = hT_dev ? hT_dev : w.hT; a.cT = cT_dev; a.err = err_dev; a.x_f64 = x_f64;
   a.hscratch = w.hscratch;
   a.ximg = w.ximg;
   {
@@ -873,7 +995,20 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   }
   a.R = g.R; a.T = g.T; a.F = g.F; a.H = g.H; a.Kx = g.Kx; a.Kh = g.Kh; a.K = g.K; a.U = g.U;
   a.C = g.C; a.Bp = g.Bp; a.ntiles = ntiles;
+  int rc;
   if (g.cell == SKB_CELL_LSTM)
-    return x_f64 ? launch_main<SKB_CELL_LSTM, double>(a, g, st) : launch_main<SKB_CELL_LSTM, float>(a, g, st);
-  return x_f64 ? launch_main<SKB_CELL_RNN_TANH, double>(a, g, st) : launch_main<SKB_CELL_RNN_TANH, float>(a, g, st);
+    rc = x_f64 ? launch_main<SKB_CELL_LSTM, double>(a, g, st) : launch_main<SKB_CELL_LSTM, float>(a, g, st);
+  else
+    rc = x_f64 ? launch_main<SKB_CELL_RNN_TANH, double>(a, g, st) : launch_main<SKB_CELL_RNN_TANH, float>(a, g, st);
+  if (rc) return rc;
+  {
+    const bool vec = (g.H % 4) == 0;
+    const long long total = (long long)g.R * g.T * (vec ? g.H / 4 : g.H);
+    const int fb = (int)min(total / 256 + 1, 148LL * 32);
+    if (vec)
+      rnn_fill_frozen_kernel<<<fb, 256, 0, st>>>(out_dev, a.hT, len_dev, w.pmax, g.R, g.T, g.H, g.Bp);
+    else
+      rnn_fill_frozen_scalar_kernel<<<fb, 256, 0, st>>>(out_dev, a.hT, len_dev, w.pmax, g.R, g.T, g.H, g.Bp);
+  }
+  return skb_check_launch();
 }

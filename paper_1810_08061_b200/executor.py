@@ -227,12 +227,15 @@ def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=N
 
 
 def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
-                 return_exceptions: bool = False) -> list:
+                 return_exceptions: bool = False, host_outputs: bool = False) -> list:
     """Run `graph` on P independent feed sets in one device launch.
 
     Weight feeds must be the same objects (or equal) across the feed sets.
     Raises the first problem's error unless ``return_exceptions`` (then the
-    failing entries of the returned list are the exception objects)."""
+    failing entries of the returned list are the exception objects).  With
+    ``host_outputs`` the whole output sequence buffer is copied to page-locked
+    host memory in one transfer (into ``host_outputs`` itself when it is a
+    float32 CPU tensor of R*T*H elements) and results are served from it."""
     torch = _torch()
     from . import runtime as rt
     rt.lib()
@@ -270,14 +273,34 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
     exe = _executable(prog, weights, Bsz, T, F, H, P, device, stream)
     R = Bsz * P
 
+    NPD = {torch.float32: np.float32, torch.float64: np.float64, torch.int64: np.int64}
+
     def cat(src, dtype):
+        """Stack the P feeds of one operand on the device.  CUDA feeds are used
+        in place (P == 1) or concatenated on the device; page-locked CPU
+        tensors are copied straight into their slice of the device buffer;
+        other host feeds go through a reused page-locked staging buffer."""
         vals = [_source_value(src, b) for b in bound]
-        if P == 1:
-            return _to_device(vals[0], dtype, device, stream)
         if all(isinstance(v, torch.Tensor) and v.is_cuda for v in vals):
+            if P == 1:
+                return _to_device(vals[0], dtype, device, stream)
             return torch.cat([v.to(dtype) for v in vals]).contiguous()
-        host = np.concatenate([np.ascontiguousarray(as_numpy(v)) for v in vals])
-        return _to_device(host, dtype, device, stream)
+        if all(isinstance(v, torch.Tensor) and v.is_pinned() and v.dtype == dtype for v in vals):
+            n0 = vals[0].shape[0] if vals[0].dim() else 1
+            dev = torch.empty((n0 * P,) + tuple(vals[0].shape[1:]), dtype=dtype, device=device)
+            for i, v in enumerate(vals):
+                dev[i * n0:(i + 1) * n0].copy_(v.reshape((n0,) + tuple(v.shape[1:])), non_blocking=True)
+            return dev
+        arrs = [as_numpy(v) for v in vals]
+        shape = (sum(a.shape[0] if a.ndim else 1 for a in arrs),) + tuple(arrs[0].shape[1:])
+        staging = _pinned(src.name or id(src), shape, dtype)
+        view = staging.numpy()
+        off = 0
+        for a in arrs:
+            n = a.shape[0] if a.ndim else 1
+            view[off:off + n] = a.astype(NPD[dtype], copy=False).reshape((n,) + shape[1:])
+            off += n
+        return staging.to(device, non_blocking=True)
 
     x32 = (isinstance(xs[0], torch.Tensor) and xs[0].dtype == torch.float32) or \
           (isinstance(xs[0], np.ndarray) and xs[0].dtype == np.float32)
@@ -300,6 +323,16 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
         max_len = lv.max(axis=1)
     if int(status[0]) == E.SKB_ERR_FP16_RANGE:
         raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
+    host_out = None
+    if host_outputs is not False and host_outputs is not None:
+        if isinstance(host_outputs, torch.Tensor):   # caller-owned page-locked buffer
+            host_out = host_outputs.view(out.shape)
+        else:
+            host_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        host_out.copy_(out)   # one D2H of the whole [R, T, H] sequence buffer
+        host_hT = hT.to("cpu") if hT is not None else None
+        host_cT = cT.to("cpu") if cT is not None else None
+        out, hT, cT = host_out, host_hT, host_cT
     results = []
     for p in range(P):
         m = int(max_len[p])
@@ -322,6 +355,24 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
                 outs.append(DeviceTensor("f64", cT[rows]))
         results.append(ExecutionResult(outs, []))
     return results
+
+
+_pinned_pool: dict = {}
+
+
+def _pinned(tag, shape, dtype):
+    """Reused page-locked staging buffers, one per operand (`tag`): execute_many
+    synchronises before returning, so a buffer is free again when the next
+    call starts, and distinct operands never share one in flight."""
+    torch = _torch()
+    key = (tag, tuple(shape), dtype, threading.get_ident())
+    buf = _pinned_pool.get(key)
+    if buf is None:
+        if len(_pinned_pool) > 32:
+            _pinned_pool.clear()
+        buf = torch.empty(shape, dtype=dtype, pin_memory=True)
+        _pinned_pool[key] = buf
+    return buf
 
 
 _exes: dict = {}

@@ -47,6 +47,10 @@ SIGNATURES = {
     "skb_rnn_forward": (ctypes.c_int, [ctypes.POINTER(RnnShape), _VP, _VP, ctypes.c_int, _VP, _VP, _VP,
                                         _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "skb_debug_rnn_trace": (ctypes.c_int, [_VP, ctypes.c_int]),
+    "skb_debug_rnn_tile_trace": (ctypes.c_int, [_VP, ctypes.c_int]),
+    "skb_profile_begin": (ctypes.c_int, [ctypes.c_int]),
+    "skb_profile_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float), ctypes.c_int]),
+    "skb_profile_end": (ctypes.c_int, []),
     "skb_diag_umma_gemm": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP]),
     "skb_diag_cluster_exchange": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP, _VP, _VP]),
 }
