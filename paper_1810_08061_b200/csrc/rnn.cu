@@ -700,44 +700,54 @@ constexpr int kNT = 64;
 // fp16 core-matrix image the recurrent kernel's MMA consumes, one image per
 // (tile, t < tile trip count).  Rows past their length are zero.
 template <typename XT>
-__global__ void pack_x_kernel(const XT* __restrict__ x, const int32_t* __restrict__ perm,
+__global__ void __launch_bounds__(256) pack_x_kernel(const XT* __restrict__ x, const int32_t* __restrict__ perm,
                               const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
                               uint8_t* __restrict__ img, int32_t* err, int ntiles, int T, int F,
                               int Kx, int Bp) {
-  const int nchunks = Kx / 8;
-  const long long per_t = (long long)kNT * nchunks;
-  const long long total = (long long)ntiles * T * per_t;
+  // One block per (tile, t) image; item = (n, kc) with n fastest, so a warp reads
+  // 32 rows x 32 B sectors and writes 512 contiguous bytes of image.  Row-steps
+  // past the row's length are skipped (their MMA columns are masked).
+  const int tile = blockIdx.x, t = blockIdx.y;
+  const int r0 = perm[tile * kNT];
+  if (r0 < 0) return;
+  const int tm0 = min(max(pmax[r0 / Bp], 0), T);
+  const long long L0 = lens[r0];
+  if (t >= (L0 < tm0 ? L0 : tm0)) return;
+  const int items = kNT * (Kx / 8);
   const uint32_t xbytes = kNT * Kx * 2;
+  uint8_t* dst0 = img + ((size_t)tile * T + t) * xbytes;
   bool bad = false;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int tile = (int)(i / (T * per_t));
-    const long long rem = i - (long long)tile * T * per_t;
-    const int t = (int)(rem / per_t);
-    const int c = (int)(rem - (long long)t * per_t);
-    const int n = c % kNT, kc = c / kNT;
-    const int r0 = perm[tile * kNT];
-    if (r0 < 0) continue;
-    const long long tm0 = (long long)min(max(pmax[r0 / Bp], 0), T);
-    const long long l0 = (long long)lens[r0];
-    const int trip0 = (int)(l0 < 0 ? 0 : (l0 < tm0 ? l0 : tm0));
-    if (t >= trip0) continue;
-    const int r = perm[tile * kNT + n];
-    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (r >= 0) {
-      const long long lr = (long long)lens[r];
-      const int len = (int)(lr < 0 ? 0 : (lr < T ? lr : T));
-      if (t < len) load_x8<XT>(x + ((size_t)r * T + t) * F, kc * 8, F, v);
-    }
-    uint32_t w[4];
+  constexpr int kB = 8;
+  for (int i0 = threadIdx.x; i0 < items; i0 += 256 * kB) {
+    float v[kB][8];
+    bool ok[kB];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      bad |= fp16_overflow(v[2 * e]) || fp16_overflow(v[2 * e + 1]);
-      __half2 h2 = __floats2half2_rn(v[2 * e], v[2 * e + 1]);
-      w[e] = *reinterpret_cast<uint32_t*>(&h2);
+    for (int m = 0; m < kB; ++m) {
+      const int i = i0 + m * 256;
+      const int n = i % kNT, kc = i / kNT;
+      ok[m] = false;
+      if (i < items) {
+        const int r = perm[tile * kNT + n];
+        if (r >= 0 && t < lens[r]) {
+          load_x8<XT>(x + ((size_t)r * T + t) * F, kc * 8, F, v[m]);
+          ok[m] = true;
+        }
+      }
     }
-    *reinterpret_cast<uint4*>(img + ((size_t)tile * T + t) * xbytes + cm_offset(n, kc * 8, kNT * 16, 128)) =
-        make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+    for (int m = 0; m < kB; ++m) {
+      if (!ok[m]) continue;
+      const int i = i0 + m * 256;
+      const int n = i % kNT, kc = i / kNT;
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        bad |= fp16_overflow(v[m][2 * e]) || fp16_overflow(v[m][2 * e + 1]);
+        __half2 h2 = __floats2half2_rn(v[m][2 * e], v[m][2 * e + 1]);
+        w[e] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+      *reinterpret_cast<uint4*>(dst0 + cm_offset(n, kc * 8, kNT * 16, 128)) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
   if (bad) set_err(err, SKB_ERR_FP16_RANGE, -1, -1);
 }
@@ -780,38 +790,29 @@ inline int64_t ws_layout(const RnnGeom& g, uint8_t* basep, Workspace* w) {
 
 // Rows past their length carry the frozen state (the reference's Where):
 // out[r, t, :] = hT[r, :] for len_r <= t < max_len_p.  Pure store stream.
-__global__ void rnn_fill_frozen_kernel(float* __restrict__ out, const float* __restrict__ hT,
+__global__ void __launch_bounds__(256) rnn_fill_frozen_kernel(float* __restrict__ out, const float* __restrict__ hT,
                                        const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
                                        int R, int T, int H, int Bp) {
-  const int h4 = H / 4;
-  const long long total = (long long)R * T * h4;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(i / ((long long)T * h4));
-    const int rem = (int)(i - (long long)r * T * h4);
-    const int t = rem / h4, j = rem - t * h4;
-    const int tmax = min(max(pmax[r / Bp], 0), T);
-    const long long L = lens[r];
-    const int len = (int)(L < 0 ? 0 : (L < tmax ? L : tmax));
-    if (t < len || t >= tmax) continue;
-    reinterpret_cast<float4*>(out + ((size_t)r * T + t) * H)[j] = reinterpret_cast<const float4*>(hT + (size_t)r * H)[j];
-  }
-}
-
-__global__ void rnn_fill_frozen_scalar_kernel(float* __restrict__ out, const float* __restrict__ hT,
-                                              const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
-                                              int R, int T, int H, int Bp) {
-  const long long total = (long long)R * T * H;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(i / ((long long)T * H));
-    const int rem = (int)(i - (long long)r * T * H);
-    const int t = rem / H, j = rem - t * H;
-    const int tmax = min(max(pmax[r / Bp], 0), T);
-    const long long L = lens[r];
-    const int len = (int)(L < 0 ? 0 : (L < tmax ? L : tmax));
-    if (t < len || t >= tmax) continue;
-    out[((size_t)r * T + t) * H + j] = hT[(size_t)r * H + j];
+  // one warp per row: out[r, t, :] = hT[r, :] for len_r <= t < max_len_p
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= R) return;
+  const int tmax = min(max(pmax[r / Bp], 0), T);
+  const long long L = lens[r];
+  const int len = (int)(L < 0 ? 0 : (L < tmax ? L : tmax));
+  if (len >= tmax) return;
+  float* orow = out + (size_t)r * T * H;
+  const float* hrow = hT + (size_t)r * H;
+  if ((H & 3) == 0) {
+    const int h4 = H / 4;
+    for (int j = lane; j < h4; j += 32) {
+      const float4 v = reinterpret_cast<const float4*>(hrow)[j];
+      for (int t = len; t < tmax; ++t) reinterpret_cast<float4*>(orow + (size_t)t * H)[j] = v;
+    }
+  } else {
+    for (int j = lane; j < H; j += 32) {
+      const float v = hrow[j];
+      for (int t = len; t < tmax; ++t) orow[(size_t)t * H + j] = v;
+    }
   }
 }
 
@@ -984,13 +985,12 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   a.hscratch = w.hscratch;
   a.ximg = w.ximg;
   {
-    const long long total = (long long)ntiles * g.T * kNT * (g.Kx / 8);
-    const int pb = (int)min(total / 256 + 1, 148LL * 16);
+    const dim3 pg(ntiles, g.T);
     if (x_f64)
-      pack_x_kernel<double><<<pb, 256, 0, st>>>((const double*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
+      pack_x_kernel<double><<<pg, 256, 0, st>>>((const double*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
                                                   err_dev, ntiles, g.T, g.F, g.Kx, g.Bp);
     else
-      pack_x_kernel<float><<<pb, 256, 0, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
+      pack_x_kernel<float><<<pg, 256, 0, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
                                                  err_dev, ntiles, g.T, g.F, g.Kx, g.Bp);
   }
   a.R = g.R; a.T = g.T; a.F = g.F; a.H = g.H; a.Kx = g.Kx; a.Kh = g.Kh; a.K = g.K; a.U = g.U;
@@ -1002,13 +1002,7 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
     rc = x_f64 ? launch_main<SKB_CELL_RNN_TANH, double>(a, g, st) : launch_main<SKB_CELL_RNN_TANH, float>(a, g, st);
   if (rc) return rc;
   {
-    const bool vec = (g.H % 4) == 0;
-    const long long total = (long long)g.R * g.T * (vec ? g.H / 4 : g.H);
-    const int fb = (int)min(total / 256 + 1, 148LL * 32);
-    if (vec)
-      rnn_fill_frozen_kernel<<<fb, 256, 0, st>>>(out_dev, a.hT, len_dev, w.pmax, g.R, g.T, g.H, g.Bp);
-    else
-      rnn_fill_frozen_scalar_kernel<<<fb, 256, 0, st>>>(out_dev, a.hT, len_dev, w.pmax, g.R, g.T, g.H, g.Bp);
+    rnn_fill_frozen_kernel<<<(g.R + 7) / 8, 256, 0, st>>>(out_dev, a.hT, len_dev, w.pmax, g.R, g.T, g.H, g.Bp);
   }
   return skb_check_launch();
 }
