@@ -19,6 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--use_fast_math", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v", "-I", os.path.join(REPO, "include")]
+if os.environ.get("SKB_TRACE") == "1":   # clock64 role-event tracing (tools/trace_c1.py)
+    FLAGS.append("-DSKB_TRACE_ENABLED")
 
 
 def sources() -> list[str]:

@@ -37,6 +37,7 @@ namespace {
 constexpr int kThreads = 320;   // warps 0-7 epilogue, 8 x loader, 9 MMA issuer + TMEM alloc
 constexpr int kEpi = 256;       // epilogue threads: warp w covers TMEM lanes 32*(w&3).. and column half w>>2
 constexpr int kMaxClusterDim = 8;
+constexpr int kGS = 36;   // sG row stride (floats): 32 units + 4 pad, conflict-free LDS.128
 
 struct RnnGeom {
   int cell, H, F, T, Bp, P, R;
@@ -74,7 +75,7 @@ inline bool make_geom(const skb_rnn_shape* s, RnnGeom* g) {
 template <int NT>
 inline size_t smem_bytes(const RnnGeom& g) {
   return (size_t)2 * NT * g.Kx * 2 + (size_t)2 * NT * g.Kh * 2 +
-         (g.cell == SKB_CELL_LSTM ? (size_t)4 * NT * 32 * 4 : 0) + 1024;
+         (g.cell == SKB_CELL_LSTM ? (size_t)4 * NT * kGS * 4 : 0) + 1024;
 }
 
 struct RnnArgs {
@@ -99,6 +100,7 @@ struct RnnArgs {
 // Optional per-step event trace of CTA 0 (debug only; set by skb_debug_rnn_trace).
 __device__ long long* g_trace = nullptr;
 __device__ int g_trace_steps = 0;
+#ifdef SKB_TRACE_ENABLED
 __device__ long long* g_ttrace = nullptr;   // per-tile events of CTA 0: [tile_iter][4]
 __device__ int g_ttrace_n = 0;
 #define SKB_TTRACE(it_, slot_)                                                             \
@@ -111,6 +113,10 @@ __device__ int g_ttrace_n = 0;
     if (g_trace != nullptr && blockIdx.x == 0 && (int)(step_) < g_trace_steps)             \
       g_trace[(size_t)(step_) * 16 + (slot_)] = clock64();                                 \
   } while (0)
+#else   // production build: trace points compile to nothing
+#define SKB_TTRACE(it_, slot_) do {} while (0)
+#define SKB_TRACE(step_, slot_) do {} while (0)
+#endif
 
 SKB_DEV void set_err(int32_t* err, int code, int problem, int t) {
   if (atomicCAS(err, 0, code) == 0) { err[1] = problem; err[2] = t; }
@@ -131,12 +137,19 @@ SKB_DEV float rcp_nr(float d) {
   y = y * fmaf(-d, y, 2.f);
   return y;
 }
-// 1/(1 + e^{k x}) with one MUFU op.
-SKB_DEV float inv1pexp(float kx) { return __fdividef(1.f, 1.f + __expf(kx)); }
+SKB_DEV float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 1/(1 + 2^a): one MUFU op (ex2) + the reciprocal on the FMA pipe.
+SKB_DEV float inv1pexp2(float a) { return rcp_nr(1.f + fminf(ex2_approx(a), 1e30f)); }
+// 1/(1 + e^{k x}) (kept for the RNN path)
+SKB_DEV float inv1pexp(float kx) { return inv1pexp2(kx * 1.4426950408889634f); }
 
 SKB_DEV float tanh_acc(float x) {
   // 1 - 2/(1+e^{2x}): saturates correctly at both ends, |err| ~ 1e-7.
-  return fmaf(-2.f, inv1pexp(2.f * x), 1.f);
+  return fmaf(-2.f, inv1pexp2(x * 2.8853900817779268f), 1.f);
 }
 
 // Load 8 consecutive x elements (k0..k0+7) of one row/time step, zero past F.
@@ -178,14 +191,14 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
   __shared__ int s_row[NT], s_len[NT], s_tmax[NT];
   __shared__ int s_trip;
 
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw;   // (no pointer re-alignment: keeps the shared address space visible to the compiler)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t q = cluster_ctarank();
   const int C = a.C, U = a.U, H = a.H, T = a.T;
   const uint32_t xbytes = NT * a.Kx * 2, hbytes = NT * a.Kh * 2, sbytes = NT * U * 2;
   uint8_t* sX = smem;                      // 2 x [NT x Kx] fp16, core-matrix layout
   uint8_t* sH = sX + 2 * xbytes;           // 2 x [NT x Kh] fp16
-  float* sG = reinterpret_cast<float*>(sH + 2 * hbytes);   // LSTM gates [4][NT][32]
+  float* sG = reinterpret_cast<float*>(sH + 2 * hbytes);   // LSTM gates [4][NT][kGS] (padded rows)
   constexpr uint32_t b_lbo = NT * 16, b_sbo = 128;    // activations: K-chunk / row-group stride
   constexpr uint32_t kWCol = 256;                     // TMEM column of the weight operand
   constexpr bool two_chains = false;                  // (a second h accumulator costs more TMEM reads than it saves)
@@ -315,8 +328,10 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
     __syncthreads();
     const int trip = s_trip;
     SKB_TTRACE(tile_iter, 1);
+#ifdef SKB_TRACE_ENABLED
     if (threadIdx.x == 0 && g_ttrace != nullptr && blockIdx.x == 0 && tile_iter < g_ttrace_n)
       g_ttrace[(size_t)tile_iter * 4 + 3] = trip;
+#endif
 
     if (warp < 8) {
       // ======================= epilogue =======================
@@ -353,9 +368,11 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
         const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16) + j * 2 * NT + ch * NHALF;
         if constexpr (CELL == SKB_CELL_LSTM) {
           // gate g = warp (warp-uniform): sigmoid for i, f, o; tanh(x) = 2*sigmoid(2x)-1 for g.
-          const float ks = (qw == 2) ? -2.f : -1.f;
+          // act = mul / (1 + 2^(kl*z + kb)) + add, z = pre-activation without bias
+          const float kl = (qw == 2) ? -2.8853900817779268f : -1.4426950408889634f;
+          const float kb = kl * bias;
           const float mul = (qw == 2) ? 2.f : 1.f, add = (qw == 2) ? -1.f : 0.f;
-          float* g_out = sG + (qw * NT + ch * NHALF) * 32 + lane;
+          float* g_out = sG + (qw * NT + ch * NHALF) * kGS + lane;
 #pragma unroll
           for (int c16 = 0; c16 < NHALF / 16; ++c16) {
             float v[16], v2[16];
@@ -366,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
             for (int i = 0; i < 16; ++i) v[i] += two_chains ? v2[i] : 0.f;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              g_out[(c16 * 16 + i) * 32] = fmaf(mul, inv1pexp(ks * (v[i] + bias)), add);
+              g_out[(c16 * 16 + i) * kGS] = fmaf(mul, inv1pexp2(fmaf(v[i], kl, kb)), add);
             }
           }
           tc_fence_before();
@@ -381,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
             float g4[4][8];
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
-              const float4* src = reinterpret_cast<const float4*>(sG + (g * NT + n) * 32 + pu[p]);
+              const float4* src = reinterpret_cast<const float4*>(sG + (g * NT + n) * kGS + pu[p]);
               const float4 x0 = src[0], x1 = src[1];
               g4[g][0] = x0.x; g4[g][1] = x0.y; g4[g][2] = x0.z; g4[g][3] = x0.w;
               g4[g][4] = x1.x; g4[g][5] = x1.y; g4[g][6] = x1.z; g4[g][7] = x1.w;
@@ -885,14 +902,22 @@ extern "C" int skb_profile_end(void) {
 }
 
 extern "C" int skb_debug_rnn_tile_trace(long long* trace_dev, int tiles) {
+#ifndef SKB_TRACE_ENABLED
+  return trace_dev ? SKB_ERR_UNSUPPORTED : SKB_OK;   // build with SKB_TRACE=1
+#else
   if (cudaMemcpyToSymbol(g_ttrace, &trace_dev, sizeof(trace_dev)) != cudaSuccess) return SKB_ERR_CUDA;
   if (cudaMemcpyToSymbol(g_ttrace_n, &tiles, sizeof(tiles)) != cudaSuccess) return SKB_ERR_CUDA;
+  #endif
   return SKB_OK;
 }
 
 extern "C" int skb_debug_rnn_trace(long long* trace_dev, int steps) {
+#ifndef SKB_TRACE_ENABLED
+  return trace_dev ? SKB_ERR_UNSUPPORTED : SKB_OK;   // build with SKB_TRACE=1
+#else
   if (cudaMemcpyToSymbol(g_trace, &trace_dev, sizeof(trace_dev)) != cudaSuccess) return SKB_ERR_CUDA;
   if (cudaMemcpyToSymbol(g_trace_steps, &steps, sizeof(steps)) != cudaSuccess) return SKB_ERR_CUDA;
+  #endif
   return SKB_OK;
 }
 
