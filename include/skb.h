@@ -111,6 +111,27 @@ skb_status skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_dev,
                            int32_t* err_dev, void* workspace_dev, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Region VM: any staged graph, its While/Cond
+ * control flow evaluated on the device.  Replaces the whole of
+ * graph/execute.py:27-238 for graphs without a fused kernel.  The bytecode,
+ * slot table and arena layout are produced by paper_1810_08061_b200/vm.py:
+ *   prog_dev:  int32[n][8] instructions {op, node uid, a0..a5}
+ *   extra_dev: int32 side table (perms, list items, print operands)
+ *   slots_dev: 64-byte value descriptors, feeds/constants pre-initialised
+ *   arena_dev: arena_bytes; bytes [0, arena_start) hold feeds and constants
+ *   scratch_dev: 2*ctas doubles;  tree_*: tree node table (NaN value = empty)
+ *   log_dev: print records (log_cap x 64 bytes);  ctl_dev: 8 x int64 control
+ *            block {err | uid<<32, detail, arena_used, log_count, steps}
+ * ctas == 1 runs one CTA (block barriers); > 1 a cooperative grid. */
+skb_status skb_vm_run(const void* prog_dev, const int32_t* extra_dev, void* slots_dev, void* arena_dev,
+                      int64_t arena_bytes, int64_t arena_start, double* scratch_dev,
+                      const double* tree_val_dev, const int32_t* tree_left_dev,
+                      const int32_t* tree_right_dev, int64_t* log_dev, int64_t log_cap, void* ctl_dev,
+                      int64_t max_steps, int ctas, void* stream);
+/* Largest cooperative grid (CTAs) the VM kernel can use on this device. */
+int skb_vm_max_ctas(void);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics (GPU self-tests of the tcgen05 / DSMEM building blocks).
  * ------------------------------------------------------------------------- */
 skb_status skb_diag_umma_gemm(const void* a_dev, const void* b_dev, void* d_dev, int n, int k,

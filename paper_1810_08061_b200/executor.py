@@ -68,7 +68,10 @@ def bind_feeds(graph, feeds: dict) -> dict:
         value = feeds[name]
         spec = param.out_types[0]
         if spec.dtype == "tree":
-            raise LoweringError("tree-valued parameters have no device lowering yet")
+            if not hasattr(value, "is_empty"):
+                raise RuntimeGraphError(f"feed {name!r} must be a tree", param.origin, E.DTYPE_MISMATCH)
+            out[name] = value
+            continue
         dtype = infer_dtype(value)
         if dtype != spec.dtype:
             raise RuntimeGraphError(f"feed {name!r} has dtype {dtype}, parameter wants {spec.dtype}",
@@ -221,9 +224,45 @@ def classify(prog: RnnProgram, max_len: int, T: int):
 
 
 # ------------------------------------------------------------------ public API
+_vm_plans: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def plan_kind(graph) -> str:
+    """'rnn' when the fused recurrent kernel applies, else 'vm'."""
+    try:
+        lower(graph)
+        return "rnn"
+    except LoweringError:
+        return "vm"
+
+
 def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=None) -> ExecutionResult:
-    """Drop-in for the reference ``execute(graph, feeds, check=True)``."""
-    return execute_many(graph, [feeds or {}], check=check, stream=stream)[0]
+    """Drop-in for the reference ``execute(graph, feeds, check=True)``.
+
+    Programs with a fused kernel (the dynamic-length recurrent loop) run
+    through it; every other graph runs on the device-resident region VM
+    (``vm.py`` / ``csrc/vm.cu``)."""
+    from . import runtime as rt
+    rt.lib()
+    if check:
+        validate(graph)
+    if plan_kind(graph) == "rnn":
+        return execute_many(graph, [feeds or {}], check=False, stream=stream)[0]
+    return execute_vm(graph, feeds, stream=stream)
+
+
+def execute_vm(graph, feeds: Optional[dict] = None, *, stream=None) -> ExecutionResult:
+    """Run any staged graph on the region VM (no validation)."""
+    from . import vm
+    bound = bind_feeds(graph, feeds or {})
+    with _plans_lock:
+        prog = _vm_plans.get(graph)
+    if prog is None:
+        prog = vm.compile_graph(graph)
+        with _plans_lock:
+            _vm_plans[graph] = prog
+    outs, log = vm.run(prog, bound, stream=stream)
+    return ExecutionResult(outs, log)
 
 
 def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,

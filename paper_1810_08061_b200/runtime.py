@@ -51,6 +51,9 @@ SIGNATURES = {
     "skb_profile_begin": (ctypes.c_int, [ctypes.c_int]),
     "skb_profile_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float), ctypes.c_int]),
     "skb_profile_end": (ctypes.c_int, []),
+    "skb_vm_run": (ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int64, ctypes.c_int64, _VP, _VP, _VP, _VP,
+                                   _VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int, _VP]),
+    "skb_vm_max_ctas": (ctypes.c_int, []),
     "skb_diag_umma_gemm": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP]),
     "skb_diag_cluster_exchange": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP, _VP, _VP]),
 }

@@ -1,0 +1,49 @@
+"""Region-VM parity on the GPU: the reference's corpus programs (manifest
+feeds) and its differential-fuzz programs (harness/fuzz.py), staged by the
+reference and executed by `paper_1810_08061_b200.execute`, against the
+reference executor's outputs, print logs and failure kinds.  The VM computes
+in float64/int64 like the reference: floats within the reference harness's
+own 1e-9 tolerance (harness/diff.py:31), ints and bools exact.  The corpus
+`dynamic_rnn` lowers to the fused fp16 tensor-core kernel instead (TOL 3e-3)."""
+
+import pytest
+
+from paper_1810_08061_b200 import LoweringError, RuntimeGraphError, execute, ir
+from paper_1810_08061_b200.executor import plan_kind
+from vm_cases import corpus, feed_value, flatten, fuzz_cases, leaf_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(graph_doc, feeds_doc, exp, rel=1e-9):
+    g = ir.from_json(graph_doc)
+    feeds = {k: feed_value(v) for k, v in feeds_doc.items()}
+    if "error" in exp:
+        with pytest.raises(RuntimeGraphError) as info:
+            execute(g, feeds)
+        assert info.value.cause_kind == exp["error"]
+        return
+    res = execute(g, feeds)
+    got = flatten(res.outputs)
+    assert len(got) == len(exp["outputs"])
+    for a, b in zip(got, exp["outputs"]):
+        assert leaf_equal(a, b, rel), (a.array if hasattr(a, "array") else a, b)
+    assert res.print_log == exp["print_log"]
+
+
+@pytest.mark.parametrize("prog", corpus(), ids=lambda p: p["name"])
+def test_corpus_programs(prog):
+    if prog["name"] == "tree_prod":
+        with pytest.raises(LoweringError):
+            _check(prog["graph"], prog["feeds"], prog["expected"])
+        return
+    rel = 3e-3 if plan_kind(ir.from_json(prog["graph"])) == "rnn" else 1e-9
+    _check(prog["graph"], prog["feeds"], prog["expected"], rel)
+
+
+CASES = fuzz_cases()
+
+
+@pytest.mark.parametrize("case", [c for _, c in CASES], ids=[n for n, _ in CASES])
+def test_fuzz_programs(case):
+    _check(case["graph"], case["feeds"], case["expected"])
