@@ -132,6 +132,31 @@ skb_status skb_vm_run(const void* prog_dev, const int32_t* extra_dev, void* slot
 int skb_vm_max_ctas(void);
 
 /* ---------------------------------------------------------------------------
+ * Vector-stream region executor (csrc/stream.cu; compiler stream.py).
+ *
+ * Replaces `execute` (graph/execute.py:27-36) for staged programs whose
+ * tensors are scalars or vectors of one shape (L-BFGS, in-graph SGD: BASELINE
+ * config C4): `_eval_while`/`_eval_cond` (execute.py:205-238) run on chip,
+ * element-wise nodes (tensor.py:227-300, 356-407) are fused into HBM streams
+ * and ReduceSum/ReduceMax (tensor.py:335-353) are the only grid exchanges.
+ *   prog_dev:  int32[n][8] scalar-phase instructions {op, uid, a0..a5}
+ *   extra_dev: fused-group descriptors and list item tables
+ *   w_init_dev / w_out_dev: int64[nwords] scalar/list state image in / out
+ *   bufptr_dev: int64[nbuf] device address of every vector buffer (feeds first)
+ *   rc_init_dev: int32[nbuf] initial reference counts (0 = free pool buffer)
+ *   part_dev: int64[2*8*grid] reduction partials;  ctl_dev: 8 x int64
+ *            {err = pc<<16|code (host sets -1), detail, steps, barriers,
+ *             arrive counter, max live buffers}
+ *   n: elements per vector; grid from skb_stream_grid(smem). */
+int64_t skb_stream_smem_bytes(int max_ops, int max_stack, int max_temp, int nwords, int nbuf);
+int skb_stream_grid(int64_t smem_bytes);
+skb_status skb_stream_run(const void* prog_dev, const int32_t* extra_dev, const int64_t* w_init_dev,
+                          int64_t* w_out_dev, const int64_t* bufptr_dev, const int32_t* rc_init_dev,
+                          int64_t* part_dev, void* ctl_dev, int64_t n, int nwords, int nbuf, int max_ops,
+                          int max_stack, int max_temp, int64_t max_steps, int grid, int64_t smem_bytes,
+                          void* stream);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics (GPU self-tests of the tcgen05 / DSMEM building blocks).
  * ------------------------------------------------------------------------- */
 skb_status skb_diag_umma_gemm(const void* a_dev, const void* b_dev, void* d_dev, int n, int k,

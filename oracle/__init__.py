@@ -33,8 +33,8 @@ _P4 = ctypes.c_void_p * 4
 
 def build() -> str:
     """Compile skb_oracle.c (gcc, via oracle/Makefile) if needed."""
-    src = os.path.join(HERE, "skb_oracle.c")
-    if not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
+    srcs = [os.path.join(HERE, f) for f in ("skb_oracle.c", "lbfgs_oracle.c", "Makefile")]
+    if not os.path.exists(LIB_PATH) or any(os.path.getmtime(LIB_PATH) < os.path.getmtime(s) for s in srcs):
         subprocess.run(["make", "-s", "-C", HERE], check=True)
     return LIB_PATH
 
@@ -53,6 +53,9 @@ def lib():
                                                            ctypes.POINTER(ctypes.c_int), ctypes.c_int]
         h.oracle_matmul.restype = None
         h.oracle_matmul.argtypes = [_D, _D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        h.oracle_lbfgs.restype = ctypes.c_int64
+        h.oracle_lbfgs.argtypes = [ctypes.c_int64, ctypes.c_int, _D, _D, _D, ctypes.c_double, ctypes.c_int64,
+                                   _D, _D]
         _lib = h
     return _lib
 
@@ -126,3 +129,16 @@ def rnn_many(cell, x, h0, c0, lens, W, U, b, P, threads):
                           _P4(*[v.ctypes.data for v in b]), _d(out), ml.ctypes.data_as(_I64),
                           st.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), int(threads))
     return out, ml, st
+
+
+def lbfgs(x0, a, b, tol, max_iter, m):
+    """The staged L-BFGS program (oracle/programs/lbfgs_m*.msl) in float64 on
+    one host thread.  Returns (x, k, margin); raises OracleError on the
+    reference's DivisionByZero."""
+    x0, a, b = _f64(x0).reshape(-1), _f64(a).reshape(-1), _f64(b).reshape(-1)
+    x = np.empty_like(x0)
+    margin = np.zeros(1)
+    k = lib().oracle_lbfgs(x0.size, int(m), _d(x0), _d(a), _d(b), float(tol), int(max_iter), _d(x), _d(margin))
+    if k < 0:
+        raise OracleError("DivisionByZero", 0)
+    return x, int(k), float(margin[0])

@@ -141,3 +141,73 @@ def load_graph_fixture(name="graph_lstm_c1"):
 
 def golden_names():
     return [c["name"] for c in CASES if os.path.exists(golden_path(c["name"]))]
+
+
+# ---------------------------------------------------------------- vector-stream programs (C4 class)
+def stream_case(name, program, entry, feeds, seed, note=""):
+    """feeds: name -> {"dtype", "shape", "dist": [lo, hi]} or {"dtype", "value"}."""
+    return {"name": name, "program": program, "entry": entry, "feeds": feeds, "seed": seed, "note": note}
+
+
+def _vecf(n, lo, hi):
+    return {"dtype": "f64", "shape": [n], "dist": [lo, hi]}
+
+
+def lbfgs_feeds(n, tol=1e-18, max_iter=100):
+    """Separable quadratic f = 1/2 sum a x^2 - b x."""
+    return {"x0": _vecf(n, -1.0, 1.0), "a": _vecf(n, 0.5, 4.0), "b": _vecf(n, -1.0, 1.0),
+            "tol": {"dtype": "f64", "value": tol}, "max_iter": {"dtype": "i64", "value": max_iter}}
+
+
+STREAM_CASES = [
+    stream_case("lbfgs_m3_n50", "lbfgs_m3.msl", "lbfgs", lbfgs_feeds(50), 41,
+                note="SURVEY App. C L-BFGS, m=3 (converges in ~30 iterations)"),
+    stream_case("lbfgs_m10_n2000", "lbfgs_m10.msl", "lbfgs", lbfgs_feeds(2000), 42,
+                note="BASELINE C4 program (m=10) at a size the reference finishes in seconds"),
+    stream_case("lbfgs_m10_n3000_cap", "lbfgs_m10.msl", "lbfgs", lbfgs_feeds(3001, 1e-30, 7), 43,
+                note="iteration cap reached (k == max_iter), ragged length"),
+    stream_case("stream_mix_n1500", "stream_mix.msl", "stream_mix",
+                {"v": _vecf(1500, -2.0, 2.0), "w": _vecf(1500, -1.0, 1.0),
+                 "iv": {"dtype": "i64", "shape": [1500], "dist": [-50, 50]},
+                 "c": {"dtype": "f64", "value": 0.25}, "n_iter": {"dtype": "i64", "value": 6}}, 44,
+                note="i64/bool vectors, floor-mod, Where, tanh/sigmoid, Cond on a reduction, list append/pop"),
+    stream_case("stream_div0", "stream_div0.msl", "stream_div0",
+                {"x": _vecf(700, -1.0, 1.0), "y": {"dtype": "f64", "shape": [700], "dist": [3, 3]},
+                 "n_iter": {"dtype": "i64", "value": 5}}, 45, note="vector division by zero -> DivisionByZero"),
+    stream_case("stream_limit", "stream_limit.msl", "stream_limit",
+                {"x": _vecf(900, -1.0, 1.0), "tol": {"dtype": "f64", "value": 1e-6}}, 46,
+                note="max_iterations=5 exceeded -> IterationLimitExceeded"),
+    stream_case("stream_limit_ok", "stream_limit.msl", "stream_limit",
+                {"x": _vecf(900, -1e-3, 1e-3), "tol": {"dtype": "f64", "value": 1e-6}}, 47,
+                note="converges within max_iterations"),
+    stream_case("stream_index_ok", "stream_index.msl", "stream_index",
+                {"x": _vecf(600, -1.0, 1.0), "j": {"dtype": "i64", "value": -1}}, 48, note="negative list index wraps"),
+    stream_case("stream_index_oob", "stream_index.msl", "stream_index",
+                {"x": _vecf(600, -1.0, 1.0), "j": {"dtype": "i64", "value": 2}}, 49,
+                note="list index 2 of 2 -> IndexOutOfRange"),
+]
+
+
+def stream_case_by_name(name):
+    for c in STREAM_CASES:
+        if c["name"] == name:
+            return c
+    raise KeyError(name)
+
+
+def make_stream_feeds(case) -> dict:
+    """Deterministic numpy feeds (float64 / int64 arrays, 0-d for scalars)."""
+    rng = np.random.default_rng(case["seed"])
+    out = {}
+    for name in sorted(case["feeds"]):
+        f = case["feeds"][name]
+        if "value" in f:
+            out[name] = np.asarray(f["value"], dtype=np.float64 if f["dtype"] == "f64" else np.int64)
+            continue
+        lo, hi = f["dist"]
+        shape = tuple(f["shape"])
+        if f["dtype"] == "f64":
+            out[name] = rng.uniform(lo, hi, shape) if lo != hi else np.full(shape, float(lo))
+        else:
+            out[name] = rng.integers(lo, hi + 1, shape).astype(np.int64)
+    return {name: out[name] for name in case["feeds"]}   # the entry's parameter order

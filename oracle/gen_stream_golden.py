@@ -1,0 +1,105 @@
+"""Golden fixtures for the vector-stream tier (TEST INFRASTRUCTURE; run in the
+build container, where the reference is importable).
+
+For every case of ``fixtures.STREAM_CASES`` the program under
+oracle/programs/ is traced with the reference's ``trace_module``
+(runtime/__init__.py:49-76) and executed with the reference's ``execute``
+(graph/execute.py:27-36) on ``fixtures.make_stream_feeds``; the traced graph
+(skb wire format), the feed spec and the reference's flattened outputs (or its
+failure cause_kind and span) go to tests/golden/<case>.json.
+
+Usage: python oracle/gen_stream_golden.py [case ...]
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+REF = os.environ.get("SKB_REF", "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+sys.path.insert(0, REF)
+
+from oracle import fixtures  # noqa: E402
+from oracle.gen_vm_golden import _flatten, _leaf_json  # noqa: E402
+from paper_1810_08061_b200 import ir  # noqa: E402
+
+
+def _ref_value(a):
+    from stagekit.graph import TensorValue
+    a = np.asarray(a)
+    if a.dtype == np.int64:
+        return TensorValue("i64", a.shape, tuple(int(v) for v in a.reshape(-1)))
+    return TensorValue("f64", a.shape, tuple(float(v) for v in a.reshape(-1)))
+
+
+def trace(case):
+    from stagekit.runtime import ParamSpec, trace_module
+    from stagekit.syntax import parse_module
+    path = os.path.join(fixtures.PROGRAMS, case["program"])
+    module = parse_module(open(path).read(), case["program"])
+    feeds = fixtures.make_stream_feeds(case)
+    specs = [ParamSpec(k, "i64" if v.dtype == np.int64 else "f64", tuple(v.shape)) for k, v in feeds.items()]
+    return trace_module(module, case["entry"], specs).graph
+
+
+def run_case(case):
+    from stagekit.errors import RuntimeGraphError
+    from stagekit.graph import execute
+    graph = trace(case)
+    feeds = {k: _ref_value(v) for k, v in fixtures.make_stream_feeds(case).items()}
+    doc = {"case": case, "generator": "oracle/gen_stream_golden.py", "graph": json.loads(ir.to_json(graph))}
+    t0 = time.time()
+    try:
+        res = execute(graph, feeds)
+        flat = []
+        for v in res.outputs:
+            flat.extend(_flatten(v))
+        doc["expected"] = {"outputs": [_leaf_json(v) for v in flat], "print_log": list(res.print_log)}
+    except RuntimeGraphError as exc:
+        doc["expected"] = {"error": exc.cause_kind,
+                           "span": [exc.span.file, exc.span.start_line, exc.span.start_col] if exc.span else None}
+    doc["reference_seconds"] = round(time.time() - t0, 3)
+    return doc
+
+
+def write_c4_graph():
+    """tests/golden/graph_lbfgs_c4.json: the C4 program (m=10) traced with a
+    dynamic vector length (f64[?]) so one graph serves every n."""
+    from stagekit.runtime import ParamSpec, trace_module
+    from stagekit.syntax import parse_module
+    path = os.path.join(fixtures.PROGRAMS, "lbfgs_m10.msl")
+    module = parse_module(open(path).read(), "lbfgs_m10.msl")
+    specs = [ParamSpec("x0", "f64", (None,)), ParamSpec("a", "f64", (None,)), ParamSpec("b", "f64", (None,)),
+             ParamSpec("tol", "f64", ()), ParamSpec("max_iter", "i64", ())]
+    graph = trace_module(module, "lbfgs", specs).graph
+    doc = {"case": {"name": "graph_lbfgs_c4", "program": "lbfgs_m10.msl", "entry": "lbfgs", "m": 10,
+                    "note": "BASELINE config C4: L-BFGS, history m=10, vector length bound at execution"},
+           "generator": "oracle/gen_stream_golden.py --graphs", "graph": json.loads(ir.to_json(graph))}
+    with open(os.path.join(fixtures.GOLDEN, "graph_lbfgs_c4.json"), "w") as f:
+        json.dump(doc, f, separators=(",", ":"))
+    print("graph_lbfgs_c4 graph only")
+
+
+def main(argv):
+    if argv and argv[0] == "--graphs":
+        write_c4_graph()
+        return
+    names = argv or [c["name"] for c in fixtures.STREAM_CASES]
+    for name in names:
+        doc = run_case(fixtures.stream_case_by_name(name))
+        with open(fixtures.golden_path(name), "w") as f:
+            json.dump(doc, f, separators=(",", ":"))
+        exp = doc["expected"]
+        what = exp.get("error") or [tuple(o["tensor"]["shape"]) for o in exp["outputs"]]
+        print(f"{name:24s} {what} ({doc['reference_seconds']} s in the reference executor)")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

@@ -1,0 +1,718 @@
+// stream.cu — vector-stream region executor: staged While/Cond programs whose
+// tensors are scalars or vectors of one large shape (L-BFGS, SGD loops,
+// element-wise iterative solvers; BASELINE config C4).
+//
+// The generic region VM (vm.cu) separates every instruction with a grid
+// barrier.  Here the execution model is split by value class instead:
+//
+//  * Scalars, lists and control flow are executed REDUNDANTLY by lane 0 of
+//    warp 0 in every CTA, on a private copy of the scalar/list state kept in
+//    shared memory (`W`, one int64 word per scalar slot, buffer ids for vector
+//    slots, [len, items...] for list slots).  Every CTA computes the same
+//    values and takes the same branches, so loop predicates are decided on
+//    chip with no host round trip and no grid barrier.
+//  * Vector values are immutable, reference-counted HBM buffers.  Element e of
+//    every vector always belongs to the same thread (tile e/1024 -> CTA
+//    (e/1024) % grid), so element-wise instructions never need a barrier: a
+//    thread only ever reads elements it wrote itself.
+//  * A fused element-wise group (VEXEC, compiled by stream.py from a chain of
+//    reference nodes) streams its vector operands through shared memory with a
+//    3-stage cp.async pipeline, evaluates a small stack program per element
+//    with the top of stack in registers, stores its materialised results and
+//    accumulates its reductions.
+//  * A reduction is the only cross-CTA exchange: per-CTA partials, one grid
+//    arrival, then every CTA combines the partials in the same fixed order
+//    (RFIN) and so holds a bit-identical scalar.
+//
+// Semantics follow the reference kernels (pkg/src/stagekit/graph/tensor.py):
+// f64/i64/bool words, `/` always f64 (tensor.py:269-270), Python floor-mod,
+// DivisionByZero on a zero divisor even for floats (tensor.py:235-241),
+// stable sigmoid (:403-407), scalar-condition whole-tensor Where (:367-368),
+// list indexing with negative wrap and IndexOutOfRange (execute.py:240-249),
+// max_iterations checked after a true test (execute.py:232-234).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include "skb_internal.h"
+
+namespace {
+
+constexpr int TPB = 256;
+constexpr int EPT = 4;              // elements per thread per tile (2 pairs)
+constexpr int TILE = TPB * EPT;     // 1024 elements
+constexpr int HALF = TILE / 2;
+constexpr int STAGES = 3;
+constexpr int RMAX = 8;             // reductions per fused group
+constexpr int kMaxGroupPtrs = 32;   // staged operands / stores per fused group
+
+enum Dt : int { DT_F64 = 0, DT_I64 = 1, DT_BOOL = 2 };
+enum BinK : int { B_ADD, B_SUB, B_MUL, B_DIV, B_MOD, B_LT, B_GT, B_LE, B_GE, B_EQ, B_NE };
+enum UnK : int { U_NEG, U_NOT, U_TANH, U_SIGMOID };
+
+// scalar-phase opcodes (stream.py SOP)
+enum SOp : int {
+  S_HALT = 0, S_BIN = 1, S_UN = 2, S_SEL = 3, S_MOV = 4, S_SELREF = 5, S_LNEW = 6, S_LAPPEND = 7,
+  S_LPOP = 8, S_LGET = 9, S_LSET = 10, S_JMP = 11, S_JZ = 12, S_ITER = 13, S_SETI = 14, S_ASSERT = 15,
+  S_RAISE = 16, S_ALLOC = 17, S_VEXEC = 18, S_RFIN = 19
+};
+// vector-phase opcodes
+enum VOp : int { V_PUSH = 1, V_BIN = 2, V_UN = 3, V_SEL = 4, V_STORE = 5, V_RED = 6, V_SAVE = 7, V_POP = 8 };
+enum Src : int { SRC_STACK = 0, SRC_VEC = 1, SRC_SCALAR = 2, SRC_TEMP = 3 };
+// slot kinds for MOV / list items
+enum Kind : int { K_SCALAR = 0, K_VEC = 1, K_LIST_S = 2, K_LIST_V = 3 };
+
+enum { E_INDEX = 10, E_EMPTY = 11, E_SHAPE = 12, E_DIV0 = 13, E_LIMIT = 14, E_ASSERT = 15,
+       E_DTYPE = 16, E_POOL = 30, E_STEPS = 31, E_CAP = 32, E_INTERNAL = 33 };
+
+struct SIns { int32_t op, uid, a[6]; };
+
+struct StreamCtl {               // device control block (host-zeroed)
+  unsigned long long err;        // (pc << 16) | code, min over reporters
+  long long detail;
+  long long steps;
+  long long barriers;
+  unsigned int arrive;           // grid-arrival counter (monotonic)
+  unsigned int pad;
+  long long max_live;            // buffer-pool high-water mark
+};
+
+struct StreamArgs {
+  const SIns* prog;
+  const int32_t* extra;
+  const long long* w_init;       // initial W image
+  long long* w_out;              // final W image (written by CTA 0)
+  const long long* bufptr;       // buffer id -> device address
+  const int32_t* rc_init;        // initial reference counts (feeds pinned)
+  long long* part;               // [2][RMAX][grid] reduction partials
+  StreamCtl* ctl;
+  long long n;                   // elements per vector
+  int nwords;
+  int nbuf;
+  int max_stack;                 // spill depth
+  int max_temp;
+  int max_ops;                   // staged operands per group
+  long long max_steps;
+};
+
+struct Smem {                    // carved from dynamic shared memory
+  long long* W;
+  int32_t* rc;
+  int32_t* freel;
+  long long* stage;              // [STAGES][max_ops][TILE]
+  long long* stk;                // [max_stack][TILE]
+  long long* tmp;                // [max_temp][TILE]
+  long long* gptr;               // [max_ops + stores] resolved addresses
+  long long* red;                // [TPB/32][RMAX]
+};
+
+struct Ctl {                     // per-CTA scalar-phase state (shared)
+  int pc, halt, nfree, barrier_gen;
+  long long steps, live, max_live;
+};
+
+__device__ __forceinline__ double as_f(long long w) { return __longlong_as_double(w); }
+__device__ __forceinline__ long long as_w(double d) { return __double_as_longlong(d); }
+__device__ __forceinline__ double num(long long w, int dt) { return dt == DT_F64 ? as_f(w) : (double)w; }
+
+__device__ double sigmoid_ref(double x) {   // reference tensor.py:403-407
+  if (x >= 0) return 1.0 / (1.0 + exp(-x));
+  const double e = exp(x);
+  return e / (1.0 + e);
+}
+__device__ __forceinline__ double py_fmod(double a, double b) {
+  double r = fmod(a, b);
+  if (r != 0.0 && ((r < 0.0) != (b < 0.0))) r += b;
+  return r;
+}
+__device__ __forceinline__ long long py_imod(long long a, long long b) {
+  long long r = a % b;
+  if (r != 0 && ((r < 0) != (b < 0))) r += b;
+  return r;
+}
+__device__ __forceinline__ long long py_ifloordiv_guard(long long b) { return b; }
+
+// One reference binop on words (tensor.py:227-287).  `dts` = dta | dtb << 4 | dto << 8.
+__device__ __forceinline__ long long binop_w(int op, int dts, long long a, long long b, bool& div0) {
+  const int dta = dts & 15, dtb = (dts >> 4) & 15, dto = (dts >> 8) & 15;
+  if (op >= B_LT) {
+    bool r;
+    if (dta == DT_F64 || dtb == DT_F64) {
+      const double x = num(a, dta), y = num(b, dtb);
+      r = op == B_LT ? x < y : op == B_GT ? x > y : op == B_LE ? x <= y : op == B_GE ? x >= y
+        : op == B_EQ ? x == y : x != y;
+    } else {
+      r = op == B_LT ? a < b : op == B_GT ? a > b : op == B_LE ? a <= b : op == B_GE ? a >= b
+        : op == B_EQ ? a == b : a != b;
+    }
+    return r ? 1 : 0;
+  }
+  if (dto == DT_F64) {
+    const double x = num(a, dta), y = num(b, dtb);
+    double r;
+    switch (op) {
+      case B_ADD: r = x + y; break;
+      case B_SUB: r = x - y; break;
+      case B_MUL: r = x * y; break;
+      case B_DIV: if (y == 0.0) { div0 = true; r = 0.0; } else r = x / y; break;
+      default:    if (y == 0.0) { div0 = true; r = 0.0; } else r = py_fmod(x, y); break;
+    }
+    return as_w(r);
+  }
+  switch (op) {
+    case B_ADD: return a + b;
+    case B_SUB: return a - b;
+    case B_MUL: return a * b;
+    default:
+      if (b == 0) { div0 = true; return 0; }
+      return py_imod(a, b);
+  }
+}
+
+__device__ __forceinline__ long long unop_w(int op, int dts, long long a) {
+  const int dta = dts & 15;
+  switch (op) {
+    case U_NEG: return dta == DT_F64 ? as_w(-as_f(a)) : -a;
+    case U_NOT: return a ? 0 : 1;
+    case U_TANH: return as_w(tanh(num(a, dta)));
+    default: return as_w(sigmoid_ref(num(a, dta)));
+  }
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+               :: "r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ------------------------------------------------------------ scalar phase
+struct Scalar {
+  const StreamArgs& a;
+  Smem& s;
+  Ctl& c;
+
+  __device__ void ref(long long id) const { if (id >= 0) s.rc[id]++; }
+  __device__ void rel(long long id) const {
+    if (id >= 0 && --s.rc[id] == 0) { s.freel[c.nfree++] = (int)id; c.live--; }
+  }
+  __device__ long long alloc() const {
+    if (c.nfree == 0) return -1;
+    const int id = s.freel[--c.nfree];
+    s.rc[id] = 1;
+    if (++c.live > c.max_live) c.max_live = c.live;
+    return id;
+  }
+  // release the contents of a list slot of vectors
+  __device__ void rel_list(int off, int kind) const {
+    if (kind == K_LIST_V) {
+      const long long n = s.W[off];
+      for (long long i = 0; i < n; ++i) rel(s.W[off + 1 + i]);
+    }
+  }
+  __device__ void set_vec(int dst, long long id) const {   // ref-before-rel
+    ref(id);
+    rel(s.W[dst]);
+    s.W[dst] = id;
+  }
+  // dst <- src for any kind (MOV / VIEW / loop-state copies)
+  __device__ void mov(int dst, int src, int kind) const {
+    if (dst == src) return;
+    if (kind == K_SCALAR) { s.W[dst] = s.W[src]; return; }
+    if (kind == K_VEC) { set_vec(dst, s.W[src]); return; }
+    const long long n = s.W[src];
+    if (kind == K_LIST_V)
+      for (long long i = 0; i < n; ++i) ref(s.W[src + 1 + i]);
+    rel_list(dst, kind);
+    s.W[dst] = n;
+    for (long long i = 0; i < n; ++i) s.W[dst + 1 + i] = s.W[src + 1 + i];
+  }
+  __device__ bool list_index(int list, long long i, long long& out) const {   // execute.py:240-245
+    const long long n = s.W[list];
+    if (!(-n <= i && i < n)) return false;
+    out = i < 0 ? i + n : i;
+    return true;
+  }
+};
+
+__device__ void report(StreamCtl* ctl, int pc, int code, long long detail) {
+  const unsigned long long w = ((unsigned long long)pc << 16) | (unsigned long long)code;
+  const unsigned long long old = atomicMin(&ctl->err, w);
+  if (w < old) ctl->detail = detail;
+}
+
+// Runs lane 0's scalar instructions from c.pc until a VEXEC, RFIN or HALT.
+// Returns the opcode it stopped at (c.pc points at it).
+__device__ int scalar_run(const StreamArgs& a, Smem& s, Ctl& c) {
+  Scalar S{a, s, c};
+  long long* W = s.W;
+  for (;;) {
+    const SIns in = a.prog[c.pc];
+    if (++c.steps > a.max_steps) { report(a.ctl, c.pc, E_STEPS, c.steps); c.halt = 1; return S_HALT; }
+    int next = c.pc + 1;
+    int fail = 0;
+    long long detail = 0;
+    switch (in.op) {
+      case S_HALT: return S_HALT;
+      case S_VEXEC: return S_VEXEC;
+      case S_RFIN: return S_RFIN;
+      case S_BIN: {
+        bool d0 = false;
+        W[in.a[0]] = binop_w(in.a[3], in.a[4], W[in.a[1]], W[in.a[2]], d0);
+        if (d0) fail = E_DIV0;
+        break;
+      }
+      case S_UN: W[in.a[0]] = unop_w(in.a[2], in.a[3], W[in.a[1]]); break;
+      case S_SEL: W[in.a[0]] = W[in.a[1]] ? W[in.a[2]] : W[in.a[3]]; break;
+      case S_MOV: S.mov(in.a[0], in.a[1], in.a[2]); break;
+      case S_SELREF: S.set_vec(in.a[0], W[in.a[1]] ? W[in.a[2]] : W[in.a[3]]); break;
+      case S_ALLOC: {
+        const long long id = S.alloc();
+        if (id < 0) { fail = E_POOL; break; }
+        S.rel(W[in.a[0]]);
+        W[in.a[0]] = id;
+        break;
+      }
+      case S_LNEW: {   // a0 dst, a1 extra off (n, item offsets), a2 kind (list), a3 cap
+        const int32_t* ex = a.extra + in.a[1];
+        const int n = ex[0];
+        if (n > in.a[3]) { fail = E_CAP; break; }
+        if (in.a[2] == K_LIST_V)
+          for (int i = 0; i < n; ++i) S.ref(W[ex[1 + i]]);
+        S.rel_list(in.a[0], in.a[2]);
+        W[in.a[0]] = n;
+        for (int i = 0; i < n; ++i) W[in.a[0] + 1 + i] = W[ex[1 + i]];
+        break;
+      }
+      case S_LAPPEND: {   // a0 dst, a1 list, a2 item, a3 kind, a4 cap
+        const long long n = W[in.a[1]];
+        if (n + 1 > in.a[4]) { fail = E_CAP; break; }
+        S.mov(in.a[0], in.a[1], in.a[3]);
+        if (in.a[3] == K_LIST_V) S.ref(W[in.a[2]]);
+        W[in.a[0] + 1 + n] = W[in.a[2]];
+        W[in.a[0]] = n + 1;
+        break;
+      }
+      case S_LPOP: {      // a0 dst list, a1 dst item, a2 list, a3 kind
+        const long long n = W[in.a[2]];
+        if (n == 0) { fail = E_EMPTY; break; }
+        const long long item = W[in.a[2] + n];
+        if (in.a[3] == K_LIST_V) S.set_vec(in.a[1], item); else W[in.a[1]] = item;
+        S.mov(in.a[0], in.a[2], in.a[3]);
+        if (in.a[3] == K_LIST_V) S.rel(W[in.a[0] + n]);
+        W[in.a[0]] = n - 1;
+        break;
+      }
+      case S_LGET: {      // a0 dst, a1 list, a2 idx slot, a3 kind
+        long long i;
+        if (!S.list_index(in.a[1], W[in.a[2]], i)) { fail = E_INDEX; detail = W[in.a[2]]; break; }
+        const long long item = W[in.a[1] + 1 + i];
+        if (in.a[3] == K_LIST_V) S.set_vec(in.a[0], item); else W[in.a[0]] = item;
+        break;
+      }
+      case S_LSET: {      // a0 dst, a1 list, a2 idx, a3 value, a4 kind
+        long long i;
+        if (!S.list_index(in.a[1], W[in.a[2]], i)) { fail = E_INDEX; detail = W[in.a[2]]; break; }
+        const long long v = W[in.a[3]];
+        S.mov(in.a[0], in.a[1], in.a[4]);
+        if (in.a[4] == K_LIST_V) { S.ref(v); S.rel(W[in.a[0] + 1 + i]); }
+        W[in.a[0] + 1 + i] = v;
+        break;
+      }
+      case S_JMP: next = in.a[0]; break;
+      case S_JZ: if (!W[in.a[0]]) next = in.a[1]; break;
+      case S_ITER: {
+        const long long it = W[in.a[0]];
+        if (it >= in.a[1]) { fail = E_LIMIT; detail = it; break; }
+        W[in.a[0]] = it + 1;
+        break;
+      }
+      case S_SETI: W[in.a[0]] = in.a[1]; break;
+      case S_ASSERT: if (!W[in.a[0]]) fail = E_ASSERT; break;
+      case S_RAISE: fail = in.a[0]; detail = in.a[1]; break;
+      default: fail = E_DTYPE + 100; break;
+    }
+    if (fail) { report(a.ctl, c.pc, fail, detail); c.halt = 1; return S_HALT; }
+    c.pc = next;
+  }
+}
+
+// ------------------------------------------------------------ vector phase
+struct Group {
+  int nops, nstores, nred, ninstr;
+  const int32_t* op_slots;
+  const int32_t* store_slots;
+  const int32_t* red_kd;
+  const int32_t* ins;
+};
+
+__device__ __forceinline__ Group decode(const int32_t* g) {
+  Group G;
+  G.nops = g[0]; G.nstores = g[1]; G.nred = g[2]; G.ninstr = g[3];
+  G.op_slots = g + 4;
+  G.store_slots = G.op_slots + G.nops;
+  G.red_kd = G.store_slots + G.nstores;
+  G.ins = G.red_kd + G.nred;
+  return G;
+}
+
+// element j (0..3) of this thread within a tile: pair j>>1, lane-pair offset j&1
+__device__ __forceinline__ int elem_of(int j) { return (j >> 1) * HALF + threadIdx.x * 2 + (j & 1); }
+
+__device__ __forceinline__ void issue_tile(const StreamArgs& a, const Smem& s, const Group& G, long long tile,
+                                           int stage) {
+  const long long base = tile * TILE;
+  for (int k = 0; k < G.nops; ++k) {
+    const long long* src = reinterpret_cast<const long long*>(s.gptr[k]);
+    long long* dst = s.stage + ((long long)stage * a.max_ops + k) * TILE;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int e = p * HALF + threadIdx.x * 2;
+      const long long ge = base + e;
+      const long long left = a.n - ge;
+      const int bytes = left >= 2 ? 16 : left == 1 ? 8 : 0;
+      cp_async16(static_cast<uint32_t>(__cvta_generic_to_shared(dst + e)), bytes ? src + ge : src, bytes);
+    }
+  }
+}
+
+__device__ __forceinline__ long long red_identity(int kd) {
+  const int kind = kd & 15, dt = kd >> 4;
+  if (kind == 0) return dt == DT_F64 ? as_w(0.0) : 0;
+  return dt == DT_F64 ? as_w(-INFINITY) : LLONG_MIN;
+}
+__device__ __forceinline__ long long red_combine(int kd, long long x, long long y) {
+  const int kind = kd & 15, dt = kd >> 4;
+  if (dt == DT_F64) {
+    const double a = as_f(x), b = as_f(y);
+    return as_w(kind == 0 ? a + b : (b > a ? b : a));
+  }
+  return kind == 0 ? x + y : (y > x ? y : x);
+}
+
+__device__ void vector_run(const StreamArgs& a, Smem& s, const Group& G, int pc, long long racc[RMAX]) {
+  const long long ntiles = (a.n + TILE - 1) / TILE;
+  const int tid = threadIdx.x;
+  int div0_q = 1 << 30;   // first vector instruction that divided by zero
+  for (int r = 0; r < RMAX; ++r) racc[r] = r < G.nred ? red_identity(G.red_kd[r]) : 0;
+  long long nmy = 0;
+  if (blockIdx.x < ntiles) nmy = (ntiles - 1 - blockIdx.x) / gridDim.x + 1;
+  // prologue
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nmy) issue_tile(a, s, G, blockIdx.x + (long long)st * gridDim.x, st);
+    cp_async_commit();
+  }
+  for (long long i = 0; i < nmy; ++i) {
+    const long long nxt = i + STAGES - 1;
+    if (nxt < nmy) issue_tile(a, s, G, blockIdx.x + nxt * gridDim.x, (int)(nxt % STAGES));
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    const long long tile = blockIdx.x + i * gridDim.x;
+    const long long base = tile * TILE;
+    const long long* stage = s.stage + (long long)(i % STAGES) * a.max_ops * TILE;
+    long long tos[EPT];
+    int sp = 0;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) tos[j] = 0;
+    for (int q = 0; q < G.ninstr; ++q) {
+      const int32_t* w = G.ins + 4 * q;
+      const int op = w[0];
+      if (op == V_PUSH || op == V_BIN) {
+        // fetch the explicit operand (vector stage / scalar / temp) into `val`
+        const int src = op == V_PUSH ? w[1] : (w[1] >> 12) & 15;
+        const int idx = w[2];
+        long long val[EPT];
+        if (src == SRC_VEC) {
+          const long long* p = stage + (long long)idx * TILE;
+#pragma unroll
+          for (int j = 0; j < EPT; j += 2) {
+            const longlong2 v = *reinterpret_cast<const longlong2*>(p + elem_of(j));
+            val[j] = v.x; val[j + 1] = v.y;
+          }
+        } else if (src == SRC_SCALAR) {
+          const long long v = s.W[idx];
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) val[j] = v;
+        } else if (src == SRC_TEMP) {
+          const long long* p = s.tmp + (long long)idx * TILE;
+#pragma unroll
+          for (int j = 0; j < EPT; j += 2) {
+            const longlong2 v = *reinterpret_cast<const longlong2*>(p + elem_of(j));
+            val[j] = v.x; val[j + 1] = v.y;
+          }
+        } else {   // SRC_STACK: pop the second operand
+          --sp;
+          const long long* p = s.stk + (long long)sp * TILE;
+#pragma unroll
+          for (int j = 0; j < EPT; j += 2) {
+            const longlong2 v = *reinterpret_cast<const longlong2*>(p + elem_of(j));
+            val[j] = v.x; val[j + 1] = v.y;
+          }
+        }
+        if (op == V_PUSH) {
+          if (w[3]) {   // spill the current TOS
+            long long* p = s.stk + (long long)sp * TILE;
+#pragma unroll
+            for (int j = 0; j < EPT; j += 2)
+              *reinterpret_cast<longlong2*>(p + elem_of(j)) = make_longlong2(tos[j], tos[j + 1]);
+            ++sp;
+          }
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) tos[j] = val[j];
+        } else {
+          const int bop = w[1] & 255, rev = (w[1] >> 8) & 1, dts = w[3];
+          // stack form: left = popped value, right = TOS; explicit operand: rev=0 -> TOS op val
+          const bool tos_left = (src == SRC_STACK) ? false : !rev;
+          if (dts == (DT_F64 | DT_F64 << 4 | DT_F64 << 8) && bop <= B_MUL) {
+#pragma unroll
+            for (int j = 0; j < EPT; ++j) {
+              const double l = as_f(tos_left ? tos[j] : val[j]), r = as_f(tos_left ? val[j] : tos[j]);
+              tos[j] = as_w(bop == B_ADD ? l + r : bop == B_SUB ? l - r : l * r);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < EPT; ++j) {
+              const long long l = tos_left ? tos[j] : val[j], r = tos_left ? val[j] : tos[j];
+              bool d = false;
+              tos[j] = binop_w(bop, dts, l, r, d);
+              if (d && base + elem_of(j) < a.n && q < div0_q) div0_q = q;
+            }
+          }
+        }
+      } else if (op == V_UN) {
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) tos[j] = unop_w(w[1], w[3], tos[j]);
+      } else if (op == V_SEL) {   // c, x popped (c deeper), TOS = y
+        const long long* px = s.stk + (long long)(sp - 1) * TILE;
+        const long long* pc_ = s.stk + (long long)(sp - 2) * TILE;
+        sp -= 2;
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          const int e = elem_of(j);
+          tos[j] = pc_[e] ? px[e] : tos[j];
+        }
+      } else if (op == V_STORE) {
+        long long* dst = reinterpret_cast<long long*>(s.gptr[kMaxGroupPtrs + w[1]]);
+#pragma unroll
+        for (int j = 0; j < EPT; j += 2) {
+          const long long ge = base + elem_of(j);
+          if (ge + 1 < a.n) {
+            *reinterpret_cast<longlong2*>(dst + ge) = make_longlong2(tos[j], tos[j + 1]);
+          } else if (ge < a.n) {
+            dst[ge] = tos[j];
+          }
+        }
+      } else if (op == V_RED) {
+        const int r = w[1];
+        const int kd = G.red_kd[r];
+#pragma unroll
+        for (int rr = 0; rr < RMAX; ++rr) {
+          if (rr != r) continue;
+#pragma unroll
+          for (int j = 0; j < EPT; ++j)
+            if (base + elem_of(j) < a.n) racc[rr] = red_combine(kd, racc[rr], tos[j]);
+        }
+      } else if (op == V_SAVE) {
+        long long* p = s.tmp + (long long)w[1] * TILE;
+#pragma unroll
+        for (int j = 0; j < EPT; j += 2)
+          *reinterpret_cast<longlong2*>(p + elem_of(j)) = make_longlong2(tos[j], tos[j + 1]);
+      } else if (op == V_POP) {
+        --sp;
+        const long long* p = s.stk + (long long)sp * TILE;
+#pragma unroll
+        for (int j = 0; j < EPT; j += 2) {
+          const longlong2 v = *reinterpret_cast<const longlong2*>(p + elem_of(j));
+          tos[j] = v.x; tos[j + 1] = v.y;
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (__syncthreads_or(div0_q != (1 << 30))) {
+    __shared__ int first_q;
+    if (tid == 0) first_q = 1 << 30;
+    __syncthreads();
+    if (div0_q != (1 << 30)) atomicMin(&first_q, div0_q);
+    __syncthreads();
+    if (tid == 0) report(a.ctl, pc, E_DIV0, first_q);   // host maps (pc, q) -> node
+  }
+}
+
+__global__ void __launch_bounds__(TPB) stream_kernel(StreamArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Ctl c;
+  Smem s;
+  {
+    unsigned char* p = smem_raw;
+    auto take = [&](size_t bytes) { unsigned char* r = p; p += (bytes + 15) & ~size_t(15); return r; };
+    s.stage = reinterpret_cast<long long*>(take(sizeof(long long) * STAGES * a.max_ops * TILE));
+    s.stk = reinterpret_cast<long long*>(take(sizeof(long long) * a.max_stack * TILE));
+    s.tmp = reinterpret_cast<long long*>(take(sizeof(long long) * a.max_temp * TILE));
+    s.W = reinterpret_cast<long long*>(take(sizeof(long long) * a.nwords));
+    s.gptr = reinterpret_cast<long long*>(take(sizeof(long long) * 2 * kMaxGroupPtrs));
+    s.red = reinterpret_cast<long long*>(take(sizeof(long long) * (TPB / 32) * RMAX));
+    s.rc = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * a.nbuf));
+    s.freel = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * a.nbuf));
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < a.nwords; i += TPB) s.W[i] = a.w_init[i];
+  for (int i = tid; i < a.nbuf; i += TPB) s.rc[i] = a.rc_init[i];
+  if (tid == 0) {
+    c.pc = 0; c.halt = 0; c.barrier_gen = 0; c.steps = 0;
+    int nf = 0, live = 0;
+    for (int i = a.nbuf - 1; i >= 0; --i) {   // lowest id allocated first
+      if (a.rc_init[i] == 0) s.freel[nf++] = i; else ++live;
+    }
+    c.nfree = nf; c.live = live; c.max_live = live;
+  }
+  __syncthreads();
+  long long racc[RMAX];
+  for (;;) {
+    if (warp == 0) {
+      for (;;) {
+        int stop = S_HALT;
+        if (lane == 0) stop = scalar_run(a, s, c);
+        stop = __shfl_sync(0xffffffffu, stop, 0);
+        __syncwarp();
+        if (stop != S_RFIN) break;
+        // RFIN: a0 dst word, a1 reduction index, a2 kind|dt<<4, a3 wait flag
+        const SIns in = a.prog[c.pc];
+        if (in.a[3]) {
+          if (lane == 0) {
+            const unsigned int target = (unsigned int)(c.barrier_gen) * gridDim.x;
+            while (ld_acquire(&a.ctl->arrive) < target) {}
+          }
+          __syncwarp();
+          const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&a.ctl->err);
+          if (e != ~0ull) {
+            if (lane == 0) c.halt = 1;
+            __syncwarp();
+            break;
+          }
+        }
+        const int kd = in.a[2];
+        const long long* part = a.part + ((long long)((c.barrier_gen - 1) & 1) * RMAX + in.a[1]) * gridDim.x;
+        long long acc = red_identity(kd);
+        for (int i = lane; i < (int)gridDim.x; i += 32) acc = red_combine(kd, acc, __ldcg(part + i));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc = red_combine(kd, acc, __shfl_xor_sync(0xffffffffu, acc, o));
+        if (lane == 0) { s.W[in.a[0]] = acc; c.pc++; }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (c.halt || a.prog[c.pc].op == S_HALT) break;
+    // VEXEC: a0 = group offset in extra
+    const int pc = c.pc;
+    const Group G = decode(a.extra + a.prog[pc].a[0]);
+    bool bad = false;
+    if (tid < G.nops + G.nstores) {
+      const int slot = tid < G.nops ? G.op_slots[tid] : G.store_slots[tid - G.nops];
+      const long long id = s.W[slot];
+      if (id < 0 || id >= a.nbuf) {
+        bad = true;
+        report(a.ctl, pc, E_INTERNAL, ((long long)slot << 32) | (id & 0xffffffffll));
+      } else {
+        s.gptr[tid < G.nops ? tid : kMaxGroupPtrs + tid - G.nops] = a.bufptr[id];
+      }
+    }
+    if (__syncthreads_or(bad)) break;   // identical in every CTA: all stop here
+    vector_run(a, s, G, pc, racc);
+    if (G.nred > 0) {
+      // block reduce in a fixed order, then one arrival per CTA
+      for (int r = 0; r < G.nred; ++r) {
+        long long v = racc[r];
+        for (int o = 16; o; o >>= 1) v = red_combine(G.red_kd[r], v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) s.red[warp * RMAX + r] = v;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const int gen = c.barrier_gen;
+        for (int r = 0; r < G.nred; ++r) {
+          long long v = s.red[r];
+          for (int w = 1; w < TPB / 32; ++w) v = red_combine(G.red_kd[r], v, s.red[w * RMAX + r]);
+          a.part[((long long)(gen & 1) * RMAX + r) * gridDim.x + blockIdx.x] = v;
+        }
+        __threadfence();
+        atomicAdd(&a.ctl->arrive, 1u);
+        c.barrier_gen = gen + 1;
+      }
+    }
+    if (tid == 0) c.pc = pc + 1;
+    __syncthreads();
+  }
+  if (blockIdx.x == 0) {
+    __syncthreads();
+    for (int i = tid; i < a.nwords; i += TPB) a.w_out[i] = s.W[i];
+    if (tid == 0) {
+      a.ctl->steps = c.steps;
+      a.ctl->barriers = c.barrier_gen;
+      a.ctl->max_live = c.max_live;
+    }
+  }
+}
+
+size_t smem_bytes(int max_ops, int max_stack, int max_temp, int nwords, int nbuf) {
+  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
+  return r(8ull * STAGES * max_ops * TILE) + r(8ull * max_stack * TILE) + r(8ull * max_temp * TILE) +
+         r(8ull * nwords) + r(8ull * 2 * kMaxGroupPtrs) + r(8ull * (TPB / 32) * RMAX) + 2 * r(4ull * nbuf);
+}
+
+}  // namespace
+
+extern "C" int64_t skb_stream_smem_bytes(int max_ops, int max_stack, int max_temp, int nwords, int nbuf) {
+  return (int64_t)smem_bytes(max_ops, max_stack, max_temp, nwords, nbuf);
+}
+
+// Grid size the cooperative stream kernel will use for this shared-memory
+// footprint (co-resident CTAs on all SMs), or <= 0 if it does not fit.
+extern "C" int skb_stream_grid(int64_t smem) {
+  int dev = 0, sms = 0, per = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (smem > optin) return 0;
+  if (cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return -1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_kernel, TPB, (size_t)smem) != cudaSuccess)
+    return -1;
+  return sms * per;
+}
+
+extern "C" int skb_stream_run(const void* prog, const int32_t* extra, const int64_t* w_init, int64_t* w_out,
+                              const int64_t* bufptr, const int32_t* rc_init, int64_t* part, void* ctl,
+                              int64_t n, int nwords, int nbuf, int max_ops, int max_stack, int max_temp,
+                              int64_t max_steps, int grid, int64_t smem, void* stream) {
+  if (grid <= 0 || n <= 0) return SKB_ERR_INVALID;
+  StreamArgs a;
+  a.prog = reinterpret_cast<const SIns*>(prog);
+  a.extra = extra;
+  a.w_init = reinterpret_cast<const long long*>(w_init);
+  a.w_out = reinterpret_cast<long long*>(w_out);
+  a.bufptr = reinterpret_cast<const long long*>(bufptr);
+  a.rc_init = rc_init;
+  a.part = reinterpret_cast<long long*>(part);
+  a.ctl = reinterpret_cast<StreamCtl*>(ctl);
+  a.n = n;
+  a.nwords = nwords;
+  a.nbuf = nbuf;
+  a.max_ops = max_ops < 1 ? 1 : max_ops;
+  a.max_stack = max_stack < 1 ? 1 : max_stack;
+  a.max_temp = max_temp < 1 ? 1 : max_temp;
+  a.max_steps = max_steps;
+  if (cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SKB_ERR_CUDA;
+  void* params[] = {&a};
+  if (cudaLaunchCooperativeKernel((void*)stream_kernel, dim3(grid), dim3(TPB), params, (size_t)smem,
+                                  (cudaStream_t)stream) != cudaSuccess)
+    return SKB_ERR_CUDA;
+  return skb_check_launch();
+}

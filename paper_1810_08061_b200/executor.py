@@ -227,13 +227,42 @@ def classify(prog: RnnProgram, max_len: int, T: int):
 _vm_plans: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
-def plan_kind(graph) -> str:
-    """'rnn' when the fused recurrent kernel applies, else 'vm'."""
+_stream_plans: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+STREAM_MIN_ELEMS = 1 << 14   # smaller vectors run on the region VM (one CTA is enough)
+
+
+def stream_plan(graph):
+    """The vector-stream program of `graph` (stream.py), or None if it has none."""
+    from . import stream
+    with _plans_lock:
+        if graph in _stream_plans:
+            return _stream_plans[graph]
+    try:
+        prog = stream.compile_graph(graph)
+    except LoweringError:
+        prog = None
+    with _plans_lock:
+        _stream_plans[graph] = prog
+    return prog
+
+
+def plan_kind(graph, feeds: Optional[dict] = None) -> str:
+    """'rnn' when the fused recurrent kernel applies, 'stream' for vector-stream
+    programs whose vectors (static shape, else the feeds') have at least
+    STREAM_MIN_ELEMS elements, else 'vm'."""
     try:
         lower(graph)
         return "rnn"
     except LoweringError:
+        pass
+    prog = stream_plan(graph)
+    if prog is None:
         return "vm"
+    n = int(np.prod(prog.shape)) if all(d is not None for d in prog.shape) else 0
+    for name, slot in prog.feeds.items():
+        if feeds and name in feeds and slot.kind == 1:
+            n = max(n, int(np.prod(shape_of(feeds[name]))))
+    return "stream" if n >= STREAM_MIN_ELEMS else "vm"
 
 
 def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=None) -> ExecutionResult:
@@ -246,9 +275,28 @@ def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=N
     rt.lib()
     if check:
         validate(graph)
-    if plan_kind(graph) == "rnn":
+    kind = plan_kind(graph, feeds)
+    if kind == "rnn":
         return execute_many(graph, [feeds or {}], check=False, stream=stream)[0]
+    if kind == "stream":
+        try:
+            return execute_stream(graph, feeds, stream=stream)
+        except LoweringError:   # e.g. a list outgrew the tier's capacity: the region VM runs it
+            pass
     return execute_vm(graph, feeds, stream=stream)
+
+
+def execute_stream(graph, feeds: Optional[dict] = None, *, stream=None) -> ExecutionResult:
+    """Run a vector-stream program (stream.py / csrc/stream.cu) at any size;
+    raises LoweringError for graphs outside that tier."""
+    from . import stream as st
+    from . import runtime as rt
+    rt.lib()
+    bound = bind_feeds(graph, feeds or {})
+    prog = stream_plan(graph)
+    if prog is None:
+        st.compile_graph(graph)   # re-raise the LoweringError with its message
+    return ExecutionResult(st.run(prog, bound, stream=stream), [])
 
 
 def execute_vm(graph, feeds: Optional[dict] = None, *, stream=None) -> ExecutionResult:
