@@ -319,12 +319,19 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config", default="c1", choices=["c1", "c4"],
+                    help="c1 = the headline metric (default); c4 = L-BFGS (benchmarks/c4.py)")
+    ap.add_argument("--n", type=int, default=0, help="c4: vector length (default 1e7)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    leg = None
+    if args.config != "c1":
+        import importlib
+        leg = importlib.import_module(f"benchmarks.{args.config}")
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        (leg.run_reference if leg else run_reference)(args, rank, world)
         return
     if world > 1:
         import torch
@@ -333,7 +340,10 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_skb(args, rank, world, local_rank)
+        if leg:
+            leg.run(args, rank, world, local_rank, ClockSampler)
+        else:
+            run_skb(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -87,9 +87,30 @@ def write_c4_graph():
     print("graph_lbfgs_c4 graph only")
 
 
+MICRO = {"micro_dot": ["x", "y"], "micro_axpy": ["x", "y"], "micro_copy": ["x"]}
+
+
+def write_micro_graphs():
+    """tests/golden/graph_micro_*.json: one-group loops (dot, axpy, scale) with a
+    dynamic vector length, for the stream-tier bandwidth probes (tools/stream_micro.py)."""
+    from stagekit.runtime import ParamSpec, trace_module
+    from stagekit.syntax import parse_module
+    for name, vecs in MICRO.items():
+        path = os.path.join(fixtures.PROGRAMS, name + ".msl")
+        module = parse_module(open(path).read(), name + ".msl")
+        specs = [ParamSpec(v, "f64", (None,)) for v in vecs] + [ParamSpec("iters", "i64", ())]
+        graph = trace_module(module, name, specs).graph
+        doc = {"case": {"name": "graph_" + name, "program": name + ".msl", "entry": name},
+               "generator": "oracle/gen_stream_golden.py --graphs", "graph": json.loads(ir.to_json(graph))}
+        with open(os.path.join(fixtures.GOLDEN, f"graph_{name}.json"), "w") as f:
+            json.dump(doc, f, separators=(",", ":"))
+        print("graph_" + name)
+
+
 def main(argv):
     if argv and argv[0] == "--graphs":
         write_c4_graph()
+        write_micro_graphs()
         return
     names = argv or [c["name"] for c in fixtures.STREAM_CASES]
     for name in names:

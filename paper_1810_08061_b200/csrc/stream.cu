@@ -37,12 +37,13 @@
 
 namespace {
 
-constexpr int TPB = 256;
+constexpr int TPB = 512;
 constexpr int EPT = 4;              // elements per thread per tile (2 pairs)
-constexpr int TILE = TPB * EPT;     // 1024 elements
-constexpr int HALF = TILE / 2;
-constexpr int STAGES = 3;
-constexpr int RMAX = 8;             // reductions per fused group
+constexpr int TILE = TPB * EPT;     // 2048 elements = 16 KB per staged operand
+constexpr int kMaxStages = 8;
+constexpr long long kSmemBudget = 220 * 1024;   // dynamic shared memory the kernel may use
+constexpr int kMaxInstr = 256;      // vector instructions per fused group
+constexpr int RMAX = 4;             // reductions per fused group
 constexpr int kMaxGroupPtrs = 32;   // staged operands / stores per fused group
 
 enum Dt : int { DT_F64 = 0, DT_I64 = 1, DT_BOOL = 2 };
@@ -91,6 +92,7 @@ struct StreamArgs {
   int max_stack;                 // spill depth
   int max_temp;
   int max_ops;                   // staged operands per group
+  long long smem;                // dynamic shared memory bytes of the launch
   long long max_steps;
 };
 
@@ -98,10 +100,14 @@ struct Smem {                    // carved from dynamic shared memory
   long long* W;
   int32_t* rc;
   int32_t* freel;
-  long long* stage;              // [STAGES][max_ops][TILE]
-  long long* stk;                // [max_stack][TILE]
-  long long* tmp;                // [max_temp][TILE]
-  long long* gptr;               // [max_ops + stores] resolved addresses
+  long long* stage;              // [stages][nops][TILE] for the running group
+  long long stage_bytes;
+  long long* gptr;               // [kMaxGroupPtrs operands | kMaxGroupPtrs stores] addresses
+  int4* gins;                    // the running group's vector instructions
+  uint64_t* bars;                // "full" mbarrier per stage (bulk-copy bytes landed)
+  uint64_t* empty;               // "empty" mbarrier per stage (all warps done with it)
+  long long* stk;                // [max_stack][TILE] spilled stack entries
+  uint32_t* uses;                // completed phases per stage mbarrier
   long long* red;                // [TPB/32][RMAX]
 };
 
@@ -129,7 +135,6 @@ __device__ __forceinline__ long long py_imod(long long a, long long b) {
   if (r != 0 && ((r < 0) != (b < 0))) r += b;
   return r;
 }
-__device__ __forceinline__ long long py_ifloordiv_guard(long long b) { return b; }
 
 // One reference binop on words (tensor.py:227-287).  `dts` = dta | dtb << 4 | dto << 8.
 __device__ __forceinline__ long long binop_w(int op, int dts, long long a, long long b, bool& div0) {
@@ -177,14 +182,6 @@ __device__ __forceinline__ long long unop_w(int op, int dts, long long a) {
     default: return as_w(sigmoid_ref(num(a, dta)));
   }
 }
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
-               :: "r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
   unsigned int v;
@@ -362,23 +359,46 @@ __device__ __forceinline__ Group decode(const int32_t* g) {
   return G;
 }
 
-// element j (0..3) of this thread within a tile: pair j>>1, lane-pair offset j&1
-__device__ __forceinline__ int elem_of(int j) { return (j >> 1) * HALF + threadIdx.x * 2 + (j & 1); }
+// Element j (0..EPT-1) of this thread within a tile: pair j>>1 of the thread
+// sits at (j>>1)*(2*TPB) + 2*tid, so every 16-byte access of a warp is one
+// contiguous 512-byte run (coalesced HBM stores, conflict-free LDS.128).
+__device__ __forceinline__ int elem_of(int j) { return (j >> 1) * (2 * TPB) + threadIdx.x * 2 + (j & 1); }
 
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const uint32_t addr = (uint32_t)__cvta_generic_to_shared(bar);
+  while (!ok) {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                  "r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+
+// One elected thread stages every vector operand of `tile` into stage `st`
+// (one 1-D bulk copy per operand, completion counted in bytes on the stage's
+// mbarrier).  The last tile is rounded up to 16 bytes; buffers are padded.
 __device__ __forceinline__ void issue_tile(const StreamArgs& a, const Smem& s, const Group& G, long long tile,
-                                           int stage) {
+                                           int st, int nops) {
   const long long base = tile * TILE;
+  const long long left = a.n - base;
+  const uint32_t bytes = (uint32_t)(((left < TILE ? left : TILE) * 8 + 15) & ~15ll);
+  uint64_t* bar = s.bars + st;
+  mbar_expect_tx(bar, bytes * G.nops);
   for (int k = 0; k < G.nops; ++k) {
-    const long long* src = reinterpret_cast<const long long*>(s.gptr[k]);
-    long long* dst = s.stage + ((long long)stage * a.max_ops + k) * TILE;
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {
-      const int e = p * HALF + threadIdx.x * 2;
-      const long long ge = base + e;
-      const long long left = a.n - ge;
-      const int bytes = left >= 2 ? 16 : left == 1 ? 8 : 0;
-      cp_async16(static_cast<uint32_t>(__cvta_generic_to_shared(dst + e)), bytes ? src + ge : src, bytes);
-    }
+    const long long* src = reinterpret_cast<const long long*>(s.gptr[k]) + base;
+    bulk_g2s(s.stage + ((long long)st * nops + k) * TILE, src, bytes, bar);
   }
 }
 
@@ -396,146 +416,199 @@ __device__ __forceinline__ long long red_combine(int kd, long long x, long long 
   return kind == 0 ? x + y : (y > x ? y : x);
 }
 
-__device__ void vector_run(const StreamArgs& a, Smem& s, const Group& G, int pc, long long racc[RMAX]) {
-  const long long ntiles = (a.n + TILE - 1) / TILE;
-  const int tid = threadIdx.x;
-  int div0_q = 1 << 30;   // first vector instruction that divided by zero
-  for (int r = 0; r < RMAX; ++r) racc[r] = r < G.nred ? red_identity(G.red_kd[r]) : 0;
-  long long nmy = 0;
-  if (blockIdx.x < ntiles) nmy = (ntiles - 1 - blockIdx.x) / gridDim.x + 1;
-  // prologue
+// This thread's EPT elements of a tile-sized shared-memory vector (stage,
+// temporary or spill slot): two LDS.128 / STS.128, bank-conflict free.
+__device__ __forceinline__ void lds_lane(const long long* p, long long (&v)[EPT]) {
 #pragma unroll
-  for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nmy) issue_tile(a, s, G, blockIdx.x + (long long)st * gridDim.x, st);
-    cp_async_commit();
+  for (int j = 0; j < EPT; j += 2) {
+    const longlong2 t = *reinterpret_cast<const longlong2*>(p + elem_of(j));
+    v[j] = t.x; v[j + 1] = t.y;
   }
-  for (long long i = 0; i < nmy; ++i) {
-    const long long nxt = i + STAGES - 1;
-    if (nxt < nmy) issue_tile(a, s, G, blockIdx.x + nxt * gridDim.x, (int)(nxt % STAGES));
-    cp_async_commit();
-    cp_async_wait<STAGES - 1>();
-    const long long tile = blockIdx.x + i * gridDim.x;
-    const long long base = tile * TILE;
-    const long long* stage = s.stage + (long long)(i % STAGES) * a.max_ops * TILE;
-    long long tos[EPT];
+}
+__device__ __forceinline__ void sts_lane(long long* p, const long long (&v)[EPT]) {
+#pragma unroll
+  for (int j = 0; j < EPT; j += 2) *reinterpret_cast<longlong2*>(p + elem_of(j)) = make_longlong2(v[j], v[j + 1]);
+}
+
+// Device encoding of the fused group's stack program (stream.py emits it):
+// the operand source is folded into the opcode so one switch dispatches.
+// Values a group both stores and reuses are recomputed from staged operands
+// by the compiler, so there are no temporaries: only the top of stack lives
+// in registers and rare spills go to a shared-memory stack.
+enum DOp : int {
+  D_PUSH_VEC = 1, D_PUSH_SCALAR = 2, D_BIN_VEC = 4, D_BIN_SCALAR = 5, D_BIN_STACK = 7, D_UN = 8,
+  D_SEL = 9, D_STORE = 10, D_RED = 11, D_POP = 13
+};
+
+__device__ __forceinline__ void lds2(uint32_t addr, long long& x, long long& y) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(addr));
+}
+__device__ __forceinline__ void sts2(uint32_t addr, long long x, long long y) {
+  asm volatile("st.shared.v2.u64 [%0], {%1, %2};" :: "r"(addr), "l"(x), "l"(y) : "memory");
+}
+// This thread's EPT elements of a tile-sized shared-memory vector at `addr`.
+__device__ __forceinline__ void lds_lane(uint32_t addr, long long (&v)[EPT]) {
+#pragma unroll
+  for (int j = 0; j < EPT; j += 2) lds2(addr + 8u * elem_of(j), v[j], v[j + 1]);
+}
+__device__ __forceinline__ void sts_lane(uint32_t addr, const long long (&v)[EPT]) {
+#pragma unroll
+  for (int j = 0; j < EPT; j += 2) sts2(addr + 8u * elem_of(j), v[j], v[j + 1]);
+}
+
+// TOS <- (TOS op val) or (val op TOS); the operation is uniform, so the
+// branch on it sits outside the element loop.
+__device__ __forceinline__ void bin_lane(long long (&tos)[EPT], const long long (&val)[EPT], int bz, int dts,
+                                         bool tos_left, long long base, long long n, int q, int& div0_q) {
+  const int bop = bz & 255;
+  if (dts == (DT_F64 | DT_F64 << 4 | DT_F64 << 8) && bop <= B_MUL) {
+    double l[EPT], r[EPT];
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      l[j] = as_f(tos_left ? tos[j] : val[j]);
+      r[j] = as_f(tos_left ? val[j] : tos[j]);
+    }
+    if (bop == B_ADD) {
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) tos[j] = as_w(l[j] + r[j]);
+    } else if (bop == B_SUB) {
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) tos[j] = as_w(l[j] - r[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) tos[j] = as_w(l[j] * r[j]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    const long long l = tos_left ? tos[j] : val[j], r = tos_left ? val[j] : tos[j];
+    bool d = false;
+    tos[j] = binop_w(bop, dts, l, r, d);
+    if (d && base + elem_of(j) < n && q < div0_q) div0_q = q;
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+// The fused group over this CTA's tiles.  Operands arrive by bulk copy into a
+// ring of S stages (full[st]: bytes landed; empty[st]: every warp is done with
+// the stage), the stack program runs over EPT elements per thread, results are
+// stored straight to HBM and reductions end in one per-CTA partial + arrival.
+__device__ __forceinline__ void vector_run(const StreamArgs& a, Smem& s, Ctl& c, const Group& G, int pc) {
+  const long long ntiles = (a.n + TILE - 1) / TILE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nops = G.nops < 1 ? 1 : G.nops;
+  int S = (int)(s.stage_bytes / ((long long)nops * TILE * 8));   // deepest pipeline the operands allow
+  if (S > kMaxStages) S = kMaxStages;
+  int div0_q = 1 << 30;   // first vector instruction that divided by zero
+  long long racc[RMAX];
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) racc[r] = r < G.nred ? red_identity(G.red_kd[r]) : 0;
+  const int nmy = blockIdx.x < ntiles ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  if (tid == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // generic stores -> bulk-copy reads
+    for (int st = 0; st < S - 1 && st < nmy; ++st)
+      issue_tile(a, s, G, blockIdx.x + (long long)st * gridDim.x, st, nops);
+  }
+  const int4* ins = s.gins;
+  const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(s.stage);
+  const uint32_t stk0 = (uint32_t)__cvta_generic_to_shared(s.stk);
+  int st = 0, round = 0;        // stage of tile i, and how many times it was used before in this group
+  int pst = S - 1, pround = 0;  // producer: stage / round of tile i + S - 1
+  for (int i = 0; i < nmy; ++i) {
+    if (tid == 0 && i + S - 1 < nmy) {
+      if (pround > 0)   // wait until every warp released this stage's previous tile
+        mbar_wait(s.empty + pst, (s.uses[pst] + (uint32_t)pround - 1) & 1);
+      issue_tile(a, s, G, blockIdx.x + (long long)(i + S - 1) * gridDim.x, pst, nops);
+    }
+    if (++pst == S) { pst = 0; ++pround; }
+    mbar_wait(s.bars + st, (s.uses[st] + (uint32_t)round) & 1);   // uses[] advance after the loop
+    const long long base = (blockIdx.x + (long long)i * gridDim.x) * TILE;
+    const bool full = base + TILE <= a.n;
+    const uint32_t stage = stage0 + (uint32_t)(st * nops * TILE * 8);
+    long long tos[EPT], val[EPT];
     int sp = 0;
-#pragma unroll
-    for (int j = 0; j < EPT; ++j) tos[j] = 0;
     for (int q = 0; q < G.ninstr; ++q) {
-      const int32_t* w = G.ins + 4 * q;
-      const int op = w[0];
-      if (op == V_PUSH || op == V_BIN) {
-        // fetch the explicit operand (vector stage / scalar / temp) into `val`
-        const int src = op == V_PUSH ? w[1] : (w[1] >> 12) & 15;
-        const int idx = w[2];
-        long long val[EPT];
-        if (src == SRC_VEC) {
-          const long long* p = stage + (long long)idx * TILE;
+      const int4 w = ins[q];
+      switch (w.x) {
+        case D_PUSH_VEC:
+          if (w.z) sts_lane(stk0 + (uint32_t)(sp++ * TILE * 8), tos);
+          lds_lane(stage + (uint32_t)(w.y * TILE * 8), tos);
+          break;
+        case D_PUSH_SCALAR: {
+          if (w.z) sts_lane(stk0 + (uint32_t)(sp++ * TILE * 8), tos);
+          const long long v = s.W[w.y];
 #pragma unroll
-          for (int j = 0; j < EPT; j += 2) {
-            const longlong2 v = *reinterpret_cast<const longlong2*>(p + elem_of(j));
-            val[j] = v.x; val[j + 1] = v.y;
-          }
-        } else if (src == SRC_SCALAR) {
-          const long long v = s.W[idx];
+          for (int j = 0; j < EPT; ++j) tos[j] = v;
+          break;
+        }
+        case D_BIN_VEC:
+          lds_lane(stage + (uint32_t)(w.y * TILE * 8), val);
+          bin_lane(tos, val, w.z, w.w, !((w.z >> 8) & 1), base, a.n, q, div0_q);
+          break;
+        case D_BIN_SCALAR: {
+          const long long v = s.W[w.y];
 #pragma unroll
           for (int j = 0; j < EPT; ++j) val[j] = v;
-        } else if (src == SRC_TEMP) {
-          const long long* p = s.tmp + (long long)idx * TILE;
-#pragma unroll
-          for (int j = 0; j < EPT; j += 2) {
-            const longlong2 v = *reinterpret_cast<const longlong2*>(p + elem_of(j));
-            val[j] = v.x; val[j + 1] = v.y;
-          }
-        } else {   // SRC_STACK: pop the second operand
-          --sp;
-          const long long* p = s.stk + (long long)sp * TILE;
-#pragma unroll
-          for (int j = 0; j < EPT; j += 2) {
-            const longlong2 v = *reinterpret_cast<const longlong2*>(p + elem_of(j));
-            val[j] = v.x; val[j + 1] = v.y;
-          }
+          bin_lane(tos, val, w.z, w.w, !((w.z >> 8) & 1), base, a.n, q, div0_q);
+          break;
         }
-        if (op == V_PUSH) {
-          if (w[3]) {   // spill the current TOS
-            long long* p = s.stk + (long long)sp * TILE;
+        case D_BIN_STACK:   // left = popped value, right = TOS
+          lds_lane(stk0 + (uint32_t)(--sp * TILE * 8), val);
+          bin_lane(tos, val, w.z, w.w, false, base, a.n, q, div0_q);
+          break;
+        case D_UN:
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) tos[j] = unop_w(w.y, w.w, tos[j]);
+          break;
+        case D_SEL: {   // c, x spilled (c deeper), TOS = y
+          long long x[EPT];
+          lds_lane(stk0 + (uint32_t)(--sp * TILE * 8), x);
+          lds_lane(stk0 + (uint32_t)(--sp * TILE * 8), val);
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) tos[j] = val[j] ? x[j] : tos[j];
+          break;
+        }
+        case D_STORE: {
+          long long* dst = reinterpret_cast<long long*>(s.gptr[kMaxGroupPtrs + w.y]) + base;
+          if (full) {
 #pragma unroll
             for (int j = 0; j < EPT; j += 2)
-              *reinterpret_cast<longlong2*>(p + elem_of(j)) = make_longlong2(tos[j], tos[j + 1]);
-            ++sp;
-          }
-#pragma unroll
-          for (int j = 0; j < EPT; ++j) tos[j] = val[j];
-        } else {
-          const int bop = w[1] & 255, rev = (w[1] >> 8) & 1, dts = w[3];
-          // stack form: left = popped value, right = TOS; explicit operand: rev=0 -> TOS op val
-          const bool tos_left = (src == SRC_STACK) ? false : !rev;
-          if (dts == (DT_F64 | DT_F64 << 4 | DT_F64 << 8) && bop <= B_MUL) {
-#pragma unroll
-            for (int j = 0; j < EPT; ++j) {
-              const double l = as_f(tos_left ? tos[j] : val[j]), r = as_f(tos_left ? val[j] : tos[j]);
-              tos[j] = as_w(bop == B_ADD ? l + r : bop == B_SUB ? l - r : l * r);
-            }
+              *reinterpret_cast<longlong2*>(dst + elem_of(j)) = make_longlong2(tos[j], tos[j + 1]);
           } else {
 #pragma unroll
-            for (int j = 0; j < EPT; ++j) {
-              const long long l = tos_left ? tos[j] : val[j], r = tos_left ? val[j] : tos[j];
-              bool d = false;
-              tos[j] = binop_w(bop, dts, l, r, d);
-              if (d && base + elem_of(j) < a.n && q < div0_q) div0_q = q;
-            }
+            for (int j = 0; j < EPT; ++j)
+              if (base + elem_of(j) < a.n) dst[elem_of(j)] = tos[j];
           }
+          break;
         }
-      } else if (op == V_UN) {
+        case D_RED: {
+          const int kd = G.red_kd[w.y];
 #pragma unroll
-        for (int j = 0; j < EPT; ++j) tos[j] = unop_w(w[1], w[3], tos[j]);
-      } else if (op == V_SEL) {   // c, x popped (c deeper), TOS = y
-        const long long* px = s.stk + (long long)(sp - 1) * TILE;
-        const long long* pc_ = s.stk + (long long)(sp - 2) * TILE;
-        sp -= 2;
+          for (int rr = 0; rr < RMAX; ++rr) {
+            if (rr != w.y) continue;
 #pragma unroll
-        for (int j = 0; j < EPT; ++j) {
-          const int e = elem_of(j);
-          tos[j] = pc_[e] ? px[e] : tos[j];
-        }
-      } else if (op == V_STORE) {
-        long long* dst = reinterpret_cast<long long*>(s.gptr[kMaxGroupPtrs + w[1]]);
-#pragma unroll
-        for (int j = 0; j < EPT; j += 2) {
-          const long long ge = base + elem_of(j);
-          if (ge + 1 < a.n) {
-            *reinterpret_cast<longlong2*>(dst + ge) = make_longlong2(tos[j], tos[j + 1]);
-          } else if (ge < a.n) {
-            dst[ge] = tos[j];
+            for (int j = 0; j < EPT; ++j)
+              if (full || base + elem_of(j) < a.n) racc[rr] = red_combine(kd, racc[rr], tos[j]);
           }
+          break;
         }
-      } else if (op == V_RED) {
-        const int r = w[1];
-        const int kd = G.red_kd[r];
-#pragma unroll
-        for (int rr = 0; rr < RMAX; ++rr) {
-          if (rr != r) continue;
-#pragma unroll
-          for (int j = 0; j < EPT; ++j)
-            if (base + elem_of(j) < a.n) racc[rr] = red_combine(kd, racc[rr], tos[j]);
-        }
-      } else if (op == V_SAVE) {
-        long long* p = s.tmp + (long long)w[1] * TILE;
-#pragma unroll
-        for (int j = 0; j < EPT; j += 2)
-          *reinterpret_cast<longlong2*>(p + elem_of(j)) = make_longlong2(tos[j], tos[j + 1]);
-      } else if (op == V_POP) {
-        --sp;
-        const long long* p = s.stk + (long long)sp * TILE;
-#pragma unroll
-        for (int j = 0; j < EPT; j += 2) {
-          const longlong2 v = *reinterpret_cast<const longlong2*>(p + elem_of(j));
-          tos[j] = v.x; tos[j + 1] = v.y;
-        }
+        default:   // D_POP
+          lds_lane(stk0 + (uint32_t)(--sp * TILE * 8), tos);
+          break;
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(s.empty + st);   // this warp is done with stage `st`
+    if (++st == S) { st = 0; ++round; }
   }
-  cp_async_wait<0>();
+  __syncthreads();
+  if (tid == 0)
+    for (int k = 0; k < S; ++k) s.uses[k] += (uint32_t)(nmy > k ? (nmy - 1 - k) / S + 1 : 0);
   if (__syncthreads_or(div0_q != (1 << 30))) {
     __shared__ int first_q;
     if (tid == 0) first_q = 1 << 30;
@@ -544,23 +617,51 @@ __device__ void vector_run(const StreamArgs& a, Smem& s, const Group& G, int pc,
     __syncthreads();
     if (tid == 0) report(a.ctl, pc, E_DIV0, first_q);   // host maps (pc, q) -> node
   }
+  if (G.nred > 0) {
+    // block reduce in a fixed order, then one arrival per CTA
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      if (r >= G.nred) break;
+      long long v = racc[r];
+      for (int o = 16; o; o >>= 1) v = red_combine(G.red_kd[r], v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) s.red[warp * RMAX + r] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int gen = c.barrier_gen;
+      for (int r = 0; r < G.nred; ++r) {
+        long long v = s.red[r];
+        for (int w = 1; w < TPB / 32; ++w) v = red_combine(G.red_kd[r], v, s.red[w * RMAX + r]);
+        a.part[((long long)(gen & 1) * RMAX + r) * gridDim.x + blockIdx.x] = v;
+      }
+      __threadfence();
+      atomicAdd(&a.ctl->arrive, 1u);
+      c.barrier_gen = gen + 1;
+    }
+  }
 }
 
-__global__ void __launch_bounds__(TPB) stream_kernel(StreamArgs a) {
+__global__ void __launch_bounds__(TPB, 1) stream_kernel(StreamArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Ctl c;
   Smem s;
   {
     unsigned char* p = smem_raw;
     auto take = [&](size_t bytes) { unsigned char* r = p; p += (bytes + 15) & ~size_t(15); return r; };
-    s.stage = reinterpret_cast<long long*>(take(sizeof(long long) * STAGES * a.max_ops * TILE));
+    s.bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * kMaxStages));
+    s.empty = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * kMaxStages));
     s.stk = reinterpret_cast<long long*>(take(sizeof(long long) * a.max_stack * TILE));
-    s.tmp = reinterpret_cast<long long*>(take(sizeof(long long) * a.max_temp * TILE));
+    s.uses = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxStages));
+    s.gins = reinterpret_cast<int4*>(take(sizeof(int4) * kMaxInstr));
     s.W = reinterpret_cast<long long*>(take(sizeof(long long) * a.nwords));
     s.gptr = reinterpret_cast<long long*>(take(sizeof(long long) * 2 * kMaxGroupPtrs));
     s.red = reinterpret_cast<long long*>(take(sizeof(long long) * (TPB / 32) * RMAX));
     s.rc = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * a.nbuf));
     s.freel = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * a.nbuf));
+    // everything left of the budget stages the running group's operands
+    p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
+    s.stage = reinterpret_cast<long long*>(p);
+    s.stage_bytes = a.smem - (long long)(p - smem_raw);
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < a.nwords; i += TPB) s.W[i] = a.w_init[i];
@@ -572,9 +673,14 @@ __global__ void __launch_bounds__(TPB) stream_kernel(StreamArgs a) {
       if (a.rc_init[i] == 0) s.freel[nf++] = i; else ++live;
     }
     c.nfree = nf; c.live = live; c.max_live = live;
+    for (int st = 0; st < kMaxStages; ++st) {
+      mbar_init(s.bars + st, 1);
+      mbar_init(s.empty + st, TPB / 32);
+      s.uses[st] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  long long racc[RMAX];
   for (;;) {
     if (warp == 0) {
       for (;;) {
@@ -624,28 +730,9 @@ __global__ void __launch_bounds__(TPB) stream_kernel(StreamArgs a) {
         s.gptr[tid < G.nops ? tid : kMaxGroupPtrs + tid - G.nops] = a.bufptr[id];
       }
     }
+    for (int q = tid; q < 4 * G.ninstr; q += TPB) reinterpret_cast<int*>(s.gins)[q] = G.ins[q];
     if (__syncthreads_or(bad)) break;   // identical in every CTA: all stop here
-    vector_run(a, s, G, pc, racc);
-    if (G.nred > 0) {
-      // block reduce in a fixed order, then one arrival per CTA
-      for (int r = 0; r < G.nred; ++r) {
-        long long v = racc[r];
-        for (int o = 16; o; o >>= 1) v = red_combine(G.red_kd[r], v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (lane == 0) s.red[warp * RMAX + r] = v;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        const int gen = c.barrier_gen;
-        for (int r = 0; r < G.nred; ++r) {
-          long long v = s.red[r];
-          for (int w = 1; w < TPB / 32; ++w) v = red_combine(G.red_kd[r], v, s.red[w * RMAX + r]);
-          a.part[((long long)(gen & 1) * RMAX + r) * gridDim.x + blockIdx.x] = v;
-        }
-        __threadfence();
-        atomicAdd(&a.ctl->arrive, 1u);
-        c.barrier_gen = gen + 1;
-      }
-    }
+    vector_run(a, s, c, G, pc);
     if (tid == 0) c.pc = pc + 1;
     __syncthreads();
   }
@@ -660,10 +747,22 @@ __global__ void __launch_bounds__(TPB) stream_kernel(StreamArgs a) {
   }
 }
 
-size_t smem_bytes(int max_ops, int max_stack, int max_temp, int nwords, int nbuf) {
+size_t fixed_bytes(int max_stack, int max_temp, int nwords, int nbuf) {
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
-  return r(8ull * STAGES * max_ops * TILE) + r(8ull * max_stack * TILE) + r(8ull * max_temp * TILE) +
-         r(8ull * nwords) + r(8ull * 2 * kMaxGroupPtrs) + r(8ull * (TPB / 32) * RMAX) + 2 * r(4ull * nbuf);
+  (void)max_temp;   // groups recompute reused values: no temporaries
+  return r(8ull * max_stack * TILE) + r(16ull * kMaxStages) + r(4ull * kMaxStages) +
+         r(16ull * kMaxInstr) + r(8ull * nwords) + r(8ull * 2 * kMaxGroupPtrs) + r(8ull * (TPB / 32) * RMAX) +
+         2 * r(4ull * nbuf) + 128;
+}
+
+// The whole budget when the widest group still gets a double-buffered pipeline.
+size_t smem_bytes(int max_ops, int max_stack, int max_temp, int nwords, int nbuf) {
+  if (max_ops < 1) max_ops = 1;
+  if (max_stack < 1) max_stack = 1;
+  if (max_temp < 1) max_temp = 1;
+  const size_t fixed = fixed_bytes(max_stack, max_temp, nwords, nbuf);
+  const size_t need = fixed + 2ull * max_ops * TILE * 8;
+  return need > (size_t)kSmemBudget ? need : (size_t)kSmemBudget;
 }
 
 }  // namespace
@@ -691,7 +790,7 @@ extern "C" int skb_stream_run(const void* prog, const int32_t* extra, const int6
                               const int64_t* bufptr, const int32_t* rc_init, int64_t* part, void* ctl,
                               int64_t n, int nwords, int nbuf, int max_ops, int max_stack, int max_temp,
                               int64_t max_steps, int grid, int64_t smem, void* stream) {
-  if (grid <= 0 || n <= 0) return SKB_ERR_INVALID;
+  if (grid <= 0 || n <= 0 || max_stack > 3) return SKB_ERR_INVALID;
   StreamArgs a;
   a.prog = reinterpret_cast<const SIns*>(prog);
   a.extra = extra;
@@ -708,6 +807,9 @@ extern "C" int skb_stream_run(const void* prog, const int32_t* extra, const int6
   a.max_stack = max_stack < 1 ? 1 : max_stack;
   a.max_temp = max_temp < 1 ? 1 : max_temp;
   a.max_steps = max_steps;
+  a.smem = smem;
+  if ((size_t)smem < fixed_bytes(a.max_stack, a.max_temp, nwords, nbuf) + 2ull * a.max_ops * TILE * 8)
+    return SKB_ERR_INVALID;
   if (cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SKB_ERR_CUDA;
   void* params[] = {&a};

@@ -17,8 +17,9 @@ Compilation (value classes, reference semantics in parentheses):
   emitted one by one: they are kept as pending expression trees and fused
   into the consumer, so `q - al * y` is one pass over q and y;
 * a fused group (VEXEC) collects every expression materialised or reduced
-  between two points where the scalar side needs a result; values reused in
-  the same group come from shared-memory temporaries, never from a re-read;
+  between two points where the scalar side needs a result; a value the group
+  stores and reuses is recomputed from the staged operands (cheap flops, no
+  HBM re-read, no temporaries);
 * each reduction (tensor.py:335-353) ends in RFIN: the only cross-CTA
   exchange, combined in a fixed order so every CTA holds the same bits.
 
@@ -48,8 +49,8 @@ BIN = {"Add": 0, "Sub": 1, "Mul": 2, "Div": 3, "Mod": 4, "Lt": 5, "Gt": 6, "Le":
 UN = {"Neg": 0, "Not": 1, "Tanh": 2, "Sigmoid": 3}
 DT = {"f64": 0, "i64": 1, "bool": 2}
 DT_NAME = {v: k for k, v in DT.items()}
-RMAX = 8
-TPB, TILE, STAGES = 256, 1024, 3
+RMAX = 4
+TPB, TILE = 512, 2048
 MAX_OPS, MAX_TEMP, MAX_STACK = 5, 4, 3
 CAUSE = {10: E.INDEX_OUT_OF_RANGE, 11: E.EMPTY_POP, 12: E.SHAPE_MISMATCH, 13: E.DIVISION_BY_ZERO,
          14: E.ITERATION_LIMIT, 15: E.ASSERTION_FAILED, 16: E.DTYPE_MISMATCH}
@@ -96,9 +97,8 @@ class Group:
     reds: list = field(default_factory=list)       # (kind|dt<<4, dst word)
     code: list = field(default_factory=list)       # 4-int vector instructions
     reads: set = field(default_factory=set)        # words read (vector + scalar)
-    temp_of: dict = field(default_factory=dict)    # word -> temp index
+    expr_of: dict = field(default_factory=dict)    # stored word -> its expression (recomputed on reuse)
     uids: dict = field(default_factory=dict)       # vector instruction index -> node uid
-    ntemp: int = 0
     depth: int = 0
 
     def empty(self):
@@ -222,6 +222,33 @@ def _result_dtype(op, a, b):
     return "f64" if "f64" in (a, b) else "i64"
 
 
+# device encoding (csrc/stream.cu DOp): the operand source folded into the opcode
+D_PUSH = {SRC_VEC: 1, SRC_SCALAR: 2}
+D_BIN = {SRC_VEC: 4, SRC_SCALAR: 5, SRC_STACK: 7}
+D_UN, D_SEL, D_STORE, D_RED, D_POP = 8, 9, 10, 11, 13
+
+
+def _device_code(code):
+    out = []
+    for k in range(0, len(code), 4):
+        op, x, y, z = code[k:k + 4]
+        if op == V_PUSH:                        # [src, idx, spill]
+            out += [D_PUSH[x], y, z, 0]
+        elif op == V_BIN:                       # [bop | rev << 8 | src << 12, idx, dts]
+            out += [D_BIN[(x >> 12) & 15], y, x & 0xFFF, z]
+        elif op == V_UN:
+            out += [D_UN, x, 0, z]
+        elif op == V_SEL:
+            out += [D_SEL, 0, 0, 0]
+        elif op == V_STORE:
+            out += [D_STORE, x, 0, 0]
+        elif op == V_RED:
+            out += [D_RED, x, 0, 0]
+        else:
+            out += [D_POP, 0, 0, 0]
+    return out
+
+
 # ------------------------------------------------------------------ compiler
 class _Compiler:
     def __init__(self, graph, shape, cap):
@@ -297,11 +324,10 @@ class _Compiler:
         self.grp = Group()
         red_words, self.red_words = self.red_words, set()
         self.max_ops = max(self.max_ops, len(g.ops))
-        self.max_temp = max(self.max_temp, g.ntemp)
         self.max_stack = max(self.max_stack, g.depth)
         self.ngroups += 1
         blk = [len(g.ops), len(g.stores), len(g.reds), len(g.code) // 4] + g.ops + g.stores + \
-            [kd for kd, _ in g.reds] + g.code
+            [kd for kd, _ in g.reds] + _device_code(g.code)
         off = self.extra_block(blk)
         self.vuids[len(self.code)] = g.uids
         self.code.append([SOP["VEXEC"], 0, off, 0, 0, 0, 0, 0])
@@ -329,21 +355,16 @@ class _Compiler:
         return s
 
     def materialize(self, e, s, node=None):
-        """Compute pending expression `e` into vector slot `s` in the open group."""
+        """Compute pending expression `e` into vector slot `s` in the open group.
+        Later readers in the same group recompute it from the staged operands
+        (csrc/stream.cu keeps no temporaries)."""
         self._prepare(e)
         self.semit("ALLOC", node or e.node, [s.word], writes=[s.word])
         g = self.grp
         self.gen(e)
         g.code += [V_STORE, len(g.stores), 0, 0]
         g.stores.append(s.word)
-        if e.uses > 1:   # reused later in this group: keep it in a temporary
-            if g.ntemp >= MAX_TEMP:
-                pass
-            else:
-                t = g.ntemp
-                g.ntemp += 1
-                g.code += [V_SAVE, t, 0, 0]
-                g.temp_of[s.word] = t
+        g.expr_of[s.word] = e
         e.slot = s
 
     def reduce_into(self, e, kind, dst, node):
@@ -359,15 +380,23 @@ class _Compiler:
         g.reds.append((kd, dst.word))
         self.red_words.add(dst.word)
 
+    def _expand(self, e):
+        """The expression to generate for `e` in the open group: values the
+        group itself stores are recomputed from their expression."""
+        g = self.grp
+        if isinstance(e, Leaf):
+            return g.expr_of.get(e.word, e) if e.vec else e
+        if e.slot is not None:
+            return g.expr_of.get(e.slot.word, Leaf(e.slot.word, e.dtype, True))
+        return e
+
     def _leaves(self, e, out):
+        e = self._expand(e)
         if isinstance(e, Leaf):
             out.append(e)
-        elif isinstance(e, Expr):
-            if e.slot is not None:
-                out.append(Leaf(e.slot.word, e.dtype, True))
-            else:
-                for a in e.args:
-                    self._leaves(a, out)
+        else:
+            for a in e.args:
+                self._leaves(a, out)
         return out
 
     def _prepare(self, e):
@@ -376,18 +405,19 @@ class _Compiler:
         leaves = self._leaves(e, [])
         if any((not l.vec) and l.word in self.red_words for l in leaves):
             self.flush()
+            leaves = self._leaves(e, [])
         g = self.grp
-        new_ops = {l.word for l in leaves if l.vec and l.word not in g.temp_of and l.word not in g.ops}
-        stale = any(l.vec and l.word in g.stores and l.word not in g.temp_of for l in leaves)
-        if stale or len(g.ops) + len(new_ops) > MAX_OPS or len(g.stores) >= 16:
+        new_ops = {l.word for l in leaves if l.vec and l.word not in g.ops}
+        if len(g.ops) + len(new_ops) > MAX_OPS or len(g.stores) >= 16:
             self.flush()
+            if len({l.word for l in self._leaves(e, []) if l.vec}) > MAX_OPS:
+                raise LoweringError("element-wise expression reads more vectors than one pass stages")
 
     def gen(self, e, live=0):
         """Postfix code leaving e's value in the TOS register.  `live` = values
         already on the virtual stack (TOS included)."""
         g = self.grp
-        if isinstance(e, Expr) and e.slot is not None:
-            e = Leaf(e.slot.word, e.dtype, True)
+        e = self._expand(e)
         if isinstance(e, Leaf):
             src, idx = self.leaf_src(e)
             g.code += [V_PUSH, src, idx, 1 if live > 0 else 0]
@@ -406,19 +436,18 @@ class _Compiler:
             return
         L, R = e.args
         dts = DT[L.dtype] | (DT[R.dtype] << 4) | (DT[e.dtype] << 8)
-        Lleaf = isinstance(L, Leaf) or (isinstance(L, Expr) and L.slot is not None)
-        Rleaf = isinstance(R, Leaf) or (isinstance(R, Expr) and R.slot is not None)
-        if Rleaf:
-            self.gen(L, live)
-            src, idx = self.leaf_src(self._as_leaf(R))
+        Lx, Rx = self._expand(L), self._expand(R)
+        if isinstance(Rx, Leaf):
+            self.gen(Lx, live)
+            src, idx = self.leaf_src(Rx)
             g.code += [V_BIN, e.code | (src << 12), idx, dts]
-        elif Lleaf:
-            self.gen(R, live)
-            src, idx = self.leaf_src(self._as_leaf(L))
+        elif isinstance(Lx, Leaf):
+            self.gen(Rx, live)
+            src, idx = self.leaf_src(Lx)
             g.code += [V_BIN, e.code | (1 << 8) | (src << 12), idx, dts]
         else:
-            self.gen(L, live)
-            self.gen(R, live + 1)
+            self.gen(Lx, live)
+            self.gen(Rx, live + 1)
             g.code += [V_BIN, e.code | (SRC_STACK << 12), 0, dts]
         if e.node is not None:
             g.uids[len(g.code) // 4 - 1] = e.node.uid
@@ -434,10 +463,8 @@ class _Compiler:
         g.reads.add(l.word)
         if not l.vec:
             return SRC_SCALAR, l.word
-        if l.word in g.temp_of:
-            return SRC_TEMP, g.temp_of[l.word]
         if l.word in g.stores:
-            raise LoweringError("internal: group reads a vector it stores without a temporary")
+            raise LoweringError("internal: group reads a vector it stores")
         if l.word not in g.ops:
             g.ops.append(l.word)
         return SRC_VEC, g.ops.index(l.word)
@@ -749,12 +776,23 @@ def _feed_tensor(v, dtype, dev):
         want = torch.float64 if dtype == "f64" else torch.int64
         if t.dtype != want:
             t = t.to(want)
-        if not t.is_contiguous() or t.data_ptr() % 16:
-            t = t.contiguous().clone()
+        if not t.is_contiguous() or t.data_ptr() % 16 or t.numel() % 2:
+            t = _padded(t)
         return t
     a = as_numpy(v).reshape(-1)
     a = a.astype(np.float64) if dtype == "f64" else a.astype(np.int64)
-    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    return _padded(torch.from_numpy(np.ascontiguousarray(a)).to(dev))
+
+
+def _padded(t):
+    """A 16-byte aligned copy whose length is even: the kernel stages whole
+    16-byte units, so the last tile of an odd-length vector reads one pad word."""
+    import torch
+    if t.numel() % 2 == 0 and t.is_contiguous() and t.data_ptr() % 16 == 0:
+        return t
+    out = torch.zeros(t.numel() + (t.numel() % 2), dtype=t.dtype, device=t.device)
+    out[:t.numel()].copy_(t.reshape(-1))
+    return out
 
 
 def run(prog: StreamProgram, feeds: dict, *, stream=None, pool: Optional[int] = None):
@@ -812,10 +850,15 @@ def run(prog: StreamProgram, feeds: dict, *, stream=None, pool: Optional[int] = 
         ctl = torch.zeros(8, dtype=torch.int64, device=dev)
         ctl[0] = -1
         g = min(grid, max(1, ntiles))
+        cs = torch.cuda.current_stream() if stream is None else stream
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(cs)
         rt.check(lib.skb_stream_run(rt.ptr(code), rt.ptr(extra), rt.ptr(w_in), rt.ptr(w_out), rt.ptr(bufptr),
                                     rt.ptr(rc), rt.ptr(part), rt.ptr(ctl), n, prog.nwords, nbuf, prog.max_ops,
                                     prog.max_stack, prog.max_temp, 1 << 40, g, smem,
                                     rt.stream_handle(stream)), "skb_stream_run")
+        ev1.record(cs)
         c = ctl.cpu().numpy()
         err = int(c[0])
         if err != -1:
@@ -826,7 +869,7 @@ def run(prog: StreamProgram, feeds: dict, *, stream=None, pool: Optional[int] = 
                 continue
             _raise(prog, code_, pc, int(c[1]))
         break
-    run.last = {"grid": g, "smem": smem, "pool": npool, "barriers": int(c[3]), "steps": int(c[2]),
+    run.last = {"kernel_ms": ev0.elapsed_time(ev1), "grid": g, "smem": smem, "pool": npool, "barriers": int(c[3]), "steps": int(c[2]),
                 "max_live": int(c[5]), "n": n}
     wo = w_out.cpu().numpy()
     outs = [_value(prog, s, wo, w_out, poolbuf, vec_feeds, nfeed, stride, n, shape) for s in prog.outputs]

@@ -161,7 +161,7 @@ def infer_dtype(v) -> str:
             return "f64" if v.dtype.is_floating_point else "i64"
     except ImportError:  # pragma: no cover
         pass
-    if isinstance(v, np.ndarray):
+    if isinstance(v, (np.ndarray, np.generic)):
         if v.dtype == np.bool_:
             return "bool"
         return "f64" if np.issubdtype(v.dtype, np.floating) else "i64"
@@ -196,6 +196,8 @@ def as_numpy(v) -> np.ndarray:
         pass
     if isinstance(v, np.ndarray):
         return v
+    if isinstance(v, np.generic):
+        return np.asarray(v)
     if hasattr(v, "dtype") and hasattr(v, "shape") and hasattr(v, "data"):
         # the reference's TensorValue: row-major tuple
         return np.asarray(v.data, dtype=NP_DTYPE[v.dtype]).reshape(tuple(v.shape))
