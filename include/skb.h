@@ -150,6 +150,7 @@ int skb_vm_max_ctas(void);
  *   n: elements per vector; grid from skb_stream_grid(smem). */
 int64_t skb_stream_smem_bytes(int max_ops, int max_stack, int max_temp, int nwords, int nbuf);
 int skb_stream_grid(int64_t smem_bytes);
+int skb_stream_tile_elems(void);   /* vector elements per CTA tile (grid sizing) */
 skb_status skb_stream_run(const void* prog_dev, const int32_t* extra_dev, const int64_t* w_init_dev,
                           int64_t* w_out_dev, const int64_t* bufptr_dev, const int32_t* rc_init_dev,
                           int64_t* part_dev, void* ctl_dev, int64_t n, int nwords, int nbuf, int max_ops,

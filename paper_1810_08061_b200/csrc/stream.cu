@@ -35,10 +35,17 @@
 #include <stdint.h>
 #include "skb_internal.h"
 
+#ifndef SKB_STREAM_TPB
+#define SKB_STREAM_TPB 512
+#endif
+#ifndef SKB_STREAM_EPT
+#define SKB_STREAM_EPT 4
+#endif
+
 namespace {
 
-constexpr int TPB = 512;
-constexpr int EPT = 4;              // elements per thread per tile (2 pairs)
+constexpr int TPB = SKB_STREAM_TPB;
+constexpr int EPT = SKB_STREAM_EPT;  // elements per thread per tile (EPT/2 pairs)
 constexpr int TILE = TPB * EPT;     // 2048 elements = 16 KB per staged operand
 constexpr int kMaxStages = 8;
 constexpr long long kSmemBudget = 220 * 1024;   // dynamic shared memory the kernel may use
@@ -532,8 +539,10 @@ __device__ __forceinline__ void vector_run(const StreamArgs& a, Smem& s, Ctl& c,
     const uint32_t stage = stage0 + (uint32_t)(st * nops * TILE * 8);
     long long tos[EPT], val[EPT];
     int sp = 0;
+    int4 wn = ins[0];
     for (int q = 0; q < G.ninstr; ++q) {
-      const int4 w = ins[q];
+      const int4 w = wn;
+      wn = ins[q + 1];   // next dispatch word in flight while this one executes (gins is padded)
       switch (w.x) {
         case D_PUSH_VEC:
           if (w.z) sts_lane(stk0 + (uint32_t)(sp++ * TILE * 8), tos);
@@ -652,7 +661,7 @@ __global__ void __launch_bounds__(TPB, 1) stream_kernel(StreamArgs a) {
     s.empty = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * kMaxStages));
     s.stk = reinterpret_cast<long long*>(take(sizeof(long long) * a.max_stack * TILE));
     s.uses = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxStages));
-    s.gins = reinterpret_cast<int4*>(take(sizeof(int4) * kMaxInstr));
+    s.gins = reinterpret_cast<int4*>(take(sizeof(int4) * (kMaxInstr + 1)));
     s.W = reinterpret_cast<long long*>(take(sizeof(long long) * a.nwords));
     s.gptr = reinterpret_cast<long long*>(take(sizeof(long long) * 2 * kMaxGroupPtrs));
     s.red = reinterpret_cast<long long*>(take(sizeof(long long) * (TPB / 32) * RMAX));
@@ -751,7 +760,7 @@ size_t fixed_bytes(int max_stack, int max_temp, int nwords, int nbuf) {
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
   (void)max_temp;   // groups recompute reused values: no temporaries
   return r(8ull * max_stack * TILE) + r(16ull * kMaxStages) + r(4ull * kMaxStages) +
-         r(16ull * kMaxInstr) + r(8ull * nwords) + r(8ull * 2 * kMaxGroupPtrs) + r(8ull * (TPB / 32) * RMAX) +
+         r(16ull * (kMaxInstr + 1)) + r(8ull * nwords) + r(8ull * 2 * kMaxGroupPtrs) + r(8ull * (TPB / 32) * RMAX) +
          2 * r(4ull * nbuf) + 128;
 }
 
@@ -766,6 +775,8 @@ size_t smem_bytes(int max_ops, int max_stack, int max_temp, int nwords, int nbuf
 }
 
 }  // namespace
+
+extern "C" int skb_stream_tile_elems(void) { return TILE; }
 
 extern "C" int64_t skb_stream_smem_bytes(int max_ops, int max_stack, int max_temp, int nwords, int nbuf) {
   return (int64_t)smem_bytes(max_ops, max_stack, max_temp, nwords, nbuf);

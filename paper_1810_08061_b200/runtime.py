@@ -16,7 +16,7 @@ import threading
 from .errors import BackendUnavailable, DeviceError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libskb.so")
+LIB_PATH = os.environ.get("SKB_LIB_PATH") or os.path.join(HERE, "libskb.so")   # override: A/B builds
 
 SKB_OK = 0
 SKB_ERR_INVALID = 1
@@ -56,6 +56,7 @@ SIGNATURES = {
     "skb_vm_max_ctas": (ctypes.c_int, []),
     "skb_stream_smem_bytes": (ctypes.c_int64, [ctypes.c_int] * 5),
     "skb_stream_grid": (ctypes.c_int, [ctypes.c_int64]),
+    "skb_stream_tile_elems": (ctypes.c_int, []),
     "skb_stream_run": (ctypes.c_int, [_VP] * 8 + [ctypes.c_int64] + [ctypes.c_int] * 5 +
                        [ctypes.c_int64, ctypes.c_int, ctypes.c_int64, _VP]),
     "skb_diag_umma_gemm": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP]),

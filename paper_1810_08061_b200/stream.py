@@ -408,7 +408,7 @@ class _Compiler:
             leaves = self._leaves(e, [])
         g = self.grp
         new_ops = {l.word for l in leaves if l.vec and l.word not in g.ops}
-        if len(g.ops) + len(new_ops) > MAX_OPS or len(g.stores) >= 16:
+        if len(g.ops) + len(new_ops) > MAX_OPS or len(g.stores) >= 16 or len(g.code) // 4 > 192:
             self.flush()
             if len({l.word for l in self._leaves(e, []) if l.vec}) > MAX_OPS:
                 raise LoweringError("element-wise expression reads more vectors than one pass stages")
@@ -835,7 +835,8 @@ def run(prog: StreamProgram, feeds: dict, *, stream=None, pool: Optional[int] = 
     grid = int(lib.skb_stream_grid(smem))
     if grid <= 0:
         raise LoweringError(f"vector-stream program needs {smem} B of shared memory")
-    ntiles = (n + TILE - 1) // TILE
+    tile = int(lib.skb_stream_tile_elems())
+    ntiles = (n + tile - 1) // tile
     for attempt in range(6):
         nbuf = nfeed + npool
         poolbuf = torch.empty(npool * stride, dtype=torch.int64, device=dev)
