@@ -132,6 +132,40 @@ skb_status skb_vm_run(const void* prog_dev, const int32_t* extra_dev, void* slot
 int skb_vm_max_ctas(void);
 
 /* ---------------------------------------------------------------------------
+ * Staged decoder with a data-dependent EOS stop (BASELINE config C3; csrc/beam.cu).
+ *
+ * The reference can stage greedy decoding (a `break` on EOS
+ * lowered into the While test, runtime/dispatch.py:275-387 +
+ * transforms/lowering.py:95-115, executed by graph/execute.py:218-238) but its
+ * IR has no log-softmax / top-k (graph/ir.py:19-27), so beam search is this
+ * extension entry; semantics in oracle/beam.py, pinned at beam 1 against the
+ * reference's greedy program.  All matrices row-major fp32:
+ *   h0 [S,H], c0 [S,H] (LSTM) or NULL, emb [V,E],
+ *   w_gates [(E+H), G] with G = 4H (LSTM, gate order i,f,g,o) or H (RNN_TANH:
+ *   [w_in; u]), b_gates [G] or NULL, w_out [H,V], b_out [V] or NULL.
+ * Outputs (device): tokens [S,K,max_len+1] (position 0 = BOS 0), scores [S,K]
+ * (sum of log-probabilities, best first), lengths [S,K]; steps_out (host) =
+ * decode steps executed (<= max_len; fewer when every beam hit EOS).
+ * ------------------------------------------------------------------------- */
+typedef struct skb_decode_shape {
+  int32_t cell;        /* SKB_CELL_LSTM or SKB_CELL_RNN_TANH */
+  int32_t sentences;   /* S */
+  int32_t beam;        /* K, 1..8 (1 = greedy) */
+  int32_t vocab;       /* V */
+  int32_t embed;       /* E */
+  int32_t hidden;      /* H */
+  int32_t max_len;
+  int32_t eos;
+  int32_t math;        /* 0: fp32 GEMMs (no TF32), 1: TF32 tensor-core GEMMs */
+  int32_t poll;        /* host polls the device stop flag every `poll` steps (0 = 4) */
+} skb_decode_shape;
+int64_t skb_decode_workspace_bytes(const skb_decode_shape* shape);
+skb_status skb_decode(const skb_decode_shape* shape, const float* h0_dev, const float* c0_dev,
+                      const float* emb_dev, const float* w_gates_dev, const float* b_gates_dev,
+                      const float* w_out_dev, const float* b_out_dev, int32_t* tokens_dev, float* scores_dev,
+                      int32_t* lengths_dev, int32_t* steps_out, void* workspace_dev, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Vector-stream region executor (csrc/stream.cu; compiler stream.py).
  *
  * Replaces `execute` (graph/execute.py:27-36) for staged programs whose

@@ -211,3 +211,35 @@ def make_stream_feeds(case) -> dict:
         else:
             out[name] = rng.integers(lo, hi + 1, shape).astype(np.int64)
     return {name: out[name] for name in case["feeds"]}   # the entry's parameter order
+
+
+# ---------------------------------------------------------------- greedy decode with EOS stop (C3)
+def greedy_case(name, V, E, H, max_len, eos, seed, uscale=0.5, note=""):
+    """tanh-RNN decoder, logits = h @ w_out, argmax, EOS `break`."""
+    return {"name": name, "program": "greedy.msl", "entry": "greedy", "dims": {"V": V, "E": E, "H": H},
+            "max_len": max_len, "eos": eos, "seed": seed, "uscale": uscale, "note": note}
+
+
+GREEDY_CASES = [
+    greedy_case("greedy_v64_stop", 64, 8, 16, 30, 46, 3, note="EOS (46) reached at step 9: data-dependent stop"),
+    greedy_case("greedy_v64_nostop", 64, 8, 16, 30, 5, 3, note="EOS never produced: runs to max_len"),
+    greedy_case("greedy_v300_stop", 300, 12, 24, 40, -1, 4, note="eos picked by the generator (first repeat)"),
+    greedy_case("greedy_v64_zero", 64, 8, 16, 0, 46, 3, note="max_len 0: no step, toks = [0]"),
+]
+
+
+def greedy_case_by_name(name):
+    for c in GREEDY_CASES:
+        if c["name"] == name:
+            return c
+    raise KeyError(name)
+
+
+def make_greedy_feeds(case) -> dict:
+    d = case["dims"]
+    V, E, H = d["V"], d["E"], d["H"]
+    rng = np.random.default_rng(case["seed"])
+    return {"h0": rng.uniform(-1, 1, (1, H)), "emb": rng.uniform(-1, 1, (V, 1, E)),
+            "w_in": rng.uniform(-1, 1, (E, H)), "u": rng.uniform(-1, 1, (H, H)) * case["uscale"],
+            "w_out": rng.uniform(-1, 1, (H, V)), "ids": np.arange(V, dtype=np.int64),
+            "eos": np.asarray(case["eos"], dtype=np.int64), "max_len": np.asarray(case["max_len"], dtype=np.int64)}

@@ -122,5 +122,45 @@ def main(argv):
         print(f"{name:24s} {what} ({doc['reference_seconds']} s in the reference executor)")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and sys.argv[1:2] != ["--greedy"]:
     main(sys.argv[1:])
+
+
+def greedy_goldens():
+    """tests/golden/greedy_*.json: SURVEY App. F greedy decoder traced and run by
+    the reference (EOS `break` lowered into the While test)."""
+    from stagekit.runtime import ParamSpec, trace_module
+    from stagekit.syntax import parse_module
+    from stagekit.graph import execute
+    path = os.path.join(fixtures.PROGRAMS, "greedy.msl")
+    for case in fixtures.GREEDY_CASES:
+        feeds = fixtures.make_greedy_feeds(case)
+        module = parse_module(open(path).read(), "greedy.msl")
+        specs = [ParamSpec(k, "i64" if v.dtype == np.int64 else "f64", tuple(v.shape)) for k, v in feeds.items()]
+        graph = trace_module(module, "greedy", specs).graph
+        ref = {k: _ref_value(v) for k, v in feeds.items()}
+        if case["eos"] == -1:   # pick the first token the decoder emits twice -> a stop inside max_len
+            probe = dict(ref, eos=_ref_value(np.asarray(-7, dtype=np.int64)))
+            toks = list(execute(graph, probe).outputs[0].data)
+            seen = set()
+            for t in toks[1:]:
+                if t in seen:
+                    case = dict(case, eos=int(t))
+                    break
+                seen.add(t)
+            ref["eos"] = _ref_value(np.asarray(case["eos"], dtype=np.int64))
+        res = execute(graph, ref)
+        flat = []
+        for v in res.outputs:
+            flat.extend(_flatten(v))
+        doc = {"case": case, "generator": "oracle/gen_stream_golden.py --greedy",
+               "graph": json.loads(ir.to_json(graph)),
+               "expected": {"outputs": [_leaf_json(v) for v in flat], "print_log": list(res.print_log)}}
+        with open(fixtures.golden_path(case["name"]), "w") as f:
+            json.dump(doc, f, separators=(",", ":"))
+        print(case["name"], "eos", case["eos"], "tokens", doc["expected"]["outputs"][0]["tensor"]["data"][:12],
+              "t", doc["expected"]["outputs"][1]["tensor"]["data"])
+
+
+if __name__ == "__main__" and sys.argv[1:2] == ["--greedy"]:
+    greedy_goldens()

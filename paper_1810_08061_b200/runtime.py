@@ -31,6 +31,12 @@ class RnnShape(ctypes.Structure):
                 ("problems", ctypes.c_int32)]
 
 
+class DecodeShape(ctypes.Structure):
+    """include/skb.h skb_decode_shape"""
+    _fields_ = [(n, ctypes.c_int32) for n in ("cell", "sentences", "beam", "vocab", "embed", "hidden", "max_len",
+                                              "eos", "math", "poll")]
+
+
 _VP = ctypes.c_void_p
 _P4 = ctypes.c_void_p * 4
 
@@ -54,6 +60,8 @@ SIGNATURES = {
     "skb_vm_run": (ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int64, ctypes.c_int64, _VP, _VP, _VP, _VP,
                                    _VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int, _VP]),
     "skb_vm_max_ctas": (ctypes.c_int, []),
+    "skb_decode_workspace_bytes": (ctypes.c_int64, [ctypes.POINTER(DecodeShape)]),
+    "skb_decode": (ctypes.c_int, [ctypes.POINTER(DecodeShape)] + [_VP] * 10 + [ctypes.POINTER(ctypes.c_int32), _VP, _VP]),
     "skb_stream_smem_bytes": (ctypes.c_int64, [ctypes.c_int] * 5),
     "skb_stream_grid": (ctypes.c_int, [ctypes.c_int64]),
     "skb_stream_tile_elems": (ctypes.c_int, []),
