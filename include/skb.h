@@ -160,6 +160,14 @@ typedef struct skb_decode_shape {
   int32_t poll;        /* host polls the device stop flag every `poll` steps (0 = 4) */
 } skb_decode_shape;
 int64_t skb_decode_workspace_bytes(const skb_decode_shape* shape);
+/* Per-phase CUDA-event timing of subsequent skb_decode calls (bench/profiling):
+ * read returns the steps timed and ms_out[4] = {embedding gather, gate GEMM +
+ * cell, logits GEMM, beam_select} summed over them. */
+int skb_decode_profile(int enable);
+/* 1 if the last skb_decode ran as one conditional-WHILE CUDA graph launch (the
+ * loop decided on the device), 0 if it used the host-polled loop. */
+int skb_decode_last_mode(void);
+int skb_decode_profile_read(float* ms_out);
 skb_status skb_decode(const skb_decode_shape* shape, const float* h0_dev, const float* c0_dev,
                       const float* emb_dev, const float* w_gates_dev, const float* b_gates_dev,
                       const float* w_out_dev, const float* b_out_dev, int32_t* tokens_dev, float* scores_dev,

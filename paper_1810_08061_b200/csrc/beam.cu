@@ -7,12 +7,13 @@
 //   GEMM         gates = xh @ W_gates       (cuBLAS; fp32 exact or TF32 tensor cores)
 //   dec_cell     rnn: h' = tanh(gates); lstm: i,f,g,o -> c', h'   (tensor.py:391-407)
 //   GEMM         logits = h' @ W_out                     (cuBLAS, same math)
-//   beam_select  ONE pass over the logits per sentence: per beam row a warp keeps
-//                an online max / sum-exp (log-softmax) and a per-lane top-K with
-//                warp-shuffle merges; the sentence's K x K candidates are ranked
-//                (score desc, flat index asc — the oracle's tie-break), then the
-//                CTA reindexes h, c, scores, tokens, lengths and history from the
-//                chosen parents and counts unfinished sentences.
+//   beam_rows    ONE pass over the logits, one CTA per beam row: it keeps
+//                an online max / sum-exp (log-softmax) and per-thread top-K lists
+//                merged by warp-shuffle argmax;
+//   beam_choose  per sentence: ranks its K x K candidates (score desc, flat index
+//                asc — the oracle's tie-break), reindexes h, c, scores, tokens,
+//                lengths and history from the chosen parents and counts
+//                unfinished sentences.
 // Every kernel of step t+1 reads that count and exits when it is zero, so the
 // stop is decided on the device; the host only polls the counter every few
 // steps to stop launching.  Semantics: oracle/beam.py (pinned against the
@@ -21,12 +22,14 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <string.h>
 #include "skb_internal.h"
 
 namespace {
 
 constexpr int KMAX = 8;          // largest beam
-constexpr int SEL_THREADS = 256;  // beam_select CTA: 8 warps, warp w handles rows w, w+8, ...
+constexpr int SEL_THREADS = 256;  // beam_choose CTA (one per sentence)
+constexpr int ROW_THREADS = 256;  // beam_rows CTA (one per beam row)
 
 struct DecodeState {             // device pointers into the workspace
   float* xh;                     // [R, E+H]
@@ -42,6 +45,10 @@ struct DecodeState {             // device pointers into the workspace
   int32_t* len[2];               // [R]
   int32_t* hist[2];              // [R, max_len+1]
   int32_t* active;               // [max_len+1] unfinished sentences after step t (active[0] = S)
+  int32_t* tstep;                // the decode step counter (device-resident loop index)
+  float* row_v;                  // [R, KMAX] each row's K best logits (pass 1)
+  int32_t* row_i;                // [R, KMAX] their vocabulary ids
+  float* row_lse;                // [R] log-sum-exp of the row
 };
 
 __device__ __forceinline__ float sigmoidf_ref(float x) {   // reference tensor.py:403-407 (two branches)
@@ -50,21 +57,28 @@ __device__ __forceinline__ float sigmoidf_ref(float x) {   // reference tensor.p
   return e / (1.f + e);
 }
 
-__global__ void dec_gather(const float* __restrict__ emb, const float* __restrict__ h, const int32_t* __restrict__ tok,
-                           float* __restrict__ xh, int R, int E, int H, const int32_t* __restrict__ active, int t) {
-  if (active[t] == 0) return;
+__global__ void dec_gather(DecodeState st, const float* __restrict__ emb, int R, int E, int H) {
+  const int t = *st.tstep;
+  if (st.active[t] == 0) return;
+  const float* __restrict__ h = st.h[t & 1];
+  const int32_t* __restrict__ tok = st.tok;
+  float* __restrict__ xh = st.xh;
   const int W = E + H;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)R * W;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(i / W), k = (int)(i % W);
-    xh[i] = k < E ? emb[(long long)tok[r] * E + k] : h[(long long)r * H + (k - E)];
+  for (int r = blockIdx.x; r < R; r += gridDim.x) {   // one CTA per row: coalesced row copies
+    const float* e = emb + (long long)tok[r] * E;
+    float* o = xh + (long long)r * W;
+    for (int k = threadIdx.x; k < E; k += blockDim.x) o[k] = e[k];
+    for (int k = threadIdx.x; k < H; k += blockDim.x) o[E + k] = h[(long long)r * H + k];
   }
 }
 
-__global__ void dec_cell(int cell, const float* __restrict__ gates, const float* __restrict__ bias,
-                         const float* __restrict__ c, float* __restrict__ hn, float* __restrict__ cn, int R, int H,
-                         const int32_t* __restrict__ active, int t) {
-  if (active[t] == 0) return;
+__global__ void dec_cell(DecodeState st, int cell, const float* __restrict__ bias, int R, int H) {
+  const int t = *st.tstep;
+  if (st.active[t] == 0) return;
+  const float* __restrict__ gates = st.gates;
+  const float* __restrict__ c = st.c[t & 1];
+  float* __restrict__ hn = st.hn;
+  float* __restrict__ cn = st.cn;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)R * H;
        i += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(i / H), k = (int)(i % H);
@@ -103,61 +117,128 @@ __device__ __forceinline__ void topk_insert(float (&v)[K], int (&ix)[K], float x
   }
 }
 
+// Pass 1 — one CTA per beam row (R CTAs fill the machine): a single HBM pass
+// over the row's logits (float4 loads) computes the log-softmax normaliser
+// (per-thread max / sum-exp, merged with warp shuffles then across warps) and
+// the row's K best (value desc, index asc) — per-thread register lists merged
+// K times by warp-shuffle argmax, then across the CTA's warps.
 template <int K>
-__global__ void __launch_bounds__(SEL_THREADS) beam_select(DecodeState st, int S, int V, int H, int LT, int eos,
-                                                           const float* __restrict__ b_out, int t, int cur) {
+__global__ void __launch_bounds__(ROW_THREADS) beam_rows(DecodeState st, int V, const float* __restrict__ b_out) {
+  const int t = *st.tstep, cur = t & 1;
   if (st.active[t] == 0) return;
-  __shared__ float row_v[KMAX][KMAX];
-  __shared__ int row_i[KMAX][KMAX];
-  __shared__ float row_lse[KMAX];
-  __shared__ int sel_par[KMAX], sel_tok[KMAX];
-  __shared__ double sel_score[KMAX];
-  const int s = blockIdx.x;
+  __shared__ float wv[ROW_THREADS / 32][K], wm[ROW_THREADS / 32], ws[ROW_THREADS / 32];
+  __shared__ int wi[ROW_THREADS / 32][K];
+  const int r = blockIdx.x;
+  if (st.fin[cur][r]) return;   // finished beams offer only (EOS, score) in pass 2
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nxt = cur ^ 1;
-  for (int b = warp; b < K; b += SEL_THREADS / 32) {
-    const int r = s * K + b;
-    if (st.fin[cur][r]) continue;   // finished beams offer only (EOS, score) below
-    const float* L = st.logits + (long long)r * V;
-    float mx = -INFINITY, sum = 0.f;
-    float tv[K];
-    int ti[K];
+  const float* L = st.logits + (long long)r * V;
+  float mx = -INFINITY, sum = 0.f;
+  float tv[K];
+  int ti[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) { tv[k] = -INFINITY; ti[k] = 0x7fffffff; }
-    for (int v = lane; v < V; v += 32) {
-      const float x = L[v] + (b_out ? b_out[v] : 0.f);
-      if (x > mx) { sum = sum * expf(mx - x) + 1.f; mx = x; } else { sum += expf(x - mx); }   // online softmax
-      topk_insert<K>(tv, ti, x, v);
+  for (int k = 0; k < K; ++k) { tv[k] = -INFINITY; ti[k] = 0x7fffffff; }
+  auto take = [&](float x, int v) {
+    if (x > mx) { sum = sum * __expf(mx - x) + 1.f; mx = x; } else { sum += __expf(x - mx); }
+    topk_insert<K>(tv, ti, x, v);
+  };
+  const int V4 = (V % 4 == 0) ? V / 4 : 0;   // rows are 16-byte aligned when V % 4 == 0
+  const float4* L4 = reinterpret_cast<const float4*>(L);
+  const float4* B4 = reinterpret_cast<const float4*>(b_out);
+  constexpr int U = 4;   // float4 loads in flight per thread before any is consumed
+  int q0 = threadIdx.x;
+  for (; q0 + (U - 1) * ROW_THREADS < V4; q0 += U * ROW_THREADS) {
+    float4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = __ldcs(L4 + q0 + u * ROW_THREADS);   // streamed once: evict-first
+    if (b_out) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float4 b = __ldg(B4 + q0 + u * ROW_THREADS);
+        x[u].x += b.x; x[u].y += b.y; x[u].z += b.z; x[u].w += b.w;
+      }
     }
-    // warp: combine (max, sum) pairs, then merge the 32 sorted lists K times
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + u * ROW_THREADS;
+      take(x[u].x, 4 * q); take(x[u].y, 4 * q + 1); take(x[u].z, 4 * q + 2); take(x[u].w, 4 * q + 3);
+    }
+  }
+  for (int q = q0; q < V4; q += ROW_THREADS) {
+    float4 x = L4[q];
+    if (b_out) { const float4 b = B4[q]; x.x += b.x; x.y += b.y; x.z += b.z; x.w += b.w; }
+    take(x.x, 4 * q); take(x.y, 4 * q + 1); take(x.z, 4 * q + 2); take(x.w, 4 * q + 3);
+  }
+  for (int v = 4 * V4 + threadIdx.x; v < V; v += ROW_THREADS) take(L[v] + (b_out ? b_out[v] : 0.f), v);
+  // normaliser: warp then CTA
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, mx, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+    const float m = fmaxf(mx, m2);
+    sum = (mx == -INFINITY ? 0.f : sum * __expf(mx - m)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - m));
+    mx = m;
+  }
+  if (lane == 0) { wm[warp] = mx; ws[warp] = sum; }
+  // top-K: merge the warp's 32 lists
+  for (int k = 0; k < K; ++k) {
+    float bv = tv[0];
+    int bi = ti[0], bl = lane;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, mx, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
-      const float m = fmaxf(mx, m2);
-      sum = (mx == -INFINITY ? 0.f : sum * expf(mx - m)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - m));
-      mx = m;
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; bl = ol; }
     }
+    if (lane == 0) { wv[warp][k] = bv; wi[warp][k] = bi; }
+    if (lane == bl) {
+#pragma unroll
+      for (int q = 0; q < K - 1; ++q) { tv[q] = tv[q + 1]; ti[q] = ti[q + 1]; }
+      tv[K - 1] = -INFINITY; ti[K - 1] = 0x7fffffff;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // normaliser across warps
+    float m = lane < ROW_THREADS / 32 ? wm[lane] : -INFINITY;
+    float sm = lane < ROW_THREADS / 32 ? ws[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sm, o);
+      const float mm = fmaxf(m, m2);
+      sm = (m == -INFINITY ? 0.f : sm * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+      m = mm;
+    }
+    // top-K across warps: lane w holds warp w's sorted list head
+    int head = 0;
     for (int k = 0; k < K; ++k) {
-      float bv = tv[0];
-      int bi = ti[0], bl = lane;
+      float bv = -INFINITY;
+      int bi = 0x7fffffff, bl = lane;
+      if (lane < ROW_THREADS / 32 && head < K) { bv = wv[lane][head]; bi = wi[lane][head]; }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
         const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
         if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; bl = ol; }
       }
-      if (lane == 0) { row_v[b][k] = bv; row_i[b][k] = bi; }
-      if (lane == bl) {   // pop the winner's head
-#pragma unroll
-        for (int q = 0; q < K - 1; ++q) { tv[q] = tv[q + 1]; ti[q] = ti[q + 1]; }
-        tv[K - 1] = -INFINITY; ti[K - 1] = 0x7fffffff;
-      }
+      if (lane == 0) { st.row_v[(long long)r * KMAX + k] = bv; st.row_i[(long long)r * KMAX + k] = bi; }
+      if (lane == bl) ++head;
     }
-    if (lane == 0) row_lse[b] = mx + logf(sum);
+    if (lane == 0) st.row_lse[r] = m + logf(sm);
   }
-  __syncthreads();
+}
+
+// Pass 2 — one CTA (warp) per sentence: rank its K x K candidates (score +
+// logit - lse for live beams, (EOS, score) for finished ones; score desc,
+// flat index b*V+v asc), then reindex state and history from the parents.
+template <int K>
+__global__ void __launch_bounds__(SEL_THREADS) beam_choose(DecodeState st, int S, int V, int H, int LT, int eos) {
+  const int t = *st.tstep, cur = t & 1;
+  if (st.active[t] == 0) return;
+  __shared__ int sel_par[KMAX], sel_tok[KMAX];
+  __shared__ double sel_score[KMAX];
+  const int s = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nxt = cur ^ 1;
   if (warp == 0) {
-    // candidates: K per live row (score + logit - lse), one (EOS, score) per finished row
     double cs[2];
     int ci[2];   // flat index b*V + v
 #pragma unroll
@@ -169,11 +250,12 @@ __global__ void __launch_bounds__(SEL_THREADS) beam_select(DecodeState st, int S
         const double sc = st.score[cur][r];
         if (st.fin[cur][r]) {
           if (k == 0) { cs[q] = sc; ci[q] = b * V + eos; }
-        } else if (sc != -INFINITY && row_i[b][k] != 0x7fffffff) {
-          cs[q] = sc + ((double)row_v[b][k] - (double)row_lse[b]);
-          ci[q] = b * V + row_i[b][k];
-        } else if (row_i[b][k] != 0x7fffffff) {
-          ci[q] = b * V + row_i[b][k];
+        } else {
+          const int v = st.row_i[(long long)r * KMAX + k];
+          if (v != 0x7fffffff) {
+            ci[q] = b * V + v;
+            if (sc != -INFINITY) cs[q] = sc + ((double)st.row_v[(long long)r * KMAX + k] - (double)st.row_lse[r]);
+          }
         }
       }
     }
@@ -246,10 +328,21 @@ __global__ void dec_init(DecodeState st, const float* __restrict__ h0, const flo
   }
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= max_len; t += gridDim.x * blockDim.x)
     st.active[t] = t == 0 ? S : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *st.tstep = 0;
 }
 
-__global__ void dec_output(DecodeState st, int R, int LT, int side, int32_t* tokens, float* scores,
-                           int32_t* lengths) {
+// The loop's end of step: advance the device step counter and, inside the
+// conditional-WHILE graph, decide whether the body runs again (the EOS stop
+// and max_len test evaluated on the device: no host round trip per step).
+__global__ void dec_advance(DecodeState st, int max_len, cudaGraphConditionalHandle cond, int use_cond) {
+  const int t = *st.tstep;
+  const int t1 = st.active[t] > 0 ? t + 1 : t;   // a step that found nothing live does not count
+  *st.tstep = t1;
+  if (use_cond) cudaGraphSetConditional(cond, (t1 < max_len && st.active[t1] > 0) ? 1u : 0u);
+}
+
+__global__ void dec_output(DecodeState st, int R, int LT, int32_t* tokens, float* scores, int32_t* lengths) {
+  const int side = *st.tstep & 1;   // step k writes side (k+1)&1
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)R * LT;
        i += (long long)gridDim.x * blockDim.x)
     tokens[i] = st.hist[side][i];
@@ -257,6 +350,19 @@ __global__ void dec_output(DecodeState st, int R, int LT, int side, int32_t* tok
     scores[r] = (float)st.score[side][r];
     lengths[r] = st.len[side][r];
   }
+}
+
+// Optional per-phase timing of skb_decode (skb_decode_profile): CUDA events
+// around each step's phases on the decode stream, summed on read.
+enum { P_GATHER_CELL = 0, P_GEMM_GATES = 1, P_GEMM_LOGITS = 2, P_SELECT = 3, P_N = 4 };
+constexpr int kProfSteps = 1024;
+bool g_dprof = false;
+cudaEvent_t g_dev[kProfSteps][P_N + 1];
+int g_dsteps = 0;
+bool g_dinit = false;
+
+void prof_mark(int step, int k, cudaStream_t cs) {
+  if (g_dprof && step < kProfSteps) cudaEventRecord(g_dev[step][k], cs);
 }
 
 size_t al(size_t b) { return (b + 255) & ~size_t(255); }
@@ -281,6 +387,10 @@ size_t layout(const skb_decode_shape& d, DecodeState* st, uint8_t* base) {
   }
   s.tok = (int32_t*)take(4 * R);
   s.active = (int32_t*)take(4 * (LT + 1));
+  s.tstep = (int32_t*)take(4);
+  s.row_v = (float*)take(4 * R * KMAX);
+  s.row_i = (int32_t*)take(4 * R * KMAX);
+  s.row_lse = (float*)take(4 * R);
   if (st) *st = s;
   return off;
 }
@@ -307,6 +417,104 @@ extern "C" int64_t skb_decode_workspace_bytes(const skb_decode_shape* d) {
   return (int64_t)layout(*d, nullptr, nullptr);
 }
 
+namespace {
+
+// One decode step on stream `cs` (kernels read the step index from st.tstep).
+bool enqueue_step(const skb_decode_shape* d, DecodeState& st, cublasHandle_t hb, cudaStream_t cs, const float* emb,
+                  const float* w_gates, const float* b_gates, const float* w_out, const float* b_out,
+                  cudaGraphConditionalHandle cond, int use_cond, int prof_step) {
+  const int S = d->sentences, K = d->beam, R = S * K, E = d->embed, H = d->hidden, V = d->vocab;
+  const int G = d->cell == SKB_CELL_LSTM ? 4 * H : H, LT = d->max_len + 1;
+  const int rows = R < 148 * 8 ? R : 148 * 8;
+  prof_mark(prof_step, 0, cs);
+  dec_gather<<<rows, 128, 0, cs>>>(st, emb, R, E, H);
+  prof_mark(prof_step, 1, cs);
+  if (!gemm(hb, d->math, st.xh, w_gates, st.gates, R, G, E + H)) return false;
+  prof_mark(prof_step, 2, cs);
+  dec_cell<<<148 * 8, 256, 0, cs>>>(st, d->cell, b_gates, R, H);
+  if (!gemm(hb, d->math, st.hn, w_out, st.logits, R, V, H)) return false;
+  prof_mark(prof_step, 3, cs);
+  switch (K) {
+#define SKB_SEL(k)                                                                               \
+  case k:                                                                                        \
+    beam_rows<k><<<R, ROW_THREADS, 0, cs>>>(st, V, b_out);                                       \
+    beam_choose<k><<<S, SEL_THREADS, 0, cs>>>(st, S, V, H, LT, d->eos);                          \
+    break;
+    SKB_SEL(1) SKB_SEL(2) SKB_SEL(3) SKB_SEL(4) SKB_SEL(5) SKB_SEL(6) SKB_SEL(7) SKB_SEL(8)
+#undef SKB_SEL
+  }
+  prof_mark(prof_step, 4, cs);
+  dec_advance<<<1, 1, 0, cs>>>(st, d->max_len, cond, use_cond);
+  return cudaPeekAtLastError() == cudaSuccess;
+}
+
+// Decode graphs: ONE conditional-WHILE node whose body is one decode step
+// (captured once per shape / buffers), so a whole decode is a single graph
+// launch and every loop decision is made on the device.
+struct GraphEntry {
+  skb_decode_shape d;
+  const void* ptrs[6];
+  cudaGraphExec_t exec;
+};
+constexpr int kGraphCache = 16;
+GraphEntry g_graphs[kGraphCache];
+int g_ngraphs = 0;
+
+cudaGraphExec_t decode_graph(const skb_decode_shape* d, DecodeState& st, cublasHandle_t hb, void* ws,
+                             const float* emb, const float* w_gates, const float* b_gates, const float* w_out,
+                             const float* b_out) {
+  const void* key[6] = {ws, emb, w_gates, b_gates, w_out, b_out};
+  for (int i = 0; i < g_ngraphs; ++i) {
+    GraphEntry& e = g_graphs[i];
+    if (memcmp(&e.d, d, sizeof(*d)) == 0 && memcmp(e.ptrs, key, sizeof(key)) == 0) return e.exec;
+  }
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;
+  cudaGraphConditionalHandle cond;
+  bool ok = cudaGraphCreate(&g, 0) == cudaSuccess &&
+            cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+  cudaGraphNodeParams p = {};
+  cudaGraphNode_t node;
+  if (ok) {
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = cond;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    ok = cudaGraphAddNode(&node, g, nullptr, 0, &p) == cudaSuccess;
+  }
+  if (ok) ok = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess;
+  if (ok) ok = cudaStreamBeginCaptureToGraph(cap, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeRelaxed) == cudaSuccess;
+  if (ok) {
+    cublasSetStream(hb, cap);
+    const bool enq = enqueue_step(d, st, hb, cap, emb, w_gates, b_gates, w_out, b_out, cond, 1, kProfSteps);
+    cudaGraph_t body = nullptr;
+    ok = cudaStreamEndCapture(cap, &body) == cudaSuccess && enq;
+  }
+  if (ok) ok = cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
+  if (cap) cudaStreamDestroy(cap);
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();   // a failed build falls back to the host-driven loop
+  if (!ok) return nullptr;
+  if (g_ngraphs == kGraphCache) {
+    cudaGraphExecDestroy(g_graphs[0].exec);
+    memmove(g_graphs, g_graphs + 1, sizeof(GraphEntry) * (kGraphCache - 1));
+    --g_ngraphs;
+  }
+  GraphEntry& e = g_graphs[g_ngraphs++];
+  e.d = *d;
+  memcpy(e.ptrs, key, sizeof(key));
+  e.exec = exec;
+  return exec;
+}
+
+int g_last_mode = 0;   // 1 = conditional graph, 0 = host-driven loop
+
+}  // namespace
+
+extern "C" int skb_decode_last_mode(void) { return g_last_mode; }
+
 extern "C" skb_status skb_decode(const skb_decode_shape* d, const float* h0, const float* c0, const float* emb,
                                  const float* w_gates, const float* b_gates, const float* w_out, const float* b_out,
                                  int32_t* tokens_out, float* scores_out, int32_t* lengths_out, int32_t* steps_out,
@@ -317,45 +525,66 @@ extern "C" skb_status skb_decode(const skb_decode_shape* d, const float* h0, con
   cudaStream_t cs = (cudaStream_t)stream;
   DecodeState st;
   layout(*d, &st, (uint8_t*)workspace);
-  const int S = d->sentences, K = d->beam, R = S * K, E = d->embed, H = d->hidden, V = d->vocab;
-  const int G = d->cell == SKB_CELL_LSTM ? 4 * H : H, LT = d->max_len + 1;
+  const int S = d->sentences, K = d->beam, R = S * K, H = d->hidden, LT = d->max_len + 1;
   cublasHandle_t hb = handle_for(stream);
   if (!hb) return SKB_ERR_CUDA;
-  const int ew = 148 * 8;
-  dec_init<<<ew, 256, 0, cs>>>(st, h0, c0, S, K, H, LT, d->max_len);
-  int32_t* active_host = nullptr;
-  cudaMallocHost(&active_host, sizeof(int32_t) * 2);
-  int t = 0, cur = 0;
-  const int poll = d->poll > 0 ? d->poll : 4;
-  for (; t < d->max_len; ++t) {
-    dec_gather<<<ew, 256, 0, cs>>>(emb, st.h[cur], st.tok, st.xh, R, E, H, st.active, t);
-    if (!gemm(hb, d->math, st.xh, w_gates, st.gates, R, G, E + H)) return SKB_ERR_CUDA;
-    dec_cell<<<ew, 256, 0, cs>>>(d->cell, st.gates, b_gates, st.c[cur], st.hn, st.cn, R, H, st.active, t);
-    if (!gemm(hb, d->math, st.hn, w_out, st.logits, R, V, H)) return SKB_ERR_CUDA;
-    switch (K) {
-#define SKB_SEL(k) case k: beam_select<k><<<S, SEL_THREADS, 0, cs>>>(st, S, V, H, LT, d->eos, b_out, t, cur); break;
-      SKB_SEL(1) SKB_SEL(2) SKB_SEL(3) SKB_SEL(4) SKB_SEL(5) SKB_SEL(6) SKB_SEL(7) SKB_SEL(8)
-#undef SKB_SEL
-    }
-    cur ^= 1;
-    if ((t + 1) % poll == 0 || t + 1 == d->max_len) {   // stop launching once the device says done
-      cudaMemcpyAsync(active_host, st.active + t + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, cs);
-      if (cudaStreamSynchronize(cs) != cudaSuccess) { cudaFreeHost(active_host); return SKB_ERR_CUDA; }
-      if (active_host[0] == 0) { ++t; break; }
+  static int32_t* host_word = nullptr;   // pinned poll / result word, allocated once
+  if (!host_word && cudaMallocHost(&host_word, sizeof(int32_t) * 2) != cudaSuccess) return SKB_ERR_CUDA;
+  dec_init<<<148 * 8, 256, 0, cs>>>(st, h0, c0, S, K, H, LT, d->max_len);
+  cudaGraphExec_t exec = nullptr;
+  if (d->max_len > 0 && !g_dprof && d->poll >= 0)
+    exec = decode_graph(d, st, hb, workspace, emb, w_gates, b_gates, w_out, b_out);
+  cublasSetStream(hb, cs);
+  g_last_mode = exec ? 1 : 0;
+  if (exec) {
+    if (cudaGraphLaunch(exec, cs) != cudaSuccess) return SKB_ERR_CUDA;
+  } else {
+    // host-driven loop (profiling, or no conditional graphs): the same kernels,
+    // the host polls the device stop flag every `poll` steps
+    const int poll = d->poll > 0 ? d->poll : 4;
+    for (int t = 0; t < d->max_len; ++t) {
+      if (!enqueue_step(d, st, hb, cs, emb, w_gates, b_gates, w_out, b_out, cudaGraphConditionalHandle(), 0, t))
+        return SKB_ERR_CUDA;
+      if ((t + 1) % poll == 0 || t + 1 == d->max_len) {
+        cudaMemcpyAsync(host_word, st.active + t + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, cs);
+        if (cudaStreamSynchronize(cs) != cudaSuccess) return SKB_ERR_CUDA;
+        g_dsteps = t + 1 < kProfSteps ? t + 1 : kProfSteps;
+        if (host_word[0] == 0) break;
+      }
     }
   }
-  // the device state after the last step that ran: steps = first t with active[t] == 0
-  int launched = t;
-  int32_t* act = (int32_t*)malloc(sizeof(int32_t) * (launched + 1));
-  cudaMemcpyAsync(act, st.active, sizeof(int32_t) * (launched + 1), cudaMemcpyDeviceToHost, cs);
-  if (cudaStreamSynchronize(cs) != cudaSuccess) { free(act); cudaFreeHost(active_host); return SKB_ERR_CUDA; }
-  int steps = launched;
-  for (int k = 0; k <= launched; ++k)
-    if (act[k] == 0) { steps = k; break; }
-  free(act);
-  cudaFreeHost(active_host);
-  const int side = steps & 1;   // step k writes side (k+1)&1; steps executed = `steps`
-  dec_output<<<ew, 256, 0, cs>>>(st, R, LT, side, tokens_out, scores_out, lengths_out);
-  if (steps_out) *steps_out = steps;
+  dec_output<<<148 * 8, 256, 0, cs>>>(st, R, LT, tokens_out, scores_out, lengths_out);
+  cudaMemcpyAsync(host_word, st.tstep, sizeof(int32_t), cudaMemcpyDeviceToHost, cs);
+  if (cudaStreamSynchronize(cs) != cudaSuccess) return SKB_ERR_CUDA;
+  if (steps_out) *steps_out = host_word[0];
   return skb_check_launch();
+}
+
+// Per-phase timing of the next skb_decode calls: enable != 0 turns it on.
+extern "C" int skb_decode_profile(int enable) {
+  if (enable && !g_dinit) {
+    for (int i = 0; i < kProfSteps; ++i)
+      for (int k = 0; k <= P_N; ++k)
+        if (cudaEventCreate(&g_dev[i][k]) != cudaSuccess) return SKB_ERR_CUDA;
+    g_dinit = true;
+  }
+  g_dprof = enable != 0;
+  g_dsteps = 0;
+  return SKB_OK;
+}
+
+// ms_out[4] = summed ms of {gather (+ idle), gate GEMM + cell, cell->logits GEMM, beam_select}
+// over the steps the last skb_decode launched; returns the step count.
+extern "C" int skb_decode_profile_read(float* ms_out) {
+  for (int k = 0; k < P_N; ++k) ms_out[k] = 0.f;
+  if (!g_dinit) return 0;
+  for (int i = 0; i < g_dsteps; ++i) {
+    if (cudaEventSynchronize(g_dev[i][P_N]) != cudaSuccess) return -1;
+    for (int k = 0; k < P_N; ++k) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, g_dev[i][k], g_dev[i][k + 1]) != cudaSuccess) return -1;
+      ms_out[k] += ms;
+    }
+  }
+  return g_dsteps;
 }

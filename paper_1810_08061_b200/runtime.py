@@ -61,6 +61,9 @@ SIGNATURES = {
                                    _VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int, _VP]),
     "skb_vm_max_ctas": (ctypes.c_int, []),
     "skb_decode_workspace_bytes": (ctypes.c_int64, [ctypes.POINTER(DecodeShape)]),
+    "skb_decode_profile": (ctypes.c_int, [ctypes.c_int]),
+    "skb_decode_last_mode": (ctypes.c_int, []),
+    "skb_decode_profile_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float)]),
     "skb_decode": (ctypes.c_int, [ctypes.POINTER(DecodeShape)] + [_VP] * 10 + [ctypes.POINTER(ctypes.c_int32), _VP, _VP]),
     "skb_stream_smem_bytes": (ctypes.c_int64, [ctypes.c_int] * 5),
     "skb_stream_grid": (ctypes.c_int, [ctypes.c_int64]),

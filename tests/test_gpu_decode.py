@@ -27,6 +27,25 @@ def test_greedy_matches_reference_program(name):
     r = decode("rnn", f["h0"], f["emb"][:, 0, :], (f["w_in"], f["u"], f["w_out"]), 1, case["eos"], case["max_len"])
     assert r["steps"] == exp_t
     assert r["tokens"][0, 0, :exp_t + 1].cpu().tolist() == exp_toks
+    from paper_1810_08061_b200 import runtime
+    if case["max_len"] > 0:   # the whole decode was one conditional-WHILE graph launch
+        assert runtime.lib().skb_decode_last_mode() == 1
+
+
+def test_host_polled_loop_agrees_with_graph():
+    from paper_1810_08061_b200 import runtime
+    doc = fixtures.load_golden("greedy_v64_stop")
+    case = doc["case"]
+    f = fixtures.make_greedy_feeds(case)
+    lib = runtime.lib()
+    lib.skb_decode_profile(1)   # profiling forces the host-driven loop
+    try:
+        r = decode("rnn", f["h0"], f["emb"][:, 0, :], (f["w_in"], f["u"], f["w_out"]), 1, case["eos"], case["max_len"])
+        assert lib.skb_decode_last_mode() == 0
+    finally:
+        lib.skb_decode_profile(0)
+    exp_toks = doc["expected"]["outputs"][0]["tensor"]["data"]
+    assert r["tokens"][0, 0, :len(exp_toks)].cpu().tolist() == exp_toks
 
 
 def _lstm_problem(S, V, E, H, seed, eos=0, eos_bias=0.0, wscale=8.0):
