@@ -133,42 +133,81 @@ __global__ void __launch_bounds__(ROW_THREADS) beam_rows(DecodeState st, int V, 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* L = st.logits + (long long)r * V;
   float mx = -INFINITY, sum = 0.f;
-  float tv[K];
-  int ti[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) { tv[k] = -INFINITY; ti[k] = 0x7fffffff; }
-  auto take = [&](float x, int v) {
-    if (x > mx) { sum = sum * __expf(mx - x) + 1.f; mx = x; } else { sum += __expf(x - mx); }
-    topk_insert<K>(tv, ti, x, v);
+  // The warp's K best so far live one per lane (lanes 0..K-1, best first);
+  // `thr` is the K-th value.  Elements are filtered by one compare + ballot
+  // and only the rare survivors are inserted (warp-cooperatively).
+  float lv = -INFINITY;
+  int li = 0x7fffffff;
+  float thr = -INFINITY;
+  int thr_i = 0x7fffffff;
+  auto offer = [&](float x, int v) {
+    unsigned m = __ballot_sync(0xffffffffu, better(x, v, thr, thr_i));
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const float cv = __shfl_sync(0xffffffffu, x, src);
+      const int ci = __shfl_sync(0xffffffffu, v, src);
+      if (!better(cv, ci, thr, thr_i)) continue;   // the threshold rose since the ballot
+      const unsigned ahead = __ballot_sync(0xffffffffu, lane < K && better(lv, li, cv, ci));
+      const int pos = __popc(ahead);                // entries that stay ahead of the candidate
+      const float uv = __shfl_up_sync(0xffffffffu, lv, 1);
+      const int ui = __shfl_up_sync(0xffffffffu, li, 1);
+      if (lane == pos) { lv = cv; li = ci; }
+      else if (lane > pos && lane < K) { lv = uv; li = ui; }
+      thr = __shfl_sync(0xffffffffu, lv, K - 1);
+      thr_i = __shfl_sync(0xffffffffu, li, K - 1);
+    }
   };
+  // Chunks of 4*U values per lane: one max per chunk rescales the running sum
+  // at most once; every element costs one exp + add and one compare.
   const int V4 = (V % 4 == 0) ? V / 4 : 0;   // rows are 16-byte aligned when V % 4 == 0
   const float4* L4 = reinterpret_cast<const float4*>(L);
   const float4* B4 = reinterpret_cast<const float4*>(b_out);
   constexpr int U = 4;   // float4 loads in flight per thread before any is consumed
-  int q0 = threadIdx.x;
-  for (; q0 + (U - 1) * ROW_THREADS < V4; q0 += U * ROW_THREADS) {
-    float4 x[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) x[u] = __ldcs(L4 + q0 + u * ROW_THREADS);   // streamed once: evict-first
-    if (b_out) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float4 b = __ldg(B4 + q0 + u * ROW_THREADS);
-        x[u].x += b.x; x[u].y += b.y; x[u].z += b.z; x[u].w += b.w;
-      }
-    }
+  const int warp_base = warp * 32 + lane;   // warps own interleaved float4 columns
+  int q0 = warp_base;
+  // every lane runs the same trip count (ballots need the whole warp);
+  // out-of-range float4s read as -inf
+  for (; q0 - warp_base < V4; q0 += U * ROW_THREADS) {
+    float x[4 * U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int q = q0 + u * ROW_THREADS;
-      take(x[u].x, 4 * q); take(x[u].y, 4 * q + 1); take(x[u].z, 4 * q + 2); take(x[u].w, 4 * q + 3);
+      float4 f = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      if (q < V4) {
+        f = __ldcs(L4 + q);   // streamed once: evict-first
+        if (b_out) {
+          const float4 b = __ldg(B4 + q);
+          f.x += b.x; f.y += b.y; f.z += b.z; f.w += b.w;
+        }
+      }
+      x[4 * u] = f.x; x[4 * u + 1] = f.y; x[4 * u + 2] = f.z; x[4 * u + 3] = f.w;
+    }
+    float cm = x[0];
+#pragma unroll
+    for (int e = 1; e < 4 * U; ++e) cm = fmaxf(cm, x[e]);
+    if (cm > mx) { sum *= __expf(mx - cm); mx = cm; }
+    if (cm != -INFINITY) {
+#pragma unroll
+      for (int e = 0; e < 4 * U; ++e) sum += __expf(x[e] - mx);
+    }
+    if (__any_sync(0xffffffffu, cm >= thr && cm != -INFINITY)) {
+#pragma unroll
+      for (int e = 0; e < 4 * U; ++e) offer(x[e], 4 * (q0 + (e >> 2) * ROW_THREADS) + (e & 3));
     }
   }
-  for (int q = q0; q < V4; q += ROW_THREADS) {
-    float4 x = L4[q];
-    if (b_out) { const float4 b = B4[q]; x.x += b.x; x.y += b.y; x.z += b.z; x.w += b.w; }
-    take(x.x, 4 * q); take(x.y, 4 * q + 1); take(x.z, 4 * q + 2); take(x.w, 4 * q + 3);
+  // rows whose length is not a multiple of 4: scalar pass, same trip count per lane
+  if (V4 == 0) {
+    for (int v0 = 0; v0 < V; v0 += ROW_THREADS) {
+      const int v = v0 + threadIdx.x;
+      const bool ok = v < V;
+      const float x = ok ? L[v] + (b_out ? b_out[v] : 0.f) : -INFINITY;
+      if (ok) {
+        if (x > mx) { sum = sum * __expf(mx - x) + 1.f; mx = x; } else { sum += __expf(x - mx); }
+      }
+      offer(x, ok ? v : 0x7fffffff);
+    }
   }
-  for (int v = 4 * V4 + threadIdx.x; v < V; v += ROW_THREADS) take(L[v] + (b_out ? b_out[v] : 0.f), v);
   // normaliser: warp then CTA
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -178,23 +217,7 @@ __global__ void __launch_bounds__(ROW_THREADS) beam_rows(DecodeState st, int V, 
     mx = m;
   }
   if (lane == 0) { wm[warp] = mx; ws[warp] = sum; }
-  // top-K: merge the warp's 32 lists
-  for (int k = 0; k < K; ++k) {
-    float bv = tv[0];
-    int bi = ti[0], bl = lane;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; bl = ol; }
-    }
-    if (lane == 0) { wv[warp][k] = bv; wi[warp][k] = bi; }
-    if (lane == bl) {
-#pragma unroll
-      for (int q = 0; q < K - 1; ++q) { tv[q] = tv[q + 1]; ti[q] = ti[q + 1]; }
-      tv[K - 1] = -INFINITY; ti[K - 1] = 0x7fffffff;
-    }
-  }
+  if (lane < K) { wv[warp][lane] = lv; wi[warp][lane] = li; }
   __syncthreads();
   if (warp == 0) {
     // normaliser across warps
@@ -282,9 +305,24 @@ __global__ void __launch_bounds__(SEL_THREADS) beam_choose(DecodeState st, int S
     const bool pfin = st.fin[cur][rp] != 0;
     const float* hs = pfin ? st.h[cur] + (long long)rp * H : st.hn + (long long)rp * H;
     const float* cs = pfin ? st.c[cur] + (long long)rp * H : st.cn + (long long)rp * H;
-    for (int k = lane; k < H; k += 32) {
-      st.h[nxt][(long long)rj * H + k] = hs[k];
-      st.c[nxt][(long long)rj * H + k] = cs[k];
+    if ((H & 3) == 0) {   // float4 row copies, all loads of a lane issued before the stores
+      const float4* hs4 = reinterpret_cast<const float4*>(hs);
+      const float4* cs4 = reinterpret_cast<const float4*>(cs);
+      float4* hd4 = reinterpret_cast<float4*>(st.h[nxt] + (long long)rj * H);
+      float4* cd4 = reinterpret_cast<float4*>(st.c[nxt] + (long long)rj * H);
+      for (int k = lane; k < H / 4; k += 64) {
+        const float4 a = hs4[k], b = cs4[k];
+        const bool two = k + 32 < H / 4;
+        float4 a2, b2;
+        if (two) { a2 = hs4[k + 32]; b2 = cs4[k + 32]; }
+        hd4[k] = a; cd4[k] = b;
+        if (two) { hd4[k + 32] = a2; cd4[k + 32] = b2; }
+      }
+    } else {
+      for (int k = lane; k < H; k += 32) {
+        st.h[nxt][(long long)rj * H + k] = hs[k];
+        st.c[nxt][(long long)rj * H + k] = cs[k];
+      }
     }
     for (int k = lane; k <= t; k += 32) st.hist[nxt][(long long)rj * LT + k] = st.hist[cur][(long long)rp * LT + k];
     if (lane == 0) {
