@@ -174,6 +174,26 @@ skb_status skb_decode(const skb_decode_shape* shape, const float* h0_dev, const 
                       int32_t* lengths_dev, int32_t* steps_out, void* workspace_dev, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Batched level-by-level TreeLSTM (BASELINE config C5; csrc/tree.cu).
+ *
+ * Replaces the reference's recursive evaluation of the TreeLSTM program
+ * (FuncCall / TreeLeft / TreeRight / TreeValue, graph/
+ * execute.py:136-146, 191-194) for a whole forest.  The host schedule
+ * (paper_1810_08061_b200/tree.py) numbers the forest's nodes, lists leaves,
+ * orders internal nodes by height (order[], level_off_host[nlevels+1]) and
+ * gives each node the X row of its parent: dest[n] = 2*row + side, -1 = root.
+ *   value [nnodes] (leaf values), wc [H], U [2H, 5H] (gate blocks i|f_l|f_r|o|u,
+ *   rows 0..H-1 multiply h_left, H..2H-1 h_right), bias [5H] (bf repeated)
+ *   h_out/c_out [nnodes, H] (every node's state), math 0 fp32 / 1 TF32.
+ * ------------------------------------------------------------------------- */
+int64_t skb_tree_workspace_bytes(int nnodes, int ninternal, int hidden);
+skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int hidden, int nlevels, const int32_t* leaves_dev,
+                         const int32_t* order_dev, const int32_t* level_off_host, const int32_t* left_dev,
+                         const int32_t* right_dev, const int32_t* dest_dev, const float* value_dev,
+                         const float* wc_dev, const float* u_dev, const float* bias_dev, int math, float* h_out_dev,
+                         float* c_out_dev, void* workspace_dev, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Vector-stream region executor (csrc/stream.cu; compiler stream.py).
  *
  * Replaces `execute` (graph/execute.py:27-36) for staged programs whose

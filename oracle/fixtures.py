@@ -243,3 +243,51 @@ def make_greedy_feeds(case) -> dict:
             "w_in": rng.uniform(-1, 1, (E, H)), "u": rng.uniform(-1, 1, (H, H)) * case["uscale"],
             "w_out": rng.uniform(-1, 1, (H, V)), "ids": np.arange(V, dtype=np.int64),
             "eos": np.asarray(case["eos"], dtype=np.int64), "max_len": np.asarray(case["max_len"], dtype=np.int64)}
+
+
+# ---------------------------------------------------------------- TreeLSTM (C5)
+TREE_WEIGHTS = ["wc", "uil", "uir", "ufll", "uflr", "ufrl", "ufrr", "uol", "uor", "uul", "uur", "bi", "bf", "bo", "bu"]
+
+
+def random_tree_arrays(n_leaves, rng):
+    """A random binary tree with n_leaves leaves as (value, left, right) arrays
+    in pre-order (node 0 = root, -1 = no child); internal values are 0."""
+    val, left, right = [], [], []
+
+    def build(n):
+        i = len(val)
+        val.append(0.0)
+        left.append(-1)
+        right.append(-1)
+        if n == 1:
+            val[i] = float(rng.uniform(-1, 1))
+            return i
+        k = int(rng.integers(1, n))
+        left[i] = build(k)
+        right[i] = build(n - k)
+        return i
+    build(n_leaves)
+    return np.asarray(val), np.asarray(left, dtype=np.int64), np.asarray(right, dtype=np.int64)
+
+
+def tree_str(val, left, right, i=0):
+    """The reference Tree's text form '(v (l) (r))', '()' for empty."""
+    if i < 0:
+        return "()"
+    return f"({float(val[i])!r} {tree_str(val, left, right, left[i])} {tree_str(val, left, right, right[i])})"
+
+
+def tree_weights(H, seed, scale=1.0):
+    rng = np.random.default_rng(seed)
+    w = {"wc": rng.uniform(-1, 1, (1, H))}
+    for k in TREE_WEIGHTS[1:11]:
+        w[k] = rng.uniform(-1, 1, (H, H)) * scale / np.sqrt(H)
+    for k in TREE_WEIGHTS[11:]:
+        w[k] = rng.uniform(-0.5, 0.5, (H,))
+    return w
+
+
+TREE_CASES = [
+    {"name": "treelstm_h8", "H": 8, "seed": 61, "leaves": [2, 3, 5, 8, 1, 13], "note": "mixed shapes incl. a single leaf"},
+    {"name": "treelstm_h16", "H": 16, "seed": 62, "leaves": [32, 7, 20], "note": "C5 leaf count (32)"},
+]

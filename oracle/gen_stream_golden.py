@@ -122,7 +122,7 @@ def main(argv):
         print(f"{name:24s} {what} ({doc['reference_seconds']} s in the reference executor)")
 
 
-if __name__ == "__main__" and sys.argv[1:2] != ["--greedy"]:
+if __name__ == "__main__" and sys.argv[1:2] not in (["--greedy"], ["--tree"]):
     main(sys.argv[1:])
 
 
@@ -164,3 +164,40 @@ def greedy_goldens():
 
 if __name__ == "__main__" and sys.argv[1:2] == ["--greedy"]:
     greedy_goldens()
+
+
+def tree_goldens():
+    """tests/golden/treelstm_*.json: the TreeLSTM program (oracle/programs/
+    tree_lstm.msl) run natively by the reference's
+    interpret_module (runtime/__init__.py:41-46) on random binary trees, plus the
+    graph of the first tree traced with a concrete Tree (unrolled, Cond-free)."""
+    from stagekit.graph.tensor import Tree
+    from stagekit.runtime import ParamSpec, interpret_module, trace_module
+    from stagekit.syntax import parse_module
+    path = os.path.join(fixtures.PROGRAMS, "tree_lstm.msl")
+    src = open(path).read()
+    for case in fixtures.TREE_CASES:
+        module = parse_module(src, "tree_lstm.msl")
+        H = case["H"]
+        w = fixtures.tree_weights(H, case["seed"])
+        rng = np.random.default_rng(case["seed"] + 1000)
+        trees, outs = [], []
+
+        def to_tree(val, left, right, i=0):
+            if i < 0:
+                return Tree()
+            return Tree(float(val[i]), to_tree(val, left, right, left[i]), to_tree(val, left, right, right[i]))
+        for n in case["leaves"]:
+            val, left, right = fixtures.random_tree_arrays(n, rng)
+            trees.append(fixtures.tree_str(val, left, right))
+            res, _ = interpret_module(module, "tree_lstm", [to_tree(val, left, right)] +
+                                      [_ref_value(w[k]) for k in fixtures.TREE_WEIGHTS])
+            outs.append([list(res.items[0].data), list(res.items[1].data)])
+        doc = {"case": case, "generator": "oracle/gen_stream_golden.py --tree", "trees": trees, "expected": outs}
+        with open(fixtures.golden_path(case["name"]), "w") as f:
+            json.dump(doc, f, separators=(",", ":"))
+        print(case["name"], len(trees), "trees; root h[0] =", [o[0][0] for o in outs])
+
+
+if __name__ == "__main__" and sys.argv[1:2] == ["--tree"]:
+    tree_goldens()

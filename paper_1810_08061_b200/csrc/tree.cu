@@ -1,0 +1,106 @@
+// tree.cu — batched level-by-level TreeLSTM (BASELINE config C5).
+//
+// The reference evaluates a TreeLSTM by recursion over `Tree` values (the
+// interpreter's FuncCall / TreeLeft / TreeRight / TreeValue, graph/execute.py:
+// 136-146, 191-194; or a concrete tree unrolled at trace time).  Here the
+// forest is scheduled by node height on the host (the tree structure is host
+// data, like the reference's Tree objects) and every height level of every
+// tree in the batch is one step:
+//   tree_leaves  all leaves: c = wc * value, h = tanh(c)   (App. D leaf rule)
+//   per level    G = X_level @ U  (X rows = [h_left, h_right] of the level's nodes,
+//                U = [2H, 5H] gate blocks i | f_l | f_r | o | u; cuBLAS)
+//                tree_cell: gates + bias -> c = i*u + f_l*c_l + f_r*c_r, h = o*tanh(c)
+// Each node's h is written straight into its parent's X row (left or right
+// half), so no gather pass exists between levels.  Semantics: oracle/tree.py
+// (bit-exact with the reference interpreter in float64).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include "blas.cuh"
+#include "skb_internal.h"
+
+namespace {
+
+__device__ __forceinline__ float sigmoidf_ref(float x) {   // reference tensor.py:403-407
+  if (x >= 0.f) return 1.f / (1.f + expf(-x));
+  const float e = expf(x);
+  return e / (1.f + e);
+}
+
+// dest[n] = 2*row + side of node n's h in its parent's X row (-1 for roots)
+__global__ void tree_leaves(const int32_t* __restrict__ leaves, int nleaves, const float* __restrict__ value,
+                            const float* __restrict__ wc, const int32_t* __restrict__ dest, float* __restrict__ h,
+                            float* __restrict__ c, float* __restrict__ X, int H) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)nleaves * H;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int l = (int)(i / H), k = (int)(i % H);
+    const int n = leaves[l];
+    const float cv = wc[k] * value[n];
+    const float hv = tanhf(cv);
+    c[(long long)n * H + k] = cv;
+    h[(long long)n * H + k] = hv;
+    const int d = dest[n];
+    if (d >= 0) X[(long long)(d >> 1) * 2 * H + (d & 1) * H + k] = hv;
+  }
+}
+
+__global__ void tree_cell(const int32_t* __restrict__ order, int row0, int nrows, const int32_t* __restrict__ left,
+                          const int32_t* __restrict__ right, const float* __restrict__ G, const float* __restrict__ bias,
+                          const int32_t* __restrict__ dest, float* __restrict__ h, float* __restrict__ c,
+                          float* __restrict__ X, int H) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)nrows * H;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int p = row0 + (int)(i / H), k = (int)(i % H);
+    const int n = order[p];
+    const float* g = G + (long long)p * 5 * H;
+    const float gi = sigmoidf_ref(g[k] + bias[k]);
+    const float gfl = sigmoidf_ref(g[H + k] + bias[H + k]);
+    const float gfr = sigmoidf_ref(g[2 * H + k] + bias[2 * H + k]);
+    const float go = sigmoidf_ref(g[3 * H + k] + bias[3 * H + k]);
+    const float gu = tanhf(g[4 * H + k] + bias[4 * H + k]);
+    const float cv = gi * gu + gfl * c[(long long)left[n] * H + k] + gfr * c[(long long)right[n] * H + k];
+    const float hv = go * tanhf(cv);
+    c[(long long)n * H + k] = cv;
+    h[(long long)n * H + k] = hv;
+    const int d = dest[n];
+    if (d >= 0) X[(long long)(d >> 1) * 2 * H + (d & 1) * H + k] = hv;
+  }
+}
+
+}  // namespace
+
+extern "C" int64_t skb_tree_workspace_bytes(int nnodes, int ninternal, int hidden) {
+  auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+  return al(4ll * ninternal * 2 * hidden) + al(4ll * ninternal * 5 * hidden) + 2 * al(4ll * nnodes * hidden);
+}
+
+extern "C" skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int hidden, int nlevels,
+                                    const int32_t* leaves, const int32_t* order, const int32_t* level_off_host,
+                                    const int32_t* left, const int32_t* right, const int32_t* dest,
+                                    const float* value, const float* wc, const float* U, const float* bias, int math,
+                                    float* h_out, float* c_out, void* workspace, void* stream) {
+  if (nnodes <= 0 || hidden <= 0 || nleaves <= 0) return SKB_ERR_INVALID;
+  cudaStream_t cs = (cudaStream_t)stream;
+  const int H = hidden;
+  auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+  uint8_t* ws = (uint8_t*)workspace;
+  float* X = (float*)ws;
+  float* G = (float*)(ws + al(4ll * ninternal * 2 * H));
+  float* h = h_out ? h_out : (float*)(ws + al(4ll * ninternal * 2 * H) + al(4ll * ninternal * 5 * H));
+  float* c = c_out ? c_out : h + (int64_t)nnodes * H;
+  const int blocks = 148 * 8;
+  tree_leaves<<<blocks, 256, 0, cs>>>(leaves, nleaves, value, wc, dest, h, c, X, H);
+  cublasHandle_t hb = skb::blas_handle(cs);
+  if (!hb) return SKB_ERR_CUDA;
+  for (int L = 0; L < nlevels; ++L) {
+    const int r0 = level_off_host[L], nr = level_off_host[L + 1] - r0;
+    if (nr <= 0) continue;
+    if (!skb::gemm_f32(hb, math, X + (int64_t)r0 * 2 * H, 2 * H, U, 5 * H, G + (int64_t)r0 * 5 * H, 5 * H, nr, 5 * H,
+                       2 * H))
+      return SKB_ERR_CUDA;
+    const long long work = (long long)nr * H;
+    const int b = (int)((work + 255) / 256 < blocks ? (work + 255) / 256 : blocks);
+    tree_cell<<<b, 256, 0, cs>>>(order, r0, nr, left, right, G, bias, dest, h, c, X, H);
+  }
+  return skb_check_launch();
+}

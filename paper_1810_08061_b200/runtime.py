@@ -65,6 +65,8 @@ SIGNATURES = {
     "skb_decode_last_mode": (ctypes.c_int, []),
     "skb_decode_profile_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float)]),
     "skb_decode": (ctypes.c_int, [ctypes.POINTER(DecodeShape)] + [_VP] * 10 + [ctypes.POINTER(ctypes.c_int32), _VP, _VP]),
+    "skb_tree_workspace_bytes": (ctypes.c_int64, [ctypes.c_int] * 3),
+    "skb_tree_lstm": (ctypes.c_int, [ctypes.c_int] * 5 + [_VP] * 10 + [ctypes.c_int, _VP, _VP, _VP, _VP]),
     "skb_stream_smem_bytes": (ctypes.c_int64, [ctypes.c_int] * 5),
     "skb_stream_grid": (ctypes.c_int, [ctypes.c_int64]),
     "skb_stream_tile_elems": (ctypes.c_int, []),

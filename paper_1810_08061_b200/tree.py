@@ -1,0 +1,136 @@
+"""Batched TreeLSTM over a forest on the GPU (BASELINE config C5; csrc/tree.cu).
+
+The reference evaluates the TreeLSTM program of SURVEY App. D by recursion
+over `Tree` values (graph/execute.py:136-146 Tree ops, :191-194 FuncCall).
+`Forest` flattens any number of trees (reference `Tree` objects, skb
+`values.Tree`, or (value, left, right) arrays in pre-order), computes every
+node's height and schedules the forest level by level: all leaves in one
+launch, then one GEMM + fused cell per height level across the whole batch.
+
+    forest = Forest(trees)
+    h_root, c_root = tree_lstm(forest, weights)      # weights: oracle.fixtures.TREE_WEIGHTS names
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from .values import DeviceTensor
+
+GATES = (("uil", "uir"), ("ufll", "uflr"), ("ufrl", "ufrr"), ("uol", "uor"), ("uul", "uur"))
+
+
+def _flatten_tree(t):
+    val, left, right = [], [], []
+    stack = [(t, -1, 0)]
+    while stack:   # iterative pre-order (trees can be deep)
+        node, parent, side = stack.pop()
+        i = len(val)
+        val.append(float(node.value) if node.value is not None else 0.0)
+        left.append(-1)
+        right.append(-1)
+        if parent >= 0:
+            (left if side == 0 else right)[parent] = i
+        l, r = getattr(node, "left", None), getattr(node, "right", None)
+        if l is not None and getattr(l, "value", None) is not None:
+            stack.append((r, i, 1))
+            stack.append((l, i, 0))
+    return np.asarray(val), np.asarray(left, dtype=np.int64), np.asarray(right, dtype=np.int64)
+
+
+class Forest:
+    """Host schedule of a batch of binary trees (leaves: both children empty)."""
+
+    def __init__(self, trees):
+        vals, lefts, rights, roots = [], [], [], []
+        base = 0
+        for t in trees:
+            val, left, right = t if isinstance(t, tuple) else _flatten_tree(t)
+            vals.append(np.asarray(val, dtype=np.float64))
+            lefts.append(np.where(left >= 0, left + base, -1))
+            rights.append(np.where(right >= 0, right + base, -1))
+            roots.append(base)
+            base += len(val)
+        self.value = np.concatenate(vals)
+        self.left = np.concatenate(lefts).astype(np.int64)
+        self.right = np.concatenate(rights).astype(np.int64)
+        self.roots = np.asarray(roots, dtype=np.int64)
+        n = len(self.value)
+        internal = self.left >= 0
+        if np.any(internal != (self.right >= 0)):
+            raise ValueError("TreeLSTM trees must be full binary trees (0 or 2 children)")
+        height = np.zeros(n, dtype=np.int64)
+        ii = np.nonzero(internal)[0]
+        while True:   # converges in max-height sweeps, each fully vectorised
+            nh = 1 + np.maximum(height[self.left[ii]], height[self.right[ii]])
+            if np.array_equal(nh, height[ii]):
+                break
+            height[ii] = nh
+        self.height = height
+        self.leaves = np.nonzero(~internal)[0]
+        self.order = ii[np.argsort(height[ii], kind="stable")]
+        row = np.full(n, -1, dtype=np.int64)
+        row[self.order] = np.arange(len(self.order))
+        hs = height[self.order]
+        self.nlevels = int(hs.max(initial=0))
+        self.level_off = np.searchsorted(hs, np.arange(1, self.nlevels + 2)).astype(np.int32)
+        parent = np.full(n, -1, dtype=np.int64)
+        side = np.zeros(n, dtype=np.int64)
+        parent[self.left[ii]] = ii
+        parent[self.right[ii]] = ii
+        side[self.right[ii]] = 1
+        self.dest = np.where(parent >= 0, 2 * row[np.maximum(parent, 0)] + side, -1)
+        self._dev = None
+
+    @property
+    def nnodes(self):
+        return len(self.value)
+
+    def device(self, dev):
+        import torch
+        if self._dev is None or self._dev[0] != dev:
+            i32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(dev)
+            self._dev = (dev, {"leaves": i32(self.leaves), "order": i32(self.order), "left": i32(self.left),
+                               "right": i32(self.right), "dest": i32(self.dest),
+                               "value": torch.from_numpy(self.value.astype(np.float32)).to(dev),
+                               "roots": torch.from_numpy(self.roots).to(dev)})
+        return self._dev[1]
+
+
+def pack_weights(w, dev):
+    """U [2H, 5H] (gate blocks i|f_l|f_r|o|u) and bias [5H] on the device."""
+    import torch
+    H = np.asarray(w["wc"]).shape[-1]
+    U = np.zeros((2 * H, 5 * H), dtype=np.float32)
+    for k, (a, b) in enumerate(GATES):
+        U[:H, k * H:(k + 1) * H] = np.asarray(w[a])
+        U[H:, k * H:(k + 1) * H] = np.asarray(w[b])
+    bias = np.concatenate([np.asarray(w[k]).reshape(-1) for k in ("bi", "bf", "bf", "bo", "bu")]).astype(np.float32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
+    return {"H": H, "wc": t(np.asarray(w["wc"]).reshape(-1)), "U": t(U), "bias": t(bias)}
+
+
+def tree_lstm(forest, weights, math="fp32", stream=None, packed=None, all_nodes=False):
+    """Root (h, c) of every tree, [ntrees, H] float32 DeviceTensors (all nodes'
+    states with all_nodes=True)."""
+    import torch
+    from . import runtime as rt
+    lib = rt.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pw = packed or pack_weights(weights, dev)
+    H = pw["H"]
+    d = forest.device(dev)
+    n, ni = forest.nnodes, len(forest.order)
+    ws = torch.empty(int(lib.skb_tree_workspace_bytes(n, max(ni, 1), H)), dtype=torch.uint8, device=dev)
+    h = torch.empty((n, H), dtype=torch.float32, device=dev)
+    c = torch.empty((n, H), dtype=torch.float32, device=dev)
+    off = np.ascontiguousarray(forest.level_off, dtype=np.int32)
+    p = rt.ptr
+    rt.check(lib.skb_tree_lstm(n, len(forest.leaves), ni, H, forest.nlevels, p(d["leaves"]), p(d["order"]),
+                               off.ctypes.data_as(ctypes.c_void_p), p(d["left"]), p(d["right"]), p(d["dest"]),
+                               p(d["value"]), p(pw["wc"]), p(pw["U"]), p(pw["bias"]), 1 if math == "tf32" else 0,
+                               p(h), p(c), p(ws), rt.stream_handle(stream)), "skb_tree_lstm")
+    if all_nodes:
+        return DeviceTensor("f64", h), DeviceTensor("f64", c)
+    return DeviceTensor("f64", h[d["roots"]]), DeviceTensor("f64", c[d["roots"]])

@@ -1,0 +1,37 @@
+"""C5 TreeLSTM on the GPU (csrc/tree.cu via paper_1810_08061_b200.tree):
+the forest's root states against the reference's own interpret_module outputs
+(tests/golden/treelstm_*.json) and the float64 restatement at larger batches.
+fp32 GEMMs: rtol 1e-5 (stated bound); TF32: 2e-3."""
+import numpy as np
+import pytest
+
+from oracle import fixtures
+from oracle import tree as otree
+from paper_1810_08061_b200.tree import Forest, tree_lstm
+from vm_cases import parse_tree
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in fixtures.TREE_CASES])
+def test_forest_matches_reference(name):
+    doc = fixtures.load_golden(name)
+    case = doc["case"]
+    w = fixtures.tree_weights(case["H"], case["seed"])
+    forest = Forest([parse_tree(s) for s in doc["trees"]])
+    h, c = tree_lstm(forest, w)
+    h_ref = np.asarray([e[0] for e in doc["expected"]])
+    c_ref = np.asarray([e[1] for e in doc["expected"]])
+    assert np.allclose(h.array, h_ref, rtol=1e-5, atol=1e-6)
+    assert np.allclose(c.array, c_ref, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("ntrees,leaves,H,math,tol", [(300, 32, 64, "fp32", 1e-5), (257, 17, 128, "tf32", 2e-3)])
+def test_forest_matches_oracle(ntrees, leaves, H, math, tol):
+    rng = np.random.default_rng(ntrees)
+    trees = [fixtures.random_tree_arrays(int(rng.integers(1, leaves + 1)), rng) for _ in range(ntrees)]
+    w = fixtures.tree_weights(H, 5)
+    h_ref, c_ref = otree.forest(trees, w)
+    h, c = tree_lstm(Forest(trees), w, math=math)
+    assert np.allclose(h.array, h_ref, rtol=tol, atol=tol)
+    assert np.allclose(c.array, c_ref, rtol=tol, atol=tol)
