@@ -122,7 +122,7 @@ def main(argv):
         print(f"{name:24s} {what} ({doc['reference_seconds']} s in the reference executor)")
 
 
-if __name__ == "__main__" and sys.argv[1:2] not in (["--greedy"], ["--tree"]):
+if __name__ == "__main__" and sys.argv[1:2] not in (["--greedy"], ["--tree"], ["--bptt"]):
     main(sys.argv[1:])
 
 
@@ -201,3 +201,49 @@ def tree_goldens():
 
 if __name__ == "__main__" and sys.argv[1:2] == ["--tree"]:
     tree_goldens()
+
+
+BPTT_CASES = [
+    {"name": "lstm_bptt_4x3", "T": 4, "B": 3, "F": 3, "H": 4, "lens": [4, 2, 1], "seed": 71},
+    {"name": "lstm_bptt_6x4", "T": 6, "B": 4, "F": 5, "H": 6, "lens": [6, 0, 3, 5], "seed": 72,
+     "note": "a zero-length row, len < T rows frozen"},
+]
+
+
+def bptt_feeds(case):
+    rng = np.random.default_rng(case["seed"])
+    T, B, F, H = case["T"], case["B"], case["F"], case["H"]
+    v = {"x": rng.uniform(-1, 1, (T, B, F)), "h0": rng.uniform(-.5, .5, (B, H)), "c0": rng.uniform(-.5, .5, (B, H)),
+         "lens": np.asarray(case["lens"], dtype=np.int64), "y": rng.uniform(-1, 1, (T, B, H))}
+    for g in "ifgo":
+        v["w" + g] = rng.uniform(-1, 1, (F, H))
+        v["u" + g] = rng.uniform(-1, 1, (H, H))
+        v["b" + g] = np.broadcast_to(rng.uniform(-.5, .5, (1, H)), (B, H)).copy()
+    v["inv_b"] = np.float64(1.0 / B)
+    return v
+
+
+def bptt_goldens():
+    """tests/golden/lstm_bptt_*.json: the hand-derived staged BPTT program
+    (oracle/programs/lstm_bptt.msl) traced and executed by the reference."""
+    from stagekit.graph import execute
+    from stagekit.runtime import ParamSpec, trace_module
+    from stagekit.syntax import parse_module
+    path = os.path.join(fixtures.PROGRAMS, "lstm_bptt.msl")
+    names = ["x", "h0", "c0", "lens", "y"] + [f"{k}{g}" for g in "ifgo" for k in "wub"] + ["inv_b"]
+    for case in BPTT_CASES:
+        v = bptt_feeds(case)
+        module = parse_module(open(path).read(), "lstm_bptt.msl")
+        specs = [ParamSpec(k, "i64" if np.asarray(v[k]).dtype == np.int64 else "f64", tuple(np.asarray(v[k]).shape))
+                 for k in names]
+        graph = trace_module(module, "lstm_bptt", specs).graph
+        res = execute(graph, {k: _ref_value(v[k]) for k in names})
+        doc = {"case": case, "generator": "oracle/gen_stream_golden.py --bptt",
+               "outputs": [{"shape": list(o.shape), "data": list(o.data)} for o in res.outputs]}
+        with open(fixtures.golden_path(case["name"]), "w") as f:
+            json.dump(doc, f, separators=(",", ":"))
+        print(case["name"], "loss", res.outputs[0].data)
+
+
+if __name__ == "__main__" and sys.argv[1:2] == ["--bptt"]:
+    bptt_goldens()
