@@ -194,6 +194,35 @@ skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int hidden, int
                          float* c_out_dev, void* workspace_dev, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Dynamic-length LSTM training step (BASELINE config C2; csrc/train.cu).
+ *
+ * Replaces the reference's hand-derived staged BPTT program (forward While
+ * storing states + reverse While, oracle/programs/lstm_bptt.msl; executed by
+ * graph/execute.py:218-238 — the reference cannot differentiate a While,
+ * graph/grad.py:159-161) for one shard of `rows` sequences:
+ *   x [rows,time,input], y [rows,time,hidden] fp32 batch-major, lens [rows] int64,
+ *   h0/c0 [rows,hidden] or NULL (zeros), params = W [input,4H] | U [H,4H] | b [4H]
+ *   (gate order i,f,g,o), grads (same layout, overwritten), loss (device fp32).
+ * loss = inv_batch * sum_{b, t < len_b} <h_{b,t}, y_{b,t}>; max_len = max(lens)
+ * (the While trip count).  graph != 0 captures the step once per (max_len,
+ * buffers) and replays it as one CUDA graph launch.  The cross-GPU gradient
+ * allreduce (NCCL) runs between this call and skb_sgd_update.
+ * ------------------------------------------------------------------------- */
+typedef struct skb_train_shape {
+  int32_t rows, time, input, hidden;
+  int32_t math;        /* 0 fp32 GEMMs, 1 TF32 tensor cores */
+  int32_t graph;       /* 1: capture/replay the step as a CUDA graph */
+  float inv_batch;     /* 1 / global batch (loss normalisation) */
+} skb_train_shape;
+int64_t skb_train_workspace_bytes(const skb_train_shape* shape);
+skb_status skb_lstm_train_step(const skb_train_shape* shape, const float* x_dev, const float* y_dev,
+                               const int64_t* lens_dev, const float* h0_dev, const float* c0_dev,
+                               const float* params_dev, float* grads_dev, float* loss_dev, int max_len,
+                               void* workspace_dev, void* stream);
+int skb_train_last_mode(void);   /* 1 = the last step replayed a CUDA graph */
+skb_status skb_sgd_update(float* params_dev, const float* grads_dev, int64_t n, float lr, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Vector-stream region executor (csrc/stream.cu; compiler stream.py).
  *
  * Replaces `execute` (graph/execute.py:27-36) for staged programs whose

@@ -1,0 +1,303 @@
+// train.cu — one dynamic-length LSTM training step (BASELINE config C2):
+// forward over the staged While, BPTT, gradients of W [F,4H], U [H,4H],
+// b [4H] (gate order i,f,g,o), and the SGD update.
+//
+// The reference cannot differentiate a While (graph/grad.py:159-161); its
+// training step is the hand-derived staged program oracle/programs/
+// lstm_bptt.msl (forward While storing states, reverse While), executed by
+// graph/execute.py:218-238.  Here, per GPU shard of B rows (batch-major
+// x [B,T,F], y [B,T,H]):
+//   forward  t = 0..n-1:  Z_t = x_t W ; Z_t += h_{t-1} U      (TF32/FP32 cuBLAS, strided views)
+//                         lstm_fwd_cell: gates, c_t, h_t with the row mask
+//                         (rows past their length keep h, c — the Where rule)
+//   loss     inv_b * sum_{b, t<len_b} <h_{b,t}, y_{b,t}>     (deterministic block reduce)
+//   backward t = n-1..0:  lstm_bwd_cell: dG_t (in place of the gate activations),
+//                         carried dh / dc for frozen rows
+//                         dh = dG_t U^T + carry ; dW += x_t^T dG_t ; dU += h_{t-1}^T dG_t
+//   db       column sums of dG
+// The whole step is captured once per (n, buffers) as a CUDA graph, so the
+// ~5n GEMMs and 2n cell kernels replay with a single launch.  The gradient
+// allreduce (NCCL, torch.distributed) and the fused SGD update run after it.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+#include "blas.cuh"
+#include "skb_internal.h"
+
+namespace {
+
+__device__ __forceinline__ float sigf(float x) { return 1.f / (1.f + expf(-x)); }
+
+struct TrainBufs {
+  float* Z;      // [B, T, 4H] pre-activations -> activations (fwd) -> dG (bwd)
+  float* Hs;     // [B, T+1, H] Hs[:, 0] = h0, Hs[:, t+1] = h after step t
+  float* Cs;     // [B, T+1, H]
+  float* dh;     // [B, H]
+  float* dc;     // [B, H]
+  double* part;  // loss partials [kLossBlocks]
+  float* bpart;  // bias-gradient partials [kBiasChunks, 4H]
+};
+constexpr int kLossBlocks = 1184;
+
+__global__ void init_states(const float* h0, const float* c0, TrainBufs w, int B, int T, int H) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)B * H;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / H), k = (int)(i % H);
+    w.Hs[(long long)b * (T + 1) * H + k] = h0 ? h0[i] : 0.f;
+    w.Cs[(long long)b * (T + 1) * H + k] = c0 ? c0[i] : 0.f;
+    w.dh[i] = 0.f;
+    w.dc[i] = 0.f;
+  }
+}
+
+__global__ void lstm_fwd_cell(TrainBufs w, const float* __restrict__ bias, const int64_t* __restrict__ lens, int B,
+                              int T, int H, int t) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)B * H;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / H), k = (int)(i % H);
+    float* z = w.Z + ((long long)b * T + t) * 4 * H;
+    const float ig = sigf(z[k] + bias[k]);
+    const float fg = sigf(z[H + k] + bias[H + k]);
+    const float gg = tanhf(z[2 * H + k] + bias[2 * H + k]);
+    const float og = sigf(z[3 * H + k] + bias[3 * H + k]);
+    const long long sp = ((long long)b * (T + 1) + t) * H + k;   // state before step t
+    const float cp = w.Cs[sp], hp = w.Hs[sp];
+    const bool live = t < lens[b];
+    const float cn = fg * cp + ig * gg;
+    const float hn = og * tanhf(cn);
+    w.Cs[sp + H] = live ? cn : cp;
+    w.Hs[sp + H] = live ? hn : hp;
+    z[k] = ig; z[H + k] = fg; z[2 * H + k] = gg; z[3 * H + k] = og;
+  }
+}
+
+__global__ void lstm_bwd_cell(TrainBufs w, const float* __restrict__ y, const int64_t* __restrict__ lens, float inv_b,
+                              int B, int T, int H, int t) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)B * H;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / H), k = (int)(i % H);
+    const bool live = t < lens[b];
+    float* z = w.Z + ((long long)b * T + t) * 4 * H;
+    float dh = w.dh[i] + (live ? y[((long long)b * T + t) * H + k] * inv_b : 0.f);
+    float dc = w.dc[i];
+    if (!live) {   // frozen row: h_t = h_{t-1}, c_t = c_{t-1}; gradients pass straight through
+      z[k] = 0.f; z[H + k] = 0.f; z[2 * H + k] = 0.f; z[3 * H + k] = 0.f;
+      w.dh[i] = dh;   // the dh GEMM accumulates onto this carry (beta = 1)
+      continue;
+    }
+    const float ig = z[k], fg = z[H + k], gg = z[2 * H + k], og = z[3 * H + k];
+    const long long sp = ((long long)b * (T + 1) + t) * H + k;
+    const float cp = w.Cs[sp], cn = w.Cs[sp + H];
+    const float tc = tanhf(cn);
+    const float dcn = dc + dh * og * (1.f - tc * tc);
+    z[k] = dcn * gg * ig * (1.f - ig);
+    z[H + k] = dcn * cp * fg * (1.f - fg);
+    z[2 * H + k] = dcn * ig * (1.f - gg * gg);
+    z[3 * H + k] = dh * tc * og * (1.f - og);
+    w.dc[i] = dcn * fg;
+    w.dh[i] = 0.f;
+  }
+}
+
+// loss partials: inv_b * sum over live (b, t) of <h_t, y_t>, fixed block order
+__global__ void loss_partials(TrainBufs w, const float* __restrict__ y, const int64_t* __restrict__ lens, float inv_b,
+                              int B, int T, int H, int n) {
+  double acc = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)B * n * H;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i % H);
+    const long long bt = i / H;
+    const int b = (int)(bt / n), t = (int)(bt % n);
+    if (t < lens[b]) acc += (double)w.Hs[((long long)b * (T + 1) + t + 1) * H + k] * y[((long long)b * T + t) * H + k];
+  }
+  __shared__ double red[32];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += red[q];
+    w.part[blockIdx.x] = s * inv_b;
+  }
+}
+
+__global__ void loss_final(const double* part, int n, float* loss) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < n; ++q) s += part[q];
+    *loss = (float)s;
+  }
+}
+
+// db = column sums of dG over (b, t < n), deterministic: stage 1 sums a chunk of
+// rows per (column, chunk) in a fixed order, stage 2 sums the chunks in order.
+constexpr int kBiasChunks = 64;
+__global__ void bias_grad_partial(TrainBufs w, float* __restrict__ part, int B, int T, int H, int n) {
+  const int G = 4 * H;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= G) return;
+  const int chunk = blockIdx.y;
+  const int b0 = (int)((long long)B * chunk / kBiasChunks), b1 = (int)((long long)B * (chunk + 1) / kBiasChunks);
+  float s = 0.f;
+  for (int b = b0; b < b1; ++b)
+    for (int t = 0; t < n; ++t) s += w.Z[((long long)b * T + t) * G + col];
+  part[(long long)chunk * G + col] = s;
+}
+__global__ void bias_grad_final(const float* __restrict__ part, float* __restrict__ db, int G) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= G) return;
+  float s = 0.f;
+  for (int c = 0; c < kBiasChunks; ++c) s += part[(long long)c * G + col];
+  db[col] = s;
+}
+
+__global__ void sgd_update(float* __restrict__ p, const float* __restrict__ g, long long n, float lr) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] -= lr * g[i];
+}
+
+// C = op(A) @ op(B), row-major; column-major C^T = op(B)^T op(A)^T
+bool gemm_rm(cublasHandle_t h, int math, bool ta, bool tb, const float* A, int lda, const float* B, int ldb, float* C,
+             int ldc, int M, int N, int K, float beta) {
+  const float one = 1.f;
+  const cublasComputeType_t ct = math == 1 ? CUBLAS_COMPUTE_32F_FAST_TF32 : CUBLAS_COMPUTE_32F_PEDANTIC;
+  return cublasGemmEx(h, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, N, M, K, &one, B,
+                      CUDA_R_32F, ldb, A, CUDA_R_32F, lda, &beta, C, CUDA_R_32F, ldc, ct,
+                      CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+}
+
+size_t al(size_t b) { return (b + 255) & ~size_t(255); }
+
+void layout(int B, int T, int H, uint8_t* base, TrainBufs* w, size_t* total) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) { uint8_t* p = base ? base + off : nullptr; off += al(bytes); return p; };
+  TrainBufs s;
+  s.Z = (float*)take(4ull * B * T * 4 * H);
+  s.Hs = (float*)take(4ull * B * (T + 1) * H);
+  s.Cs = (float*)take(4ull * B * (T + 1) * H);
+  s.dh = (float*)take(4ull * B * H);
+  s.dc = (float*)take(4ull * B * H);
+  s.part = (double*)take(8ull * kLossBlocks);
+  s.bpart = (float*)take(4ull * kBiasChunks * 4 * H);
+  if (w) *w = s;
+  if (total) *total = off;
+}
+
+bool enqueue(cublasHandle_t hb, cudaStream_t cs, const skb_train_shape& d, TrainBufs& w, const float* x,
+             const float* y, const int64_t* lens, const float* h0, const float* c0, const float* params,
+             float* grads, float* loss, int n) {
+  const int B = d.rows, T = d.time, F = d.input, H = d.hidden, G = 4 * H;
+  const float* W = params;
+  const float* U = params + (size_t)F * G;
+  const float* bias = U + (size_t)H * G;
+  float* dW = grads;
+  float* dU = grads + (size_t)F * G;
+  float* db = dU + (size_t)H * G;
+  const int blocks = 148 * 8;
+  const float inv_b = d.inv_batch;
+  init_states<<<blocks, 256, 0, cs>>>(h0, c0, w, B, T, H);
+  cudaMemsetAsync(grads, 0, sizeof(float) * ((size_t)F * G + (size_t)H * G), cs);
+  for (int t = 0; t < n; ++t) {
+    float* Zt = w.Z + (size_t)t * G;
+    if (!gemm_rm(hb, d.math, false, false, x + (size_t)t * F, T * F, W, G, Zt, T * G, B, G, F, 0.f)) return false;
+    if (!gemm_rm(hb, d.math, false, false, w.Hs + (size_t)t * H, (T + 1) * H, U, G, Zt, T * G, B, G, H, 1.f))
+      return false;
+    lstm_fwd_cell<<<blocks, 256, 0, cs>>>(w, bias, lens, B, T, H, t);
+  }
+  loss_partials<<<kLossBlocks, 256, 0, cs>>>(w, y, lens, inv_b, B, T, H, n);
+  loss_final<<<1, 32, 0, cs>>>(w.part, kLossBlocks, loss);
+  for (int t = n - 1; t >= 0; --t) {
+    float* Zt = w.Z + (size_t)t * G;
+    lstm_bwd_cell<<<blocks, 256, 0, cs>>>(w, y, lens, inv_b, B, T, H, t);
+    // dh_{t-1} = dG_t U^T + carry ; dW += x_t^T dG_t ; dU += h_{t-1}^T dG_t
+    if (!gemm_rm(hb, d.math, false, true, Zt, T * G, U, G, w.dh, H, B, H, G, 1.f)) return false;
+    if (!gemm_rm(hb, d.math, true, false, x + (size_t)t * F, T * F, Zt, T * G, dW, G, F, G, B, 1.f)) return false;
+    if (!gemm_rm(hb, d.math, true, false, w.Hs + (size_t)t * H, (T + 1) * H, Zt, T * G, dU, G, H, G, B, 1.f))
+      return false;
+  }
+  bias_grad_partial<<<dim3((G + 255) / 256, kBiasChunks), 256, 0, cs>>>(w, w.bpart, B, T, H, n);
+  bias_grad_final<<<(G + 255) / 256, 256, 0, cs>>>(w.bpart, db, G);
+  return cudaPeekAtLastError() == cudaSuccess;
+}
+
+struct TrainGraph {
+  skb_train_shape d;
+  const void* ptrs[9];
+  int n;
+  cudaGraphExec_t exec;
+};
+constexpr int kTrainGraphs = 8;
+TrainGraph g_tg[kTrainGraphs];
+int g_ntg = 0;
+int g_train_mode = 0;
+
+}  // namespace
+
+extern "C" int64_t skb_train_workspace_bytes(const skb_train_shape* d) {
+  if (!d) return -1;
+  size_t total = 0;
+  layout(d->rows, d->time, d->hidden, nullptr, nullptr, &total);
+  return (int64_t)total;
+}
+
+extern "C" int skb_train_last_mode(void) { return g_train_mode; }
+
+extern "C" skb_status skb_lstm_train_step(const skb_train_shape* d, const float* x, const float* y,
+                                          const int64_t* lens, const float* h0, const float* c0, const float* params,
+                                          float* grads, float* loss, int max_len, void* workspace, void* stream) {
+  if (!d || d->rows < 1 || d->time < 1 || d->input < 1 || d->hidden < 1 || max_len < 0 || max_len > d->time)
+    return SKB_ERR_INVALID;
+  cudaStream_t cs = (cudaStream_t)stream;
+  TrainBufs w;
+  layout(d->rows, d->time, d->hidden, (uint8_t*)workspace, &w, nullptr);
+  cublasHandle_t hb = skb::blas_handle(cs);
+  if (!hb) return SKB_ERR_CUDA;
+  const void* key[9] = {x, y, lens, h0, c0, params, grads, loss, workspace};
+  cudaGraphExec_t exec = nullptr;
+  for (int i = 0; i < g_ntg; ++i)
+    if (g_tg[i].n == max_len && memcmp(&g_tg[i].d, d, sizeof(*d)) == 0 && memcmp(g_tg[i].ptrs, key, sizeof(key)) == 0)
+      exec = g_tg[i].exec;
+  if (!exec && d->graph) {
+    cudaStream_t cap = nullptr;
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      cublasSetStream(hb, cap);
+      const bool enq = enqueue(hb, cap, *d, w, x, y, lens, h0, c0, params, grads, loss, max_len);
+      ok = cudaStreamEndCapture(cap, &g) == cudaSuccess && enq;
+    }
+    if (ok) ok = cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (cap) cudaStreamDestroy(cap);
+    cublasSetStream(hb, cs);
+    cudaGetLastError();
+    if (!ok) exec = nullptr;
+    if (exec) {
+      if (g_ntg == kTrainGraphs) {
+        cudaGraphExecDestroy(g_tg[0].exec);
+        memmove(g_tg, g_tg + 1, sizeof(TrainGraph) * (kTrainGraphs - 1));
+        --g_ntg;
+      }
+      TrainGraph& e = g_tg[g_ntg++];
+      e.d = *d;
+      memcpy(e.ptrs, key, sizeof(key));
+      e.n = max_len;
+      e.exec = exec;
+    }
+  }
+  g_train_mode = exec ? 1 : 0;
+  if (exec) {
+    if (cudaGraphLaunch(exec, cs) != cudaSuccess) return SKB_ERR_CUDA;
+  } else if (!enqueue(hb, cs, *d, w, x, y, lens, h0, c0, params, grads, loss, max_len)) {
+    return SKB_ERR_CUDA;
+  }
+  return skb_check_launch();
+}
+
+extern "C" skb_status skb_sgd_update(float* params, const float* grads, int64_t n, float lr, void* stream) {
+  if (n < 0) return SKB_ERR_INVALID;
+  sgd_update<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(params, grads, n, lr);
+  return skb_check_launch();
+}

@@ -37,6 +37,13 @@ class DecodeShape(ctypes.Structure):
                                               "eos", "math", "poll")]
 
 
+class TrainShape(ctypes.Structure):
+    """include/skb.h skb_train_shape"""
+    _fields_ = [("rows", ctypes.c_int32), ("time", ctypes.c_int32), ("input", ctypes.c_int32),
+                ("hidden", ctypes.c_int32), ("math", ctypes.c_int32), ("graph", ctypes.c_int32),
+                ("inv_batch", ctypes.c_float)]
+
+
 _VP = ctypes.c_void_p
 _P4 = ctypes.c_void_p * 4
 
@@ -67,6 +74,10 @@ SIGNATURES = {
     "skb_decode": (ctypes.c_int, [ctypes.POINTER(DecodeShape)] + [_VP] * 10 + [ctypes.POINTER(ctypes.c_int32), _VP, _VP]),
     "skb_tree_workspace_bytes": (ctypes.c_int64, [ctypes.c_int] * 3),
     "skb_tree_lstm": (ctypes.c_int, [ctypes.c_int] * 5 + [_VP] * 10 + [ctypes.c_int, _VP, _VP, _VP, _VP]),
+    "skb_train_workspace_bytes": (ctypes.c_int64, [ctypes.POINTER(TrainShape)]),
+    "skb_lstm_train_step": (ctypes.c_int, [ctypes.POINTER(TrainShape)] + [_VP] * 8 + [ctypes.c_int, _VP, _VP]),
+    "skb_train_last_mode": (ctypes.c_int, []),
+    "skb_sgd_update": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_float, _VP]),
     "skb_stream_smem_bytes": (ctypes.c_int64, [ctypes.c_int] * 5),
     "skb_stream_grid": (ctypes.c_int, [ctypes.c_int64]),
     "skb_stream_tile_elems": (ctypes.c_int, []),

@@ -1,0 +1,63 @@
+"""C2 training step on the GPU (csrc/train.cu via paper_1810_08061_b200.train)
+against the float64 BPTT restatement oracle/bptt.py (itself pinned to the
+reference executing the staged BPTT program).  FP32 GEMMs: rtol 1e-4 on loss
+and gradients (stated bound); TF32: 3e-2 relative to the gradient norm."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import bptt
+from paper_1810_08061_b200 import runtime
+from paper_1810_08061_b200.train import LstmTrainer
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(B, T, F, H, seed, lens=None):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, (B, T, F))
+    y = rng.uniform(-1, 1, (B, T, H))
+    h0, c0 = rng.uniform(-.5, .5, (B, H)), rng.uniform(-.5, .5, (B, H))
+    if lens is None:
+        lens = rng.integers(0, T + 1, B)
+    s = 1 / np.sqrt(H)
+    W, U, b = rng.uniform(-s, s, (F, 4 * H)), rng.uniform(-s, s, (H, 4 * H)), rng.uniform(-s, s, 4 * H)
+    return x, y, h0, c0, np.asarray(lens, dtype=np.int64), W, U, b
+
+
+def _dev(a, dt=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device="cuda", dtype=dt)
+
+
+@pytest.mark.parametrize("B,T,F,H,math,tol,graph", [
+    (6, 7, 5, 8, "fp32", 1e-4, True),
+    (16, 20, 32, 64, "fp32", 1e-4, False),
+    (64, 33, 64, 128, "tf32", 3e-2, True),
+])
+def test_train_step_matches_oracle(B, T, F, H, math, tol, graph):
+    x, y, h0, c0, lens, W, U, b = _problem(B, T, F, H, B + T)
+    loss_ref, dW, dU, db = bptt.forward_backward(x, h0, c0, lens, y, W, U, b, 1.0 / B)
+    tr = LstmTrainer(F, H, B, T, global_batch=B, lr=0.0, math=math, graph=graph,
+                     params=np.concatenate([W.reshape(-1), U.reshape(-1), b]))
+    loss = tr.forward_backward(_dev(x), _dev(y), _dev(lens, torch.int64), _dev(h0), _dev(c0))
+    assert runtime.lib().skb_train_last_mode() == (1 if graph else 0)
+    gW, gU, gb = (t.cpu().numpy().astype(np.float64) for t in tr.views(tr.grads))
+    assert abs(float(loss.item()) - loss_ref) <= tol * max(1.0, abs(loss_ref))
+    for got, ref in ((gW, dW), (gU, dU), (gb, db)):
+        assert np.max(np.abs(got - ref)) <= tol * max(1.0, np.max(np.abs(ref))), np.max(np.abs(got - ref))
+
+
+def test_sgd_step_and_replay():
+    B, T, F, H = 8, 9, 6, 16
+    x, y, h0, c0, lens, W, U, b = _problem(B, T, F, H, 5)
+    p0 = np.concatenate([W.reshape(-1), U.reshape(-1), b])
+    tr = LstmTrainer(F, H, B, T, global_batch=B, lr=0.5, math="fp32", params=p0)
+    args = (_dev(x), _dev(y), _dev(lens, torch.int64), _dev(h0), _dev(c0))
+    tr.step(*args)
+    _, dW, dU, db = bptt.forward_backward(x, h0, c0, lens, y, W, U, b, 1.0 / B)
+    p1 = p0 - 0.5 * np.concatenate([dW.reshape(-1), dU.reshape(-1), db])
+    assert np.allclose(tr.params.cpu().numpy(), p1, rtol=1e-4, atol=1e-5)
+    l2 = float(tr.step(*args).item())   # graph replay with the updated parameters
+    W2, U2, b2 = (v.cpu().numpy().astype(np.float64) for v in tr.views(torch.from_numpy(p1.astype(np.float32))))
+    ref2 = bptt.forward_backward(x, h0, c0, lens, y, W2, U2, b2, 1.0 / B)[0]
+    assert abs(l2 - ref2) < 1e-4
