@@ -223,6 +223,21 @@ int skb_train_last_mode(void);   /* 1 = the last step replayed a CUDA graph */
 skb_status skb_sgd_update(float* params_dev, const float* grads_dev, int64_t n, float lr, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * MAML sinusoid meta-gradient (BASELINE config C5; csrc/maml.cu).
+ *
+ * Replaces executing the reference's gradient() (graph/grad.py:35-70) of the
+ * staged one-task program oracle/programs/maml.msl once per task: MLP
+ * 1-H-H-1 ReLU, one inner SGD step (alpha), query MSE; second-order
+ * meta-gradient g_q - alpha * H_s g_q.  theta: w1[H] | b1[H] | w2[H*H] | b2[H]
+ * | w3[H] | b3 (P = H*H + 4H + 1 floats); xs/ys/xq/yq [tasks, shots] fp32.
+ * meta_grad [P] and mean_loss [1] are task means (fixed summation order).
+ * ------------------------------------------------------------------------- */
+int64_t skb_maml_workspace_bytes(int hidden, int tasks);
+skb_status skb_maml_meta_grad(int hidden, int shots, int tasks, const float* theta_dev, const float* xs_dev,
+                              const float* ys_dev, const float* xq_dev, const float* yq_dev, float alpha,
+                              float* meta_grad_dev, float* mean_loss_dev, void* workspace_dev, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Vector-stream region executor (csrc/stream.cu; compiler stream.py).
  *
  * Replaces `execute` (graph/execute.py:27-36) for staged programs whose

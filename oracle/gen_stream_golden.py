@@ -122,7 +122,7 @@ def main(argv):
         print(f"{name:24s} {what} ({doc['reference_seconds']} s in the reference executor)")
 
 
-if __name__ == "__main__" and sys.argv[1:2] not in (["--greedy"], ["--tree"], ["--bptt"]):
+if __name__ == "__main__" and sys.argv[1:2] not in (["--greedy"], ["--tree"], ["--bptt"], ["--maml"]):
     main(sys.argv[1:])
 
 
@@ -247,3 +247,45 @@ def bptt_goldens():
 
 if __name__ == "__main__" and sys.argv[1:2] == ["--bptt"]:
     bptt_goldens()
+
+
+MAML_CASES = [{"name": "maml_h8_k5", "H": 8, "K": 5, "tasks": 3, "seed": 81, "alpha": 0.01},
+              {"name": "maml_h40_k10", "H": 40, "K": 10, "tasks": 2, "seed": 82, "alpha": 0.01}]
+
+
+def maml_goldens():
+    """tests/golden/maml_*.json: per-task query loss and second-order
+    meta-gradient from the reference's gradient() (graph/grad.py:35-70) over
+    the staged one-task MAML program (oracle/programs/maml.msl)."""
+    from oracle import maml as omaml
+    from stagekit.graph import execute
+    from stagekit.graph.grad import gradient
+    from stagekit.runtime import ParamSpec, trace_module
+    from stagekit.syntax import parse_module
+    path = os.path.join(fixtures.PROGRAMS, "maml.msl")
+    for case in MAML_CASES:
+        H, K = case["H"], case["K"]
+        th = omaml.init_theta(H, case["seed"])
+        xs, ys, xq, yq = omaml.sinusoid_tasks(case["tasks"], K, case["seed"] + 1)
+        module = parse_module(open(path).read(), "maml.msl")
+        names = list(omaml.NAMES) + ["xs", "ys", "xq", "yq", "ones", "alpha", "inv_k"]
+        shapes = {k: th[k].shape for k in omaml.NAMES}
+        shapes.update(xs=(K, 1), ys=(K, 1), xq=(K, 1), yq=(K, 1), ones=(K, 1), alpha=(), inv_k=())
+        graph = gradient(trace_module(module, "maml_task", [ParamSpec(k, "f64", shapes[k]) for k in names]).graph,
+                         0, list(omaml.NAMES))
+        outs = []
+        for t in range(case["tasks"]):
+            feeds = {k: _ref_value(th[k]) for k in omaml.NAMES}
+            feeds.update(xs=_ref_value(xs[t]), ys=_ref_value(ys[t]), xq=_ref_value(xq[t]), yq=_ref_value(yq[t]),
+                         ones=_ref_value(np.ones((K, 1))), alpha=_ref_value(np.float64(case["alpha"])),
+                         inv_k=_ref_value(np.float64(1.0 / K)))
+            res = execute(graph, feeds)
+            outs.append([list(o.data) for o in res.outputs])
+        doc = {"case": case, "generator": "oracle/gen_stream_golden.py --maml", "outputs": outs}
+        with open(fixtures.golden_path(case["name"]), "w") as f:
+            json.dump(doc, f, separators=(",", ":"))
+        print(case["name"], "losses", [o[0][0] for o in outs])
+
+
+if __name__ == "__main__" and sys.argv[1:2] == ["--maml"]:
+    maml_goldens()

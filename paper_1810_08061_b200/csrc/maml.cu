@@ -1,0 +1,267 @@
+// maml.cu — MAML sinusoid meta-gradient (BASELINE config C5).
+//
+// The reference differentiates the staged one-task program
+// oracle/programs/maml.msl (MLP 1-H-H-1, ReLU as where(z>0,z,0*z), one
+// hand-written inner SGD step) with gradient() (graph/grad.py:35-70), second
+// order included, and executes the result once per task.  Here one CTA owns a
+// task and keeps everything in shared memory:
+//   support forward + backward       -> g_s, theta' = theta - alpha g_s
+//   query forward + backward at theta' -> g_q (= v)
+//   R-operator of the support pass along v -> H_s v
+//   meta-gradient = g_q - alpha H_s v      (closed form of the reference's
+//                                            second-order adjoint; oracle/maml.py)
+// Per-task meta-gradients are summed in a fixed task order (deterministic) and
+// averaged; the cross-GPU allreduce (tasks sharded) and the meta-update follow.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "skb_internal.h"
+
+namespace {
+
+constexpr int HMAX = 64, KMAXT = 32, TPB = 128;
+
+struct Theta {        // views into a flat parameter block: w1 | b1 | w2 | b2 | w3 | b3
+  float *w1, *b1, *w2, *b2, *w3, *b3;
+};
+__device__ __forceinline__ Theta view(float* p, int H) {
+  Theta t;
+  t.w1 = p; t.b1 = p + H; t.w2 = p + 2 * H; t.b2 = t.w2 + H * H; t.w3 = t.b2 + H; t.b3 = t.w3 + H;
+  return t;
+}
+
+// y[K,H] = relu-input z = x w1 + b1 (x: [K], w1: [H])
+__device__ void layer1(const float* x, const float* w1, const float* b1, float* z, float* a, int K, int H) {
+  for (int i = threadIdx.x; i < K * H; i += TPB) {
+    const int k = i / H, j = i % H;
+    const float v = x[k] * w1[j] + b1[j];
+    z[i] = v;
+    if (a) a[i] = v > 0.f ? v : 0.f;
+  }
+}
+// z2[K,H] = a1 @ w2 + b2
+__device__ void layer2(const float* a1, const float* w2, const float* b2, float* z2, float* a2, int K, int H) {
+  for (int i = threadIdx.x; i < K * H; i += TPB) {
+    const int k = i / H, j = i % H;
+    float s = 0.f;
+    for (int q = 0; q < H; ++q) s += a1[k * H + q] * w2[q * H + j];
+    s += b2[j];
+    z2[i] = s;
+    if (a2) a2[i] = s > 0.f ? s : 0.f;
+  }
+}
+// p[K] = a2 @ w3 + b3
+__device__ void layer3(const float* a2, const float* w3, const float* b3, float* p, int K, int H) {
+  for (int k = threadIdx.x; k < K; k += TPB) {
+    float s = 0.f;
+    for (int q = 0; q < H; ++q) s += a2[k * H + q] * w3[q];
+    p[k] = s + b3[0];
+  }
+}
+
+// Backward of the MLP for output adjoint dp[K]; writes gradients into g.
+// dz2 / dz1 scratch [K,H].  All extra operands optional (R-op reuse).
+__device__ void backward(const float* x, Theta th, const float* z1, const float* a1, const float* z2,
+                         const float* a2, const float* dp, float* dz1, float* dz2, Theta g, int K, int H) {
+  for (int i = threadIdx.x; i < K * H; i += TPB) {   // dz2 = (dp w3^T) * [z2 > 0]
+    const int k = i / H, j = i % H;
+    dz2[i] = z2[i] > 0.f ? dp[k] * th.w3[j] : 0.f;
+  }
+  for (int j = threadIdx.x; j < H; j += TPB) {      // gw3 = a2^T dp, gb3
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += a2[k * H + j] * dp[k];
+    g.w3[j] = s;
+  }
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += dp[k];
+    g.b3[0] = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < H * H; i += TPB) {  // gw2 = a1^T dz2
+    const int q = i / H, j = i % H;
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += a1[k * H + q] * dz2[k * H + j];
+    g.w2[i] = s;
+  }
+  for (int j = threadIdx.x; j < H; j += TPB) {
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += dz2[k * H + j];
+    g.b2[j] = s;
+  }
+  for (int i = threadIdx.x; i < K * H; i += TPB) {  // dz1 = (dz2 w2^T) * [z1 > 0]
+    const int k = i / H, q = i % H;
+    float s = 0.f;
+    for (int j = 0; j < H; ++j) s += dz2[k * H + j] * th.w2[q * H + j];
+    dz1[i] = z1[i] > 0.f ? s : 0.f;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < H; j += TPB) {      // gw1 = x^T dz1, gb1
+    float s = 0.f, t = 0.f;
+    for (int k = 0; k < K; ++k) { s += x[k] * dz1[k * H + j]; t += dz1[k * H + j]; }
+    g.w1[j] = s;
+    g.b1[j] = t;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(TPB) maml_task_kernel(int H, int K, int P, const float* __restrict__ theta_g,
+                                                        const float* __restrict__ xs, const float* __restrict__ ys,
+                                                        const float* __restrict__ xq, const float* __restrict__ yq,
+                                                        float alpha, float* __restrict__ task_grad,
+                                                        float* __restrict__ task_loss) {
+  extern __shared__ float sm[];
+  const int task = blockIdx.x;
+  const int KH = K * H;
+  float* th_p = sm;              // P
+  float* th2_p = th_p + P;       // P  adapted weights
+  float* gs_p = th2_p + P;       // P  support gradient, then reused for H_s v
+  float* gq_p = gs_p + P;        // P  query gradient (= v)
+  float* z1 = gq_p + P; float* a1 = z1 + KH; float* z2 = a1 + KH; float* a2 = z2 + KH;
+  float* dz1 = a2 + KH; float* dz2 = dz1 + KH;
+  float* q1 = dz2 + KH; float* qa1 = q1 + KH; float* q2 = qa1 + KH; float* qa2 = q2 + KH;
+  float* r1 = qa2 + KH; float* r2 = r1 + KH; float* rd2 = r2 + KH; float* rd1 = rd2 + KH;
+  float* x = rd1 + KH; float* y = x + KMAXT; float* xqs = y + KMAXT; float* yqs = xqs + KMAXT;
+  float* p = yqs + KMAXT; float* dp = p + KMAXT; float* rp = dp + KMAXT; float* rdp = rp + KMAXT;
+  for (int i = threadIdx.x; i < P; i += TPB) th_p[i] = theta_g[i];
+  for (int k = threadIdx.x; k < K; k += TPB) {
+    x[k] = xs[(long long)task * K + k]; y[k] = ys[(long long)task * K + k];
+    xqs[k] = xq[(long long)task * K + k]; yqs[k] = yq[(long long)task * K + k];
+  }
+  __syncthreads();
+  const Theta th = view(th_p, H), th2 = view(th2_p, H), gs = view(gs_p, H), gq = view(gq_p, H);
+  const float inv_k = 1.f / (float)K;
+  // support pass
+  layer1(x, th.w1, th.b1, z1, a1, K, H);
+  __syncthreads();
+  layer2(a1, th.w2, th.b2, z2, a2, K, H);
+  __syncthreads();
+  layer3(a2, th.w3, th.b3, p, K, H);
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += TPB) dp[k] = (p[k] - y[k]) * (2.f * inv_k);
+  __syncthreads();
+  backward(x, th, z1, a1, z2, a2, dp, dz1, dz2, gs, K, H);
+  for (int i = threadIdx.x; i < P; i += TPB) th2_p[i] = th_p[i] - alpha * gs_p[i];
+  __syncthreads();
+  // query pass at theta'
+  layer1(xqs, th2.w1, th2.b1, q1, qa1, K, H);
+  __syncthreads();
+  layer2(qa1, th2.w2, th2.b2, q2, qa2, K, H);
+  __syncthreads();
+  layer3(qa2, th2.w3, th2.b3, rp, K, H);   // rp holds the query prediction for now
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float l = 0.f;
+    for (int k = 0; k < K; ++k) { const float e = rp[k] - yqs[k]; l += e * e; }
+    task_loss[task] = l * inv_k;
+  }
+  for (int k = threadIdx.x; k < K; k += TPB) rdp[k] = (rp[k] - yqs[k]) * (2.f * inv_k);
+  __syncthreads();
+  backward(xqs, th2, q1, qa1, q2, qa2, rdp, rd1, rd2, gq, K, H);
+  // R-operator of the support pass along v = g_q
+  const Theta v = gq;
+  for (int i = threadIdx.x; i < KH; i += TPB) {      // R{a1} = (x v_w1 + v_b1) [z1>0]
+    const int k = i / H, j = i % H;
+    const float rz = x[k] * v.w1[j] + v.b1[j];
+    r1[i] = z1[i] > 0.f ? rz : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < KH; i += TPB) {      // R{a2} = (R{a1} w2 + a1 v_w2 + v_b2) [z2>0]
+    const int k = i / H, j = i % H;
+    float s = v.b2[j];
+    for (int q = 0; q < H; ++q) s += r1[k * H + q] * th.w2[q * H + j] + a1[k * H + q] * v.w2[q * H + j];
+    r2[i] = z2[i] > 0.f ? s : 0.f;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += TPB) {       // R{dp} = (2/K)(R{a2} w3 + a2 v_w3 + v_b3)
+    float s = v.b3[0];
+    for (int q = 0; q < H; ++q) s += r2[k * H + q] * th.w3[q] + a2[k * H + q] * v.w3[q];
+    rdp[k] = s * (2.f * inv_k);
+  }
+  __syncthreads();
+  // H_s v, written over g_s: w3/b3, then R{dz2}, w2/b2, R{dz1}, w1/b1
+  for (int j = threadIdx.x; j < H; j += TPB) {
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += r2[k * H + j] * dp[k] + a2[k * H + j] * rdp[k];
+    gs.w3[j] = s;
+  }
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += rdp[k];
+    gs.b3[0] = s;
+  }
+  for (int i = threadIdx.x; i < KH; i += TPB) {      // R{dz2} = (R{dp} w3^T + dp v_w3^T) [z2>0]
+    const int k = i / H, j = i % H;
+    rd2[i] = z2[i] > 0.f ? rdp[k] * th.w3[j] + dp[k] * v.w3[j] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < H * H; i += TPB) {   // R{gw2} = R{a1}^T dz2 + a1^T R{dz2}
+    const int q = i / H, j = i % H;
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += r1[k * H + q] * dz2[k * H + j] + a1[k * H + q] * rd2[k * H + j];
+    gs.w2[i] = s;
+  }
+  for (int j = threadIdx.x; j < H; j += TPB) {
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += rd2[k * H + j];
+    gs.b2[j] = s;
+  }
+  for (int i = threadIdx.x; i < KH; i += TPB) {      // R{dz1} = (R{dz2} w2^T + dz2 v_w2^T) [z1>0]
+    const int k = i / H, q = i % H;
+    float s = 0.f;
+    for (int j = 0; j < H; ++j) s += rd2[k * H + j] * th.w2[q * H + j] + dz2[k * H + j] * v.w2[q * H + j];
+    rd1[i] = z1[i] > 0.f ? s : 0.f;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < H; j += TPB) {
+    float s = 0.f, t = 0.f;
+    for (int k = 0; k < K; ++k) { s += x[k] * rd1[k * H + j]; t += rd1[k * H + j]; }
+    gs.w1[j] = s;
+    gs.b1[j] = t;
+  }
+  __syncthreads();
+  float* out = task_grad + (long long)task * P;
+  for (int i = threadIdx.x; i < P; i += TPB) out[i] = gq_p[i] - alpha * gs_p[i];
+}
+
+// mean over tasks in a fixed order (deterministic), one thread per parameter
+__global__ void maml_reduce(const float* __restrict__ task_grad, const float* __restrict__ task_loss, int n, int P,
+                            float* __restrict__ grad, float* __restrict__ loss) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= P; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    if (i < P) {
+      for (int t = 0; t < n; ++t) s += task_grad[(long long)t * P + i];
+      grad[i] = (float)(s / n);
+    } else {
+      for (int t = 0; t < n; ++t) s += task_loss[t];
+      loss[0] = (float)(s / n);
+    }
+  }
+}
+
+size_t smem_for(int H, int K) {
+  const int P = H * H + 4 * H + 1;
+  return sizeof(float) * (4 * (size_t)P + 14 * (size_t)K * H + 8 * KMAXT);
+}
+
+}  // namespace
+
+extern "C" int64_t skb_maml_workspace_bytes(int hidden, int tasks) {
+  const int P = hidden * hidden + 4 * hidden + 1;
+  return (int64_t)sizeof(float) * ((int64_t)tasks * P + tasks);
+}
+
+extern "C" skb_status skb_maml_meta_grad(int hidden, int shots, int tasks, const float* theta, const float* xs,
+                                         const float* ys, const float* xq, const float* yq, float alpha,
+                                         float* meta_grad, float* mean_loss, void* workspace, void* stream) {
+  if (hidden < 1 || hidden > HMAX || shots < 1 || shots > KMAXT || tasks < 1) return SKB_ERR_INVALID;
+  const int P = hidden * hidden + 4 * hidden + 1;
+  float* task_grad = (float*)workspace;
+  float* task_loss = task_grad + (size_t)tasks * P;
+  const size_t sm = smem_for(hidden, shots);
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (cudaFuncSetAttribute(maml_task_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+    return SKB_ERR_CUDA;
+  maml_task_kernel<<<tasks, TPB, sm, cs>>>(hidden, shots, P, theta, xs, ys, xq, yq, alpha, task_grad, task_loss);
+  maml_reduce<<<(P + 256) / 256, 256, 0, cs>>>(task_grad, task_loss, tasks, P, meta_grad, mean_loss);
+  return skb_check_launch();
+}
