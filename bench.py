@@ -319,7 +319,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4", "c5"],
+    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4", "c5", "c5m"],
                     help="c1 = the headline metric (default); c3 = beam-search decoder; c4 = L-BFGS "
                          "(benchmarks/c*.py)")
     ap.add_argument("--sentences", type=int, default=128, help="c3: sentences per GPU")

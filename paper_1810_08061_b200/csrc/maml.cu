@@ -223,18 +223,29 @@ __global__ void __launch_bounds__(TPB) maml_task_kernel(int H, int K, int P, con
   for (int i = threadIdx.x; i < P; i += TPB) out[i] = gq_p[i] - alpha * gs_p[i];
 }
 
-// mean over tasks in a fixed order (deterministic), one thread per parameter
-__global__ void maml_reduce(const float* __restrict__ task_grad, const float* __restrict__ task_loss, int n, int P,
-                            float* __restrict__ grad, float* __restrict__ loss) {
+// mean over tasks in a fixed order (deterministic): stage 1 sums a chunk of
+// tasks per (parameter, chunk), stage 2 sums the chunks in order.
+constexpr int kTaskChunks = 64;
+__global__ void maml_reduce_partial(const float* __restrict__ task_grad, const float* __restrict__ task_loss, int n,
+                                    int P, double* __restrict__ part) {
+  const int chunk = blockIdx.y;
+  const int t0 = (int)((long long)n * chunk / kTaskChunks), t1 = (int)((long long)n * (chunk + 1) / kTaskChunks);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= P; i += gridDim.x * blockDim.x) {
     double s = 0.0;
     if (i < P) {
-      for (int t = 0; t < n; ++t) s += task_grad[(long long)t * P + i];
-      grad[i] = (float)(s / n);
+      for (int t = t0; t < t1; ++t) s += task_grad[(long long)t * P + i];
     } else {
-      for (int t = 0; t < n; ++t) s += task_loss[t];
-      loss[0] = (float)(s / n);
+      for (int t = t0; t < t1; ++t) s += task_loss[t];
     }
+    part[(long long)chunk * (P + 1) + i] = s;
+  }
+}
+__global__ void maml_reduce_final(const double* __restrict__ part, int n, int P, float* __restrict__ grad,
+                                  float* __restrict__ loss) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= P; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < kTaskChunks; ++c) s += part[(long long)c * (P + 1) + i];
+    if (i < P) grad[i] = (float)(s / n); else loss[0] = (float)(s / n);
   }
 }
 
@@ -247,7 +258,7 @@ size_t smem_for(int H, int K) {
 
 extern "C" int64_t skb_maml_workspace_bytes(int hidden, int tasks) {
   const int P = hidden * hidden + 4 * hidden + 1;
-  return (int64_t)sizeof(float) * ((int64_t)tasks * P + tasks);
+  return (int64_t)sizeof(float) * ((int64_t)tasks * P + tasks) + 16 + (int64_t)sizeof(double) * kTaskChunks * (P + 1);
 }
 
 extern "C" skb_status skb_maml_meta_grad(int hidden, int shots, int tasks, const float* theta, const float* xs,
@@ -262,6 +273,8 @@ extern "C" skb_status skb_maml_meta_grad(int hidden, int shots, int tasks, const
   if (cudaFuncSetAttribute(maml_task_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return SKB_ERR_CUDA;
   maml_task_kernel<<<tasks, TPB, sm, cs>>>(hidden, shots, P, theta, xs, ys, xq, yq, alpha, task_grad, task_loss);
-  maml_reduce<<<(P + 256) / 256, 256, 0, cs>>>(task_grad, task_loss, tasks, P, meta_grad, mean_loss);
+  double* part = (double*)(((uintptr_t)(task_loss + tasks) + 15) & ~(uintptr_t)15);
+  maml_reduce_partial<<<dim3((P + 256) / 256, kTaskChunks), 256, 0, cs>>>(task_grad, task_loss, tasks, P, part);
+  maml_reduce_final<<<(P + 256) / 256, 256, 0, cs>>>(part, tasks, P, meta_grad, mean_loss);
   return skb_check_launch();
 }
