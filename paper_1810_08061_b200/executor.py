@@ -56,16 +56,23 @@ def lower(graph) -> RnnProgram:
 
 
 # ------------------------------------------------------------------ feeds
-def bind_feeds(graph, feeds: dict) -> dict:
+def bind_feeds(graph, feeds: dict, memo: Optional[dict] = None) -> dict:
     """Check every main-frame parameter against its feed (reference
     execute.py:39-65): missing -> MissingFeed, dtype -> DtypeMismatch,
-    incompatible declared shape -> ShapeMismatch."""
+    incompatible declared shape -> ShapeMismatch.  `memo` (one dict per
+    execute_many call) checks a value object shared by many feed sets once."""
     out = {}
     for param in graph.main.params:
         name = param.attrs.get("name")
         if name not in feeds:
             raise RuntimeGraphError(f"missing feed for parameter {name!r}", param.origin, E.MISSING_FEED)
         value = feeds[name]
+        if memo is not None:
+            key = (id(param), id(value))
+            if key in memo:
+                out[name] = value
+                continue
+            memo[key] = value   # keeps the object alive, so its id is not reused during the call
         spec = param.out_types[0]
         if spec.dtype == "tree":
             if not hasattr(value, "is_empty"):
@@ -329,7 +336,8 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
     if check:
         validate(graph)
     prog = lower(graph)
-    bound = [bind_feeds(graph, f or {}) for f in feeds_list]
+    memo = {}
+    bound = [bind_feeds(graph, f or {}, memo) for f in feeds_list]
     P = len(bound)
     if P == 0:
         return []
@@ -392,6 +400,11 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
     x32 = (isinstance(xs[0], torch.Tensor) and xs[0].dtype == torch.float32) or \
           (isinstance(xs[0], np.ndarray) and xs[0].dtype == np.float32)
     x_dtype = torch.float32 if x32 else torch.float64
+    if host_outputs is not False and host_outputs is not None and T > 0 and P >= 2 * PIPELINE_CHUNKS and \
+            _all_pinned(prog, bound):
+        out_host, hT_h, cT_h, max_len, status = _run_pipelined(prog, weights, bound, Bsz, T, F, H, P, device, x_dtype,
+                                                              host_outputs, stream)
+        return _assemble(prog, out_host, hT_h, cT_h, max_len, status, Bsz, T, P, return_exceptions)
     x = cat(prog.x, x_dtype)
     h0 = cat(prog.h0, torch.float32).reshape(R, H)
     c0 = cat(prog.c0, torch.float32).reshape(R, H) if prog.cell == CELL_LSTM else None
@@ -408,10 +421,8 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
         status = torch.zeros(4, dtype=torch.int32)
         lv = as_numpy(lens.to("cpu")).reshape(P, Bsz)
         max_len = lv.max(axis=1)
-    if int(status[0]) == E.SKB_ERR_FP16_RANGE:
-        raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
     host_out = None
-    if host_outputs is not False and host_outputs is not None:
+    if host_outputs is not False and host_outputs is not None and int(status[0]) != E.SKB_ERR_FP16_RANGE:
         if isinstance(host_outputs, torch.Tensor):   # caller-owned page-locked buffer
             host_out = host_outputs.view(out.shape)
         else:
@@ -420,6 +431,108 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
         host_hT = hT.to("cpu") if hT is not None else None
         host_cT = cT.to("cpu") if cT is not None else None
         out, hT, cT = host_out, host_hT, host_cT
+    return _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions)
+
+
+PIPELINE_CHUNKS = 4
+
+
+def _all_pinned(prog, bound) -> bool:
+    torch = _torch()
+    srcs = [prog.x, prog.h0, prog.lens] + ([prog.c0] if prog.cell == CELL_LSTM else [])
+    for b in bound:
+        for src in srcs:
+            v = _source_value(src, b)
+            if not (isinstance(v, torch.Tensor) and not v.is_cuda and v.is_pinned()):
+                return False
+    return True
+
+
+def _adjacent_run(vals, shape):
+    """If the tensors are back-to-back contiguous views of one host allocation,
+    one tensor spanning all of them (so the copy is a single DMA), else None."""
+    torch = _torch()
+    v0 = vals[0]
+    if not all(isinstance(v, torch.Tensor) and v.is_contiguous() and v.dtype == v0.dtype for v in vals):
+        return None
+    nb = v0.numel() * v0.element_size()
+    base = v0.data_ptr()
+    if any(v.data_ptr() != base + i * nb or v.numel() != v0.numel() for i, v in enumerate(vals)):
+        return None
+    try:
+        return torch.as_strided(v0, shape, torch.empty(shape, device="meta").stride())
+    except RuntimeError:
+        return None
+
+
+def _run_pipelined(prog, weights, bound, Bsz, T, F, H, P, device, x_dtype, host_outputs, stream):
+    """Host-to-host execute_many in PIPELINE_CHUNKS chunks of problems on three
+    streams: the H2D copy of chunk k+1, the kernels of chunk k and the D2H of
+    chunk k-1 overlap (PCIe full duplex), instead of copy-in, run, copy-out."""
+    torch = _torch()
+    R = Bsz * P
+    comp = stream or torch.cuda.current_stream()
+    s_in, s_out = torch.cuda.Stream(device=device), torch.cuda.Stream(device=device)
+    if isinstance(host_outputs, torch.Tensor):
+        host_out = host_outputs.view(R, T, H)
+    else:
+        host_out = torch.empty((R, T, H), dtype=torch.float32, pin_memory=True)
+    want = {o.kind for o in prog.outputs}
+    hT = torch.empty((R, H), dtype=torch.float32, device=device) if "h_final" in want else None
+    cT = torch.empty((R, H), dtype=torch.float32, device=device) if "c_final" in want else None
+    max_len = torch.zeros(P, dtype=torch.int32, device=device)
+    status = torch.zeros(4, dtype=torch.int32, device=device)
+    step = -(-P // PIPELINE_CHUNKS)
+    keep = []
+    for p0 in range(0, P, step):
+        p1 = min(P, p0 + step)
+        pc = p1 - p0
+        exe = _executable(prog, weights, Bsz, T, F, H, pc, device, comp)
+        rows = slice(p0 * Bsz, p1 * Bsz)
+
+        def stack(src, dtype, shape):
+            dev = torch.empty((pc * Bsz,) + shape, dtype=dtype, device=device)
+            vals = [_source_value(src, b) for b in bound[p0:p1]]
+            run = _adjacent_run(vals, (pc * Bsz,) + shape)
+            if run is not None:   # the chunk's feeds are one contiguous host range: one DMA
+                dev.copy_(run, non_blocking=True)
+                return dev
+            for i, v in enumerate(vals):
+                dev[i * Bsz:(i + 1) * Bsz].copy_(v.reshape((Bsz,) + shape), non_blocking=True)
+            return dev
+        with torch.cuda.stream(s_in):
+            x = stack(prog.x, x_dtype, (T, F))
+            h0 = stack(prog.h0, torch.float32, (H,))
+            c0 = stack(prog.c0, torch.float32, (H,)) if prog.cell == CELL_LSTM else None
+            lens = stack(prog.lens, torch.int64, ())
+            ev_in = torch.cuda.Event()
+            ev_in.record(s_in)
+        out = torch.empty((pc * Bsz, T, H), dtype=torch.float32, device=device)
+        comp.wait_event(ev_in)
+        with torch.cuda.stream(comp):
+            exe.run(x, h0, c0, lens, out, hT[rows] if hT is not None else None,
+                    cT[rows] if cT is not None else None, stream=comp)
+            max_len[p0:p1].copy_(exe.max_len)
+            torch.maximum(status, exe.err, out=status)
+            ev_out = torch.cuda.Event()
+            ev_out.record(comp)
+        s_out.wait_event(ev_out)
+        with torch.cuda.stream(s_out):
+            host_out[rows].copy_(out, non_blocking=True)
+        for t_ in (x, h0, c0, lens, out):   # keep device buffers alive until the streams drain
+            if t_ is not None:
+                t_.record_stream(s_out)
+                t_.record_stream(comp)
+        keep.append((x, h0, c0, lens, out))
+    s_out.synchronize()
+    comp.synchronize()
+    return (host_out, hT.to("cpu") if hT is not None else None, cT.to("cpu") if cT is not None else None,
+            max_len.to("cpu").numpy(), status.to("cpu"))
+
+
+def _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions):
+    if int(status[0]) == E.SKB_ERR_FP16_RANGE:
+        raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
     results = []
     for p in range(P):
         m = int(max_len[p])

@@ -149,18 +149,29 @@ class ListValue:
 
 
 # ------------------------------------------------------------------ coercion
+def _torch_mod():
+    global _TORCH
+    if _TORCH is None:
+        try:
+            import torch
+            _TORCH = torch
+        except ImportError:  # pragma: no cover
+            _TORCH = False
+    return _TORCH
+
+
+_TORCH = None
+
+
 def infer_dtype(v) -> str:
     """Reference dtype string of a feed (reference tensor.py:105-147)."""
+    torch = _torch_mod()
+    if torch and isinstance(v, torch.Tensor):
+        if v.dtype == torch.bool:
+            return "bool"
+        return "f64" if v.dtype.is_floating_point else "i64"
     if hasattr(v, "dtype") and isinstance(getattr(v, "dtype"), str):
         return v.dtype
-    try:
-        import torch
-        if isinstance(v, torch.Tensor):
-            if v.dtype == torch.bool:
-                return "bool"
-            return "f64" if v.dtype.is_floating_point else "i64"
-    except ImportError:  # pragma: no cover
-        pass
     if isinstance(v, (np.ndarray, np.generic)):
         if v.dtype == np.bool_:
             return "bool"
@@ -178,6 +189,9 @@ def infer_dtype(v) -> str:
 
 
 def shape_of(v) -> tuple:
+    torch = _torch_mod()
+    if torch and isinstance(v, torch.Tensor):
+        return tuple(v.shape)
     s = getattr(v, "shape", None)
     if s is not None:
         return tuple(int(d) for d in s)

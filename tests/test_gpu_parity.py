@@ -134,3 +134,27 @@ def test_errors_per_problem(c1_graph):
     res = execute_many(c1_graph, feeds, return_exceptions=True)
     assert isinstance(res[1], RuntimeGraphError) and res[1].cause_kind == "IndexOutOfRange"
     assert not isinstance(res[0], Exception) and not isinstance(res[2], Exception)
+
+
+def test_pipelined_host_to_host_matches_device_path(c1_graph):
+    """Pinned host feeds + host_outputs run in overlapped chunks (H2D / kernels /
+    D2H on three streams); results are bit-identical to one device-resident launch."""
+    import torch
+    from paper_1810_08061_b200 import execute_many
+    feeds = _c1_problems(10, seed=4)
+    dev = execute_many(c1_graph, feeds)
+    pinned = []
+    for f in feeds:
+        g = dict(f)
+        for k in ("input_data", "h0", "c0", "sequence_len"):
+            t = torch.from_numpy(np.ascontiguousarray(f[k]))
+            g[k] = (t.float() if k == "input_data" else t).pin_memory()
+        pinned.append(g)
+    host = execute_many(c1_graph, pinned, host_outputs=True)
+    for a, b in zip(host, dev):
+        assert not a.outputs[0].tensor.is_cuda
+        ref = execute_many(c1_graph, [dict(feeds[0], input_data=np.float32(feeds[0]["input_data"]))])
+        break
+    dev32 = execute_many(c1_graph, [dict(f, input_data=f["input_data"].astype(np.float32)) for f in feeds])
+    for a, b in zip(host, dev32):
+        assert np.array_equal(a.outputs[0].array, b.outputs[0].array)
