@@ -187,6 +187,11 @@ skb_status skb_decode(const skb_decode_shape* shape, const float* h0_dev, const 
  *   h_out/c_out [nnodes, H] (every node's state), math 0 fp32 / 1 TF32.
  * ------------------------------------------------------------------------- */
 int64_t skb_tree_workspace_bytes(int nnodes, int ninternal, int hidden);
+/* Host-side forest schedule (native, O(nodes)): heights, height-sorted internal
+ * nodes with level offsets, leaf list and parent-row destinations (see tree.cu).
+ * Returns the maximum height, or -1 for a node with exactly one child. */
+int skb_tree_schedule(int64_t nnodes, const int64_t* left, const int64_t* right, int32_t* height,
+                      int32_t* order, int32_t* level_off, int32_t* leaves, int32_t* dest);
 skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int hidden, int nlevels, const int32_t* leaves_dev,
                          const int32_t* order_dev, const int32_t* level_off_host, const int32_t* left_dev,
                          const int32_t* right_dev, const int32_t* dest_dev, const float* value_dev,

@@ -104,3 +104,47 @@ extern "C" skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int 
   }
   return skb_check_launch();
 }
+
+// Host-side forest scheduler (native runtime, O(nodes)): heights by one
+// reverse pre-order sweep, internal nodes counting-sorted by height, and each
+// node's destination row/side in its parent's GEMM row.  left/right hold
+// global node ids (-1 for none) with children after their parent (pre-order).
+// Outputs: height[n], order[n_internal], level_off[max_height + 1] (level L
+// occupies order[level_off[L-1] .. level_off[L]) for L = 1..max_height),
+// leaves[n_leaves], dest[n].  Returns max_height, or -1 if a node has exactly
+// one child (TreeLSTM trees are full binary trees).
+extern "C" int skb_tree_schedule(int64_t n, const int64_t* left, const int64_t* right, int32_t* height,
+                                 int32_t* order, int32_t* level_off, int32_t* leaves, int32_t* dest) {
+  int maxh = 0;
+  int64_t nleaf = 0;
+  for (int64_t i = n - 1; i >= 0; --i) {
+    const int64_t l = left[i], r = right[i];
+    if ((l < 0) != (r < 0)) return -1;
+    if (l < 0) { height[i] = 0; continue; }
+    const int h = 1 + (height[l] > height[r] ? height[l] : height[r]);
+    height[i] = h;
+    if (h > maxh) maxh = h;
+  }
+  // counting sort of internal nodes by height (stable in node order)
+  int64_t* cnt = (int64_t*)calloc((size_t)maxh + 2, sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) {
+    if (left[i] < 0) leaves[nleaf++] = (int32_t)i; else cnt[height[i]]++;
+  }
+  int64_t acc = 0;
+  for (int h = 1; h <= maxh; ++h) { level_off[h - 1] = (int32_t)acc; acc += cnt[h]; cnt[h] = level_off[h - 1]; }
+  level_off[maxh] = (int32_t)acc;
+  int32_t* row = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) {
+    row[i] = -1;
+    if (left[i] >= 0) { const int64_t p = cnt[height[i]]++; order[p] = (int32_t)i; row[i] = (int32_t)p; }
+  }
+  for (int64_t i = 0; i < n; ++i) dest[i] = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    if (left[i] < 0) continue;
+    dest[left[i]] = 2 * row[i];
+    dest[right[i]] = 2 * row[i] + 1;
+  }
+  free(row);
+  free(cnt);
+  return maxh;
+}

@@ -73,6 +73,7 @@ SIGNATURES = {
     "skb_decode_profile_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float)]),
     "skb_decode": (ctypes.c_int, [ctypes.POINTER(DecodeShape)] + [_VP] * 10 + [ctypes.POINTER(ctypes.c_int32), _VP, _VP]),
     "skb_tree_workspace_bytes": (ctypes.c_int64, [ctypes.c_int] * 3),
+    "skb_tree_schedule": (ctypes.c_int, [ctypes.c_int64] + [_VP] * 7),
     "skb_tree_lstm": (ctypes.c_int, [ctypes.c_int] * 5 + [_VP] * 10 + [ctypes.c_int, _VP, _VP, _VP, _VP]),
     "skb_train_workspace_bytes": (ctypes.c_int64, [ctypes.POINTER(TrainShape)]),
     "skb_lstm_train_step": (ctypes.c_int, [ctypes.POINTER(TrainShape)] + [_VP] * 8 + [ctypes.c_int, _VP, _VP]),
@@ -117,6 +118,19 @@ def lib() -> ctypes.CDLL:
                                          "(there is no CPU fallback)")
             _lib = load_library()
         return _lib
+
+
+_host_lib = None
+
+
+def host_lib() -> ctypes.CDLL:
+    """The bound library for host-only entry points (e.g. skb_tree_schedule):
+    no CUDA device needed, no device work issued."""
+    global _host_lib
+    with _lock:
+        if _host_lib is None:
+            _host_lib = _lib if _lib is not None else load_library()
+        return _host_lib
 
 
 def check(status: int, what: str):

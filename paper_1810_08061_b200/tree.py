@@ -40,47 +40,40 @@ def _flatten_tree(t):
 
 
 class Forest:
-    """Host schedule of a batch of binary trees (leaves: both children empty)."""
+    """Host schedule of a batch of binary trees (leaves: both children empty);
+    the O(nodes) scheduling pass is native (skb_tree_schedule in csrc/tree.cu)."""
 
     def __init__(self, trees):
-        vals, lefts, rights, roots = [], [], [], []
-        base = 0
-        for t in trees:
-            val, left, right = t if isinstance(t, tuple) else _flatten_tree(t)
-            vals.append(np.asarray(val, dtype=np.float64))
-            lefts.append(np.where(left >= 0, left + base, -1))
-            rights.append(np.where(right >= 0, right + base, -1))
-            roots.append(base)
-            base += len(val)
-        self.value = np.concatenate(vals)
-        self.left = np.concatenate(lefts).astype(np.int64)
-        self.right = np.concatenate(rights).astype(np.int64)
-        self.roots = np.asarray(roots, dtype=np.int64)
+        flat = [t if isinstance(t, tuple) else _flatten_tree(t) for t in trees]
+        sizes = np.fromiter((len(f[0]) for f in flat), dtype=np.int64, count=len(flat))
+        bases = np.concatenate([[0], np.cumsum(sizes)[:-1]]) if len(flat) else np.zeros(0, np.int64)
+        shift = np.repeat(bases, sizes)   # every node's tree offset, one vectorised pass
+        self.value = np.concatenate([np.asarray(f[0], dtype=np.float64) for f in flat])
+        left = np.concatenate([np.asarray(f[1], dtype=np.int64) for f in flat])
+        right = np.concatenate([np.asarray(f[2], dtype=np.int64) for f in flat])
+        self.left = np.where(left >= 0, left + shift, -1)
+        self.right = np.where(right >= 0, right + shift, -1)
+        self.roots = bases.astype(np.int64)
         n = len(self.value)
-        internal = self.left >= 0
-        if np.any(internal != (self.right >= 0)):
+        from . import runtime as rt
+        lib = rt.host_lib()   # the scheduler is host code
+        self.height = np.empty(n, dtype=np.int32)
+        order = np.empty(n, dtype=np.int32)
+        level_off = np.empty(n + 1, dtype=np.int32)
+        leaves = np.empty(n, dtype=np.int32)
+        self.dest = np.empty(n, dtype=np.int32)
+        c = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+        self.left = np.ascontiguousarray(self.left, dtype=np.int64)
+        self.right = np.ascontiguousarray(self.right, dtype=np.int64)
+        maxh = lib.skb_tree_schedule(n, c(self.left), c(self.right), c(self.height), c(order), c(level_off),
+                                     c(leaves), c(self.dest))
+        if maxh < 0:
             raise ValueError("TreeLSTM trees must be full binary trees (0 or 2 children)")
-        height = np.zeros(n, dtype=np.int64)
-        ii = np.nonzero(internal)[0]
-        while True:   # converges in max-height sweeps, each fully vectorised
-            nh = 1 + np.maximum(height[self.left[ii]], height[self.right[ii]])
-            if np.array_equal(nh, height[ii]):
-                break
-            height[ii] = nh
-        self.height = height
-        self.leaves = np.nonzero(~internal)[0]
-        self.order = ii[np.argsort(height[ii], kind="stable")]
-        row = np.full(n, -1, dtype=np.int64)
-        row[self.order] = np.arange(len(self.order))
-        hs = height[self.order]
-        self.nlevels = int(hs.max(initial=0))
-        self.level_off = np.searchsorted(hs, np.arange(1, self.nlevels + 2)).astype(np.int32)
-        parent = np.full(n, -1, dtype=np.int64)
-        side = np.zeros(n, dtype=np.int64)
-        parent[self.left[ii]] = ii
-        parent[self.right[ii]] = ii
-        side[self.right[ii]] = 1
-        self.dest = np.where(parent >= 0, 2 * row[np.maximum(parent, 0)] + side, -1)
+        self.nlevels = int(maxh)
+        self.level_off = level_off[:maxh + 1].copy()
+        ninternal = int(self.level_off[-1]) if maxh > 0 else 0
+        self.order = order[:ninternal].copy()
+        self.leaves = leaves[:n - ninternal].copy()
         self._dev = None
 
     @property
