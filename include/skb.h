@@ -187,6 +187,7 @@ skb_status skb_decode(const skb_decode_shape* shape, const float* h0_dev, const 
  *   h_out/c_out [nnodes, H] (every node's state), math 0 fp32 / 1 TF32.
  * ------------------------------------------------------------------------- */
 int64_t skb_tree_workspace_bytes(int nnodes, int ninternal, int hidden);
+int skb_tree_last_mode(void);   /* 1 = the last skb_tree_lstm replayed a captured CUDA graph */
 /* Host-side forest schedule (native, O(nodes)): heights, height-sorted internal
  * nodes with level offsets, leaf list and parent-row destinations (see tree.cu).
  * Returns the maximum height, or -1 for a node with exactly one child. */

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 #include "blas.cuh"
 #include "skb_internal.h"
 
@@ -27,20 +29,23 @@ __device__ __forceinline__ float sigmoidf_ref(float x) {   // reference tensor.p
   return e / (1.f + e);
 }
 
-// dest[n] = 2*row + side of node n's h in its parent's X row (-1 for roots)
+// dest[n] = 2*row + side of node n's h in its parent's X row (-1 for roots).
+// One CTA row per node (blockDim.x covers H): no per-element integer division.
 __global__ void tree_leaves(const int32_t* __restrict__ leaves, int nleaves, const float* __restrict__ value,
                             const float* __restrict__ wc, const int32_t* __restrict__ dest, float* __restrict__ h,
                             float* __restrict__ c, float* __restrict__ X, int H) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)nleaves * H;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int l = (int)(i / H), k = (int)(i % H);
+  for (int l = blockIdx.x * blockDim.y + threadIdx.y; l < nleaves; l += gridDim.x * blockDim.y) {
     const int n = leaves[l];
-    const float cv = wc[k] * value[n];
-    const float hv = tanhf(cv);
-    c[(long long)n * H + k] = cv;
-    h[(long long)n * H + k] = hv;
+    const float v = value[n];
     const int d = dest[n];
-    if (d >= 0) X[(long long)(d >> 1) * 2 * H + (d & 1) * H + k] = hv;
+    float* xrow = d >= 0 ? X + (long long)(d >> 1) * 2 * H + (d & 1) * H : nullptr;
+    for (int k = threadIdx.x; k < H; k += blockDim.x) {
+      const float cv = wc[k] * v;
+      const float hv = tanhf(cv);
+      c[(long long)n * H + k] = cv;
+      h[(long long)n * H + k] = hv;
+      if (xrow) xrow[k] = hv;
+    }
   }
 }
 
@@ -48,22 +53,26 @@ __global__ void tree_cell(const int32_t* __restrict__ order, int row0, int nrows
                           const int32_t* __restrict__ right, const float* __restrict__ G, const float* __restrict__ bias,
                           const int32_t* __restrict__ dest, float* __restrict__ h, float* __restrict__ c,
                           float* __restrict__ X, int H) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)nrows * H;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int p = row0 + (int)(i / H), k = (int)(i % H);
+  for (int rr = blockIdx.x * blockDim.y + threadIdx.y; rr < nrows; rr += gridDim.x * blockDim.y) {
+    const int p = row0 + rr;
     const int n = order[p];
     const float* g = G + (long long)p * 5 * H;
-    const float gi = sigmoidf_ref(g[k] + bias[k]);
-    const float gfl = sigmoidf_ref(g[H + k] + bias[H + k]);
-    const float gfr = sigmoidf_ref(g[2 * H + k] + bias[2 * H + k]);
-    const float go = sigmoidf_ref(g[3 * H + k] + bias[3 * H + k]);
-    const float gu = tanhf(g[4 * H + k] + bias[4 * H + k]);
-    const float cv = gi * gu + gfl * c[(long long)left[n] * H + k] + gfr * c[(long long)right[n] * H + k];
-    const float hv = go * tanhf(cv);
-    c[(long long)n * H + k] = cv;
-    h[(long long)n * H + k] = hv;
+    const float* cl = c + (long long)left[n] * H;
+    const float* cr = c + (long long)right[n] * H;
     const int d = dest[n];
-    if (d >= 0) X[(long long)(d >> 1) * 2 * H + (d & 1) * H + k] = hv;
+    float* xrow = d >= 0 ? X + (long long)(d >> 1) * 2 * H + (d & 1) * H : nullptr;
+    for (int k = threadIdx.x; k < H; k += blockDim.x) {
+      const float gi = sigmoidf_ref(g[k] + bias[k]);
+      const float gfl = sigmoidf_ref(g[H + k] + bias[H + k]);
+      const float gfr = sigmoidf_ref(g[2 * H + k] + bias[2 * H + k]);
+      const float go = sigmoidf_ref(g[3 * H + k] + bias[3 * H + k]);
+      const float gu = tanhf(g[4 * H + k] + bias[4 * H + k]);
+      const float cv = gi * gu + gfl * cl[k] + gfr * cr[k];
+      const float hv = go * tanhf(cv);
+      c[(long long)n * H + k] = cv;
+      h[(long long)n * H + k] = hv;
+      if (xrow) xrow[k] = hv;
+    }
   }
 }
 
@@ -74,12 +83,53 @@ extern "C" int64_t skb_tree_workspace_bytes(int nnodes, int ninternal, int hidde
   return al(4ll * ninternal * 2 * hidden) + al(4ll * ninternal * 5 * hidden) + 2 * al(4ll * nnodes * hidden);
 }
 
+namespace {
+
+bool enqueue_forest(cublasHandle_t hb, cudaStream_t cs, int nnodes, int nleaves, int ninternal, int H, int nlevels,
+                    const int32_t* leaves, const int32_t* order, const int32_t* level_off_host, const int32_t* left,
+                    const int32_t* right, const int32_t* dest, const float* value, const float* wc, const float* U,
+                    const float* bias, int math, float* h, float* c, float* X, float* G) {
+  const int blocks = 148 * 8;
+  const int tx = H >= 128 ? 128 : (H >= 64 ? 64 : 32), ty = 256 / tx;   // threads over H x rows per CTA
+  const dim3 blk(tx, ty);
+  tree_leaves<<<(nleaves + ty - 1) / ty < blocks ? (nleaves + ty - 1) / ty : blocks, blk, 0, cs>>>(
+      leaves, nleaves, value, wc, dest, h, c, X, H);
+  for (int L = 0; L < nlevels; ++L) {
+    const int r0 = level_off_host[L], nr = level_off_host[L + 1] - r0;
+    if (nr <= 0) continue;
+    if (!skb::gemm_f32(hb, math, X + (int64_t)r0 * 2 * H, 2 * H, U, 5 * H, G + (int64_t)r0 * 5 * H, 5 * H, nr, 5 * H,
+                       2 * H))
+      return false;
+    const int b = (nr + ty - 1) / ty < blocks ? (nr + ty - 1) / ty : blocks;
+    tree_cell<<<b, blk, 0, cs>>>(order, r0, nr, left, right, G, bias, dest, h, c, X, H);
+  }
+  return cudaPeekAtLastError() == cudaSuccess;
+}
+
+// Forest graphs: the leaf pass and every level's GEMM + cell captured once per
+// (buffers, schedule) and replayed as one launch (the per-level launch gaps
+// dominate the many small top levels).
+struct ForestGraph {
+  const void* ptrs[13];
+  int dims[6];
+  int32_t* levels;
+  cudaGraphExec_t exec;
+};
+constexpr int kForestGraphs = 8;
+ForestGraph g_fg[kForestGraphs];
+int g_nfg = 0;
+int g_tree_mode = 0;
+
+}  // namespace
+
+extern "C" int skb_tree_last_mode(void) { return g_tree_mode; }
+
 extern "C" skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int hidden, int nlevels,
                                     const int32_t* leaves, const int32_t* order, const int32_t* level_off_host,
                                     const int32_t* left, const int32_t* right, const int32_t* dest,
                                     const float* value, const float* wc, const float* U, const float* bias, int math,
                                     float* h_out, float* c_out, void* workspace, void* stream) {
-  if (nnodes <= 0 || hidden <= 0 || nleaves <= 0) return SKB_ERR_INVALID;
+  if (nnodes <= 0 || hidden <= 0 || nleaves <= 0 || nlevels < 0) return SKB_ERR_INVALID;
   cudaStream_t cs = (cudaStream_t)stream;
   const int H = hidden;
   auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
@@ -88,19 +138,73 @@ extern "C" skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int 
   float* G = (float*)(ws + al(4ll * ninternal * 2 * H));
   float* h = h_out ? h_out : (float*)(ws + al(4ll * ninternal * 2 * H) + al(4ll * ninternal * 5 * H));
   float* c = c_out ? c_out : h + (int64_t)nnodes * H;
-  const int blocks = 148 * 8;
-  tree_leaves<<<blocks, 256, 0, cs>>>(leaves, nleaves, value, wc, dest, h, c, X, H);
   cublasHandle_t hb = skb::blas_handle(cs);
   if (!hb) return SKB_ERR_CUDA;
-  for (int L = 0; L < nlevels; ++L) {
-    const int r0 = level_off_host[L], nr = level_off_host[L + 1] - r0;
-    if (nr <= 0) continue;
-    if (!skb::gemm_f32(hb, math, X + (int64_t)r0 * 2 * H, 2 * H, U, 5 * H, G + (int64_t)r0 * 5 * H, 5 * H, nr, 5 * H,
-                       2 * H))
-      return SKB_ERR_CUDA;
-    const long long work = (long long)nr * H;
-    const int b = (int)((work + 255) / 256 < blocks ? (work + 255) / 256 : blocks);
-    tree_cell<<<b, 256, 0, cs>>>(order, r0, nr, left, right, G, bias, dest, h, c, X, H);
+  const void* key[13] = {leaves, order, left, right, dest, value, wc, U, bias, h, c, workspace, nullptr};
+  const int dims[6] = {nnodes, nleaves, ninternal, H, nlevels, math};
+  cudaGraphExec_t exec = nullptr;
+  for (int i = 0; i < g_nfg && !exec; ++i) {
+    const ForestGraph& e = g_fg[i];
+    if (memcmp(e.ptrs, key, sizeof(key)) == 0 && memcmp(e.dims, dims, sizeof(dims)) == 0 &&
+        memcmp(e.levels, level_off_host, sizeof(int32_t) * (nlevels + 1)) == 0)
+      exec = e.exec;
+  }
+  // capture only for a schedule seen before (repeated evaluation of one forest)
+  static uint64_t seen[16] = {0};
+  uint64_t hsh = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = (const unsigned char*)p;
+    for (size_t i = 0; i < n; ++i) hsh = (hsh ^ b[i]) * 1099511628211ull;
+  };
+  mix(key, sizeof(key));
+  mix(dims, sizeof(dims));
+  mix(level_off_host, sizeof(int32_t) * (nlevels + 1));
+  bool again = false;
+  for (int i = 0; i < 16; ++i) again |= seen[i] == hsh;
+  if (!again) {
+    static int next = 0;
+    seen[next] = hsh;
+    next = (next + 1) % 16;
+  }
+  if (!exec && again) {
+    cudaStream_t cap = nullptr;
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      cublasSetStream(hb, cap);
+      const bool enq = enqueue_forest(hb, cap, nnodes, nleaves, ninternal, H, nlevels, leaves, order, level_off_host,
+                                      left, right, dest, value, wc, U, bias, math, h, c, X, G);
+      ok = cudaStreamEndCapture(cap, &g) == cudaSuccess && enq;
+    }
+    if (ok) ok = cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (cap) cudaStreamDestroy(cap);
+    cublasSetStream(hb, cs);
+    cudaGetLastError();
+    if (!ok) {
+      exec = nullptr;
+    } else {
+      if (g_nfg == kForestGraphs) {
+        cudaGraphExecDestroy(g_fg[0].exec);
+        free(g_fg[0].levels);
+        memmove(g_fg, g_fg + 1, sizeof(ForestGraph) * (kForestGraphs - 1));
+        --g_nfg;
+      }
+      ForestGraph& e = g_fg[g_nfg++];
+      memcpy(e.ptrs, key, sizeof(key));
+      memcpy(e.dims, dims, sizeof(dims));
+      e.levels = (int32_t*)malloc(sizeof(int32_t) * (nlevels + 1));
+      memcpy(e.levels, level_off_host, sizeof(int32_t) * (nlevels + 1));
+      e.exec = exec;
+    }
+  }
+  g_tree_mode = exec ? 1 : 0;
+  if (exec) {
+    if (cudaGraphLaunch(exec, cs) != cudaSuccess) return SKB_ERR_CUDA;
+  } else if (!enqueue_forest(hb, cs, nnodes, nleaves, ninternal, H, nlevels, leaves, order, level_off_host, left,
+                             right, dest, value, wc, U, bias, math, h, c, X, G)) {
+    return SKB_ERR_CUDA;
   }
   return skb_check_launch();
 }

@@ -73,6 +73,7 @@ SIGNATURES = {
     "skb_decode_profile_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float)]),
     "skb_decode": (ctypes.c_int, [ctypes.POINTER(DecodeShape)] + [_VP] * 10 + [ctypes.POINTER(ctypes.c_int32), _VP, _VP]),
     "skb_tree_workspace_bytes": (ctypes.c_int64, [ctypes.c_int] * 3),
+    "skb_tree_last_mode": (ctypes.c_int, []),
     "skb_tree_schedule": (ctypes.c_int, [ctypes.c_int64] + [_VP] * 7),
     "skb_tree_lstm": (ctypes.c_int, [ctypes.c_int] * 5 + [_VP] * 10 + [ctypes.c_int, _VP, _VP, _VP, _VP]),
     "skb_train_workspace_bytes": (ctypes.c_int64, [ctypes.POINTER(TrainShape)]),

@@ -115,9 +115,13 @@ def tree_lstm(forest, weights, math="fp32", stream=None, packed=None, all_nodes=
     H = pw["H"]
     d = forest.device(dev)
     n, ni = forest.nnodes, len(forest.order)
-    ws = torch.empty(int(lib.skb_tree_workspace_bytes(n, max(ni, 1), H)), dtype=torch.uint8, device=dev)
-    h = torch.empty((n, H), dtype=torch.float32, device=dev)
-    c = torch.empty((n, H), dtype=torch.float32, device=dev)
+    bufs = d.get(("bufs", H))
+    if bufs is None:   # reused across evaluations of this forest (stable pointers -> CUDA graph replay)
+        bufs = (torch.empty(int(lib.skb_tree_workspace_bytes(n, max(ni, 1), H)), dtype=torch.uint8, device=dev),
+                torch.empty((n, H), dtype=torch.float32, device=dev),
+                torch.empty((n, H), dtype=torch.float32, device=dev))
+        d[("bufs", H)] = bufs
+    ws, h, c = bufs
     off = np.ascontiguousarray(forest.level_off, dtype=np.int32)
     p = rt.ptr
     rt.check(lib.skb_tree_lstm(n, len(forest.leaves), ni, H, forest.nlevels, p(d["leaves"]), p(d["order"]),
@@ -125,5 +129,5 @@ def tree_lstm(forest, weights, math="fp32", stream=None, packed=None, all_nodes=
                                p(d["value"]), p(pw["wc"]), p(pw["U"]), p(pw["bias"]), 1 if math == "tf32" else 0,
                                p(h), p(c), p(ws), rt.stream_handle(stream)), "skb_tree_lstm")
     if all_nodes:
-        return DeviceTensor("f64", h), DeviceTensor("f64", c)
+        return DeviceTensor("f64", h.clone()), DeviceTensor("f64", c.clone())
     return DeviceTensor("f64", h[d["roots"]]), DeviceTensor("f64", c[d["roots"]])

@@ -35,3 +35,19 @@ def test_forest_matches_oracle(ntrees, leaves, H, math, tol):
     h, c = tree_lstm(Forest(trees), w, math=math)
     assert np.allclose(h.array, h_ref, rtol=tol, atol=tol)
     assert np.allclose(c.array, c_ref, rtol=tol, atol=tol)
+
+
+def test_repeated_forest_replays_graph():
+    from paper_1810_08061_b200 import runtime
+    from paper_1810_08061_b200.tree import pack_weights
+    import torch
+    rng = np.random.default_rng(9)
+    trees = [fixtures.random_tree_arrays(int(rng.integers(1, 20)), rng) for _ in range(50)]
+    w = fixtures.tree_weights(32, 6)
+    forest = Forest(trees)
+    pw = pack_weights(w, torch.device("cuda"))
+    first = tree_lstm(forest, w, packed=pw)[0].array
+    outs = [tree_lstm(forest, w, packed=pw)[0].array for _ in range(3)]
+    assert runtime.lib().skb_tree_last_mode() == 1
+    for o in outs:
+        assert np.array_equal(o, first)
