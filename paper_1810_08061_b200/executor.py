@@ -253,15 +253,35 @@ def stream_plan(graph):
     return prog
 
 
+_decode_plans: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def decode_plan(graph):
+    """The staged greedy decoder's operand roles (lowering_decode.py), or None."""
+    from .lowering_decode import lower_greedy
+    with _plans_lock:
+        if graph in _decode_plans:
+            return _decode_plans[graph]
+    try:
+        prog = lower_greedy(graph)
+    except (LoweringError, KeyError, IndexError, AttributeError, StopIteration):
+        prog = None
+    with _plans_lock:
+        _decode_plans[graph] = prog
+    return prog
+
+
 def plan_kind(graph, feeds: Optional[dict] = None) -> str:
-    """'rnn' when the fused recurrent kernel applies, 'stream' for vector-stream
-    programs whose vectors (static shape, else the feeds') have at least
-    STREAM_MIN_ELEMS elements, else 'vm'."""
+    """'rnn' when the fused recurrent kernel applies, 'decode' for the staged
+    greedy decoder, 'stream' for vector-stream programs whose vectors (static
+    shape, else the feeds') have at least STREAM_MIN_ELEMS elements, else 'vm'."""
     try:
         lower(graph)
         return "rnn"
     except LoweringError:
         pass
+    if decode_plan(graph) is not None:
+        return "decode"
     prog = stream_plan(graph)
     if prog is None:
         return "vm"
@@ -290,7 +310,54 @@ def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=N
             return execute_stream(graph, feeds, stream=stream)
         except LoweringError:   # e.g. a list outgrew the tier's capacity: the region VM runs it
             pass
+    if kind == "decode":
+        try:
+            return execute_decode_many(graph, [feeds or {}], stream=stream)[0]
+        except LoweringError:   # feeds outside the fused decoder's contract (e.g. ids != 0..V-1)
+            pass
     return execute_vm(graph, feeds, stream=stream)
+
+
+def execute_decode_many(graph, feeds_list: list, *, stream=None) -> list:
+    """The staged greedy decoder for P feed sets sharing one
+    weight set, eos and max_len: the P sentences decode together in one
+    device-resident loop (csrc/beam.cu, beam 1), each stopping at its own EOS."""
+    torch = _torch()
+    from .decode import Decoder
+    prog = decode_plan(graph)
+    if prog is None:
+        raise LoweringError("not the staged greedy decoder")
+    memo = {}
+    bound = [bind_feeds(graph, f or {}, memo) for f in feeds_list]
+    f0 = bound[0]
+    shared = (prog.emb, prog.w_in, prog.u, prog.w_out, prog.ids, prog.eos, prog.max_len)
+    for b in bound[1:]:
+        for k in shared:
+            if b[k] is not f0[k] and not np.array_equal(as_numpy(b[k]), as_numpy(f0[k])):
+                raise LoweringError("batched greedy decoding needs one weight set, eos and max_len")
+    emb = as_numpy(f0[prog.emb])
+    V = emb.shape[0]
+    if not np.array_equal(as_numpy(f0[prog.ids]).reshape(-1), np.arange(V)):
+        raise LoweringError("ids must be 0..V-1 for the fused argmax")
+    eos = int(as_numpy(f0[prog.eos]).reshape(-1)[0])
+    max_len = int(as_numpy(f0[prog.max_len]).reshape(-1)[0])
+    P = len(bound)
+    if max_len < 0 or not 0 <= eos < V:
+        raise LoweringError("max_len / eos outside the fused decoder's contract")
+    h0 = np.concatenate([as_numpy(b[prog.h0]).reshape(1, -1) for b in bound], axis=0)
+    dec = Decoder("rnn", emb.reshape(V, -1), (as_numpy(f0[prog.w_in]), as_numpy(f0[prog.u]),
+                                             as_numpy(f0[prog.w_out])), P, 1, max_len, eos)
+    out = dec(h0, stream=stream)
+    lengths = out["lengths"][:, 0].to("cpu").numpy()
+    toks = out["tokens"][:, 0, :].to(torch.int64)
+    results = []
+    for p in range(P):
+        n = int(lengths[p])
+        vals = [None, None]
+        vals[prog.toks_out] = DeviceTensor("i64", toks[p, :n + 1])
+        vals[prog.steps_out] = DeviceTensor("i64", torch.tensor(n, dtype=torch.int64, device=toks.device))
+        results.append(ExecutionResult(vals, []))
+    return results
 
 
 def execute_stream(graph, feeds: Optional[dict] = None, *, stream=None) -> ExecutionResult:

@@ -90,3 +90,39 @@ def test_full_size_beam8_properties():
     r32 = decode("lstm", h0, emb, w, K, 2, T, c0=c0, math="fp32")
     same = (r["tokens"][:, 0] == r32["tokens"][:, 0]).all(dim=1).float().mean().item()
     assert same >= 0.5   # TF32 vs fp32 best beams mostly agree (stated looser bound)
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in fixtures.GREEDY_CASES])
+def test_execute_lowers_staged_greedy_graph(name):
+    """The reference's own staged greedy graph through plain `execute`: lowered
+    onto the fused decoder (plan 'decode'), outputs equal the reference's."""
+    from paper_1810_08061_b200 import execute, ir
+    from paper_1810_08061_b200.executor import plan_kind
+    doc = fixtures.load_golden(name)
+    g = ir.from_json(doc["graph"])
+    assert plan_kind(g) == "decode"
+    res = execute(g, fixtures.make_greedy_feeds(doc["case"]))
+    toks, t = res.outputs
+    assert toks.tensor.is_cuda and toks.dtype == "i64"
+    assert toks.array.tolist() == doc["expected"]["outputs"][0]["tensor"]["data"]
+    assert int(t.item()) == doc["expected"]["outputs"][1]["tensor"]["data"][0]
+
+
+def test_greedy_graph_batched_sentences_match_region_vm():
+    """execute_decode_many: 64 sentences (different h0) in one decode loop, each
+    stopping at its own EOS, against the f64 region VM running the same graph."""
+    from paper_1810_08061_b200 import ir
+    from paper_1810_08061_b200.executor import execute_decode_many, execute_vm
+    doc = fixtures.load_golden("greedy_v300_stop")
+    g = ir.from_json(doc["graph"])
+    base = fixtures.make_greedy_feeds(doc["case"])
+    rng = np.random.default_rng(5)
+    feeds = [dict(base, h0=rng.uniform(-1, 1, base["h0"].shape)) for _ in range(64)]
+    fused = execute_decode_many(g, feeds)
+    stops = set()
+    for f, r in zip(feeds[:16], fused[:16]):
+        ref = execute_vm(g, f)
+        assert r.outputs[0].array.tolist() == ref.outputs[0].array.tolist()
+        assert int(r.outputs[1].item()) == int(ref.outputs[1].item())
+        stops.add(int(r.outputs[1].item()))
+    assert len(stops) > 1   # sentences stopped at different steps
