@@ -144,13 +144,19 @@ def cpu_run(P, threads, seed=0):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(threads):
+def cpu_baseline(threads, target_s=10.0):
+    """A bounded sample of ~target_s seconds of CPU work: batches of P problems
+    until the budget is spent."""
     P = max(threads, 32)
-    dt = cpu_run(P, threads, seed=123)
-    return {"value": P * B / dt, "unit": "examples/s", "cores": threads, "kind": "port",
-            "sample": f"{P} C1 problems ({P * B} examples) of the float64 C port of the reference "
+    done, dt, k = 0, 0.0, 0
+    while dt < target_s and k < 64:
+        dt += cpu_run(P, threads, seed=123 + k)
+        done += P
+        k += 1
+    return {"value": done * B / dt, "unit": "examples/s", "cores": threads, "kind": "port",
+            "sample": f"{done} C1 problems ({done * B} examples) of the float64 C port of the reference "
                       f"executor's arithmetic (oracle/skb_oracle.c, bit-exact with the reference) "
-                      f"on {threads} host threads, {dt:.2f} s wall"}
+                      f"on {threads} host threads, {dt:.1f} s wall"}
 
 
 def run_reference(args, rank, world):
