@@ -216,7 +216,7 @@ skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int hidden, int
  * ------------------------------------------------------------------------- */
 typedef struct skb_train_shape {
   int32_t rows, time, input, hidden;
-  int32_t math;        /* 0 fp32 GEMMs, 1 TF32 tensor cores */
+  int32_t math;        /* 0 fp32 GEMMs, 1 TF32 tensor cores, 2 bf16 operands / fp32 accumulate */
   int32_t graph;       /* 1: capture/replay the step as a CUDA graph */
   float inv_batch;     /* 1 / global batch (loss normalisation) */
 } skb_train_shape;

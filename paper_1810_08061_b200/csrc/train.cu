@@ -22,6 +22,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
+#include <cuda_bf16.h>
 #include "blas.cuh"
 #include "skb_internal.h"
 
@@ -37,6 +38,8 @@ struct TrainBufs {
   float* dc;     // [B, H]
   double* part;  // loss partials [kLossBlocks]
   float* bpart;  // bias-gradient partials [kBiasChunks, 4H]
+  // bf16 GEMM operands (math == 2): x, h states, dG and the weights
+  __nv_bfloat16 *Xb, *Hb, *Zb, *Wb, *Ub;
 };
 constexpr int kLossBlocks = 1184;
 
@@ -45,6 +48,7 @@ __global__ void init_states(const float* h0, const float* c0, TrainBufs w, int B
        i += (long long)gridDim.x * blockDim.x) {
     const int b = (int)(i / H), k = (int)(i % H);
     w.Hs[(long long)b * (T + 1) * H + k] = h0 ? h0[i] : 0.f;
+    if (w.Hb) w.Hb[(long long)b * (T + 1) * H + k] = __float2bfloat16(h0 ? h0[i] : 0.f);
     w.Cs[(long long)b * (T + 1) * H + k] = c0 ? c0[i] : 0.f;
     w.dh[i] = 0.f;
     w.dc[i] = 0.f;
@@ -68,6 +72,7 @@ __global__ void lstm_fwd_cell(TrainBufs w, const float* __restrict__ bias, const
     const float hn = og * tanhf(cn);
     w.Cs[sp + H] = live ? cn : cp;
     w.Hs[sp + H] = live ? hn : hp;
+    if (w.Hb) w.Hb[sp + H] = __float2bfloat16(live ? hn : hp);
     z[k] = ig; z[H + k] = fg; z[2 * H + k] = gg; z[3 * H + k] = og;
   }
 }
@@ -81,8 +86,10 @@ __global__ void lstm_bwd_cell(TrainBufs w, const float* __restrict__ y, const in
     float* z = w.Z + ((long long)b * T + t) * 4 * H;
     float dh = w.dh[i] + (live ? y[((long long)b * T + t) * H + k] * inv_b : 0.f);
     float dc = w.dc[i];
+    __nv_bfloat16* zb = w.Zb ? w.Zb + ((long long)b * T + t) * 4 * H : nullptr;
     if (!live) {   // frozen row: h_t = h_{t-1}, c_t = c_{t-1}; gradients pass straight through
       z[k] = 0.f; z[H + k] = 0.f; z[2 * H + k] = 0.f; z[3 * H + k] = 0.f;
+      if (zb) { zb[k] = zb[H + k] = zb[2 * H + k] = zb[3 * H + k] = __float2bfloat16(0.f); }
       w.dh[i] = dh;   // the dh GEMM accumulates onto this carry (beta = 1)
       continue;
     }
@@ -95,6 +102,10 @@ __global__ void lstm_bwd_cell(TrainBufs w, const float* __restrict__ y, const in
     z[H + k] = dcn * cp * fg * (1.f - fg);
     z[2 * H + k] = dcn * ig * (1.f - gg * gg);
     z[3 * H + k] = dh * tc * og * (1.f - og);
+    if (zb) {
+      zb[k] = __float2bfloat16(z[k]); zb[H + k] = __float2bfloat16(z[H + k]);
+      zb[2 * H + k] = __float2bfloat16(z[2 * H + k]); zb[3 * H + k] = __float2bfloat16(z[3 * H + k]);
+    }
     w.dc[i] = dcn * fg;
     w.dh[i] = 0.f;
   }
@@ -157,6 +168,20 @@ __global__ void sgd_update(float* __restrict__ p, const float* __restrict__ g, l
     p[i] -= lr * g[i];
 }
 
+__global__ void to_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16(src[i]);
+}
+
+// bf16 operands, fp32 accumulate/output (math == 2); same row-major convention
+bool gemm_bf(cublasHandle_t h, bool ta, bool tb, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, int ldb,
+             float* C, int ldc, int M, int N, int K, float beta) {
+  const float one = 1.f;
+  return cublasGemmEx(h, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, N, M, K, &one, B,
+                      CUDA_R_16BF, ldb, A, CUDA_R_16BF, lda, &beta, C, CUDA_R_32F, ldc, CUBLAS_COMPUTE_32F,
+                      CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+}
+
 // C = op(A) @ op(B), row-major; column-major C^T = op(B)^T op(A)^T
 bool gemm_rm(cublasHandle_t h, int math, bool ta, bool tb, const float* A, int lda, const float* B, int ldb, float* C,
              int ldc, int M, int N, int K, float beta) {
@@ -169,7 +194,7 @@ bool gemm_rm(cublasHandle_t h, int math, bool ta, bool tb, const float* A, int l
 
 size_t al(size_t b) { return (b + 255) & ~size_t(255); }
 
-void layout(int B, int T, int H, uint8_t* base, TrainBufs* w, size_t* total) {
+void layout(int B, int T, int F, int H, bool bf16, uint8_t* base, TrainBufs* w, size_t* total) {
   size_t off = 0;
   auto take = [&](size_t bytes) { uint8_t* p = base ? base + off : nullptr; off += al(bytes); return p; };
   TrainBufs s;
@@ -180,6 +205,15 @@ void layout(int B, int T, int H, uint8_t* base, TrainBufs* w, size_t* total) {
   s.dc = (float*)take(4ull * B * H);
   s.part = (double*)take(8ull * kLossBlocks);
   s.bpart = (float*)take(4ull * kBiasChunks * 4 * H);
+  if (bf16) {
+    s.Xb = (__nv_bfloat16*)take(2ull * B * T * F);
+    s.Hb = (__nv_bfloat16*)take(2ull * B * (T + 1) * H);
+    s.Zb = (__nv_bfloat16*)take(2ull * B * T * 4 * H);
+    s.Wb = (__nv_bfloat16*)take(2ull * F * 4 * H);
+    s.Ub = (__nv_bfloat16*)take(2ull * H * 4 * H);
+  } else {
+    s.Xb = s.Hb = s.Zb = s.Wb = s.Ub = nullptr;
+  }
   if (w) *w = s;
   if (total) *total = off;
 }
@@ -198,11 +232,23 @@ bool enqueue(cublasHandle_t hb, cudaStream_t cs, const skb_train_shape& d, Train
   const float inv_b = d.inv_batch;
   init_states<<<blocks, 256, 0, cs>>>(h0, c0, w, B, T, H);
   cudaMemsetAsync(grads, 0, sizeof(float) * ((size_t)F * G + (size_t)H * G), cs);
+  const bool bf = d.math == 2;
+  if (bf) {   // bf16 copies of the GEMM operands that do not change during the step
+    to_bf16<<<blocks, 256, 0, cs>>>(x, w.Xb, (long long)B * T * F);
+    to_bf16<<<blocks, 256, 0, cs>>>(W, w.Wb, (long long)F * G);
+    to_bf16<<<blocks, 256, 0, cs>>>(U, w.Ub, (long long)H * G);
+  }
   for (int t = 0; t < n; ++t) {
     float* Zt = w.Z + (size_t)t * G;
-    if (!gemm_rm(hb, d.math, false, false, x + (size_t)t * F, T * F, W, G, Zt, T * G, B, G, F, 0.f)) return false;
-    if (!gemm_rm(hb, d.math, false, false, w.Hs + (size_t)t * H, (T + 1) * H, U, G, Zt, T * G, B, G, H, 1.f))
-      return false;
+    if (bf) {
+      if (!gemm_bf(hb, false, false, w.Xb + (size_t)t * F, T * F, w.Wb, G, Zt, T * G, B, G, F, 0.f)) return false;
+      if (!gemm_bf(hb, false, false, w.Hb + (size_t)t * H, (T + 1) * H, w.Ub, G, Zt, T * G, B, G, H, 1.f))
+        return false;
+    } else {
+      if (!gemm_rm(hb, d.math, false, false, x + (size_t)t * F, T * F, W, G, Zt, T * G, B, G, F, 0.f)) return false;
+      if (!gemm_rm(hb, d.math, false, false, w.Hs + (size_t)t * H, (T + 1) * H, U, G, Zt, T * G, B, G, H, 1.f))
+        return false;
+    }
     lstm_fwd_cell<<<blocks, 256, 0, cs>>>(w, bias, lens, B, T, H, t);
   }
   loss_partials<<<kLossBlocks, 256, 0, cs>>>(w, y, lens, inv_b, B, T, H, n);
@@ -211,10 +257,18 @@ bool enqueue(cublasHandle_t hb, cudaStream_t cs, const skb_train_shape& d, Train
     float* Zt = w.Z + (size_t)t * G;
     lstm_bwd_cell<<<blocks, 256, 0, cs>>>(w, y, lens, inv_b, B, T, H, t);
     // dh_{t-1} = dG_t U^T + carry ; dW += x_t^T dG_t ; dU += h_{t-1}^T dG_t
-    if (!gemm_rm(hb, d.math, false, true, Zt, T * G, U, G, w.dh, H, B, H, G, 1.f)) return false;
-    if (!gemm_rm(hb, d.math, true, false, x + (size_t)t * F, T * F, Zt, T * G, dW, G, F, G, B, 1.f)) return false;
-    if (!gemm_rm(hb, d.math, true, false, w.Hs + (size_t)t * H, (T + 1) * H, Zt, T * G, dU, G, H, G, B, 1.f))
-      return false;
+    if (bf) {
+      const __nv_bfloat16* Zb = w.Zb + (size_t)t * G;
+      if (!gemm_bf(hb, false, true, Zb, T * G, w.Ub, G, w.dh, H, B, H, G, 1.f)) return false;
+      if (!gemm_bf(hb, true, false, w.Xb + (size_t)t * F, T * F, Zb, T * G, dW, G, F, G, B, 1.f)) return false;
+      if (!gemm_bf(hb, true, false, w.Hb + (size_t)t * H, (T + 1) * H, Zb, T * G, dU, G, H, G, B, 1.f))
+        return false;
+    } else {
+      if (!gemm_rm(hb, d.math, false, true, Zt, T * G, U, G, w.dh, H, B, H, G, 1.f)) return false;
+      if (!gemm_rm(hb, d.math, true, false, x + (size_t)t * F, T * F, Zt, T * G, dW, G, F, G, B, 1.f)) return false;
+      if (!gemm_rm(hb, d.math, true, false, w.Hs + (size_t)t * H, (T + 1) * H, Zt, T * G, dU, G, H, G, B, 1.f))
+        return false;
+    }
   }
   bias_grad_partial<<<dim3((G + 255) / 256, kBiasChunks), 256, 0, cs>>>(w, w.bpart, B, T, H, n);
   bias_grad_final<<<(G + 255) / 256, 256, 0, cs>>>(w.bpart, db, G);
@@ -237,7 +291,7 @@ int g_train_mode = 0;
 extern "C" int64_t skb_train_workspace_bytes(const skb_train_shape* d) {
   if (!d) return -1;
   size_t total = 0;
-  layout(d->rows, d->time, d->hidden, nullptr, nullptr, &total);
+  layout(d->rows, d->time, d->input, d->hidden, d->math == 2, nullptr, nullptr, &total);
   return (int64_t)total;
 }
 
@@ -250,7 +304,7 @@ extern "C" skb_status skb_lstm_train_step(const skb_train_shape* d, const float*
     return SKB_ERR_INVALID;
   cudaStream_t cs = (cudaStream_t)stream;
   TrainBufs w;
-  layout(d->rows, d->time, d->hidden, (uint8_t*)workspace, &w, nullptr);
+  layout(d->rows, d->time, d->input, d->hidden, d->math == 2, (uint8_t*)workspace, &w, nullptr);
   cublasHandle_t hb = skb::blas_handle(cs);
   if (!hb) return SKB_ERR_CUDA;
   const void* key[9] = {x, y, lens, h0, c0, params, grads, loss, workspace};

@@ -55,7 +55,8 @@ class LstmTrainer:
         self.params = torch.as_tensor(np.asarray(params, dtype=np.float32)).to(self.dev).contiguous()
         self.grads = torch.zeros_like(self.params)
         self.loss = torch.zeros(1, dtype=torch.float32, device=self.dev)
-        self.shape = rt.TrainShape(rows, time, input_size, hidden, 1 if math == "tf32" else 0, 1 if graph else 0,
+        self.shape = rt.TrainShape(rows, time, input_size, hidden, {"fp32": 0, "tf32": 1, "bf16": 2}[math],
+                                   1 if graph else 0,
                                    1.0 / float(global_batch or rows))
         self.ws = torch.empty(int(self.lib.skb_train_workspace_bytes(ctypes.byref(self.shape))), dtype=torch.uint8,
                               device=self.dev)
