@@ -35,22 +35,20 @@
 #include <stdint.h>
 #include "skb_internal.h"
 
-#ifndef SKB_STREAM_TPB
-#define SKB_STREAM_TPB 512
-#endif
-#ifndef SKB_STREAM_EPT
-#define SKB_STREAM_EPT 4
-#endif
 
 namespace {
 
-constexpr int TPB = SKB_STREAM_TPB;
-constexpr int EPT = SKB_STREAM_EPT;  // elements per thread per tile (EPT/2 pairs)
-constexpr int TILE = TPB * EPT;     // 2048 elements = 16 KB per staged operand
+constexpr int TPB = 512;
+// A CTA owns whole 4096-element units of every vector (unit u -> CTA u mod grid).
+// A group processes a unit as one tile of 8 elements per thread (32 KB per
+// operand per stage) when two such stages fit in shared memory, else as two
+// 2048-element tiles of 4 per thread, so its stage ring still holds two stages.
+constexpr int UNIT = TPB * 8;
+constexpr int TILE = UNIT;          // largest tile (spill-slot size)
 constexpr int kMaxStages = 8;
 constexpr long long kSmemBudget = 220 * 1024;   // dynamic shared memory the kernel may use
 constexpr int kMaxInstr = 256;      // vector instructions per fused group
-constexpr int RMAX = 4;             // reductions per fused group
+constexpr int RMAX = 4;             // reductions per fused group (D_RSUM cases cover 0..3)
 constexpr int kMaxGroupPtrs = 32;   // staged operands / stores per fused group
 
 enum Dt : int { DT_F64 = 0, DT_I64 = 1, DT_BOOL = 2 };
@@ -370,6 +368,8 @@ __device__ __forceinline__ Group decode(const int32_t* g) {
 // sits at (j>>1)*(2*TPB) + 2*tid, so every 16-byte access of a warp is one
 // contiguous 512-byte run (coalesced HBM stores, conflict-free LDS.128).
 __device__ __forceinline__ int elem_of(int j) { return (j >> 1) * (2 * TPB) + threadIdx.x * 2 + (j & 1); }
+// (the pair layout is the same for both tile sizes: an 8-per-thread tile is
+//  two 4-per-thread tiles back to back)
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count)
@@ -396,16 +396,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // One elected thread stages every vector operand of `tile` into stage `st`
 // (one 1-D bulk copy per operand, completion counted in bytes on the stage's
 // mbarrier).  The last tile is rounded up to 16 bytes; buffers are padded.
-__device__ __forceinline__ void issue_tile(const StreamArgs& a, const Smem& s, const Group& G, long long tile,
-                                           int st, int nops) {
-  const long long base = tile * TILE;
+template <int TL>
+__device__ __forceinline__ void issue_tile(const StreamArgs& a, const Smem& s, const Group& G, long long base, int st,
+                                           int nops) {
   const long long left = a.n - base;
-  const uint32_t bytes = (uint32_t)(((left < TILE ? left : TILE) * 8 + 15) & ~15ll);
+  const long long cnt = left < 0 ? 0 : (left < TL ? left : TL);
+  const uint32_t bytes = (uint32_t)((cnt * 8 + 15) & ~15ll);
   uint64_t* bar = s.bars + st;
   mbar_expect_tx(bar, bytes * G.nops);
+  if (bytes == 0) return;
   for (int k = 0; k < G.nops; ++k) {
     const long long* src = reinterpret_cast<const long long*>(s.gptr[k]) + base;
-    bulk_g2s(s.stage + ((long long)st * nops + k) * TILE, src, bytes, bar);
+    bulk_g2s(s.stage + ((long long)st * nops + k) * TL, src, bytes, bar);
   }
 }
 
@@ -425,6 +427,7 @@ __device__ __forceinline__ long long red_combine(int kd, long long x, long long 
 
 // This thread's EPT elements of a tile-sized shared-memory vector (stage,
 // temporary or spill slot): two LDS.128 / STS.128, bank-conflict free.
+template <int EPT>
 __device__ __forceinline__ void lds_lane(const long long* p, long long (&v)[EPT]) {
 #pragma unroll
   for (int j = 0; j < EPT; j += 2) {
@@ -432,6 +435,7 @@ __device__ __forceinline__ void lds_lane(const long long* p, long long (&v)[EPT]
     v[j] = t.x; v[j + 1] = t.y;
   }
 }
+template <int EPT>
 __device__ __forceinline__ void sts_lane(long long* p, const long long (&v)[EPT]) {
 #pragma unroll
   for (int j = 0; j < EPT; j += 2) *reinterpret_cast<longlong2*>(p + elem_of(j)) = make_longlong2(v[j], v[j + 1]);
@@ -444,7 +448,12 @@ __device__ __forceinline__ void sts_lane(long long* p, const long long (&v)[EPT]
 // in registers and rare spills go to a shared-memory stack.
 enum DOp : int {
   D_PUSH_VEC = 1, D_PUSH_SCALAR = 2, D_BIN_VEC = 4, D_BIN_SCALAR = 5, D_BIN_STACK = 7, D_UN = 8,
-  D_SEL = 9, D_STORE = 10, D_RED = 11, D_POP = 13
+  D_SEL = 9, D_STORE = 10, D_RED = 11, D_POP = 13,
+  // f64 fast forms (no per-element dtype / operand-order decisions):
+  // D_FV + 2*op + rev: TOS = TOS op vec (rev: vec op TOS), op in {add, sub, mul}
+  D_FV = 20, D_FS = 30,           // ... same with a broadcast scalar operand
+  D_FK = 40,                      // D_FK + op: TOS = popped op TOS
+  D_RSUM = 50                     // D_RSUM + r: f64 sum reduction r (0..RMAX-1)
 };
 
 __device__ __forceinline__ void lds2(uint32_t addr, long long& x, long long& y) {
@@ -454,10 +463,12 @@ __device__ __forceinline__ void sts2(uint32_t addr, long long x, long long y) {
   asm volatile("st.shared.v2.u64 [%0], {%1, %2};" :: "r"(addr), "l"(x), "l"(y) : "memory");
 }
 // This thread's EPT elements of a tile-sized shared-memory vector at `addr`.
+template <int EPT>
 __device__ __forceinline__ void lds_lane(uint32_t addr, long long (&v)[EPT]) {
 #pragma unroll
   for (int j = 0; j < EPT; j += 2) lds2(addr + 8u * elem_of(j), v[j], v[j + 1]);
 }
+template <int EPT>
 __device__ __forceinline__ void sts_lane(uint32_t addr, const long long (&v)[EPT]) {
 #pragma unroll
   for (int j = 0; j < EPT; j += 2) sts2(addr + 8u * elem_of(j), v[j], v[j + 1]);
@@ -465,6 +476,7 @@ __device__ __forceinline__ void sts_lane(uint32_t addr, const long long (&v)[EPT
 
 // TOS <- (TOS op val) or (val op TOS); the operation is uniform, so the
 // branch on it sits outside the element loop.
+template <int EPT>
 __device__ __forceinline__ void bin_lane(long long (&tos)[EPT], const long long (&val)[EPT], int bz, int dts,
                                          bool tos_left, long long base, long long n, int q, int& div0_q) {
   const int bop = bz & 255;
@@ -505,21 +517,25 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // ring of S stages (full[st]: bytes landed; empty[st]: every warp is done with
 // the stage), the stack program runs over EPT elements per thread, results are
 // stored straight to HBM and reductions end in one per-CTA partial + arrival.
+template <int EPT>
 __device__ __forceinline__ void vector_run(const StreamArgs& a, Smem& s, Ctl& c, const Group& G, int pc) {
-  const long long ntiles = (a.n + TILE - 1) / TILE;
+  constexpr int TL = TPB * EPT, SUB = UNIT / TL;   // tile elements, tiles per owned unit
+  const long long nunits = (a.n + UNIT - 1) / UNIT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nops = G.nops < 1 ? 1 : G.nops;
-  int S = (int)(s.stage_bytes / ((long long)nops * TILE * 8));   // deepest pipeline the operands allow
+  int S = (int)(s.stage_bytes / ((long long)nops * TL * 8));   // deepest pipeline the operands allow
   if (S > kMaxStages) S = kMaxStages;
+  auto tile_base = [&](long long i) {   // i-th tile of this CTA
+    return (blockIdx.x + (i / SUB) * gridDim.x) * UNIT + (i % SUB) * TL;
+  };
   int div0_q = 1 << 30;   // first vector instruction that divided by zero
   long long racc[RMAX];
 #pragma unroll
   for (int r = 0; r < RMAX; ++r) racc[r] = r < G.nred ? red_identity(G.red_kd[r]) : 0;
-  const int nmy = blockIdx.x < ntiles ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  const int nmy = blockIdx.x < nunits ? (int)((nunits - 1 - blockIdx.x) / gridDim.x + 1) * SUB : 0;
   if (tid == 0) {
     asm volatile("fence.proxy.async.global;" ::: "memory");   // generic stores -> bulk-copy reads
-    for (int st = 0; st < S - 1 && st < nmy; ++st)
-      issue_tile(a, s, G, blockIdx.x + (long long)st * gridDim.x, st, nops);
+    for (int st = 0; st < S - 1 && st < nmy; ++st) issue_tile<TL>(a, s, G, tile_base(st), st, nops);
   }
   const int4* ins = s.gins;
   const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(s.stage);
@@ -530,13 +546,13 @@ __device__ __forceinline__ void vector_run(const StreamArgs& a, Smem& s, Ctl& c,
     if (tid == 0 && i + S - 1 < nmy) {
       if (pround > 0)   // wait until every warp released this stage's previous tile
         mbar_wait(s.empty + pst, (s.uses[pst] + (uint32_t)pround - 1) & 1);
-      issue_tile(a, s, G, blockIdx.x + (long long)(i + S - 1) * gridDim.x, pst, nops);
+      issue_tile<TL>(a, s, G, tile_base(i + S - 1), pst, nops);
     }
     if (++pst == S) { pst = 0; ++pround; }
     mbar_wait(s.bars + st, (s.uses[st] + (uint32_t)round) & 1);   // uses[] advance after the loop
-    const long long base = (blockIdx.x + (long long)i * gridDim.x) * TILE;
-    const bool full = base + TILE <= a.n;
-    const uint32_t stage = stage0 + (uint32_t)(st * nops * TILE * 8);
+    const long long base = tile_base(i);
+    const bool full = base + TL <= a.n;
+    const uint32_t stage = stage0 + (uint32_t)(st * nops * TL * 8);
     long long tos[EPT], val[EPT];
     int sp = 0;
     int4 wn = ins[0];
@@ -545,18 +561,18 @@ __device__ __forceinline__ void vector_run(const StreamArgs& a, Smem& s, Ctl& c,
       wn = ins[q + 1];   // next dispatch word in flight while this one executes (gins is padded)
       switch (w.x) {
         case D_PUSH_VEC:
-          if (w.z) sts_lane(stk0 + (uint32_t)(sp++ * TILE * 8), tos);
-          lds_lane(stage + (uint32_t)(w.y * TILE * 8), tos);
+          if (w.z) sts_lane(stk0 + (uint32_t)(sp++ * TL * 8), tos);
+          lds_lane(stage + (uint32_t)(w.y * TL * 8), tos);
           break;
         case D_PUSH_SCALAR: {
-          if (w.z) sts_lane(stk0 + (uint32_t)(sp++ * TILE * 8), tos);
+          if (w.z) sts_lane(stk0 + (uint32_t)(sp++ * TL * 8), tos);
           const long long v = s.W[w.y];
 #pragma unroll
           for (int j = 0; j < EPT; ++j) tos[j] = v;
           break;
         }
         case D_BIN_VEC:
-          lds_lane(stage + (uint32_t)(w.y * TILE * 8), val);
+          lds_lane(stage + (uint32_t)(w.y * TL * 8), val);
           bin_lane(tos, val, w.z, w.w, !((w.z >> 8) & 1), base, a.n, q, div0_q);
           break;
         case D_BIN_SCALAR: {
@@ -567,7 +583,7 @@ __device__ __forceinline__ void vector_run(const StreamArgs& a, Smem& s, Ctl& c,
           break;
         }
         case D_BIN_STACK:   // left = popped value, right = TOS
-          lds_lane(stk0 + (uint32_t)(--sp * TILE * 8), val);
+          lds_lane(stk0 + (uint32_t)(--sp * TL * 8), val);
           bin_lane(tos, val, w.z, w.w, false, base, a.n, q, div0_q);
           break;
         case D_UN:
@@ -576,8 +592,8 @@ __device__ __forceinline__ void vector_run(const StreamArgs& a, Smem& s, Ctl& c,
           break;
         case D_SEL: {   // c, x spilled (c deeper), TOS = y
           long long x[EPT];
-          lds_lane(stk0 + (uint32_t)(--sp * TILE * 8), x);
-          lds_lane(stk0 + (uint32_t)(--sp * TILE * 8), val);
+          lds_lane(stk0 + (uint32_t)(--sp * TL * 8), x);
+          lds_lane(stk0 + (uint32_t)(--sp * TL * 8), val);
 #pragma unroll
           for (int j = 0; j < EPT; ++j) tos[j] = val[j] ? x[j] : tos[j];
           break;
@@ -606,8 +622,53 @@ __device__ __forceinline__ void vector_run(const StreamArgs& a, Smem& s, Ctl& c,
           }
           break;
         }
+#define SKB_FAST(OPC, EXPR)                                                       \
+  case OPC: {                                                                     \
+    _Pragma("unroll") for (int j = 0; j < EPT; ++j) {                             \
+      const double t_ = as_f(tos[j]), v_ = as_f(val[j]);                          \
+      tos[j] = as_w(EXPR);                                                        \
+    }                                                                             \
+    break;                                                                        \
+  }
+#define SKB_FAST_SET(BASE)                                                        \
+  SKB_FAST(BASE + 0, t_ + v_) SKB_FAST(BASE + 1, v_ + t_)                         \
+  SKB_FAST(BASE + 2, t_ - v_) SKB_FAST(BASE + 3, v_ - t_)                         \
+  SKB_FAST(BASE + 4, t_ * v_) SKB_FAST(BASE + 5, v_ * t_)
+        case D_FV: case D_FV + 1: case D_FV + 2: case D_FV + 3: case D_FV + 4: case D_FV + 5:
+          lds_lane(stage + (uint32_t)(w.y * TL * 8), val);
+          switch (w.x) { SKB_FAST_SET(D_FV) }
+          break;
+        case D_FS: case D_FS + 1: case D_FS + 2: case D_FS + 3: case D_FS + 4: case D_FS + 5: {
+          const long long v = s.W[w.y];
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) val[j] = v;
+          switch (w.x) { SKB_FAST_SET(D_FS) }
+          break;
+        }
+        case D_FK: case D_FK + 1: case D_FK + 2:   // left = popped value (val), right = TOS
+          lds_lane(stk0 + (uint32_t)(--sp * TL * 8), val);
+          switch (w.x) {
+            SKB_FAST(D_FK + 0, v_ + t_) SKB_FAST(D_FK + 1, v_ - t_) SKB_FAST(D_FK + 2, v_ * t_)
+          }
+          break;
+#undef SKB_FAST_SET
+#undef SKB_FAST
+#define SKB_RSUM(R)                                                               \
+  case D_RSUM + R: {                                                              \
+    double acc_ = as_f(racc[R]);                                                  \
+    if (full) {                                                                   \
+      _Pragma("unroll") for (int j = 0; j < EPT; ++j) acc_ += as_f(tos[j]);       \
+    } else {                                                                      \
+      _Pragma("unroll") for (int j = 0; j < EPT; ++j)                             \
+        if (base + elem_of(j) < a.n) acc_ += as_f(tos[j]);                        \
+    }                                                                             \
+    racc[R] = as_w(acc_);                                                         \
+    break;                                                                        \
+  }
+        SKB_RSUM(0) SKB_RSUM(1) SKB_RSUM(2) SKB_RSUM(3)
+#undef SKB_RSUM
         default:   // D_POP
-          lds_lane(stk0 + (uint32_t)(--sp * TILE * 8), tos);
+          lds_lane(stk0 + (uint32_t)(--sp * TL * 8), tos);
           break;
       }
     }
@@ -741,7 +802,9 @@ __global__ void __launch_bounds__(TPB, 1) stream_kernel(StreamArgs a) {
     }
     for (int q = tid; q < 4 * G.ninstr; q += TPB) reinterpret_cast<int*>(s.gins)[q] = G.ins[q];
     if (__syncthreads_or(bad)) break;   // identical in every CTA: all stop here
-    vector_run(a, s, c, G, pc);
+    // 8 elements per thread when two stages of full-unit tiles fit, else half tiles
+    if (2ll * (G.nops < 1 ? 1 : G.nops) * UNIT * 8 <= s.stage_bytes) vector_run<8>(a, s, c, G, pc);
+    else vector_run<4>(a, s, c, G, pc);
     if (tid == 0) c.pc = pc + 1;
     __syncthreads();
   }
@@ -770,13 +833,13 @@ size_t smem_bytes(int max_ops, int max_stack, int max_temp, int nwords, int nbuf
   if (max_stack < 1) max_stack = 1;
   if (max_temp < 1) max_temp = 1;
   const size_t fixed = fixed_bytes(max_stack, max_temp, nwords, nbuf);
-  const size_t need = fixed + 2ull * max_ops * TILE * 8;
+  const size_t need = fixed + 2ull * max_ops * (TILE / 2) * 8;   // two stages of half tiles at least
   return need > (size_t)kSmemBudget ? need : (size_t)kSmemBudget;
 }
 
 }  // namespace
 
-extern "C" int skb_stream_tile_elems(void) { return TILE; }
+extern "C" int skb_stream_tile_elems(void) { return UNIT; }   // elements per CTA-owned unit
 
 extern "C" int64_t skb_stream_smem_bytes(int max_ops, int max_stack, int max_temp, int nwords, int nbuf) {
   return (int64_t)smem_bytes(max_ops, max_stack, max_temp, nwords, nbuf);
@@ -819,7 +882,7 @@ extern "C" int skb_stream_run(const void* prog, const int32_t* extra, const int6
   a.max_temp = max_temp < 1 ? 1 : max_temp;
   a.max_steps = max_steps;
   a.smem = smem;
-  if ((size_t)smem < fixed_bytes(a.max_stack, a.max_temp, nwords, nbuf) + 2ull * a.max_ops * TILE * 8)
+  if ((size_t)smem < fixed_bytes(a.max_stack, a.max_temp, nwords, nbuf) + 2ull * a.max_ops * (TILE / 2) * 8)
     return SKB_ERR_INVALID;
   if (cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SKB_ERR_CUDA;

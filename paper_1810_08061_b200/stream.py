@@ -226,6 +226,8 @@ def _result_dtype(op, a, b):
 D_PUSH = {SRC_VEC: 1, SRC_SCALAR: 2}
 D_BIN = {SRC_VEC: 4, SRC_SCALAR: 5, SRC_STACK: 7}
 D_UN, D_SEL, D_STORE, D_RED, D_POP = 8, 9, 10, 11, 13
+D_FV, D_FS, D_FK, D_RSUM = 20, 30, 40, 50
+F64_ALL = 0 | (0 << 4) | (0 << 8)   # dta | dtb << 4 | dto << 8, all f64
 
 
 def _device_code(code):
@@ -235,15 +237,26 @@ def _device_code(code):
         if op == V_PUSH:                        # [src, idx, spill]
             out += [D_PUSH[x], y, z, 0]
         elif op == V_BIN:                       # [bop | rev << 8 | src << 12, idx, dts]
-            out += [D_BIN[(x >> 12) & 15], y, x & 0xFFF, z]
+            bop, rev, src = x & 255, (x >> 8) & 1, (x >> 12) & 15
+            if z == F64_ALL and bop <= 2:       # f64 add/sub/mul: a specialised dispatch case
+                if src == SRC_VEC:
+                    out += [D_FV + 2 * bop + rev, y, 0, 0]
+                    continue
+                if src == SRC_SCALAR:
+                    out += [D_FS + 2 * bop + rev, y, 0, 0]
+                    continue
+                if src == SRC_STACK:
+                    out += [D_FK + bop, 0, 0, 0]
+                    continue
+            out += [D_BIN[src], y, x & 0xFFF, z]
         elif op == V_UN:
             out += [D_UN, x, 0, z]
         elif op == V_SEL:
             out += [D_SEL, 0, 0, 0]
         elif op == V_STORE:
             out += [D_STORE, x, 0, 0]
-        elif op == V_RED:
-            out += [D_RED, x, 0, 0]
+        elif op == V_RED:                       # [r, kind, dt]
+            out += [D_RSUM + x, 0, 0, 0] if (y == 0 and z == DT["f64"]) else [D_RED, x, 0, 0]
         else:
             out += [D_POP, 0, 0, 0]
     return out
