@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <climits>
+#include <cstdlib>
 #include "sm100.cuh"
 #include "skb_internal.h"
 
@@ -34,8 +35,18 @@ using namespace skb;
 
 namespace {
 
-constexpr int kThreads = 320;   // warps 0-7 epilogue, 8 x loader, 9 MMA issuer + TMEM alloc
-constexpr int kEpi = 256;       // epilogue threads: warp w covers TMEM lanes 32*(w&3).. and column half w>>2
+// Block: EW epilogue warps (warp w covers TMEM lane quarter w&3 and batch-column
+// slice w>>2), an x loader warp and an MMA-issuer warp (+ TMEM alloc).
+// EW = 16 halves each epilogue thread's share of a step (the recurrence's
+// critical path); SKB_RNN_EW=8 selects the narrower variant.
+inline int rnn_ew() {
+  static int ew = 0;
+  if (!ew) {
+    const char* e = getenv("SKB_RNN_EW");
+    ew = (e && atoi(e) == 8) ? 8 : 16;
+  }
+  return ew;
+}
 constexpr int kMaxClusterDim = 8;
 constexpr int kGS = 36;   // sG row stride (floats): 32 units + 4 pad, conflict-free LDS.128
 
@@ -183,8 +194,12 @@ SKB_DEV void load_x8<double>(const double* __restrict__ p, int k0, int F, float 
   }
 }
 
-template <int CELL, int NT, typename XT>
-__global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
+template <int CELL, int NT, typename XT, int EW>
+__global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs a) {
+  // EW epilogue warps (8 or 16), then the x loader warp and the MMA warp.
+  constexpr int kEpi = EW * 32, kThreads = kEpi + 64;
+  constexpr int NCOL = NT / (EW / 4);            // batch columns per epilogue warp
+  constexpr int UG = (EW >= 16) ? 4 : 8;         // LSTM units per cell-phase item
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ uint64_t xfull[2], xempty[2], hfull[2], mdone[2], dfree[2];
   __shared__ uint32_t tmem_s;
@@ -213,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
     }
     fence_mbar_init();
   }
-  if (warp == 9) tmem_alloc<512>(&tmem_s);
+  if (warp == EW + 1) tmem_alloc<512>(&tmem_s);
   for (uint32_t i = tid; i < (2 * xbytes + 2 * hbytes) / 16; i += kThreads)
     reinterpret_cast<uint4*>(sX)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
@@ -235,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
     }
     tmem_st_wait();
   }
-  if (warp < 8) bias = a.bpack[q * 128 + (warp & 3) * 32 + lane];
+  if (warp < EW) bias = a.bpack[q * 128 + (warp & 3) * 32 + lane];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -249,22 +264,21 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
   //         (G8 = U/8 unit groups per CTA), so h/c/out/stage are 16/32-byte vectors.
   //   RNN : unit = 32*qw + lane; the thread owns the NT/2 columns of its half.
   const int qw = warp & 3, ch = warp >> 2;
-  constexpr int NHALF = NT / 2;
-  constexpr int NP = (CELL == SKB_CELL_LSTM) ? (NT * 4 + kEpi - 1) / kEpi : 1;   // max pairs per thread
-  constexpr int NCELL = (CELL == SKB_CELL_LSTM) ? NP * 8 : NHALF;
-  const int G8 = U / 8;
+    constexpr int NP = (CELL == SKB_CELL_LSTM) ? (NT * (32 / UG) + kEpi - 1) / kEpi : 1;   // max items per thread
+  constexpr int NCELL = (CELL == SKB_CELL_LSTM) ? NP * UG : NCOL;
+  const int G8 = U / UG;
   int pn[NP], pu[NP];
   bool pv[NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
     const int idx = tid + kEpi * p;
     pn[p] = G8 ? idx / G8 : 0;
-    pu[p] = G8 ? (idx % G8) * 8 : 0;
+    pu[p] = G8 ? (idx % G8) * UG : 0;
     pv[p] = (CELL == SKB_CELL_LSTM) && tid < kEpi && idx < NT * G8;
   }
   const int rnn_u = qw * 32 + lane;
   const int rnn_unit = (int)q * U + rnn_u;
-  const bool rnn_valid = (CELL != SKB_CELL_LSTM) && (warp < 8) && (rnn_u < U) && (rnn_unit < H);
+  const bool rnn_valid = (CELL != SKB_CELL_LSTM) && (warp < EW) && (rnn_u < U) && (rnn_unit < H);
   float hp[NCELL], cc[NCELL];
   uint8_t* gscr = a.hscratch + (size_t)cluster_id_x() * 2 * hbytes;   // this cluster's h_t exchange buffers
 
@@ -333,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
       g_ttrace[(size_t)tile_iter * 4 + 3] = trip;
 #endif
 
-    if (warp < 8) {
+    if (warp < EW) {
       // ======================= epilogue =======================
       if constexpr (CELL == SKB_CELL_LSTM) {
 #pragma unroll
@@ -349,12 +363,12 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
             for (int e = 0; e < 8; ++e) hv[e] = cv[e] = 0.f;
           }
 #pragma unroll
-          for (int e = 0; e < 8; ++e) { hp[p * 8 + e] = hv[e]; cc[p * 8 + e] = cv[e]; }
+          for (int e = 0; e < UG; ++e) { hp[p * UG + e] = hv[e]; cc[p * UG + e] = cv[e]; }
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < NHALF; ++i) {
-          const int r = s_row[ch * NHALF + i];
+        for (int i = 0; i < NCOL; ++i) {
+          const int r = s_row[ch * NCOL + i];
           hp[i] = (rnn_valid && r >= 0) ? a.h0[(size_t)r * H + rnn_unit] : 0.f;
         }
       }
@@ -365,16 +379,16 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
         mbar_wait(&mdone[j], use & 1);
         if (tid == 0) SKB_TRACE(s, 4);
         tc_fence_after();
-        const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16) + j * 2 * NT + ch * NHALF;
+        const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16) + j * 2 * NT + ch * NCOL;
         if constexpr (CELL == SKB_CELL_LSTM) {
           // gate g = warp (warp-uniform): sigmoid for i, f, o; tanh(x) = 2*sigmoid(2x)-1 for g.
           // act = mul / (1 + 2^(kl*z + kb)) + add, z = pre-activation without bias
           const float kl = (qw == 2) ? -2.8853900817779268f : -1.4426950408889634f;
           const float kb = kl * bias;
           const float mul = (qw == 2) ? 2.f : 1.f, add = (qw == 2) ? -1.f : 0.f;
-          float* g_out = sG + (qw * NT + ch * NHALF) * kGS + lane;
+          float* g_out = sG + (qw * NT + ch * NCOL) * kGS + lane;
 #pragma unroll
-          for (int c16 = 0; c16 < NHALF / 16; ++c16) {
+          for (int c16 = 0; c16 < NCOL / 16; ++c16) {
             float v[16], v2[16];
             tmem_ld16(trow + c16 * 16, v);
             if (two_chains) tmem_ld16(trow + NT + c16 * 16, v2);
@@ -395,41 +409,46 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
           for (int p = 0; p < NP; ++p) {
             if (!pv[p]) continue;
             const int n = pn[p];
-            float g4[4][8];
+            float g4[4][UG];
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               const float4* src = reinterpret_cast<const float4*>(sG + (g * NT + n) * kGS + pu[p]);
-              const float4 x0 = src[0], x1 = src[1];
-              g4[g][0] = x0.x; g4[g][1] = x0.y; g4[g][2] = x0.z; g4[g][3] = x0.w;
-              g4[g][4] = x1.x; g4[g][5] = x1.y; g4[g][6] = x1.z; g4[g][7] = x1.w;
+#pragma unroll
+              for (int v4 = 0; v4 < UG / 4; ++v4) {
+                const float4 x0 = src[v4];
+                g4[g][4 * v4] = x0.x; g4[g][4 * v4 + 1] = x0.y; g4[g][4 * v4 + 2] = x0.z; g4[g][4 * v4 + 3] = x0.w;
+              }
             }
             const bool live = t < s_len[n];
-            uint32_t hw[4];
+            uint32_t hw[UG / 2];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float c2 = fmaf(g4[1][e], cc[p * 8 + e], g4[0][e] * g4[2][e]);
+            for (int e = 0; e < UG; ++e) {
+              const float c2 = fmaf(g4[1][e], cc[p * UG + e], g4[0][e] * g4[2][e]);
               const float h2 = g4[3][e] * tanh_acc(c2);
-              cc[p * 8 + e] = live ? c2 : cc[p * 8 + e];
-              hp[p * 8 + e] = live ? h2 : hp[p * 8 + e];
+              cc[p * UG + e] = live ? c2 : cc[p * UG + e];
+              hp[p * UG + e] = live ? h2 : hp[p * UG + e];
             }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __half2 h2 = __floats2half2_rn(hp[p * 8 + 2 * e], hp[p * 8 + 2 * e + 1]);
+            for (int e = 0; e < UG / 2; ++e) {
+              __half2 h2 = __floats2half2_rn(hp[p * UG + 2 * e], hp[p * UG + 2 * e + 1]);
               hw[e] = *reinterpret_cast<uint32_t*>(&h2);
             }
-            if (t + 1 < trip)
-              *reinterpret_cast<uint4*>(gslice + cm_offset(n, pu[p], b_lbo, b_sbo)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            if (t + 1 < trip) {
+              uint8_t* dst = gslice + cm_offset(n, pu[p], b_lbo, b_sbo);
+              if constexpr (UG == 8) *reinterpret_cast<uint4*>(dst) = make_uint4(hw[0], hw[1], hw[2], hw[3 % (UG / 2)]);
+              else *reinterpret_cast<uint2*>(dst) = make_uint2(hw[0], hw[1 % (UG / 2)]);
+            }
           }
         } else {
 #pragma unroll
-          for (int c16 = 0; c16 < NHALF / 16; ++c16) {
+          for (int c16 = 0; c16 < NCOL / 16; ++c16) {
             float v[16], v2[16];
             tmem_ld16(trow + c16 * 16, v);
             if (two_chains) tmem_ld16(trow + NT + c16 * 16, v2);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const int n = ch * NHALF + c16 * 16 + i;
+              const int n = ch * NCOL + c16 * 16 + i;
               v[i] += two_chains ? v2[i] : 0.f;
               const float h2 = tanh_acc(v[i] + bias);
               hp[c16 * 16 + i] = (t < s_len[n]) ? h2 : hp[c16 * 16 + i];
@@ -440,8 +459,8 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
           if (lane == 0) mbar_arrive(&dfree[j]);
           if (t + 1 < trip && rnn_u < U) {
 #pragma unroll
-            for (int i = 0; i < NHALF; ++i)
-              *reinterpret_cast<__half*>(gslice + cm_offset(ch * NHALF + i, rnn_u, b_lbo, b_sbo)) = __float2half_rn(hp[i]);
+            for (int i = 0; i < NCOL; ++i)
+              *reinterpret_cast<__half*>(gslice + cm_offset(ch * NCOL + i, rnn_u, b_lbo, b_sbo)) = __float2half_rn(hp[i]);
           }
         }
         if (tid == 0) SKB_TRACE(s, 6);
@@ -465,18 +484,20 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
             if (r < 0 || t >= s_len[n]) continue;   // frozen steps: rnn_fill_frozen_kernel
             const int unit0 = (int)q * U + pu[p];
             float* o = a.out + ((size_t)r * T + t) * H + unit0;
-            if (unit0 + 8 <= H && (H & 3) == 0) {
-              reinterpret_cast<float4*>(o)[0] = make_float4(hp[p * 8], hp[p * 8 + 1], hp[p * 8 + 2], hp[p * 8 + 3]);
-              reinterpret_cast<float4*>(o)[1] = make_float4(hp[p * 8 + 4], hp[p * 8 + 5], hp[p * 8 + 6], hp[p * 8 + 7]);
+            if (unit0 + UG <= H && (H & 3) == 0) {
+#pragma unroll
+              for (int v4 = 0; v4 < UG / 4; ++v4)
+                reinterpret_cast<float4*>(o)[v4] = make_float4(hp[p * UG + 4 * v4], hp[p * UG + 4 * v4 + 1],
+                                                               hp[p * UG + 4 * v4 + 2], hp[p * UG + 4 * v4 + 3]);
             } else {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) if (unit0 + e < H) o[e] = hp[p * 8 + e];
+              for (int e = 0; e < UG; ++e) if (unit0 + e < H) o[e] = hp[p * UG + e];
             }
           }
         } else if (rnn_valid) {
 #pragma unroll
-          for (int i = 0; i < NHALF; ++i) {
-            const int n = ch * NHALF + i, r = s_row[n];
+          for (int i = 0; i < NCOL; ++i) {
+            const int n = ch * NCOL + i, r = s_row[n];
             if (r >= 0 && t < s_len[n]) a.out[((size_t)r * T + t) * H + rnn_unit] = hp[i];
           }
         }
@@ -491,25 +512,25 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
           const int n = pn[p], r = s_row[n];
           if (r < 0) continue;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
+          for (int e = 0; e < UG; ++e) {
             const int unit = (int)q * U + pu[p] + e;
             if (unit >= H) continue;
-            a.hT[(size_t)r * H + unit] = hp[p * 8 + e];
-            if (a.cT) a.cT[(size_t)r * H + unit] = cc[p * 8 + e];
+            a.hT[(size_t)r * H + unit] = hp[p * UG + e];
+            if (a.cT) a.cT[(size_t)r * H + unit] = cc[p * UG + e];
           }
         }
       } else if (rnn_valid) {
 #pragma unroll
-        for (int i = 0; i < NHALF; ++i) {
-          const int r = s_row[ch * NHALF + i];
+        for (int i = 0; i < NCOL; ++i) {
+          const int r = s_row[ch * NCOL + i];
           if (r >= 0) a.hT[(size_t)r * H + rnn_unit] = hp[i];
         }
       }
-    } else if (warp == 8) {
+    } else if (warp == EW) {
       // ======================= x_t loader =======================
       // x_t arrives pre-converted (fp16, core-matrix image, see pack_x_kernel):
       // one bulk async copy per step, prefetched two steps ahead.
-      if (tid == 256) {
+      if (tid == kEpi) {
         const uint8_t* img = a.ximg + (size_t)tile * T * xbytes;
         for (int t = 0; t < trip; ++t) {
           const uint32_t s = step + t, j = s & 1, use = s >> 1;
@@ -521,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
           SKB_TRACE(s, 9);
         }
       }
-    } else if (warp == 9) {
+    } else if (warp == EW + 1) {
       // ======================= MMA issuer (whole warp, elected lane issues) =======================
       const uint32_t idesc = idesc_f16_f32(128, NT);
       const uint32_t x_addr = smem_u32(sX), h_addr = smem_u32(sH);
@@ -574,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) rnn_fwd_kernel(const RnnArgs a) {
   tc_fence_before();
   __syncthreads();
   cluster_sync();
-  if (warp == 9) tmem_dealloc<512>(tmem);
+  if (warp == EW + 1) tmem_dealloc<512>(tmem);
 }
 
 // ------------------------------------------------------------------ packing
@@ -839,9 +860,10 @@ constexpr int kProfMax = 256;
 cudaEvent_t g_prof_ev[2 * kProfMax];
 int g_prof_cap = 0, g_prof_n = 0;
 
-template <int CELL, typename XT>
-int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
-  auto kern = rnn_fwd_kernel<CELL, kNT, XT>;
+template <int CELL, typename XT, int EW>
+int launch_main_ew(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
+  auto kern = rnn_fwd_kernel<CELL, kNT, XT, EW>;
+  constexpr int kThreads = EW * 32 + 64;
   const size_t smem = smem_bytes<kNT>(g);
   if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -868,6 +890,11 @@ int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
   if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
   if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n++ + 1], stream);
   return skb_check_launch();
+}
+
+template <int CELL, typename XT>
+int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
+  return rnn_ew() == 8 ? launch_main_ew<CELL, XT, 8>(args, g, stream) : launch_main_ew<CELL, XT, 16>(args, g, stream);
 }
 
 }  // namespace
@@ -927,7 +954,8 @@ extern "C" int skb_rnn_plan(const skb_rnn_shape* shape, int32_t* clusters, int32
   if (!make_geom(shape, &g)) return SKB_ERR_INVALID;
   const size_t smem = smem_bytes<kNT>(g);
   if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
-  auto kern = rnn_fwd_kernel<SKB_CELL_LSTM, kNT, float>;
+  auto kern = rnn_fwd_kernel<SKB_CELL_LSTM, kNT, float, 16>;
+  const int kThreads = 16 * 32 + 64;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SKB_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
