@@ -598,6 +598,286 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
   if (warp == EW + 1) tmem_dealloc<512>(tmem);
 }
 
+// ------------------------------------------------------------------ ping-pong LSTM kernel
+// The rows of a 64-row tile form two independent 32-row recurrences (halves).
+// The MMA warp alternates halves: while half A's epilogue (warps 0-7) turns
+// its gates into h_t and exchanges it, half B's h-part MMA (N = 32) runs on
+// the tensor pipe, and vice versa — the serial MMA -> epilogue -> exchange
+// chain of one recurrence overlaps the other's.  Each half has its own TMEM
+// accumulators, mbarriers, named barriers and contiguous h exchange buffers
+// (core-matrix layout with LBO = 32*16 B); the x image is shared.
+template <typename XT>
+__global__ void __launch_bounds__(16 * 32 + 64, 1) rnn_fwd_pp_kernel(const RnnArgs a) {
+  constexpr int NT = 64, NH = NT / 2, EW = 16, kEpi = EW * 32, kThreads = kEpi + 64, UG = 4;   // NT == kNT
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint64_t xfull[2], xempty[2], hfull[2][2], mdone[2][2], dfree[2][2];
+  __shared__ uint32_t tmem_s;
+  __shared__ int s_row[NT], s_len[NT], s_tmax[NT];
+  __shared__ int s_trip;
+
+  uint8_t* smem = smem_raw;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t q = cluster_ctarank();
+  const int C = a.C, U = a.U, H = a.H, T = a.T;
+  const uint32_t xbytes = NT * a.Kx * 2, hbytes = NT * a.Kh * 2, hhalf = hbytes / 2, shalf = NH * U * 2;
+  uint8_t* sX = smem;
+  uint8_t* sH = sX + 2 * xbytes;     // [buf][half][NH x Kh] fp16, LBO = NH*16
+  float* sG = reinterpret_cast<float*>(sH + 2 * hbytes);
+  constexpr uint32_t x_lbo = NT * 16, h_lbo = NH * 16, c_sbo = 128;
+  constexpr uint32_t kWCol = 256;
+
+  if (tid == 0) {
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&xfull[j], 1);
+      mbar_init(&xempty[j], 1);
+      for (int h = 0; h < 2; ++h) {
+        mbar_init(&hfull[h][j], 1);
+        mbar_init(&mdone[h][j], 1);
+        mbar_init(&dfree[h][j], 8);
+      }
+    }
+    fence_mbar_init();
+  }
+  if (warp == EW + 1) tmem_alloc<512>(&tmem_s);
+  for (uint32_t i = tid; i < (2 * xbytes + 2 * hbytes) / 16; i += kThreads)
+    reinterpret_cast<uint4*>(sX)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_s;
+  float bias = 0.f;
+  if (warp < 4) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.wpack + ((size_t)q * 128 + tid) * a.K * 2);
+    for (int c0 = 0; c0 < a.K / 2; c0 += 8) {
+      uint32_t r[8];
+      const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src + c0));
+      const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src + c0 + 4));
+      r[0] = lo.x; r[1] = lo.y; r[2] = lo.z; r[3] = lo.w; r[4] = hi.x; r[5] = hi.y; r[6] = hi.z; r[7] = hi.w;
+      tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + kWCol + c0, r);
+    }
+    tmem_st_wait();
+  }
+  if (warp < EW) bias = a.bpack[q * 128 + (warp & 3) * 32 + lane];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  cluster_sync();
+
+  // epilogue group hw = warp >> 3 owns rows [hw*NH, hw*NH + NH); within it warp
+  // wl reads TMEM lane quarter qw = wl & 3 and columns ch*16.. of the half;
+  // in the cell phase thread gt owns row nl = gt / G4 and units pu..pu+3.
+  const int hw = warp >> 3, wl = warp & 7, qw = wl & 3, ch = wl >> 2, gt = tid & 255;
+  const int G4 = U / UG;
+  const int nl = G4 ? gt / G4 : 0, pu = G4 ? (gt % G4) * UG : 0;
+  const bool pv = warp < EW && G4 && nl < NH;
+  const int nrow = hw * NH + nl;
+  float hp[UG], cc[UG];
+  uint8_t* gscr = a.hscratch + (size_t)cluster_id_x() * 2 * hbytes;
+
+  uint32_t step = 0;
+  uint32_t hwait[2][2] = {{0u, 0u}, {0u, 0u}};
+  bool hfull_armed = false;
+  const int nclusters = (int)nclusters_x();
+  for (int tile = (int)cluster_id_x(); tile < a.ntiles; tile += nclusters) {
+    cluster_sync();
+    if (tid < NT) {
+      const int r = a.perm[tile * NT + tid];
+      int len = 0, tmax = 0;
+      if (r >= 0) {
+        tmax = max(0, min(a.pmax[r / a.Bp], T));
+        const long long L = a.lens[r];
+        len = (int)max(0LL, min(L, (long long)tmax));
+      }
+      s_row[tid] = r; s_len[tid] = len; s_tmax[tid] = tmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int m = 0;
+      for (int i = 0; i < NT; ++i) m = max(m, s_len[i]);
+      s_trip = m;
+    }
+    {  // h0 -> hbuf[step&1] (both halves)
+      uint8_t* hb = sH + (step & 1) * hbytes;
+      const int kch = a.Kh / 8;
+      for (int i = tid; i < NT * kch; i += kThreads) {
+        const int n = i / kch, kc = i - n * kch;
+        const int r = s_row[n];
+        float v[8];
+        if (r >= 0) load_x8<float>(a.h0 + (size_t)r * H, kc * 8, H, v);
+        else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = 0.f;
+        }
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __half2 h2 = __floats2half2_rn(v[2 * e], v[2 * e + 1]);
+          w[e] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        *reinterpret_cast<uint4*>(hb + (n / NH) * hhalf + cm_offset(n % NH, kc * 8, h_lbo, c_sbo)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    const int trip = s_trip;
+
+    if (warp < EW) {
+      // ======================= epilogue (half hw) =======================
+      {
+        const int r = pv ? s_row[nrow] : -1;
+        float hv[8], cv[8];
+        if (r >= 0) {
+          load_x8<float>(a.h0 + (size_t)r * H, (int)q * U + pu, H, hv);
+          load_x8<float>(a.c0 + (size_t)r * H, (int)q * U + pu, H, cv);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) hv[e] = cv[e] = 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < UG; ++e) { hp[e] = hv[e]; cc[e] = cv[e]; }
+      }
+      const float kl = (qw == 2) ? -2.8853900817779268f : -1.4426950408889634f;
+      const float kb = kl * bias;
+      const float mul = (qw == 2) ? 2.f : 1.f, add = (qw == 2) ? -1.f : 0.f;
+      const uint32_t bar_g = 1 + 2 * hw, bar_x = 2 + 2 * hw;   // named barriers of this half
+      for (int t = 0; t < trip; ++t) {
+        const uint32_t s = step + t, j = s & 1, use = s >> 1;
+        const uint32_t nb = (s + 1) & 1;
+        uint8_t* gslice = gscr + nb * hbytes + hw * hhalf + q * shalf;
+        mbar_wait(&mdone[hw][j], use & 1);
+        tc_fence_after();
+        const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16) + j * 2 * NT + hw * NH + ch * 16;
+        float* g_out = sG + (qw * NT + hw * NH + ch * 16) * kGS + lane;
+        {
+          float v[16];
+          tmem_ld16(trow, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) g_out[i * kGS] = fmaf(mul, inv1pexp2(fmaf(v[i], kl, kb)), add);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dfree[hw][j]);
+        named_bar_sync(bar_g, 256);
+        if (pv) {
+          float g4[4][UG];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const float4 x0 = *reinterpret_cast<const float4*>(sG + (g * NT + nrow) * kGS + pu);
+            g4[g][0] = x0.x; g4[g][1] = x0.y; g4[g][2] = x0.z; g4[g][3] = x0.w;
+          }
+          const bool live = t < s_len[nrow];
+#pragma unroll
+          for (int e = 0; e < UG; ++e) {
+            const float c2 = fmaf(g4[1][e], cc[e], g4[0][e] * g4[2][e]);
+            const float h2 = g4[3][e] * tanh_acc(c2);
+            cc[e] = live ? c2 : cc[e];
+            hp[e] = live ? h2 : hp[e];
+          }
+          if (t + 1 < trip) {
+            __half2 h01 = __floats2half2_rn(hp[0], hp[1]), h23 = __floats2half2_rn(hp[2], hp[3]);
+            *reinterpret_cast<uint2*>(gslice + cm_offset(nl, pu, h_lbo, c_sbo)) =
+                make_uint2(*reinterpret_cast<uint32_t*>(&h01), *reinterpret_cast<uint32_t*>(&h23));
+          }
+        }
+        fence_proxy_async_global();
+        named_bar_sync(bar_x, 256);   // also: sG rows of this half are rewritten only after every read
+        if (t + 1 < trip && gt == 0)
+          bulk_g2s_multicast(sH + nb * hbytes + hw * hhalf + q * shalf, gslice, shalf, &hfull[hw][nb],
+                             (uint16_t)((1u << C) - 1));
+        if (pv) {   // output sequence [R, T, H] (live steps; the frozen tail is filled later)
+          const int r = s_row[nrow];
+          if (r >= 0 && t < s_len[nrow]) {
+            const int unit0 = (int)q * U + pu;
+            float* o = a.out + ((size_t)r * T + t) * H + unit0;
+            if (unit0 + UG <= H && (H & 3) == 0) {
+              *reinterpret_cast<float4*>(o) = make_float4(hp[0], hp[1], hp[2], hp[3]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < UG; ++e) if (unit0 + e < H) o[e] = hp[e];
+            }
+          }
+        }
+      }
+      if (pv) {
+        const int r = s_row[nrow];
+        if (r >= 0) {
+#pragma unroll
+          for (int e = 0; e < UG; ++e) {
+            const int unit = (int)q * U + pu + e;
+            if (unit >= H) continue;
+            a.hT[(size_t)r * H + unit] = hp[e];
+            if (a.cT) a.cT[(size_t)r * H + unit] = cc[e];
+          }
+        }
+      }
+    } else if (warp == EW) {
+      // ======================= x_t loader =======================
+      if (lane == 0) {
+        const uint8_t* img = a.ximg + (size_t)tile * T * xbytes;
+        for (int t = 0; t < trip; ++t) {
+          const uint32_t s = step + t, j = s & 1, use = s >> 1;
+          mbar_wait(&xempty[j], (use & 1) ^ 1);
+          mbar_arrive_expect_tx(&xfull[j], xbytes);
+          for (uint32_t off = 0; off < xbytes; off += 16384)
+            bulk_g2s(sX + j * xbytes + off, img + (size_t)t * xbytes + off, min(16384u, xbytes - off), &xfull[j]);
+        }
+      }
+    } else {
+      // ======================= MMA issuer (both halves) =======================
+      const uint32_t idesc = idesc_f16_f32(128, NH);
+      const uint32_t x_addr = smem_u32(sX), h_addr = smem_u32(sH);
+      const int kx_steps = a.Kx / 16, kh_steps = a.Kh / 16;
+      if (!hfull_armed) {
+        if (lane == 0)
+          for (int h = 0; h < 2; ++h)
+            for (int b = 0; b < 2; ++b) mbar_arrive_expect_tx(&hfull[h][b], C * shalf);
+        hfull_armed = true;
+      }
+      for (int t = 0; t < trip; ++t) {
+        const uint32_t s = step + t, j = s & 1, use = s >> 1;
+        mbar_wait(&xfull[j], use & 1);
+        for (int h = 0; h < 2; ++h) {   // x parts (independent of the recurrence)
+          mbar_wait(&dfree[h][j], (use & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + j * 2 * NT + h * NH;
+          const uint64_t xdesc0 = sdesc_kmajor_noswz(x_addr + j * xbytes + h * (NH / 8) * c_sbo, x_lbo, c_sbo);
+#pragma unroll 4
+          for (int ks = 0; ks < kx_steps; ++ks)
+            umma_f16_ts_warp(d, tmem + kWCol + ks * 8, xdesc0 + (uint64_t)(ks * 2 * x_lbo >> 4), idesc,
+                             ks > 0 ? 1u : 0u);
+        }
+        umma_commit_warp(&xempty[j]);
+        for (int h = 0; h < 2; ++h) {   // h parts: each waits for its own half's exchange
+          if (t > 0) {
+            const uint32_t hb = s & 1;
+            mbar_wait(&hfull[h][hb], hwait[h][hb] & 1);
+            ++hwait[h][hb];
+            if (lane == 0) mbar_arrive_expect_tx(&hfull[h][hb], C * shalf);
+          }
+          tc_fence_after();
+          const uint32_t d = tmem + j * 2 * NT + h * NH;
+          const uint64_t hdesc0 = sdesc_kmajor_noswz(h_addr + (s & 1) * hbytes + h * hhalf, h_lbo, c_sbo);
+#pragma unroll 4
+          for (int ks = 0; ks < kh_steps; ++ks)
+            umma_f16_ts_warp(d, tmem + kWCol + (kx_steps + ks) * 8, hdesc0 + (uint64_t)(ks * 2 * h_lbo >> 4),
+                             idesc, 1u);
+          umma_commit_warp(&mdone[h][j]);
+        }
+      }
+    }
+    __syncwarp();
+    step += trip;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == EW + 1) tmem_dealloc<512>(tmem);
+}
+
 // ------------------------------------------------------------------ packing
 struct PackArgs {
   const void* w[4];
@@ -892,8 +1172,54 @@ int launch_main_ew(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
   return skb_check_launch();
 }
 
+// Ping-pong halves (LSTM) are opt-in (SKB_RNN_PP=1): measured slower on B200
+// (1.89 vs 1.45 ms at C1) — two N=32 MMA chains cost as many tensor-pipe issue
+// slots as two N=64 chains, so the MMA issue rate, not the epilogue, bounds a step.
+inline bool rnn_pp() {
+  static int pp = -1;
+  if (pp < 0) {
+    const char* e = getenv("SKB_RNN_PP");
+    pp = (e && atoi(e) == 1) ? 1 : 0;
+  }
+  return pp == 1;
+}
+
+template <typename XT>
+int launch_pp(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
+  auto kern = rnn_fwd_pp_kernel<XT>;
+  constexpr int kThreads = 16 * 32 + 64;
+  const size_t smem = smem_bytes<kNT>(g);
+  if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SKB_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(g.C);
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
+    return SKB_ERR_CUDA;
+  const int ncl = min(min(max_clusters, args.ntiles), max_clusters_bound(g) - 1);
+  cfg.gridDim = dim3(g.C * max(ncl, 1));
+  const bool prof = g_prof_n < g_prof_cap;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], stream);
+  if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n++ + 1], stream);
+  return skb_check_launch();
+}
+
 template <int CELL, typename XT>
 int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
+  // the ping-pong kernel needs 32-unit CTA slices (U = 32: H a multiple of 32)
+  if (CELL == SKB_CELL_LSTM && rnn_pp() && g.U == 32 && g.Kh == g.C * 32) return launch_pp<XT>(args, g, stream);
   return rnn_ew() == 8 ? launch_main_ew<CELL, XT, 8>(args, g, stream) : launch_main_ew<CELL, XT, 16>(args, g, stream);
 }
 

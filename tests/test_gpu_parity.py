@@ -158,3 +158,33 @@ def test_pipelined_host_to_host_matches_device_path(c1_graph):
     dev32 = execute_many(c1_graph, [dict(f, input_data=f["input_data"].astype(np.float32)) for f in feeds])
     for a, b in zip(host, dev32):
         assert np.array_equal(a.outputs[0].array, b.outputs[0].array)
+
+
+@pytest.mark.parametrize("variant", ["SKB_RNN_EW=8", "SKB_RNN_PP=1"])
+def test_kernel_variants_bit_identical_to_default(c1_graph, variant):
+    """The alternative C1 kernel layouts (8-warp epilogue; ping-pong halves)
+    produce results identical to the default kernel (same arithmetic per
+    element).  Each variant runs in a fresh process (selection is read once)."""
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+            "from test_gpu_parity import _c1_problems;"
+            "from oracle.fixtures import load_graph_fixture;"
+            "from paper_1810_08061_b200 import execute_many;"
+            "g, _ = load_graph_fixture('graph_lstm_c1');"
+            "r = execute_many(g, _c1_problems(6, seed=9));"
+            "np.save(sys.argv[1], np.concatenate([x.outputs[0].array.reshape(-1) for x in r]))")
+    import os
+    import tempfile
+    outs = []
+    for env in (None, variant):
+        f = tempfile.mktemp(suffix=".npy")
+        e = dict(os.environ)
+        if env:
+            k, v = env.split("=")
+            e[k] = v
+        subprocess.run([sys.executable, "-c", code, f], check=True, env=e,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        outs.append(np.load(f))
+        os.unlink(f)
+    assert np.array_equal(outs[0], outs[1])
