@@ -7,14 +7,16 @@
 // lstm_bptt.msl (forward While storing states, reverse While), executed by
 // graph/execute.py:218-238.  Here, per GPU shard of B rows (batch-major
 // x [B,T,F], y [B,T,H]):
-//   forward  t = 0..n-1:  Z_t = x_t W ; Z_t += h_{t-1} U      (TF32/FP32 cuBLAS, strided views)
+//   forward  Z = X W for every step in one GEMM (K = F, rows (b, t)), then
+//            t = 0..n-1:  Z_t += h_{t-1} U                  (cuBLAS, strided views)
 //                         lstm_fwd_cell: gates, c_t, h_t with the row mask
 //                         (rows past their length keep h, c — the Where rule)
 //   loss     inv_b * sum_{b, t<len_b} <h_{b,t}, y_{b,t}>     (deterministic block reduce)
 //   backward t = n-1..0:  lstm_bwd_cell: dG_t (in place of the gate activations),
 //                         carried dh / dc for frozen rows
-//                         dh = dG_t U^T + carry ; dW += x_t^T dG_t ; dU += h_{t-1}^T dG_t
-//   db       column sums of dG
+//                         dh = dG_t U^T + carry
+//   grads    dW = X^T dG and dU = H_prev^T dG as two GEMMs over all (b, t) (bf16 path;
+//            the fp32 path accumulates dU per step), db = column sums of dG
 // The whole step is captured once per (n, buffers) as a CUDA graph, so the
 // ~5n GEMMs and 2n cell kernels replay with a single launch.  The gradient
 // allreduce (NCCL, torch.distributed) and the fused SGD update run after it.
@@ -38,7 +40,7 @@ struct TrainBufs {
   float* dc;     // [B, H]
   double* part;  // loss partials [kLossBlocks]
   float* bpart;  // bias-gradient partials [kBiasChunks, 4H]
-  // bf16 GEMM operands (math == 2): x, h states, dG and the weights
+  // bf16 GEMM operands (math == 2): x, h_{t-1} [B, T, H], dG and the weights
   __nv_bfloat16 *Xb, *Hb, *Zb, *Wb, *Ub;
 };
 constexpr int kLossBlocks = 1184;
@@ -48,7 +50,7 @@ __global__ void init_states(const float* h0, const float* c0, TrainBufs w, int B
        i += (long long)gridDim.x * blockDim.x) {
     const int b = (int)(i / H), k = (int)(i % H);
     w.Hs[(long long)b * (T + 1) * H + k] = h0 ? h0[i] : 0.f;
-    if (w.Hb) w.Hb[(long long)b * (T + 1) * H + k] = __float2bfloat16(h0 ? h0[i] : 0.f);
+    if (w.Hb) w.Hb[(long long)b * T * H + k] = __float2bfloat16(h0 ? h0[i] : 0.f);   // h_{-1} at t = 0
     w.Cs[(long long)b * (T + 1) * H + k] = c0 ? c0[i] : 0.f;
     w.dh[i] = 0.f;
     w.dc[i] = 0.f;
@@ -57,9 +59,9 @@ __global__ void init_states(const float* h0, const float* c0, TrainBufs w, int B
 
 __global__ void lstm_fwd_cell(TrainBufs w, const float* __restrict__ bias, const int64_t* __restrict__ lens, int B,
                               int T, int H, int t) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)B * H;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int b = (int)(i / H), k = (int)(i % H);
+  const int b = blockIdx.y;   // one grid row per sequence, threads over units: no index division
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < H; k += gridDim.x * blockDim.x) {
+    const long long i = (long long)b * H + k;
     float* z = w.Z + ((long long)b * T + t) * 4 * H;
     const float ig = sigf(z[k] + bias[k]);
     const float fg = sigf(z[H + k] + bias[H + k]);
@@ -72,16 +74,16 @@ __global__ void lstm_fwd_cell(TrainBufs w, const float* __restrict__ bias, const
     const float hn = og * tanhf(cn);
     w.Cs[sp + H] = live ? cn : cp;
     w.Hs[sp + H] = live ? hn : hp;
-    if (w.Hb) w.Hb[sp + H] = __float2bfloat16(live ? hn : hp);
+    if (w.Hb && t + 1 < T) w.Hb[((long long)b * T + t + 1) * H + k] = __float2bfloat16(live ? hn : hp);
     z[k] = ig; z[H + k] = fg; z[2 * H + k] = gg; z[3 * H + k] = og;
   }
 }
 
 __global__ void lstm_bwd_cell(TrainBufs w, const float* __restrict__ y, const int64_t* __restrict__ lens, float inv_b,
                               int B, int T, int H, int t) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)B * H;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int b = (int)(i / H), k = (int)(i % H);
+  const int b = blockIdx.y;   // one grid row per sequence, threads over units: no index division
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < H; k += gridDim.x * blockDim.x) {
+    const long long i = (long long)b * H + k;
     const bool live = t < lens[b];
     float* z = w.Z + ((long long)b * T + t) * 4 * H;
     float dh = w.dh[i] + (live ? y[((long long)b * T + t) * H + k] * inv_b : 0.f);
@@ -163,6 +165,19 @@ __global__ void bias_grad_final(const float* __restrict__ part, float* __restric
   db[col] = s;
 }
 
+// rows t >= n of every sequence take no part in the step: zero their Z / dG so
+// the whole-sequence gradient GEMMs (K = B*T) see exact zeros there
+__global__ void zero_tail(TrainBufs w, int B, int T, int H, int n) {
+  const long long G = 4ll * H, per = (long long)(T - n) * G;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)B * per;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / per, r = i % per;
+    const long long off = (b * T + n) * G + r;
+    w.Z[off] = 0.f;
+    if (w.Zb) w.Zb[off] = __float2bfloat16(0.f);
+  }
+}
+
 __global__ void sgd_update(float* __restrict__ p, const float* __restrict__ g, long long n, float lr) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] -= lr * g[i];
@@ -207,7 +222,7 @@ void layout(int B, int T, int F, int H, bool bf16, uint8_t* base, TrainBufs* w, 
   s.bpart = (float*)take(4ull * kBiasChunks * 4 * H);
   if (bf16) {
     s.Xb = (__nv_bfloat16*)take(2ull * B * T * F);
-    s.Hb = (__nv_bfloat16*)take(2ull * B * (T + 1) * H);
+    s.Hb = (__nv_bfloat16*)take(2ull * B * T * H);   // h_{t-1} of step t (GEMM operand)
     s.Zb = (__nv_bfloat16*)take(2ull * B * T * 4 * H);
     s.Wb = (__nv_bfloat16*)take(2ull * F * 4 * H);
     s.Ub = (__nv_bfloat16*)take(2ull * H * 4 * H);
@@ -238,37 +253,41 @@ bool enqueue(cublasHandle_t hb, cudaStream_t cs, const skb_train_shape& d, Train
     to_bf16<<<blocks, 256, 0, cs>>>(W, w.Wb, (long long)F * G);
     to_bf16<<<blocks, 256, 0, cs>>>(U, w.Ub, (long long)H * G);
   }
-  for (int t = 0; t < n; ++t) {
+  // input projection of every step at once: Z = X W (rows (b, t), K = F)
+  if (bf) {
+    if (!gemm_bf(hb, false, false, w.Xb, F, w.Wb, G, w.Z, G, B * T, G, F, 0.f)) return false;
+  } else if (!gemm_rm(hb, d.math, false, false, x, F, W, G, w.Z, G, B * T, G, F, 0.f)) {
+    return false;
+  }
+  for (int t = 0; t < n; ++t) {   // the recurrence: Z_t += h_{t-1} U, then the cell
     float* Zt = w.Z + (size_t)t * G;
     if (bf) {
-      if (!gemm_bf(hb, false, false, w.Xb + (size_t)t * F, T * F, w.Wb, G, Zt, T * G, B, G, F, 0.f)) return false;
-      if (!gemm_bf(hb, false, false, w.Hb + (size_t)t * H, (T + 1) * H, w.Ub, G, Zt, T * G, B, G, H, 1.f))
-        return false;
-    } else {
-      if (!gemm_rm(hb, d.math, false, false, x + (size_t)t * F, T * F, W, G, Zt, T * G, B, G, F, 0.f)) return false;
-      if (!gemm_rm(hb, d.math, false, false, w.Hs + (size_t)t * H, (T + 1) * H, U, G, Zt, T * G, B, G, H, 1.f))
-        return false;
+      if (!gemm_bf(hb, false, false, w.Hb + (size_t)t * H, T * H, w.Ub, G, Zt, T * G, B, G, H, 1.f)) return false;
+    } else if (!gemm_rm(hb, d.math, false, false, w.Hs + (size_t)t * H, (T + 1) * H, U, G, Zt, T * G, B, G, H, 1.f)) {
+      return false;
     }
-    lstm_fwd_cell<<<blocks, 256, 0, cs>>>(w, bias, lens, B, T, H, t);
+    lstm_fwd_cell<<<dim3((H + 255) / 256, B), 256, 0, cs>>>(w, bias, lens, B, T, H, t);
   }
   loss_partials<<<kLossBlocks, 256, 0, cs>>>(w, y, lens, inv_b, B, T, H, n);
   loss_final<<<1, 32, 0, cs>>>(w.part, kLossBlocks, loss);
-  for (int t = n - 1; t >= 0; --t) {
+  for (int t = n - 1; t >= 0; --t) {   // BPTT: only dh_{t-1} = dG_t U^T + carry stays per step
     float* Zt = w.Z + (size_t)t * G;
-    lstm_bwd_cell<<<blocks, 256, 0, cs>>>(w, y, lens, inv_b, B, T, H, t);
-    // dh_{t-1} = dG_t U^T + carry ; dW += x_t^T dG_t ; dU += h_{t-1}^T dG_t
+    lstm_bwd_cell<<<dim3((H + 255) / 256, B), 256, 0, cs>>>(w, y, lens, inv_b, B, T, H, t);
     if (bf) {
-      const __nv_bfloat16* Zb = w.Zb + (size_t)t * G;
-      if (!gemm_bf(hb, false, true, Zb, T * G, w.Ub, G, w.dh, H, B, H, G, 1.f)) return false;
-      if (!gemm_bf(hb, true, false, w.Xb + (size_t)t * F, T * F, Zb, T * G, dW, G, F, G, B, 1.f)) return false;
-      if (!gemm_bf(hb, true, false, w.Hb + (size_t)t * H, (T + 1) * H, Zb, T * G, dU, G, H, G, B, 1.f))
-        return false;
+      if (!gemm_bf(hb, false, true, w.Zb + (size_t)t * G, T * G, w.Ub, G, w.dh, H, B, H, G, 1.f)) return false;
     } else {
       if (!gemm_rm(hb, d.math, false, true, Zt, T * G, U, G, w.dh, H, B, H, G, 1.f)) return false;
-      if (!gemm_rm(hb, d.math, true, false, x + (size_t)t * F, T * F, Zt, T * G, dW, G, F, G, B, 1.f)) return false;
       if (!gemm_rm(hb, d.math, true, false, w.Hs + (size_t)t * H, (T + 1) * H, Zt, T * G, dU, G, H, G, B, 1.f))
         return false;
     }
+  }
+  if (n < T) zero_tail<<<blocks, 256, 0, cs>>>(w, B, T, H, n);
+  // weight gradients over every (b, t) at once (K = B*T): dW = X^T dG, dU = H_prev^T dG
+  if (bf) {
+    if (!gemm_bf(hb, true, false, w.Xb, F, w.Zb, G, dW, G, F, G, B * T, 0.f)) return false;
+    if (!gemm_bf(hb, true, false, w.Hb, H, w.Zb, G, dU, G, H, G, B * T, 0.f)) return false;
+  } else if (!gemm_rm(hb, d.math, true, false, x, F, w.Z, G, dW, G, F, G, B * T, 0.f)) {
+    return false;
   }
   bias_grad_partial<<<dim3((G + 255) / 256, kBiasChunks), 256, 0, cs>>>(w, w.bpart, B, T, H, n);
   bias_grad_final<<<(G + 255) / 256, 256, 0, cs>>>(w.bpart, db, G);
