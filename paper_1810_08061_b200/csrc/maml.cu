@@ -18,15 +18,26 @@
 
 namespace {
 
-constexpr int HMAX = 64, KMAXT = 32, TPB = 128;
+constexpr int HMAX = 64, KMAXT = 32, TPB = 256;
 
-struct Theta {        // views into a flat parameter block: w1 | b1 | w2 | b2 | w3 | b3
+// Shared-memory parameter block: w1 | b1 | w2 (H rows of stride LD = H + 1, so
+// column walks are bank-conflict free) | b2 | w3 | b3.  Global memory holds the
+// flat, unpadded layout (P = H*H + 4H + 1).
+struct Theta {
   float *w1, *b1, *w2, *b2, *w3, *b3;
+  int ld;
 };
 __device__ __forceinline__ Theta view(float* p, int H) {
   Theta t;
-  t.w1 = p; t.b1 = p + H; t.w2 = p + 2 * H; t.b2 = t.w2 + H * H; t.w3 = t.b2 + H; t.b3 = t.w3 + H;
+  t.ld = H + 1;
+  t.w1 = p; t.b1 = p + H; t.w2 = p + 2 * H; t.b2 = t.w2 + H * t.ld; t.w3 = t.b2 + H; t.b3 = t.w3 + H;
   return t;
+}
+__device__ __forceinline__ int padded_of(int i, int H) {   // flat index -> padded index
+  const int w2o = 2 * H, w2e = 2 * H + H * H;
+  if (i < w2o) return i;
+  if (i < w2e) { const int r = (i - w2o) / H, c = (i - w2o) % H; return w2o + r * (H + 1) + c; }
+  return i + H;
 }
 
 // y[K,H] = relu-input z = x w1 + b1 (x: [K], w1: [H])
@@ -43,7 +54,7 @@ __device__ void layer2(const float* a1, const float* w2, const float* b2, float*
   for (int i = threadIdx.x; i < K * H; i += TPB) {
     const int k = i / H, j = i % H;
     float s = 0.f;
-    for (int q = 0; q < H; ++q) s += a1[k * H + q] * w2[q * H + j];
+    for (int q = 0; q < H; ++q) s += a1[k * H + q] * w2[q * (H + 1) + j];
     s += b2[j];
     z2[i] = s;
     if (a2) a2[i] = s > 0.f ? s : 0.f;
@@ -81,7 +92,7 @@ __device__ void backward(const float* x, Theta th, const float* z1, const float*
     const int q = i / H, j = i % H;
     float s = 0.f;
     for (int k = 0; k < K; ++k) s += a1[k * H + q] * dz2[k * H + j];
-    g.w2[i] = s;
+    g.w2[q * g.ld + j] = s;
   }
   for (int j = threadIdx.x; j < H; j += TPB) {
     float s = 0.f;
@@ -91,7 +102,7 @@ __device__ void backward(const float* x, Theta th, const float* z1, const float*
   for (int i = threadIdx.x; i < K * H; i += TPB) {  // dz1 = (dz2 w2^T) * [z1 > 0]
     const int k = i / H, q = i % H;
     float s = 0.f;
-    for (int j = 0; j < H; ++j) s += dz2[k * H + j] * th.w2[q * H + j];
+    for (int j = 0; j < H; ++j) s += dz2[k * H + j] * th.w2[q * th.ld + j];
     dz1[i] = z1[i] > 0.f ? s : 0.f;
   }
   __syncthreads();
@@ -112,17 +123,20 @@ __global__ void __launch_bounds__(TPB) maml_task_kernel(int H, int K, int P, con
   extern __shared__ float sm[];
   const int task = blockIdx.x;
   const int KH = K * H;
-  float* th_p = sm;              // P
-  float* th2_p = th_p + P;       // P  adapted weights
-  float* gs_p = th2_p + P;       // P  support gradient, then reused for H_s v
-  float* gq_p = gs_p + P;        // P  query gradient (= v)
-  float* z1 = gq_p + P; float* a1 = z1 + KH; float* z2 = a1 + KH; float* a2 = z2 + KH;
+  const int PP = P + H;          // padded block (w2 rows of H + 1)
+  float* th_p = sm;              // PP
+  float* th2_p = th_p + PP;      // PP adapted weights
+  float* gs_p = th2_p + PP;      // PP support gradient, then reused for H_s v
+  float* gq_p = gs_p + PP;       // PP query gradient (= v)
+  float* z1 = gq_p + PP; float* a1 = z1 + KH; float* z2 = a1 + KH; float* a2 = z2 + KH;
   float* dz1 = a2 + KH; float* dz2 = dz1 + KH;
   float* q1 = dz2 + KH; float* qa1 = q1 + KH; float* q2 = qa1 + KH; float* qa2 = q2 + KH;
   float* r1 = qa2 + KH; float* r2 = r1 + KH; float* rd2 = r2 + KH; float* rd1 = rd2 + KH;
   float* x = rd1 + KH; float* y = x + KMAXT; float* xqs = y + KMAXT; float* yqs = xqs + KMAXT;
   float* p = yqs + KMAXT; float* dp = p + KMAXT; float* rp = dp + KMAXT; float* rdp = rp + KMAXT;
-  for (int i = threadIdx.x; i < P; i += TPB) th_p[i] = theta_g[i];
+  for (int i = threadIdx.x; i < PP; i += TPB) th_p[i] = 0.f;
+  __syncthreads();
+  for (int i = threadIdx.x; i < P; i += TPB) th_p[padded_of(i, H)] = theta_g[i];
   for (int k = threadIdx.x; k < K; k += TPB) {
     x[k] = xs[(long long)task * K + k]; y[k] = ys[(long long)task * K + k];
     xqs[k] = xq[(long long)task * K + k]; yqs[k] = yq[(long long)task * K + k];
@@ -140,7 +154,7 @@ __global__ void __launch_bounds__(TPB) maml_task_kernel(int H, int K, int P, con
   for (int k = threadIdx.x; k < K; k += TPB) dp[k] = (p[k] - y[k]) * (2.f * inv_k);
   __syncthreads();
   backward(x, th, z1, a1, z2, a2, dp, dz1, dz2, gs, K, H);
-  for (int i = threadIdx.x; i < P; i += TPB) th2_p[i] = th_p[i] - alpha * gs_p[i];
+  for (int i = threadIdx.x; i < PP; i += TPB) th2_p[i] = th_p[i] - alpha * gs_p[i];
   __syncthreads();
   // query pass at theta'
   layer1(xqs, th2.w1, th2.b1, q1, qa1, K, H);
@@ -168,7 +182,7 @@ __global__ void __launch_bounds__(TPB) maml_task_kernel(int H, int K, int P, con
   for (int i = threadIdx.x; i < KH; i += TPB) {      // R{a2} = (R{a1} w2 + a1 v_w2 + v_b2) [z2>0]
     const int k = i / H, j = i % H;
     float s = v.b2[j];
-    for (int q = 0; q < H; ++q) s += r1[k * H + q] * th.w2[q * H + j] + a1[k * H + q] * v.w2[q * H + j];
+    for (int q = 0; q < H; ++q) s += r1[k * H + q] * th.w2[q * th.ld + j] + a1[k * H + q] * v.w2[q * v.ld + j];
     r2[i] = z2[i] > 0.f ? s : 0.f;
   }
   __syncthreads();
@@ -198,7 +212,7 @@ __global__ void __launch_bounds__(TPB) maml_task_kernel(int H, int K, int P, con
     const int q = i / H, j = i % H;
     float s = 0.f;
     for (int k = 0; k < K; ++k) s += r1[k * H + q] * dz2[k * H + j] + a1[k * H + q] * rd2[k * H + j];
-    gs.w2[i] = s;
+    gs.w2[q * gs.ld + j] = s;
   }
   for (int j = threadIdx.x; j < H; j += TPB) {
     float s = 0.f;
@@ -208,7 +222,7 @@ __global__ void __launch_bounds__(TPB) maml_task_kernel(int H, int K, int P, con
   for (int i = threadIdx.x; i < KH; i += TPB) {      // R{dz1} = (R{dz2} w2^T + dz2 v_w2^T) [z1>0]
     const int k = i / H, q = i % H;
     float s = 0.f;
-    for (int j = 0; j < H; ++j) s += rd2[k * H + j] * th.w2[q * H + j] + dz2[k * H + j] * v.w2[q * H + j];
+    for (int j = 0; j < H; ++j) s += rd2[k * H + j] * th.w2[q * th.ld + j] + dz2[k * H + j] * v.w2[q * v.ld + j];
     rd1[i] = z1[i] > 0.f ? s : 0.f;
   }
   __syncthreads();
@@ -220,7 +234,10 @@ __global__ void __launch_bounds__(TPB) maml_task_kernel(int H, int K, int P, con
   }
   __syncthreads();
   float* out = task_grad + (long long)task * P;
-  for (int i = threadIdx.x; i < P; i += TPB) out[i] = gq_p[i] - alpha * gs_p[i];
+  for (int i = threadIdx.x; i < P; i += TPB) {
+    const int pi = padded_of(i, H);
+    out[i] = gq_p[pi] - alpha * gs_p[pi];
+  }
 }
 
 // mean over tasks in a fixed order (deterministic): stage 1 sums a chunk of
@@ -251,7 +268,7 @@ __global__ void maml_reduce_final(const double* __restrict__ part, int n, int P,
 
 size_t smem_for(int H, int K) {
   const int P = H * H + 4 * H + 1;
-  return sizeof(float) * (4 * (size_t)P + 14 * (size_t)K * H + 8 * KMAXT);
+  return sizeof(float) * (4 * (size_t)(P + H) + 14 * (size_t)K * H + 8 * KMAXT);
 }
 
 }  // namespace
