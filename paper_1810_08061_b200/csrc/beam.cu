@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(ROW_THREADS) beam_rows(DecodeState st, int V, 
   const int V4 = (V % 4 == 0) ? V / 4 : 0;   // rows are 16-byte aligned when V % 4 == 0
   const float4* L4 = reinterpret_cast<const float4*>(L);
   const float4* B4 = reinterpret_cast<const float4*>(b_out);
-  constexpr int U = 4;   // float4 loads in flight per thread before any is consumed
+  constexpr int U = 8;   // float4 loads in flight per thread before any is consumed
   const int warp_base = warp * 32 + lane;   // warps own interleaved float4 columns
   int q0 = warp_base;
   // every lane runs the same trip count (ballots need the whole warp);
