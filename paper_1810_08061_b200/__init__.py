@@ -6,7 +6,8 @@ Public API (drop-in for the reference CPU executor, graph/execute.py:27):
     from paper_1810_08061_b200 import execute
     result = execute(graph, feeds)          # ExecutionResult(outputs, print_log)
 
-plus ``execute_many`` (many feed sets, one launch), the IR mirror and its
+plus ``gradient`` (reverse mode through While/Cond/FuncCall, autodiff.py),
+``execute_many`` (many feed sets, one launch), the IR mirror and its
 JSON wire format (``ir``), and the error classes (``errors``).
 """
 
@@ -14,13 +15,14 @@ from .errors import (BackendUnavailable, DeviceError, IterationLimitExceeded, Lo
                      RuntimeGraphError, SkbError, ValidationError)
 from .executor import (ExecutionResult, PrecisionRangeError, RnnExecutable, bind_feeds, execute,
                        execute_many, lower)
+from .autodiff import NotDifferentiable, gradient
 from .values import DeviceTensor, TensorValue, allclose, max_rel_error
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BackendUnavailable", "DeviceError", "DeviceTensor", "ExecutionResult", "IterationLimitExceeded",
-    "LoweringError", "PrecisionRangeError", "RnnExecutable", "RuntimeGraphError", "SkbError",
-    "TensorValue", "ValidationError", "allclose", "bind_feeds", "execute", "execute_many", "lower",
+    "LoweringError", "NotDifferentiable", "PrecisionRangeError", "RnnExecutable", "RuntimeGraphError", "SkbError",
+    "TensorValue", "ValidationError", "allclose", "bind_feeds", "execute", "execute_many", "gradient", "lower",
     "max_rel_error",
 ]
