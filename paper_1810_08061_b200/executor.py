@@ -15,6 +15,7 @@ in libskb kernels; PyTorch only allocates device memory and moves bytes.
 
 from __future__ import annotations
 
+import os
 import threading
 import weakref
 from dataclasses import dataclass, field
@@ -404,27 +405,28 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
         validate(graph)
     prog = lower(graph)
     memo = {}
-    bound = [bind_feeds(graph, f or {}, memo) for f in feeds_list]
-    P = len(bound)
+    P = len(feeds_list)
     if P == 0:
         return []
-    f0 = bound[0]
-    xs = [_source_value(prog.x, b) for b in bound]
-    xshape = shape_of(xs[0])
+    f0 = bind_feeds(graph, feeds_list[0] or {}, memo)
+    xshape = shape_of(_source_value(prog.x, f0))
     if len(xshape) != 3:
         raise RuntimeGraphError(f"x must be rank 3, got {list(xshape)}", prog.x.node.origin if prog.x.node else None,
                                 E.SHAPE_MISMATCH)
     Bsz, T, F = xshape
-    for x in xs[1:]:
-        if shape_of(x) != xshape:
-            raise LoweringError("execute_many needs feed sets of one shape")
     weights = [tuple(_source_value(s, f0) for s in trip) for trip in prog.gates]
-    for b in bound[1:]:
+
+    def bind(feeds):
+        """bind_feeds plus the execute_many contract: one x shape, one shared weight set"""
+        b = bind_feeds(graph, feeds or {}, memo)
+        if shape_of(_source_value(prog.x, b)) != xshape:
+            raise LoweringError("execute_many needs feed sets of one shape")
         for trip_src, trip in zip(prog.gates, weights):
-            for s, w in zip(trip_src, trip):
-                v = _source_value(s, b)
+            for s_, w in zip(trip_src, trip):
+                v = _source_value(s_, b)
                 if v is not w and not np.array_equal(as_numpy(v), as_numpy(w)):
                     raise LoweringError("execute_many needs one weight set shared by all feed sets")
+        return b
     H = shape_of(weights[0][1])[0]
     if Bsz == 0:
         err = RuntimeGraphError("reduce_max of empty tensor", prog.reduce_node.origin, E.SHAPE_MISMATCH)
@@ -432,7 +434,6 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
             return [err] * P
         raise err
     device = torch.device("cuda", torch.cuda.current_device())
-    exe = _executable(prog, weights, Bsz, T, F, H, P, device, stream)
     R = Bsz * P
 
     NPD = {torch.float32: np.float32, torch.float64: np.float64, torch.int64: np.int64}
@@ -464,14 +465,17 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
             off += n
         return staging.to(device, non_blocking=True)
 
-    x32 = (isinstance(xs[0], torch.Tensor) and xs[0].dtype == torch.float32) or \
-          (isinstance(xs[0], np.ndarray) and xs[0].dtype == np.float32)
+    x0 = _source_value(prog.x, f0)
+    x32 = (isinstance(x0, torch.Tensor) and x0.dtype == torch.float32) or \
+          (isinstance(x0, np.ndarray) and x0.dtype == np.float32)
     x_dtype = torch.float32 if x32 else torch.float64
-    if host_outputs is not False and host_outputs is not None and T > 0 and P >= 2 * PIPELINE_CHUNKS and \
-            _all_pinned(prog, bound):
-        out_host, hT_h, cT_h, max_len, status = _run_pipelined(prog, weights, bound, Bsz, T, F, H, P, device, x_dtype,
-                                                              host_outputs, stream)
+    if host_outputs is not False and host_outputs is not None and T > 0 and P >= 4 and _all_pinned(prog, [f0]):
+        # feed sets are bound chunk by chunk inside the pipeline, overlapping the copies
+        out_host, hT_h, cT_h, max_len, status = _run_pipelined(prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P,
+                                                              device, x_dtype, host_outputs, stream)
         return _assemble(prog, out_host, hT_h, cT_h, max_len, status, Bsz, T, P, return_exceptions)
+    bound = [f0] + [bind(f) for f in feeds_list[1:]]
+    exe = _executable(prog, weights, Bsz, T, F, H, P, device, stream)
     x = cat(prog.x, x_dtype)
     h0 = cat(prog.h0, torch.float32).reshape(R, H)
     c0 = cat(prog.c0, torch.float32).reshape(R, H) if prog.cell == CELL_LSTM else None
@@ -501,7 +505,7 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
     return _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions)
 
 
-PIPELINE_CHUNKS = 4
+PIPELINE_CHUNKS = int(os.environ.get("SKB_PIPELINE_CHUNKS", "16"))   # copy/compute pipeline depth
 
 
 def _all_pinned(prog, bound) -> bool:
@@ -532,14 +536,30 @@ def _adjacent_run(vals, shape):
         return None
 
 
-def _run_pipelined(prog, weights, bound, Bsz, T, F, H, P, device, x_dtype, host_outputs, stream):
+def _run_pipelined(prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device, x_dtype, host_outputs, stream):
     """Host-to-host execute_many in PIPELINE_CHUNKS chunks of problems on three
     streams: the H2D copy of chunk k+1, the kernels of chunk k and the D2H of
-    chunk k-1 overlap (PCIe full duplex), instead of copy-in, run, copy-out."""
+    chunk k-1 overlap (PCIe full duplex), instead of copy-in, run, copy-out.
+    Each chunk's feed sets are bound (checked) just before its copies are
+    queued, so host-side checking overlaps the transfers of earlier chunks."""
     torch = _torch()
     R = Bsz * P
     comp = stream or torch.cuda.current_stream()
-    s_in, s_out = torch.cuda.Stream(device=device), torch.cuda.Stream(device=device)
+    lstm = prog.cell == CELL_LSTM
+    key = (str(device), R, T, F, H, x_dtype, lstm, threading.get_ident())
+    bufs = _pipe_bufs.get(key)
+    if bufs is None:   # device buffers and copy streams reused across calls (the call drains them before returning)
+        if len(_pipe_bufs) > 4:
+            _pipe_bufs.clear()
+        bufs = {"x": torch.empty((R, T, F), dtype=x_dtype, device=device),
+                "h0": torch.empty((R, H), dtype=torch.float32, device=device),
+                "c0": torch.empty((R, H), dtype=torch.float32, device=device) if lstm else None,
+                "lens": torch.empty((R,), dtype=torch.int64, device=device),
+                "out": torch.empty((R, T, H), dtype=torch.float32, device=device),
+                "s_in": torch.cuda.Stream(device=device), "s_out": torch.cuda.Stream(device=device)}
+        _pipe_bufs[key] = bufs
+    s_in, s_out = bufs["s_in"], bufs["s_out"]
+    s_in.wait_stream(comp)   # earlier work on the caller's stream may still read the reused buffers
     if isinstance(host_outputs, torch.Tensor):
         host_out = host_outputs.view(R, T, H)
     else:
@@ -549,32 +569,34 @@ def _run_pipelined(prog, weights, bound, Bsz, T, F, H, P, device, x_dtype, host_
     cT = torch.empty((R, H), dtype=torch.float32, device=device) if "c_final" in want else None
     max_len = torch.zeros(P, dtype=torch.int32, device=device)
     status = torch.zeros(4, dtype=torch.int32, device=device)
-    step = -(-P // PIPELINE_CHUNKS)
-    keep = []
+    step = -(-P // max(2, min(PIPELINE_CHUNKS, P // 2)))
     for p0 in range(0, P, step):
         p1 = min(P, p0 + step)
         pc = p1 - p0
         exe = _executable(prog, weights, Bsz, T, F, H, pc, device, comp)
         rows = slice(p0 * Bsz, p1 * Bsz)
+        chunk = [f0 if p == 0 else bind(feeds_list[p]) for p in range(p0, p1)]
 
-        def stack(src, dtype, shape):
-            dev = torch.empty((pc * Bsz,) + shape, dtype=dtype, device=device)
-            vals = [_source_value(src, b) for b in bound[p0:p1]]
+        def stack(src, dtype, shape, buf):
+            dev = buf[rows]
+            vals = [_source_value(src, b) for b in chunk]
             run = _adjacent_run(vals, (pc * Bsz,) + shape)
             if run is not None:   # the chunk's feeds are one contiguous host range: one DMA
                 dev.copy_(run, non_blocking=True)
                 return dev
             for i, v in enumerate(vals):
+                if not isinstance(v, torch.Tensor):
+                    v = torch.as_tensor(as_numpy(v)).to(dtype)
                 dev[i * Bsz:(i + 1) * Bsz].copy_(v.reshape((Bsz,) + shape), non_blocking=True)
             return dev
         with torch.cuda.stream(s_in):
-            x = stack(prog.x, x_dtype, (T, F))
-            h0 = stack(prog.h0, torch.float32, (H,))
-            c0 = stack(prog.c0, torch.float32, (H,)) if prog.cell == CELL_LSTM else None
-            lens = stack(prog.lens, torch.int64, ())
+            x = stack(prog.x, x_dtype, (T, F), bufs["x"])
+            h0 = stack(prog.h0, torch.float32, (H,), bufs["h0"])
+            c0 = stack(prog.c0, torch.float32, (H,), bufs["c0"]) if lstm else None
+            lens = stack(prog.lens, torch.int64, (), bufs["lens"])
             ev_in = torch.cuda.Event()
             ev_in.record(s_in)
-        out = torch.empty((pc * Bsz, T, H), dtype=torch.float32, device=device)
+        out = bufs["out"][rows]
         comp.wait_event(ev_in)
         with torch.cuda.stream(comp):
             exe.run(x, h0, c0, lens, out, hT[rows] if hT is not None else None,
@@ -586,11 +608,6 @@ def _run_pipelined(prog, weights, bound, Bsz, T, F, H, P, device, x_dtype, host_
         s_out.wait_event(ev_out)
         with torch.cuda.stream(s_out):
             host_out[rows].copy_(out, non_blocking=True)
-        for t_ in (x, h0, c0, lens, out):   # keep device buffers alive until the streams drain
-            if t_ is not None:
-                t_.record_stream(s_out)
-                t_.record_stream(comp)
-        keep.append((x, h0, c0, lens, out))
     s_out.synchronize()
     comp.synchronize()
     return (host_out, hT.to("cpu") if hT is not None else None, cT.to("cpu") if cT is not None else None,
@@ -625,6 +642,7 @@ def _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions):
 
 
 _pinned_pool: dict = {}
+_pipe_bufs: dict = {}
 
 
 def _pinned(tag, shape, dtype):
