@@ -13,7 +13,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libskb.so")
+LIB = os.environ.get("SKB_BUILD_OUT") or os.path.join(HERE, "libskb.so")   # override: A/B or trace builds
 REPO = os.path.dirname(HERE)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -39,7 +39,8 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build", os.path.basename(LIB)[:-3]) if os.environ.get("SKB_BUILD_OUT") \
+        else os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in sources():

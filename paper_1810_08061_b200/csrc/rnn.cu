@@ -47,6 +47,18 @@ inline int rnn_ew() {
   }
   return ew;
 }
+// LSTM gate activations: 1 (default) = tanh.approx, one MUFU op per gate (the
+// epilogue's MUFU/FMA work is on the recurrence's critical path; C1 step -18%,
+// accuracy vs the f64 oracle unchanged within the fp16-operand error, see
+// tools/c1_err.py); SKB_RNN_ACT=0 = ex2 + Newton reciprocal (rel. err ~1e-7).
+inline int rnn_act() {
+  static int act = -1;
+  if (act < 0) {
+    const char* e = getenv("SKB_RNN_ACT");
+    act = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return act;
+}
 constexpr int kMaxClusterDim = 8;
 constexpr int kGS = 36;   // sG row stride (floats): 32 units + 4 pad, conflict-free LDS.128
 
@@ -158,6 +170,11 @@ SKB_DEV float inv1pexp2(float a) { return rcp_nr(1.f + fminf(ex2_approx(a), 1e30
 // 1/(1 + e^{k x}) (kept for the RNN path)
 SKB_DEV float inv1pexp(float kx) { return inv1pexp2(kx * 1.4426950408889634f); }
 
+SKB_DEV float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 SKB_DEV float tanh_acc(float x) {
   // 1 - 2/(1+e^{2x}): saturates correctly at both ends, |err| ~ 1e-7.
   return fmaf(-2.f, inv1pexp2(x * 2.8853900817779268f), 1.f);
@@ -194,7 +211,30 @@ SKB_DEV void load_x8<double>(const double* __restrict__ p, int k0, int F, float 
   }
 }
 
-template <int CELL, int NT, typename XT, int EW>
+// LSTM gate activations.  ACT 0: act = mul / (1 + 2^(kl*z + kb)) + add with ex2 and a
+// Newton reciprocal (tanh(x) = 2 sigmoid(2x) - 1 for the g gate).  ACT 1: one MUFU
+// op per gate, act = mul * tanh(kl*z + kb) + add (sigmoid(y) = 0.5 tanh(y/2) + 0.5).
+template <int ACT>
+SKB_DEV void gate_consts(int gate, float bias, float& kl, float& kb, float& mul, float& add) {
+  if (ACT) {
+    kl = (gate == 2) ? 1.f : 0.5f;
+    mul = kl;
+    add = (gate == 2) ? 0.f : 0.5f;
+  } else {
+    kl = (gate == 2) ? -2.8853900817779268f : -1.4426950408889634f;
+    mul = (gate == 2) ? 2.f : 1.f;
+    add = (gate == 2) ? -1.f : 0.f;
+  }
+  kb = kl * bias;
+}
+template <int ACT>
+SKB_DEV float gate_act(float z, float kl, float kb, float mul, float add) {
+  return ACT ? fmaf(mul, tanh_approx(fmaf(z, kl, kb)), add) : fmaf(mul, inv1pexp2(fmaf(z, kl, kb)), add);
+}
+template <int ACT>
+SKB_DEV float cell_tanh(float c) { return ACT ? tanh_approx(c) : tanh_acc(c); }
+
+template <int CELL, int NT, typename XT, int EW, int ACT = 0>
 __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs a) {
   // EW epilogue warps (8 or 16), then the x loader warp and the MMA warp.
   constexpr int kEpi = EW * 32, kThreads = kEpi + 64;
@@ -383,9 +423,8 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
         if constexpr (CELL == SKB_CELL_LSTM) {
           // gate g = warp (warp-uniform): sigmoid for i, f, o; tanh(x) = 2*sigmoid(2x)-1 for g.
           // act = mul / (1 + 2^(kl*z + kb)) + add, z = pre-activation without bias
-          const float kl = (qw == 2) ? -2.8853900817779268f : -1.4426950408889634f;
-          const float kb = kl * bias;
-          const float mul = (qw == 2) ? 2.f : 1.f, add = (qw == 2) ? -1.f : 0.f;
+          float kl, kb, mul, add;
+          gate_consts<ACT>(qw, bias, kl, kb, mul, add);
           float* g_out = sG + (qw * NT + ch * NCOL) * kGS + lane;
 #pragma unroll
           for (int c16 = 0; c16 < NCOL / 16; ++c16) {
@@ -397,7 +436,7 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
             for (int i = 0; i < 16; ++i) v[i] += two_chains ? v2[i] : 0.f;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              g_out[(c16 * 16 + i) * kGS] = fmaf(mul, inv1pexp2(fmaf(v[i], kl, kb)), add);
+              g_out[(c16 * 16 + i) * kGS] = gate_act<ACT>(v[i], kl, kb, mul, add);
             }
           }
           tc_fence_before();
@@ -424,7 +463,7 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
 #pragma unroll
             for (int e = 0; e < UG; ++e) {
               const float c2 = fmaf(g4[1][e], cc[p * UG + e], g4[0][e] * g4[2][e]);
-              const float h2 = g4[3][e] * tanh_acc(c2);
+              const float h2 = g4[3][e] * cell_tanh<ACT>(c2);
               cc[p * UG + e] = live ? c2 : cc[p * UG + e];
               hp[p * UG + e] = live ? h2 : hp[p * UG + e];
             }
@@ -606,7 +645,7 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
 // chain of one recurrence overlaps the other's.  Each half has its own TMEM
 // accumulators, mbarriers, named barriers and contiguous h exchange buffers
 // (core-matrix layout with LBO = 32*16 B); the x image is shared.
-template <typename XT>
+template <typename XT, int ACT = 0>
 __global__ void __launch_bounds__(16 * 32 + 64, 1) rnn_fwd_pp_kernel(const RnnArgs a) {
   constexpr int NT = 64, NH = NT / 2, EW = 16, kEpi = EW * 32, kThreads = kEpi + 64, UG = 4;   // NT == kNT
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -738,9 +777,8 @@ __global__ void __launch_bounds__(16 * 32 + 64, 1) rnn_fwd_pp_kernel(const RnnAr
 #pragma unroll
         for (int e = 0; e < UG; ++e) { hp[e] = hv[e]; cc[e] = cv[e]; }
       }
-      const float kl = (qw == 2) ? -2.8853900817779268f : -1.4426950408889634f;
-      const float kb = kl * bias;
-      const float mul = (qw == 2) ? 2.f : 1.f, add = (qw == 2) ? -1.f : 0.f;
+      float kl, kb, mul, add;
+      gate_consts<ACT>(qw, bias, kl, kb, mul, add);
       const uint32_t bar_g = 1 + 2 * hw, bar_x = 2 + 2 * hw;   // named barriers of this half
       for (int t = 0; t < trip; ++t) {
         const uint32_t s = step + t, j = s & 1, use = s >> 1;
@@ -755,7 +793,7 @@ __global__ void __launch_bounds__(16 * 32 + 64, 1) rnn_fwd_pp_kernel(const RnnAr
           tmem_ld16(trow, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) g_out[i * kGS] = fmaf(mul, inv1pexp2(fmaf(v[i], kl, kb)), add);
+          for (int i = 0; i < 16; ++i) g_out[i * kGS] = gate_act<ACT>(v[i], kl, kb, mul, add);
         }
         tc_fence_before();
         __syncwarp();
@@ -772,7 +810,7 @@ __global__ void __launch_bounds__(16 * 32 + 64, 1) rnn_fwd_pp_kernel(const RnnAr
 #pragma unroll
           for (int e = 0; e < UG; ++e) {
             const float c2 = fmaf(g4[1][e], cc[e], g4[0][e] * g4[2][e]);
-            const float h2 = g4[3][e] * tanh_acc(c2);
+            const float h2 = g4[3][e] * cell_tanh<ACT>(c2);
             cc[e] = live ? c2 : cc[e];
             hp[e] = live ? h2 : hp[e];
           }
@@ -1070,6 +1108,59 @@ __global__ void __launch_bounds__(256) pack_x_kernel(const XT* __restrict__ x, c
   if (bad) set_err(err, SKB_ERR_FP16_RANGE, -1, -1);
 }
 
+// Coalesced variant for fp32 x with F % 128 == 0 (the C1 shape): one block per
+// (tile, t) image.  Each warp reads whole 4*F-byte rows (lane k*4.., fully
+// coalesced), converts to fp16 into a padded row-major shared tile, then all
+// threads write the image in core-matrix order ([Kx/8][64 rows][8] halves) as
+// contiguous 16-byte stores.  Rows past their length are written as zeros.
+template <int NQ>
+__global__ void __launch_bounds__(256) pack_x_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
+                                   const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
+                                   uint8_t* __restrict__ img, int32_t* err, int T, int Bp) {
+  constexpr int F = NQ * 128, kRow = F * 2 + 16;   // padded fp16 row: 16-byte reads of 8 lanes hit distinct banks
+  extern __shared__ __align__(16) uint8_t srow[];
+  const int tile = blockIdx.x, t = blockIdx.y;
+  const int r0 = perm[tile * kNT];
+  if (r0 < 0) return;
+  const int tm0 = min(max(pmax[r0 / Bp], 0), T);
+  const long long L0 = lens[r0];
+  if (t >= (L0 < tm0 ? L0 : tm0)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bool bad = false;
+  float4 v[8][NQ];
+  bool on[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int n = warp * 8 + i;
+    const int r = perm[tile * kNT + n];
+    on[i] = r >= 0 && t < lens[r];
+    const float4* row = reinterpret_cast<const float4*>(x + ((size_t)(on[i] ? r : 0) * T + t) * F);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[i][q] = on[i] ? __ldcs(row + q * 32 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint8_t* dst = srow + (warp * 8 + i) * kRow;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const float4 a = v[i][q];
+      bad |= fp16_overflow(a.x) || fp16_overflow(a.y) || fp16_overflow(a.z) || fp16_overflow(a.w);
+      __half2 lo = __floats2half2_rn(a.x, a.y), hi = __floats2half2_rn(a.z, a.w);
+      *reinterpret_cast<uint2*>(dst + (q * 128 + lane * 4) * 2) =
+          make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    }
+  }
+  __syncthreads();
+  constexpr int kChunks = kNT * F / 8;   // 16-byte chunks of the image, row fastest
+  uint4* out = reinterpret_cast<uint4*>(img + ((size_t)tile * T + t) * (kNT * F * 2));
+#pragma unroll 4
+  for (int o = threadIdx.x; o < kChunks; o += 256) {
+    const int n = o % kNT, kc = o / kNT;
+    out[o] = *reinterpret_cast<const uint4*>(srow + n * kRow + kc * 16);
+  }
+  if (bad) set_err(err, SKB_ERR_FP16_RANGE, -1, -1);
+}
+
 struct Workspace {
   int32_t *perm, *pmax, *hist, *base, *cursor;
   uint8_t* hscratch;
@@ -1140,9 +1231,9 @@ constexpr int kProfMax = 256;
 cudaEvent_t g_prof_ev[2 * kProfMax];
 int g_prof_cap = 0, g_prof_n = 0;
 
-template <int CELL, typename XT, int EW>
+template <int CELL, typename XT, int EW, int ACT = 0>
 int launch_main_ew(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
-  auto kern = rnn_fwd_kernel<CELL, kNT, XT, EW>;
+  auto kern = rnn_fwd_kernel<CELL, kNT, XT, EW, ACT>;
   constexpr int kThreads = EW * 32 + 64;
   const size_t smem = smem_bytes<kNT>(g);
   if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
@@ -1184,9 +1275,9 @@ inline bool rnn_pp() {
   return pp == 1;
 }
 
-template <typename XT>
+template <typename XT, int ACT>
 int launch_pp(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
-  auto kern = rnn_fwd_pp_kernel<XT>;
+  auto kern = rnn_fwd_pp_kernel<XT, ACT>;
   constexpr int kThreads = 16 * 32 + 64;
   const size_t smem = smem_bytes<kNT>(g);
   if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
@@ -1218,8 +1309,15 @@ int launch_pp(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
 
 template <int CELL, typename XT>
 int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
-  // the ping-pong kernel needs 32-unit CTA slices (U = 32: H a multiple of 32)
-  if (CELL == SKB_CELL_LSTM && rnn_pp() && g.U == 32 && g.Kh == g.C * 32) return launch_pp<XT>(args, g, stream);
+  if constexpr (CELL == SKB_CELL_LSTM) {
+    const bool act = rnn_act() == 1;
+    // the ping-pong kernel needs 32-unit CTA slices (U = 32: H a multiple of 32)
+    if (rnn_pp() && g.U == 32 && g.Kh == g.C * 32)
+      return act ? launch_pp<XT, 1>(args, g, stream) : launch_pp<XT, 0>(args, g, stream);
+    if (rnn_ew() == 8)
+      return act ? launch_main_ew<CELL, XT, 8, 1>(args, g, stream) : launch_main_ew<CELL, XT, 8, 0>(args, g, stream);
+    return act ? launch_main_ew<CELL, XT, 16, 1>(args, g, stream) : launch_main_ew<CELL, XT, 16, 0>(args, g, stream);
+  }
   return rnn_ew() == 8 ? launch_main_ew<CELL, XT, 8>(args, g, stream) : launch_main_ew<CELL, XT, 16>(args, g, stream);
 }
 
@@ -1365,10 +1463,26 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   a.ximg = w.ximg;
   {
     const dim3 pg(ntiles, g.T);
+    const bool rows_ok = !x_f64 && g.F == g.Kx && (reinterpret_cast<uintptr_t>(x_dev) & 15) == 0 &&
+                         (g.F == 128 || g.F == 256 || g.F == 512) && !getenv("SKB_PACK_X_LEGACY");
     if (x_f64)
       pack_x_kernel<double><<<pg, 256, 0, st>>>((const double*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
                                                   err_dev, ntiles, g.T, g.F, g.Kx, g.Bp);
-    else
+    else if (rows_ok) {
+      const size_t sm = (size_t)kNT * (g.F * 2 + 16);
+      if (g.F == 128)
+        pack_x_rows_kernel<1><<<pg, 256, sm, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg, err_dev, g.T, g.Bp);
+      else if (g.F == 256)
+        pack_x_rows_kernel<2><<<pg, 256, sm, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg, err_dev, g.T, g.Bp);
+      else {
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(pack_x_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          attr = true;
+        }
+        pack_x_rows_kernel<4><<<pg, 256, sm, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg, err_dev, g.T, g.Bp);
+      }
+    } else
       pack_x_kernel<float><<<pg, 256, 0, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
                                                  err_dev, ntiles, g.T, g.F, g.Kx, g.Bp);
   }
