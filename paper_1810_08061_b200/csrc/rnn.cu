@@ -124,12 +124,12 @@ struct RnnArgs {
 __device__ long long* g_trace = nullptr;
 __device__ int g_trace_steps = 0;
 #ifdef SKB_TRACE_ENABLED
-__device__ long long* g_ttrace = nullptr;   // per-tile events of CTA 0: [tile_iter][4]
+__device__ long long* g_ttrace = nullptr;   // per-tile events of CTA 0: [tile_iter][8]
 __device__ int g_ttrace_n = 0;
 #define SKB_TTRACE(it_, slot_)                                                             \
   do {                                                                                     \
     if (g_ttrace != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && (it_) < g_ttrace_n)  \
-      g_ttrace[(size_t)(it_) * 4 + (slot_)] = clock64();                                   \
+      g_ttrace[(size_t)(it_) * 8 + (slot_)] = clock64();                                   \
   } while (0)
 #define SKB_TRACE(step_, slot_)                                                            \
   do {                                                                                     \
@@ -170,6 +170,7 @@ SKB_DEV float inv1pexp2(float a) { return rcp_nr(1.f + fminf(ex2_approx(a), 1e30
 // 1/(1 + e^{k x}) (kept for the RNN path)
 SKB_DEV float inv1pexp(float kx) { return inv1pexp2(kx * 1.4426950408889634f); }
 
+SKB_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" :: "l"(p)); }
 SKB_DEV float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -327,68 +328,64 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
   bool hfull_armed = false;
   const int nclusters = (int)nclusters_x();
   int tile_iter = 0;
-  for (int tile = (int)cluster_id_x(); tile < a.ntiles; tile += nclusters, ++tile_iter) {
-    SKB_TTRACE(tile_iter, 0);
-    cluster_sync();   // previous tile retired cluster-wide (no copies in flight)
-    if (tid < NT) {
-      const int r = a.perm[tile * NT + tid];
-      int len = 0, tmax = 0;
+  // Row metadata of a tile (thread tid < NT owns row tid): loaded one tile
+  // ahead, and the next tile's h0/c0 rows prefetched into L2, so a tile's
+  // setup does not wait on dependent global loads.
+  static_assert(NT == 64, "the tile metadata reduction assumes 64-row tiles");
+  auto tile_meta = [&](int tl, int& r, int& len, int& tmax) {
+    r = -1; len = 0; tmax = 0;
+    if (tl < a.ntiles && tid < NT) {
+      r = a.perm[tl * NT + tid];
       if (r >= 0) {
         tmax = max(0, min(a.pmax[r / a.Bp], T));
         const long long L = a.lens[r];
         len = (int)max(0LL, min(L, (long long)tmax));
       }
-      s_row[tid] = r; s_len[tid] = len; s_tmax[tid] = tmax;
     }
+  };
+  int m_r, m_len, m_tmax;
+  tile_meta((int)cluster_id_x(), m_r, m_len, m_tmax);
+  for (int tile = (int)cluster_id_x(); tile < a.ntiles; tile += nclusters, ++tile_iter) {
+    SKB_TTRACE(tile_iter, 0);
+    // No cluster barrier between tiles: a peer's first h exchange of the next tile
+    // targets hbuf[s0&1], whose last reader (this CTA's MMA of step s0-2) has
+    // completed before this CTA's step s0-2 h slice -- which the peer needed to
+    // finish step s0-1 -- was sent; every other buffer and barrier phase is
+    // per-CTA and carried across tiles.
+    __syncthreads();   // this CTA's previous tile retired (s_row/s_len are rewritten below)
+    SKB_TTRACE(tile_iter, 4);
+    if (tid < NT) { s_row[tid] = m_r; s_len[tid] = m_len; s_tmax[tid] = m_tmax; }
     __syncthreads();
-    if (tid == 0) {
-      int m = 0;
-      for (int i = 0; i < NT; ++i) m = max(m, s_len[i]);
-      s_trip = m;
+    if (warp == 0) {
+      int m = max(s_len[lane], s_len[lane + 32]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) s_trip = m;
     }
-    {  // h0 -> hbuf[step&1] (fp16, full Kh, zero padding); 8-element chunks, batched loads
-      uint8_t* hb = sH + (step & 1) * hbytes;
-      const int kch = a.Kh / 8;
-      constexpr int kB = 4;
-      for (int i0 = tid; i0 < NT * kch; i0 += kThreads * kB) {
-        float v[kB][8];
-#pragma unroll
-        for (int m = 0; m < kB; ++m) {
-          const int i = i0 + m * kThreads;
-          const int n = i / kch, kc = i - n * kch;
-          const int r = (i < NT * kch) ? s_row[n] : -1;
-          if (r >= 0) load_x8<float>(a.h0 + (size_t)r * H, kc * 8, H, v[m]);
-          else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) v[m][e] = 0.f;
-          }
-        }
-#pragma unroll
-        for (int m = 0; m < kB; ++m) {
-          const int i = i0 + m * kThreads;
-          if (i >= NT * kch) continue;
-          const int n = i / kch, kc = i - n * kch;
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            __half2 h2 = __floats2half2_rn(v[m][2 * e], v[m][2 * e + 1]);
-            w[e] = *reinterpret_cast<uint32_t*>(&h2);
-          }
-          *reinterpret_cast<uint4*>(hb + cm_offset(n, kc * 8, b_lbo, b_sbo)) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-      }
-    }
+    SKB_TTRACE(tile_iter, 5);
+    SKB_TTRACE(tile_iter, 6);
     fence_proxy_async_smem();
     __syncthreads();
     const int trip = s_trip;
     SKB_TTRACE(tile_iter, 1);
 #ifdef SKB_TRACE_ENABLED
     if (threadIdx.x == 0 && g_ttrace != nullptr && blockIdx.x == 0 && tile_iter < g_ttrace_n)
-      g_ttrace[(size_t)tile_iter * 4 + 3] = trip;
+      g_ttrace[(size_t)tile_iter * 8 + 3] = trip;
 #endif
 
     if (warp < EW) {
       // ======================= epilogue =======================
+      if (tid < NT) {   // next tile's metadata (consumed next iteration) and its h0/c0 rows -> L2, off the critical path
+        tile_meta(tile + nclusters, m_r, m_len, m_tmax);
+        if (m_r >= 0) {
+          const char* h0n = reinterpret_cast<const char*>(a.h0 + (size_t)m_r * H);
+          const char* c0n = a.c0 ? reinterpret_cast<const char*>(a.c0 + (size_t)m_r * H) : nullptr;
+          for (int off = 0; off < H * 4; off += 128) {
+            prefetch_l2(h0n + off);
+            if (c0n) prefetch_l2(c0n + off);
+          }
+        }
+      }
       if constexpr (CELL == SKB_CELL_LSTM) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -411,6 +408,33 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
           const int r = s_row[ch * NCOL + i];
           hp[i] = (rnn_valid && r >= 0) ? a.h0[(size_t)r * H + rnn_unit] : 0.f;
         }
+      }
+      if (trip > 0) {   // h0 reaches every CTA's hbuf[step&1] like any h_t: own fp16 slice -> L2 -> multicast
+        uint8_t* gs0 = gscr + (step & 1) * hbytes + q * sbytes;
+        if constexpr (CELL == SKB_CELL_LSTM) {
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            if (!pv[p]) continue;
+            uint32_t hw[UG / 2];
+#pragma unroll
+            for (int e = 0; e < UG / 2; ++e) {
+              __half2 h2 = __floats2half2_rn(hp[p * UG + 2 * e], hp[p * UG + 2 * e + 1]);
+              hw[e] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            uint8_t* dst = gs0 + cm_offset(pn[p], pu[p], b_lbo, b_sbo);
+            if constexpr (UG == 8) *reinterpret_cast<uint4*>(dst) = make_uint4(hw[0], hw[1], hw[2], hw[3 % (UG / 2)]);
+            else *reinterpret_cast<uint2*>(dst) = make_uint2(hw[0], hw[1 % (UG / 2)]);
+          }
+        } else if (rnn_u < U) {
+#pragma unroll
+          for (int i = 0; i < NCOL; ++i)
+            *reinterpret_cast<__half*>(gs0 + cm_offset(ch * NCOL + i, rnn_u, b_lbo, b_sbo)) = __float2half_rn(hp[i]);
+        }
+        fence_proxy_async_global();
+        named_bar_sync(1, kEpi);
+        if (tid == 0)
+          bulk_g2s_multicast(sH + (step & 1) * hbytes + q * sbytes, gs0, sbytes, &hfull[step & 1],
+                             (uint16_t)((1u << C) - 1));
       }
       for (int t = 0; t < trip; ++t) {
         const uint32_t s = step + t, j = s & 1, use = s >> 1;
@@ -607,7 +631,7 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
           umma_f16_ts_warp(d, tmem + kWCol + ks * 8, xdesc0 + (uint64_t)(ks * 2 * b_lbo >> 4), idesc,
                            ks > 0 ? 1u : 0u);
         umma_commit_warp(&xempty[j]);
-        if (t > 0) {
+        {   // h_t (h0 at a tile's first step) from every CTA of the cluster
           const uint32_t hb = s & 1;
           mbar_wait(&hfull[hb], hwait[hb] & 1);
           ++hwait[hb];

@@ -24,14 +24,14 @@ lib = runtime.lib()
 for _ in range(3):
     exe.run(x, h0, c0, lens, out)
 tr = torch.zeros(4096 * 16, dtype=torch.int64, device=dev)
-tt = torch.zeros(256 * 4, dtype=torch.int64, device=dev)
+tt = torch.zeros(256 * 8, dtype=torch.int64, device=dev)
 lib.skb_debug_rnn_trace(ctypes.c_void_p(tr.data_ptr()), 4096)
 lib.skb_debug_rnn_tile_trace(ctypes.c_void_p(tt.data_ptr()), 256)
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record(); exe.run(x, h0, c0, lens, out); e1.record(); torch.cuda.synchronize()
 print("run ms", e0.elapsed_time(e1))
 lib.skb_debug_rnn_trace(None, 0); lib.skb_debug_rnn_tile_trace(None, 0)
-a = tr.view(4096, 16).cpu().numpy(); t = tt.view(256, 4).cpu().numpy()
+a = tr.view(4096, 16).cpu().numpy(); t = tt.view(256, 8).cpu().numpy()
 ntile = int((t[:, 0] != 0).sum())
 base = t[0, 0]
 tot_setup = tot_loop = tot_tail = 0
@@ -43,6 +43,9 @@ for i in range(ntile):
     if i < 6 or i == ntile - 1:
         print(f"tile {i}: trip {t[i,3]} setup {setup} loop {loop} ({loop / max(t[i,3],1):.0f}/step) tail {tail}")
 print(f"tiles {ntile}: setup {tot_setup} loop {tot_loop} tail {tot_tail} cycles")
+sel = slice(1, ntile - 1)
+print("setup parts (median): cluster_sync", np.median(t[sel, 4] - t[sel, 0]), "meta+trip", np.median(t[sel, 5] - t[sel, 4]),
+      "h0 image", np.median(t[sel, 6] - t[sel, 5]), "fence+sync", np.median(t[sel, 1] - t[sel, 6]))
 nsteps = int(t[:ntile, 3].sum())
 names = {10: "epi:act", 0: "mma:xfull", 1: "mma:dfree", 2: "mma:hfull", 3: "mma:commit", 4: "epi:mdone", 6: "epi:math", 7: "epi:sent", 8: "ld:start", 9: "ld:done"}
 d = np.diff(a[:nsteps, 4])
