@@ -661,6 +661,296 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
   if (warp == EW + 1) tmem_dealloc<512>(tmem);
 }
 
+// ------------------------------------------------------------------ dual-lane LSTM kernel
+// Two independent recurrences ("lanes") per CTA, each a full 64-row tile with
+// N = 64 MMAs: lane L runs tiles 2*cluster + L, 2*cluster + L + 2*nclusters, ...
+// with its own 8 epilogue warps, x loader warp, MMA warp, TMEM accumulators,
+// shared buffers and mbarriers; the [W;U] slice in TMEM is shared.  While one
+// lane's epilogue turns its gates into h_t and exchanges it across the cluster,
+// the other lane's MMAs run on the tensor pipe, so the serial MMA -> epilogue ->
+// exchange chain of one recurrence overlaps the other's (with N = 64 MMAs, unlike
+// the ping-pong halves above).  Shared memory per lane: one x_t image, one h_t
+// image, the gate exchange; a single h buffer is safe because a lane only
+// multicasts h_{t+1} after every CTA's MMA of step t has retired (hempty: one
+// remote arrival per CTA per step).
+template <typename XT, int ACT = 1>
+__global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a) {
+  constexpr int NT = 64, EWL = 8, kEpiL = EWL * 32, NCOL = NT / (EWL / 4), UG = 8;   // NT == kNT
+  constexpr int kLoad0 = 16, kMma0 = 18;   // warps: 0-15 epilogue (lane = warp >> 3), 16-17 loaders, 18-19 MMA
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint64_t xfull[2], xempty[2], hfull[2], hempty[2][2], mdone[2][2], dfree[2][2];
+  __shared__ uint32_t tmem_s;
+  __shared__ int s_row[2][NT], s_len[2][NT];
+  __shared__ int s_trip[2];
+
+  uint8_t* smem = smem_raw;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int L = warp < kLoad0 ? (warp >> 3) : (warp < kMma0 ? warp - kLoad0 : warp - kMma0);
+  const uint32_t q = cluster_ctarank();
+  const int C = a.C, U = a.U, H = a.H, T = a.T;
+  const uint32_t xbytes = NT * a.Kx * 2, hbytes = NT * a.Kh * 2, sbytes = NT * U * 2;
+  const uint32_t gbytes = 4 * NT * kGS * 4, lane_bytes = xbytes + hbytes + gbytes;
+  uint8_t* sX = smem + L * lane_bytes;     // [NT x Kx] fp16, core-matrix layout
+  uint8_t* sH = sX + xbytes;               // [NT x Kh] fp16
+  float* sG = reinterpret_cast<float*>(sH + hbytes);   // gates [4][NT][kGS]
+  constexpr uint32_t b_lbo = NT * 16, b_sbo = 128;
+  constexpr uint32_t kWCol = 256;          // TMEM: lane L's D pair at L*128 + j*64, weights at 256
+
+  if (tid == 0) {
+    for (int l = 0; l < 2; ++l) {
+      mbar_init(&xfull[l], 1);
+      mbar_init(&xempty[l], 1);
+      mbar_init(&hfull[l], 1);
+      for (int j = 0; j < 2; ++j) {
+        mbar_init(&hempty[l][j], C);
+        mbar_init(&mdone[l][j], 1);
+        mbar_init(&dfree[l][j], EWL);
+      }
+    }
+    fence_mbar_init();
+  }
+  if (warp == kMma0) tmem_alloc<512>(&tmem_s);
+  for (uint32_t i = tid; i < 2 * lane_bytes / 16; i += 20 * 32)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_s;
+  float bias = 0.f;
+  if (warp < 4) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.wpack + ((size_t)q * 128 + tid) * a.K * 2);
+    for (int c0 = 0; c0 < a.K / 2; c0 += 8) {
+      uint32_t r[8];
+      const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src + c0));
+      const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src + c0 + 4));
+      r[0] = lo.x; r[1] = lo.y; r[2] = lo.z; r[3] = lo.w; r[4] = hi.x; r[5] = hi.y; r[6] = hi.z; r[7] = hi.w;
+      tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + kWCol + c0, r);
+    }
+    tmem_st_wait();
+  }
+  if (warp < kLoad0) bias = a.bpack[q * 128 + (warp & 3) * 32 + lane];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  cluster_sync();   // every CTA's barriers are initialised before any remote traffic
+
+  // epilogue thread e (0..255 within the lane): gate phase = warp quarter qw, column
+  // half ch; cell phase = row n = e / G8, units pu..pu+7 (G8 = U / 8 = 4)
+  const int wl = warp & 7, qw = wl & 3, ch = wl >> 2, e = tid & (kEpiL - 1);
+  const int G8 = U / UG;
+  const int pn = e / G8, pu = (e % G8) * UG;
+  float hp[UG], cc[UG];
+  uint8_t* gslice = a.hscratch + ((size_t)cluster_id_x() * 2 + L) * hbytes + q * sbytes;   // our h slice (lane L)
+  const uint32_t tile_bar = 5 + L, xch_bar = 1 + 2 * L, gate_bar = 2 + 2 * L;   // named barriers of lane L
+  constexpr uint32_t kLaneThreads = kEpiL + 64;
+
+  uint32_t step = 0;
+  const int nclusters = (int)nclusters_x();
+  const int stride = 2 * nclusters;
+  int m_r = -1, m_len = 0;
+  auto tile_meta = [&](int tl) {
+    m_r = -1; m_len = 0;
+    if (tl < a.ntiles) {
+      m_r = a.perm[tl * NT + e];
+      if (m_r >= 0) {
+        const int tmax = max(0, min(a.pmax[m_r / a.Bp], T));
+        m_len = (int)max(0LL, min((long long)a.lens[m_r], (long long)tmax));
+      }
+    }
+  };
+  const int tile0 = 2 * (int)cluster_id_x() + L;
+  if (warp < kLoad0 && e < NT) tile_meta(tile0);
+  if (warp == kMma0 + L && lane == 0) mbar_arrive_expect_tx(&hfull[L], C * sbytes);   // arm phase 0
+
+  for (int tile = tile0; tile < a.ntiles; tile += stride) {
+    named_bar_sync(tile_bar, kLaneThreads);   // this lane's previous tile retired (s_row/s_len rewritten)
+    if (warp < kLoad0 && e < NT) { s_row[L][e] = m_r; s_len[L][e] = m_len; }
+    named_bar_sync(tile_bar, kLaneThreads);
+    if (warp == 8 * L) {
+      int m = max(s_len[L][lane], s_len[L][lane + 32]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) s_trip[L] = m;
+    }
+    named_bar_sync(tile_bar, kLaneThreads);
+    const int trip = s_trip[L];
+
+    if (warp < kLoad0) {
+      // ======================= epilogue (lane L) =======================
+      if (e < NT) {   // next tile's metadata and its h0/c0 rows -> L2
+        tile_meta(tile + stride);
+        if (m_r >= 0) {
+          const char* h0n = reinterpret_cast<const char*>(a.h0 + (size_t)m_r * H);
+          const char* c0n = reinterpret_cast<const char*>(a.c0 + (size_t)m_r * H);
+          for (int off = 0; off < H * 4; off += 128) { prefetch_l2(h0n + off); prefetch_l2(c0n + off); }
+        }
+      }
+      {
+        const int r = s_row[L][pn];
+        const int unit0 = (int)q * U + pu;
+        float hv[8], cv[8];
+        if (r >= 0) {
+          load_x8<float>(a.h0 + (size_t)r * H, unit0, H, hv);
+          load_x8<float>(a.c0 + (size_t)r * H, unit0, H, cv);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) hv[k] = cv[k] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < UG; ++k) { hp[k] = hv[k]; cc[k] = cv[k]; }
+      }
+      // write h (fp16) for step u into our L2 slice and multicast it into every CTA's sH
+      // once every CTA's MMA of step u-1 (the buffer's last reader) has retired
+      auto send_h = [&](uint32_t u) {
+        uint32_t hw[UG / 2];
+#pragma unroll
+        for (int k = 0; k < UG / 2; ++k) {
+          __half2 h2 = __floats2half2_rn(hp[2 * k], hp[2 * k + 1]);
+          hw[k] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        *reinterpret_cast<uint4*>(gslice + cm_offset(pn, pu, b_lbo, b_sbo)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        fence_proxy_async_global();
+        named_bar_sync(xch_bar, kEpiL);
+        if (e == 0) {
+          if (L == 0 && u > 0) SKB_TRACE(u - 1, 6);
+          if (u > 0) mbar_wait_cluster(&hempty[L][(u - 1) & 1], ((u - 1) >> 1) & 1);
+          if (L == 0 && u > 0) SKB_TRACE(u - 1, 11);
+          bulk_g2s_multicast(sH + q * sbytes, gslice, sbytes, &hfull[L], (uint16_t)((1u << C) - 1));
+          if (L == 0 && u > 0) SKB_TRACE(u - 1, 7);
+        }
+      };
+      if (trip > 0) send_h(step);
+      float kl, kb, mul, add;
+      gate_consts<ACT>(qw, bias, kl, kb, mul, add);
+      for (int t = 0; t < trip; ++t) {
+        const uint32_t s = step + t, j = s & 1, use = s >> 1;
+        mbar_wait(&mdone[L][j], use & 1);
+        if (e == 0 && L == 0) SKB_TRACE(s, 4);
+        tc_fence_after();
+        const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16) + L * 128 + j * NT + ch * NCOL;
+        float* g_out = sG + (qw * NT + ch * NCOL) * kGS + lane;
+#pragma unroll
+        for (int c16 = 0; c16 < NCOL / 16; ++c16) {
+          float v[16];
+          tmem_ld16(trow + c16 * 16, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) g_out[(c16 * 16 + i) * kGS] = gate_act<ACT>(v[i], kl, kb, mul, add);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dfree[L][j]);
+        named_bar_sync(gate_bar, kEpiL);
+        if (e == 0 && L == 0) SKB_TRACE(s, 10);
+        {
+          float g4[4][UG];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const float4* src = reinterpret_cast<const float4*>(sG + (g * NT + pn) * kGS + pu);
+#pragma unroll
+            for (int v4 = 0; v4 < UG / 4; ++v4) {
+              const float4 x0 = src[v4];
+              g4[g][4 * v4] = x0.x; g4[g][4 * v4 + 1] = x0.y; g4[g][4 * v4 + 2] = x0.z; g4[g][4 * v4 + 3] = x0.w;
+            }
+          }
+          const bool live = t < s_len[L][pn];
+#pragma unroll
+          for (int k = 0; k < UG; ++k) {
+            const float c2 = fmaf(g4[1][k], cc[k], g4[0][k] * g4[2][k]);
+            const float h2 = g4[3][k] * cell_tanh<ACT>(c2);
+            cc[k] = live ? c2 : cc[k];
+            hp[k] = live ? h2 : hp[k];
+          }
+        }
+        if (t + 1 < trip) send_h(s + 1);
+        else named_bar_sync(xch_bar, kEpiL);   // sG is rewritten next step only after every read
+        // output sequence [R, T, H] (frozen tails: rnn_fill_frozen_kernel)
+        {
+          const int r = s_row[L][pn];
+          if (r >= 0 && t < s_len[L][pn]) {
+            float* o = a.out + ((size_t)r * T + t) * H + (int)q * U + pu;
+            reinterpret_cast<float4*>(o)[0] = make_float4(hp[0], hp[1], hp[2], hp[3]);
+            reinterpret_cast<float4*>(o)[1] = make_float4(hp[4], hp[5], hp[6], hp[7]);
+          }
+        }
+      }
+      {
+        const int r = s_row[L][pn];
+        if (r >= 0) {
+          float* hT = a.hT + (size_t)r * H + (int)q * U + pu;
+          reinterpret_cast<float4*>(hT)[0] = make_float4(hp[0], hp[1], hp[2], hp[3]);
+          reinterpret_cast<float4*>(hT)[1] = make_float4(hp[4], hp[5], hp[6], hp[7]);
+          if (a.cT) {
+            float* cT = a.cT + (size_t)r * H + (int)q * U + pu;
+            reinterpret_cast<float4*>(cT)[0] = make_float4(cc[0], cc[1], cc[2], cc[3]);
+            reinterpret_cast<float4*>(cT)[1] = make_float4(cc[4], cc[5], cc[6], cc[7]);
+          }
+        }
+      }
+    } else if (warp < kMma0) {
+      // ======================= x_t loader (lane L): one buffer, filled once x-part(s-1) retired
+      if (lane == 0) {
+        const uint8_t* img = a.ximg + (size_t)tile * T * xbytes;
+        for (int t = 0; t < trip; ++t) {
+          const uint32_t s = step + t;
+          mbar_wait(&xempty[L], (s & 1) ^ 1);
+          mbar_arrive_expect_tx(&xfull[L], xbytes);
+          for (uint32_t off = 0; off < xbytes; off += 16384)
+            bulk_g2s(sX + off, img + (size_t)t * xbytes + off, min(16384u, xbytes - off), &xfull[L]);
+        }
+      }
+    } else {
+      // ======================= MMA issuer (lane L)
+      // order: x-part(s0); then per step h-part(s), x-part(s+1) -- a late x_{s+1}
+      // (single buffer) never holds back the h-part on the recurrence's critical path
+      const uint32_t idesc = idesc_f16_f32(128, NT);
+      const uint32_t x_addr = smem_u32(sX), h_addr = smem_u32(sH);
+      const int kx_steps = a.Kx / 16, kh_steps = a.Kh / 16;
+      const uint64_t xdesc0 = sdesc_kmajor_noswz(x_addr, b_lbo, b_sbo);
+      const uint64_t hdesc0 = sdesc_kmajor_noswz(h_addr, b_lbo, b_sbo);
+      auto x_part = [&](uint32_t s) {
+        const uint32_t j = s & 1, use = s >> 1;
+        mbar_wait(&xfull[L], s & 1);
+        if (lane == 0 && L == 0) SKB_TRACE(s, 0);
+        mbar_wait(&dfree[L][j], (use & 1) ^ 1);
+        if (lane == 0 && L == 0) SKB_TRACE(s, 1);
+        tc_fence_after();
+        const uint32_t d = tmem + L * 128 + j * NT;
+#pragma unroll 4
+        for (int ks = 0; ks < kx_steps; ++ks)
+          umma_f16_ts_warp(d, tmem + kWCol + ks * 8, xdesc0 + (uint64_t)(ks * 2 * b_lbo >> 4), idesc, ks > 0 ? 1u : 0u);
+        umma_commit_warp(&xempty[L]);
+      };
+      if (trip > 0) x_part(step);
+      for (int t = 0; t < trip; ++t) {
+        const uint32_t s = step + t, j = s & 1;
+        const uint32_t d = tmem + L * 128 + j * NT;
+        mbar_wait(&hfull[L], s & 1);
+        if (lane == 0 && L == 0) SKB_TRACE(s, 2);
+        if (lane == 0) mbar_arrive_expect_tx(&hfull[L], C * sbytes);   // arm the next phase
+        tc_fence_after();
+#pragma unroll 4
+        for (int ks = 0; ks < kh_steps; ++ks)
+          umma_f16_ts_warp(d, tmem + kWCol + (kx_steps + ks) * 8, hdesc0 + (uint64_t)(ks * 2 * b_lbo >> 4), idesc, 1u);
+        umma_commit_warp(&mdone[L][j]);
+        // the retirement of this CTA's MMAs of step s (the last reader of sH) is
+        // counted on hempty[s&1] of every CTA of the cluster
+        umma_commit_warp_multicast(&hempty[L][j], (uint16_t)((1u << C) - 1));
+        if (lane == 0 && L == 0) SKB_TRACE(s, 3);
+        if (t + 1 < trip) x_part(s + 1);
+      }
+    }
+    __syncwarp();
+    step += trip;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();   // peers' last hempty arrivals have landed before any CTA exits
+  if (warp == kMma0) tmem_dealloc<512>(tmem);
+}
+
 // ------------------------------------------------------------------ ping-pong LSTM kernel
 // The rows of a 64-row tile form two independent 32-row recurrences (halves).
 // The MMA warp alternates halves: while half A's epilogue (warps 0-7) turns
@@ -1331,11 +1621,56 @@ int launch_pp(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
   return skb_check_launch();
 }
 
+// Dual-lane kernel (default for the LSTM when U == 32): SKB_RNN_DL=0 selects the
+// single-lane kernel.
+inline bool rnn_dl() {
+  static int dl = -1;
+  if (dl < 0) {
+    const char* e = getenv("SKB_RNN_DL");
+    dl = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return dl == 1;
+}
+
+template <typename XT, int ACT>
+int launch_dl(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
+  auto kern = rnn_fwd_dl_kernel<XT, ACT>;
+  constexpr int kThreads = 20 * 32;
+  const size_t smem = (size_t)2 * (kNT * g.Kx * 2 + kNT * g.Kh * 2 + 4 * kNT * kGS * 4) + 1024;
+  if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SKB_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(g.C);
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
+    return SKB_ERR_CUDA;
+  const int ncl = min(min(max_clusters, (args.ntiles + 1) / 2), max_clusters_bound(g) - 1);
+  cfg.gridDim = dim3(g.C * max(ncl, 1));
+  const bool prof = g_prof_n < g_prof_cap;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], stream);
+  if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n++ + 1], stream);
+  return skb_check_launch();
+}
+
 template <int CELL, typename XT>
 int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
   if constexpr (CELL == SKB_CELL_LSTM) {
     const bool act = rnn_act() == 1;
-    // the ping-pong kernel needs 32-unit CTA slices (U = 32: H a multiple of 32)
+    // the ping-pong and dual-lane kernels need 32-unit CTA slices (U = 32: H a multiple of 32)
+    if (rnn_dl() && !rnn_pp() && rnn_ew() == 16 && g.U == 32 && g.H == g.C * 32 && g.Kh == g.H && args.c0)
+      return act ? launch_dl<XT, 1>(args, g, stream) : launch_dl<XT, 0>(args, g, stream);
     if (rnn_pp() && g.U == 32 && g.Kh == g.C * 32)
       return act ? launch_pp<XT, 1>(args, g, stream) : launch_pp<XT, 0>(args, g, stream);
     if (rnn_ew() == 8)

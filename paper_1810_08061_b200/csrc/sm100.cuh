@@ -59,6 +59,12 @@ SKB_DEV void mbar_remote_arrive(uint32_t cluster_bar_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];"
                :: "r"(cluster_bar_addr) : "memory");
 }
+// Relaxed remote arrival: a pure "done" signal with nothing to publish (no
+// release fence, so it never waits on the issuing thread's outstanding stores).
+SKB_DEV void mbar_remote_arrive_relaxed(uint32_t cluster_bar_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];"
+               :: "r"(cluster_bar_addr) : "memory");
+}
 SKB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile("{\n\t.reg .pred p;\n\t"
@@ -158,6 +164,13 @@ SKB_DEV void umma_commit_warp(uint64_t* bar) {
                "elect.sync rx|e, 0xffffffff;\n\t"
                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
                :: "r"(smem_u32(bar)) : "memory");
+}
+// The same, arriving on the mbarrier at this offset in every CTA of `cta_mask`.
+SKB_DEV void umma_commit_warp_multicast(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 rx;\n\t"
+               "elect.sync rx|e, 0xffffffff;\n\t"
+               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+               :: "r"(smem_u32(bar)), "h"(cta_mask) : "memory");
 }
 // Warp-wide store of 8 consecutive 32-bit columns into the warp's 32 TMEM lanes.
 SKB_DEV void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {

@@ -160,7 +160,7 @@ def test_pipelined_host_to_host_matches_device_path(c1_graph):
         assert np.array_equal(a.outputs[0].array, b.outputs[0].array)
 
 
-@pytest.mark.parametrize("variant", ["SKB_RNN_EW=8", "SKB_RNN_PP=1", "SKB_RNN_ACT=0"])
+@pytest.mark.parametrize("variant", ["SKB_RNN_EW=8", "SKB_RNN_PP=1", "SKB_RNN_DL=0", "SKB_RNN_ACT=0"])
 def test_kernel_variants_bit_identical_to_default(c1_graph, variant):
     """The alternative C1 kernel layouts (8-warp epilogue; ping-pong halves)
     produce results identical to the default kernel (same arithmetic per

@@ -46,8 +46,8 @@ print(f"tiles {ntile}: setup {tot_setup} loop {tot_loop} tail {tot_tail} cycles"
 sel = slice(1, ntile - 1)
 print("setup parts (median): cluster_sync", np.median(t[sel, 4] - t[sel, 0]), "meta+trip", np.median(t[sel, 5] - t[sel, 4]),
       "h0 image", np.median(t[sel, 6] - t[sel, 5]), "fence+sync", np.median(t[sel, 1] - t[sel, 6]))
-nsteps = int(t[:ntile, 3].sum())
-names = {10: "epi:act", 0: "mma:xfull", 1: "mma:dfree", 2: "mma:hfull", 3: "mma:commit", 4: "epi:mdone", 6: "epi:math", 7: "epi:sent", 8: "ld:start", 9: "ld:done"}
+nsteps = int(t[:ntile, 3].sum()) if ntile else int((a[:, 4] != 0).sum())
+names = {11: "epi:hempty ok", 10: "epi:act", 0: "mma:xfull", 1: "mma:dfree", 2: "mma:hfull", 3: "mma:commit", 4: "epi:mdone", 6: "epi:math", 7: "epi:sent", 8: "ld:start", 9: "ld:done"}
 d = np.diff(a[:nsteps, 4])
 print("steps", nsteps, "median step cycles", np.median(d))
 for k in sorted(names):
