@@ -262,7 +262,7 @@ def run_skb(args, rank, world, local_rank):
             pass
         roofline = {"bound": "tensor", "achieved": achieved, "peak": sust, "unit": "TFLOP/s",
                     "frac": achieved / sust, "traffic": traffic,
-                    "kernel": "rnn_fwd_kernel (persistent 8-CTA clusters, tcgen05 f16)",
+                    "kernel": "rnn_fwd_dl_kernel (persistent 8-CTA clusters, two 64-row recurrences per CTA, tcgen05 f16)",
                     "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / ms,
                     "flops_per_launch": useful,
                     "flop_basis": "useful 2*(F+H)*4H per (row, t < len), SURVEY 8(d)",
