@@ -471,9 +471,20 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
     x_dtype = torch.float32 if x32 else torch.float64
     if host_outputs is not False and host_outputs is not None and T > 0 and P >= 4 and _all_pinned(prog, [f0]):
         # feed sets are bound chunk by chunk inside the pipeline, overlapping the copies
-        out_host, hT_h, cT_h, max_len, status = _run_pipelined(prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P,
-                                                              device, x_dtype, host_outputs, stream)
-        return _assemble(prog, out_host, hT_h, cT_h, max_len, status, Bsz, T, P, return_exceptions)
+        out_host, hT_h, cT_h, ml_host, status_h, ml_dev, finish = _run_pipelined(
+            prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device, x_dtype, host_outputs, stream)
+        # results are views of the host buffers: built while the last copies are in flight
+        results = _assemble(prog, out_host, hT_h, cT_h, ml_host, None, Bsz, T, P, True)
+        finish()
+        if int(status_h[0]) == E.SKB_ERR_FP16_RANGE:
+            raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
+        if not np.array_equal(ml_dev.numpy(), ml_host):   # (host and device trip counts agree by construction)
+            results = _assemble(prog, out_host, hT_h, cT_h, ml_dev.numpy(), None, Bsz, T, P, True)
+        if not return_exceptions:
+            for r in results:
+                if isinstance(r, Exception):
+                    raise r
+        return results
     bound = [f0] + [bind(f) for f in feeds_list[1:]]
     exe = _executable(prog, weights, Bsz, T, F, H, P, device, stream)
     x = cat(prog.x, x_dtype)
@@ -570,12 +581,14 @@ def _run_pipelined(prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device,
     max_len = torch.zeros(P, dtype=torch.int32, device=device)
     status = torch.zeros(4, dtype=torch.int32, device=device)
     step = -(-P // max(2, min(PIPELINE_CHUNKS, P // 2)))
+    lens_vals = []
     for p0 in range(0, P, step):
         p1 = min(P, p0 + step)
         pc = p1 - p0
         exe = _executable(prog, weights, Bsz, T, F, H, pc, device, comp)
         rows = slice(p0 * Bsz, p1 * Bsz)
         chunk = [f0 if p == 0 else bind(feeds_list[p]) for p in range(p0, p1)]
+        lens_vals.extend(_source_value(prog.lens, b) for b in chunk)
 
         def stack(src, dtype, shape, buf):
             dev = buf[rows]
@@ -608,14 +621,34 @@ def _run_pipelined(prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device,
         s_out.wait_event(ev_out)
         with torch.cuda.stream(s_out):
             host_out[rows].copy_(out, non_blocking=True)
-    s_out.synchronize()
-    comp.synchronize()
-    return (host_out, hT.to("cpu") if hT is not None else None, cT.to("cpu") if cT is not None else None,
-            max_len.to("cpu").numpy(), status.to("cpu"))
+    # final states, trip counts and status follow the last output chunk on the copy-out stream
+    s_out.wait_stream(comp)
+    hT_h = torch.empty((R, H), dtype=torch.float32, pin_memory=True) if hT is not None else None
+    cT_h = torch.empty((R, H), dtype=torch.float32, pin_memory=True) if cT is not None else None
+    ml_dev = torch.empty(P, dtype=torch.int32, pin_memory=True)
+    status_h = torch.empty(4, dtype=torch.int32, pin_memory=True)
+    with torch.cuda.stream(s_out):
+        if hT is not None:
+            hT_h.copy_(hT, non_blocking=True)
+        if cT is not None:
+            cT_h.copy_(cT, non_blocking=True)
+        ml_dev.copy_(max_len, non_blocking=True)
+        status_h.copy_(status, non_blocking=True)
+    # the trip counts again on the host (reduce_max of each problem's lengths), for building results early
+    run = _adjacent_run(lens_vals, (P * Bsz,))
+    if run is not None:
+        ml_host = run.view(P, Bsz).max(dim=1).values.numpy().astype(np.int64)
+    else:
+        ml_host = np.array([int(torch.as_tensor(as_numpy(v)).max()) for v in lens_vals], dtype=np.int64)
+
+    def finish():
+        s_out.synchronize()
+        comp.synchronize()
+    return host_out, hT_h, cT_h, ml_host, status_h, ml_dev, finish
 
 
 def _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions):
-    if int(status[0]) == E.SKB_ERR_FP16_RANGE:
+    if status is not None and int(status[0]) == E.SKB_ERR_FP16_RANGE:
         raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
     results = []
     for p in range(P):

@@ -194,3 +194,31 @@ def test_kernel_variants_bit_identical_to_default(c1_graph, variant):
         assert max_rel_error(outs[0], outs[1]) <= TOL
     else:
         assert np.array_equal(outs[0], outs[1])
+
+
+def test_pipelined_errors_and_final_states(c1_graph):
+    """The pipelined host-to-host path builds results before its last copies land:
+    per-problem failures (lengths > T, all-zero lengths) and the final-state
+    outputs must match the device-resident path."""
+    import torch
+    from paper_1810_08061_b200 import RuntimeGraphError, execute_many
+    feeds = _c1_problems(8, seed=6)
+    feeds[2] = dict(feeds[2], sequence_len=np.full(32, 70, dtype=np.int64))   # > T: IndexOutOfRange
+    feeds[5] = dict(feeds[5], sequence_len=np.zeros(32, dtype=np.int64))      # empty stack: EmptyPop
+    dev = execute_many(c1_graph, [dict(f, input_data=f["input_data"].astype(np.float32)) for f in feeds],
+                       return_exceptions=True)
+    pinned = []
+    for f in feeds:
+        g = dict(f)
+        for k in ("input_data", "h0", "c0", "sequence_len"):
+            t = torch.from_numpy(np.ascontiguousarray(f[k]))
+            g[k] = (t.float() if k == "input_data" else t).pin_memory()
+        pinned.append(g)
+    host = execute_many(c1_graph, pinned, host_outputs=True, return_exceptions=True)
+    for i, (a, b) in enumerate(zip(host, dev)):
+        if isinstance(b, Exception):
+            assert isinstance(a, RuntimeGraphError) and a.cause_kind == b.cause_kind, i
+            continue
+        assert np.array_equal(a.outputs[0].array, b.outputs[0].array)
+    with pytest.raises(RuntimeGraphError):
+        execute_many(c1_graph, pinned, host_outputs=True)
