@@ -76,6 +76,77 @@ __global__ void tree_cell(const int32_t* __restrict__ order, int row0, int nrows
   }
 }
 
+// float4 variants (H % 4 == 0): a warp covers 128 consecutive units of one row
+// with 16-byte loads/stores; identical per-element arithmetic.
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+__global__ void tree_leaves4(const int32_t* __restrict__ leaves, int nleaves, const float* __restrict__ value,
+                             const float* __restrict__ wc, const int32_t* __restrict__ dest, float* __restrict__ h,
+                             float* __restrict__ c, float* __restrict__ X, int H) {
+  const int H4 = H >> 2;
+  for (int l = blockIdx.x * blockDim.y + threadIdx.y; l < nleaves; l += gridDim.x * blockDim.y) {
+    const int n = leaves[l];
+    const float v = value[n];
+    const int d = dest[n];
+    float* xrow = d >= 0 ? X + (long long)(d >> 1) * 2 * H + (d & 1) * H : nullptr;
+    for (int k4 = threadIdx.x; k4 < H4; k4 += blockDim.x) {
+      const int k = 4 * k4;
+      const float4 w = ld4(wc + k);
+      const float4 cv = make_float4(w.x * v, w.y * v, w.z * v, w.w * v);
+      const float4 hv = make_float4(tanhf(cv.x), tanhf(cv.y), tanhf(cv.z), tanhf(cv.w));
+      st4(c + (long long)n * H + k, cv);
+      st4(h + (long long)n * H + k, hv);
+      if (xrow) st4(xrow + k, hv);
+    }
+  }
+}
+
+__global__ void tree_cell4(const int32_t* __restrict__ order, int row0, int nrows, const int32_t* __restrict__ left,
+                           const int32_t* __restrict__ right, const float* __restrict__ G,
+                           const float* __restrict__ bias, const int32_t* __restrict__ dest, float* __restrict__ h,
+                           float* __restrict__ c, float* __restrict__ X, int H) {
+  const int H4 = H >> 2;
+  for (int rr = blockIdx.x * blockDim.y + threadIdx.y; rr < nrows; rr += gridDim.x * blockDim.y) {
+    const int p = row0 + rr;
+    const int n = order[p];
+    const float* g = G + (long long)p * 5 * H;
+    const float* cl = c + (long long)left[n] * H;
+    const float* cr = c + (long long)right[n] * H;
+    const int d = dest[n];
+    float* xrow = d >= 0 ? X + (long long)(d >> 1) * 2 * H + (d & 1) * H : nullptr;
+    for (int k4 = threadIdx.x; k4 < H4; k4 += blockDim.x) {
+      const int k = 4 * k4;
+      float gi[4], gfl[4], gfr[4], go[4], gu[4], l4[4], r4[4], cv[4], hv[4];
+      const float4 a0 = ld4(g + k), a1 = ld4(g + H + k), a2 = ld4(g + 2 * H + k), a3 = ld4(g + 3 * H + k),
+                   a4 = ld4(g + 4 * H + k);
+      const float4 b0 = ld4(bias + k), b1 = ld4(bias + H + k), b2 = ld4(bias + 2 * H + k),
+                   b3 = ld4(bias + 3 * H + k), b4 = ld4(bias + 4 * H + k);
+      const float4 L = ld4(cl + k), R = ld4(cr + k);
+      const float za[4][5] = {{a0.x + b0.x, a1.x + b1.x, a2.x + b2.x, a3.x + b3.x, a4.x + b4.x},
+                              {a0.y + b0.y, a1.y + b1.y, a2.y + b2.y, a3.y + b3.y, a4.y + b4.y},
+                              {a0.z + b0.z, a1.z + b1.z, a2.z + b2.z, a3.z + b3.z, a4.z + b4.z},
+                              {a0.w + b0.w, a1.w + b1.w, a2.w + b2.w, a3.w + b3.w, a4.w + b4.w}};
+      l4[0] = L.x; l4[1] = L.y; l4[2] = L.z; l4[3] = L.w;
+      r4[0] = R.x; r4[1] = R.y; r4[2] = R.z; r4[3] = R.w;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        gi[e] = sigmoidf_ref(za[e][0]);
+        gfl[e] = sigmoidf_ref(za[e][1]);
+        gfr[e] = sigmoidf_ref(za[e][2]);
+        go[e] = sigmoidf_ref(za[e][3]);
+        gu[e] = tanhf(za[e][4]);
+        cv[e] = gi[e] * gu[e] + gfl[e] * l4[e] + gfr[e] * r4[e];
+        hv[e] = go[e] * tanhf(cv[e]);
+      }
+      const float4 C4 = make_float4(cv[0], cv[1], cv[2], cv[3]), H4v = make_float4(hv[0], hv[1], hv[2], hv[3]);
+      st4(c + (long long)n * H + k, C4);
+      st4(h + (long long)n * H + k, H4v);
+      if (xrow) st4(xrow + k, H4v);
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" int64_t skb_tree_workspace_bytes(int nnodes, int ninternal, int hidden) {
@@ -90,10 +161,16 @@ bool enqueue_forest(cublasHandle_t hb, cudaStream_t cs, int nnodes, int nleaves,
                     const int32_t* right, const int32_t* dest, const float* value, const float* wc, const float* U,
                     const float* bias, int math, float* h, float* c, float* X, float* G) {
   const int blocks = 148 * 8;
-  const int tx = H >= 128 ? 128 : (H >= 64 ? 64 : 32), ty = 256 / tx;   // threads over H x rows per CTA
+  // float4 path when H % 4 == 0 (rows of 16-byte chunks); scalar path otherwise
+  const bool v4 = (H & 3) == 0 && !getenv("SKB_TREE_SCALAR");
+  const int cols = v4 ? H / 4 : H;
+  const int tx = cols >= 128 ? 128 : (cols >= 64 ? 64 : 32), ty = 256 / tx;   // threads over H x rows per CTA
   const dim3 blk(tx, ty);
-  tree_leaves<<<(nleaves + ty - 1) / ty < blocks ? (nleaves + ty - 1) / ty : blocks, blk, 0, cs>>>(
-      leaves, nleaves, value, wc, dest, h, c, X, H);
+  const int lb = (nleaves + ty - 1) / ty < blocks ? (nleaves + ty - 1) / ty : blocks;
+  if (v4)
+    tree_leaves4<<<lb, blk, 0, cs>>>(leaves, nleaves, value, wc, dest, h, c, X, H);
+  else
+    tree_leaves<<<lb, blk, 0, cs>>>(leaves, nleaves, value, wc, dest, h, c, X, H);
   for (int L = 0; L < nlevels; ++L) {
     const int r0 = level_off_host[L], nr = level_off_host[L + 1] - r0;
     if (nr <= 0) continue;
@@ -101,7 +178,10 @@ bool enqueue_forest(cublasHandle_t hb, cudaStream_t cs, int nnodes, int nleaves,
                        2 * H))
       return false;
     const int b = (nr + ty - 1) / ty < blocks ? (nr + ty - 1) / ty : blocks;
-    tree_cell<<<b, blk, 0, cs>>>(order, r0, nr, left, right, G, bias, dest, h, c, X, H);
+    if (v4)
+      tree_cell4<<<b, blk, 0, cs>>>(order, r0, nr, left, right, G, bias, dest, h, c, X, H);
+    else
+      tree_cell<<<b, blk, 0, cs>>>(order, r0, nr, left, right, G, bias, dest, h, c, X, H);
   }
   return cudaPeekAtLastError() == cudaSuccess;
 }
