@@ -113,6 +113,120 @@ __global__ void lstm_bwd_cell(TrainBufs w, const float* __restrict__ y, const in
   }
 }
 
+// float4 variants (H % 4 == 0): thread = 4 consecutive units of one sequence row,
+// same per-element arithmetic as lstm_fwd_cell / lstm_bwd_cell.
+__device__ __forceinline__ float4 f4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void s4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+
+__global__ void lstm_fwd_cell4(TrainBufs w, const float* __restrict__ bias, const int64_t* __restrict__ lens, int B,
+                               int T, int H, int t) {
+  const int b = blockIdx.y;
+  const bool live = t < lens[b];
+  for (int k = 4 * (blockIdx.x * blockDim.x + threadIdx.x); k < H; k += 4 * gridDim.x * blockDim.x) {
+    float* z = w.Z + ((long long)b * T + t) * 4 * H;
+    const float4 zi = f4(z + k), zf = f4(z + H + k), zg = f4(z + 2 * H + k), zo = f4(z + 3 * H + k);
+    const float4 bi = f4(bias + k), bf = f4(bias + H + k), bg = f4(bias + 2 * H + k), bo = f4(bias + 3 * H + k);
+    const long long sp = ((long long)b * (T + 1) + t) * H + k;
+    const float4 cp = f4(w.Cs + sp), hp = f4(w.Hs + sp);
+    const float zin[4][4] = {{zi.x + bi.x, zi.y + bi.y, zi.z + bi.z, zi.w + bi.w},
+                             {zf.x + bf.x, zf.y + bf.y, zf.z + bf.z, zf.w + bf.w},
+                             {zg.x + bg.x, zg.y + bg.y, zg.z + bg.z, zg.w + bg.w},
+                             {zo.x + bo.x, zo.y + bo.y, zo.z + bo.z, zo.w + bo.w}};
+    const float cpv[4] = {cp.x, cp.y, cp.z, cp.w}, hpv[4] = {hp.x, hp.y, hp.z, hp.w};
+    float ig[4], fg[4], gg[4], og[4], cn[4], hn[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      ig[e] = sigf(zin[0][e]);
+      fg[e] = sigf(zin[1][e]);
+      gg[e] = tanhf(zin[2][e]);
+      og[e] = sigf(zin[3][e]);
+      const float c2 = fg[e] * cpv[e] + ig[e] * gg[e];
+      const float h2 = og[e] * tanhf(c2);
+      cn[e] = live ? c2 : cpv[e];
+      hn[e] = live ? h2 : hpv[e];
+    }
+    s4(w.Cs + sp + H, cn[0], cn[1], cn[2], cn[3]);
+    s4(w.Hs + sp + H, hn[0], hn[1], hn[2], hn[3]);
+    if (w.Hb && t + 1 < T) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(hn[0], hn[1]), hi = __floats2bfloat162_rn(hn[2], hn[3]);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&lo);
+      u.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(w.Hb + ((long long)b * T + t + 1) * H + k) = u;
+    }
+    s4(z + k, ig[0], ig[1], ig[2], ig[3]);
+    s4(z + H + k, fg[0], fg[1], fg[2], fg[3]);
+    s4(z + 2 * H + k, gg[0], gg[1], gg[2], gg[3]);
+    s4(z + 3 * H + k, og[0], og[1], og[2], og[3]);
+  }
+}
+
+__device__ __forceinline__ void st_bf4(__nv_bfloat16* p, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
+__global__ void lstm_bwd_cell4(TrainBufs w, const float* __restrict__ y, const int64_t* __restrict__ lens, float inv_b,
+                               int B, int T, int H, int t) {
+  const int b = blockIdx.y;
+  const bool live = t < lens[b];
+  for (int k = 4 * (blockIdx.x * blockDim.x + threadIdx.x); k < H; k += 4 * gridDim.x * blockDim.x) {
+    const long long i = (long long)b * H + k;
+    float* z = w.Z + ((long long)b * T + t) * 4 * H;
+    __nv_bfloat16* zb = w.Zb ? w.Zb + ((long long)b * T + t) * 4 * H : nullptr;
+    float4 dh = f4(w.dh + i);
+    if (live) {
+      const float4 yv = f4(y + ((long long)b * T + t) * H + k);
+      dh.x += yv.x * inv_b; dh.y += yv.y * inv_b; dh.z += yv.z * inv_b; dh.w += yv.w * inv_b;
+    }
+    if (!live) {   // frozen row: gradients pass straight through
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        s4(z + g * H + k, 0.f, 0.f, 0.f, 0.f);
+        if (zb) st_bf4(zb + g * H + k, 0.f, 0.f, 0.f, 0.f);
+      }
+      s4(w.dh + i, dh.x, dh.y, dh.z, dh.w);
+      continue;
+    }
+    const float4 dcv = f4(w.dc + i);
+    const float4 ig4 = f4(z + k), fg4 = f4(z + H + k), gg4 = f4(z + 2 * H + k), og4 = f4(z + 3 * H + k);
+    const long long sp = ((long long)b * (T + 1) + t) * H + k;
+    const float4 cp4 = f4(w.Cs + sp), cn4 = f4(w.Cs + sp + H);
+    const float dhv[4] = {dh.x, dh.y, dh.z, dh.w}, dcs[4] = {dcv.x, dcv.y, dcv.z, dcv.w};
+    const float ig[4] = {ig4.x, ig4.y, ig4.z, ig4.w}, fg[4] = {fg4.x, fg4.y, fg4.z, fg4.w};
+    const float gg[4] = {gg4.x, gg4.y, gg4.z, gg4.w}, og[4] = {og4.x, og4.y, og4.z, og4.w};
+    const float cp[4] = {cp4.x, cp4.y, cp4.z, cp4.w}, cn[4] = {cn4.x, cn4.y, cn4.z, cn4.w};
+    float di[4], df[4], dg[4], dO[4], dcn_out[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float tc = tanhf(cn[e]);
+      const float dcn = dcs[e] + dhv[e] * og[e] * (1.f - tc * tc);
+      di[e] = dcn * gg[e] * ig[e] * (1.f - ig[e]);
+      df[e] = dcn * cp[e] * fg[e] * (1.f - fg[e]);
+      dg[e] = dcn * ig[e] * (1.f - gg[e] * gg[e]);
+      dO[e] = dhv[e] * tc * og[e] * (1.f - og[e]);
+      dcn_out[e] = dcn * fg[e];
+    }
+    s4(z + k, di[0], di[1], di[2], di[3]);
+    s4(z + H + k, df[0], df[1], df[2], df[3]);
+    s4(z + 2 * H + k, dg[0], dg[1], dg[2], dg[3]);
+    s4(z + 3 * H + k, dO[0], dO[1], dO[2], dO[3]);
+    if (zb) {
+      st_bf4(zb + k, di[0], di[1], di[2], di[3]);
+      st_bf4(zb + H + k, df[0], df[1], df[2], df[3]);
+      st_bf4(zb + 2 * H + k, dg[0], dg[1], dg[2], dg[3]);
+      st_bf4(zb + 3 * H + k, dO[0], dO[1], dO[2], dO[3]);
+    }
+    s4(w.dc + i, dcn_out[0], dcn_out[1], dcn_out[2], dcn_out[3]);
+    s4(w.dh + i, 0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 // loss partials: inv_b * sum over live (b, t) of <h_t, y_t>, fixed block order
 __global__ void loss_partials(TrainBufs w, const float* __restrict__ y, const int64_t* __restrict__ lens, float inv_b,
                               int B, int T, int H, int n) {
@@ -248,6 +362,7 @@ bool enqueue(cublasHandle_t hb, cudaStream_t cs, const skb_train_shape& d, Train
   init_states<<<blocks, 256, 0, cs>>>(h0, c0, w, B, T, H);
   cudaMemsetAsync(grads, 0, sizeof(float) * ((size_t)F * G + (size_t)H * G), cs);
   const bool bf = d.math == 2;
+  const bool v4 = (H & 3) == 0 && !getenv("SKB_TRAIN_SCALAR");   // float4 cell kernels
   if (bf) {   // bf16 copies of the GEMM operands that do not change during the step
     to_bf16<<<blocks, 256, 0, cs>>>(x, w.Xb, (long long)B * T * F);
     to_bf16<<<blocks, 256, 0, cs>>>(W, w.Wb, (long long)F * G);
@@ -266,13 +381,21 @@ bool enqueue(cublasHandle_t hb, cudaStream_t cs, const skb_train_shape& d, Train
     } else if (!gemm_rm(hb, d.math, false, false, w.Hs + (size_t)t * H, (T + 1) * H, U, G, Zt, T * G, B, G, H, 1.f)) {
       return false;
     }
-    lstm_fwd_cell<<<dim3((H + 255) / 256, B), 256, 0, cs>>>(w, bias, lens, B, T, H, t);
+    if (v4)
+      lstm_fwd_cell4<<<dim3((H / 4 + 255) / 256, B), H / 4 < 256 ? ((H / 4 + 31) / 32) * 32 : 256, 0, cs>>>(
+          w, bias, lens, B, T, H, t);
+    else
+      lstm_fwd_cell<<<dim3((H + 255) / 256, B), 256, 0, cs>>>(w, bias, lens, B, T, H, t);
   }
   loss_partials<<<kLossBlocks, 256, 0, cs>>>(w, y, lens, inv_b, B, T, H, n);
   loss_final<<<1, 32, 0, cs>>>(w.part, kLossBlocks, loss);
   for (int t = n - 1; t >= 0; --t) {   // BPTT: only dh_{t-1} = dG_t U^T + carry stays per step
     float* Zt = w.Z + (size_t)t * G;
-    lstm_bwd_cell<<<dim3((H + 255) / 256, B), 256, 0, cs>>>(w, y, lens, inv_b, B, T, H, t);
+    if (v4)
+      lstm_bwd_cell4<<<dim3((H / 4 + 255) / 256, B), H / 4 < 256 ? ((H / 4 + 31) / 32) * 32 : 256, 0, cs>>>(
+          w, y, lens, inv_b, B, T, H, t);
+    else
+      lstm_bwd_cell<<<dim3((H + 255) / 256, B), 256, 0, cs>>>(w, y, lens, inv_b, B, T, H, t);
     if (bf) {
       if (!gemm_bf(hb, false, true, w.Zb + (size_t)t * G, T * G, w.Ub, G, w.dh, H, B, H, G, 1.f)) return false;
     } else {
