@@ -7,8 +7,9 @@ Public API (drop-in for the reference CPU executor, graph/execute.py:27):
     result = execute(graph, feeds)          # ExecutionResult(outputs, print_log)
 
 plus ``gradient`` (reverse mode through While/Cond/FuncCall, autodiff.py),
-``execute_many`` (many feed sets, one launch), the IR mirror and its
-JSON wire format (``ir``), and the error classes (``errors``).
+``execute_many`` (many feed sets, one launch), the IR mirror with its JSON
+(``ir``) and s-expression (``from_sexpr``/``to_sexpr``) wire formats, and the
+error classes (``errors``).
 """
 
 from .errors import (BackendUnavailable, DeviceError, IterationLimitExceeded, LoweringError,
@@ -16,13 +17,14 @@ from .errors import (BackendUnavailable, DeviceError, IterationLimitExceeded, Lo
 from .executor import (ExecutionResult, PrecisionRangeError, RnnExecutable, bind_feeds, execute,
                        execute_many, lower)
 from .autodiff import NotDifferentiable, gradient
+from .sexpr import SexprError, from_sexpr, to_sexpr
 from .values import DeviceTensor, TensorValue, allclose, max_rel_error
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BackendUnavailable", "DeviceError", "DeviceTensor", "ExecutionResult", "IterationLimitExceeded",
-    "LoweringError", "NotDifferentiable", "PrecisionRangeError", "RnnExecutable", "RuntimeGraphError", "SkbError",
-    "TensorValue", "ValidationError", "allclose", "bind_feeds", "execute", "execute_many", "gradient", "lower",
-    "max_rel_error",
+    "LoweringError", "NotDifferentiable", "PrecisionRangeError", "SexprError", "RnnExecutable", "RuntimeGraphError", "SkbError",
+    "TensorValue", "ValidationError", "allclose", "bind_feeds", "execute", "execute_many", "from_sexpr", "gradient", "lower",
+    "max_rel_error", "to_sexpr",
 ]
