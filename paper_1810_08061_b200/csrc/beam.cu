@@ -95,6 +95,48 @@ __global__ void dec_cell(DecodeState st, int cell, const float* __restrict__ bia
   }
 }
 
+// Row-parallel variants (H % 4 == 0, E % 4 == 0): blockIdx.y = row, float4 over
+// units, no per-element index division; same per-element arithmetic.
+__global__ void dec_gather4(DecodeState st, const float* __restrict__ emb, int R, int E, int H) {
+  const int t = *st.tstep;
+  if (st.active[t] == 0) return;
+  const int r = blockIdx.y, W = E + H;
+  const float4* e = reinterpret_cast<const float4*>(emb + (long long)st.tok[r] * E);
+  const float4* h = reinterpret_cast<const float4*>(st.h[t & 1] + (long long)r * H);
+  float4* o = reinterpret_cast<float4*>(st.xh + (long long)r * W);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < (E + H) / 4; k += gridDim.x * blockDim.x)
+    o[k] = k < E / 4 ? e[k] : h[k - E / 4];
+}
+
+__global__ void dec_cell4(DecodeState st, const float* __restrict__ bias, int R, int H) {
+  const int t = *st.tstep;
+  if (st.active[t] == 0) return;
+  const int r = blockIdx.y;
+  const float* g = st.gates + (long long)r * 4 * H;
+  const float* c = st.c[t & 1] + (long long)r * H;
+  for (int k = 4 * (blockIdx.x * blockDim.x + threadIdx.x); k < H; k += 4 * gridDim.x * blockDim.x) {
+    const float4 gi = *reinterpret_cast<const float4*>(g + k), gf = *reinterpret_cast<const float4*>(g + H + k);
+    const float4 gg = *reinterpret_cast<const float4*>(g + 2 * H + k), go = *reinterpret_cast<const float4*>(g + 3 * H + k);
+    const float4 cv = *reinterpret_cast<const float4*>(c + k);
+    float a[4][4] = {{gi.x, gi.y, gi.z, gi.w}, {gf.x, gf.y, gf.z, gf.w}, {gg.x, gg.y, gg.z, gg.w}, {go.x, go.y, go.z, go.w}};
+    if (bias) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a[q][e] += bias[q * H + k + e];
+    }
+    const float cp[4] = {cv.x, cv.y, cv.z, cv.w};
+    float cn[4], hn[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      cn[e] = sigmoidf_ref(a[1][e]) * cp[e] + sigmoidf_ref(a[0][e]) * tanhf(a[2][e]);
+      hn[e] = sigmoidf_ref(a[3][e]) * tanhf(cn[e]);
+    }
+    *reinterpret_cast<float4*>(st.cn + (long long)r * H + k) = make_float4(cn[0], cn[1], cn[2], cn[3]);
+    *reinterpret_cast<float4*>(st.hn + (long long)r * H + k) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+  }
+}
+
 // (value desc, index asc): does (va, ia) rank before (vb, ib)?
 __device__ __forceinline__ bool better(float va, int ia, float vb, int ib) {
   return va > vb || (va == vb && ia < ib);
@@ -465,11 +507,18 @@ bool enqueue_step(const skb_decode_shape* d, DecodeState& st, cublasHandle_t hb,
   const int G = d->cell == SKB_CELL_LSTM ? 4 * H : H, LT = d->max_len + 1;
   const int rows = R < 148 * 8 ? R : 148 * 8;
   prof_mark(prof_step, 0, cs);
-  dec_gather<<<rows, 128, 0, cs>>>(st, emb, R, E, H);
+  const bool v4 = (E & 3) == 0 && (H & 3) == 0 && !getenv("SKB_DEC_SCALAR");
+  if (v4)
+    dec_gather4<<<dim3(((E + H) / 4 + 127) / 128, R), 128, 0, cs>>>(st, emb, R, E, H);
+  else
+    dec_gather<<<rows, 128, 0, cs>>>(st, emb, R, E, H);
   prof_mark(prof_step, 1, cs);
   if (!gemm(hb, d->math, st.xh, w_gates, st.gates, R, G, E + H)) return false;
   prof_mark(prof_step, 2, cs);
-  dec_cell<<<148 * 8, 256, 0, cs>>>(st, d->cell, b_gates, R, H);
+  if (v4 && d->cell == SKB_CELL_LSTM)
+    dec_cell4<<<dim3((H / 4 + 127) / 128, R), 128, 0, cs>>>(st, b_gates, R, H);
+  else
+    dec_cell<<<148 * 8, 256, 0, cs>>>(st, d->cell, b_gates, R, H);
   if (!gemm(hb, d->math, st.hn, w_out, st.logits, R, V, H)) return false;
   prof_mark(prof_step, 3, cs);
   switch (K) {
