@@ -42,7 +42,7 @@ RNN_CASES = [
     {"name": "ad_rnn_break", "T": 7, "B": 2, "F": 3, "H": 4, "lens": [7, 6], "limit": None, "seed": 92,
      "note": "limit set between two iterations' sum(h*h): the loop breaks early"},
 ]
-RNN_WRT = ["h0", "w", "u", "b", "scale", "yl"]
+RNN_WRT = ["x", "h0", "w", "u", "b", "scale", "yl"]
 
 
 def to_reference(g):

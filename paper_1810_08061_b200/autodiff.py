@@ -15,9 +15,11 @@ whose result any backend executes (on the B200: the region VM, vm.py):
   the loop's captures; append-only list states (`hs.append(h)`) take their
   item adjoints from the stacked adjoint of the post-loop `ListStack`;
 * everything else follows the reference's rules (grad.py:148-290): the same
-  per-op adjoints, `_reduce_like` broadcasting limits, constant-index Index
-  rule, ListNew/ListAppend stack chains, and a gradient Cond whose branches
-  recompute the primal branch;
+  per-op adjoints, `_reduce_like` broadcasting limits, ListNew/ListAppend
+  stack chains, and a gradient Cond whose branches recompute the primal
+  branch; the Index rule is extended from a constant index into a vector to
+  any index into a tensor with a static leading dimension (so d loss / d x
+  of `x[t]` inside a loop works);
 * FuncCalls are inlined rather than turned into `<fn>_grad` functions, and an
   activity analysis skips adjoints of values that do not depend on `wrt`
   (so `x[t]` of a non-differentiated input needs no scatter rule).
@@ -342,15 +344,27 @@ class _Sweep:
         return f.op1("MatMul", [x, y], TypeSpec("f64", shape))
 
     def index(self, n, f, env, adj, dz):
-        """grad.py _index_rule: a constant index into a statically sized vector."""
+        """grad.py _index_rule (a constant index into a statically sized vector),
+        extended to any index into a tensor with a static leading dimension:
+        row r of the adjoint is Where(i == r, dz, 0)."""
         xr, ir = n.inputs
         if _key(xr) not in self.act:
             return
         shape = xr.type.shape
-        if ir.node.op != "Const" or shape is None or len(shape) != 1 or shape[0] is None:
-            raise NotDifferentiable("index gradient needs a constant index into a statically sized vector")
-        i = int(_scalar(ir.node.attrs["value"]))
-        elems = [dz if j == i else f.zeros_like(dz) for j in range(shape[0])]
+        if shape is None or len(shape) == 0 or shape[0] is None:
+            raise NotDifferentiable("index gradient needs a statically sized leading dimension")
+        if ir.node.op == "Const" and len(shape) == 1:
+            i = int(_scalar(ir.node.attrs["value"]))
+            elems = [dz if j == i else f.zeros_like(dz) for j in range(shape[0])]
+        else:
+            iv = env[_key(ir)]
+            zero = f.zeros_like(dz)
+            elems = []
+            for r in range(shape[0]):
+                # the reference wraps negative indices (tensor.py:420-430)
+                hit = f.op1("Eq", [f.op1("Mod", [iv, f.const(shape[0], "i64")], TypeSpec("i64", ())),
+                                   f.const(r, "i64")], TypeSpec("bool", ()))
+                elems.append(f.op1("Where", [hit, dz, zero], dz.type))
         lst = f.op1("ListNew", elems, TypeSpec("list", None, dz.type))
         st = f.op1("ListStack", [lst], TypeSpec(xr.type.dtype, (shape[0],) + tuple(dz.type.shape or ())))
         self.acc(adj, f, xr, env, st)
