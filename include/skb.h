@@ -266,8 +266,8 @@ int skb_stream_tile_elems(void);   /* vector elements per CTA tile (grid sizing)
 skb_status skb_stream_run(const void* prog_dev, const int32_t* extra_dev, const int64_t* w_init_dev,
                           int64_t* w_out_dev, const int64_t* bufptr_dev, const int32_t* rc_init_dev,
                           int64_t* part_dev, void* ctl_dev, int64_t n, int nwords, int nbuf, int max_ops,
-                          int max_stack, int max_temp, int64_t max_steps, int grid, int64_t smem_bytes,
-                          void* stream);
+                          int max_stack, int max_temp, int64_t max_steps, int nprog, int grid,
+                          int64_t smem_bytes, void* stream);   /* nprog: scalar instructions in prog_dev */
 
 /* ---------------------------------------------------------------------------
  * Diagnostics (GPU self-tests of the tcgen05 / DSMEM building blocks).

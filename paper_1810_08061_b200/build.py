@@ -21,6 +21,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--use_fast_math", "-Xcompiler", "-fP
          "-Xptxas", "-v", "-I", os.path.join(REPO, "include")]
 if os.environ.get("SKB_TRACE") == "1":   # clock64 role-event tracing (tools/trace_c1.py)
     FLAGS.append("-DSKB_TRACE_ENABLED")
+    FLAGS.append("-DSKB_STREAM_TIMING")    # stream kernel phase totals (tools/stream_phases.py)
 
 
 def sources() -> list[str]:

@@ -80,7 +80,15 @@ struct StreamCtl {               // device control block (host-zeroed)
   unsigned int arrive;           // grid-arrival counter (monotonic)
   unsigned int pad;
   long long max_live;            // buffer-pool high-water mark
+  long long t_scalar, t_rfin, t_vec, t_sync;   // CTA 0 clock64 totals (SKB_STREAM_TIMING builds only)
 };
+#ifdef SKB_STREAM_TIMING
+#define SKB_T0(v) const long long v = clock64()
+#define SKB_TADD(field, t0) do { if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->field += clock64() - (t0); } while (0)
+#else
+#define SKB_T0(v) do {} while (0)
+#define SKB_TADD(field, t0) do {} while (0)
+#endif
 
 struct StreamArgs {
   const SIns* prog;
@@ -99,6 +107,7 @@ struct StreamArgs {
   int max_ops;                   // staged operands per group
   long long smem;                // dynamic shared memory bytes of the launch
   long long max_steps;
+  int nprog;                     // scalar instructions (copied into shared memory when they fit)
 };
 
 struct Smem {                    // carved from dynamic shared memory
@@ -114,7 +123,9 @@ struct Smem {                    // carved from dynamic shared memory
   long long* stk;                // [max_stack][TILE] spilled stack entries
   uint32_t* uses;                // completed phases per stage mbarrier
   long long* red;                // [TPB/32][RMAX]
+  const SIns* prog;              // the scalar program (shared-memory copy, or global)
 };
+constexpr int kProgSmemMax = 32 * 1024;   // scalar programs up to this size run from shared memory
 
 struct Ctl {                     // per-CTA scalar-phase state (shared)
   int pc, halt, nfree, barrier_gen;
@@ -255,7 +266,7 @@ __device__ int scalar_run(const StreamArgs& a, Smem& s, Ctl& c) {
   Scalar S{a, s, c};
   long long* W = s.W;
   for (;;) {
-    const SIns in = a.prog[c.pc];
+    const SIns in = s.prog[c.pc];
     if (++c.steps > a.max_steps) { report(a.ctl, c.pc, E_STEPS, c.steps); c.halt = 1; return S_HALT; }
     int next = c.pc + 1;
     int fail = 0;
@@ -726,6 +737,10 @@ __global__ void __launch_bounds__(TPB, 1) stream_kernel(StreamArgs a) {
     s.W = reinterpret_cast<long long*>(take(sizeof(long long) * a.nwords));
     s.gptr = reinterpret_cast<long long*>(take(sizeof(long long) * 2 * kMaxGroupPtrs));
     s.red = reinterpret_cast<long long*>(take(sizeof(long long) * (TPB / 32) * RMAX));
+    // the scalar program from shared memory: the interpreter's instruction fetches sit on the
+    // serial path between vector groups (one thread, every L-BFGS iteration)
+    const size_t prog_bytes = sizeof(SIns) * (size_t)a.nprog;
+    s.prog = prog_bytes <= (size_t)kProgSmemMax ? reinterpret_cast<const SIns*>(take(prog_bytes)) : a.prog;
     s.rc = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * a.nbuf));
     s.freel = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * a.nbuf));
     // everything left of the budget stages the running group's operands
@@ -734,6 +749,11 @@ __global__ void __launch_bounds__(TPB, 1) stream_kernel(StreamArgs a) {
     s.stage_bytes = a.smem - (long long)(p - smem_raw);
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (s.prog != a.prog) {
+    int4* dst = const_cast<int4*>(reinterpret_cast<const int4*>(s.prog));
+    const int4* src = reinterpret_cast<const int4*>(a.prog);
+    for (int i = tid; i < a.nprog * (int)(sizeof(SIns) / sizeof(int4)); i += TPB) dst[i] = src[i];
+  }
   for (int i = tid; i < a.nwords; i += TPB) s.W[i] = a.w_init[i];
   for (int i = tid; i < a.nbuf; i += TPB) s.rc[i] = a.rc_init[i];
   if (tid == 0) {
@@ -755,16 +775,20 @@ __global__ void __launch_bounds__(TPB, 1) stream_kernel(StreamArgs a) {
     if (warp == 0) {
       for (;;) {
         int stop = S_HALT;
+        SKB_T0(ts0);
         if (lane == 0) stop = scalar_run(a, s, c);
+        SKB_TADD(t_scalar, ts0);
         stop = __shfl_sync(0xffffffffu, stop, 0);
         __syncwarp();
         if (stop != S_RFIN) break;
         // RFIN: a0 dst word, a1 reduction index, a2 kind|dt<<4, a3 wait flag
-        const SIns in = a.prog[c.pc];
+        const SIns in = s.prog[c.pc];
         if (in.a[3]) {
           if (lane == 0) {
             const unsigned int target = (unsigned int)(c.barrier_gen) * gridDim.x;
+            SKB_T0(tr0);
             while (ld_acquire(&a.ctl->arrive) < target) {}
+            SKB_TADD(t_rfin, tr0);
           }
           __syncwarp();
           const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&a.ctl->err);
@@ -785,10 +809,10 @@ __global__ void __launch_bounds__(TPB, 1) stream_kernel(StreamArgs a) {
       }
     }
     __syncthreads();
-    if (c.halt || a.prog[c.pc].op == S_HALT) break;
+    if (c.halt || s.prog[c.pc].op == S_HALT) break;
     // VEXEC: a0 = group offset in extra
     const int pc = c.pc;
-    const Group G = decode(a.extra + a.prog[pc].a[0]);
+    const Group G = decode(a.extra + s.prog[pc].a[0]);
     bool bad = false;
     if (tid < G.nops + G.nstores) {
       const int slot = tid < G.nops ? G.op_slots[tid] : G.store_slots[tid - G.nops];
@@ -803,8 +827,10 @@ __global__ void __launch_bounds__(TPB, 1) stream_kernel(StreamArgs a) {
     for (int q = tid; q < 4 * G.ninstr; q += TPB) reinterpret_cast<int*>(s.gins)[q] = G.ins[q];
     if (__syncthreads_or(bad)) break;   // identical in every CTA: all stop here
     // 8 elements per thread when two stages of full-unit tiles fit, else half tiles
+    SKB_T0(tv0);
     if (2ll * (G.nops < 1 ? 1 : G.nops) * UNIT * 8 <= s.stage_bytes) vector_run<8>(a, s, c, G, pc);
     else vector_run<4>(a, s, c, G, pc);
+    SKB_TADD(t_vec, tv0);
     if (tid == 0) c.pc = pc + 1;
     __syncthreads();
   }
@@ -863,7 +889,7 @@ extern "C" int skb_stream_grid(int64_t smem) {
 extern "C" int skb_stream_run(const void* prog, const int32_t* extra, const int64_t* w_init, int64_t* w_out,
                               const int64_t* bufptr, const int32_t* rc_init, int64_t* part, void* ctl,
                               int64_t n, int nwords, int nbuf, int max_ops, int max_stack, int max_temp,
-                              int64_t max_steps, int grid, int64_t smem, void* stream) {
+                              int64_t max_steps, int nprog, int grid, int64_t smem, void* stream) {
   if (grid <= 0 || n <= 0 || max_stack > 3) return SKB_ERR_INVALID;
   StreamArgs a;
   a.prog = reinterpret_cast<const SIns*>(prog);
@@ -881,6 +907,7 @@ extern "C" int skb_stream_run(const void* prog, const int32_t* extra, const int6
   a.max_stack = max_stack < 1 ? 1 : max_stack;
   a.max_temp = max_temp < 1 ? 1 : max_temp;
   a.max_steps = max_steps;
+  a.nprog = nprog;
   a.smem = smem;
   if ((size_t)smem < fixed_bytes(a.max_stack, a.max_temp, nwords, nbuf) + 2ull * a.max_ops * (TILE / 2) * 8)
     return SKB_ERR_INVALID;

@@ -86,7 +86,7 @@ SIGNATURES = {
     "skb_stream_grid": (ctypes.c_int, [ctypes.c_int64]),
     "skb_stream_tile_elems": (ctypes.c_int, []),
     "skb_stream_run": (ctypes.c_int, [_VP] * 8 + [ctypes.c_int64] + [ctypes.c_int] * 5 +
-                       [ctypes.c_int64, ctypes.c_int, ctypes.c_int64, _VP]),
+                       [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _VP]),
     "skb_diag_umma_gemm": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP]),
     "skb_diag_cluster_exchange": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP, _VP, _VP]),
 }

@@ -861,7 +861,7 @@ def run(prog: StreamProgram, feeds: dict, *, stream=None, pool: Optional[int] = 
         w_in = torch.from_numpy(w).to(dev)
         w_out = torch.empty_like(w_in)
         part = torch.empty(2 * RMAX * grid, dtype=torch.int64, device=dev)
-        ctl = torch.zeros(8, dtype=torch.int64, device=dev)
+        ctl = torch.zeros(16, dtype=torch.int64, device=dev)
         ctl[0] = -1
         g = min(grid, max(1, ntiles))
         cs = torch.cuda.current_stream() if stream is None else stream
@@ -870,7 +870,7 @@ def run(prog: StreamProgram, feeds: dict, *, stream=None, pool: Optional[int] = 
         ev0.record(cs)
         rt.check(lib.skb_stream_run(rt.ptr(code), rt.ptr(extra), rt.ptr(w_in), rt.ptr(w_out), rt.ptr(bufptr),
                                     rt.ptr(rc), rt.ptr(part), rt.ptr(ctl), n, prog.nwords, nbuf, prog.max_ops,
-                                    prog.max_stack, prog.max_temp, 1 << 40, g, smem,
+                                    prog.max_stack, prog.max_temp, 1 << 40, len(prog.code), g, smem,
                                     rt.stream_handle(stream)), "skb_stream_run")
         ev1.record(cs)
         c = ctl.cpu().numpy()
@@ -884,7 +884,8 @@ def run(prog: StreamProgram, feeds: dict, *, stream=None, pool: Optional[int] = 
             _raise(prog, code_, pc, int(c[1]))
         break
     run.last = {"kernel_ms": ev0.elapsed_time(ev1), "grid": g, "smem": smem, "pool": npool, "barriers": int(c[3]), "steps": int(c[2]),
-                "max_live": int(c[5]), "n": n}
+                "max_live": int(c[5]), "n": n, "cycles_cta0": {"scalar": int(c[6]), "rfin_wait": int(c[7]),
+                                                                "vector": int(c[8])}}
     wo = w_out.cpu().numpy()
     outs = [_value(prog, s, wo, w_out, poolbuf, vec_feeds, nfeed, stride, n, shape) for s in prog.outputs]
     return outs
