@@ -41,7 +41,7 @@ __device__ __forceinline__ int padded_of(int i, int H) {   // flat index -> padd
 }
 
 // y[K,H] = relu-input z = x w1 + b1 (x: [K], w1: [H])
-__device__ void layer1(const float* x, const float* w1, const float* b1, float* z, float* a, int K, int H) {
+__device__ __forceinline__ void layer1(const float* x, const float* w1, const float* b1, float* z, float* a, int K, int H) {
   for (int i = threadIdx.x; i < K * H; i += TPB) {
     const int k = i / H, j = i % H;
     const float v = x[k] * w1[j] + b1[j];
@@ -50,7 +50,7 @@ __device__ void layer1(const float* x, const float* w1, const float* b1, float* 
   }
 }
 // z2[K,H] = a1 @ w2 + b2
-__device__ void layer2(const float* a1, const float* w2, const float* b2, float* z2, float* a2, int K, int H) {
+__device__ __forceinline__ void layer2(const float* a1, const float* w2, const float* b2, float* z2, float* a2, int K, int H) {
   for (int i = threadIdx.x; i < K * H; i += TPB) {
     const int k = i / H, j = i % H;
     float s = 0.f;
@@ -61,7 +61,7 @@ __device__ void layer2(const float* a1, const float* w2, const float* b2, float*
   }
 }
 // p[K] = a2 @ w3 + b3
-__device__ void layer3(const float* a2, const float* w3, const float* b3, float* p, int K, int H) {
+__device__ __forceinline__ void layer3(const float* a2, const float* w3, const float* b3, float* p, int K, int H) {
   for (int k = threadIdx.x; k < K; k += TPB) {
     float s = 0.f;
     for (int q = 0; q < H; ++q) s += a2[k * H + q] * w3[q];
@@ -71,7 +71,7 @@ __device__ void layer3(const float* a2, const float* w3, const float* b3, float*
 
 // Backward of the MLP for output adjoint dp[K]; writes gradients into g.
 // dz2 / dz1 scratch [K,H].  All extra operands optional (R-op reuse).
-__device__ void backward(const float* x, Theta th, const float* z1, const float* a1, const float* z2,
+__device__ __forceinline__ void backward(const float* x, Theta th, const float* z1, const float* a1, const float* z2,
                          const float* a2, const float* dp, float* dz1, float* dz2, Theta g, int K, int H) {
   for (int i = threadIdx.x; i < K * H; i += TPB) {   // dz2 = (dp w3^T) * [z2 > 0]
     const int k = i / H, j = i % H;
@@ -115,12 +115,17 @@ __device__ void backward(const float* x, Theta th, const float* z1, const float*
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(TPB) maml_task_kernel(int H, int K, int P, const float* __restrict__ theta_g,
+// HC > 0: the hidden width as a compile-time constant (every K x H / H x H loop's
+// index division becomes a multiply-shift); HC == 0: runtime width.
+template <int HC, int KC = 0>
+__global__ void __launch_bounds__(TPB) maml_task_kernel(int H_, int K_, int P, const float* __restrict__ theta_g,
                                                         const float* __restrict__ xs, const float* __restrict__ ys,
                                                         const float* __restrict__ xq, const float* __restrict__ yq,
                                                         float alpha, float* __restrict__ task_grad,
                                                         float* __restrict__ task_loss) {
   extern __shared__ float sm[];
+  const int H = HC ? HC : H_;
+  const int K = KC ? KC : K_;
   const int task = blockIdx.x;
   const int KH = K * H;
   const int PP = P + H;          // padded block (w2 rows of H + 1)
@@ -287,9 +292,11 @@ extern "C" skb_status skb_maml_meta_grad(int hidden, int shots, int tasks, const
   float* task_loss = task_grad + (size_t)tasks * P;
   const size_t sm = smem_for(hidden, shots);
   cudaStream_t cs = (cudaStream_t)stream;
-  if (cudaFuncSetAttribute(maml_task_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+  // the C5 shape (H = 40, K = 10) as compile-time constants
+  auto kern = hidden == 40 ? (shots == 10 ? maml_task_kernel<40, 10> : maml_task_kernel<40, 0>) : maml_task_kernel<0, 0>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return SKB_ERR_CUDA;
-  maml_task_kernel<<<tasks, TPB, sm, cs>>>(hidden, shots, P, theta, xs, ys, xq, yq, alpha, task_grad, task_loss);
+  kern<<<tasks, TPB, sm, cs>>>(hidden, shots, P, theta, xs, ys, xq, yq, alpha, task_grad, task_loss);
   double* part = (double*)(((uintptr_t)(task_loss + tasks) + 15) & ~(uintptr_t)15);
   maml_reduce_partial<<<dim3((P + 256) / 256, kTaskChunks), 256, 0, cs>>>(task_grad, task_loss, tasks, P, part);
   maml_reduce_final<<<(P + 256) / 256, 256, 0, cs>>>(part, tasks, P, meta_grad, mean_loss);
