@@ -516,7 +516,7 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
     return _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions)
 
 
-PIPELINE_CHUNKS = int(os.environ.get("SKB_PIPELINE_CHUNKS", "16"))   # copy/compute pipeline depth
+PIPELINE_CHUNKS = int(os.environ.get("SKB_PIPELINE_CHUNKS", "12"))   # copy/compute pipeline depth
 
 
 def _all_pinned(prog, bound) -> bool:
