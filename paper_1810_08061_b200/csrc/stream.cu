@@ -265,16 +265,21 @@ __device__ void report(StreamCtl* ctl, int pc, int code, long long detail) {
 __device__ int scalar_run(const StreamArgs& a, Smem& s, Ctl& c) {
   Scalar S{a, s, c};
   long long* W = s.W;
+  int pc = c.pc;               // program counter and step count in registers; written back on exit
+  long long steps = c.steps;
   for (;;) {
-    const SIns in = s.prog[c.pc];
-    if (++c.steps > a.max_steps) { report(a.ctl, c.pc, E_STEPS, c.steps); c.halt = 1; return S_HALT; }
-    int next = c.pc + 1;
+    const SIns in = s.prog[pc];
+    if (++steps > a.max_steps) {
+      c.pc = pc; c.steps = steps;
+      report(a.ctl, pc, E_STEPS, steps); c.halt = 1; return S_HALT;
+    }
+    int next = pc + 1;
     int fail = 0;
     long long detail = 0;
     switch (in.op) {
-      case S_HALT: return S_HALT;
-      case S_VEXEC: return S_VEXEC;
-      case S_RFIN: return S_RFIN;
+      case S_HALT: c.pc = pc; c.steps = steps; return S_HALT;
+      case S_VEXEC: c.pc = pc; c.steps = steps; return S_VEXEC;
+      case S_RFIN: c.pc = pc; c.steps = steps; return S_RFIN;
       case S_BIN: {
         bool d0 = false;
         W[in.a[0]] = binop_w(in.a[3], in.a[4], W[in.a[1]], W[in.a[2]], d0);
@@ -351,8 +356,8 @@ __device__ int scalar_run(const StreamArgs& a, Smem& s, Ctl& c) {
       case S_RAISE: fail = in.a[0]; detail = in.a[1]; break;
       default: fail = E_DTYPE + 100; break;
     }
-    if (fail) { report(a.ctl, c.pc, fail, detail); c.halt = 1; return S_HALT; }
-    c.pc = next;
+    if (fail) { c.pc = pc; c.steps = steps; report(a.ctl, pc, fail, detail); c.halt = 1; return S_HALT; }
+    pc = next;
   }
 }
 
