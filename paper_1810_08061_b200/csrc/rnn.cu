@@ -945,9 +945,16 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a)
     step += trip;
   }
 
+  // Every CTA's tcgen05.commit of a lane's last step arrives (multicast) on this CTA's
+  // hempty: wait for that phase, so no arrival is in flight to this CTA's shared memory
+  // when it exits.
+  if (warp < kLoad0 && e == 0 && step > 0) {
+    const uint32_t last = step - 1;
+    mbar_wait_cluster(&hempty[L][last & 1], (last >> 1) & 1);
+  }
   tc_fence_before();
   __syncthreads();
-  cluster_sync();   // peers' last hempty arrivals have landed before any CTA exits
+  cluster_sync();
   if (warp == kMma0) tmem_dealloc<512>(tmem);
 }
 
