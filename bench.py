@@ -321,7 +321,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="skb", choices=["skb", "reference"])
-    ap.add_argument("--problems", type=int, default=576, help="batch-32 problems per GPU per step")
+    ap.add_argument("--problems", type=int, default=1152, help="batch-32 problems per GPU per step")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
