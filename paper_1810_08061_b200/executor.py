@@ -582,45 +582,51 @@ def _run_pipelined(prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device,
     status = torch.zeros(4, dtype=torch.int32, device=device)
     step = -(-P // max(2, min(PIPELINE_CHUNKS, P // 2)))
     lens_vals = []
-    for p0 in range(0, P, step):
-        p1 = min(P, p0 + step)
-        pc = p1 - p0
-        exe = _executable(prog, weights, Bsz, T, F, H, pc, device, comp)
-        rows = slice(p0 * Bsz, p1 * Bsz)
-        chunk = [f0 if p == 0 else bind(feeds_list[p]) for p in range(p0, p1)]
-        lens_vals.extend(_source_value(prog.lens, b) for b in chunk)
+    try:
+        for p0 in range(0, P, step):
+            p1 = min(P, p0 + step)
+            pc = p1 - p0
+            exe = _executable(prog, weights, Bsz, T, F, H, pc, device, comp)
+            rows = slice(p0 * Bsz, p1 * Bsz)
+            chunk = [f0 if p == 0 else bind(feeds_list[p]) for p in range(p0, p1)]
+            lens_vals.extend(_source_value(prog.lens, b) for b in chunk)
 
-        def stack(src, dtype, shape, buf):
-            dev = buf[rows]
-            vals = [_source_value(src, b) for b in chunk]
-            run = _adjacent_run(vals, (pc * Bsz,) + shape)
-            if run is not None:   # the chunk's feeds are one contiguous host range: one DMA
-                dev.copy_(run, non_blocking=True)
+            def stack(src, dtype, shape, buf):
+                dev = buf[rows]
+                vals = [_source_value(src, b) for b in chunk]
+                run = _adjacent_run(vals, (pc * Bsz,) + shape)
+                if run is not None:   # the chunk's feeds are one contiguous host range: one DMA
+                    dev.copy_(run, non_blocking=True)
+                    return dev
+                for i, v in enumerate(vals):
+                    if not isinstance(v, torch.Tensor):
+                        v = torch.as_tensor(as_numpy(v)).to(dtype)
+                    dev[i * Bsz:(i + 1) * Bsz].copy_(v.reshape((Bsz,) + shape), non_blocking=True)
                 return dev
-            for i, v in enumerate(vals):
-                if not isinstance(v, torch.Tensor):
-                    v = torch.as_tensor(as_numpy(v)).to(dtype)
-                dev[i * Bsz:(i + 1) * Bsz].copy_(v.reshape((Bsz,) + shape), non_blocking=True)
-            return dev
-        with torch.cuda.stream(s_in):
-            x = stack(prog.x, x_dtype, (T, F), bufs["x"])
-            h0 = stack(prog.h0, torch.float32, (H,), bufs["h0"])
-            c0 = stack(prog.c0, torch.float32, (H,), bufs["c0"]) if lstm else None
-            lens = stack(prog.lens, torch.int64, (), bufs["lens"])
-            ev_in = torch.cuda.Event()
-            ev_in.record(s_in)
-        out = bufs["out"][rows]
-        comp.wait_event(ev_in)
-        with torch.cuda.stream(comp):
-            exe.run(x, h0, c0, lens, out, hT[rows] if hT is not None else None,
-                    cT[rows] if cT is not None else None, stream=comp)
-            max_len[p0:p1].copy_(exe.max_len)
-            torch.maximum(status, exe.err, out=status)
-            ev_out = torch.cuda.Event()
-            ev_out.record(comp)
-        s_out.wait_event(ev_out)
-        with torch.cuda.stream(s_out):
-            host_out[rows].copy_(out, non_blocking=True)
+            with torch.cuda.stream(s_in):
+                x = stack(prog.x, x_dtype, (T, F), bufs["x"])
+                h0 = stack(prog.h0, torch.float32, (H,), bufs["h0"])
+                c0 = stack(prog.c0, torch.float32, (H,), bufs["c0"]) if lstm else None
+                lens = stack(prog.lens, torch.int64, (), bufs["lens"])
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_in)
+            out = bufs["out"][rows]
+            comp.wait_event(ev_in)
+            with torch.cuda.stream(comp):
+                exe.run(x, h0, c0, lens, out, hT[rows] if hT is not None else None,
+                        cT[rows] if cT is not None else None, stream=comp)
+                max_len[p0:p1].copy_(exe.max_len)
+                torch.maximum(status, exe.err, out=status)
+                ev_out = torch.cuda.Event()
+                ev_out.record(comp)
+            s_out.wait_event(ev_out)
+            with torch.cuda.stream(s_out):
+                host_out[rows].copy_(out, non_blocking=True)
+    except BaseException:   # a later feed set failed to bind: drain the queued copies before raising
+        s_in.synchronize()
+        comp.synchronize()
+        s_out.synchronize()
+        raise
     # final states, trip counts and status follow the last output chunk on the copy-out stream
     s_out.wait_stream(comp)
     hT_h = torch.empty((R, H), dtype=torch.float32, pin_memory=True) if hT is not None else None

@@ -222,3 +222,27 @@ def test_pipelined_errors_and_final_states(c1_graph):
         assert np.array_equal(a.outputs[0].array, b.outputs[0].array)
     with pytest.raises(RuntimeGraphError):
         execute_many(c1_graph, pinned, host_outputs=True)
+
+
+def test_pipelined_bind_error_in_a_later_chunk(c1_graph):
+    """A feed set that fails to bind after earlier chunks were queued raises
+    MissingFeed (the queued copies are drained first) and the next call works."""
+    import torch
+    from paper_1810_08061_b200 import RuntimeGraphError, execute_many
+    feeds = _c1_problems(8, seed=8)
+    pinned = []
+    for f in feeds:
+        g = dict(f)
+        for k in ("input_data", "h0", "c0", "sequence_len"):
+            t = torch.from_numpy(np.ascontiguousarray(f[k]))
+            g[k] = (t.float() if k == "input_data" else t).pin_memory()
+        pinned.append(g)
+    broken = list(pinned)
+    broken[7] = {k: v for k, v in pinned[7].items() if k != "h0"}
+    with pytest.raises(RuntimeGraphError) as info:
+        execute_many(c1_graph, broken, host_outputs=True)
+    assert info.value.cause_kind == "MissingFeed"
+    ok = execute_many(c1_graph, pinned, host_outputs=True)
+    ref = execute_many(c1_graph, [dict(f, input_data=f["input_data"].astype(np.float32)) for f in feeds])
+    for a, b in zip(ok, ref):
+        assert np.array_equal(a.outputs[0].array, b.outputs[0].array)
