@@ -205,7 +205,23 @@ def rnn_cases():
         print(case["name"], "trips", int(base[1][0]), "autodiff vs finite differences rel err", err)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not sys.argv[1:]:
     lstm_cases()
     maml_cases()
     rnn_cases()
+
+
+def bench_graph():
+    """tests/golden/graph_lstm_loss_bench.json: the forward LSTM loss program traced
+    by the reference at the gradient-bench shape (T=16, B=32, F=H=64)."""
+    case = {"name": "bench", "T": 16, "B": 32, "F": 64, "H": 64, "lens": list(range(1, 17)) * 2, "seed": 5}
+    v = bptt_feeds(case)
+    order = ["x", "h0", "c0", "lens", "y"] + LSTM_W + ["inv_b"]
+    g = trace("lstm_loss.msl", "lstm_loss", v, order)
+    write("graph_lstm_loss_bench", {"case": case, "generator": "oracle/gen_autodiff_golden.py --bench",
+                                    "graph": json.loads(ir.to_json(g)), "order": order})
+    print("graph_lstm_loss_bench written")
+
+
+if __name__ == "__main__" and sys.argv[1:2] == ["--bench"]:
+    bench_graph()

@@ -149,11 +149,19 @@ struct Vm {
   }
   // Make sure slot `d` owns >= bytes; returns the data offset.  Only the leader
   // writes the descriptor; everyone gets the same answer.
-  __device__ int64_t own_storage(int d, int64_t bytes, VmVal& nv) {
+  // The instruction's inputs (x0..x2) must not live in that storage: threads
+  // write output elements while others still read input elements (matmul,
+  // transpose, broadcasts, scalars), so an aliased input gets fresh storage.
+  __device__ int64_t own_storage(int d, int64_t bytes, VmVal& nv, const VmVal* x0 = nullptr,
+                                 const VmVal* x1 = nullptr, const VmVal* x2 = nullptr) {
     const VmVal cur = S(d);
     int64_t off = cur.own;
     int64_t cap = cur.own_cap;
-    if (off < 0 || cap < bytes) {
+    auto aliased = [&](const VmVal* x) {
+      return x != nullptr && x->dtype != DT_LIST && x->dtype != DT_TREE && off >= 0 && x->view >= off &&
+             x->view < off + cap;
+    };
+    if (off < 0 || cap < bytes || aliased(x0) || aliased(x1) || aliased(x2)) {
       cap = bytes < 64 ? 64 : bytes;
       off = alloc(cap);
     }
@@ -215,7 +223,7 @@ __device__ void op_copy(Vm& vm, const VmIns& in) {
     vm.commit(d, c);
     return;
   }
-  const int64_t off = vm.own_storage(d, src.numel * 8, nv);
+  const int64_t off = vm.own_storage(d, src.numel * 8, nv, &src);
   nv.numel = src.numel; nv.dtype = src.dtype; nv.rank = src.rank;
   for (int i = 0; i < kMaxRank; ++i) nv.shape[i] = src.shape[i];
   const int64_t* sp = reinterpret_cast<const int64_t*>(vm.P(src.view));
@@ -242,7 +250,7 @@ __device__ void op_binop(Vm& vm, const VmIns& in) {
   }
   const int64_t n = numel_of(shape, rank);
   VmVal nv = vm.S(d);
-  const int64_t off = vm.own_storage(d, n * 8, nv);
+  const int64_t off = vm.own_storage(d, n * 8, nv, &A, &B);
   nv.numel = n; nv.dtype = out_dt; nv.rank = rank;
   for (int i = 0; i < kMaxRank; ++i) nv.shape[i] = i < rank ? shape[i] : 0;
   BIdx ba, bb;
@@ -321,7 +329,7 @@ __device__ void op_matmul(Vm& vm, const VmIns& in) {   // reference tensor.py:30
   const int n = A.shape[0], k = A.shape[1], m = B.shape[1];
   if (B.shape[0] != k) { vm.fail(E_SHAPE, in.uid, 1); return; }
   VmVal nv = vm.S(d);
-  const int64_t off = vm.own_storage(d, (int64_t)n * m * 8, nv);
+  const int64_t off = vm.own_storage(d, (int64_t)n * m * 8, nv, &A, &B);
   nv.numel = (int64_t)n * m; nv.dtype = out_dt; nv.rank = 2;
   nv.shape[0] = n; nv.shape[1] = m;
   for (int i = 2; i < kMaxRank; ++i) nv.shape[i] = 0;
@@ -353,7 +361,7 @@ __device__ void op_transpose(Vm& vm, const VmIns& in) {   // reference tensor.py
   int32_t shape[kMaxRank];
   for (int i = 0; i < A.rank; ++i) shape[i] = A.shape[perm[i]];
   VmVal nv = vm.S(d);
-  const int64_t off = vm.own_storage(d, A.numel * 8, nv);
+  const int64_t off = vm.own_storage(d, A.numel * 8, nv, &A);
   nv.numel = A.numel; nv.dtype = A.dtype; nv.rank = A.rank;
   for (int i = 0; i < kMaxRank; ++i) nv.shape[i] = i < A.rank ? shape[i] : 0;
   int64_t sstride[kMaxRank], ostride[kMaxRank];
@@ -380,7 +388,7 @@ __device__ void op_reduce(Vm& vm, const VmIns& in) {   // reference tensor.py:33
   const VmVal A = vm.S(in.a[1]);
   if (is_max && A.numel == 0) { vm.fail(E_SHAPE, in.uid, 0); return; }
   VmVal nv = vm.S(d);
-  const int64_t off = vm.own_storage(d, 8, nv);
+  const int64_t off = vm.own_storage(d, 8, nv, &A);
   nv.numel = 1; nv.dtype = A.dtype; nv.rank = 0;
   for (int i = 0; i < kMaxRank; ++i) nv.shape[i] = 0;
   const uint8_t* pa = vm.P(A.view);
@@ -463,7 +471,7 @@ __device__ void op_where(Vm& vm, const VmIns& in) {   // reference tensor.py:356
   else if (Cn.rank == 1 && A.rank >= 1 && Cn.shape[0] == A.shape[0]) mode = 2;
   else { vm.fail(E_SHAPE, in.uid, 1); return; }
   VmVal nv = vm.S(d);
-  const int64_t off = vm.own_storage(d, A.numel * 8, nv);
+  const int64_t off = vm.own_storage(d, A.numel * 8, nv, &Cn, &A, &B);
   nv.numel = A.numel; nv.dtype = A.dtype; nv.rank = A.rank;
   for (int i = 0; i < kMaxRank; ++i) nv.shape[i] = A.shape[i];
   const int64_t row = mode == 2 ? (A.shape[0] ? A.numel / A.shape[0] : 0) : 1;
@@ -505,7 +513,7 @@ __device__ void op_range(Vm& vm, const VmIns& in) {   // reference tensor.py:414
   const int64_t n = ld_i(vm.P(N.view), 0);
   if (n < 0) { vm.fail(E_SHAPE, in.uid, n); return; }
   VmVal nv = vm.S(d);
-  const int64_t off = vm.own_storage(d, n * 8, nv);
+  const int64_t off = vm.own_storage(d, n * 8, nv, &N);
   nv.numel = n; nv.dtype = DT_I64; nv.rank = 1;
   nv.shape[0] = (int32_t)n;
   for (int i = 1; i < kMaxRank; ++i) nv.shape[i] = 0;
@@ -523,7 +531,7 @@ __device__ void op_index(Vm& vm, const VmIns& in) {   // reference tensor.py:420
   if (i < 0) i += n;
   const int64_t row = n ? A.numel / n : 0;
   VmVal nv = vm.S(d);
-  const int64_t off = vm.own_storage(d, row * 8, nv);
+  const int64_t off = vm.own_storage(d, row * 8, nv, &A, &I);
   nv.numel = row; nv.dtype = A.dtype; nv.rank = A.rank - 1;
   for (int k = 0; k < kMaxRank; ++k) nv.shape[k] = k + 1 < A.rank ? A.shape[k + 1] : 0;
   const int64_t* pa = reinterpret_cast<const int64_t*>(vm.P(A.view)) + i * row;
@@ -577,9 +585,12 @@ __device__ void op_list_new(Vm& vm, const VmIns& in) {
 __device__ void op_list_append(Vm& vm, const VmIns& in) {   // reference execute.py:153-156
   const int d = in.a[0];
   const VmVal L = vm.S(in.a[1]);
-  const VmVal item = snapshot(vm, vm.S(in.a[2]));
+  // Every thread must see the header before the leader bumps its high-water mark below,
+  // or threads disagree on copy-on-write and their bump allocators diverge.
   const int64_t* hdr = reinterpret_cast<const int64_t*>(vm.P(L.view - 16));
   const int64_t cap = hdr[0], hw = hdr[1];
+  const VmVal item = snapshot(vm, vm.S(in.a[2]));
+  vm.sync();
   int64_t arr = L.view;
   if (L.numel != hw || L.numel >= cap) {   // copy-on-write / grow
     const int64_t ncap = L.numel + 1 > cap ? 2 * cap : cap;

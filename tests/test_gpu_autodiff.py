@@ -35,3 +35,35 @@ def test_gradient_through_while_on_device(name):
         assert close(a, b, 1e-9)
     if "trips" in d:
         assert int(outs[1][0]) == d["trips"]
+
+
+def test_gradient_medium_shape_matches_bptt_oracle():
+    """The automatic BPTT of the staged LSTM loss at T=16, B=32, F=H=64
+    (tests/golden/graph_lstm_loss_bench.json, traced by the reference) on the
+    region VM against the float64 BPTT restatement (oracle/bptt.py, pinned to
+    the reference's hand-written BPTT program) — all 12 gradients, run three
+    times: this shape once exposed a VM list-append race (threads disagreeing
+    on copy-on-write) that the tiny fixtures did not."""
+    from oracle import bptt, fixtures
+    from oracle.gen_stream_golden import bptt_feeds
+    from paper_1810_08061_b200 import ir
+    doc = fixtures.load_golden("graph_lstm_loss_bench")
+    g = ir.from_json(doc["graph"])
+    wrt = [f"{k}{q}" for q in "ifgo" for k in "wub"]
+    gg = gradient(g, 0, wrt)
+    v = bptt_feeds(doc["case"])
+    feeds = {k: np.asarray(v[k]) for k in doc["order"]}
+    W = np.concatenate([v["w" + q] for q in "ifgo"], axis=1)
+    U = np.concatenate([v["u" + q] for q in "ifgo"], axis=1)
+    b = np.concatenate([v["b" + q][0] for q in "ifgo"])
+    loss, dW, dU, db = bptt.forward_backward(np.transpose(v["x"], (1, 0, 2)), v["h0"], v["c0"], v["lens"],
+                                             np.transpose(v["y"], (1, 0, 2)), W, U, b, float(v["inv_b"]))
+    H = v["h0"].shape[1]
+    for _ in range(3):
+        outs = [_arr(o) for o in execute(gg, feeds).outputs]
+        assert abs(outs[0][0] - loss) < 1e-12
+        for k in range(4):
+            assert np.allclose(outs[1 + 3 * k].reshape(-1, H), dW[:, k * H:(k + 1) * H], rtol=1e-9, atol=1e-12)
+            assert np.allclose(outs[2 + 3 * k].reshape(H, H), dU[:, k * H:(k + 1) * H], rtol=1e-9, atol=1e-12)
+            assert np.allclose(outs[3 + 3 * k].reshape(-1, H).sum(axis=0), db[k * H:(k + 1) * H], rtol=1e-9,
+                               atol=1e-12)
