@@ -129,14 +129,42 @@ def run(args, rank, world, local_rank, clocks_cls):
                 "flop_basis": "3 * 2*B*n*(F+H)*4H padded to the trip count n",
                 "peak_source": f"{src} dense bf16 sustained"}
     # e2e: host x / y / lens every step, loss back to the host
+    # Two device input buffer sets, reused across steps as a training loop does (the captured
+    # step graph is keyed by their addresses); the H2D copy of step k+1 runs on a copy stream
+    # while step k computes, and every step's loss is read back on the host.
     hx, hy, hl = x.cpu().pin_memory(), y.cpu().pin_memory(), lens.cpu().pin_memory()
+    bufs = [(torch.empty_like(x), torch.empty_like(y), torch.empty_like(lens)) for _ in range(2)]
+    comp, cp = torch.cuda.current_stream(), torch.cuda.Stream()
+    done = [None, None]   # event: the step that last used buffer set j finished
     ke = max(1, min(args.steps, 3))
+
+    def copy_in(j):
+        with torch.cuda.stream(cp):
+            if done[j] is not None:
+                cp.wait_event(done[j])
+            for d_, h_ in zip(bufs[j], (hx, hy, hl)):
+                d_.copy_(h_, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cp)
+        return ev
+
+    def run_steps(count):
+        lv = None
+        ready = copy_in(0)
+        for k in range(count):
+            j = k & 1
+            comp.wait_event(ready)
+            loss = tr.step(*bufs[j], max_len=n)
+            done[j] = torch.cuda.Event()
+            done[j].record(comp)
+            if k + 1 < count:
+                ready = copy_in(j ^ 1)
+            lv = float(loss.item())
+        return lv
+    run_steps(4)   # each buffer set seen twice: both step graphs captured before timing
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(ke):
-        dx, dy, dl = hx.to(dev, non_blocking=True), hy.to(dev, non_blocking=True), hl.to(dev, non_blocking=True)
-        loss = tr.step(dx, dy, dl, max_len=n)
-        lv = float(loss.item())
+    lv = run_steps(ke)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / ke
     dt_t = torch.tensor([dt], device=dev)
