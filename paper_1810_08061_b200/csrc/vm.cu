@@ -168,6 +168,11 @@ struct Vm {
     nv.own = off;
     nv.own_cap = cap;
     nv.view = off;
+    // Every thread has read this instruction's slot descriptors (inputs, and S(d) above)
+    // before the leader can commit the output descriptor at the end of the op: without
+    // this barrier a lagging thread (or CTA, in grid mode) could read the new descriptor,
+    // take the other allocation branch and desynchronise the replicated bump allocator.
+    sync();
     return off;
   }
   __device__ void commit(int d, const VmVal& nv) const {

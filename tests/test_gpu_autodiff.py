@@ -67,3 +67,46 @@ def test_gradient_medium_shape_matches_bptt_oracle():
             assert np.allclose(outs[2 + 3 * k].reshape(H, H), dU[:, k * H:(k + 1) * H], rtol=1e-9, atol=1e-12)
             assert np.allclose(outs[3 + 3 * k].reshape(-1, H).sum(axis=0), db[k * H:(k + 1) * H], rtol=1e-9,
                                atol=1e-12)
+
+
+@pytest.mark.parametrize("shape", [(16, 64, 64, 64), (8, 128, 64, 64)], ids=["T16B64", "T8B128"])
+def test_gradient_grid_mode_matches_bptt_oracle(shape):
+    """Tensors of >= 64 K elements run the region VM as a grid of CTAs: the
+    traced 4x3 LSTM-loss graph with its shapes relaxed, at a larger shape, run
+    twice against the f64 BPTT oracle (this once exposed cross-CTA descriptor
+    races in the VM)."""
+    from oracle import bptt
+    from paper_1810_08061_b200.ir import TypeSpec
+    d = load("ad_lstm_4x3")
+    g = d["graph_obj"]
+
+    def relax(t):
+        if t is None or t.dtype == "tree":
+            return t
+        if t.dtype == "list":
+            return TypeSpec("list", None, relax(t.elem))
+        return t if t.shape in ((), None) else TypeSpec(t.dtype, tuple(None for _ in t.shape))
+    for n in g.iter_nodes():
+        n.out_types = [relax(t) for t in n.out_types]
+    gg = gradient(g, 0, d["wrt"])
+    T, B, F, H = shape
+    rng = np.random.default_rng(11)
+    v = {"x": rng.uniform(-1, 1, (T, B, F)), "h0": rng.uniform(-.5, .5, (B, H)), "c0": rng.uniform(-.5, .5, (B, H)),
+         "lens": rng.integers(0, T + 1, B).astype(np.int64), "y": rng.uniform(-1, 1, (T, B, H))}
+    v["lens"][0] = T
+    for q in "ifgo":
+        v["w" + q] = rng.uniform(-1, 1, (F, H))
+        v["u" + q] = rng.uniform(-1, 1, (H, H))
+        v["b" + q] = np.broadcast_to(rng.uniform(-.5, .5, (1, H)), (B, H)).copy()
+    v["inv_b"] = np.float64(1.0 / B)
+    W = np.concatenate([v["w" + q] for q in "ifgo"], axis=1)
+    U = np.concatenate([v["u" + q] for q in "ifgo"], axis=1)
+    b = np.concatenate([v["b" + q][0] for q in "ifgo"])
+    loss, dW, dU, _ = bptt.forward_backward(np.transpose(v["x"], (1, 0, 2)), v["h0"], v["c0"], v["lens"],
+                                            np.transpose(v["y"], (1, 0, 2)), W, U, b, float(v["inv_b"]))
+    for _ in range(2):
+        outs = [_arr(o) for o in execute(gg, v, check=False).outputs]
+        assert abs(outs[0][0] - loss) < 1e-9 * max(1.0, abs(loss))
+        for k in range(4):
+            assert np.allclose(outs[1 + 3 * k].reshape(F, H), dW[:, k * H:(k + 1) * H], rtol=1e-9, atol=1e-11)
+            assert np.allclose(outs[2 + 3 * k].reshape(H, H), dU[:, k * H:(k + 1) * H], rtol=1e-9, atol=1e-11)
