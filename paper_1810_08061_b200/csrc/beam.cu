@@ -303,42 +303,35 @@ __global__ void __launch_bounds__(SEL_THREADS) beam_choose(DecodeState st, int S
   const int s = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nxt = cur ^ 1;
-  if (warp == 0) {
-    double cs[2];
-    int ci[2];   // flat index b*V + v
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int slot = lane + 32 * q;   // K*K <= 64
-      cs[q] = -INFINITY; ci[q] = 0x7fffffff;
-      if (slot < K * K) {
-        const int b = slot / K, k = slot % K, r = s * K + b;
-        const double sc = st.score[cur][r];
-        if (st.fin[cur][r]) {
-          if (k == 0) { cs[q] = sc; ci[q] = b * V + eos; }
-        } else {
-          const int v = st.row_i[(long long)r * KMAX + k];
-          if (v != 0x7fffffff) {
-            ci[q] = b * V + v;
-            if (sc != -INFINITY) cs[q] = sc + ((double)st.row_v[(long long)r * KMAX + k] - (double)st.row_lse[r]);
-          }
-        }
+  // K*K <= 64 candidates, one per thread of the first two warps; a candidate's rank is
+  // the number of candidates that order before it (score desc, flat index asc: a total
+  // order, so ranks are distinct) and the K best write themselves to slots 0..K-1.
+  __shared__ double cand_s[KMAX * KMAX];
+  __shared__ int cand_i[KMAX * KMAX];
+  const int slot = threadIdx.x;
+  double cs = -INFINITY;
+  int ci = 0x7fffffff;   // flat index b*V + v
+  if (slot < K * K) {
+    const int b = slot / K, k = slot % K, r = s * K + b;
+    const double sc = st.score[cur][r];
+    if (st.fin[cur][r]) {
+      if (k == 0) { cs = sc; ci = b * V + eos; }
+    } else {
+      const int v = st.row_i[(long long)r * KMAX + k];
+      if (v != 0x7fffffff) {
+        ci = b * V + v;
+        if (sc != -INFINITY) cs = sc + ((double)st.row_v[(long long)r * KMAX + k] - (double)st.row_lse[r]);
       }
     }
-    for (int j = 0; j < K; ++j) {
-      double bv = cs[0];
-      int bi = ci[0], bq = 0;
-      if (better_d(cs[1], ci[1], bv, bi)) { bv = cs[1]; bi = ci[1]; bq = 1; }
-      int bl = lane;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        const int ol = __shfl_xor_sync(0xffffffffu, bl, o), oq = __shfl_xor_sync(0xffffffffu, bq, o);
-        if (better_d(ov, oi, bv, bi)) { bv = ov; bi = oi; bl = ol; bq = oq; }
-      }
-      if (lane == 0) { sel_score[j] = bv; sel_par[j] = bi / V; sel_tok[j] = bi % V; }
-      if (lane == bl) { cs[bq] = -INFINITY; ci[bq] = 0x7fffffff; }
-    }
+    cand_s[slot] = cs;
+    cand_i[slot] = ci;
+  }
+  __syncthreads();
+  if (slot < K * K) {
+    int rank = 0;
+#pragma unroll 8
+    for (int o = 0; o < K * K; ++o) rank += better_d(cand_s[o], cand_i[o], cs, ci) ? 1 : 0;
+    if (rank < K) { sel_score[rank] = cs; sel_par[rank] = ci / V; sel_tok[rank] = ci % V; }
   }
   __syncthreads();
   // reindex: beam j of the next step continues parent p = sel_par[j]
