@@ -351,7 +351,10 @@ class _Reader:
 
 def from_sexpr(text: str) -> Graph:
     """Reference s-expression program (sexpr.py:4-21) -> executable skb Graph."""
-    return _Reader(parse(text)).read()
+    try:
+        return _Reader(parse(text)).read()
+    except RecursionError:   # the reader recurses once per nesting level, like the emitter
+        raise SexprError("s-expression nested deeper than the reader's recursion limit") from None
 
 
 # ------------------------------------------------------------------ writer
