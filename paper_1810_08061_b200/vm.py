@@ -27,6 +27,7 @@ print log and device errors (node uid -> span, reference cause_kind) back.
 
 from __future__ import annotations
 
+import os
 import math
 from dataclasses import dataclass, field
 from typing import Optional
@@ -416,7 +417,7 @@ def run(prog: Program, feeds: dict, *, stream=None, arena_bytes: Optional[int] =
         extra = torch.from_numpy(np.asarray(prog.extra + [0], dtype=np.int32)).to(dev)
         dslots = torch.from_numpy(slots.view(np.uint8).copy()).to(dev)
         ctas = 1
-        if big >= 1 << 16:
+        if big >= int(os.environ.get("SKB_VM_GRID_MIN", 1 << 13)):   # grid of CTAs from 8 K-element tensors
             ctas = max(1, int(lib.skb_vm_max_ctas()))
         scratch = torch.zeros(2 * max(ctas, 1), dtype=torch.float64, device=dev)
         tv = torch.tensor(trees.val + [0.0], dtype=torch.float64, device=dev)
