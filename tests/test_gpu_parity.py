@@ -246,3 +246,33 @@ def test_pipelined_bind_error_in_a_later_chunk(c1_graph):
     ref = execute_many(c1_graph, [dict(f, input_data=f["input_data"].astype(np.float32)) for f in feeds])
     for a, b in zip(ok, ref):
         assert np.array_equal(a.outputs[0].array, b.outputs[0].array)
+
+
+@pytest.mark.parametrize("H", [32, 64, 128])
+def test_dual_lane_kernel_widths_against_oracle(c1_graph, H):
+    """The dual-lane kernel at cluster sizes 1, 2 and 4 (H = 32 C units) vs the
+    float64 C oracle on 4 problems of 32 rows x 64 steps, F = H."""
+    import torch
+    from paper_1810_08061_b200 import lower, max_rel_error
+    from paper_1810_08061_b200.executor import RnnExecutable
+    B, T, F, P = 32, 64, H, 4
+    rng = np.random.default_rng(H)
+    W = [rng.uniform(-0.1, 0.1, (F, H)) for _ in range(4)]
+    U = [rng.uniform(-0.1, 0.1, (H, H)) for _ in range(4)]
+    b = [rng.uniform(-0.1, 0.1, (H,)) for _ in range(4)]
+    R = P * B
+    x = rng.uniform(-1, 1, (R, T, F))
+    h0, c0 = rng.uniform(-0.1, 0.1, (R, H)), rng.uniform(-0.1, 0.1, (R, H))
+    lens = rng.integers(1, T + 1, R).astype(np.int64)
+    exe = RnnExecutable(lower(c1_graph), [(W[i], U[i], b[i]) for i in range(4)], B, T, F, H, P)
+    dev = torch.device("cuda")
+    out = torch.empty((R, T, H), device=dev)
+    exe.run(torch.tensor(x, dtype=torch.float32, device=dev), torch.tensor(h0, dtype=torch.float32, device=dev),
+            torch.tensor(c0, dtype=torch.float32, device=dev), torch.tensor(lens, device=dev), out)
+    torch.cuda.synchronize()
+    ref, ml, st = oracle.rnn_many(1, x, h0, c0, lens, W, U, b, P, 4)
+    got = out.cpu().numpy().astype(np.float64)
+    for p in range(P):
+        m = int(ml[p])
+        r = ref.reshape(P, B * T * H)[p, :B * m * H].reshape(B, m, H)
+        assert max_rel_error(got[p * B:(p + 1) * B, :m], r) <= TOL

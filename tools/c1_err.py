@@ -13,9 +13,10 @@ from oracle.fixtures import load_graph_fixture  # noqa: E402
 from paper_1810_08061_b200 import lower  # noqa: E402
 from paper_1810_08061_b200.executor import RnnExecutable  # noqa: E402
 
-B, T, F, H = 32, 64, 256, 256
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 scale = float(sys.argv[2]) if len(sys.argv) > 2 else 0.1
+H = int(sys.argv[3]) if len(sys.argv) > 3 else 256
+B, T, F = 32, 64, H
 R = P * B
 g, _ = load_graph_fixture("graph_lstm_c1")
 prog = lower(g)
@@ -40,4 +41,4 @@ for p in range(P):
     m = int(ml[p])
     a, r = got[p * B:(p + 1) * B, :m], ref.reshape(P, B * T * H)[p, :B * m * H].reshape(B, m, H)
     errs.append(float(np.max(np.abs(a - r) / np.maximum(1, np.maximum(np.abs(a), np.abs(r))))))
-print(f"act={os.environ.get('SKB_RNN_ACT', '1 (default)')} scale={scale} max rel err {max(errs):.3e} mean {np.mean(errs):.3e}")
+print(f"H={H} act={os.environ.get('SKB_RNN_ACT', '1 (default)')} scale={scale} max rel err {max(errs):.3e} mean {np.mean(errs):.3e}")
