@@ -122,12 +122,13 @@ skb_status skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_dev,
  *   scratch_dev: 2*ctas doubles;  tree_*: tree node table (NaN value = empty)
  *   log_dev: print records (log_cap x 64 bytes);  ctl_dev: 8 x int64 control
  *            block {err | uid<<32, detail, arena_used, log_count, steps}
- * ctas == 1 runs one CTA (block barriers); > 1 a cooperative grid. */
+ * ctas == 1 runs one CTA (block barriers); > 1 a cooperative grid.  slots_dev holds one copy of
+ * the nslots descriptors per CTA (ctas x nslots; results are read from copy 0). */
 skb_status skb_vm_run(const void* prog_dev, const int32_t* extra_dev, void* slots_dev, void* arena_dev,
                       int64_t arena_bytes, int64_t arena_start, double* scratch_dev,
                       const double* tree_val_dev, const int32_t* tree_left_dev,
                       const int32_t* tree_right_dev, int64_t* log_dev, int64_t log_cap, void* ctl_dev,
-                      int64_t max_steps, int ctas, void* stream);
+                      int64_t max_steps, int ctas, int nslots, void* stream);
 /* Largest cooperative grid (CTAs) the VM kernel can use on this device. */
 int skb_vm_max_ctas(void);
 

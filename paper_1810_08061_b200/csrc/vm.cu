@@ -81,6 +81,7 @@ struct VmArgs {
   int64_t log_cap;
   VmCtl* ctl;
   int64_t max_steps;
+  int nslots;             // slots per CTA: every CTA of a grid keeps its own copy of the table
 };
 
 struct Sync {
@@ -135,7 +136,9 @@ struct Vm {
   Sync sync;
   int64_t bump;           // identical in every thread
 
-  __device__ VmVal& S(int i) const { return a.slots[i]; }
+  // Slot descriptors: a private copy per CTA (every CTA computes the same values), so an
+  // op's descriptor reads only race with its own CTA's commit (block barrier, not grid).
+  __device__ VmVal& S(int i) const { return a.slots[(int64_t)blockIdx.x * a.nslots + i]; }
   __device__ uint8_t* P(int64_t off) const { return a.arena + off; }
 
   __device__ void fail(int code, int uid, int64_t detail) const {
@@ -169,14 +172,15 @@ struct Vm {
     nv.own_cap = cap;
     nv.view = off;
     // Every thread has read this instruction's slot descriptors (inputs, and S(d) above)
-    // before the leader can commit the output descriptor at the end of the op: without
-    // this barrier a lagging thread (or CTA, in grid mode) could read the new descriptor,
-    // take the other allocation branch and desynchronise the replicated bump allocator.
-    sync();
+    // before its CTA's leader commits the output descriptor at the end of the op: without
+    // this barrier a lagging thread could read the new descriptor, take the other
+    // allocation branch and desynchronise the replicated bump allocator.  (Tables are
+    // per CTA, so a block barrier suffices in grid mode too.)
+    __syncthreads();
     return off;
   }
   __device__ void commit(int d, const VmVal& nv) const {
-    if (leader()) S(d) = nv;
+    if (threadIdx.x == 0) S(d) = nv;   // each CTA's own table
   }
 };
 
@@ -653,7 +657,7 @@ __device__ void op_list_pop(Vm& vm, const VmIns& in) {
   nl.view = L.view; nl.numel = L.numel - 1; nl.dtype = DT_LIST; nl.rank = 0;
   const VmVal cur = vm.S(di);
   it.own = cur.own; it.own_cap = cur.own_cap;
-  if (leader()) { vm.S(dl) = nl; vm.S(di) = it; }
+  if (threadIdx.x == 0) { vm.S(dl) = nl; vm.S(di) = it; }
 }
 
 __device__ void op_list_stack(Vm& vm, const VmIns& in) {   // reference execute.py:171-184
@@ -727,7 +731,7 @@ __global__ void __launch_bounds__(256) vm_kernel(VmArgs a, int grid_sync) {
       }
       case OP_SWAP: {
         const VmVal x = vm.S(in.a[0]), y = vm.S(in.a[1]);
-        if (leader()) { vm.S(in.a[0]) = y; vm.S(in.a[1]) = x; }
+        if (threadIdx.x == 0) { vm.S(in.a[0]) = y; vm.S(in.a[1]) = x; }
         break;
       }
       case OP_BINOP: op_binop(vm, in); break;
@@ -803,7 +807,7 @@ extern "C" int skb_vm_run(const void* prog, const int32_t* extra, void* slots, v
                           int64_t arena_bytes, int64_t arena_start, double* scratch,
                           const double* tree_val, const int32_t* tree_left, const int32_t* tree_right,
                           int64_t* log, int64_t log_cap, void* ctl, int64_t max_steps, int ctas,
-                          void* stream) {
+                          int nslots, void* stream) {
   VmArgs a;
   a.prog = reinterpret_cast<const VmIns*>(prog);
   a.extra = extra;
@@ -816,6 +820,7 @@ extern "C" int skb_vm_run(const void* prog, const int32_t* extra, void* slots, v
   a.log = log; a.log_cap = log_cap;
   a.ctl = reinterpret_cast<VmCtl*>(ctl);
   a.max_steps = max_steps;
+  a.nslots = nslots;
   cudaStream_t st = (cudaStream_t)stream;
   if (ctas <= 1) {
     vm_kernel<<<1, 256, 0, st>>>(a, 0);

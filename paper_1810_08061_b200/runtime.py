@@ -65,7 +65,7 @@ SIGNATURES = {
     "skb_profile_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float), ctypes.c_int]),
     "skb_profile_end": (ctypes.c_int, []),
     "skb_vm_run": (ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int64, ctypes.c_int64, _VP, _VP, _VP, _VP,
-                                   _VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int, _VP]),
+                                   _VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _VP]),
     "skb_vm_max_ctas": (ctypes.c_int, []),
     "skb_decode_workspace_bytes": (ctypes.c_int64, [ctypes.POINTER(DecodeShape)]),
     "skb_decode_profile": (ctypes.c_int, [ctypes.c_int]),

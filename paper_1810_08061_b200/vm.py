@@ -415,10 +415,11 @@ def run(prog: Program, feeds: dict, *, stream=None, arena_bytes: Optional[int] =
         arena[:static_bytes].copy_(torch.from_numpy(host.view(np.uint8)[:static_bytes]))
         code = torch.from_numpy(np.asarray(prog.code, dtype=np.int32).reshape(-1)).to(dev)
         extra = torch.from_numpy(np.asarray(prog.extra + [0], dtype=np.int32)).to(dev)
-        dslots = torch.from_numpy(slots.view(np.uint8).copy()).to(dev)
         ctas = 1
         if big >= int(os.environ.get("SKB_VM_GRID_MIN", 1 << 13)):   # grid of CTAs from 8 K-element tensors
             ctas = max(1, int(lib.skb_vm_max_ctas()))
+        # one copy of the slot table per CTA (results are read from copy 0)
+        dslots = torch.from_numpy(np.tile(slots.view(np.uint8), ctas)).to(dev)
         scratch = torch.zeros(2 * max(ctas, 1), dtype=torch.float64, device=dev)
         tv = torch.tensor(trees.val + [0.0], dtype=torch.float64, device=dev)
         tl = torch.tensor(trees.left + [0], dtype=torch.int32, device=dev)
@@ -428,7 +429,7 @@ def run(prog: Program, feeds: dict, *, stream=None, arena_bytes: Optional[int] =
         ctl = torch.zeros(8, dtype=torch.int64, device=dev)
         rt.check(lib.skb_vm_run(rt.ptr(code), rt.ptr(extra), rt.ptr(dslots), rt.ptr(arena), arena_bytes,
                                 static_bytes, rt.ptr(scratch), rt.ptr(tv), rt.ptr(tl), rt.ptr(tr), rt.ptr(log),
-                                log_cap, rt.ptr(ctl), 1 << 40, ctas, rt.stream_handle(stream)), "skb_vm_run")
+                                log_cap, rt.ptr(ctl), 1 << 40, ctas, len(slots), rt.stream_handle(stream)), "skb_vm_run")
         c = ctl.cpu().numpy()
         err = int(c[0] & 0xFFFFFFFF)
         if err == E_ARENA and attempt < 3:
@@ -445,7 +446,7 @@ def run(prog: Program, feeds: dict, *, stream=None, arena_bytes: Optional[int] =
         if err in CAUSE:
             raise RuntimeGraphError(_message(err, node, int(c[1])), span, CAUSE[err])
         raise E.DeviceError(f"VM failure code {err} at node {err_uid}")
-    host_slots = np.frombuffer(dslots.cpu().numpy().tobytes(), dtype=VAL_DTYPE)
+    host_slots = np.frombuffer(dslots[:slots.nbytes].cpu().numpy().tobytes(), dtype=VAL_DTYPE)
     outs = [_value(arena, host_slots[s], trees) for s in prog.outputs]
     log_count = int(c[3])
     plog = _print_log(prog, arena, log, log_count, trees) if log_count else []
