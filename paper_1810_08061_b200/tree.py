@@ -48,9 +48,10 @@ class Forest:
         sizes = np.fromiter((len(f[0]) for f in flat), dtype=np.int64, count=len(flat))
         bases = np.concatenate([[0], np.cumsum(sizes)[:-1]]) if len(flat) else np.zeros(0, np.int64)
         shift = np.repeat(bases, sizes)   # every node's tree offset, one vectorised pass
-        self.value = np.concatenate([np.asarray(f[0], dtype=np.float64) for f in flat])
-        left = np.concatenate([np.asarray(f[1], dtype=np.int64) for f in flat])
-        right = np.concatenate([np.asarray(f[2], dtype=np.int64) for f in flat])
+        # (np.concatenate converts array-likes itself; one dtype cast per field)
+        self.value = np.concatenate([f[0] for f in flat]).astype(np.float64, copy=False)
+        left = np.concatenate([f[1] for f in flat]).astype(np.int64, copy=False)
+        right = np.concatenate([f[2] for f in flat]).astype(np.int64, copy=False)
         self.left = np.where(left >= 0, left + shift, -1)
         self.right = np.where(right >= 0, right + shift, -1)
         self.roots = bases.astype(np.int64)
