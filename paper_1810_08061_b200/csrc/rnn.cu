@@ -759,11 +759,16 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a)
       }
     }
   };
-  const int tile0 = 2 * (int)cluster_id_x() + L;
+  // Tiles are sorted longest first; round k hands out tiles [k*stride, (k+1)*stride) in
+  // snake order (reversed on odd rounds), so no lane or cluster always takes the longer tile.
+  const int pos = 2 * (int)cluster_id_x() + L;
+  auto tile_of = [&](int k) { return k * stride + ((k & 1) ? stride - 1 - pos : pos); };
+  const int tile0 = tile_of(0);
   if (warp < kLoad0 && e < NT) tile_meta(tile0);
   if (warp == kMma0 + L && lane == 0) mbar_arrive_expect_tx(&hfull[L], C * sbytes);   // arm phase 0
 
-  for (int tile = tile0; tile < a.ntiles; tile += stride) {
+  for (int round = 0, tile = tile0; tile < a.ntiles || round * stride < a.ntiles; tile = tile_of(++round)) {
+    if (tile >= a.ntiles) continue;   // a partial last round
     named_bar_sync(tile_bar, kLaneThreads);   // this lane's previous tile retired (s_row/s_len rewritten)
     if (warp < kLoad0 && e < NT) { s_row[L][e] = m_r; s_len[L][e] = m_len; }
     named_bar_sync(tile_bar, kLaneThreads);
@@ -779,7 +784,7 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a)
     if (warp < kLoad0) {
       // ======================= epilogue (lane L) =======================
       if (e < NT) {   // next tile's metadata and its h0/c0 rows -> L2
-        tile_meta(tile + stride);
+        tile_meta(tile_of(round + 1));
         if (m_r >= 0) {
           const char* h0n = reinterpret_cast<const char*>(a.h0 + (size_t)m_r * H);
           const char* c0n = reinterpret_cast<const char*>(a.c0 + (size_t)m_r * H);
