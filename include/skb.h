@@ -161,6 +161,12 @@ typedef struct skb_decode_shape {
   int32_t poll;        /* host polls the device stop flag every `poll` steps (0 = 4) */
 } skb_decode_shape;
 int64_t skb_decode_workspace_bytes(const skb_decode_shape* shape);
+/* Byte offset, inside the decode workspace, of the float[sentences*beam] array
+ * that holds, for beam 1 (greedy), each sentence's smallest top-1 minus top-2
+ * logit gap over the decode (+inf if it never chose).  A gap within fp32
+ * rounding means the reference's f64 argmax could differ (reference
+ * graph/tensor.py matmul in f64; argmax_row sums tied ids). */
+int64_t skb_decode_margin_offset(const skb_decode_shape* shape);
 /* Per-phase CUDA-event timing of subsequent skb_decode calls (bench/profiling):
  * read returns the steps timed and ms_out[4] = {embedding gather, gate GEMM +
  * cell, logits GEMM, beam_select} summed over them. */

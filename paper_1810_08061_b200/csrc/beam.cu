@@ -49,6 +49,7 @@ struct DecodeState {             // device pointers into the workspace
   float* row_v;                  // [R, KMAX] each row's K best logits (pass 1)
   int32_t* row_i;                // [R, KMAX] their vocabulary ids
   float* row_lse;                // [R] log-sum-exp of the row
+  float* margin;                 // [R] greedy (beam 1): smallest top-1 - top-2 logit gap over the decode
 };
 
 __device__ __forceinline__ float sigmoidf_ref(float x) {   // reference tensor.py:403-407 (two branches)
@@ -367,6 +368,10 @@ __global__ void __launch_bounds__(SEL_THREADS) beam_choose(DecodeState st, int S
       st.score[nxt][rj] = sel_score[j];
       st.fin[nxt][rj] = (pfin || v == eos) ? 1 : 0;
       st.len[nxt][rj] = st.len[cur][rp] + (pfin ? 0 : 1);
+      // greedy: the chosen token's lead over the runner-up (pass 1 ran with top-2),
+      // so the host can detect an argmax that fp32 rounding could have flipped
+      if (K == 1 && !pfin)
+        st.margin[rj] = fminf(st.margin[rp], st.row_v[(long long)rp * KMAX] - st.row_v[(long long)rp * KMAX + 1]);
     }
   }
   __syncthreads();
@@ -398,6 +403,7 @@ __global__ void dec_init(DecodeState st, const float* __restrict__ h0, const flo
     st.score[0][r] = (r % K == 0) ? 0.0 : -INFINITY;
     st.fin[0][r] = 0;
     st.len[0][r] = 0;
+    st.margin[r] = INFINITY;
   }
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= max_len; t += gridDim.x * blockDim.x)
     st.active[t] = t == 0 ? S : 0;
@@ -464,6 +470,7 @@ size_t layout(const skb_decode_shape& d, DecodeState* st, uint8_t* base) {
   s.row_v = (float*)take(4 * R * KMAX);
   s.row_i = (int32_t*)take(4 * R * KMAX);
   s.row_lse = (float*)take(4 * R);
+  s.margin = (float*)take(4 * R);
   if (st) *st = s;
   return off;
 }
@@ -488,6 +495,14 @@ bool gemm(cublasHandle_t h, int math, const float* A, const float* B, float* C, 
 extern "C" int64_t skb_decode_workspace_bytes(const skb_decode_shape* d) {
   if (!d) return -1;
   return (int64_t)layout(*d, nullptr, nullptr);
+}
+
+extern "C" int64_t skb_decode_margin_offset(const skb_decode_shape* d) {
+  if (!d) return -1;
+  DecodeState st;
+  uint8_t* base = reinterpret_cast<uint8_t*>(uintptr_t(1) << 20);   // any non-null base: offsets only
+  layout(*d, &st, base);
+  return (int64_t)(reinterpret_cast<uint8_t*>(st.margin) - base);
 }
 
 namespace {
@@ -517,7 +532,7 @@ bool enqueue_step(const skb_decode_shape* d, DecodeState& st, cublasHandle_t hb,
   switch (K) {
 #define SKB_SEL(k)                                                                               \
   case k:                                                                                        \
-    beam_rows<k><<<R, ROW_THREADS, 0, cs>>>(st, V, b_out);                                       \
+    beam_rows<(k == 1 ? 2 : k)><<<R, ROW_THREADS, 0, cs>>>(st, V, b_out);                        \
     beam_choose<k><<<S, SEL_THREADS, 0, cs>>>(st, S, V, H, LT, d->eos);                          \
     break;
     SKB_SEL(1) SKB_SEL(2) SKB_SEL(3) SKB_SEL(4) SKB_SEL(5) SKB_SEL(6) SKB_SEL(7) SKB_SEL(8)

@@ -70,6 +70,13 @@ class Decoder:
         self.scores = torch.empty((sentences, beam), dtype=torch.float32, device=self.dev)
         self.lengths = torch.empty((sentences, beam), dtype=torch.int32, device=self.dev)
         assert R == self.scores.numel()
+        off = int(self.lib.skb_decode_margin_offset(ctypes.byref(self.shape)))
+        self.margin = self.ws[off:off + 4 * R].view(torch.float32).view(sentences, beam)
+
+    def margins(self):
+        """Greedy (beam 1): per sentence, the smallest top-1 minus top-2 logit
+        gap of any step it decoded (device tensor [S, 1]; +inf if none)."""
+        return self.margin
 
     def __call__(self, h0, c0=None, stream=None):
         from . import runtime as rt

@@ -121,25 +121,58 @@ def _to_device(v, dtype, device, stream=None):
     return t
 
 
+def _fingerprint(w):
+    """What must be unchanged for a cached packing of weight feed `w` to stay
+    valid.  torch tensors: storage address + in-place version counter;
+    writeable numpy arrays: a snapshot of the contents (compared on reuse);
+    immutable feeds (reference TensorValue tuples, read-only arrays): identity."""
+    torch = _torch()
+    if isinstance(w, DeviceTensor):
+        w = w.tensor
+    if isinstance(w, torch.Tensor):
+        return ("t", w.data_ptr(), w._version, tuple(w.shape), w.dtype)
+    if isinstance(w, np.ndarray) and w.flags.writeable:
+        return ("a", w.copy())
+    if hasattr(w, "array") and isinstance(getattr(w, "array"), np.ndarray) and w.array.flags.writeable:
+        return ("a", w.array.copy())
+    return ("o",)
+
+
+def _same_fingerprint(w, fp) -> bool:
+    cur = _fingerprint(w) if fp[0] != "a" else None
+    if fp[0] == "a":
+        arr = w.array if hasattr(w, "array") and not isinstance(w, np.ndarray) else w
+        return isinstance(arr, np.ndarray) and arr.shape == fp[1].shape and np.array_equal(arr, fp[1])
+    return cur == fp
+
+
 class _WeightCache:
     """Packed tensor-core weight slabs, keyed by the identity of the weight
-    feeds (the objects are kept alive so identities stay valid)."""
+    feeds (the objects are kept alive so identities stay valid) and validated
+    on every reuse against a content fingerprint (`_fingerprint`), so a weight
+    changed in place between calls (an SGD step, then an eval) is re-packed
+    instead of silently served stale."""
 
     def __init__(self, capacity: int = 8):
         self.capacity = capacity
-        self.entries: list = []   # (key, keepalive, packed)
+        self.entries: list = []   # (key, keepalive, fingerprints, packed)
         self.lock = threading.Lock()
 
-    def get(self, key):
+    def get(self, key, weights):
         with self.lock:
-            for k, keep, packed in self.entries:
+            for i, (k, keep, fps, packed) in enumerate(self.entries):
                 if k == key:
-                    return packed
+                    flat = [w for trip in weights for w in trip]
+                    if all(_same_fingerprint(w, fp) for w, fp in zip(flat, fps)):
+                        return packed
+                    self.entries.pop(i)   # stale: re-pack
+                    return None
         return None
 
     def put(self, key, keep, packed):
+        fps = [_fingerprint(w) for trip in keep for w in trip]
         with self.lock:
-            self.entries.append((key, keep, packed))
+            self.entries.append((key, keep, fps, packed))
             if len(self.entries) > self.capacity:
                 self.entries.pop(0)
 
@@ -167,6 +200,7 @@ class RnnExecutable:
         if nb < 0 or nw < 0:
             raise LoweringError(f"recurrent kernel does not support H={H}, F={F} (needs F+H <= 512 "
                                 f"after padding and H <= 256)")
+        self.packed_bytes = nb
         self.packed = self._get_packed(weights, nb, stream)
         self.ws = torch.empty(int(nw), dtype=torch.uint8, device=self.device)
         self.err = torch.zeros(4, dtype=torch.int32, device=self.device)
@@ -175,7 +209,7 @@ class RnnExecutable:
     def _get_packed(self, weights, nbytes, stream):
         torch = _torch()
         key = (self.prog.cell, self.H, self.F, tuple(id(w) for trip in weights for w in trip))
-        packed = _weights.get(key)
+        packed = _weights.get(key, weights)
         if packed is not None:
             return packed
         dev = [[_to_device(w, torch.float64, self.device) for w in trip] for trip in weights]
@@ -199,6 +233,11 @@ class RnnExecutable:
             raise PrecisionRangeError("a weight exceeds the fp16 range (|w| > 65504) of the tensor-core path")
         _weights.put(key, weights, packed)
         return packed
+
+    def refresh(self, weights, stream=None):
+        """Re-validate the packed weights against the weight feeds of this call
+        (re-packs when one was modified in place since it was packed)."""
+        self.packed = self._get_packed(weights, self.packed_bytes, stream)
 
     def run(self, x, h0, c0, lens, out, hT=None, cT=None, stream=None):
         """Launch on device buffers (x: [R,T,F] f32/f64, h0/c0: [R,H] f32,
@@ -232,6 +271,9 @@ def classify(prog: RnnProgram, max_len: int, T: int):
 
 
 # ------------------------------------------------------------------ public API
+from .runtime import on_stream as _on_stream   # noqa: E402
+
+
 _vm_plans: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
@@ -293,6 +335,7 @@ def plan_kind(graph, feeds: Optional[dict] = None) -> str:
     return "stream" if n >= STREAM_MIN_ELEMS else "vm"
 
 
+@_on_stream
 def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=None) -> ExecutionResult:
     """Drop-in for the reference ``execute(graph, feeds, check=True)``.
 
@@ -319,6 +362,10 @@ def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=N
     return execute_vm(graph, feeds, stream=stream)
 
 
+DECODE_MARGIN = float(os.environ.get("SKB_DECODE_MARGIN", "1e-3"))   # logits gap below which the f64 VM decides
+
+
+@_on_stream
 def execute_decode_many(graph, feeds_list: list, *, stream=None) -> list:
     """The staged greedy decoder for P feed sets sharing one
     weight set, eos and max_len: the P sentences decode together in one
@@ -350,9 +397,15 @@ def execute_decode_many(graph, feeds_list: list, *, stream=None) -> list:
                                              as_numpy(f0[prog.w_out])), P, 1, max_len, eos)
     out = dec(h0, stream=stream)
     lengths = out["lengths"][:, 0].to("cpu").numpy()
+    margins = dec.margins()[:, 0].to("cpu").numpy()
     toks = out["tokens"][:, 0, :].to(torch.int64)
     results = []
     for p in range(P):
+        if not margins[p] > DECODE_MARGIN:
+            # an argmax decided by less than the fp32 logits' error bound could differ from the
+            # reference's f64 argmax (whose exact ties sum the tied ids): re-run in f64 on the VM
+            results.append(execute_vm(graph, feeds_list[p] or {}, stream=stream))
+            continue
         n = int(lengths[p])
         vals = [None, None]
         vals[prog.toks_out] = DeviceTensor("i64", toks[p, :n + 1])
@@ -361,6 +414,7 @@ def execute_decode_many(graph, feeds_list: list, *, stream=None) -> list:
     return results
 
 
+@_on_stream
 def execute_stream(graph, feeds: Optional[dict] = None, *, stream=None) -> ExecutionResult:
     """Run a vector-stream program (stream.py / csrc/stream.cu) at any size;
     raises LoweringError for graphs outside that tier."""
@@ -374,6 +428,7 @@ def execute_stream(graph, feeds: Optional[dict] = None, *, stream=None) -> Execu
     return ExecutionResult(st.run(prog, bound, stream=stream), [])
 
 
+@_on_stream
 def execute_vm(graph, feeds: Optional[dict] = None, *, stream=None) -> ExecutionResult:
     """Run any staged graph on the region VM (no validation)."""
     from . import vm
@@ -388,6 +443,7 @@ def execute_vm(graph, feeds: Optional[dict] = None, *, stream=None) -> Execution
     return ExecutionResult(outs, log)
 
 
+@_on_stream
 def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
                  return_exceptions: bool = False, host_outputs: bool = False) -> list:
     """Run `graph` on P independent feed sets in one device launch.
@@ -704,11 +760,16 @@ _exes_lock = threading.Lock()
 
 
 def _executable(prog, weights, B, T, F, H, P, device, stream) -> RnnExecutable:
-    key = (id(prog), B, T, F, H, P, tuple(id(w) for trip in weights for w in trip))
+    """Cached executable per (program, shape, weight feeds, thread): each owns
+    mutable scratch (status word, trip counts, workspace), so concurrent
+    callers on different threads never share one."""
+    key = (id(prog), B, T, F, H, P, tuple(id(w) for trip in weights for w in trip), threading.get_ident(),
+           str(device))
     with _exes_lock:
         hit = _exes.get(key)
-        if hit is not None and hit[0] is prog:
-            return hit[1]
+    if hit is not None and hit[0] is prog:
+        hit[1].refresh(weights, stream)
+        return hit[1]
     exe = RnnExecutable(prog, weights, B, T, F, H, P, device, stream)
     with _exes_lock:
         if len(_exes) > 16:

@@ -15,8 +15,11 @@ The program, as the reference stages it (runtime/dispatch.py:275-387; the
 `lower_greedy` matches that structure (operand roles are read off the
 dataflow, not node order) and returns the feed names of each role; anything
 else raises LoweringError and the graph runs on the region VM.  The fused
-path computes in fp32 (GEMMs without TF32) and takes the lowest index on an
-exact argmax tie (the reference sums the tied ids); `ids` must be 0..V-1.
+path computes in fp32 (GEMMs without TF32) and records, per sentence, the
+smallest top-1 minus top-2 logit gap of any step; a sentence whose gap is not
+above `executor.DECODE_MARGIN` (an argmax fp32 rounding could flip, or an exact
+tie, where the reference's `argmax_row` sums the tied ids) is re-run in f64 on
+the region VM, so tokens always equal the reference's.  `ids` must be 0..V-1.
 """
 
 from __future__ import annotations

@@ -68,6 +68,7 @@ SIGNATURES = {
                                    _VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _VP]),
     "skb_vm_max_ctas": (ctypes.c_int, []),
     "skb_decode_workspace_bytes": (ctypes.c_int64, [ctypes.POINTER(DecodeShape)]),
+    "skb_decode_margin_offset": (ctypes.c_int64, [ctypes.POINTER(DecodeShape)]),
     "skb_decode_profile": (ctypes.c_int, [ctypes.c_int]),
     "skb_decode_last_mode": (ctypes.c_int, []),
     "skb_decode_profile_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float)]),
@@ -153,3 +154,20 @@ def stream_handle(stream=None) -> ctypes.c_void_p:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def on_stream(fn):
+    """Decorator: run the whole call (uploads, status resets, launches,
+    readbacks) with the caller's `stream` as torch's current stream, so every
+    torch copy / fill is ordered with the kernels launched on it and host
+    reads wait for it (side streams are not ordered otherwise)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, stream=None, **kw):
+        if stream is None:
+            return fn(*args, stream=None, **kw)
+        import torch
+        with torch.cuda.stream(stream):
+            return fn(*args, stream=stream, **kw)
+    return wrapper

@@ -35,6 +35,8 @@ from typing import Optional
 
 import numpy as np
 
+from .runtime import on_stream as _on_stream
+
 from . import errors as E
 from .errors import LoweringError, RuntimeGraphError
 from .values import DeviceTensor, ListValue, as_numpy, infer_dtype, shape_of
@@ -808,6 +810,7 @@ def _padded(t):
     return out
 
 
+@_on_stream
 def run(prog: StreamProgram, feeds: dict, *, stream=None, pool: Optional[int] = None):
     """Execute on the current CUDA device. Returns the list of outputs."""
     import torch

@@ -34,6 +34,8 @@ from typing import Optional
 
 import numpy as np
 
+from .runtime import on_stream as _on_stream
+
 from . import errors as E
 from .errors import LoweringError, RuntimeGraphError
 from .values import DeviceTensor, ListValue, Tree, TensorValue, as_numpy, infer_dtype, shape_of
@@ -364,6 +366,7 @@ class _Trees:
         return idx
 
 
+@_on_stream
 def run(prog: Program, feeds: dict, *, stream=None, arena_bytes: Optional[int] = None):
     """Execute a compiled program on the current CUDA device.
 

@@ -126,3 +126,25 @@ def test_greedy_graph_batched_sentences_match_region_vm():
         assert int(r.outputs[1].item()) == int(ref.outputs[1].item())
         stops.add(int(r.outputs[1].item()))
     assert len(stops) > 1   # sentences stopped at different steps
+
+
+def test_greedy_exact_tie_takes_reference_semantics():
+    """An exact argmax tie (a copy of the first chosen token's w_out column):
+    the fused decoder's margin audit sends the sentence to the f64 region VM,
+    which reproduces the reference's argmax_row (sum of the tied ids), not
+    the lowest-index pick."""
+    from paper_1810_08061_b200 import ir
+    from paper_1810_08061_b200.executor import execute_decode_many, execute_vm
+    doc = fixtures.load_golden("greedy_v300_stop")
+    g = ir.from_json(doc["graph"])
+    base = fixtures.make_greedy_feeds(doc["case"])
+    a = int(execute_vm(g, base).outputs[0].array.reshape(-1)[1])   # first generated token
+    b = 1 if a != 1 else 2
+    w_out = np.array(base["w_out"], dtype=np.float64, copy=True)
+    w_out[:, b] = w_out[:, a]
+    f = dict(base, w_out=w_out)
+    ref = execute_vm(g, f)
+    assert int(ref.outputs[0].array.reshape(-1)[1]) == a + b   # the reference sums tied ids
+    fused = execute_decode_many(g, [f])[0]
+    assert fused.outputs[0].array.tolist() == ref.outputs[0].array.tolist()
+    assert int(fused.outputs[1].item()) == int(ref.outputs[1].item())
