@@ -49,14 +49,15 @@ enum Op : int32_t {
   OP_REDUCE = 7, OP_WHERE = 8, OP_SHAPE = 9, OP_RANGE = 10, OP_INDEX = 11, OP_LIST_NEW = 12,
   OP_LIST_APPEND = 13, OP_LIST_POP = 14, OP_LIST_GET = 15, OP_LIST_SET = 16, OP_LIST_STACK = 17,
   OP_JMP = 18, OP_JZ = 19, OP_ITER = 20, OP_PRINT = 21, OP_ASSERT = 22, OP_TREE = 23,
-  OP_VIEW = 24, OP_SET_I64 = 25, OP_RAISE = 26, OP_SWAP = 27
+  OP_VIEW = 24, OP_SET_I64 = 25, OP_RAISE = 26, OP_SWAP = 27, OP_CALL = 28, OP_RET = 29
 };
 enum BinK : int32_t { B_ADD, B_SUB, B_MUL, B_DIV, B_MOD, B_LT, B_GT, B_LE, B_GE, B_EQ, B_NE };
 enum UnK : int32_t { U_NEG, U_NOT, U_TANH, U_SIGMOID };
 
 // error codes (include/skb.h) + VM-only kinds
 enum { E_INDEX = 10, E_EMPTY = 11, E_SHAPE = 12, E_DIV0 = 13, E_LIMIT = 14, E_ASSERT = 15,
-       E_DTYPE = 16, E_TYPE = 17, E_ARENA = 30 };
+       E_DTYPE = 16, E_TYPE = 17, E_ARENA = 30, E_DEPTH = 32 };
+constexpr int kMaxCallDepth = 1 << 16;
 
 struct VmCtl {            // device control block
   int32_t err, err_uid;
@@ -708,6 +709,63 @@ __device__ void op_tree(Vm& vm, const VmIns& in) {   // reference execute.py:136
   vm.commit(d, nv);
 }
 
+// Recursive FuncCall (reference graph/execute.py:191-193): a device call stack of
+// arena frame records.  Record at `rec`: a shared header (written identically by
+// every CTA) {prev fp, return pc, call-site extra, per-CTA bytes, lo, n}, then one
+// portion per CTA: the n saved slot descriptors of the callee's range [lo, lo+n)
+// followed by a scratch area for the call's arguments / results.  Only thread 0
+// of a CTA touches its CTA's slot table; the instruction barrier publishes it.
+__device__ void op_call(Vm& vm, const VmIns& in, int pc, int64_t& fp, int& depth) {
+  const int lo = in.a[2], n = in.a[3] - in.a[2];
+  const int32_t* ex = vm.a.extra + in.a[1];
+  const int nargs = ex[0], ndest = ex[1 + nargs];
+  const int32_t* px = vm.a.extra + in.a[4];
+  const int64_t per = (int64_t)(n + (nargs > ndest ? nargs : ndest)) * (int64_t)sizeof(VmVal);
+  const int64_t rec = vm.alloc(64 + per * gridDim.x);
+  if (vm.bump > vm.a.arena_bytes) return;   // E_ARENA is raised by the loop
+  if (threadIdx.x == 0) {
+    int64_t* hdr = reinterpret_cast<int64_t*>(vm.P(rec));
+    hdr[0] = fp; hdr[1] = pc + 1; hdr[2] = in.a[1]; hdr[3] = per; hdr[4] = lo; hdr[5] = n;
+    VmVal* saved = reinterpret_cast<VmVal*>(vm.P(rec + 64 + per * blockIdx.x));
+    VmVal* tmp = saved + n;
+    for (int i = 0; i < n; ++i) saved[i] = vm.S(lo + i);
+    for (int k = 0; k < nargs; ++k) tmp[k] = vm.S(ex[1 + k]);
+    for (int i = 0; i < n; ++i) { vm.S(lo + i).own = -1; vm.S(lo + i).own_cap = 0; }   // fresh storage
+    for (int k = 0; k < px[0] && k < nargs; ++k) {
+      VmVal v = tmp[k];
+      v.own = -1; v.own_cap = 0;
+      vm.S(px[1 + k]) = v;
+    }
+  }
+  fp = rec;
+  ++depth;
+}
+
+__device__ int op_ret(Vm& vm, const VmIns& in, int64_t& fp, int& depth) {
+  const int64_t* hdr = reinterpret_cast<const int64_t*>(vm.P(fp));
+  const int64_t prev = hdr[0], per = hdr[3];
+  const int ret = (int)hdr[1], lo = (int)hdr[4], n = (int)hdr[5];
+  const int32_t* ex = vm.a.extra + hdr[2];
+  const int nargs = ex[0], ndest = ex[1 + nargs];
+  const int32_t* dest = ex + 2 + nargs;
+  const int32_t* rx = vm.a.extra + in.a[0];
+  if (threadIdx.x == 0) {
+    VmVal* saved = reinterpret_cast<VmVal*>(vm.P(fp + 64 + per * blockIdx.x));
+    VmVal* tmp = saved + n;
+    for (int k = 0; k < rx[0] && k < ndest; ++k) tmp[k] = vm.S(rx[1 + k]);
+    for (int i = 0; i < n; ++i) vm.S(lo + i) = saved[i];
+    for (int k = 0; k < rx[0] && k < ndest; ++k) {
+      VmVal v = tmp[k];
+      const VmVal cur = vm.S(dest[k]);
+      v.own = cur.own; v.own_cap = cur.own_cap;
+      vm.S(dest[k]) = v;
+    }
+  }
+  fp = prev;
+  --depth;
+  return ret;
+}
+
 __global__ void __launch_bounds__(256) vm_kernel(VmArgs a, int grid_sync) {
   Vm vm;
   vm.a = a;
@@ -715,6 +773,8 @@ __global__ void __launch_bounds__(256) vm_kernel(VmArgs a, int grid_sync) {
   vm.bump = a.arena_start;
   int pc = 0;
   int64_t steps = 0;
+  int64_t fp = 0;   // current call frame record (0: main)
+  int depth = 0;
   for (;;) {
     const VmIns in = a.prog[pc];
     int next = pc + 1;
@@ -791,6 +851,16 @@ __global__ void __launch_bounds__(256) vm_kernel(VmArgs a, int grid_sync) {
         break;
       }
       case OP_RAISE: vm.fail(in.a[0], in.uid, in.a[1]); break;
+      case OP_CALL:
+        if (depth >= kMaxCallDepth) { vm.fail(E_DEPTH, in.uid, depth); break; }
+        __syncthreads();   // every thread read the slot table of the previous instruction
+        op_call(vm, in, pc, fp, depth);
+        next = in.a[0];
+        break;
+      case OP_RET:
+        __syncthreads();
+        next = op_ret(vm, in, fp, depth);
+        break;
       default: vm.fail(E_TYPE + 100, in.uid, in.op); break;
     }
     if (vm.bump > a.arena_bytes) vm.fail(E_ARENA, in.uid, vm.bump);

@@ -335,18 +335,33 @@ def plan_kind(graph, feeds: Optional[dict] = None) -> str:
     return "stream" if n >= STREAM_MIN_ELEMS else "vm"
 
 
+PRECISIONS = ("fast", "f64")
+
+
 @_on_stream
-def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=None) -> ExecutionResult:
+def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=None,
+            precision: Optional[str] = None) -> ExecutionResult:
     """Drop-in for the reference ``execute(graph, feeds, check=True)``.
 
     Programs with a fused kernel (the dynamic-length recurrent loop) run
     through it; every other graph runs on the device-resident region VM
-    (``vm.py`` / ``csrc/vm.cu``)."""
+    (``vm.py`` / ``csrc/vm.cu``).
+
+    ``precision`` (default: env SKB_PRECISION, else "fast"): "fast" lets the
+    fused recurrent kernel run a matching program on fp16 tensor cores (fp32
+    state, stated bound 3e-3); "f64" keeps every float in float64 like the
+    reference (the region VM / vector-stream tier), for callers that need the
+    reference's 1e-9 agreement (its differential harness)."""
     from . import runtime as rt
     rt.lib()
     if check:
         validate(graph)
+    precision = precision or os.environ.get("SKB_PRECISION", "fast")
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision {precision!r} (expected one of {PRECISIONS})")
     kind = plan_kind(graph, feeds)
+    if kind == "rnn" and precision == "f64":
+        kind = "vm"
     if kind == "rnn":
         return execute_many(graph, [feeds or {}], check=False, stream=stream)[0]
     if kind == "stream":

@@ -16,7 +16,15 @@ device interpreter in csrc/vm.cu executes:
 * `Cond` (execute.py:205-216) becomes JZ pred -> ELSE ; then ; VIEW outs ;
   JMP END ; ELSE: else ; VIEW outs ; END — only the taken branch runs, so
   effects (Print/Assert) happen exactly as in the reference;
-* `FuncCall` bodies are inlined (recursive calls raise LoweringError);
+* `FuncCall` bodies are inlined, except functions on a call-graph cycle
+  (recursion, reference graph/execute.py:191-193, e.g. corpus/tree_prod.msl):
+  those are compiled once, out of line, over their own slot range [lo, hi),
+  and called through a device call stack — CALL saves the range's slot
+  descriptors in an arena frame record (one copy per CTA), detaches the
+  range from its storage (the callee allocates fresh storage, so the caller's
+  values survive), binds the arguments and jumps; RET reads the results,
+  restores the caller's descriptors and binds the results to the call
+  site's slots;
 * static dtype failures (reference tensor.py:252-267, validate rules) compile
   to a RAISE at the failing node, so they fire only if the node executes.
 
@@ -44,7 +52,7 @@ from .values import DeviceTensor, ListValue, Tree, TensorValue, as_numpy, infer_
 OP = dict(HALT=0, COPY=2, BINOP=3, UNARY=4, MATMUL=5, TRANSPOSE=6, REDUCE=7, WHERE=8, SHAPE=9,
           RANGE=10, INDEX=11, LIST_NEW=12, LIST_APPEND=13, LIST_POP=14, LIST_GET=15, LIST_SET=16,
           LIST_STACK=17, JMP=18, JZ=19, ITER=20, PRINT=21, ASSERT=22, TREE=23, VIEW=24, SET_I64=25,
-          RAISE=26, SWAP=27)
+          RAISE=26, SWAP=27, CALL=28, RET=29)
 BIN = {"Add": 0, "Sub": 1, "Mul": 2, "Div": 3, "Mod": 4, "Lt": 5, "Gt": 6, "Le": 7, "Ge": 8, "Eq": 9, "Ne": 10}
 BIN_SYMBOL = {"Add": "+", "Sub": "-", "Mul": "*", "Div": "/", "Mod": "%", "Lt": "<", "Gt": ">",
               "Le": "<=", "Ge": ">=", "Eq": "==", "Ne": "!="}
@@ -58,6 +66,7 @@ CAUSE = {10: E.INDEX_OUT_OF_RANGE, 11: E.EMPTY_POP, 12: E.SHAPE_MISMATCH, 13: E.
          14: E.ITERATION_LIMIT, 15: E.ASSERTION_FAILED, 16: E.DTYPE_MISMATCH, 17: "MslTypeError"}
 E_ARENA = 30
 E_STEPS = 31
+E_DEPTH = 32
 
 VAL_DTYPE = np.dtype([("view", "<i8"), ("own", "<i8"), ("own_cap", "<i8"), ("numel", "<i8"),
                       ("dtype", "<i4"), ("rank", "<i4"), ("shape", "<i4", (MAX_RANK,))])
@@ -82,6 +91,9 @@ class _Compiler:
         self.p = Program()
         self.slot = {}              # (id(node), out) -> slot
         self.call_stack = []
+        self.recursive = _recursive_functions(graph)
+        self.entries = {}           # recursive function -> (entry pc, lo, hi, param slots)
+        self.call_sites = []        # (instruction index, function name) to patch with the entry pc
 
     # ---------------------------------------------------------------- helpers
     def new_slot(self):
@@ -292,8 +304,10 @@ class _Compiler:
 
     def call(self, n):
         name = n.attrs["fn_name"]
+        if name in self.recursive:
+            return self.call_out_of_line(n, name)
         if name in self.call_stack:
-            raise LoweringError(f"recursive FuncCall {name!r} has no VM lowering yet")
+            raise LoweringError(f"recursive FuncCall {name!r} has no VM lowering")
         fn = self.g.functions[name]
         self.call_stack.append(name)
         outs = self.frame(fn.body, [self.of(r) for r in n.inputs])
@@ -303,6 +317,75 @@ class _Compiler:
             o = self.new_slot()
             self.emit("VIEW", n, o, s)
             self.bind(n, k, o)
+
+
+    def call_out_of_line(self, n, name):
+        """CALL of a recursive function (compiled once by `function`): extra =
+        [nargs, args..., nres, dests...]; the frame range and entry are read
+        from the function's header (patched in `finish`)."""
+        args = [self.of(r) for r in n.inputs]
+        dests = [self.new_slot() for _ in n.out_types]
+        ex = self.extra([len(args)] + args + [len(dests)] + dests)
+        at = self.emit("CALL", n, 0, ex, 0, 0)
+        self.call_sites.append((at, name))
+        for k, d in enumerate(dests):
+            self.bind(n, k, d)
+
+    def function(self, name):
+        """Out-of-line body of a recursive function: params, body, RET."""
+        fn = self.g.functions[name]
+        entry = self.here()
+        lo = self.p.nslots
+        params = [self.new_slot() for _ in fn.body.params]
+        outs = self.frame(fn.body, params)
+        hi = self.p.nslots
+        self.emit("RET", None, self.extra([len(outs)] + outs))
+        self.entries[name] = (entry, lo, hi, params)
+
+    def finish(self):
+        """Compile every recursive function after main's HALT and patch the
+        call sites: CALL a = [entry, extra, lo, hi, params extra]."""
+        for name in sorted(self.recursive):
+            if name in self.g.functions:
+                self.function(name)
+        for at, name in self.call_sites:
+            entry, lo, hi, params = self.entries[name]
+            self.patch(at, 0, entry)
+            self.patch(at, 2, lo)
+            self.patch(at, 3, hi)
+            self.patch(at, 4, self.extra([len(params)] + params))
+
+
+def _recursive_functions(graph) -> set:
+    """Functions that can reach themselves through FuncCall (any nesting of
+    Cond / While regions in their bodies)."""
+    fns = getattr(graph, "functions", {}) or {}
+    callees = {}
+
+    def scan(sg, out):
+        for node in sg.nodes:
+            if node.op == "FuncCall":
+                out.add(node.attrs["fn_name"])
+            for key in ("then_graph", "else_graph", "test_graph", "body_graph"):
+                sub = node.attrs.get(key) if hasattr(node, "attrs") else None
+                if sub is not None and hasattr(sub, "nodes"):
+                    scan(sub, out)
+    for name, fn in fns.items():
+        callees[name] = set()
+        scan(fn.body, callees[name])
+    rec = set()
+    for start in fns:
+        seen, todo = set(), list(callees.get(start, ()))
+        while todo:
+            f = todo.pop()
+            if f == start:
+                rec.add(start)
+                break
+            if f in seen or f not in callees:
+                continue
+            seen.add(f)
+            todo.extend(callees[f])
+    return rec
 
 
 def _result_dtype(op, a, b):
@@ -332,6 +415,7 @@ def compile_graph(graph) -> Program:
         c.node(node)
     c.p.outputs = [c.of(r) for r in graph.main.outputs]
     c.emit("HALT")
+    c.finish()
     return c.p
 
 
@@ -448,6 +532,8 @@ def run(prog: Program, feeds: dict, *, stream=None, arena_bytes: Optional[int] =
             raise E.IterationLimitExceeded(f"loop exceeded max_iterations={limit}", span)
         if err in CAUSE:
             raise RuntimeGraphError(_message(err, node, int(c[1])), span, CAUSE[err])
+        if err == E_DEPTH:
+            raise E.DeviceError(f"recursion deeper than {int(c[1])} calls at node {err_uid}")
         raise E.DeviceError(f"VM failure code {err} at node {err_uid}")
     host_slots = np.frombuffer(dslots[:slots.nbytes].cpu().numpy().tobytes(), dtype=VAL_DTYPE)
     outs = [_value(arena, host_slots[s], trees) for s in prog.outputs]

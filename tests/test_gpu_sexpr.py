@@ -30,10 +30,6 @@ def test_sexpr_program_on_device(case):
     g = sexpr.from_sexpr(case["sexpr"])
     feeds = {k: feed_value(v) for k, v in src["feeds"].items()}
     exp = src["expected"]
-    if case["key"] == "tree_prod":   # recursive FuncCall: no device lowering (as for the JSON graph)
-        with pytest.raises(LoweringError):
-            execute(g, feeds)
-        return
     if "error" in exp:
         with pytest.raises(RuntimeGraphError) as info:
             execute(g, feeds)

@@ -33,10 +33,6 @@ def _check(graph_doc, feeds_doc, exp, rel=1e-9):
 
 @pytest.mark.parametrize("prog", corpus(), ids=lambda p: p["name"])
 def test_corpus_programs(prog):
-    if prog["name"] == "tree_prod":
-        with pytest.raises(LoweringError):
-            _check(prog["graph"], prog["feeds"], prog["expected"])
-        return
     rel = 3e-3 if plan_kind(ir.from_json(prog["graph"])) == "rnn" else 1e-9
     _check(prog["graph"], prog["feeds"], prog["expected"], rel)
 
@@ -47,3 +43,11 @@ CASES = fuzz_cases()
 @pytest.mark.parametrize("case", [c for _, c in CASES], ids=[n for n, _ in CASES])
 def test_fuzz_programs(case):
     _check(case["graph"], case["feeds"], case["expected"])
+
+
+@pytest.mark.parametrize("prog", __import__("vm_cases").recursion(), ids=lambda p: p["name"])
+def test_recursive_funccall_programs(prog):
+    """Recursive FuncCall (reference graph/execute.py:191-193) on the device
+    call stack: outputs, print logs (pre-order effects) and the AssertionFailed
+    raised 1 call deep equal the reference executor's."""
+    _check(prog["graph"], prog["feeds"], prog["expected"])

@@ -83,3 +83,9 @@ def leaf_equal(got, exp, rel=1e-9):
         return False
     fin = ~nan & ~inf
     return bool(np.all(np.abs(a[fin] - b[fin]) <= rel * np.maximum(1.0, np.maximum(np.abs(a[fin]), np.abs(b[fin])))))
+
+
+def recursion():
+    """Recursive FuncCall programs (oracle/gen_recursion_golden.py)."""
+    with open(os.path.join(GOLDEN, "vm_recursion.json")) as f:
+        return json.load(f)["programs"]
