@@ -46,7 +46,11 @@ enum {
 /* Cell kinds recognised by the lowering of a staged `While` region. */
 enum {
   SKB_CELL_LSTM = 1,      /* i,f,g,o gates; c' = f*c + i*g; h' = o*tanh(c')  */
-  SKB_CELL_RNN_TANH = 2   /* h' = tanh(x W + h U + b)  (corpus/dynamic_rnn.msl) */
+  SKB_CELL_RNN_TANH = 2,  /* h' = tanh(x W + h U + b)  (corpus/dynamic_rnn.msl) */
+  SKB_CELL_GRU = 3        /* z,r = sigmoid(x W + h U + b); n = tanh(x Wn + bn + r*(h Un + bhn));
+                             h' = (1-z)*n + z*h  (oracle/programs/gru.msl).  Packed as four
+                             gate blocks z, r, n_x = [Wn | 0], n_h = [0 | Un] (biases bz, br,
+                             bn, bhn): pass w = {Wz, Wr, Wn, NULL}, u = {Uz, Ur, NULL, Un}. */
 };
 
 /* Library / device information. */
@@ -68,7 +72,7 @@ int skb_last_cuda_error(void); /* cudaError_t of the last SKB_ERR_CUDA */
  * frozen state exactly as the reference's Where does.
  * ------------------------------------------------------------------------- */
 typedef struct skb_rnn_shape {
-  int32_t cell;               /* SKB_CELL_*                                   */
+  int32_t cell;               /* SKB_CELL_* (LSTM, RNN_TANH, GRU)              */
   int32_t hidden;             /* H                                            */
   int32_t input;              /* F                                            */
   int32_t time;               /* T: time extent of x (leading dim after the transpose) */

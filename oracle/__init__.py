@@ -23,7 +23,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "liboracle.so")
 
 CAUSE = {10: "IndexOutOfRange", 11: "EmptyPop", 12: "ShapeMismatch", 14: "IterationLimitExceeded"}
-CELL_LSTM, CELL_RNN = 1, 2
+CELL_LSTM, CELL_RNN, CELL_GRU = 1, 2, 3
 
 _lib = None
 _D = ctypes.POINTER(ctypes.c_double)

@@ -24,11 +24,19 @@ PROGRAMS = os.path.join(HERE, "programs")
 LSTM_PARAMS = ["input_data", "h0", "c0", "sequence_len"] + \
     [f"{k}{g}" for g in "ifgo" for k in ("w", "u", "b")]
 RNN_PARAMS = ["input_data", "initial_state", "sequence_len", "w_x", "w_h", "b"]
+GRU_PARAMS = ["input_data", "h0", "sequence_len", "wz", "uz", "bz", "wr", "ur", "br", "wn", "un", "bn", "bhn"]
 
 
 def lstm_case(name, B, T, F, H, lens, seed, program="lstm.msl", entry="dynamic_lstm", wscale=0.1,
               xscale=1.0, note=""):
     return {"name": name, "program": program, "entry": entry, "cell": "lstm",
+            "dims": {"B": B, "T": T, "F": F, "H": H}, "lens": lens, "seed": seed,
+            "wscale": wscale, "xscale": xscale, "note": note}
+
+
+def gru_case(name, B, T, F, H, lens, seed, program="gru.msl", entry="dynamic_gru", wscale=0.1,
+             xscale=1.0, note=""):
+    return {"name": name, "program": program, "entry": entry, "cell": "gru",
             "dims": {"B": B, "T": T, "F": F, "H": H}, "lens": lens, "seed": seed,
             "wscale": wscale, "xscale": xscale, "note": note}
 
@@ -68,6 +76,14 @@ CASES = [
     lstm_case("lstm_mixed_negative", 3, 4, 8, 8, [-2, 3, 0], 31, note="negative row is frozen at h0"),
     lstm_case("lstm_large_inputs", 3, 5, 8, 8, [5, 4, 2], 32, xscale=100.0, wscale=0.5,
               note="saturating gates"),
+    gru_case("gru_4x8x8", 4, 8, 8, 8, [8, 3, 1, 6], 41, note="GRU cell (oracle/programs/gru.msl)"),
+    gru_case("gru_zero_len_rows", 3, 5, 8, 8, [5, 0, 2], 42, note="a row of length 0 keeps h0"),
+    gru_case("gru_ragged_12x20", 5, 6, 12, 20, [6, 1, 3, 6, 2], 43, note="F != H, H not a multiple of 16"),
+    gru_case("gru_32x16x64", 32, 16, 64, 64, "random", 44),
+    gru_case("gru_4x6x256", 4, 6, 256, 256, [6, 2, 5, 1], 45, note="C1 widths (H=F=256): dual-lane kernel"),
+    gru_case("gru_len_gt_T", 3, 4, 8, 8, [2, 6, 1], 46, note="len > T -> IndexOutOfRange"),
+    gru_case("gru_all_zero", 3, 4, 8, 8, [0, 0, 0], 47, note="max_len 0 -> EmptyPop"),
+    gru_case("gru_large_inputs", 3, 5, 8, 8, [5, 4, 2], 48, xscale=100.0, wscale=0.5, note="saturating gates"),
 ]
 
 
@@ -79,7 +95,7 @@ def case_by_name(name):
 
 
 def param_names(case):
-    return LSTM_PARAMS if case["cell"] == "lstm" else RNN_PARAMS
+    return {"lstm": LSTM_PARAMS, "gru": GRU_PARAMS}.get(case["cell"], RNN_PARAMS)
 
 
 def make_feeds(case) -> dict:
@@ -101,6 +117,14 @@ def make_feeds(case) -> dict:
             feeds["w" + g] = rng.uniform(-ws, ws, (F, H))
             feeds["u" + g] = rng.uniform(-ws, ws, (H, H))
             feeds["b" + g] = rng.uniform(-ws, ws, (H,))
+    elif case["cell"] == "gru":
+        feeds["h0"] = rng.uniform(-0.1, 0.1, (B, H))
+        feeds["sequence_len"] = lens.astype(np.int64)
+        for g in "zrn":
+            feeds["w" + g] = rng.uniform(-ws, ws, (F, H))
+            feeds["u" + g] = rng.uniform(-ws, ws, (H, H))
+            feeds["b" + g] = rng.uniform(-ws, ws, (H,))
+        feeds["bhn"] = rng.uniform(-ws, ws, (H,))
     else:
         feeds["initial_state"] = rng.uniform(-1, 1, (B, H))
         feeds["sequence_len"] = lens.astype(np.int64)
@@ -116,6 +140,10 @@ def oracle_args(case, feeds):
         return (1, feeds["input_data"], feeds["h0"], feeds["c0"], feeds["sequence_len"],
                 [feeds["w" + g] for g in "ifgo"], [feeds["u" + g] for g in "ifgo"],
                 [feeds["b" + g] for g in "ifgo"])
+    if case["cell"] == "gru":
+        return (3, feeds["input_data"], feeds["h0"], None, feeds["sequence_len"],
+                [feeds["w" + g] for g in "zrn"], [feeds["u" + g] for g in "zrn"],
+                [feeds["b" + g] for g in "zrn"] + [feeds["bhn"]])
     return (2, feeds["input_data"], feeds["initial_state"], None, feeds["sequence_len"],
             [feeds["w_x"]], [feeds["w_h"]], [feeds["b"]])
 

@@ -23,6 +23,9 @@
  *                     LSTM: i = sigmoid((x_t@Wi + h@Ui) + bi) ... c' = f*c + i*g;
  *                           h' = o*tanh(c')            (SURVEY App. A op order)
  *                     RNN:  h' = tanh((x_t@Wx + h@Wh) + b)     corpus/dynamic_rnn.msl
+ *                     GRU:  z = sigmoid((x_t@Wz + h@Uz) + bz); r likewise;
+ *                           n = tanh((x_t@Wn + bn) + r*(h@Un + bhn));
+ *                           h' = (1.0 - z)*n + z*h         oracle/programs/gru.msl
  *                     h = where(idx < len, h', h) ...; outputs.append(h)
  *                   stack(outputs) (empty -> EmptyPop)  execute.py:171-174
  *                   transpose(stack, [1,0,2])
@@ -34,7 +37,7 @@
 #include <string.h>
 
 enum { OK = 0, ERR_INDEX = 10, ERR_EMPTY = 11, ERR_SHAPE = 12, ERR_LIMIT = 14 };
-enum { CELL_LSTM = 1, CELL_RNN = 2 };
+enum { CELL_LSTM = 1, CELL_RNN = 2, CELL_GRU = 3 };
 
 /* out[n,m] = a[n,k] @ b[k,m]; per element: acc = 0.0; acc += a*b in t order.
  * The j-inner loop keeps that per-element order while vectorising. */
@@ -82,7 +85,7 @@ int oracle_rnn_program(int cell, int B, int T, int F, int H, const double* x, co
     if (lens[r] > m) m = lens[r];
   *max_len_out = m;
   if (m < 0) return ERR_SHAPE; /* Range(max_len) */
-  const int G = cell == CELL_LSTM ? 4 : 1;
+  const int G = cell == CELL_LSTM ? 4 : cell == CELL_GRU ? 3 : 1;
   const int64_t mo = m < T ? m : T; /* row stride of out (== max_len whenever there is no error) */
   double* h = malloc(sizeof(double) * B * H);
   double* c = malloc(sizeof(double) * B * H);
@@ -99,13 +102,37 @@ int oracle_rnn_program(int cell, int B, int T, int F, int H, const double* x, co
     if (t >= T) { rc = ERR_INDEX; break; }
     for (int r = 0; r < B; ++r)
       memcpy(xt + (size_t)r * F, x + ((size_t)r * T + t) * F, sizeof(double) * F);
-    for (int g = 0; g < G; ++g) {
+    for (int g = 0; g < G && cell != CELL_GRU; ++g) {
       double* z = gates + (size_t)g * B * H;
       affine_gate(xt, h, W[g], U[g], bias[g], z, tmp, B, F, H);
       const int is_tanh = (cell == CELL_RNN) || (g == 2);
       for (int i = 0; i < B * H; ++i) z[i] = is_tanh ? tanh(z[i]) : oracle_sigmoid(z[i]);
     }
-    if (cell == CELL_LSTM) {
+    if (cell == CELL_GRU) {
+      double *gz = gates, *gr = gates + (size_t)B * H, *gn = gates + (size_t)2 * B * H;
+      for (int g = 0; g < 2; ++g) {
+        double* z = gates + (size_t)g * B * H;
+        affine_gate(xt, h, W[g], U[g], bias[g], z, tmp, B, F, H);
+        for (int i = 0; i < B * H; ++i) z[i] = oracle_sigmoid(z[i]);
+      }
+      /* n = tanh((x@Wn + bn) + r * (h@Un + bhn)) */
+      oracle_matmul(xt, W[2], gn, B, F, H);
+      oracle_matmul(h, U[2], tmp, B, H, H);
+      for (int r = 0; r < B; ++r)
+        for (int j = 0; j < H; ++j) {
+          const size_t i = (size_t)r * H + j;
+          double a = gn[i] + bias[2][j];
+          double hn = tmp[i] + bias[3][j];
+          double rh = gr[i] * hn;
+          gn[i] = tanh(a + rh);
+        }
+      for (int i = 0; i < B * H; ++i) {
+        double one_minus = 1.0 - gz[i];
+        double p1 = one_minus * gn[i];
+        double p2 = gz[i] * h[i];
+        nh[i] = p1 + p2;
+      }
+    } else if (cell == CELL_LSTM) {
       const double *gi = gates, *gf = gates + (size_t)B * H, *gg = gates + (size_t)2 * B * H,
                    *go = gates + (size_t)3 * B * H;
       for (int i = 0; i < B * H; ++i) {

@@ -77,7 +77,7 @@ inline bool make_geom(const skb_rnn_shape* s, RnnGeom* g) {
       s->problems <= 0)
     return false;
   g->cell = s->cell;
-  if (s->cell == SKB_CELL_LSTM) g->G = 4;
+  if (s->cell == SKB_CELL_LSTM || s->cell == SKB_CELL_GRU) g->G = 4;
   else if (s->cell == SKB_CELL_RNN_TANH) g->G = 1;
   else return false;
   g->H = s->hidden; g->F = s->input; g->T = s->time;
@@ -98,7 +98,7 @@ inline bool make_geom(const skb_rnn_shape* s, RnnGeom* g) {
 template <int NT>
 inline size_t smem_bytes(const RnnGeom& g) {
   return (size_t)2 * NT * g.Kx * 2 + (size_t)2 * NT * g.Kh * 2 +
-         (g.cell == SKB_CELL_LSTM ? (size_t)4 * NT * kGS * 4 : 0) + 1024;
+         (g.G == 4 ? (size_t)4 * NT * kGS * 4 : 0) + 1024;
 }
 
 struct RnnArgs {
@@ -235,6 +235,37 @@ SKB_DEV float gate_act(float z, float kl, float kb, float mul, float add) {
 template <int ACT>
 SKB_DEV float cell_tanh(float c) { return ACT ? tanh_approx(c) : tanh_acc(c); }
 
+// Four-gate-block cells (LSTM i,f,g,o; GRU z,r,n_x,n_h): the gate phase of TMEM
+// lane quarter qw (warp-uniform).  GRU: z and r are sigmoids, n_x / n_h stay
+// affine (+ bias) until the cell phase combines them.
+template <int CELL, int ACT>
+struct GateAct {
+  float kl, kb, mul, add, bias;
+  bool affine;
+  SKB_DEV GateAct(int qw, float b) : bias(b) {
+    affine = (CELL == SKB_CELL_GRU) && qw >= 2;
+    gate_consts<ACT>(CELL == SKB_CELL_GRU ? 0 : qw, b, kl, kb, mul, add);
+  }
+  SKB_DEV float operator()(float z) const { return affine ? z + bias : gate_act<ACT>(z, kl, kb, mul, add); }
+};
+
+// The cell update from the four activated blocks, masked by `live` (the reference's Where).
+//   LSTM: c' = f*c + i*g, h' = o*tanh(c')
+//   GRU : n = tanh(n_x + r*n_h), h' = (1-z)*n + z*h = n + z*(h - n)
+template <int CELL, int ACT>
+SKB_DEV void cell_update(float g0, float g1, float g2, float g3, float& c, float& h, bool live) {
+  if constexpr (CELL == SKB_CELL_GRU) {
+    const float n = cell_tanh<ACT>(fmaf(g1, g3, g2));
+    const float h2 = fmaf(g0, h - n, n);
+    h = live ? h2 : h;
+  } else {
+    const float c2 = fmaf(g1, c, g0 * g2);
+    const float h2 = g3 * cell_tanh<ACT>(c2);
+    c = live ? c2 : c;
+    h = live ? h2 : h;
+  }
+}
+
 template <int CELL, int NT, typename XT, int EW, int ACT = 0>
 __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs a) {
   // EW epilogue warps (8 or 16), then the x loader warp and the MMA warp.
@@ -305,8 +336,9 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
   //         (G8 = U/8 unit groups per CTA), so h/c/out/stage are 16/32-byte vectors.
   //   RNN : unit = 32*qw + lane; the thread owns the NT/2 columns of its half.
   const int qw = warp & 3, ch = warp >> 2;
-    constexpr int NP = (CELL == SKB_CELL_LSTM) ? (NT * (32 / UG) + kEpi - 1) / kEpi : 1;   // max items per thread
-  constexpr int NCELL = (CELL == SKB_CELL_LSTM) ? NP * UG : NCOL;
+  constexpr bool kGated = CELL == SKB_CELL_LSTM || CELL == SKB_CELL_GRU;   // four gate blocks
+  constexpr int NP = kGated ? (NT * (32 / UG) + kEpi - 1) / kEpi : 1;   // max items per thread
+  constexpr int NCELL = kGated ? NP * UG : NCOL;
   const int G8 = U / UG;
   int pn[NP], pu[NP];
   bool pv[NP];
@@ -315,11 +347,11 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
     const int idx = tid + kEpi * p;
     pn[p] = G8 ? idx / G8 : 0;
     pu[p] = G8 ? (idx % G8) * UG : 0;
-    pv[p] = (CELL == SKB_CELL_LSTM) && tid < kEpi && idx < NT * G8;
+    pv[p] = kGated && tid < kEpi && idx < NT * G8;
   }
   const int rnn_u = qw * 32 + lane;
   const int rnn_unit = (int)q * U + rnn_u;
-  const bool rnn_valid = (CELL != SKB_CELL_LSTM) && (warp < EW) && (rnn_u < U) && (rnn_unit < H);
+  const bool rnn_valid = !kGated && (warp < EW) && (rnn_u < U) && (rnn_unit < H);
   float hp[NCELL], cc[NCELL];
   uint8_t* gscr = a.hscratch + (size_t)cluster_id_x() * 2 * hbytes;   // this cluster's h_t exchange buffers
 
@@ -386,7 +418,7 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
           }
         }
       }
-      if constexpr (CELL == SKB_CELL_LSTM) {
+      if constexpr (kGated) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           const int r = pv[p] ? s_row[pn[p]] : -1;
@@ -394,7 +426,12 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
           float hv[8], cv[8];
           if (r >= 0) {
             load_x8<float>(a.h0 + (size_t)r * H, unit0, H, hv);
-            load_x8<float>(a.c0 + (size_t)r * H, unit0, H, cv);
+            if (a.c0) {
+              load_x8<float>(a.c0 + (size_t)r * H, unit0, H, cv);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) cv[e] = 0.f;
+            }
           } else {
 #pragma unroll
             for (int e = 0; e < 8; ++e) hv[e] = cv[e] = 0.f;
@@ -411,7 +448,7 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
       }
       if (trip > 0) {   // h0 reaches every CTA's hbuf[step&1] like any h_t: own fp16 slice -> L2 -> multicast
         uint8_t* gs0 = gscr + (step & 1) * hbytes + q * sbytes;
-        if constexpr (CELL == SKB_CELL_LSTM) {
+        if constexpr (kGated) {
 #pragma unroll
           for (int p = 0; p < NP; ++p) {
             if (!pv[p]) continue;
@@ -444,11 +481,10 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
         if (tid == 0) SKB_TRACE(s, 4);
         tc_fence_after();
         const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16) + j * 2 * NT + ch * NCOL;
-        if constexpr (CELL == SKB_CELL_LSTM) {
+        if constexpr (kGated) {
           // gate g = warp (warp-uniform): sigmoid for i, f, o; tanh(x) = 2*sigmoid(2x)-1 for g.
           // act = mul / (1 + 2^(kl*z + kb)) + add, z = pre-activation without bias
-          float kl, kb, mul, add;
-          gate_consts<ACT>(qw, bias, kl, kb, mul, add);
+          const GateAct<CELL, ACT> act(qw, bias);
           float* g_out = sG + (qw * NT + ch * NCOL) * kGS + lane;
 #pragma unroll
           for (int c16 = 0; c16 < NCOL / 16; ++c16) {
@@ -460,7 +496,7 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
             for (int i = 0; i < 16; ++i) v[i] += two_chains ? v2[i] : 0.f;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              g_out[(c16 * 16 + i) * kGS] = gate_act<ACT>(v[i], kl, kb, mul, add);
+              g_out[(c16 * 16 + i) * kGS] = act(v[i]);
             }
           }
           tc_fence_before();
@@ -485,12 +521,8 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
             const bool live = t < s_len[n];
             uint32_t hw[UG / 2];
 #pragma unroll
-            for (int e = 0; e < UG; ++e) {
-              const float c2 = fmaf(g4[1][e], cc[p * UG + e], g4[0][e] * g4[2][e]);
-              const float h2 = g4[3][e] * cell_tanh<ACT>(c2);
-              cc[p * UG + e] = live ? c2 : cc[p * UG + e];
-              hp[p * UG + e] = live ? h2 : hp[p * UG + e];
-            }
+            for (int e = 0; e < UG; ++e)
+              cell_update<CELL, ACT>(g4[0][e], g4[1][e], g4[2][e], g4[3][e], cc[p * UG + e], hp[p * UG + e], live);
 #pragma unroll
             for (int e = 0; e < UG / 2; ++e) {
               __half2 h2 = __floats2half2_rn(hp[p * UG + 2 * e], hp[p * UG + 2 * e + 1]);
@@ -539,7 +571,7 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
         }
         // output sequence (stacked + transposed layout [R, T, H]); off the
         // critical path: the h_t exchange is already in flight.
-        if constexpr (CELL == SKB_CELL_LSTM) {
+        if constexpr (kGated) {
 #pragma unroll
           for (int p = 0; p < NP; ++p) {
             if (!pv[p]) continue;
@@ -568,7 +600,7 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
       SKB_TTRACE(tile_iter, 2);
       // final states (the frozen tail [len, max_len_p) of the output sequence is
       // written by rnn_fill_frozen_kernel from hT, off the recurrence)
-      if constexpr (CELL == SKB_CELL_LSTM) {
+      if constexpr (kGated) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           if (!pv[p]) continue;
@@ -673,7 +705,7 @@ __global__ void __launch_bounds__(EW * 32 + 64, 1) rnn_fwd_kernel(const RnnArgs 
 // image, the gate exchange; a single h buffer is safe because a lane only
 // multicasts h_{t+1} after every CTA's MMA of step t has retired (hempty: one
 // remote arrival per CTA per step).
-template <typename XT, int ACT = 1>
+template <typename XT, int ACT = 1, int CELL = SKB_CELL_LSTM>
 __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a) {
   constexpr int NT = 64, EWL = 8, kEpiL = EWL * 32, NCOL = NT / (EWL / 4), UG = 8;   // NT == kNT
   constexpr int kLoad0 = 16, kMma0 = 18;   // warps: 0-15 epilogue (lane = warp >> 3), 16-17 loaders, 18-19 MMA
@@ -787,8 +819,11 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a)
         tile_meta(tile_of(round + 1));
         if (m_r >= 0) {
           const char* h0n = reinterpret_cast<const char*>(a.h0 + (size_t)m_r * H);
-          const char* c0n = reinterpret_cast<const char*>(a.c0 + (size_t)m_r * H);
-          for (int off = 0; off < H * 4; off += 128) { prefetch_l2(h0n + off); prefetch_l2(c0n + off); }
+          const char* c0n = a.c0 ? reinterpret_cast<const char*>(a.c0 + (size_t)m_r * H) : nullptr;
+          for (int off = 0; off < H * 4; off += 128) {
+            prefetch_l2(h0n + off);
+            if (c0n) prefetch_l2(c0n + off);
+          }
         }
       }
       {
@@ -797,7 +832,12 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a)
         float hv[8], cv[8];
         if (r >= 0) {
           load_x8<float>(a.h0 + (size_t)r * H, unit0, H, hv);
-          load_x8<float>(a.c0 + (size_t)r * H, unit0, H, cv);
+          if (a.c0) {
+            load_x8<float>(a.c0 + (size_t)r * H, unit0, H, cv);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cv[k] = 0.f;
+          }
         } else {
 #pragma unroll
           for (int k = 0; k < 8; ++k) hv[k] = cv[k] = 0.f;
@@ -826,8 +866,7 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a)
         }
       };
       if (trip > 0) send_h(step);
-      float kl, kb, mul, add;
-      gate_consts<ACT>(qw, bias, kl, kb, mul, add);
+      const GateAct<CELL, ACT> act(qw, bias);
       for (int t = 0; t < trip; ++t) {
         const uint32_t s = step + t, j = s & 1, use = s >> 1;
         mbar_wait(&mdone[L][j], use & 1);
@@ -841,7 +880,7 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a)
           tmem_ld16(trow + c16 * 16, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) g_out[(c16 * 16 + i) * kGS] = gate_act<ACT>(v[i], kl, kb, mul, add);
+          for (int i = 0; i < 16; ++i) g_out[(c16 * 16 + i) * kGS] = act(v[i]);
         }
         tc_fence_before();
         __syncwarp();
@@ -861,12 +900,7 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a)
           }
           const bool live = t < s_len[L][pn];
 #pragma unroll
-          for (int k = 0; k < UG; ++k) {
-            const float c2 = fmaf(g4[1][k], cc[k], g4[0][k] * g4[2][k]);
-            const float h2 = g4[3][k] * cell_tanh<ACT>(c2);
-            cc[k] = live ? c2 : cc[k];
-            hp[k] = live ? h2 : hp[k];
-          }
+          for (int k = 0; k < UG; ++k) cell_update<CELL, ACT>(g4[0][k], g4[1][k], g4[2][k], g4[3][k], cc[k], hp[k], live);
         }
         if (t + 1 < trip) send_h(s + 1);
         else named_bar_sync(xch_bar, kEpiL);   // sG is rewritten next step only after every read
@@ -1277,8 +1311,9 @@ __global__ void rnn_pack_kernel(const PackArgs a) {
       const int k = kc * 8 + e;
       float v = 0.f;
       if (valid) {
-        if (k < a.F) v = ld_any(a.w[g], (size_t)k * a.H + unit, a.f64);
-        else if (k >= a.Kx && k - a.Kx < a.H) v = ld_any(a.u[g], (size_t)(k - a.Kx) * a.H + unit, a.f64);
+        if (k < a.F) v = a.w[g] ? ld_any(a.w[g], (size_t)k * a.H + unit, a.f64) : 0.f;   // NULL block: zeros (GRU n_h)
+        else if (k >= a.Kx && k - a.Kx < a.H)
+          v = a.u[g] ? ld_any(a.u[g], (size_t)(k - a.Kx) * a.H + unit, a.f64) : 0.f;   // (GRU n_x)
       }
       bad |= fp16_overflow(v);
       hv[e] = __float2half_rn(v);
@@ -1644,9 +1679,9 @@ inline bool rnn_dl() {
   return dl == 1;
 }
 
-template <typename XT, int ACT>
+template <typename XT, int ACT, int CELL = SKB_CELL_LSTM>
 int launch_dl(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
-  auto kern = rnn_fwd_dl_kernel<XT, ACT>;
+  auto kern = rnn_fwd_dl_kernel<XT, ACT, CELL>;
   constexpr int kThreads = 20 * 32;
   const size_t smem = (size_t)2 * (kNT * g.Kx * 2 + kNT * g.Kh * 2 + 4 * kNT * kGS * 4) + 1024;
   if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
@@ -1685,6 +1720,14 @@ int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
       return act ? launch_dl<XT, 1>(args, g, stream) : launch_dl<XT, 0>(args, g, stream);
     if (rnn_pp() && g.U == 32 && g.Kh == g.C * 32)
       return act ? launch_pp<XT, 1>(args, g, stream) : launch_pp<XT, 0>(args, g, stream);
+    if (rnn_ew() == 8)
+      return act ? launch_main_ew<CELL, XT, 8, 1>(args, g, stream) : launch_main_ew<CELL, XT, 8, 0>(args, g, stream);
+    return act ? launch_main_ew<CELL, XT, 16, 1>(args, g, stream) : launch_main_ew<CELL, XT, 16, 0>(args, g, stream);
+  }
+  if constexpr (CELL == SKB_CELL_GRU) {
+    const bool act = rnn_act() == 1;
+    if (rnn_dl() && rnn_ew() == 16 && g.U == 32 && g.H == g.C * 32 && g.Kh == g.H)
+      return act ? launch_dl<XT, 1, CELL>(args, g, stream) : launch_dl<XT, 0, CELL>(args, g, stream);
     if (rnn_ew() == 8)
       return act ? launch_main_ew<CELL, XT, 8, 1>(args, g, stream) : launch_main_ew<CELL, XT, 8, 0>(args, g, stream);
     return act ? launch_main_ew<CELL, XT, 16, 1>(args, g, stream) : launch_main_ew<CELL, XT, 16, 0>(args, g, stream);
@@ -1787,7 +1830,9 @@ extern "C" int skb_rnn_pack(const skb_rnn_shape* shape, const void* const* w_dev
   PackArgs a = {};
   for (int i = 0; i < g.G; ++i) {
     a.w[i] = w_dev[i]; a.u[i] = u_dev[i]; a.b[i] = b_dev[i];
-    if (!a.w[i] || !a.u[i] || !a.b[i]) return SKB_ERR_INVALID;
+    const bool gru_zero_block = g.cell == SKB_CELL_GRU && ((i == 3 && !a.w[i]) || (i == 2 && !a.u[i]));
+    if ((!a.w[i] || !a.u[i]) && !gru_zero_block) return SKB_ERR_INVALID;
+    if (!a.b[i]) return SKB_ERR_INVALID;
   }
   a.f64 = f64;
   a.slab = reinterpret_cast<uint8_t*>(packed_dev);
@@ -1862,6 +1907,8 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   int rc;
   if (g.cell == SKB_CELL_LSTM)
     rc = x_f64 ? launch_main<SKB_CELL_LSTM, double>(a, g, st) : launch_main<SKB_CELL_LSTM, float>(a, g, st);
+  else if (g.cell == SKB_CELL_GRU)
+    rc = x_f64 ? launch_main<SKB_CELL_GRU, double>(a, g, st) : launch_main<SKB_CELL_GRU, float>(a, g, st);
   else
     rc = x_f64 ? launch_main<SKB_CELL_RNN_TANH, double>(a, g, st) : launch_main<SKB_CELL_RNN_TANH, float>(a, g, st);
   if (rc) return rc;

@@ -97,6 +97,8 @@ def _render(spec) -> str:
 
 
 def _source_value(src, feeds):
+    if src is None:   # an all-zero weight block (GRU n_x has no U, n_h no W)
+        return None
     return feeds[src.name] if src.kind == "param" else src.value
 
 
@@ -212,7 +214,8 @@ class RnnExecutable:
         packed = _weights.get(key, weights)
         if packed is not None:
             return packed
-        dev = [[_to_device(w, torch.float64, self.device) for w in trip] for trip in weights]
+        dev = [[None if w is None else _to_device(w, torch.float64, self.device) for w in trip]
+               for trip in weights]
         ws_ = [t[0] for t in dev] + [dev[0][0]] * (4 - len(dev))
         us_ = [t[1] for t in dev] + [dev[0][1]] * (4 - len(dev))
         bs_ = []
@@ -227,7 +230,8 @@ class RnnExecutable:
         err = torch.zeros(4, dtype=torch.int32, device=self.device)
         st = self.rt.stream_handle(stream)
         self.rt.check(self.lib.skb_rnn_pack(
-            self.shape, P4(*[t.data_ptr() for t in ws_]), P4(*[t.data_ptr() for t in us_]),
+            self.shape, P4(*[t.data_ptr() if t is not None else None for t in ws_]),
+            P4(*[t.data_ptr() if t is not None else None for t in us_]),
             P4(*[t.data_ptr() for t in bs_]), 1, self.rt.ptr(packed), self.rt.ptr(err), st), "skb_rnn_pack")
         if int(err[0].item()) == E.SKB_ERR_FP16_RANGE:
             raise PrecisionRangeError("a weight exceeds the fp16 range (|w| > 65504) of the tensor-core path")
@@ -494,6 +498,8 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
             raise LoweringError("execute_many needs feed sets of one shape")
         for trip_src, trip in zip(prog.gates, weights):
             for s_, w in zip(trip_src, trip):
+                if s_ is None:
+                    continue
                 v = _source_value(s_, b)
                 if v is not w and not np.array_equal(as_numpy(v), as_numpy(w)):
                     raise LoweringError("execute_many needs one weight set shared by all feed sets")

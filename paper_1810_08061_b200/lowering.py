@@ -17,6 +17,8 @@ node list is dumped in SURVEY §8(a) A1):
   body:  x_t = Index(x_tm, idx)
          gate_k = act_k(MatMul(x_t, W_k) + MatMul(h, U_k) + b_k)   (any + order)
          LSTM: c' = f*c + i*g ; h' = o*tanh(c')     |  RNN: h' = tanh(...)
+         GRU (oracle/programs/gru.msl): z, r = sigmoid(x_t Wz + h Uz + bz), ...;
+              n = tanh(x_t Wn + bn + r * (h Un + bhn)); h' = (1 - z) * n + z * h
          mask = Lt(idx, seq_len); s = Where(mask, s', s) for each state
          outputs = ListAppend(outputs, h) ; idx' = idx + 1
 """
@@ -30,6 +32,7 @@ from .errors import LoweringError
 
 CELL_LSTM = 1
 CELL_RNN_TANH = 2
+CELL_GRU = 3
 
 
 @dataclass
@@ -57,7 +60,8 @@ class RnnProgram:
     lens: Source              # i64 [B]
     h0: Source
     c0: Optional[Source]
-    gates: list               # per gate (W, U, b) Sources; order i, f, g, o (LSTM) or (h,) RNN
+    gates: list               # per gate block (W, U, b) Sources; i, f, g, o (LSTM), (h,) RNN,
+                              # z, r, n_x = (Wn, None, bn), n_h = (None, Un, bhn) (GRU)
     outputs: list             # OutputSpec per graph output
     while_node: object = None
     index_node: object = None     # Index(x_tm, idx): IndexOutOfRange span
@@ -263,16 +267,76 @@ def lower_rnn_program(graph) -> RnnProgram:
             return None
         return ref.node.inputs[0]
 
+    def gru(new_h, h_k):
+        """h' = (1 - z) * n + z * h (either order of every + and *)."""
+        if not _is(new_h, "Add"):
+            return None
+        for a, b in (new_h.node.inputs, new_h.node.inputs[::-1]):
+            if not (_is(a, "Mul") and _is(b, "Mul")):
+                continue
+            for omz, n in (a.node.inputs, a.node.inputs[::-1]):
+                if not (_is(omz, "Sub") and _scalar_const(omz.node.inputs[0]) == 1 and _is(n, "Tanh")):
+                    continue
+                z = omz.node.inputs[1]
+                for zz, hh in (b.node.inputs, b.node.inputs[::-1]):
+                    if _same(zz, z) and B.is_state(hh, h_k) and _is(z, "Sigmoid"):
+                        return z, n
+        return None
+
+    def gru_candidate(n, h_k):
+        """n = tanh(x_t Wn + bn + r * (h Un + bhn)) -> (r ref, (Wn, None, bn), (None, Un, bhn))."""
+        terms = _flatten_add(n.node.inputs[0], [])
+        wn = bn = gated = None
+        for tr in terms:
+            if _is(tr, "MatMul") and tr.node.inputs[0].node is ix and wn is None:
+                cap = B.capture(tr.node.inputs[1])
+                if cap is None:
+                    _fail("GRU n-gate weight is not a captured value")
+                wn = _main_source(cap)
+            elif _is(tr, "Mul") and gated is None:
+                gated = tr
+            elif B.capture(tr) is not None and bn is None:
+                bn = _main_source(B.capture(tr))
+            else:
+                _fail("GRU n-gate is not x_t Wn + bn + r * (h Un + bhn)")
+        if wn is None or bn is None or gated is None:
+            _fail("GRU n-gate is not x_t Wn + bn + r * (h Un + bhn)")
+        for r, inner in (gated.node.inputs, gated.node.inputs[::-1]):
+            if not _is(r, "Sigmoid"):
+                continue
+            un = bhn = None
+            for tr in _flatten_add(inner, []):
+                if _is(tr, "MatMul") and B.is_state(tr.node.inputs[0], h_k) and un is None:
+                    cap = B.capture(tr.node.inputs[1])
+                    if cap is None:
+                        _fail("GRU Un is not a captured value")
+                    un = _main_source(cap)
+                elif B.capture(tr) is not None and bhn is None:
+                    bhn = _main_source(B.capture(tr))
+                else:
+                    un = None
+                    break
+            if un is not None and bhn is not None:
+                return r, (wn, None, bn), (None, un, bhn)
+        _fail("GRU reset gate does not multiply (h Un + bhn)")
+
     if len(tensor_states) == 1:
         (h_k, new_h, where_h), = tensor_states
-        pre = unary(new_h, "Tanh")
-        if pre is None:
-            _fail("single-state cell is not tanh(x W + h U + b)")
-        gates = [affine(pre, h_k)]
-        cell = CELL_RNN_TANH
         c_k = None
         if not _same(appended, where_h):
             _fail("output list does not collect the masked state")
+        pre = unary(new_h, "Tanh")
+        zn = gru(new_h, h_k) if pre is None else None
+        if pre is not None:
+            gates = [affine(pre, h_k)]
+            cell = CELL_RNN_TANH
+        elif zn is not None:
+            z_ref, n_ref = zn
+            r_ref, nx, nh = gru_candidate(n_ref, h_k)
+            gates = [affine(unary(z_ref, "Sigmoid"), h_k), affine(unary(r_ref, "Sigmoid"), h_k), nx, nh]
+            cell = CELL_GRU
+        else:
+            _fail("single-state cell is neither tanh(x W + h U + b) nor a GRU")
     elif len(tensor_states) == 2:
         # identify c: its new value is f*c + i*g ; h's new value is o*tanh(c')
         cell = CELL_LSTM
@@ -306,7 +370,7 @@ def lower_rnn_program(graph) -> RnnProgram:
         gates = [affine(unary(r, "Sigmoid" if r is not g_ref else "Tanh"), h_k)
                  for r in (i_ref, f_ref, g_ref, o_ref)]
     else:
-        _fail(f"{len(tensor_states)} tensor states (RNN has 1, LSTM 2)")
+        _fail(f"{len(tensor_states)} tensor states (RNN / GRU have 1, LSTM 2)")
 
     h0 = _main_source(init[h_k])
     c0 = _main_source(init[c_k]) if c_k is not None else None

@@ -28,9 +28,11 @@ from .values import ListValue, Tree
 
 
 def _sk():
-    import stagekit.errors as sk_errors
-    import stagekit.graph.execute as sk_execute
-    import stagekit.graph.tensor as sk_tensor
+    import importlib
+    sk_errors = importlib.import_module("stagekit.errors")
+    # (stagekit.graph re-exports the function `execute`, which shadows the module attribute)
+    sk_execute = importlib.import_module("stagekit.graph.execute")
+    sk_tensor = importlib.import_module("stagekit.graph.tensor")
     return sk_errors, sk_execute, sk_tensor
 
 

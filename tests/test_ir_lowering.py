@@ -11,7 +11,7 @@ from oracle import fixtures
 from paper_1810_08061_b200 import errors as E
 from paper_1810_08061_b200 import ir
 from paper_1810_08061_b200.executor import bind_feeds
-from paper_1810_08061_b200.lowering import CELL_LSTM, CELL_RNN_TANH, lower_rnn_program
+from paper_1810_08061_b200.lowering import CELL_GRU, CELL_LSTM, CELL_RNN_TANH, lower_rnn_program
 from paper_1810_08061_b200.validate import validate
 
 
@@ -37,9 +37,13 @@ def test_reference_graphs_lower_to_the_recurrent_kernel(name):
     case = fixtures.case_by_name(name)
     g = _graph(name)
     prog = lower_rnn_program(g)
-    assert prog.cell == (CELL_LSTM if case["cell"] == "lstm" else CELL_RNN_TANH)
+    assert prog.cell == {"lstm": CELL_LSTM, "gru": CELL_GRU}.get(case["cell"], CELL_RNN_TANH)
     assert prog.x.name == "input_data" and prog.lens.name == "sequence_len"
-    if case["cell"] == "lstm":
+    if case["cell"] == "gru":   # blocks z, r, n_x = (Wn, -, bn), n_h = (-, Un, bhn)
+        names = [tuple(s.name if s is not None else None for s in t) for t in prog.gates]
+        assert names == [("wz", "uz", "bz"), ("wr", "ur", "br"), ("wn", None, "bn"), (None, "un", "bhn")]
+        assert prog.h0.name == "h0" and prog.c0 is None
+    elif case["cell"] == "lstm":
         assert [t[0].name for t in prog.gates] == ["wi", "wf", "wg", "wo"]
         assert [t[1].name for t in prog.gates] == ["ui", "uf", "ug", "uo"]
         assert [t[2].name for t in prog.gates] == ["bi", "bf", "bg", "bo"]
