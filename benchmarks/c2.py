@@ -103,8 +103,7 @@ def run(args, rank, world, local_rank, clocks_cls):
         a.record(stream)
         tr.forward_backward(x, y, lens, max_len=n)
         b.record(stream)
-        from paper_1810_08061_b200.train import allreduce_
-        allreduce_(tr.grads)
+        tr.sync.reduce_(tr.grads)   # NCCL allreduce behind the libskb C ABI (skb_comm_allreduce)
         from paper_1810_08061_b200 import runtime as rt
         rt.check(tr.lib.skb_sgd_update(rt.ptr(tr.params), rt.ptr(tr.grads), tr.n_params, tr.lr,
                                        rt.stream_handle(None)), "skb_sgd_update")

@@ -281,6 +281,29 @@ skb_status skb_stream_run(const void* prog_dev, const int32_t* extra_dev, const 
                           int64_t smem_bytes, void* stream);   /* nprog: scalar instructions in prog_dev */
 
 /* ---------------------------------------------------------------------------
+ * Multi-GPU collective (SURVEY §8(b) skb_comm_init / skb_allreduce_f32; csrc/comm.cu).
+ * One rank per GPU; the training configs (C2 BPTT, C5 MAML) sum per-shard
+ * gradients with one NCCL allreduce over NVLink / NVSwitch, enqueued on the
+ * caller's stream.  NCCL is resolved at run time: the copy already loaded in
+ * the process (PyTorch's), else `nccl_path` of skb_comm_load, else the system
+ * libnccl.so.2.  The host exchanges the 128-byte unique id out of band.
+ * Replaces the reference's nothing: stagekit is single-process; these back the
+ * data-parallel trainers that replace its per-graph gradient() runs
+ * (graph/grad.py:35-70) and the hand BPTT program (oracle/programs/lstm_bptt.msl).
+ * ------------------------------------------------------------------------- */
+enum { SKB_DT_F32 = 0, SKB_DT_F64 = 1, SKB_DT_I32 = 2, SKB_DT_I64 = 3 };
+enum { SKB_OP_SUM = 0, SKB_OP_MAX = 1 };
+skb_status skb_comm_load(const char* nccl_path);      /* optional: NULL = default search */
+const char* skb_comm_last_error(void);
+int skb_comm_nccl_version(void);                       /* e.g. 22809, or -1 */
+skb_status skb_comm_unique_id(uint8_t* uid_out128);    /* rank 0 creates, host broadcasts */
+skb_status skb_comm_init(int rank, int world, const uint8_t* uid128, void** comm_out);
+skb_status skb_comm_allreduce(void* comm, void* buf_dev, int64_t n, int dtype, int op, void* stream);
+skb_status skb_allreduce_f32(void* comm, float* buf_dev, int64_t n, void* stream);   /* in place, sum */
+skb_status skb_allreduce_f64(void* comm, double* buf_dev, int64_t n, void* stream);
+skb_status skb_comm_destroy(void* comm);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics (GPU self-tests of the tcgen05 / DSMEM building blocks).
  * ------------------------------------------------------------------------- */
 skb_status skb_diag_umma_gemm(const void* a_dev, const void* b_dev, void* d_dev, int n, int k,

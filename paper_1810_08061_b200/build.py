@@ -53,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if res.returncode:
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda", "-lcublas"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda", "-lcublas", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode:
         sys.stderr.write(res.stdout + res.stderr)

@@ -3,8 +3,8 @@
 Replaces executing the reference's `gradient()` of the staged one-task MAML
 program (oracle/programs/maml.msl; graph/grad.py:35-70) task by task: one
 launch computes every task's second-order meta-gradient (one CTA per task)
-and their mean; `step` adds the cross-GPU mean (NCCL allreduce through
-torch.distributed, tasks sharded by rank) and the meta-SGD update.
+and their mean; `step` adds the cross-GPU mean (NCCL allreduce behind the
+libskb C ABI, comm.py; tasks sharded by rank) and the meta-SGD update.
 
     tr = MamlTrainer(hidden=40, shots=10, tasks=4096, alpha=0.01, beta=0.001)
     loss = tr.step(xs, ys, xq, yq)        # [tasks, shots] each
@@ -32,13 +32,15 @@ def unflatten(flat, H):
 
 class MamlTrainer:
     def __init__(self, hidden=40, shots=10, tasks=4096, alpha=0.01, beta=0.001, theta=None, seed=0, device=None,
-                 group=None):
+                 group=None, comm="auto"):
         import torch
         from . import runtime as rt
         self.lib = rt.lib()
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         self.H, self.K, self.tasks = hidden, shots, tasks
         self.alpha, self.beta, self.group = alpha, beta, group
+        from .comm import ShardedStep, default_comm
+        self.sync = ShardedStep(default_comm(group) if comm == "auto" else comm)
         self.P = hidden * hidden + 4 * hidden + 1
         if theta is None:
             rng = np.random.default_rng(seed)
@@ -64,12 +66,10 @@ class MamlTrainer:
         return self.grad, self.loss
 
     def step(self, xs, ys, xq, yq, stream=None):
-        import torch.distributed as dist
         from . import runtime as rt
-        from .train import allreduce_
         self.meta_grad(xs, ys, xq, yq, stream)
-        world = dist.get_world_size(self.group) if dist.is_available() and dist.is_initialized() else 1
-        allreduce_(self.grad, self.group)   # sum of per-rank task means -> lr / world below
-        rt.check(self.lib.skb_sgd_update(rt.ptr(self.theta), rt.ptr(self.grad), self.P, self.beta / world,
+        self.sync.reduce_(self.grad, stream)   # sum of per-rank task means (NCCL, C ABI) -> lr / world
+        lr = self.beta * self.sync.lr_scale(mean_of_means=True)
+        rt.check(self.lib.skb_sgd_update(rt.ptr(self.theta), rt.ptr(self.grad), self.P, lr,
                                          rt.stream_handle(stream)), "skb_sgd_update")
         return self.loss

@@ -88,6 +88,15 @@ SIGNATURES = {
     "skb_stream_tile_elems": (ctypes.c_int, []),
     "skb_stream_run": (ctypes.c_int, [_VP] * 8 + [ctypes.c_int64] + [ctypes.c_int] * 5 +
                        [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _VP]),
+    "skb_comm_load": (ctypes.c_int, [ctypes.c_char_p]),
+    "skb_comm_last_error": (ctypes.c_char_p, []),
+    "skb_comm_nccl_version": (ctypes.c_int, []),
+    "skb_comm_unique_id": (ctypes.c_int, [_VP]),
+    "skb_comm_init": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _VP, ctypes.POINTER(ctypes.c_void_p)]),
+    "skb_comm_allreduce": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _VP]),
+    "skb_allreduce_f32": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, _VP]),
+    "skb_allreduce_f64": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, _VP]),
+    "skb_comm_destroy": (ctypes.c_int, [_VP]),
     "skb_diag_umma_gemm": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP]),
     "skb_diag_cluster_exchange": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP, _VP, _VP]),
 }

@@ -1,8 +1,9 @@
 """Dynamic-length LSTM training on B200s (BASELINE config C2; csrc/train.cu).
 
 One `step` = forward over the staged While (per-row lengths), BPTT, the
-gradient allreduce across ranks (NCCL through torch.distributed — the only
-data-path collective of the backend) and the SGD update.  It replaces the
+gradient allreduce across ranks (NCCL behind the libskb C ABI,
+`skb_allreduce_f32` on the trainer's stream — the only data-path collective of
+the backend; comm.py) and the SGD update.  It replaces the
 reference's hand-derived staged BPTT program (oracle/programs/lstm_bptt.msl;
 the reference cannot differentiate a While, graph/grad.py:159-161).
 
@@ -20,25 +21,12 @@ import ctypes
 import numpy as np
 
 
-def shard_rows(global_batch: int, rank: int, world: int) -> slice:
-    """Rows of the global batch owned by `rank` (contiguous, sizes differ by <= 1)."""
-    lo = global_batch * rank // world
-    hi = global_batch * (rank + 1) // world
-    return slice(lo, hi)
-
-
-def allreduce_(flat, group=None):
-    """Sum a flat gradient buffer over the ranks of `group` in place (no-op
-    when torch.distributed is not initialised or the world is 1)."""
-    import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
-    return flat
+from .comm import ShardedStep, default_comm, shard_rows  # noqa: F401  (shard_rows: public)
 
 
 class LstmTrainer:
     def __init__(self, input_size, hidden, rows, time, global_batch=None, lr=0.1, math="tf32", seed=0,
-                 params=None, device=None, group=None, graph=True):
+                 params=None, device=None, group=None, graph=True, comm="auto"):
         import torch
         from . import runtime as rt
         self.lib = rt.lib()
@@ -46,6 +34,7 @@ class LstmTrainer:
         self.F, self.H, self.rows, self.time = input_size, hidden, rows, time
         self.lr = lr
         self.group = group
+        self.sync = ShardedStep(default_comm(group) if comm == "auto" else comm, global_batch or rows)
         G = 4 * hidden
         self.n_params = input_size * G + hidden * G + G
         if params is None:
@@ -81,7 +70,7 @@ class LstmTrainer:
     def step(self, x, y, lens, h0=None, c0=None, max_len=None, stream=None):
         from . import runtime as rt
         loss = self.forward_backward(x, y, lens, h0, c0, max_len, stream)
-        allreduce_(self.grads, self.group)
+        self.sync.reduce_(self.grads, stream)   # NCCL sum over ranks, on `stream` (C ABI)
         rt.check(self.lib.skb_sgd_update(rt.ptr(self.params), rt.ptr(self.grads), self.n_params, self.lr,
                                          rt.stream_handle(stream)), "skb_sgd_update")
         return loss
