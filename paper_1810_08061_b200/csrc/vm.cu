@@ -56,7 +56,7 @@ enum UnK : int32_t { U_NEG, U_NOT, U_TANH, U_SIGMOID };
 
 // error codes (include/skb.h) + VM-only kinds
 enum { E_INDEX = 10, E_EMPTY = 11, E_SHAPE = 12, E_DIV0 = 13, E_LIMIT = 14, E_ASSERT = 15,
-       E_DTYPE = 16, E_TYPE = 17, E_ARENA = 30, E_DEPTH = 32 };
+       E_DTYPE = 16, E_TYPE = 17, E_ARENA = 30, E_DEPTH = 32, E_OVERFLOW = 33 };
 constexpr int kMaxCallDepth = 1 << 16;
 
 struct VmCtl {            // device control block
@@ -125,6 +125,22 @@ __device__ double py_fmod(double a, double b) {   // Python float %: sign of the
   if (r != 0.0 && ((r < 0.0) != (b < 0.0))) r += b;
   return r;
 }
+// i64 arithmetic with overflow detection: the reference's ints are unbounded
+// Python ints (tensor.py), so a result outside int64 cannot be represented on
+// the device — it is reported (E_OVERFLOW), never wrapped.
+__device__ __forceinline__ bool add_ovf(int64_t x, int64_t y, int64_t& r) {
+  r = (int64_t)((uint64_t)x + (uint64_t)y);
+  return ((x ^ r) & (y ^ r)) < 0;
+}
+__device__ __forceinline__ bool sub_ovf(int64_t x, int64_t y, int64_t& r) {
+  r = (int64_t)((uint64_t)x - (uint64_t)y);
+  return ((x ^ y) & (x ^ r)) < 0;
+}
+__device__ __forceinline__ bool mul_ovf(int64_t x, int64_t y, int64_t& r) {
+  r = (int64_t)((uint64_t)x * (uint64_t)y);
+  return __mul64hi(x, y) != (r >> 63);
+}
+
 __device__ int64_t py_imod(int64_t a, int64_t b) {
   int64_t r = a % b;
   if (r != 0 && ((r < 0) != (b < 0))) r += b;
@@ -288,7 +304,8 @@ __device__ void op_binop(Vm& vm, const VmIns& in) {
           if (y == 0) { vm.fail(E_DIV0, in.uid, 0); continue; }
           r = py_imod(x, y);
         } else {
-          r = kind == B_ADD ? x + y : kind == B_SUB ? x - y : x * y;
+          const bool ovf = kind == B_ADD ? add_ovf(x, y, r) : kind == B_SUB ? sub_ovf(x, y, r) : mul_ovf(x, y, r);
+          if (ovf) { vm.fail(E_OVERFLOW, in.uid, 0); continue; }
         }
         st_i(po, i, r);
       }

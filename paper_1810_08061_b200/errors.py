@@ -79,3 +79,9 @@ STATUS_TO_CAUSE = {
     15: ASSERTION_FAILED,
 }
 SKB_ERR_FP16_RANGE = 20
+
+
+class IntegerOverflow(SkbError):
+    """An i64 result outside int64.  The reference's integers are unbounded
+    Python ints (graph/tensor.py); the device computes in int64 and reports
+    the overflow instead of wrapping."""

@@ -212,10 +212,14 @@ def as_numpy(v) -> np.ndarray:
         return v
     if isinstance(v, np.generic):
         return np.asarray(v)
-    if hasattr(v, "dtype") and hasattr(v, "shape") and hasattr(v, "data"):
-        # the reference's TensorValue: row-major tuple
-        return np.asarray(v.data, dtype=NP_DTYPE[v.dtype]).reshape(tuple(v.shape))
-    return np.asarray(v)
+    try:
+        if hasattr(v, "dtype") and hasattr(v, "shape") and hasattr(v, "data"):
+            # the reference's TensorValue: row-major tuple
+            return np.asarray(v.data, dtype=NP_DTYPE[v.dtype]).reshape(tuple(v.shape))
+        return np.asarray(v)
+    except OverflowError:   # a Python int beyond int64 (the reference's ints are unbounded)
+        from .errors import IntegerOverflow
+        raise IntegerOverflow("an integer value exceeds int64, the device's integer type") from None
 
 
 def allclose(a, b, rel: float) -> bool:

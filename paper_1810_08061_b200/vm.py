@@ -67,6 +67,7 @@ CAUSE = {10: E.INDEX_OUT_OF_RANGE, 11: E.EMPTY_POP, 12: E.SHAPE_MISMATCH, 13: E.
 E_ARENA = 30
 E_STEPS = 31
 E_DEPTH = 32
+E_OVERFLOW = 33
 
 VAL_DTYPE = np.dtype([("view", "<i8"), ("own", "<i8"), ("own_cap", "<i8"), ("numel", "<i8"),
                       ("dtype", "<i4"), ("rank", "<i4"), ("shape", "<i4", (MAX_RANK,))])
@@ -422,7 +423,12 @@ def compile_graph(graph) -> Program:
 # ---------------------------------------------------------------- runtime
 def _words(arr, dtype):
     """Host value -> int64 words (f64 bit patterns, i64, bool as 0/1)."""
-    a = np.ascontiguousarray(arr)
+    try:
+        a = np.ascontiguousarray(arr)
+    except OverflowError:
+        raise E.IntegerOverflow("an integer constant or feed exceeds int64 (the reference's ints are unbounded)")
+    if a.dtype == object:
+        raise E.IntegerOverflow("an integer constant or feed exceeds int64 (the reference's ints are unbounded)")
     if dtype == "f64":
         return a.astype(np.float64).view(np.int64).reshape(-1)
     return a.astype(np.int64).reshape(-1)
@@ -532,6 +538,8 @@ def run(prog: Program, feeds: dict, *, stream=None, arena_bytes: Optional[int] =
             raise E.IterationLimitExceeded(f"loop exceeded max_iterations={limit}", span)
         if err in CAUSE:
             raise RuntimeGraphError(_message(err, node, int(c[1])), span, CAUSE[err])
+        if err == E_OVERFLOW:
+            raise E.IntegerOverflow(f"int64 overflow at node {err_uid} (the reference's ints are unbounded)", span)
         if err == E_DEPTH:
             raise E.DeviceError(f"recursion deeper than {int(c[1])} calls at node {err_uid}")
         raise E.DeviceError(f"VM failure code {err} at node {err_uid}")

@@ -51,3 +51,19 @@ def test_recursive_funccall_programs(prog):
     call stack: outputs, print logs (pre-order effects) and the AssertionFailed
     raised 1 call deep equal the reference executor's."""
     _check(prog["graph"], prog["feeds"], prog["expected"])
+
+
+def test_int64_overflow_is_reported_not_wrapped():
+    """The reference's ints are unbounded Python ints; the VM computes in int64
+    and raises IntegerOverflow where a result leaves int64 (never wraps)."""
+    import numpy as np
+    from paper_1810_08061_b200 import sexpr
+    from paper_1810_08061_b200.errors import IntegerOverflow
+    g = sexpr.from_sexpr("(def main ((x i64)) (mul x x))")
+    ok = execute(g, {"x": np.asarray(3_000_000_000, dtype=np.int64)})
+    assert int(ok.outputs[0].item()) == 9_000_000_000_000_000_000
+    with pytest.raises(IntegerOverflow):
+        execute(g, {"x": np.asarray(4_000_000_000, dtype=np.int64)})
+    g2 = sexpr.from_sexpr("(def main ((x i64)) (sub x 2))")
+    with pytest.raises(IntegerOverflow):
+        execute(g2, {"x": np.asarray(-(2 ** 63) + 1, dtype=np.int64)})

@@ -51,7 +51,7 @@ def main():
 
     ref_execute = diff.execute
     counts_ref, counts_skb = {}, {}
-    disagreements, crashes, plans = [], [], {}
+    disagreements, crashes, overflow = [], [], []
     t_ref = t_skb = 0.0
     for seed in range(args.start, args.start + args.seeds):
         diff.execute = ref_execute
@@ -62,6 +62,9 @@ def main():
         t0 = time.perf_counter()
         try:
             skb_reports = diff.diff_seed(seed)
+        except executor.E.IntegerOverflow as exc:   # Python ints beyond int64: unrepresentable on the device
+            overflow.append({"seed": seed, "error": str(exc)[:200]})
+            continue
         except Exception as exc:   # anything that is not a reference error class
             crashes.append({"seed": seed, "error": f"{type(exc).__name__}: {exc}"[:300]})
             continue
@@ -90,6 +93,7 @@ def main():
         "disagreement_samples": disagreements[:20],
         "crashes": crashes[:20],
         "n_crashes": len(crashes),
+        "int64_overflow_seeds": overflow,
         "seconds_reference_executor": round(t_ref, 1),
         "seconds_skb": round(t_skb, 1),
         "corpus": None if corpus is None else {"total": corpus.total, "passed": corpus.passed,
