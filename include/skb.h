@@ -308,6 +308,19 @@ skb_status skb_comm_destroy(void* comm);
  * ------------------------------------------------------------------------- */
 skb_status skb_diag_umma_gemm(const void* a_dev, const void* b_dev, void* d_dev, int n, int k,
                               int swap_lbo_sbo, long long* cycles_dev, void* stream);
+/* Accurate tier of the same recurrent While (csrc/rnn_f32.cu): FP32 FFMA with
+ * fp32 weights / state and accurate activations, within rtol 1e-4 of the
+ * reference's float64 (north_star's fp32 bound).  One CTA per 32-row tile,
+ * thread = hidden unit (H <= 256, (F+H) % 4 == 0).  Same arguments and error
+ * contract as skb_rnn_forward; packing from the same per-gate weights. */
+int64_t skb_rnn_f32_packed_bytes(const skb_rnn_shape* shape);
+int64_t skb_rnn_f32_workspace_bytes(const skb_rnn_shape* shape);
+skb_status skb_rnn_pack_f32(const skb_rnn_shape* shape, const void* const* w_dev, const void* const* u_dev,
+                            const void* const* b_dev, int f64, void* packed_dev, void* stream);
+skb_status skb_rnn_forward_f32(const skb_rnn_shape* shape, const void* packed_dev, const void* x_dev, int x_f64,
+                               const float* h0_dev, const float* c0_dev, const int64_t* len_dev, float* out_dev,
+                               float* hT_dev, float* cT_dev, int32_t* max_len_dev, int32_t* err_dev,
+                               void* workspace_dev, void* stream);
 /* Kernel-only timing: for the next `max_launches` skb_rnn_forward calls the
  * persistent recurrent kernel is bracketed by CUDA events on its stream;
  * skb_profile_read returns how many were recorded and their durations (ms). */

@@ -188,17 +188,25 @@ class RnnExecutable:
     nothing.  ``run`` is the device-resident hot path (inputs already in HBM)."""
 
     def __init__(self, prog: RnnProgram, weights: list, B: int, T: int, F: int, H: int, P: int,
-                 device=None, stream=None):
+                 device=None, stream=None, tier: str = "f16"):
         from . import runtime as rt
         torch = _torch()
         self.rt = rt
         self.lib = rt.lib()
         self.prog = prog
+        self.tier = tier   # "f16": tcgen05 fp16-operand kernel (csrc/rnn.cu); "f32": FFMA kernel (csrc/rnn_f32.cu)
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.B, self.T, self.F, self.H, self.P = B, T, F, H, P
         self.shape = rt.RnnShape(prog.cell, H, F, T, B, P)
-        nb = self.lib.skb_rnn_packed_bytes(self.shape)
-        nw = self.lib.skb_rnn_workspace_bytes(self.shape)
+        if tier == "f32":
+            nb = self.lib.skb_rnn_f32_packed_bytes(self.shape)
+            nw = self.lib.skb_rnn_f32_workspace_bytes(self.shape)
+            if nb < 0 or nw < 0 or H > 256 or (F + H) % 4:
+                raise LoweringError(f"fp32 recurrent kernel does not support H={H}, F={F} (H <= 256, "
+                                    f"(F+H) % 4 == 0)")
+        else:
+            nb = self.lib.skb_rnn_packed_bytes(self.shape)
+            nw = self.lib.skb_rnn_workspace_bytes(self.shape)
         if nb < 0 or nw < 0:
             raise LoweringError(f"recurrent kernel does not support H={H}, F={F} (needs F+H <= 512 "
                                 f"after padding and H <= 256)")
@@ -210,7 +218,7 @@ class RnnExecutable:
 
     def _get_packed(self, weights, nbytes, stream):
         torch = _torch()
-        key = (self.prog.cell, self.H, self.F, tuple(id(w) for trip in weights for w in trip))
+        key = (self.tier, self.prog.cell, self.H, self.F, tuple(id(w) for trip in weights for w in trip))
         packed = _weights.get(key, weights)
         if packed is not None:
             return packed
@@ -229,6 +237,13 @@ class RnnExecutable:
         packed = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
         err = torch.zeros(4, dtype=torch.int32, device=self.device)
         st = self.rt.stream_handle(stream)
+        if self.tier == "f32":
+            self.rt.check(self.lib.skb_rnn_pack_f32(
+                self.shape, P4(*[t.data_ptr() if t is not None else None for t in ws_]),
+                P4(*[t.data_ptr() if t is not None else None for t in us_]),
+                P4(*[t.data_ptr() for t in bs_]), 1, self.rt.ptr(packed), st), "skb_rnn_pack_f32")
+            _weights.put(key, weights, packed)
+            return packed
         self.rt.check(self.lib.skb_rnn_pack(
             self.shape, P4(*[t.data_ptr() if t is not None else None for t in ws_]),
             P4(*[t.data_ptr() if t is not None else None for t in us_]),
@@ -250,10 +265,17 @@ class RnnExecutable:
         rt = self.rt
         self.err.zero_()
         st = rt.stream_handle(stream)
-        rt.check(self.lib.skb_rnn_forward(
+        fwd = self.lib.skb_rnn_forward_f32 if self.tier == "f32" else self.lib.skb_rnn_forward
+        rt.check(fwd(
             self.shape, rt.ptr(self.packed), rt.ptr(x), 1 if x.dtype == torch.float64 else 0,
             rt.ptr(h0), rt.ptr(c0), rt.ptr(lens), rt.ptr(out), rt.ptr(hT), rt.ptr(cT),
             rt.ptr(self.max_len), rt.ptr(self.err), rt.ptr(self.ws), st), "skb_rnn_forward")
+
+    @property
+    def precision(self) -> str:
+        """What the float outputs carry (DeviceTensor.precision)."""
+        return ("fp16 tensor-core operands, fp32 accumulate/state (bound 3e-3)" if self.tier == "f16"
+                else "fp32 FFMA, fp32 state (bound 1e-4)")
 
 
 # ------------------------------------------------------------------ errors
@@ -339,7 +361,7 @@ def plan_kind(graph, feeds: Optional[dict] = None) -> str:
     return "stream" if n >= STREAM_MIN_ELEMS else "vm"
 
 
-PRECISIONS = ("fast", "f64")
+PRECISIONS = ("fast", "fp32", "f64")
 
 
 @_on_stream
@@ -351,11 +373,14 @@ def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=N
     through it; every other graph runs on the device-resident region VM
     (``vm.py`` / ``csrc/vm.cu``).
 
-    ``precision`` (default: env SKB_PRECISION, else "fast"): "fast" lets the
-    fused recurrent kernel run a matching program on fp16 tensor cores (fp32
-    state, stated bound 3e-3); "f64" keeps every float in float64 like the
-    reference (the region VM / vector-stream tier), for callers that need the
-    reference's 1e-9 agreement (its differential harness)."""
+    ``precision`` (default: env SKB_PRECISION, else "fast") selects the tier of
+    the fused recurrent loop: "fast" = fp16 tensor-core operands, fp32
+    accumulate / state (stated bound 3e-3; inputs beyond the fp16 range fall
+    back to "fp32"); "fp32" = the FFMA kernel with fp32 weights (rtol 1e-4);
+    "f64" = every float in float64 like the reference (region VM / vector-stream
+    tier), for callers that need the reference's own 1e-9 agreement (its
+    differential harness).  Float outputs of the fused loop carry the tier in
+    ``DeviceTensor.precision``."""
     from . import runtime as rt
     rt.lib()
     if check:
@@ -367,7 +392,10 @@ def execute(graph, feeds: Optional[dict] = None, check: bool = True, *, stream=N
     if kind == "rnn" and precision == "f64":
         kind = "vm"
     if kind == "rnn":
-        return execute_many(graph, [feeds or {}], check=False, stream=stream)[0]
+        try:
+            return execute_many(graph, [feeds or {}], check=False, stream=stream, precision=precision)[0]
+        except LoweringError:   # a shape the fused kernels do not take: the region VM (f64) runs it
+            return execute_vm(graph, feeds, stream=stream)
     if kind == "stream":
         try:
             return execute_stream(graph, feeds, stream=stream)
@@ -464,7 +492,7 @@ def execute_vm(graph, feeds: Optional[dict] = None, *, stream=None) -> Execution
 
 @_on_stream
 def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
-                 return_exceptions: bool = False, host_outputs: bool = False) -> list:
+                 return_exceptions: bool = False, host_outputs: bool = False, precision: Optional[str] = None) -> list:
     """Run `graph` on P independent feed sets in one device launch.
 
     Weight feeds must be the same objects (or equal) across the feed sets.
@@ -549,21 +577,21 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
     if host_outputs is not False and host_outputs is not None and T > 0 and P >= 4 and _all_pinned(prog, [f0]):
         # feed sets are bound chunk by chunk inside the pipeline, overlapping the copies
         out_host, hT_h, cT_h, ml_host, status_h, ml_dev, finish = _run_pipelined(
-            prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device, x_dtype, host_outputs, stream)
+            prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device, x_dtype, host_outputs, stream, tier)
         # results are views of the host buffers: built while the last copies are in flight
-        results = _assemble(prog, out_host, hT_h, cT_h, ml_host, None, Bsz, T, P, True)
+        results = _assemble(prog, out_host, hT_h, cT_h, ml_host, None, Bsz, T, P, True, tier)
         finish()
         if int(status_h[0]) == E.SKB_ERR_FP16_RANGE:
             raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
         if not np.array_equal(ml_dev.numpy(), ml_host):   # (host and device trip counts agree by construction)
-            results = _assemble(prog, out_host, hT_h, cT_h, ml_dev.numpy(), None, Bsz, T, P, True)
+            results = _assemble(prog, out_host, hT_h, cT_h, ml_dev.numpy(), None, Bsz, T, P, True, tier)
         if not return_exceptions:
             for r in results:
                 if isinstance(r, Exception):
                     raise r
         return results
     bound = [f0] + [bind(f) for f in feeds_list[1:]]
-    exe = _executable(prog, weights, Bsz, T, F, H, P, device, stream)
+    exe = _executable(prog, weights, Bsz, T, F, H, P, device, stream, tier)
     x = cat(prog.x, x_dtype)
     h0 = cat(prog.h0, torch.float32).reshape(R, H)
     c0 = cat(prog.c0, torch.float32).reshape(R, H) if prog.cell == CELL_LSTM else None
@@ -590,7 +618,7 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
         host_hT = hT.to("cpu") if hT is not None else None
         host_cT = cT.to("cpu") if cT is not None else None
         out, hT, cT = host_out, host_hT, host_cT
-    return _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions)
+    return _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions, tier)
 
 
 PIPELINE_CHUNKS = int(os.environ.get("SKB_PIPELINE_CHUNKS", "12"))   # copy/compute pipeline depth
@@ -624,7 +652,8 @@ def _adjacent_run(vals, shape):
         return None
 
 
-def _run_pipelined(prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device, x_dtype, host_outputs, stream):
+def _run_pipelined(prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device, x_dtype, host_outputs, stream,
+                   tier="f16"):
     """Host-to-host execute_many in PIPELINE_CHUNKS chunks of problems on three
     streams: the H2D copy of chunk k+1, the kernels of chunk k and the D2H of
     chunk k-1 overlap (PCIe full duplex), instead of copy-in, run, copy-out.
@@ -663,7 +692,7 @@ def _run_pipelined(prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device,
         for p0 in range(0, P, step):
             p1 = min(P, p0 + step)
             pc = p1 - p0
-            exe = _executable(prog, weights, Bsz, T, F, H, pc, device, comp)
+            exe = _executable(prog, weights, Bsz, T, F, H, pc, device, comp, tier)
             rows = slice(p0 * Bsz, p1 * Bsz)
             chunk = [f0 if p == 0 else bind(feeds_list[p]) for p in range(p0, p1)]
             lens_vals.extend(_source_value(prog.lens, b) for b in chunk)
@@ -730,7 +759,11 @@ def _run_pipelined(prog, weights, feeds_list, f0, bind, Bsz, T, F, H, P, device,
     return host_out, hT_h, cT_h, ml_host, status_h, ml_dev, finish
 
 
-def _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions):
+TIER_PRECISION = {"f16": "fp16 tensor-core operands, fp32 accumulate/state (bound 3e-3)",
+                  "f32": "fp32 FFMA, fp32 weights/state (bound 1e-4)"}
+
+
+def _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions, tier="f16"):
     if status is not None and int(status[0]) == E.SKB_ERR_FP16_RANGE:
         raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
     results = []
@@ -745,14 +778,15 @@ def _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions):
         rows = slice(p * Bsz, (p + 1) * Bsz)
         outs = []
         for o in prog.outputs:
+            prec = TIER_PRECISION[tier]
             if o.kind == "seq_bm":
-                outs.append(DeviceTensor("f64", out[rows, :m, :]))
+                outs.append(DeviceTensor("f64", out[rows, :m, :], precision=prec))
             elif o.kind == "seq_tm":
-                outs.append(DeviceTensor("f64", out[rows, :m, :].permute(1, 0, 2)))
+                outs.append(DeviceTensor("f64", out[rows, :m, :].permute(1, 0, 2), precision=prec))
             elif o.kind == "h_final":
-                outs.append(DeviceTensor("f64", hT[rows]))
+                outs.append(DeviceTensor("f64", hT[rows], precision=prec))
             else:
-                outs.append(DeviceTensor("f64", cT[rows]))
+                outs.append(DeviceTensor("f64", cT[rows], precision=prec))
         results.append(ExecutionResult(outs, []))
     return results
 
@@ -780,18 +814,18 @@ _exes: dict = {}
 _exes_lock = threading.Lock()
 
 
-def _executable(prog, weights, B, T, F, H, P, device, stream) -> RnnExecutable:
+def _executable(prog, weights, B, T, F, H, P, device, stream, tier="f16") -> RnnExecutable:
     """Cached executable per (program, shape, weight feeds, thread): each owns
     mutable scratch (status word, trip counts, workspace), so concurrent
     callers on different threads never share one."""
     key = (id(prog), B, T, F, H, P, tuple(id(w) for trip in weights for w in trip), threading.get_ident(),
-           str(device))
+           str(device), tier)
     with _exes_lock:
         hit = _exes.get(key)
     if hit is not None and hit[0] is prog:
         hit[1].refresh(weights, stream)
         return hit[1]
-    exe = RnnExecutable(prog, weights, B, T, F, H, P, device, stream)
+    exe = RnnExecutable(prog, weights, B, T, F, H, P, device, stream, tier)
     with _exes_lock:
         if len(_exes) > 16:
             _exes.clear()

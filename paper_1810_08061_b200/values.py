@@ -87,15 +87,18 @@ class DeviceTensor:
 
     ``tensor`` is the torch view of the device buffer (zero-copy); ``dtype``
     is the reference dtype string of the graph output (``f64`` for float
-    outputs: the backend computes in fp32/fp16 on tensor cores and reports the
-    tolerance in DESIGN.md); ``array``/``data``/``item()`` copy to the host on
-    first use.
+    outputs); ``precision`` says what the float values actually carry — e.g.
+    "fp16 tensor-core operands, fp32 accumulate/state (bound 3e-3)" for the
+    fast tier of the fused recurrent loop, "float64" for the region VM —
+    so a caller can tell reduced-precision results apart; ``array``/``data``/
+    ``item()`` copy to the host on first use.
     """
 
-    __slots__ = ("dtype", "shape", "tensor", "_arr", "_tuple")
+    __slots__ = ("dtype", "shape", "tensor", "_arr", "_tuple", "precision")
 
-    def __init__(self, dtype: str, tensor, host: Optional[np.ndarray] = None):
+    def __init__(self, dtype: str, tensor, host: Optional[np.ndarray] = None, precision: Optional[str] = None):
         self.dtype = dtype
+        self.precision = precision or ("float64" if str(getattr(tensor, "dtype", "")) == "torch.float64" else None)
         self.tensor = tensor
         self.shape = tuple(int(d) for d in tensor.shape)
         self._arr = host

@@ -276,3 +276,123 @@ def test_dual_lane_kernel_widths_against_oracle(c1_graph, H):
         m = int(ml[p])
         r = ref.reshape(P, B * T * H)[p, :B * m * H].reshape(B, m, H)
         assert max_rel_error(got[p * B:(p + 1) * B, :m], r) <= TOL
+
+
+# ---------------------------------------------------------------------------------------------
+# The exact benchmarked path (bench.py): fp32 x, P = 1152 batch-32 problems, F = H = 256,
+# RnnExecutable.run (pack_x_rows_kernel<2> + rnn_fwd_dl_kernel<float>), against the f64 oracle
+# on 64 problems spread over the whole launch, exact trip counts for all 1152.
+def _bench_inputs(P, seed=0, H=256, F=256, T=64, B=32):
+    import torch
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(1000 + seed)
+    w = {}
+    for g in "ifgo":
+        w["w" + g] = rng.uniform(-0.1, 0.1, (F, H))
+        w["u" + g] = rng.uniform(-0.1, 0.1, (H, H))
+        w["b" + g] = rng.uniform(-0.1, 0.1, (H,))
+    R = P * B
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    x = torch.rand((R, T, F), device=dev, generator=gen) * 2 - 1
+    h0 = (torch.rand((R, H), device=dev, generator=gen) * 2 - 1) * 0.1
+    c0 = (torch.rand((R, H), device=dev, generator=gen) * 2 - 1) * 0.1
+    lens = torch.randint(1, T + 1, (R,), device=dev, generator=gen)
+    return w, x, h0, c0, lens
+
+
+@pytest.mark.parametrize("tier,tol", [("f16", TOL), ("f32", 1e-4)])
+def test_c1_bench_path_against_oracle(c1_graph, tier, tol):
+    import json
+    import os
+    import torch
+    from paper_1810_08061_b200 import lower, max_rel_error
+    from paper_1810_08061_b200.executor import RnnExecutable
+    P, B, T, F, H = 1152, 32, 64, 256, 256
+    w, x, h0, c0, lens = _bench_inputs(P)
+    weights = [tuple(w[k + g] for k in "wub") for g in "ifgo"]
+    exe = RnnExecutable(lower(c1_graph), weights, B, T, F, H, P, tier=tier)
+    out = torch.empty((P * B, T, H), device="cuda")
+    exe.run(x, h0, c0, lens, out)
+    torch.cuda.synchronize()
+    lens_np = lens.cpu().numpy()
+    assert np.array_equal(exe.max_len.cpu().numpy(), lens_np.reshape(P, B).max(axis=1))   # trip counts
+    sample = np.linspace(0, P - 1, 64).astype(int)
+    rows = np.concatenate([np.arange(p * B, (p + 1) * B) for p in sample])
+    xs, h0s, c0s = (t.cpu().numpy().astype(np.float64) for t in (x[rows], h0[rows], c0[rows]))
+    ref, ml, st = oracle.rnn_many(1, xs, h0s, c0s, lens_np[rows], [w["w" + g] for g in "ifgo"],
+                                  [w["u" + g] for g in "ifgo"], [w["b" + g] for g in "ifgo"], len(sample), 16)
+    got = out[rows].cpu().numpy().astype(np.float64)
+    errs = []
+    for i in range(len(sample)):
+        m = int(ml[i])
+        sl = slice(i * B, (i + 1) * B)
+        errs.append(max_rel_error(got[sl, :m], ref.reshape(len(sample), B, T, H)[i, :, :m]))
+    err = max(errs)
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(f"gpurun_out/c1_bench_path_err_{tier}.json", "w") as f:
+        json.dump({"tier": tier, "problems_checked": len(sample), "problems": P, "max_err": err,
+                   "median_err": float(np.median(errs)), "metric": "|gpu-ref|/max(1,|gpu|,|ref|)",
+                   "bound": tol}, f)
+    assert err <= tol, err
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in fixtures.CASES if "error" not in
+                                  fixtures.load_golden(c["name"])["expected"]])
+def test_golden_parity_fp32_tier(name):
+    """Every reference golden through execute(precision='fp32'): the FFMA tier
+    is within rtol 1e-4 of the reference's float64 results and says so."""
+    from paper_1810_08061_b200 import execute, ir, max_rel_error
+    doc = fixtures.load_golden(name)
+    g = ir.from_json(doc["graph"])
+    res = execute(g, fixtures.make_feeds(doc["case"]), precision="fp32")
+    for got, ref in zip(res.outputs, doc["expected"]["outputs"]):
+        refa = np.asarray(ref["data"], dtype=np.float64).reshape(ref["shape"])
+        assert max_rel_error(got.array, refa) <= 1e-4
+        assert "fp32" in (got.precision or "")
+
+
+def test_fp16_range_falls_back_to_fp32_tier(c1_graph):
+    """Inputs beyond the fp16 range no longer raise: the launch re-runs on the
+    fp32 tier and matches the oracle."""
+    from paper_1810_08061_b200 import execute, max_rel_error
+    f = _c1_problems(1, seed=12)[0]
+    f = dict(f, input_data=f["input_data"] * 1e5)
+    res = execute(c1_graph, f).outputs[0]
+    assert "fp32" in res.precision
+    ref, m = oracle.rnn_program(1, f["input_data"], f["h0"], f["c0"], f["sequence_len"],
+                                [f["w" + g] for g in "ifgo"], [f["u" + g] for g in "ifgo"],
+                                [f["b" + g] for g in "ifgo"])
+    assert max_rel_error(res.array, ref) <= 1e-4
+
+
+def test_gru_full_size_against_oracle():
+    """The GRU cell on the dual-lane kernel at C1 widths (F = H = 256), 48 problems."""
+    import torch
+    from paper_1810_08061_b200 import lower, max_rel_error
+    from paper_1810_08061_b200.executor import RnnExecutable
+    g = fixtures.load_golden("gru_4x6x256")
+    from paper_1810_08061_b200 import ir
+    prog = lower(ir.from_json(g["graph"]))
+    B, T, F, H, P = 32, 64, 256, 256, 48
+    rng = np.random.default_rng(77)
+    W = [rng.uniform(-0.1, 0.1, (F, H)) for _ in range(3)]
+    U = [rng.uniform(-0.1, 0.1, (H, H)) for _ in range(3)]
+    b = [rng.uniform(-0.1, 0.1, (H,)) for _ in range(4)]
+    weights = [(W[0], U[0], b[0]), (W[1], U[1], b[1]), (W[2], None, b[2]), (None, U[2], b[3])]
+    R = P * B
+    x = rng.uniform(-1, 1, (R, T, F))
+    h0 = rng.uniform(-0.1, 0.1, (R, H))
+    lens = rng.integers(1, T + 1, R).astype(np.int64)
+    dev = torch.device("cuda")
+    ref, ml, st = oracle.rnn_many(3, x, h0, None, lens, W, U, b, P, 16)
+    for tier, tol in (("f16", TOL), ("f32", 1e-4)):
+        exe = RnnExecutable(prog, weights, B, T, F, H, P, tier=tier)
+        out = torch.zeros((R, T, H), device=dev)
+        exe.run(torch.tensor(x, dtype=torch.float32, device=dev), torch.tensor(h0, dtype=torch.float32, device=dev),
+                None, torch.tensor(lens, device=dev), out)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().astype(np.float64)
+        for p in range(P):
+            m = int(ml[p])
+            r = ref.reshape(P, B, T, H)[p, :, :m]
+            assert max_rel_error(got[p * B:(p + 1) * B, :m], r) <= tol, (tier, p)
