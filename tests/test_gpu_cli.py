@@ -32,6 +32,6 @@ def test_run_tree_program(tmp_path, capsys):
 
 def test_runtime_failure_exit_code(tmp_path, capsys):
     g = tmp_path / "div.sexpr"
-    g.write_text("(def main ((x f64)) (div x 0.0))")
+    g.write_text("(def main ((x f64)) (div x (const f64 0.0)))")
     assert cli.main(["run", str(g), "--feed", "x=f64:1.0"]) == 4
     assert ": runtime: " in capsys.readouterr().err
