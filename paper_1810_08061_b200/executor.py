@@ -500,7 +500,34 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
     failing entries of the returned list are the exception objects).  With
     ``host_outputs`` the whole output sequence buffer is copied to page-locked
     host memory in one transfer (into ``host_outputs`` itself when it is a
-    float32 CPU tensor of R*T*H elements) and results are served from it."""
+    float32 CPU tensor of R*T*H elements) and results are served from it.
+    ``precision``: "fast" (default) or "fp32" (see ``execute``); a fast-tier
+    launch whose inputs exceed the fp16 range is re-run on the fp32 tier."""
+    precision = precision or os.environ.get("SKB_PRECISION", "fast")
+    if precision == "f64":
+        raise LoweringError("execute_many runs the fused recurrent kernels; use execute(precision='f64')")
+    tier = "f32" if precision == "fp32" else "f16"
+    try:
+        return _execute_many(graph, feeds_list, check, stream, return_exceptions, host_outputs, tier)
+    except PrecisionRangeError:
+        if tier == "f32":
+            raise
+        return _execute_many(graph, feeds_list, False, stream, return_exceptions, host_outputs, "f32")
+    except _OverlapStarved:   # a side-stream producer missed its bounded wait: run this call sequentially
+        from . import runtime as rt
+        lib = rt.lib()
+        lib.skb_rnn_set_overlap(0)
+        try:
+            return _execute_many(graph, feeds_list, False, stream, return_exceptions, host_outputs, tier)
+        finally:
+            lib.skb_rnn_set_overlap(1)
+
+
+class _OverlapStarved(Exception):
+    pass
+
+
+def _execute_many(graph, feeds_list, check, stream, return_exceptions, host_outputs, tier):
     torch = _torch()
     from . import runtime as rt
     rt.lib()
@@ -581,6 +608,8 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
         # results are views of the host buffers: built while the last copies are in flight
         results = _assemble(prog, out_host, hT_h, cT_h, ml_host, None, Bsz, T, P, True, tier)
         finish()
+        if int(status_h[0]) == E.SKB_ERR_OVERLAP:
+            raise _OverlapStarved()
         if int(status_h[0]) == E.SKB_ERR_FP16_RANGE:
             raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
         if not np.array_equal(ml_dev.numpy(), ml_host):   # (host and device trip counts agree by construction)
@@ -764,6 +793,8 @@ TIER_PRECISION = {"f16": "fp16 tensor-core operands, fp32 accumulate/state (boun
 
 
 def _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions, tier="f16"):
+    if status is not None and int(status[0]) == E.SKB_ERR_OVERLAP:
+        raise _OverlapStarved()
     if status is not None and int(status[0]) == E.SKB_ERR_FP16_RANGE:
         raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
     results = []
