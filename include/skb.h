@@ -40,9 +40,7 @@ enum {
   SKB_ERR_DIVISION_BY_ZERO = 13,   /* "DivisionByZero"  tensor.py:235-241     */
   SKB_ERR_ITERATION_LIMIT = 14,    /* "IterationLimitExceeded" execute.py:232 */
   SKB_ERR_ASSERTION_FAILED = 15,   /* "AssertionFailed" execute.py:198-202    */
-  SKB_ERR_FP16_RANGE = 20,         /* input outside the fp16 tensor-core range */
-  SKB_ERR_OVERLAP = 21             /* overlapped C1 launch: a side-stream producer was starved
-                                      (bounded wait expired); the host re-runs sequentially */
+  SKB_ERR_FP16_RANGE = 20          /* input outside the fp16 tensor-core range */
 };
 
 /* Cell kinds recognised by the lowering of a staged `While` region. */
@@ -315,13 +313,6 @@ skb_status skb_diag_umma_gemm(const void* a_dev, const void* b_dev, void* d_dev,
  * reference's float64 (north_star's fp32 bound).  One CTA per 32-row tile,
  * thread = hidden unit (H <= 256, (F+H) % 4 == 0).  Same arguments and error
  * contract as skb_rnn_forward; packing from the same per-gate weights. */
-/* 1 if the last skb_rnn_forward ran overlapped: the recurrent kernel on a
- * high-priority stream, the x packer and frozen-tail filler on side streams
- * over the SMs its clusters leave idle (per-tile release/acquire counters,
- * bounded waits; SKB_RNN_OVERLAP=0 disables).  All three join the caller's
- * stream before skb_rnn_forward's work is complete. */
-int skb_rnn_last_overlap(void);
-int skb_rnn_set_overlap(int enable);   /* process-wide switch; returns the previous setting */
 int64_t skb_rnn_f32_packed_bytes(const skb_rnn_shape* shape);
 int64_t skb_rnn_f32_workspace_bytes(const skb_rnn_shape* shape);
 skb_status skb_rnn_pack_f32(const skb_rnn_shape* shape, const void* const* w_dev, const void* const* u_dev,

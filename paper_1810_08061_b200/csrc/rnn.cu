@@ -60,7 +60,6 @@ inline int rnn_act() {
   return act;
 }
 constexpr int kMaxClusterDim = 8;
-int g_last_clusters = 0;   // clusters of the last dual-lane launch (overlapped mode sizes its side grids)
 constexpr int kGS = 36;   // sG row stride (floats): 32 units + 4 pad, conflict-free LDS.128
 
 struct RnnGeom {
@@ -117,40 +116,9 @@ struct RnnArgs {
   const uint8_t* ximg; // [ntiles][T][NT x Kx] fp16 core-matrix images of x_t
   uint8_t* hscratch;   // per cluster: 2 x [NT x Kh] fp16 h_t exchange buffers (L2)
   int32_t* err;
-  // overlapped mode (x images packed and frozen tails filled by side-stream kernels on
-  // the SMs the clusters leave idle): per-tile counters, NULL when not overlapped
-  int32_t* xready;     // [ntiles] x_t images of the tile packed so far (pack_x_stream)
-  int32_t* hdone;      // [ntiles] CTAs of the cluster that wrote the tile's final h (fill_frozen_stream)
   int x_f64;
   int R, T, F, H, Kx, Kh, K, U, C, Bp, ntiles;
 };
-
-// Overlap handshakes.  Release: the producer's stores, a gpu-scope fence, then the
-// counter bump.  Acquire: the consumer polls with ld.acquire; a bulk (async-proxy)
-// reader then orders itself after the generic-proxy writes with a proxy fence.
-// Every wait is bounded (globaltimer): a starved producer ends in an error the host
-// answers by re-running the launch sequentially, never in a hang.
-constexpr unsigned long long kOverlapTimeoutNs = 200ull * 1000 * 1000;
-SKB_DEV int ld_acquire_gpu(const int32_t* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-SKB_DEV unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// true: the counter reached `want`; false: timed out
-SKB_DEV bool wait_counter(const int32_t* p, int want) {
-  if (ld_acquire_gpu(p) >= want) return true;
-  const unsigned long long t0 = globaltimer();
-  while (ld_acquire_gpu(p) < want) {
-    __nanosleep(256);
-    if (globaltimer() - t0 > kOverlapTimeoutNs) return false;
-  }
-  return true;
-}
 
 // Optional per-step event trace of CTA 0 (debug only; set by skb_debug_rnn_trace).
 __device__ long long* g_trace = nullptr;
@@ -959,19 +927,10 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a)
           }
         }
       }
-      if (a.hdone) {   // overlapped mode: this CTA's slice of the tile's final h is in HBM
-        __threadfence();
-        named_bar_sync(xch_bar, kEpiL);
-        if (e == 0) atomicAdd(a.hdone + tile, 1);
-      }
     } else if (warp < kMma0) {
       // ======================= x_t loader (lane L): one buffer, filled once x-part(s-1) retired
       if (lane == 0) {
         const uint8_t* img = a.ximg + (size_t)tile * T * xbytes;
-        if (a.xready && trip > 0) {   // overlapped mode: the side-stream packer publishes per tile
-          if (!wait_counter(a.xready + tile, trip)) set_err(a.err, SKB_ERR_OVERLAP, tile, 0);
-          fence_proxy_async_global();
-        }
         for (int t = 0; t < trip; ++t) {
           const uint32_t s = step + t;
           mbar_wait(&xempty[L], (s & 1) ^ 1);
@@ -1381,8 +1340,6 @@ struct SchedArgs {
   int32_t* max_len_out;
   int32_t* err;
   int R, Bp, P, T, npad;
-  int32_t* flags;     // overlapped-mode per-tile counters, zeroed every launch
-  int nflags;
 };
 
 __global__ void sched_init(const SchedArgs a) {
@@ -1391,7 +1348,6 @@ __global__ void sched_init(const SchedArgs a) {
   for (int p = i; p < a.P; p += stride) a.pmax[p] = INT_MIN;
   for (int b = i; b <= a.T; b += stride) { a.hist[b] = 0; a.cursor[b] = 0; }
   for (int r = a.R + i; r < a.npad; r += stride) a.perm[r] = -1;
-  for (int f = i; f < a.nflags; f += stride) a.flags[f] = 0;
 }
 
 SKB_DEV int len_bin(long long L, int T) { return (int)max(0LL, min(L, (long long)T)); }
@@ -1518,18 +1474,18 @@ __global__ void __launch_bounds__(256) pack_x_kernel(const XT* __restrict__ x, c
 // coalesced), converts to fp16 into a padded row-major shared tile, then all
 // threads write the image in core-matrix order ([Kx/8][64 rows][8] halves) as
 // contiguous 16-byte stores.  Rows past their length are written as zeros.
-// One (tile, t) image; returns false when the step is past the tile's trip count.
 template <int NQ>
-SKB_DEV bool pack_rows_item(const float* __restrict__ x, const int32_t* __restrict__ perm,
-                            const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
-                            uint8_t* __restrict__ img, int32_t* err, int T, int Bp, int tile, int t,
-                            uint8_t* srow) {
+__global__ void __launch_bounds__(256) pack_x_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
+                                   const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
+                                   uint8_t* __restrict__ img, int32_t* err, int T, int Bp) {
   constexpr int F = NQ * 128, kRow = F * 2 + 16;   // padded fp16 row: 16-byte reads of 8 lanes hit distinct banks
+  extern __shared__ __align__(16) uint8_t srow[];
+  const int tile = blockIdx.x, t = blockIdx.y;
   const int r0 = perm[tile * kNT];
-  if (r0 < 0) return false;
+  if (r0 < 0) return;
   const int tm0 = min(max(pmax[r0 / Bp], 0), T);
   const long long L0 = lens[r0];
-  if (t >= (L0 < tm0 ? L0 : tm0)) return false;
+  if (t >= (L0 < tm0 ? L0 : tm0)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   bool bad = false;
   float4 v[8][NQ];
@@ -1564,46 +1520,10 @@ SKB_DEV bool pack_rows_item(const float* __restrict__ x, const int32_t* __restri
     out[o] = *reinterpret_cast<const uint4*>(srow + n * kRow + kc * 16);
   }
   if (bad) set_err(err, SKB_ERR_FP16_RANGE, -1, -1);
-  return true;
-}
-
-// Coalesced variant for fp32 x with F % 128 == 0 (the C1 shape): one block per
-// (tile, t) image.  Each warp reads whole 4*F-byte rows (lane k*4.., fully
-// coalesced), converts to fp16 into a padded row-major shared tile, then all
-// threads write the image in core-matrix order ([Kx/8][64 rows][8] halves) as
-// contiguous 16-byte stores.  Rows past their length are written as zeros.
-template <int NQ>
-__global__ void __launch_bounds__(256) pack_x_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
-                                   const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
-                                   uint8_t* __restrict__ img, int32_t* err, int T, int Bp) {
-  extern __shared__ __align__(16) uint8_t srow[];
-  pack_rows_item<NQ>(x, perm, lens, pmax, img, err, T, Bp, blockIdx.x, blockIdx.y, srow);
-}
-
-// Overlapped mode: a small persistent grid on a side stream (the SMs the
-// recurrent kernel's clusters leave idle) packs the images in the order the
-// recurrent kernel consumes them (tile-major) and publishes, per tile, the number
-// of images packed (release); the loader warp of the tile's lane waits for all of
-// them (acquire).  It never waits on anything itself.
-template <int NQ>
-__global__ void __launch_bounds__(256) pack_x_stream_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
-                                     const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
-                                     uint8_t* __restrict__ img, int32_t* err, int32_t* xready, int ntiles, int T,
-                                     int Bp) {
-  extern __shared__ __align__(16) uint8_t srow[];
-  const long long items = (long long)ntiles * T;
-  for (long long i = blockIdx.x; i < items; i += gridDim.x) {
-    const int tile = (int)(i / T), t = (int)(i % T);
-    const bool did = pack_rows_item<NQ>(x, perm, lens, pmax, img, err, T, Bp, tile, t, srow);
-    __threadfence();
-    __syncthreads();   // every thread's image stores (and srow reads) are done
-    if (did && threadIdx.x == 0) atomicAdd(xready + tile, 1);
-  }
 }
 
 struct Workspace {
   int32_t *perm, *pmax, *hist, *base, *cursor;
-  int32_t *xready, *hdone, *filled;   // overlapped mode: per-tile counters / marks
   uint8_t* hscratch;
   uint8_t* ximg;
   float* hT;
@@ -1625,11 +1545,7 @@ inline int64_t ws_layout(const RnnGeom& g, uint8_t* basep, Workspace* w) {
   int64_t o_hs = take((int64_t)max_clusters_bound(g) * 2 * kNT * g.Kh * 2 / 4);
   int64_t o_x = take((int64_t)ntiles * g.T * kNT * g.Kx * 2 / 4);
   int64_t o_hT = take((int64_t)g.R * g.H);
-  int64_t o_flags = take((int64_t)3 * ntiles);
   if (w) {
-    w->xready = reinterpret_cast<int32_t*>(basep + o_flags);
-    w->hdone = w->xready + ntiles;
-    w->filled = w->hdone + ntiles;
     w->perm = reinterpret_cast<int32_t*>(basep + o_perm);
     w->pmax = reinterpret_cast<int32_t*>(basep + o_pmax);
     w->hist = reinterpret_cast<int32_t*>(basep + o_hist);
@@ -1665,59 +1581,6 @@ __global__ void __launch_bounds__(256) rnn_fill_frozen_kernel(float* __restrict_
   } else {
     for (int j = lane; j < H; j += 32) {
       const float v = hrow[j];
-      for (int t = len; t < tmax; ++t) orow[(size_t)t * H + j] = v;
-    }
-  }
-}
-
-// Overlapped mode: frozen tails of a tile's rows, as soon as every CTA of the
-// tile's cluster has published its final h (hdone == C); tiles in the recurrent
-// kernel's completion order (tile-major).  Bounded wait: a tile still pending at
-// the timeout is left to rnn_fill_pending_kernel (main stream, after the
-// recurrent kernel), which fills every tile whose `filled` mark is unset.
-__global__ void __launch_bounds__(256) fill_frozen_stream_kernel(float* __restrict__ out, const float* __restrict__ hT,
-                                          const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
-                                          const int32_t* __restrict__ perm, const int32_t* hdone,
-                                          int32_t* filled, int ntiles, int C, int T, int H, int Bp) {
-  __shared__ int s_ok;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    if (threadIdx.x == 0) s_ok = wait_counter(hdone + tile, C) ? 1 : 0;
-    __syncthreads();
-    if (!s_ok) return;   // starved: the cleanup kernel fills the rest
-    for (int n = warp; n < kNT; n += 8) {
-      const int r = perm[tile * kNT + n];
-      if (r < 0) continue;
-      const int tmax = min(max(pmax[r / Bp], 0), T);
-      const long long L = lens[r];
-      const int len = (int)(L < 0 ? 0 : (L < tmax ? L : tmax));
-      float* orow = out + (size_t)r * T * H;
-      const float4* hrow = reinterpret_cast<const float4*>(hT + (size_t)r * H);
-      for (int j = lane; j < H / 4; j += 32) {
-        const float4 v = __ldcg(hrow + j);
-        for (int t = len; t < tmax; ++t) reinterpret_cast<float4*>(orow + (size_t)t * H)[j] = v;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) filled[tile] = 1;
-  }
-}
-
-__global__ void __launch_bounds__(256) rnn_fill_pending_kernel(float* __restrict__ out, const float* __restrict__ hT,
-                                        const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
-                                        const int32_t* __restrict__ perm, const int32_t* filled, int ntiles,
-                                        int T, int H, int Bp) {
-  const int tile = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (tile >= ntiles || filled[tile]) return;
-  for (int n = warp; n < kNT; n += 8) {
-    const int r = perm[tile * kNT + n];
-    if (r < 0) continue;
-    const int tmax = min(max(pmax[r / Bp], 0), T);
-    const long long L = lens[r];
-    const int len = (int)(L < 0 ? 0 : (L < tmax ? L : tmax));
-    float* orow = out + (size_t)r * T * H;
-    for (int j = lane; j < H; j += 32) {
-      const float v = hT[(size_t)r * H + j];
       for (int t = len; t < tmax; ++t) orow[(size_t)t * H + j] = v;
     }
   }
@@ -1841,7 +1704,6 @@ int launch_dl(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
     return SKB_ERR_CUDA;
   const int ncl = min(min(max_clusters, (args.ntiles + 1) / 2), max_clusters_bound(g) - 1);
   cfg.gridDim = dim3(g.C * max(ncl, 1));
-  g_last_clusters = max(ncl, 1);
   const bool prof = g_prof_n < g_prof_cap;
   if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], stream);
   if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
@@ -1873,50 +1735,7 @@ int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
   return rnn_ew() == 8 ? launch_main_ew<CELL, XT, 8>(args, g, stream) : launch_main_ew<CELL, XT, 16>(args, g, stream);
 }
 
-inline bool dl_eligible(const RnnGeom& g, const RnnArgs& a) {
-  if (g.cell != SKB_CELL_LSTM && g.cell != SKB_CELL_GRU) return false;
-  if (!(rnn_dl() && rnn_ew() == 16 && g.U == 32 && g.H == g.C * 32 && g.Kh == g.H)) return false;
-  return g.cell == SKB_CELL_GRU || (!rnn_pp() && a.c0 != nullptr);
-}
-
-// Overlapped C1 launch (default for the dual-lane kernel with fp32 x rows; SKB_RNN_OVERLAP=0
-// disables): the recurrent kernel runs on a high-priority stream, the x packer and
-// the frozen-tail filler on two side streams, on the SMs its clusters leave idle.
-int g_overlap_override = -1;   // skb_rnn_set_overlap
-inline bool rnn_overlap() {
-  static int ov = -1;
-  if (ov < 0) {
-    const char* e = getenv("SKB_RNN_OVERLAP");
-    ov = (e && atoi(e) == 0) ? 0 : 1;
-  }
-  return g_overlap_override >= 0 ? g_overlap_override == 1 : ov == 1;
-}
-
-struct SideStreams {
-  cudaStream_t hi = nullptr, pack = nullptr, fill = nullptr;
-  bool ok = false;
-};
-SideStreams g_side[16];
-
-SideStreams* side_streams() {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
-  SideStreams& s = g_side[dev];
-  if (!s.ok) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&s.hi, cudaStreamNonBlocking, hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&s.pack, cudaStreamNonBlocking, lo) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&s.fill, cudaStreamNonBlocking, lo) != cudaSuccess)
-      return nullptr;
-    s.ok = true;
-  }
-  return &s;
-}
-
 }  // namespace
-
-extern "C" int skb_rnn_last_overlap(void);
 
 extern "C" int skb_profile_begin(int max_launches) {
   if (max_launches < 0 || max_launches > kProfMax) return SKB_ERR_INVALID;
@@ -2027,74 +1846,6 @@ extern "C" int skb_rnn_pack(const skb_rnn_shape* shape, const void* const* w_dev
   return skb_check_launch();
 }
 
-namespace {
-int g_last_overlap = 0;
-
-template <int NQ>
-void launch_pack_stream(const RnnArgs& a, const Workspace& w, int grid, cudaStream_t s) {
-  const size_t sm = (size_t)kNT * (NQ * 128 * 2 + 16);
-  static bool attr = false;
-  if (!attr && sm > 48 * 1024) {
-    cudaFuncSetAttribute(pack_x_stream_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
-  pack_x_stream_kernel<NQ><<<grid, 256, sm, s>>>((const float*)a.x, w.perm, a.lens, w.pmax, w.ximg, a.err,
-                                                   w.xready, a.ntiles, a.T, a.Bp);
-}
-
-int forward_overlapped(const RnnGeom& g, RnnArgs a, const Workspace& w, SideStreams* ss, cudaStream_t st,
-                       float* out_dev, const int64_t* len_dev) {
-  cudaEvent_t ev_sched, ev_rnn, ev_pack, ev_fill;
-  cudaEventCreateWithFlags(&ev_sched, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&ev_rnn, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&ev_pack, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&ev_fill, cudaEventDisableTiming);
-  cudaEventRecord(ev_sched, st);
-  cudaStreamWaitEvent(ss->hi, ev_sched, 0);
-  cudaStreamWaitEvent(ss->pack, ev_sched, 0);
-  cudaStreamWaitEvent(ss->fill, ev_sched, 0);
-  a.xready = w.xready;
-  a.hdone = w.hdone;
-  // the recurrent kernel first (high priority: its clusters are placed before the side grids)
-  int rc = g.cell == SKB_CELL_LSTM ? launch_main<SKB_CELL_LSTM, float>(a, g, ss->hi)
-                                   : launch_main<SKB_CELL_GRU, float>(a, g, ss->hi);
-  if (rc == SKB_OK) {
-    int sms = 148, dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int idle = max(4, sms - g_last_clusters * g.C);
-    if (g.F == 128) launch_pack_stream<1>(a, w, 2 * idle, ss->pack);
-    else if (g.F == 256) launch_pack_stream<2>(a, w, 2 * idle, ss->pack);
-    else launch_pack_stream<4>(a, w, idle, ss->pack);
-    fill_frozen_stream_kernel<<<idle, 256, 0, ss->fill>>>(out_dev, a.hT, len_dev, w.pmax, w.perm, w.hdone, w.filled,
-                                                           a.ntiles, g.C, g.T, g.H, g.Bp);
-    rc = skb_check_launch();
-  }
-  cudaEventRecord(ev_rnn, ss->hi);
-  cudaEventRecord(ev_pack, ss->pack);
-  cudaEventRecord(ev_fill, ss->fill);
-  cudaStreamWaitEvent(st, ev_rnn, 0);
-  cudaStreamWaitEvent(st, ev_pack, 0);
-  cudaStreamWaitEvent(st, ev_fill, 0);
-  if (rc == SKB_OK) {   // tiles the filler gave up on (bounded wait) are filled here, after the kernel
-    rnn_fill_pending_kernel<<<a.ntiles, 256, 0, st>>>(out_dev, a.hT, len_dev, w.pmax, w.perm, w.filled, a.ntiles,
-                                                       g.T, g.H, g.Bp);
-    rc = skb_check_launch();
-  }
-  cudaEventDestroy(ev_sched);
-  cudaEventDestroy(ev_rnn);
-  cudaEventDestroy(ev_pack);
-  cudaEventDestroy(ev_fill);
-  return rc;
-}
-}  // namespace
-
-extern "C" int skb_rnn_last_overlap(void) { return g_last_overlap; }
-extern "C" int skb_rnn_set_overlap(int enable) {
-  const int prev = rnn_overlap() ? 1 : 0;
-  g_overlap_override = enable ? 1 : 0;
-  return prev;
-}
-
 extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_dev, const void* x_dev,
                                int x_f64, const float* h0_dev, const float* c0_dev,
                                const int64_t* len_dev, float* out_dev, float* hT_dev, float* cT_dev,
@@ -2112,9 +1863,7 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   const int ntiles = (g.R + kNT - 1) / kNT;
   SchedArgs sa = {len_dev, w.perm, w.pmax, w.hist, w.base, w.cursor, max_len_dev, err_dev,
                   g.R, g.Bp, g.P, g.T, ntiles * kNT};
-  sa.flags = w.xready;
-  sa.nflags = 3 * ntiles;
-  const int blocks = min(1184, max(1, (max(max(g.R, g.P), 3 * ntiles) + 255) / 256));
+  const int blocks = min(1184, max(1, (max(g.R, g.P) + 255) / 256));
   sched_init<<<blocks, 256, 0, st>>>(sa);
   sched_hist<<<blocks, 256, 0, st>>>(sa);
   sched_scan<<<1, 1024, 0, st>>>(sa);
@@ -2128,15 +1877,10 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   a.out = out_dev; a.hT = hT_dev ? hT_dev : w.hT; a.cT = cT_dev; a.err = err_dev; a.x_f64 = x_f64;
   a.hscratch = w.hscratch;
   a.ximg = w.ximg;
-  a.R = g.R; a.T = g.T; a.F = g.F; a.H = g.H; a.Kx = g.Kx; a.Kh = g.Kh; a.K = g.K; a.U = g.U;
-  a.C = g.C; a.Bp = g.Bp; a.ntiles = ntiles;
-  const bool rows_ok = !x_f64 && g.F == g.Kx && (reinterpret_cast<uintptr_t>(x_dev) & 15) == 0 &&
-                       (g.F == 128 || g.F == 256 || g.F == 512) && !getenv("SKB_PACK_X_LEGACY");
-  SideStreams* ss = (rows_ok && rnn_overlap() && dl_eligible(g, a) && g.T > 0) ? side_streams() : nullptr;
-  g_last_overlap = ss != nullptr;
-  if (ss) return forward_overlapped(g, a, w, ss, st, out_dev, len_dev);
   {
     const dim3 pg(ntiles, g.T);
+    const bool rows_ok = !x_f64 && g.F == g.Kx && (reinterpret_cast<uintptr_t>(x_dev) & 15) == 0 &&
+                         (g.F == 128 || g.F == 256 || g.F == 512) && !getenv("SKB_PACK_X_LEGACY");
     if (x_f64)
       pack_x_kernel<double><<<pg, 256, 0, st>>>((const double*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
                                                   err_dev, ntiles, g.T, g.F, g.Kx, g.Bp);
@@ -2158,6 +1902,8 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
       pack_x_kernel<float><<<pg, 256, 0, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
                                                  err_dev, ntiles, g.T, g.F, g.Kx, g.Bp);
   }
+  a.R = g.R; a.T = g.T; a.F = g.F; a.H = g.H; a.Kx = g.Kx; a.Kh = g.Kh; a.K = g.K; a.U = g.U;
+  a.C = g.C; a.Bp = g.Bp; a.ntiles = ntiles;
   int rc;
   if (g.cell == SKB_CELL_LSTM)
     rc = x_f64 ? launch_main<SKB_CELL_LSTM, double>(a, g, st) : launch_main<SKB_CELL_LSTM, float>(a, g, st);

@@ -79,7 +79,6 @@ STATUS_TO_CAUSE = {
     15: ASSERTION_FAILED,
 }
 SKB_ERR_FP16_RANGE = 20
-SKB_ERR_OVERLAP = 21   # overlapped C1 launch: a side-stream producer was starved (host re-runs sequentially)
 
 
 class IntegerOverflow(SkbError):

@@ -513,18 +513,6 @@ def execute_many(graph, feeds_list: list, check: bool = True, *, stream=None,
         if tier == "f32":
             raise
         return _execute_many(graph, feeds_list, False, stream, return_exceptions, host_outputs, "f32")
-    except _OverlapStarved:   # a side-stream producer missed its bounded wait: run this call sequentially
-        from . import runtime as rt
-        lib = rt.lib()
-        lib.skb_rnn_set_overlap(0)
-        try:
-            return _execute_many(graph, feeds_list, False, stream, return_exceptions, host_outputs, tier)
-        finally:
-            lib.skb_rnn_set_overlap(1)
-
-
-class _OverlapStarved(Exception):
-    pass
 
 
 def _execute_many(graph, feeds_list, check, stream, return_exceptions, host_outputs, tier):
@@ -608,8 +596,6 @@ def _execute_many(graph, feeds_list, check, stream, return_exceptions, host_outp
         # results are views of the host buffers: built while the last copies are in flight
         results = _assemble(prog, out_host, hT_h, cT_h, ml_host, None, Bsz, T, P, True, tier)
         finish()
-        if int(status_h[0]) == E.SKB_ERR_OVERLAP:
-            raise _OverlapStarved()
         if int(status_h[0]) == E.SKB_ERR_FP16_RANGE:
             raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
         if not np.array_equal(ml_dev.numpy(), ml_host):   # (host and device trip counts agree by construction)
@@ -793,8 +779,6 @@ TIER_PRECISION = {"f16": "fp16 tensor-core operands, fp32 accumulate/state (boun
 
 
 def _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions, tier="f16"):
-    if status is not None and int(status[0]) == E.SKB_ERR_OVERLAP:
-        raise _OverlapStarved()
     if status is not None and int(status[0]) == E.SKB_ERR_FP16_RANGE:
         raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
     results = []

@@ -64,8 +64,6 @@ SIGNATURES = {
     "skb_rnn_pack_f32": (ctypes.c_int, [ctypes.POINTER(RnnShape), _P4, _P4, _P4, ctypes.c_int, _VP, _VP]),
     "skb_rnn_forward_f32": (ctypes.c_int, [ctypes.POINTER(RnnShape), _VP, _VP, ctypes.c_int, _VP, _VP, _VP,
                                             _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
-    "skb_rnn_last_overlap": (ctypes.c_int, []),
-    "skb_rnn_set_overlap": (ctypes.c_int, [ctypes.c_int]),
     "skb_debug_rnn_trace": (ctypes.c_int, [_VP, ctypes.c_int]),
     "skb_debug_rnn_tile_trace": (ctypes.c_int, [_VP, ctypes.c_int]),
     "skb_profile_begin": (ctypes.c_int, [ctypes.c_int]),
