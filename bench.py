@@ -47,6 +47,13 @@ B, T, F, H = 32, 64, 256, 256
 FLOP_PER_ROW_STEP = 2 * (F + H) * 4 * H          # 1.049 MFLOP
 
 
+KERNELS = {4: "rnn_fwd_pair4_kernel (persistent 8-CTA clusters of 4 CTA pairs, M=256 cta_group::2 tcgen05 f16 "
+                "MMAs, four independent 64-row recurrences per pair)",
+           5: "rnn_fwd_pair_kernel (persistent 8-CTA clusters of 4 CTA pairs, M=256 cta_group::2 tcgen05 f16 "
+                "MMAs, two 128-row recurrences per pair)",
+           3: "rnn_fwd_dl_kernel (persistent 8-CTA clusters, two 64-row recurrences per CTA, tcgen05 f16)"}
+
+
 def peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -235,6 +242,10 @@ def run_skb(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    status = int(exe.err[0].item())
+    if status != 0:
+        raise RuntimeError(f"C1 launch reported status {status}")
+    kernel_id, nclus = int(lib.skb_rnn_last_kernel()), int(lib.skb_rnn_last_clusters())
     ms = e0.elapsed_time(e1) / args.steps
     import ctypes
     kms = (ctypes.c_float * args.steps)()
@@ -266,7 +277,7 @@ def run_skb(args, rank, world, local_rank):
         # a ~1.4 ms kernel at the 1965 MHz max clock (no power cap): the burst peak applies
         roofline = {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
                     "frac": achieved / burst, "traffic": traffic, "traffic_source": traffic_src,
-                    "kernel": "rnn_fwd_dl_kernel (persistent 8-CTA clusters, two 64-row recurrences per CTA, tcgen05 f16)",
+                    "kernel": KERNELS.get(kernel_id, str(kernel_id)), "clusters": nclus,
                     "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / ms,
                     "flops_per_launch": useful,
                     "flop_basis": "useful 2*(F+H)*4H per (row, t < len), SURVEY 8(d)",

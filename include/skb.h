@@ -308,11 +308,25 @@ skb_status skb_comm_destroy(void* comm);
  * ------------------------------------------------------------------------- */
 skb_status skb_diag_umma_gemm(const void* a_dev, const void* b_dev, void* d_dev, int n, int k,
                               int swap_lbo_sbo, long long* cycles_dev, void* stream);
+/* CTA-pair (cta_group::2) MMA with A from TMEM: D[256 x n] = reps * A[256 x k] B[n x k]^T,
+ * read back through 32x32b (d_dev) and 16x256b (d2_dev) TMEM loads; cycles of the chain. */
+skb_status skb_diag_umma_pair(const void* a_dev, const void* b_dev, void* d_dev, void* d2_dev, int n, int k,
+                              int reps, long long* cycles_dev, void* stream);
 /* Accurate tier of the same recurrent While (csrc/rnn_f32.cu): FP32 FFMA with
  * fp32 weights / state and accurate activations, within rtol 1e-4 of the
  * reference's float64 (north_star's fp32 bound).  One CTA per 32-row tile,
  * thread = hidden unit (H <= 256, (F+H) % 4 == 0).  Same arguments and error
  * contract as skb_rnn_forward; packing from the same per-gate weights. */
+/* Which recurrent kernel the last skb_rnn_forward launched, and its cluster count. */
+enum {
+  SKB_RNN_KERNEL_SINGLE = 1,      /* one 64-row recurrence per cluster */
+  SKB_RNN_KERNEL_PING_PONG = 2,   /* two 32-row halves (SKB_RNN_PP=1) */
+  SKB_RNN_KERNEL_DUAL_LANE = 3,   /* two 64-row recurrences per CTA (SKB_RNN_PAIR=0) */
+  SKB_RNN_KERNEL_PAIR = 4,        /* CTA pairs, M=256 cta_group::2 MMAs, four 64-row lanes (default) */
+  SKB_RNN_KERNEL_PAIR2 = 5        /* CTA pairs, two 128-row lanes (SKB_RNN_PAIR=2) */
+};
+int skb_rnn_last_kernel(void);
+int skb_rnn_last_clusters(void);
 int64_t skb_rnn_f32_packed_bytes(const skb_rnn_shape* shape);
 int64_t skb_rnn_f32_workspace_bytes(const skb_rnn_shape* shape);
 skb_status skb_rnn_pack_f32(const skb_rnn_shape* shape, const void* const* w_dev, const void* const* u_dev,

@@ -166,6 +166,87 @@ cluster_exchange_kernel(int slice_bytes, int rounds, long long* cycles, int* err
   if (bad) atomicAdd(errors, bad);
 }
 
+// CTA-pair MMA self-test/rate probe: D[256 x N] = A[256 x K] * B[N x K]^T with one
+// cta_group::2 tcgen05.mma chain issued by the leader (A rows split across the two
+// CTAs' TMEM, B rows split across their shared memory), `reps` passes accumulated.
+// D is read back twice: 32x32b (D) and 16x256b (D2, pins that load's thread layout).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+umma_pair_kernel(const __half* __restrict__ A, const __half* __restrict__ B, float* __restrict__ D,
+                 float* __restrict__ D2, int N, int K, int reps, long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar_done;
+  __shared__ uint32_t tmem_s;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, rank = cluster_ctarank();
+  const int Nh = N / 2;
+  const uint32_t b_lbo = Nh * 16, b_sbo = 128;
+  for (int i = tid; i < Nh * (K / 8); i += blockDim.x) {
+    const int r = i % Nh, kc = i / Nh;
+    *reinterpret_cast<uint4*>(smem + cm_offset(r, kc * 8, b_lbo, b_sbo)) =
+        *reinterpret_cast<const uint4*>(B + (size_t)(rank * Nh + r) * K + kc * 8);
+  }
+  fence_proxy_async_smem();
+  if (tid == 0) { mbar_init(&bar_done, 1); fence_mbar_init(); }
+  if (warp == 0) tmem_alloc_pair<512>(&tmem_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_s;
+  {
+    const uint32_t row = rank * 128 + warp * 32 + lane;
+    for (int c0 = 0; c0 < K / 2; c0 += 8) {
+      uint32_t r[8];
+      for (int i = 0; i < 8; ++i) {
+        __half2 h2 = __halves2half2(A[(size_t)row * K + 2 * (c0 + i)], A[(size_t)row * K + 2 * (c0 + i) + 1]);
+        r[i] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+      tmem_st8(tmem + ((warp * 32) << 16) + 256 + c0, r);
+    }
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (rank == 0 && warp == 0) {
+    const uint32_t idesc = idesc_f16_f32(256, N);
+    const uint64_t b0 = sdesc_kmajor_noswz(smem_u32(smem), b_lbo, b_sbo);
+    const long long t0 = clock64();
+    for (int rp = 0; rp < reps; ++rp)
+      for (int ks = 0; ks < K / 16; ++ks)
+        umma_f16_ts_pair_warp(tmem, tmem + 256 + ks * 8, b0 + (uint64_t)(ks * 2 * b_lbo >> 4), idesc,
+                              (rp | ks) ? 1u : 0u);
+    umma_commit_pair_warp(&bar_done, (uint16_t)3);
+    mbar_wait(&bar_done, 0);
+    const long long t1 = clock64();
+    if (lane == 0 && cycles) *cycles = t1 - t0;
+  } else if (tid == 0) {
+    mbar_wait(&bar_done, 0);
+  }
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t lrow = warp * 32 + lane;
+  for (int c = 0; c < N; c += 16) {
+    float v[16];
+    tmem_ld16(tmem + ((warp * 32) << 16) + c, v);
+    tmem_ld_wait();
+    for (int j = 0; j < 16; ++j) D[(size_t)(rank * 128 + lrow) * N + c + j] = v[j];
+  }
+  for (int half = 0; half < 2; ++half)
+    for (int c = 0; c < N; c += 16) {
+      float v[8];
+      tmem_ld_16x256b_x2(tmem + ((warp * 32 + half * 16) << 16) + c, v);
+      tmem_ld_wait();
+      const int l0 = warp * 32 + half * 16 + lane / 4, c0 = c + 2 * (lane % 4);
+      const int ls[8] = {l0, l0, l0 + 8, l0 + 8, l0, l0, l0 + 8, l0 + 8};
+      const int cs[8] = {c0, c0 + 1, c0, c0 + 1, c0 + 8, c0 + 9, c0 + 8, c0 + 9};
+      for (int j = 0; j < 8; ++j) D2[(size_t)(rank * 128 + ls[j]) * N + cs[j]] = v[j];
+    }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 0) tmem_dealloc_pair<512>(tmem);
+}
+
 }  // namespace
 
 extern "C" int skb_diag_umma_gemm(const void* A, const void* B, void* D, int N, int K,
@@ -196,5 +277,15 @@ extern "C" int skb_diag_cluster_exchange(int cluster, int slice_bytes, int round
 #undef SKB_CASE
     default: return SKB_ERR_INVALID;
   }
+  return skb_check_launch();
+}
+
+extern "C" int skb_diag_umma_pair(const void* A, const void* B, void* D, void* D2, int N, int K, int reps,
+                                  long long* cycles, void* stream) {
+  if (N % 32 || N < 32 || N > 256 || K % 16 || K <= 0 || K > 512 || reps < 1) return SKB_ERR_INVALID;
+  const size_t smem = (size_t)(N / 2) * K * 2;
+  cudaFuncSetAttribute(umma_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  umma_pair_kernel<<<2, 128, smem, (cudaStream_t)stream>>>((const __half*)A, (const __half*)B, (float*)D,
+                                                          (float*)D2, N, K, reps, cycles);
   return skb_check_launch();
 }

@@ -39,6 +39,10 @@ namespace {
 // slice w>>2), an x loader warp and an MMA-issuer warp (+ TMEM alloc).
 // EW = 16 halves each epilogue thread's share of a step (the recurrence's
 // critical path); SKB_RNN_EW=8 selects the narrower variant.
+inline int env_flag(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
 inline int rnn_ew() {
   static int ew = 0;
   if (!ew) {
@@ -51,15 +55,19 @@ inline int rnn_ew() {
 // epilogue's MUFU/FMA work is on the recurrence's critical path; C1 step -18%,
 // accuracy vs the f64 oracle unchanged within the fp16-operand error, see
 // tools/c1_err.py); SKB_RNN_ACT=0 = ex2 + Newton reciprocal (rel. err ~1e-7).
+// SKB_RNN_ACT=2: the CTA-pair kernel evaluates activations with tanh.approx.f16x2
+// (measured slower: sm_100 issues it as two MUFU.TANH.F16, plus the conversions).
 inline int rnn_act() {
   static int act = -1;
   if (act < 0) {
     const char* e = getenv("SKB_RNN_ACT");
-    act = (e && atoi(e) == 0) ? 0 : 1;
+    act = e ? (atoi(e) == 0 ? 0 : (atoi(e) == 2 ? 2 : 1)) : 1;
   }
   return act;
 }
 constexpr int kMaxClusterDim = 8;
+int g_last_clusters = 0;   // clusters of the last recurrent-kernel launch (skb_rnn_last_clusters)
+int g_last_kernel = 0;     // which recurrent kernel it was (skb_rnn_last_kernel)
 constexpr int kGS = 36;   // sG row stride (floats): 32 units + 4 pad, conflict-free LDS.128
 
 struct RnnGeom {
@@ -117,6 +125,7 @@ struct RnnArgs {
   uint8_t* hscratch;   // per cluster: 2 x [NT x Kh] fp16 h_t exchange buffers (L2)
   int32_t* err;
   int x_f64;
+  int fill_inkernel;   // pair4 kernel: write the frozen tails itself (no fill pass)
   int R, T, F, H, Kx, Kh, K, U, C, Bp, ntiles;
 };
 
@@ -136,9 +145,15 @@ __device__ int g_ttrace_n = 0;
     if (g_trace != nullptr && blockIdx.x == 0 && (int)(step_) < g_trace_steps)             \
       g_trace[(size_t)(step_) * 16 + (slot_)] = clock64();                                 \
   } while (0)
+#define SKB_TRACE_CTA(cta_, step_, slot_)                                                  \
+  do {                                                                                     \
+    if (g_trace != nullptr && blockIdx.x == (cta_) && (int)(step_) < g_trace_steps)        \
+      g_trace[(size_t)(step_) * 16 + (slot_)] = clock64();                                 \
+  } while (0)
 #else   // production build: trace points compile to nothing
 #define SKB_TTRACE(it_, slot_) do {} while (0)
 #define SKB_TRACE(step_, slot_) do {} while (0)
+#define SKB_TRACE_CTA(cta_, step_, slot_) do {} while (0)
 #endif
 
 SKB_DEV void set_err(int32_t* err, int code, int problem, int t) {
@@ -171,6 +186,11 @@ SKB_DEV float inv1pexp2(float a) { return rcp_nr(1.f + fminf(ex2_approx(a), 1e30
 SKB_DEV float inv1pexp(float kx) { return inv1pexp2(kx * 1.4426950408889634f); }
 
 SKB_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" :: "l"(p)); }
+// L2 prefetch of one x row (bytes rounded down to 16; the bulk form needs 16-byte alignment)
+SKB_DEV void prefetch_l2_bulk_row(const void* p, int bytes) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0 && bytes >= 16) bulk_prefetch_l2(p, (uint32_t)(bytes & ~15));
+  else prefetch_l2(p);
+}
 SKB_DEV float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -997,6 +1017,772 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_dl_kernel(const RnnArgs a)
   if (warp == kMma0) tmem_dealloc<512>(tmem);
 }
 
+// ------------------------------------------------------------------ CTA-pair kernel
+// The default LSTM/GRU kernel for 32-unit CTA slices with an even CTA count
+// (H = 64, 128, 192, 256).  Measured on the dual-lane kernel: a 128x64x16
+// tcgen05.mma costs ~60 cycles, about half the per-SM rate of N >= 128
+// (profiles/r01_umma_rate.txt), and its shared-memory gate exchange sits on the
+// recurrence's critical path.  Here
+//   * CTAs 2p, 2p+1 of the cluster form a CTA pair; the even CTA issues M=256
+//     cta_group::2 MMAs: A = the pair's 256 gate rows (each CTA's 128 [W;U] rows
+//     resident in its own TMEM), B = x_t / h_t of a 128-row tile, 64 rows per CTA
+//     in shared memory, D = 128 gate rows x 128 tile rows in each CTA's TMEM:
+//     N = 128 per instruction at the shared-memory footprint of a 64-row tile.
+//   * TMEM lane quarter w holds units 8w..8w+7 of the CTA's 32-unit slice with the
+//     four gate blocks at lanes +0/+8/+16/+24, so two 16x256b tcgen05.ld hand each
+//     epilogue thread all four gates of one unit for 16 batch rows: no gate
+//     exchange, and c/h stay in registers for the whole tile.
+//   * h_t is double-buffered in shared memory, so nothing waits for "buffer free":
+//     h_{t+1} exists only after every CTA of the cluster consumed h_{t-1}.  Each CTA
+//     writes its fp16 slice for rows 0-63 / 64-127 to L2 and multicasts it to the
+//     even / odd CTAs.
+//   * Two independent 128-row recurrences ("lanes") per CTA interleave on the
+//     tensor pipe.  TMEM columns: D of lane 0 [0,128), lane 1 [128,256), weights
+//     [256,512).
+//   * The odd CTA's MMA warp relays its local "x_t landed" / "h_t landed" phases to
+//     the leader (remote mbarrier arrivals); the epilogue warps of both CTAs release
+//     D on the leader's dfree barrier.
+SKB_DEV float2 tanh2_approx(float a, float b) {   // two tanh in one MUFU op (fp16 precision, ~2^-11)
+  __half2 x = __floats2half2_rn(a, b);
+  uint32_t r;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(r) : "r"(*reinterpret_cast<uint32_t*>(&x)));
+  return __half22float2(*reinterpret_cast<__half2*>(&r));
+}
+// Gate activations of two cells (ACT 2: tanh.approx.f16x2; otherwise per cell via pact)
+template <int CELL, int ACT, int G>
+SKB_DEV float2 pact2(float z0, float z1, float kb);
+// Cell update of two cells from their activated gate pairs (ACT 2: tanh(c) / tanh(n) in f16x2)
+template <int CELL, int ACT>
+SKB_DEV void cell_update2(float2 g0, float2 g1, float2 g2, float2 g3, float& c0, float& c1, float& h0, float& h1,
+                          bool live0, bool live1) {
+  if constexpr (ACT == 2) {
+    if constexpr (CELL == SKB_CELL_GRU) {
+      const float2 n = tanh2_approx(fmaf(g1.x, g3.x, g2.x), fmaf(g1.y, g3.y, g2.y));
+      const float a0 = fmaf(g0.x, h0 - n.x, n.x), a1 = fmaf(g0.y, h1 - n.y, n.y);
+      h0 = live0 ? a0 : h0;
+      h1 = live1 ? a1 : h1;
+    } else {
+      const float ca = fmaf(g1.x, c0, g0.x * g2.x), cb = fmaf(g1.y, c1, g0.y * g2.y);
+      const float2 th = tanh2_approx(ca, cb);
+      const float ha = g3.x * th.x, hb = g3.y * th.y;
+      c0 = live0 ? ca : c0;
+      c1 = live1 ? cb : c1;
+      h0 = live0 ? ha : h0;
+      h1 = live1 ? hb : h1;
+    }
+  } else {
+    cell_update<CELL, ACT>(g0.x, g1.x, g2.x, g3.x, c0, h0, live0);
+    cell_update<CELL, ACT>(g0.y, g1.y, g2.y, g3.y, c1, h1, live1);
+  }
+}
+
+template <int CELL, int ACT, int G>
+SKB_DEV float pact(float z, float kb) {
+  if constexpr (CELL == SKB_CELL_GRU && G >= 2) {
+    return z + kb;   // GRU n_x / n_h stay affine (+ bias) until the cell combines them
+  } else {
+    constexpr bool th = (CELL != SKB_CELL_GRU) && G == 2;   // LSTM g gate: tanh; the rest sigmoid
+    if constexpr (ACT != 0) {
+      constexpr float kl = th ? 1.f : 0.5f, add = th ? 0.f : 0.5f;
+      return fmaf(kl, tanh_approx(fmaf(z, kl, kb)), add);
+    } else {
+      constexpr float kl = th ? -2.8853900817779268f : -1.4426950408889634f;
+      constexpr float mul = th ? 2.f : 1.f, add = th ? -1.f : 0.f;
+      return fmaf(mul, inv1pexp2(fmaf(z, kl, kb)), add);
+    }
+  }
+}
+template <int CELL, int ACT, int G>
+SKB_DEV float pact_kb(float bias) {
+  if constexpr (CELL == SKB_CELL_GRU && G >= 2) {
+    return bias;
+  } else {
+    constexpr bool th = (CELL != SKB_CELL_GRU) && G == 2;
+    if constexpr (ACT != 0) return (th ? 1.f : 0.5f) * bias;
+    else return (th ? -2.8853900817779268f : -1.4426950408889634f) * bias;
+  }
+}
+
+template <int CELL, int ACT, int G>
+SKB_DEV float2 pact2(float z0, float z1, float kb) {
+  if constexpr (ACT != 2 || (CELL == SKB_CELL_GRU && G >= 2)) {
+    return make_float2(pact<CELL, ACT, G>(z0, kb), pact<CELL, ACT, G>(z1, kb));
+  } else {
+    constexpr bool th = (CELL != SKB_CELL_GRU) && G == 2;
+    constexpr float kl = th ? 1.f : 0.5f, add = th ? 0.f : 0.5f;
+    const float2 t = tanh2_approx(fmaf(z0, kl, kb), fmaf(z1, kl, kb));
+    return th ? t : make_float2(fmaf(kl, t.x, add), fmaf(kl, t.y, add));
+  }
+}
+
+template <typename XT, int ACT = 1, int CELL = SKB_CELL_LSTM>
+__global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_pair_kernel(const RnnArgs a) {
+  constexpr int NT = 128, NH = 64, EWL = 8, kEpiL = EWL * 32;
+  constexpr int kLoad0 = 16, kMma0 = 18;   // warps: 0-15 epilogue (lane = warp >> 3), 16-17 loaders, 18-19 MMA / relay
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint64_t xfull[2], xempty[2], hfull[2][2], mdone[2], dfree[2];
+  __shared__ uint32_t tmem_s;
+  __shared__ int2 s_meta[2][NT];   // (row, clamped length) of the lane's tile rows
+  __shared__ int s_trip[2][3];     // [lane]: tile trip, trip of rows 0-63, trip of rows 64-127
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int L = warp < kLoad0 ? (warp >> 3) : (warp < kMma0 ? warp - kLoad0 : warp - kMma0);
+  const uint32_t q = cluster_ctarank(), odd = q & 1u, peer = q ^ 1u;
+  const bool leader = odd == 0;
+  const int C = a.C, H = a.H, T = a.T;
+  const uint32_t xbytes = NH * a.Kx * 2, hbytes = NH * a.Kh * 2;
+  constexpr uint32_t sbytes = NH * 32 * 2;   // one CTA's h slice of one 64-row half (4 KB)
+  const uint32_t lane_bytes = xbytes + 2 * hbytes;
+  uint8_t* sX = smem_raw + L * lane_bytes;   // [NH x Kx] fp16, core-matrix layout
+  uint8_t* sH = sX + xbytes;                 // 2 x [NH x Kh] fp16
+  constexpr uint32_t b_lbo = NH * 16, b_sbo = 128;
+  constexpr uint32_t kWCol = 256;
+  const uint16_t pair_mask = (uint16_t)(3u << (q & ~1u));
+  uint16_t even_mask = 0;
+  for (int i = 0; i < C; i += 2) even_mask |= (uint16_t)(1u << i);
+  const uint16_t odd_mask = (uint16_t)(even_mask << 1);
+
+  if (tid == 0) {
+    for (int l = 0; l < 2; ++l) {
+      mbar_init(&xfull[l], leader ? 2 : 1);      // own loader (+ the odd CTA's relay)
+      mbar_init(&xempty[l], 1);
+      mbar_init(&hfull[l][0], leader ? 2 : 1);   // own arm (+ relay)
+      mbar_init(&hfull[l][1], leader ? 2 : 1);
+      mbar_init(&mdone[l], 1);
+      mbar_init(&dfree[l], 2 * EWL);             // epilogue warps of both CTAs (leader's copy is used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == kMma0) tmem_alloc_pair<512>(&tmem_s);
+  for (uint32_t i = tid; i < 2 * lane_bytes / 16; i += 20 * 32)
+    reinterpret_cast<uint4*>(smem_raw)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_s;
+  if (warp < 4) {
+    // TMEM lane l = 32w + 8g + u <- packed slab row 32g + 8w + u (gate g of unit 8w + u)
+    const int srow = ((tid & 31) >> 3) * 32 + warp * 8 + (tid & 7);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.wpack + ((size_t)q * 128 + srow) * a.K * 2);
+    for (int c0 = 0; c0 < a.K / 2; c0 += 8) {
+      uint32_t r[8];
+      const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src + c0));
+      const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src + c0 + 4));
+      r[0] = lo.x; r[1] = lo.y; r[2] = lo.z; r[3] = lo.w; r[4] = hi.x; r[5] = hi.y; r[6] = hi.z; r[7] = hi.w;
+      tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + kWCol + c0, r);
+    }
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  cluster_sync();   // every CTA's barriers and TMEM are initialised before any remote traffic
+
+  // epilogue thread: TMEM lane quarter qw, column half ch (= tile rows 64ch..64ch+63),
+  // unit uc = 8qw + lane/4 of the CTA's slice, rows 64ch + 8k + 2(lane%4) + {0,1}, k < 8
+  const int wl = warp & 7, qw = wl & 3, ch = wl >> 2, cq = lane & 3, e = tid & (kEpiL - 1);
+  const int uc = qw * 8 + (lane >> 2), unit = (int)q * 32 + uc;
+  float kb0 = 0.f, kb1 = 0.f, kb2 = 0.f, kb3 = 0.f;
+  if (warp < kLoad0) {
+    const float* bp = a.bpack + q * 128 + uc;
+    kb0 = pact_kb<CELL, ACT, 0>(bp[0]);
+    kb1 = pact_kb<CELL, ACT, 1>(bp[32]);
+    kb2 = pact_kb<CELL, ACT, 2>(bp[64]);
+    kb3 = pact_kb<CELL, ACT, 3>(bp[96]);
+  }
+  float hh[16], cc[16];
+  const uint32_t tile_bar = 5 + L;
+  constexpr uint32_t kLaneThreads = kEpiL + 64;
+  auto cell_row = [&](int ci) { return ch * 64 + (ci >> 3) * 32 + ((ci >> 1) & 3) * 8 + 2 * cq + (ci & 1); };
+
+  uint32_t step = 0;
+  const int nclusters = (int)nclusters_x();
+  const int stride = 2 * nclusters;
+  int2 m_meta = make_int2(-1, 0);
+  auto tile_meta = [&](int tl) {
+    m_meta = make_int2(-1, 0);
+    if (tl < a.ntiles) {
+      const int r = a.perm[tl * NT + e];
+      if (r >= 0) {
+        const int tmax = max(0, min(a.pmax[r / a.Bp], T));
+        m_meta = make_int2(r, (int)max(0LL, min((long long)a.lens[r], (long long)tmax)));
+      }
+    }
+  };
+  const int pos = 2 * (int)cluster_id_x() + L;
+  auto tile_of = [&](int k) { return k * stride + ((k & 1) ? stride - 1 - pos : pos); };
+  const int tile0 = tile_of(0);
+  if (warp < kLoad0 && e < NT) tile_meta(tile0);
+  if (warp == kMma0 + L && lane == 0) {   // arm the h phases of steps 0 and 1
+    mbar_arrive_expect_tx(&hfull[L][0], C * sbytes);
+    mbar_arrive_expect_tx(&hfull[L][1], C * sbytes);
+  }
+
+  for (int round = 0, tile = tile0; tile < a.ntiles || round * stride < a.ntiles; tile = tile_of(++round)) {
+    if (tile >= a.ntiles) continue;   // a partial last round
+    named_bar_sync(tile_bar, kLaneThreads);   // this lane's previous tile retired (s_meta rewritten)
+    if (warp < kLoad0 && e < NT) s_meta[L][e] = m_meta;
+    named_bar_sync(tile_bar, kLaneThreads);
+    if (warp == 8 * L) {
+      int ma = max(s_meta[L][lane].y, s_meta[L][lane + 32].y);
+      int mb = max(s_meta[L][lane + 64].y, s_meta[L][lane + 96].y);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ma = max(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+        mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+      }
+      if (lane == 0) { s_trip[L][0] = max(ma, mb); s_trip[L][1] = ma; s_trip[L][2] = mb; }
+    }
+    named_bar_sync(tile_bar, kLaneThreads);
+    const int trip = s_trip[L][0];
+
+    if (warp < kLoad0) {
+      // ======================= epilogue (lane L)
+      if (e < NT) {   // next tile's metadata and its h0/c0 rows -> L2
+        tile_meta(tile_of(round + 1));
+        if (m_meta.x >= 0) {
+          const char* h0n = reinterpret_cast<const char*>(a.h0 + (size_t)m_meta.x * H);
+          const char* c0n = a.c0 ? reinterpret_cast<const char*>(a.c0 + (size_t)m_meta.x * H) : nullptr;
+          for (int off = 0; off < H * 4; off += 128) {
+            prefetch_l2(h0n + off);
+            if (c0n) prefetch_l2(c0n + off);
+          }
+        }
+      }
+#pragma unroll
+      for (int ci = 0; ci < 16; ++ci) {
+        const int r = s_meta[L][cell_row(ci)].x;
+        hh[ci] = r >= 0 ? __ldg(a.h0 + (size_t)r * H + unit) : 0.f;
+        cc[ci] = (r >= 0 && a.c0) ? __ldg(a.c0 + (size_t)r * H + unit) : 0.f;
+      }
+      // fp16 h slice for step u -> L2 -> multicast into sH[u&1] of the even (ch 0) or odd (ch 1) CTAs
+      // Unit pairs: lanes l and l^4 hold units u, u^1 of the same rows; after one shuffle the
+      // even-unit lane holds (h_u, h_u+1) of row 2cq and the odd-unit lane those of row 2cq+1
+      // (within column group k), i.e. 2 consecutive units of one row per lane.
+      const bool ueven = ((lane >> 2) & 1) == 0;
+      const int ul = (lane >> 2) & ~1, er = ueven ? 0 : 1;
+      auto unit_pair = [&](int k) {
+        const int ci = (k >> 2) * 8 + (k & 3) * 2;
+        const float send = ueven ? hh[ci + 1] : hh[ci];
+        const float recv = __shfl_xor_sync(0xffffffffu, send, 4);
+        return ueven ? make_float2(hh[ci], recv) : make_float2(recv, hh[ci + 1]);
+      };
+      // fp16 h slice for step u -> L2 -> multicast into sH[u&1] of the even (ch 0) or odd (ch 1) CTAs
+      auto send_h = [&](uint32_t u) {
+        uint8_t* gs = a.hscratch + (((size_t)cluster_id_x() * 2 + L) * 2 + (u & 1)) * (size_t)(NT * a.Kh * 2) +
+                      (size_t)q * (NT * 64) + ch * sbytes;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float2 p = unit_pair(k);
+          const int nl = k * 8 + 2 * cq + er;
+          *reinterpret_cast<__half2*>(gs + qw * 1024 + (nl >> 3) * 128 + (nl & 7) * 16 + ul * 2) =
+              __floats2half2_rn(p.x, p.y);
+        }
+        fence_proxy_async_global();
+        named_bar_sync(1 + 2 * L + ch, 128);
+        if (qw == 0 && lane == 0)
+          bulk_g2s_multicast(sH + (u & 1) * hbytes + q * sbytes, gs, sbytes, &hfull[L][u & 1],
+                             ch ? odd_mask : even_mask);
+      };
+      if (trip > 0) send_h(step);
+      for (int t = 0; t < trip; ++t) {
+        const uint32_t s = step + t;
+        mbar_wait_sleep(&mdone[L], s & 1);
+        if (e == 0 && L == 0) SKB_TRACE(s, 4);
+        if (e == 0 && L == 0) SKB_TRACE_CTA(1, s, 11);
+        tc_fence_after();
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float ga[16], gb[16];
+          const uint32_t col = tmem + L * 128 + ch * 64 + half * 32;
+          tmem_ld_16x256b_x4(col + ((uint32_t)(qw * 32) << 16), ga);
+          tmem_ld_16x256b_x4(col + ((uint32_t)(qw * 32 + 16) << 16), gb);
+          tmem_ld_wait();
+          if (e == 0 && L == 0) SKB_TRACE(s, 5 + 5 * half);
+          if (e == 0 && L == 0 && half == 1) SKB_TRACE_CTA(1, s, 12);
+          if (half == 1) {   // D fully read: the next step's x-part may overwrite it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (leader) mbar_arrive(&dfree[L]);
+              else mbar_remote_arrive_relaxed(mapa(smem_u32(&dfree[L]), peer));   // no stores to publish
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {   // cells ci, ci+1: same unit, tile rows r, r+1
+            const int ci = half * 8 + j * 2;
+            const bool live0 = t < s_meta[L][cell_row(ci)].y, live1 = t < s_meta[L][cell_row(ci + 1)].y;
+            const float2 g0 = pact2<CELL, ACT, 0>(ga[4 * j], ga[4 * j + 1], kb0);
+            const float2 g1 = pact2<CELL, ACT, 1>(ga[4 * j + 2], ga[4 * j + 3], kb1);
+            const float2 g2 = pact2<CELL, ACT, 2>(gb[4 * j], gb[4 * j + 1], kb2);
+            const float2 g3 = pact2<CELL, ACT, 3>(gb[4 * j + 2], gb[4 * j + 3], kb3);
+            cell_update2<CELL, ACT>(g0, g1, g2, g3, cc[ci], cc[ci + 1], hh[ci], hh[ci + 1], live0, live1);
+          }
+        }
+        if (e == 0 && L == 0) SKB_TRACE(s, 6);
+        if (t + 1 < trip) send_h(s + 1);
+        if (e == 0 && L == 0) SKB_TRACE(s, 7);
+        if (e == 0 && L == 0) SKB_TRACE_CTA(1, s, 13);
+        // output sequence [R, T, H], two units per store (frozen tails: rnn_fill_frozen_kernel)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float2 p = unit_pair(k);
+          const int2 m = s_meta[L][ch * 64 + k * 8 + 2 * cq + er];
+          if (m.x >= 0 && t < m.y)
+            *reinterpret_cast<float2*>(a.out + ((size_t)m.x * T + t) * H + (int)q * 32 + qw * 8 + ul) = p;
+        }
+        if (e == 0 && L == 0) SKB_TRACE(s, 9);
+      }
+#pragma unroll
+      for (int ci = 0; ci < 16; ++ci) {
+        const int r = s_meta[L][cell_row(ci)].x;
+        if (r >= 0) {
+          a.hT[(size_t)r * H + unit] = hh[ci];
+          if (a.cT) a.cT[(size_t)r * H + unit] = cc[ci];
+        }
+      }
+    } else if (warp < kMma0) {
+      // ======================= x_t loader (lane L): this CTA's 64-row half of the tile
+      if (lane == 0) {
+        const int tself = s_trip[L][1 + odd];
+        const uint8_t* img = a.ximg + (size_t)(2 * tile + (int)odd) * T * xbytes;
+        for (int t = 0; t < trip; ++t) {
+          const uint32_t s = step + t;
+          mbar_wait_sleep(&xempty[L], (s & 1) ^ 1);
+          if (t < tself) {
+            mbar_arrive_expect_tx(&xfull[L], xbytes);
+            for (uint32_t off = 0; off < xbytes; off += 16384)
+              bulk_g2s(sX + off, img + (size_t)t * xbytes + off, min(16384u, xbytes - off), &xfull[L]);
+          } else {
+            mbar_arrive(&xfull[L]);   // every row of this half is past its length: stale (finite) image
+          }
+        }
+      }
+    } else if (leader) {
+      // ======================= MMA issuer (lane L): x-part(s0); then per step h-part(s), x-part(s+1)
+      const uint32_t idesc = idesc_f16_f32(256, NT);
+      const int kx_steps = a.Kx / 16, kh_steps = a.Kh / 16;
+      const uint64_t xdesc0 = sdesc_kmajor_noswz(smem_u32(sX), b_lbo, b_sbo);
+      const uint32_t d = tmem + L * 128;
+      auto x_part = [&](uint32_t s) {
+        mbar_wait_sleep(&xfull[L], s & 1);
+        if (lane == 0 && L == 0) SKB_TRACE(s, 0);
+        mbar_wait_sleep(&dfree[L], (s & 1) ^ 1);
+        if (lane == 0 && L == 0) SKB_TRACE(s, 1);
+        tc_fence_after();
+#pragma unroll 4
+        for (int ks = 0; ks < kx_steps; ++ks)
+          umma_f16_ts_pair_warp(d, tmem + kWCol + ks * 8, xdesc0 + (uint64_t)(ks * 2 * b_lbo >> 4), idesc,
+                                ks > 0 ? 1u : 0u);
+        umma_commit_pair_warp(&xempty[L], pair_mask);
+      };
+      if (trip > 0) x_part(step);
+      for (int t = 0; t < trip; ++t) {
+        const uint32_t s = step + t, j = s & 1;
+        mbar_wait_sleep(&hfull[L][j], (s >> 1) & 1);
+        if (lane == 0 && L == 0) SKB_TRACE(s, 2);
+        if (lane == 0) mbar_arrive_expect_tx(&hfull[L][j], C * sbytes);   // arm step s+2
+        tc_fence_after();
+        const uint64_t hdesc0 = sdesc_kmajor_noswz(smem_u32(sH + j * hbytes), b_lbo, b_sbo);
+#pragma unroll 4
+        for (int ks = 0; ks < kh_steps; ++ks)
+          umma_f16_ts_pair_warp(d, tmem + kWCol + (kx_steps + ks) * 8, hdesc0 + (uint64_t)(ks * 2 * b_lbo >> 4),
+                                idesc, 1u);
+        umma_commit_pair_warp(&mdone[L], pair_mask);
+        if (lane == 0 && L == 0) SKB_TRACE(s, 3);
+        if (t + 1 < trip) x_part(s + 1);
+      }
+    } else {
+      // ======================= relay (odd CTA, lane L): local x_t / h_t phases -> the leader
+      const uint32_t rx = mapa(smem_u32(&xfull[L]), peer);
+      if (trip > 0) {
+        mbar_wait_sleep(&xfull[L], step & 1);
+        if (lane == 0) mbar_remote_arrive(rx);
+      }
+      for (int t = 0; t < trip; ++t) {
+        const uint32_t s = step + t, j = s & 1;
+        mbar_wait_sleep(&hfull[L][j], (s >> 1) & 1);
+        if (lane == 0 && L == 0) SKB_TRACE_CTA(1, s, 14);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&hfull[L][j], C * sbytes);   // arm step s+2
+          mbar_remote_arrive(mapa(smem_u32(&hfull[L][j]), peer));
+        }
+        if (t + 1 < trip) {
+          mbar_wait_sleep(&xfull[L], (s + 1) & 1);
+          if (lane == 0 && L == 0) SKB_TRACE_CTA(1, s + 1, 15);
+          if (lane == 0) mbar_remote_arrive(rx);
+        }
+      }
+    }
+    __syncwarp();
+    step += trip;
+  }
+
+  // Drain the asynchronous arrivals aimed at this CTA before it exits: the last
+  // x-part's retire (xempty, both CTAs) and the peer's last D release (dfree, leader).
+  if (step > 0 && lane == 0) {
+    if (warp == kLoad0 + L) mbar_wait_sleep(&xempty[L], (step - 1) & 1);
+    if (leader && warp == 8 * L) mbar_wait_sleep(&dfree[L], (step - 1) & 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == kMma0) tmem_dealloc_pair<512>(tmem);
+}
+
+// ------------------------------------------------------------------ CTA-pair kernel, four lanes
+// Default for LSTM/GRU with 32-unit slices and an even CTA count.  The two-lane pair
+// kernel above leaves the tensor pipe half idle: per 128-row step its chain
+// (h-part MMAs -> MUFU-bound epilogue (~1.3 K cycles) -> L2 multicast exchange
+// (~3 K cycles)) is ~7.7 K cycles against 2 x 2.1 K cycles of MMA (tools/trace_pair.py).
+// A cta_group::2 MMA with N = 64 still runs at 89% of the N = 128 rate (36 vs 65
+// cycles, profiles/r02_umma_pair.txt), so this kernel runs four independent 64-row
+// recurrences per CTA pair in the same TMEM (D: 4 x 64 columns + weights) and shared
+// memory (per lane: x_t 32 rows + 2 x h_t 32 rows): each lane's chain is ~half as
+// long and four of them interleave on the tensor pipe.
+//   * warps 0-15: epilogue, lane L = warp / 4, TMEM quarter = warp % 4; each thread
+//     owns one unit x 16 rows (cols 0-31 of D = the even CTA's rows, 32-63 the odd's);
+//   * warps 16-19: lane L's role warp: x_t loader (+ L2 prefetch of x_{t+2}) and, in
+//     the even CTA, the MMA issuer; in the odd CTA the relay of its x_t / h_t phases.
+//   * x_t images are packed per 32-row half ("halves" layout of the pack kernels).
+template <typename XT, int ACT = 1, int CELL = SKB_CELL_LSTM>
+__global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_pair4_kernel(const RnnArgs a) {
+  constexpr int NL = 4, NT = 64, NH = 32, EWL = 4, kEpiL = EWL * 32;
+  constexpr int kRole0 = 16;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint64_t xfull[NL], xempty[NL], hfull[NL][2], mdone[NL], dfree[NL];
+  __shared__ uint32_t tmem_s;
+  __shared__ int2 s_meta[NL][NT];   // (row, clamped length) of the lane's tile rows
+  __shared__ int s_trip[NL][3];     // [lane]: tile trip, trip of rows 0-31, trip of rows 32-63
+  __shared__ int s_tmax[NL][NT];    // the row's problem trip count (its output rows)
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int L = warp < kRole0 ? (warp >> 2) : warp - kRole0;
+  const uint32_t q = cluster_ctarank(), odd = q & 1u, peer = q ^ 1u;
+  const bool leader = odd == 0;
+  const int C = a.C, H = a.H, T = a.T;
+  const uint32_t xbytes = NH * a.Kx * 2, hbytes = NH * a.Kh * 2;
+  constexpr uint32_t sbytes = NH * 32 * 2;   // one CTA's h slice of one 32-row half (2 KB)
+  const uint32_t lane_bytes = xbytes + 2 * hbytes;
+  uint8_t* sX = smem_raw + L * lane_bytes;   // [NH x Kx] fp16, core-matrix layout
+  uint8_t* sH = sX + xbytes;                 // 2 x [NH x Kh] fp16
+  constexpr uint32_t b_lbo = NH * 16, b_sbo = 128;
+  constexpr uint32_t kWCol = 256;
+  const uint16_t pair_mask = (uint16_t)(3u << (q & ~1u));
+  uint16_t even_mask = 0;
+  for (int i = 0; i < C; i += 2) even_mask |= (uint16_t)(1u << i);
+  const uint16_t odd_mask = (uint16_t)(even_mask << 1);
+
+  if (tid == 0) {
+    for (int l = 0; l < NL; ++l) {
+      mbar_init(&xfull[l], leader ? 2 : 1);      // own bulk load (+ the odd CTA's relay)
+      mbar_init(&xempty[l], 1);
+      mbar_init(&hfull[l][0], leader ? 2 : 1);   // own arm (+ relay)
+      mbar_init(&hfull[l][1], leader ? 2 : 1);
+      mbar_init(&mdone[l], 1);
+      mbar_init(&dfree[l], 2 * EWL);             // epilogue warps of both CTAs (leader's copy is used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == kRole0) tmem_alloc_pair<512>(&tmem_s);
+  for (uint32_t i = tid; i < NL * lane_bytes / 16; i += 20 * 32)
+    reinterpret_cast<uint4*>(smem_raw)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_s;
+  if (warp < 4) {
+    // TMEM lane l = 32w + 8g + u <- packed slab row 32g + 8w + u (gate g of unit 8w + u)
+    const int srow = ((tid & 31) >> 3) * 32 + warp * 8 + (tid & 7);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.wpack + ((size_t)q * 128 + srow) * a.K * 2);
+    for (int c0 = 0; c0 < a.K / 2; c0 += 8) {
+      uint32_t r[8];
+      const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src + c0));
+      const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src + c0 + 4));
+      r[0] = lo.x; r[1] = lo.y; r[2] = lo.z; r[3] = lo.w; r[4] = hi.x; r[5] = hi.y; r[6] = hi.z; r[7] = hi.w;
+      tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + kWCol + c0, r);
+    }
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  cluster_sync();   // every CTA's barriers and TMEM are initialised before any remote traffic
+
+  // epilogue thread: TMEM quarter qw, unit uc = 8qw + lane/4 of the CTA's slice,
+  // tile rows 32h + 8j + 2(lane%4) + e  (h: D column half = destination parity)
+  const int qw = warp & 3, cq = lane & 3, e = tid & (kEpiL - 1);
+  const int uc = qw * 8 + (lane >> 2), unit = (int)q * 32 + uc;
+  float kb0 = 0.f, kb1 = 0.f, kb2 = 0.f, kb3 = 0.f;
+  if (warp < kRole0) {
+    const float* bp = a.bpack + q * 128 + uc;
+    kb0 = pact_kb<CELL, ACT, 0>(bp[0]);
+    kb1 = pact_kb<CELL, ACT, 1>(bp[32]);
+    kb2 = pact_kb<CELL, ACT, 2>(bp[64]);
+    kb3 = pact_kb<CELL, ACT, 3>(bp[96]);
+  }
+  float hh[16], cc[16];
+  const uint32_t tile_bar = 1 + L, xch_bar = 1 + NL + L;
+  constexpr uint32_t kLaneThreads = kEpiL + 32;
+  auto cell_row = [&](int ci) { return (ci >> 3) * 32 + ((ci >> 1) & 3) * 8 + 2 * cq + (ci & 1); };
+
+  uint32_t step = 0;
+  const int nclusters = (int)nclusters_x();
+  const int stride = NL * nclusters;
+  int2 m_meta = make_int2(-1, 0);
+  int m_tmax = 0;
+  auto tile_meta = [&](int tl) {
+    m_meta = make_int2(-1, 0);
+    m_tmax = 0;
+    if (tl < a.ntiles) {
+      const int r = a.perm[tl * NT + e];
+      if (r >= 0) {
+        m_tmax = max(0, min(a.pmax[r / a.Bp], T));
+        m_meta = make_int2(r, (int)max(0LL, min((long long)a.lens[r], (long long)m_tmax)));
+      }
+    }
+  };
+  // tiles sorted longest first; round k hands out [k*stride, (k+1)*stride) in snake order
+  const int pos = NL * (int)cluster_id_x() + L;
+  auto tile_of = [&](int k) { return k * stride + ((k & 1) ? stride - 1 - pos : pos); };
+  const int tile0 = tile_of(0);
+  if (warp < kRole0 && e < NT) tile_meta(tile0);
+  if (warp == kRole0 + L && lane == 0) {   // arm the h phases of steps 0 and 1
+    mbar_arrive_expect_tx(&hfull[L][0], C * sbytes);
+    mbar_arrive_expect_tx(&hfull[L][1], C * sbytes);
+  }
+
+  for (int round = 0, tile = tile0; tile < a.ntiles || round * stride < a.ntiles; tile = tile_of(++round)) {
+    if (tile >= a.ntiles) continue;   // a partial last round
+    named_bar_sync(tile_bar, kLaneThreads);   // this lane's previous tile retired (s_meta rewritten)
+    if (warp < kRole0 && e < NT) { s_meta[L][e] = m_meta; s_tmax[L][e] = m_tmax; }
+    named_bar_sync(tile_bar, kLaneThreads);
+    if (warp == kRole0 + L) {
+      int ma = s_meta[L][lane].y, mb = s_meta[L][lane + 32].y;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ma = max(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+        mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+      }
+      if (lane == 0) { s_trip[L][0] = max(ma, mb); s_trip[L][1] = ma; s_trip[L][2] = mb; }
+    }
+    named_bar_sync(tile_bar, kLaneThreads);
+    const int trip = s_trip[L][0];
+
+    if (warp < kRole0) {
+      // ======================= epilogue (lane L)
+      if (e < NT) {   // next tile's metadata and its h0/c0 rows -> L2
+        tile_meta(tile_of(round + 1));
+        if (m_meta.x >= 0) {
+          const char* h0n = reinterpret_cast<const char*>(a.h0 + (size_t)m_meta.x * H);
+          const char* c0n = a.c0 ? reinterpret_cast<const char*>(a.c0 + (size_t)m_meta.x * H) : nullptr;
+          for (int off = 0; off < H * 4; off += 128) {
+            prefetch_l2(h0n + off);
+            if (c0n) prefetch_l2(c0n + off);
+          }
+        }
+      }
+#pragma unroll
+      for (int ci = 0; ci < 16; ++ci) {
+        const int r = s_meta[L][cell_row(ci)].x;
+        hh[ci] = r >= 0 ? __ldg(a.h0 + (size_t)r * H + unit) : 0.f;
+        cc[ci] = (r >= 0 && a.c0) ? __ldg(a.c0 + (size_t)r * H + unit) : 0.f;
+      }
+      // lanes l and l^4 hold units u, u^1 of the same rows: after one shuffle the even-unit
+      // lane holds (h_u, h_u+1) of row 2cq, the odd-unit lane those of row 2cq+1 (group k)
+      const bool ueven = ((lane >> 2) & 1) == 0;
+      const int ul = (lane >> 2) & ~1, er = ueven ? 0 : 1;
+      auto unit_pair = [&](int k) {
+        const int ci = (k >> 2) * 8 + (k & 3) * 2;
+        const float send = ueven ? hh[ci + 1] : hh[ci];
+        const float recv = __shfl_xor_sync(0xffffffffu, send, 4);
+        return ueven ? make_float2(hh[ci], recv) : make_float2(recv, hh[ci + 1]);
+      };
+      // fp16 h slices for step u -> L2 -> multicast: rows 0-31 into sH[u&1] of the even
+      // CTAs, rows 32-63 into the odd CTAs'
+      auto send_h = [&](uint32_t u) {
+        uint8_t* gs = a.hscratch + (((size_t)cluster_id_x() * NL + L) * 2 + (u & 1)) * (size_t)(NT * a.Kh * 2) +
+                      (size_t)q * (2 * sbytes);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float2 p = unit_pair(k);
+          const int nl = (k & 3) * 8 + 2 * cq + er;   // row within the half k >> 2
+          *reinterpret_cast<__half2*>(gs + (k >> 2) * sbytes + qw * (NH * 16) + (nl >> 3) * 128 + (nl & 7) * 16 +
+                                      ul * 2) = __floats2half2_rn(p.x, p.y);
+        }
+        fence_proxy_async_global();
+        named_bar_sync(xch_bar, kEpiL);
+        if (qw < 2 && lane == 0)
+          bulk_g2s_multicast(sH + (u & 1) * hbytes + q * sbytes, gs + qw * sbytes, sbytes, &hfull[L][u & 1],
+                             qw ? odd_mask : even_mask);
+      };
+      if (trip > 0) send_h(step);
+      for (int t = 0; t < trip; ++t) {
+        const uint32_t s = step + t;
+        mbar_wait_sleep(&mdone[L], s & 1);
+        if (e == 0 && L == 0) SKB_TRACE(s, 4);
+        tc_fence_after();
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float ga[16], gb[16];
+          const uint32_t col = tmem + L * NT + half * 32;
+          tmem_ld_16x256b_x4(col + ((uint32_t)(qw * 32) << 16), ga);
+          tmem_ld_16x256b_x4(col + ((uint32_t)(qw * 32 + 16) << 16), gb);
+          tmem_ld_wait();
+          if (half == 1) {   // D fully read: the next step's x-part may overwrite it
+            if (e == 0 && L == 0) SKB_TRACE(s, 10);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (leader) mbar_arrive(&dfree[L]);
+              else mbar_remote_arrive_relaxed(mapa(smem_u32(&dfree[L]), peer));   // no stores to publish
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {   // cells ci, ci+1: same unit, tile rows r, r+1
+            const int ci = half * 8 + j * 2;
+            const bool live0 = t < s_meta[L][cell_row(ci)].y, live1 = t < s_meta[L][cell_row(ci + 1)].y;
+            const float2 g0 = pact2<CELL, ACT, 0>(ga[4 * j], ga[4 * j + 1], kb0);
+            const float2 g1 = pact2<CELL, ACT, 1>(ga[4 * j + 2], ga[4 * j + 3], kb1);
+            const float2 g2 = pact2<CELL, ACT, 2>(gb[4 * j], gb[4 * j + 1], kb2);
+            const float2 g3 = pact2<CELL, ACT, 3>(gb[4 * j + 2], gb[4 * j + 3], kb3);
+            cell_update2<CELL, ACT>(g0, g1, g2, g3, cc[ci], cc[ci + 1], hh[ci], hh[ci + 1], live0, live1);
+          }
+        }
+        if (e == 0 && L == 0) SKB_TRACE(s, 6);
+        if (t + 1 < trip) {
+          send_h(s + 1);
+          if (e == 0 && L == 0) SKB_TRACE(s, 7);
+        }
+        if (e == 0 && L == 0) SKB_TRACE(s, 8);
+        // output sequence [R, T, H] for t < the problem's trip count (frozen rows repeat h),
+        // two units per store
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float2 p = unit_pair(k);
+          const int n = (k >> 2) * 32 + (k & 3) * 8 + 2 * cq + er;
+          const int r = s_meta[L][n].x;
+          if (r >= 0 && t < (a.fill_inkernel ? s_tmax[L][n] : s_meta[L][n].y))
+            *reinterpret_cast<float2*>(a.out + ((size_t)r * T + t) * H + (int)q * 32 + qw * 8 + ul) = p;
+        }
+        if (e == 0 && L == 0) SKB_TRACE(s, 9);
+      }
+      // frozen tails past the tile's trip count: out[r, t, :] = h_T for trip <= t < tmax
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float2 p = unit_pair(k);
+        const int n = (k >> 2) * 32 + (k & 3) * 8 + 2 * cq + er;
+        const int r = s_meta[L][n].x, tm = s_tmax[L][n];
+        if (r >= 0 && a.fill_inkernel) {
+          float* o = a.out + ((size_t)r * T) * H + (int)q * 32 + qw * 8 + ul;
+          for (int t = trip; t < tm; ++t) *reinterpret_cast<float2*>(o + (size_t)t * H) = p;
+        }
+      }
+#pragma unroll
+      for (int ci = 0; ci < 16; ++ci) {
+        const int r = s_meta[L][cell_row(ci)].x;
+        if (r >= 0) {
+          a.hT[(size_t)r * H + unit] = hh[ci];
+          if (a.cT) a.cT[(size_t)r * H + unit] = cc[ci];
+        }
+      }
+    } else {
+      // ======================= role warp (lane L): x_t image loads (pre-pass images), MMA
+      // issuer (even CTA) / relay (odd CTA)
+      const int tself = s_trip[L][1 + odd];
+      const uint8_t* img = a.ximg + ((size_t)tile * T * 2 + odd) * xbytes;   // [tile][t][half] images
+      auto bulk_x = [&](int t, uint32_t u) {   // slot free: x-part(u-1) retired
+        mbar_wait_sleep(&xempty[L], (u & 1) ^ 1);
+        if (lane == 0) {
+          if (t < tself) {
+            mbar_arrive_expect_tx(&xfull[L], xbytes);
+            bulk_g2s(sX, img + (size_t)t * 2 * xbytes, xbytes, &xfull[L]);
+            // the image two steps ahead -> L2 (an HBM miss here delays x-part(t+1) and with it
+            // the h-part queued behind it: measured 1.2 vs 2.5 ms per launch)
+            if (t + 2 < tself) bulk_prefetch_l2(img + (size_t)(t + 2) * 2 * xbytes, xbytes);
+          } else {
+            mbar_arrive(&xfull[L]);   // every row of this half is past its length: stale (finite) image
+          }
+        }
+        __syncwarp();
+      };
+      if (leader) {
+        const uint32_t idesc = idesc_f16_f32(256, NT);
+        const int kx_steps = a.Kx / 16, kh_steps = a.Kh / 16;
+        const uint64_t xdesc0 = sdesc_kmajor_noswz(smem_u32(sX), b_lbo, b_sbo);
+        const uint32_t d = tmem + L * NT;
+        auto x_part = [&](uint32_t s) {
+          mbar_wait_sleep(&xfull[L], s & 1);
+          if (lane == 0 && L == 0) SKB_TRACE(s, 0);
+          mbar_wait_sleep(&dfree[L], (s & 1) ^ 1);
+          if (lane == 0 && L == 0) SKB_TRACE(s, 1);
+          tc_fence_after();
+#pragma unroll 4
+          for (int ks = 0; ks < kx_steps; ++ks)
+            umma_f16_ts_pair_warp(d, tmem + kWCol + ks * 8, xdesc0 + (uint64_t)(ks * 2 * b_lbo >> 4), idesc,
+                                  ks > 0 ? 1u : 0u);
+          umma_commit_pair_warp(&xempty[L], pair_mask);
+        };
+        if (trip > 0) {
+          if (tself > 1 && lane == 0) bulk_prefetch_l2(img + (size_t)2 * xbytes, xbytes);
+          bulk_x(0, step);
+          x_part(step);
+        }
+        for (int t = 0; t < trip; ++t) {
+          const uint32_t s = step + t, j = s & 1;
+          mbar_wait_sleep(&hfull[L][j], (s >> 1) & 1);
+          if (lane == 0 && L == 0) SKB_TRACE(s, 2);
+          if (lane == 0) mbar_arrive_expect_tx(&hfull[L][j], C * sbytes);   // arm step s+2
+          tc_fence_after();
+          const uint64_t hdesc0 = sdesc_kmajor_noswz(smem_u32(sH + j * hbytes), b_lbo, b_sbo);
+#pragma unroll 4
+          for (int ks = 0; ks < kh_steps; ++ks)
+            umma_f16_ts_pair_warp(d, tmem + kWCol + (kx_steps + ks) * 8, hdesc0 + (uint64_t)(ks * 2 * b_lbo >> 4),
+                                  idesc, 1u);
+          umma_commit_pair_warp(&mdone[L], pair_mask);
+          if (lane == 0 && L == 0) SKB_TRACE(s, 3);
+          if (t + 1 < trip) {
+            bulk_x(t + 1, s + 1);
+            x_part(s + 1);
+          }
+        }
+      } else {
+        const uint32_t rx = mapa(smem_u32(&xfull[L]), peer);
+        auto relay_x = [&](int t, uint32_t s) {
+          bulk_x(t, s);
+          mbar_wait_sleep(&xfull[L], s & 1);
+          if (lane == 0) mbar_remote_arrive(rx);
+        };
+        if (trip > 0) relay_x(0, step);
+        for (int t = 0; t < trip; ++t) {
+          const uint32_t s = step + t, j = s & 1;
+          mbar_wait_sleep(&hfull[L][j], (s >> 1) & 1);
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&hfull[L][j], C * sbytes);   // arm step s+2
+            mbar_remote_arrive(mapa(smem_u32(&hfull[L][j]), peer));
+          }
+          if (t + 1 < trip) relay_x(t + 1, s + 1);
+        }
+      }
+    }
+    __syncwarp();
+    step += trip;
+  }
+
+  // Drain the asynchronous arrivals aimed at this CTA before it exits: the last
+  // x-part's retire (xempty, both CTAs) and the peer's last D release (dfree, leader).
+  if (step > 0 && lane == 0 && warp == kRole0 + L) {
+    mbar_wait_sleep(&xempty[L], (step - 1) & 1);
+    if (leader) mbar_wait_sleep(&dfree[L], (step - 1) & 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == kRole0) tmem_dealloc_pair<512>(tmem);
+}
+
 // ------------------------------------------------------------------ ping-pong LSTM kernel
 // The rows of a 64-row tile form two independent 32-row recurrences (halves).
 // The MMA warp alternates halves: while half A's epilogue (warps 0-7) turns
@@ -1420,7 +2206,7 @@ template <typename XT>
 __global__ void __launch_bounds__(256) pack_x_kernel(const XT* __restrict__ x, const int32_t* __restrict__ perm,
                               const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
                               uint8_t* __restrict__ img, int32_t* err, int ntiles, int T, int F,
-                              int Kx, int Bp) {
+                              int Kx, int Bp, int halves) {
   // One block per (tile, t) image; item = (n, kc) with n fastest, so a warp reads
   // 32 rows x 32 B sectors and writes 512 contiguous bytes of image.  Row-steps
   // past the row's length are skipped (their MMA columns are masked).
@@ -1463,7 +2249,9 @@ __global__ void __launch_bounds__(256) pack_x_kernel(const XT* __restrict__ x, c
         __half2 h2 = __floats2half2_rn(v[m][2 * e], v[m][2 * e + 1]);
         w[e] = *reinterpret_cast<uint32_t*>(&h2);
       }
-      *reinterpret_cast<uint4*>(dst0 + cm_offset(n, kc * 8, kNT * 16, 128)) = make_uint4(w[0], w[1], w[2], w[3]);
+      const uint32_t off = halves ? (n >> 5) * (32 * Kx * 2) + cm_offset(n & 31, kc * 8, 32 * 16, 128)
+                                  : cm_offset(n, kc * 8, kNT * 16, 128);
+      *reinterpret_cast<uint4*>(dst0 + off) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
   if (bad) set_err(err, SKB_ERR_FP16_RANGE, -1, -1);
@@ -1477,7 +2265,7 @@ __global__ void __launch_bounds__(256) pack_x_kernel(const XT* __restrict__ x, c
 template <int NQ>
 __global__ void __launch_bounds__(256) pack_x_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
                                    const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
-                                   uint8_t* __restrict__ img, int32_t* err, int T, int Bp) {
+                                   uint8_t* __restrict__ img, int32_t* err, int T, int Bp, int halves) {
   constexpr int F = NQ * 128, kRow = F * 2 + 16;   // padded fp16 row: 16-byte reads of 8 lanes hit distinct banks
   extern __shared__ __align__(16) uint8_t srow[];
   const int tile = blockIdx.x, t = blockIdx.y;
@@ -1517,7 +2305,8 @@ __global__ void __launch_bounds__(256) pack_x_rows_kernel(const float* __restric
 #pragma unroll 4
   for (int o = threadIdx.x; o < kChunks; o += 256) {
     const int n = o % kNT, kc = o / kNT;
-    out[o] = *reinterpret_cast<const uint4*>(srow + n * kRow + kc * 16);
+    out[halves ? (n >> 5) * (32 * F / 8) + kc * 32 + (n & 31) : o] =
+        *reinterpret_cast<const uint4*>(srow + n * kRow + kc * 16);
   }
   if (bad) set_err(err, SKB_ERR_FP16_RANGE, -1, -1);
 }
@@ -1535,14 +2324,18 @@ inline int max_clusters_bound(const RnnGeom& g) {
   return sms / g.C + 1;
 }
 
+// 64-row x-image tiles, padded to an even count (the pair kernel's 128-row tiles)
+inline int n_tiles64(const RnnGeom& g) { return round_up((g.R + kNT - 1) / kNT, 2); }
+
 inline int64_t ws_layout(const RnnGeom& g, uint8_t* basep, Workspace* w) {
-  const int ntiles = (g.R + kNT - 1) / kNT;
+  const int ntiles = n_tiles64(g);
   int64_t off = 0;
   auto take = [&](int64_t n) { int64_t o = off; off += (n * 4 + 255) / 256 * 256; return o; };
   int64_t o_perm = take((int64_t)ntiles * kNT), o_pmax = take(g.P), o_hist = take(g.T + 1),
           o_base = take(g.T + 1), o_cur = take(g.T + 1);
-  // h_t exchange scratch: per cluster 2 x [NT x Kh] fp16 (int32 units for take())
-  int64_t o_hs = take((int64_t)max_clusters_bound(g) * 2 * kNT * g.Kh * 2 / 4);
+  // h_t exchange scratch (int32 units for take()): per cluster 2 x [64 x Kh] fp16 (dual-lane
+  // kernel) or 2 lanes x 2 step parities x [128 x Kh] fp16 (pair kernel)
+  int64_t o_hs = take((int64_t)max_clusters_bound(g) * 4 * 2 * kNT * g.Kh * 2 / 4);
   int64_t o_x = take((int64_t)ntiles * g.T * kNT * g.Kx * 2 / 4);
   int64_t o_hT = take((int64_t)g.R * g.H);
   if (w) {
@@ -1595,6 +2388,7 @@ int g_prof_cap = 0, g_prof_n = 0;
 template <int CELL, typename XT, int EW, int ACT = 0>
 int launch_main_ew(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
   auto kern = rnn_fwd_kernel<CELL, kNT, XT, EW, ACT>;
+  g_last_kernel = SKB_RNN_KERNEL_SINGLE;
   constexpr int kThreads = EW * 32 + 64;
   const size_t smem = smem_bytes<kNT>(g);
   if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
@@ -1617,6 +2411,7 @@ int launch_main_ew(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
     return SKB_ERR_CUDA;
   const int ncl = min(min(max_clusters, args.ntiles), max_clusters_bound(g) - 1);
   cfg.gridDim = dim3(g.C * max(ncl, 1));
+  g_last_clusters = max(ncl, 1);
   const bool prof = g_prof_n < g_prof_cap;
   if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], stream);
   if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
@@ -1639,6 +2434,7 @@ inline bool rnn_pp() {
 template <typename XT, int ACT>
 int launch_pp(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
   auto kern = rnn_fwd_pp_kernel<XT, ACT>;
+  g_last_kernel = SKB_RNN_KERNEL_PING_PONG;
   constexpr int kThreads = 16 * 32 + 64;
   const size_t smem = smem_bytes<kNT>(g);
   if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
@@ -1661,6 +2457,7 @@ int launch_pp(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
     return SKB_ERR_CUDA;
   const int ncl = min(min(max_clusters, args.ntiles), max_clusters_bound(g) - 1);
   cfg.gridDim = dim3(g.C * max(ncl, 1));
+  g_last_clusters = max(ncl, 1);
   const bool prof = g_prof_n < g_prof_cap;
   if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], stream);
   if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
@@ -1682,6 +2479,7 @@ inline bool rnn_dl() {
 template <typename XT, int ACT, int CELL = SKB_CELL_LSTM>
 int launch_dl(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
   auto kern = rnn_fwd_dl_kernel<XT, ACT, CELL>;
+  g_last_kernel = SKB_RNN_KERNEL_DUAL_LANE;
   constexpr int kThreads = 20 * 32;
   const size_t smem = (size_t)2 * (kNT * g.Kx * 2 + kNT * g.Kh * 2 + 4 * kNT * kGS * 4) + 1024;
   if (smem > 227 * 1024) return SKB_ERR_UNSUPPORTED;
@@ -1704,6 +2502,7 @@ int launch_dl(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
     return SKB_ERR_CUDA;
   const int ncl = min(min(max_clusters, (args.ntiles + 1) / 2), max_clusters_bound(g) - 1);
   cfg.gridDim = dim3(g.C * max(ncl, 1));
+  g_last_clusters = max(ncl, 1);
   const bool prof = g_prof_n < g_prof_cap;
   if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], stream);
   if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
@@ -1711,23 +2510,133 @@ int launch_dl(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
   return skb_check_launch();
 }
 
+// CTA-pair kernel (default for LSTM/GRU with 32-unit slices and an even CTA count;
+// SKB_RNN_PAIR=0 selects the dual-lane kernel).
+inline bool rnn_pair() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SKB_RNN_PAIR");
+    v = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+inline size_t pair_smem(const RnnGeom& g) { return (size_t)2 * (64 * g.Kx * 2 + 2 * 64 * g.Kh * 2) + 1024; }
+inline size_t pair4_smem(const RnnGeom& g) { return (size_t)4 * (32 * g.Kx * 2 + 2 * 32 * g.Kh * 2) + 1024; }
+inline bool pair_ok(const RnnGeom& g) {
+  return rnn_pair() && g.U == 32 && g.H == g.C * 32 && g.Kh == g.H && g.C % 2 == 0 && g.C >= 2 &&
+         pair_smem(g) <= 227 * 1024;
+}
+
+template <typename XT, int ACT, int CELL = SKB_CELL_LSTM>
+int launch_pair(RnnArgs args, const RnnGeom& g, cudaStream_t stream) {
+  auto kern = rnn_fwd_pair_kernel<XT, ACT, CELL>;
+  g_last_kernel = SKB_RNN_KERNEL_PAIR2;
+  constexpr int kThreads = 20 * 32;
+  const size_t smem = pair_smem(g);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SKB_ERR_CUDA;
+  args.ntiles = (args.ntiles + 1) / 2;   // 128-row tiles = pairs of 64-row x-image tiles
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(g.C);
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
+    return SKB_ERR_CUDA;
+  const int ncl = min(min(max_clusters, (args.ntiles + 1) / 2), max_clusters_bound(g) - 1);
+  cfg.gridDim = dim3(g.C * max(ncl, 1));
+  g_last_clusters = max(ncl, 1);
+  const bool prof = g_prof_n < g_prof_cap;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], stream);
+  if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n++ + 1], stream);
+  return skb_check_launch();
+}
+template <typename XT, int ACT, int CELL = SKB_CELL_LSTM>
+int launch_pair4(RnnArgs args, const RnnGeom& g, cudaStream_t stream) {
+  auto kern = rnn_fwd_pair4_kernel<XT, ACT, CELL>;
+  g_last_kernel = SKB_RNN_KERNEL_PAIR;
+  constexpr int kThreads = 20 * 32;
+  const size_t smem = pair4_smem(g);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SKB_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(g.C);
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
+    return SKB_ERR_CUDA;
+  const int ncl = min(min(max_clusters, (args.ntiles + 3) / 4), max_clusters_bound(g) - 1);
+  cfg.gridDim = dim3(g.C * max(ncl, 1));
+  g_last_clusters = max(ncl, 1);
+  const bool prof = g_prof_n < g_prof_cap;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], stream);
+  if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n++ + 1], stream);
+  return skb_check_launch();
+}
+
+
+// Which recurrent kernel runs (SKB_RNN_KERNEL_*): the CTA-pair kernels for LSTM/GRU with
+// 32-unit slices and an even CTA count (SKB_RNN_PAIR: 1 = four 64-row lanes, the default;
+// 2 = two 128-row lanes; 0 = off), else the dual-lane / ping-pong / single kernels.
+inline int rnn_pair_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SKB_RNN_PAIR");
+    v = e ? atoi(e) : 1;
+    if (v < 0 || v > 2) v = 1;
+  }
+  return v;
+}
+inline int kernel_choice(const RnnGeom& g, bool has_c0) {
+  const bool slices32 = g.U == 32 && g.H == g.C * 32 && g.Kh == g.H;
+  const bool cell4 = g.cell == SKB_CELL_GRU || (g.cell == SKB_CELL_LSTM && has_c0);
+  if (g.cell == SKB_CELL_LSTM || g.cell == SKB_CELL_GRU) {
+    if (rnn_dl() && !rnn_pp() && rnn_ew() == 16 && cell4 && pair_ok(g) && rnn_pair_mode() != 0)
+      return rnn_pair_mode() == 2 ? SKB_RNN_KERNEL_PAIR2 : SKB_RNN_KERNEL_PAIR;
+    if (rnn_dl() && !rnn_pp() && rnn_ew() == 16 && slices32 && cell4) return SKB_RNN_KERNEL_DUAL_LANE;
+    if (g.cell == SKB_CELL_LSTM && rnn_pp() && g.U == 32 && g.Kh == g.C * 32) return SKB_RNN_KERNEL_PING_PONG;
+  }
+  return SKB_RNN_KERNEL_SINGLE;
+}
+
 template <int CELL, typename XT>
 int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
-  if constexpr (CELL == SKB_CELL_LSTM) {
-    const bool act = rnn_act() == 1;
-    // the ping-pong and dual-lane kernels need 32-unit CTA slices (U = 32: H a multiple of 32)
-    if (rnn_dl() && !rnn_pp() && rnn_ew() == 16 && g.U == 32 && g.H == g.C * 32 && g.Kh == g.H && args.c0)
-      return act ? launch_dl<XT, 1>(args, g, stream) : launch_dl<XT, 0>(args, g, stream);
-    if (rnn_pp() && g.U == 32 && g.Kh == g.C * 32)
-      return act ? launch_pp<XT, 1>(args, g, stream) : launch_pp<XT, 0>(args, g, stream);
-    if (rnn_ew() == 8)
-      return act ? launch_main_ew<CELL, XT, 8, 1>(args, g, stream) : launch_main_ew<CELL, XT, 8, 0>(args, g, stream);
-    return act ? launch_main_ew<CELL, XT, 16, 1>(args, g, stream) : launch_main_ew<CELL, XT, 16, 0>(args, g, stream);
-  }
-  if constexpr (CELL == SKB_CELL_GRU) {
-    const bool act = rnn_act() == 1;
-    if (rnn_dl() && rnn_ew() == 16 && g.U == 32 && g.H == g.C * 32 && g.Kh == g.H)
+  const int act = rnn_act();
+  const int k = kernel_choice(g, args.c0 != nullptr);
+  if constexpr (CELL == SKB_CELL_LSTM || CELL == SKB_CELL_GRU) {
+    if (k == SKB_RNN_KERNEL_PAIR)
+      return act == 2 ? launch_pair4<XT, 2, CELL>(args, g, stream)
+                      : (act ? launch_pair4<XT, 1, CELL>(args, g, stream) : launch_pair4<XT, 0, CELL>(args, g, stream));
+    if (k == SKB_RNN_KERNEL_PAIR2)
+      return act == 2 ? launch_pair<XT, 2, CELL>(args, g, stream)
+                      : (act ? launch_pair<XT, 1, CELL>(args, g, stream) : launch_pair<XT, 0, CELL>(args, g, stream));
+    if (k == SKB_RNN_KERNEL_DUAL_LANE)
       return act ? launch_dl<XT, 1, CELL>(args, g, stream) : launch_dl<XT, 0, CELL>(args, g, stream);
+  }
+  if constexpr (CELL == SKB_CELL_LSTM) {
+    if (k == SKB_RNN_KERNEL_PING_PONG)
+      return act ? launch_pp<XT, 1>(args, g, stream) : launch_pp<XT, 0>(args, g, stream);
+  }
+  if constexpr (CELL == SKB_CELL_LSTM || CELL == SKB_CELL_GRU) {
     if (rnn_ew() == 8)
       return act ? launch_main_ew<CELL, XT, 8, 1>(args, g, stream) : launch_main_ew<CELL, XT, 8, 0>(args, g, stream);
     return act ? launch_main_ew<CELL, XT, 16, 1>(args, g, stream) : launch_main_ew<CELL, XT, 16, 0>(args, g, stream);
@@ -1736,6 +2645,9 @@ int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
 }
 
 }  // namespace
+
+extern "C" int skb_rnn_last_kernel(void) { return g_last_kernel; }
+extern "C" int skb_rnn_last_clusters(void) { return g_last_clusters; }
 
 extern "C" int skb_profile_begin(int max_launches) {
   if (max_launches < 0 || max_launches > kProfMax) return SKB_ERR_INVALID;
@@ -1860,7 +2772,7 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   cudaStream_t st = (cudaStream_t)stream;
   Workspace w;
   ws_layout(g, reinterpret_cast<uint8_t*>(workspace_dev), &w);
-  const int ntiles = (g.R + kNT - 1) / kNT;
+  const int ntiles = n_tiles64(g);
   SchedArgs sa = {len_dev, w.perm, w.pmax, w.hist, w.base, w.cursor, max_len_dev, err_dev,
                   g.R, g.Bp, g.P, g.T, ntiles * kNT};
   const int blocks = min(1184, max(1, (max(g.R, g.P) + 255) / 256));
@@ -1877,30 +2789,35 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   a.out = out_dev; a.hT = hT_dev ? hT_dev : w.hT; a.cT = cT_dev; a.err = err_dev; a.x_f64 = x_f64;
   a.hscratch = w.hscratch;
   a.ximg = w.ximg;
+  // the four-lane pair kernel reads 32-row half images; it can write the frozen tails
+  // itself (SKB_RNN_INFILL=1)
+  const bool pair4 = kernel_choice(g, c0_dev != nullptr) == SKB_RNN_KERNEL_PAIR;
+  a.fill_inkernel = pair4 && env_flag("SKB_RNN_INFILL", 0);
   {
     const dim3 pg(ntiles, g.T);
+    const int halves = pair4 ? 1 : 0;
     const bool rows_ok = !x_f64 && g.F == g.Kx && (reinterpret_cast<uintptr_t>(x_dev) & 15) == 0 &&
                          (g.F == 128 || g.F == 256 || g.F == 512) && !getenv("SKB_PACK_X_LEGACY");
     if (x_f64)
       pack_x_kernel<double><<<pg, 256, 0, st>>>((const double*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
-                                                  err_dev, ntiles, g.T, g.F, g.Kx, g.Bp);
+                                                  err_dev, ntiles, g.T, g.F, g.Kx, g.Bp, halves);
     else if (rows_ok) {
       const size_t sm = (size_t)kNT * (g.F * 2 + 16);
       if (g.F == 128)
-        pack_x_rows_kernel<1><<<pg, 256, sm, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg, err_dev, g.T, g.Bp);
+        pack_x_rows_kernel<1><<<pg, 256, sm, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg, err_dev, g.T, g.Bp, halves);
       else if (g.F == 256)
-        pack_x_rows_kernel<2><<<pg, 256, sm, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg, err_dev, g.T, g.Bp);
+        pack_x_rows_kernel<2><<<pg, 256, sm, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg, err_dev, g.T, g.Bp, halves);
       else {
         static bool attr = false;
         if (!attr) {
           cudaFuncSetAttribute(pack_x_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
           attr = true;
         }
-        pack_x_rows_kernel<4><<<pg, 256, sm, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg, err_dev, g.T, g.Bp);
+        pack_x_rows_kernel<4><<<pg, 256, sm, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg, err_dev, g.T, g.Bp, halves);
       }
     } else
       pack_x_kernel<float><<<pg, 256, 0, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
-                                                 err_dev, ntiles, g.T, g.F, g.Kx, g.Bp);
+                                                 err_dev, ntiles, g.T, g.F, g.Kx, g.Bp, halves);
   }
   a.R = g.R; a.T = g.T; a.F = g.F; a.H = g.H; a.Kx = g.Kx; a.Kh = g.Kh; a.K = g.K; a.U = g.U;
   a.C = g.C; a.Bp = g.Bp; a.ntiles = ntiles;
@@ -1912,8 +2829,7 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   else
     rc = x_f64 ? launch_main<SKB_CELL_RNN_TANH, double>(a, g, st) : launch_main<SKB_CELL_RNN_TANH, float>(a, g, st);
   if (rc) return rc;
-  {
+  if (!a.fill_inkernel)
     rnn_fill_frozen_kernel<<<(g.R + 7) / 8, 256, 0, st>>>(out_dev, a.hT, len_dev, w.pmax, g.R, g.T, g.H, g.Bp);
-  }
   return skb_check_launch();
 }

@@ -84,6 +84,17 @@ SKB_DEV bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
 SKB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {}
 }
+// try_wait with a long suspend-time hint: the waiting warp sleeps until the phase
+// completes instead of re-polling (frees issue slots for the warps doing work).
+SKB_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u) : "memory");
+  } while (!ok);
+}
 SKB_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait_cluster(bar, parity)) {}
 }
@@ -111,6 +122,10 @@ SKB_DEV void bulk_g2s_multicast(void* smem_dst, const void* gmem_src, uint32_t b
                " [%0], [%1], %2, [%3], %4;"
                :: "r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask)
                : "memory");
+}
+// Bulk prefetch of [gmem, gmem + bytes) into L2 (bytes a multiple of 16).
+SKB_DEV void bulk_prefetch_l2(const void* gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(gmem), "r"(bytes) : "memory");
 }
 SKB_DEV void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -200,6 +215,64 @@ SKB_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 SKB_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ---------------------------------------------------------------- CTA pairs (cta_group::2)
+// A pair is two CTAs of a cluster with ranks 2p, 2p+1.  One M=256 MMA issued by the
+// even (leader) CTA computes D[128 x N] in each CTA's TMEM: A rows [128r, 128r+128)
+// come from CTA r's TMEM (same address in both), B columns [r*N/2, (r+1)*N/2) from
+// CTA r's shared memory (same offset in both).  TMEM of a pair is allocated and freed
+// by one warp of the same index in each CTA.
+template <uint32_t NCOLS>
+SKB_DEV void tmem_alloc_pair(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+               :: "r"(smem_u32(dst_smem)), "n"(NCOLS) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t NCOLS>
+SKB_DEV void tmem_dealloc_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(taddr), "n"(NCOLS) : "memory");
+}
+// Warp-collective pair MMA (leader CTA only), A from TMEM.
+SKB_DEV void umma_f16_ts_pair_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                   uint32_t accumulate) {
+  asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 rx;\n\t"
+               "elect.sync rx|e, 0xffffffff;\n\t"
+               "setp.ne.b32 p, %4, 0;\n\t"
+               "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+               :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+// Completion of the leader's previously issued pair MMAs, arriving on the mbarrier at
+// this offset in every CTA of `cta_mask`.
+SKB_DEV void umma_commit_pair_warp(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 rx;\n\t"
+               "elect.sync rx|e, 0xffffffff;\n\t"
+               "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+               :: "r"(smem_u32(bar)), "h"(cta_mask) : "memory");
+}
+// 16 TMEM lanes x 256 bits, .x2 (16 columns): thread i receives lanes base + i/4 and
+// base + 8 + i/4, columns 2(i%4), 2(i%4)+1 and 8 + 2(i%4), 9 + 2(i%4):
+//   v[0] (l, c0)  v[1] (l, c0+1)  v[2] (l+8, c0)  v[3] (l+8, c0+1)
+//   v[4] (l, c0+8) v[5] (l, c0+9) v[6] (l+8, c0+8) v[7] (l+8, c0+9)
+SKB_DEV void tmem_ld_16x256b_x2(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+// .x4: 32 columns; v[4j..4j+3] as .x2's v[0..3] for columns 8j + ...
+SKB_DEV void tmem_ld_16x256b_x4(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+               "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+                 "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
 
 // ---------------------------------------------------------------- descriptors
 // Instruction descriptor, kind::f16, fp16 x fp16 -> fp32, both operands K-major.

@@ -103,6 +103,9 @@ SIGNATURES = {
     "skb_allreduce_f64": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, _VP]),
     "skb_comm_destroy": (ctypes.c_int, [_VP]),
     "skb_diag_umma_gemm": (ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP]),
+    "skb_rnn_last_kernel": (ctypes.c_int, []),
+    "skb_rnn_last_clusters": (ctypes.c_int, []),
+    "skb_diag_umma_pair": (ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP]),
     "skb_diag_cluster_exchange": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP, _VP, _VP]),
 }
 

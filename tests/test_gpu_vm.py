@@ -64,6 +64,6 @@ def test_int64_overflow_is_reported_not_wrapped():
     assert int(ok.outputs[0].item()) == 9_000_000_000_000_000_000
     with pytest.raises(IntegerOverflow):
         execute(g, {"x": np.asarray(4_000_000_000, dtype=np.int64)})
-    g2 = sexpr.from_sexpr("(def main ((x i64)) (sub x 2))")
+    g2 = sexpr.from_sexpr("(def main ((x i64)) (sub x (const i64 2)))")
     with pytest.raises(IntegerOverflow):
         execute(g2, {"x": np.asarray(-(2 ** 63) + 1, dtype=np.int64)})
