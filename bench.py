@@ -54,6 +54,9 @@ KERNELS = {4: "rnn_fwd_pair4_kernel (persistent 8-CTA clusters of 4 CTA pairs, M
            3: "rnn_fwd_dl_kernel (persistent 8-CTA clusters, two 64-row recurrences per CTA, tcgen05 f16)"}
 
 
+KERNEL_KEYS = {4: "rnn_fwd_pair4_kernel", 5: "rnn_fwd_pair_kernel", 3: "rnn_fwd_dl_kernel"}   # ncu_summary.json
+
+
 def peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -268,7 +271,7 @@ def run_skb(args, rank, world, local_rank):
         traffic, traffic_src = None, None
         try:   # dram bytes of one launch from `ncu --set full` of this kernel at this shape (profiles/)
             with open(os.path.join(REPO, "profiles", "ncu_summary.json")) as f:
-                ent = json.load(f).get("rnn_fwd_dl_kernel", {})
+                ent = json.load(f).get(KERNEL_KEYS.get(kernel_id, ""), {})
             if ent.get("problems") == P:
                 traffic = ent.get("dram_bytes_per_launch")
                 traffic_src = f"ncu --set full, {ent.get('capture')}, commit {ent.get('commit')}"

@@ -40,7 +40,9 @@ enum {
   SKB_ERR_DIVISION_BY_ZERO = 13,   /* "DivisionByZero"  tensor.py:235-241     */
   SKB_ERR_ITERATION_LIMIT = 14,    /* "IterationLimitExceeded" execute.py:232 */
   SKB_ERR_ASSERTION_FAILED = 15,   /* "AssertionFailed" execute.py:198-202    */
-  SKB_ERR_FP16_RANGE = 20          /* input outside the fp16 tensor-core range */
+  SKB_ERR_FP16_RANGE = 20,         /* input outside the fp16 tensor-core range */
+  SKB_ERR_HANDOFF = 21             /* internal: a producer/consumer handoff between
+                                      concurrent kernels timed out (never expected) */
 };
 
 /* Cell kinds recognised by the lowering of a staged `While` region. */
@@ -327,6 +329,14 @@ enum {
 };
 int skb_rnn_last_kernel(void);
 int skb_rnn_last_clusters(void);
+/* Concurrency of the last skb_rnn_forward: bit 0 = x images packed, bit 1 = frozen tails
+ * filled by the auxiliary grid on the SMs the pair4 kernel's clusters leave idle, while
+ * the recurrent kernel runs (on a high-priority side stream; joined on the caller's). */
+int skb_rnn_last_overlap(void);
+/* enable = 0: never use the auxiliary grid (pre-pass packer + fill pass), e.g. after a
+ * launch reported SKB_ERR_HANDOFF; 1: as selected by SKB_RNN_XOVL / SKB_RNN_FOVL (both
+ * default 0: measured slower than the sequential passes). */
+int skb_rnn_set_overlap(int enable);
 int64_t skb_rnn_f32_packed_bytes(const skb_rnn_shape* shape);
 int64_t skb_rnn_f32_workspace_bytes(const skb_rnn_shape* shape);
 skb_status skb_rnn_pack_f32(const skb_rnn_shape* shape, const void* const* w_dev, const void* const* u_dev,

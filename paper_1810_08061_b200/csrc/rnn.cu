@@ -124,6 +124,8 @@ struct RnnArgs {
   const uint8_t* ximg; // [ntiles][T][NT x Kx] fp16 core-matrix images of x_t
   uint8_t* hscratch;   // per cluster: 2 x [NT x Kh] fp16 h_t exchange buffers (L2)
   int32_t* err;
+  const int32_t* xflag; // pair4 kernel with the concurrent packer: [ntiles][T] image-ready flags, else null
+  int32_t* tdone;       // pair4 kernel with the concurrent filler: [ntiles] CTAs that published h_T, else null
   int x_f64;
   int fill_inkernel;   // pair4 kernel: write the frozen tails itself (no fill pass)
   int R, T, F, H, Kx, Kh, K, U, C, Bp, ntiles;
@@ -158,6 +160,43 @@ __device__ int g_ttrace_n = 0;
 
 SKB_DEV void set_err(int32_t* err, int code, int problem, int t) {
   if (atomicCAS(err, 0, code) == 0) { err[1] = problem; err[2] = t; }
+}
+
+// Handoff from the concurrent x packer (pack_x_stream_kernel): the packer's image
+// stores, a gpu-scope release of the (tile, t) flag; the loader polls with ld.acquire
+// and orders its bulk (async-proxy) read after them with a proxy fence.  The packer
+// never waits on anything, so the wait always ends; it is still bounded (a lost flag
+// would be a bug: the launch reports SKB_ERR_HANDOFF instead of hanging).
+SKB_DEV int ld_acquire_gpu(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+SKB_DEV void st_release_gpu(int32_t* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+SKB_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+SKB_DEV void red_release_gpu_add(int32_t* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+// Wait for *p >= want.  A timed-out wait marks the launch (err = SKB_ERR_HANDOFF) and
+// every later wait of the launch gives up at once, so a lost producer costs one timeout.
+SKB_DEV bool wait_flag(const int32_t* p, int want, int32_t* err) {
+  if (ld_acquire_gpu(p) >= want) return true;
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_gpu(p) < want) {
+    if (*reinterpret_cast<volatile int32_t*>(err) == SKB_ERR_HANDOFF) return false;
+    __nanosleep(64);
+    if (globaltimer_ns() - t0 > 200000000ull) {
+      atomicExch(err, SKB_ERR_HANDOFF);
+      return false;
+    }
+  }
+  return true;
 }
 
 SKB_DEV float sel4(float a, float b, float c, float d, int i) {
@@ -1446,19 +1485,26 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_pair_kernel(const RnnArgs 
 //   * warps 16-19: lane L's role warp: x_t loader (+ L2 prefetch of x_{t+2}) and, in
 //     the even CTA, the MMA issuer; in the odd CTA the relay of its x_t / h_t phases.
 //   * x_t images are packed per 32-row half ("halves" layout of the pack kernels).
-template <typename XT, int ACT = 1, int CELL = SKB_CELL_LSTM>
-__global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_pair4_kernel(const RnnArgs a) {
+//   * FW = 1 (SKB_RNN_FILLW=1): warp 20 is the fill warp.  At the end of each tile the lane's
+//     epilogue hands the tile's rows (row, length, problem trip count) to it through a
+//     two-slot shared-memory queue; it writes the frozen tails out[r, len <= t < tmax,
+//     CTA slice] = h_T from the final states, off the recurrence's critical path (the
+//     separate rnn_fill_frozen_kernel pass then does not run).
+template <typename XT, int ACT = 1, int CELL = SKB_CELL_LSTM, int FW = 0>
+__global__ void __launch_bounds__((20 + FW) * 32, 1) rnn_fwd_pair4_kernel(const RnnArgs a) {
   constexpr int NL = 4, NT = 64, NH = 32, EWL = 4, kEpiL = EWL * 32;
-  constexpr int kRole0 = 16;
+  constexpr int kRole0 = 16, kFill = 20;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ uint64_t xfull[NL], xempty[NL], hfull[NL][2], mdone[NL], dfree[NL];
+  __shared__ uint64_t fq_full[NL][2], fq_empty[NL][2];   // fill queue (FW)
   __shared__ uint32_t tmem_s;
   __shared__ int2 s_meta[NL][NT];   // (row, clamped length) of the lane's tile rows
   __shared__ int s_trip[NL][3];     // [lane]: tile trip, trip of rows 0-31, trip of rows 32-63
   __shared__ int s_tmax[NL][NT];    // the row's problem trip count (its output rows)
+  __shared__ int4 s_fq[FW ? NL : 1][2][NT];   // fill queue entries (row, length, tmax)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int L = warp < kRole0 ? (warp >> 2) : warp - kRole0;
+  const int L = warp < kRole0 ? (warp >> 2) : (warp < kFill ? warp - kRole0 : 0);
   const uint32_t q = cluster_ctarank(), odd = q & 1u, peer = q ^ 1u;
   const bool leader = odd == 0;
   const int C = a.C, H = a.H, T = a.T;
@@ -1482,11 +1528,17 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_pair4_kernel(const RnnArgs
       mbar_init(&hfull[l][1], leader ? 2 : 1);
       mbar_init(&mdone[l], 1);
       mbar_init(&dfree[l], 2 * EWL);             // epilogue warps of both CTAs (leader's copy is used)
+      if (FW) {
+        mbar_init(&fq_full[l][0], kEpiL);
+        mbar_init(&fq_full[l][1], kEpiL);
+        mbar_init(&fq_empty[l][0], 1);
+        mbar_init(&fq_empty[l][1], 1);
+      }
     }
     fence_mbar_init();
   }
   if (warp == kRole0) tmem_alloc_pair<512>(&tmem_s);
-  for (uint32_t i = tid; i < NL * lane_bytes / 16; i += 20 * 32)
+  for (uint32_t i = tid; i < NL * lane_bytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(smem_raw)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
   tc_fence_before();
@@ -1554,7 +1606,47 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_pair4_kernel(const RnnArgs
     mbar_arrive_expect_tx(&hfull[L][1], C * sbytes);
   }
 
-  for (int round = 0, tile = tile0; tile < a.ntiles || round * stride < a.ntiles; tile = tile_of(++round)) {
+  if (FW && warp == kFill) {
+    // ======================= fill warp: frozen tails of every finished tile of the CTA
+    int cnt[NL], done[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const int pl = NL * (int)cluster_id_x() + l;
+      cnt[l] = 0;
+      done[l] = 0;
+      for (int k = 0; k * stride < a.ntiles; ++k)
+        if (k * stride + ((k & 1) ? stride - 1 - pl : pl) < a.ntiles) ++cnt[l];
+    }
+    const int sub = lane & 7, grp = lane >> 3;
+    for (;;) {
+      bool more = false, any = false;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        if (done[l] >= cnt[l]) continue;
+        more = true;
+        const int slot = done[l] & 1;
+        const uint32_t ph = (done[l] >> 1) & 1;
+        const bool ready = __shfl_sync(0xffffffffu, mbar_try_wait(&fq_full[l][slot], ph) ? 1 : 0, 0) != 0;
+        if (!ready) continue;
+        mbar_wait(&fq_full[l][slot], ph);   // complete: acquire for every lane
+        for (int i = grp; i < NT; i += 4) {
+          const int4 m = s_fq[FW ? l : 0][slot][i];
+          if (m.x >= 0 && m.z > m.y) {
+            const float4 v = *(reinterpret_cast<const float4*>(a.hT + (size_t)m.x * H + (int)q * 32) + sub);
+            float4* o = reinterpret_cast<float4*>(a.out + (size_t)m.x * T * H + (int)q * 32) + sub;
+            for (int t = m.y; t < m.z; ++t) __stcs(o + (size_t)t * (H / 4), v);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fq_empty[l][slot]);
+        ++done[l];
+        any = true;
+      }
+      if (!more) break;
+      if (!any) __nanosleep(256);
+    }
+  } else
+  for (int round = 0, tile = tile0, ntl = 0; tile < a.ntiles || round * stride < a.ntiles; tile = tile_of(++round)) {
     if (tile >= a.ntiles) continue;   // a partial last round
     named_bar_sync(tile_bar, kLaneThreads);   // this lane's previous tile retired (s_meta rewritten)
     if (warp < kRole0 && e < NT) { s_meta[L][e] = m_meta; s_tmax[L][e] = m_tmax; }
@@ -1688,6 +1780,17 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_pair4_kernel(const RnnArgs
           if (a.cT) a.cT[(size_t)r * H + unit] = cc[ci];
         }
       }
+      if (a.tdone) {   // concurrent filler: this CTA's h_T slice of the tile is published
+        __threadfence();
+        named_bar_sync(xch_bar, kEpiL);
+        if (e == 0) red_release_gpu_add(a.tdone + tile, 1);
+      }
+      if constexpr (FW != 0) {   // hand the tile's rows and final states to the fill warp
+        const int slot = ntl & 1;
+        mbar_wait_sleep(&fq_empty[L][slot], ((ntl >> 1) & 1) ^ 1);
+        if (e < NT) s_fq[L][slot][e] = make_int4(s_meta[L][e].x, s_meta[L][e].y, s_tmax[L][e], 0);
+        mbar_arrive(&fq_full[L][slot]);   // release: the h_T stores and the entries
+      }
     } else {
       // ======================= role warp (lane L): x_t image loads (pre-pass images), MMA
       // issuer (even CTA) / relay (odd CTA)
@@ -1697,6 +1800,10 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_pair4_kernel(const RnnArgs
         mbar_wait_sleep(&xempty[L], (u & 1) ^ 1);
         if (lane == 0) {
           if (t < tself) {
+            if (a.xflag) {   // concurrent packer: image (tile, t) published?
+              wait_flag(a.xflag + (size_t)tile * T + t, 1, a.err);
+              fence_proxy_async_global();
+            }
             mbar_arrive_expect_tx(&xfull[L], xbytes);
             bulk_g2s(sX, img + (size_t)t * 2 * xbytes, xbytes, &xfull[L]);
             // the image two steps ahead -> L2 (an HBM miss here delays x-part(t+1) and with it
@@ -1769,6 +1876,7 @@ __global__ void __launch_bounds__(20 * 32, 1) rnn_fwd_pair4_kernel(const RnnArgs
     }
     __syncwarp();
     step += trip;
+    ++ntl;
   }
 
   // Drain the asynchronous arrivals aimed at this CTA before it exits: the last
@@ -2125,7 +2233,9 @@ struct SchedArgs {
   int32_t* cursor;    // [T+1]
   int32_t* max_len_out;
   int32_t* err;
-  int R, Bp, P, T, npad;
+  int32_t* xflag;     // [nflags] concurrent-packer image flags, cleared here
+  int32_t* tdone;     // [ntdone] concurrent-filler tile counters, cleared here
+  int R, Bp, P, T, npad, nflags, ntdone;
 };
 
 __global__ void sched_init(const SchedArgs a) {
@@ -2134,6 +2244,8 @@ __global__ void sched_init(const SchedArgs a) {
   for (int p = i; p < a.P; p += stride) a.pmax[p] = INT_MIN;
   for (int b = i; b <= a.T; b += stride) { a.hist[b] = 0; a.cursor[b] = 0; }
   for (int r = a.R + i; r < a.npad; r += stride) a.perm[r] = -1;
+  for (int f = i; f < a.nflags; f += stride) a.xflag[f] = 0;
+  for (int f = i; f < a.ntdone; f += stride) a.tdone[f] = 0;
 }
 
 SKB_DEV int len_bin(long long L, int T) { return (int)max(0LL, min(L, (long long)T)); }
@@ -2262,18 +2374,18 @@ __global__ void __launch_bounds__(256) pack_x_kernel(const XT* __restrict__ x, c
 // coalesced), converts to fp16 into a padded row-major shared tile, then all
 // threads write the image in core-matrix order ([Kx/8][64 rows][8] halves) as
 // contiguous 16-byte stores.  Rows past their length are written as zeros.
+// One (tile, t) image; false (nothing written) when t is past the tile's trip count.
 template <int NQ>
-__global__ void __launch_bounds__(256) pack_x_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
-                                   const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
-                                   uint8_t* __restrict__ img, int32_t* err, int T, int Bp, int halves) {
+SKB_DEV bool pack_rows_item(const float* __restrict__ x, const int32_t* __restrict__ perm,
+                            const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
+                            uint8_t* __restrict__ img, int32_t* err, int T, int Bp, int halves, int tile, int t,
+                            uint8_t* srow) {
   constexpr int F = NQ * 128, kRow = F * 2 + 16;   // padded fp16 row: 16-byte reads of 8 lanes hit distinct banks
-  extern __shared__ __align__(16) uint8_t srow[];
-  const int tile = blockIdx.x, t = blockIdx.y;
   const int r0 = perm[tile * kNT];
-  if (r0 < 0) return;
+  if (r0 < 0) return false;
   const int tm0 = min(max(pmax[r0 / Bp], 0), T);
   const long long L0 = lens[r0];
-  if (t >= (L0 < tm0 ? L0 : tm0)) return;
+  if (t >= (L0 < tm0 ? L0 : tm0)) return false;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   bool bad = false;
   float4 v[8][NQ];
@@ -2309,10 +2421,92 @@ __global__ void __launch_bounds__(256) pack_x_rows_kernel(const float* __restric
         *reinterpret_cast<const uint4*>(srow + n * kRow + kc * 16);
   }
   if (bad) set_err(err, SKB_ERR_FP16_RANGE, -1, -1);
+  return true;
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(256) pack_x_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
+                                   const int64_t* __restrict__ lens, const int32_t* __restrict__ pmax,
+                                   uint8_t* __restrict__ img, int32_t* err, int T, int Bp, int halves) {
+  extern __shared__ __align__(16) uint8_t srow[];
+  pack_rows_item<NQ>(x, perm, lens, pmax, img, err, T, Bp, halves, blockIdx.x, blockIdx.y, srow);
+}
+
+// Concurrent auxiliary grid of the pair4 kernel (default for fp32 x rows): a small
+// persistent grid on the SMs the recurrent kernel's 8-CTA clusters leave idle.
+//  1. packer: the x images, in the order the lanes consume them (round k of the
+//     snake-order tile assignment, then t, then lane position); each (tile, t) image
+//     is published with a gpu-scope release of its flag.  Never waits.
+//  2. filler: the frozen tails out[r, len <= t < tmax, :] = h_T of each tile, as soon as
+//     all C CTAs of the tile's cluster have published their h_T slices (tdone).
+// Both flag arrays are cleared by sched_init.  Launched after the recurrent kernel on a
+// lower-priority stream, preloaded (no lazy-loading stall while the recurrence waits).
+struct AuxArgs {
+  const float* x;
+  const int32_t* perm;
+  const int64_t* lens;
+  const int32_t* pmax;
+  uint8_t* img;
+  int32_t* err;
+  int32_t* xflag;        // null: no packing phase
+  const int32_t* tdone;  // null: no filling phase
+  float* out;
+  const float* hT;
+  int ntiles, T, H, Bp, stride, C;
+};
+
+template <int NQ>
+__global__ void __launch_bounds__(256) rnn_aux_kernel(const AuxArgs a) {
+  extern __shared__ __align__(16) uint8_t srow[];
+  __shared__ int s_ok;
+  const int rounds = (a.ntiles + a.stride - 1) / a.stride;
+  if (a.xflag) {
+    const long long items = (long long)rounds * a.T * a.stride;
+    for (long long i = blockIdx.x; i < items; i += gridDim.x) {
+      const int pos = (int)(i % a.stride);
+      const long long kt = i / a.stride;
+      const int t = (int)(kt % a.T), k = (int)(kt / a.T);
+      const int tile = k * a.stride + ((k & 1) ? a.stride - 1 - pos : pos);
+      if (tile >= a.ntiles) continue;
+      if (!pack_rows_item<NQ>(a.x, a.perm, a.lens, a.pmax, a.img, a.err, a.T, a.Bp, 1, tile, t, srow)) continue;
+      fence_proxy_async_global();   // the image is read by the consumer's bulk copies
+      __syncthreads();              // every thread's image stores (and srow reads) are done
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_gpu(a.xflag + (size_t)tile * a.T + t, 1);
+      }
+    }
+  }
+  if (a.tdone) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, H4 = a.H / 4;
+    for (int j = blockIdx.x; j < rounds * a.stride; j += gridDim.x) {
+      const int k = j / a.stride, pos = j % a.stride;
+      const int tile = k * a.stride + ((k & 1) ? a.stride - 1 - pos : pos);
+      if (tile >= a.ntiles) continue;
+      __syncthreads();
+      if (threadIdx.x == 0) s_ok = wait_flag(a.tdone + tile, a.C, a.err) ? 1 : 0;
+      __syncthreads();
+      if (!s_ok) return;
+      for (int n = warp; n < kNT; n += 8) {
+        const int r = a.perm[tile * kNT + n];
+        if (r < 0) continue;
+        const int tmax = min(max(a.pmax[r / a.Bp], 0), a.T);
+        const long long L = a.lens[r];
+        const int len = (int)(L < 0 ? 0 : (L < tmax ? L : tmax));
+        if (len >= tmax) continue;
+        float4* orow = reinterpret_cast<float4*>(a.out + (size_t)r * a.T * a.H);
+        const float4* hrow = reinterpret_cast<const float4*>(a.hT + (size_t)r * a.H);
+        for (int c = lane; c < H4; c += 32) {
+          const float4 v = __ldcg(hrow + c);
+          for (int t = len; t < tmax; ++t) __stcs(orow + (size_t)t * H4 + c, v);
+        }
+      }
+    }
+  }
 }
 
 struct Workspace {
-  int32_t *perm, *pmax, *hist, *base, *cursor;
+  int32_t *perm, *pmax, *hist, *base, *cursor, *xflag, *tdone;
   uint8_t* hscratch;
   uint8_t* ximg;
   float* hT;
@@ -2338,7 +2532,11 @@ inline int64_t ws_layout(const RnnGeom& g, uint8_t* basep, Workspace* w) {
   int64_t o_hs = take((int64_t)max_clusters_bound(g) * 4 * 2 * kNT * g.Kh * 2 / 4);
   int64_t o_x = take((int64_t)ntiles * g.T * kNT * g.Kx * 2 / 4);
   int64_t o_hT = take((int64_t)g.R * g.H);
+  int64_t o_fl = take((int64_t)ntiles * g.T);
+  int64_t o_td = take((int64_t)ntiles);
   if (w) {
+    w->xflag = reinterpret_cast<int32_t*>(basep + o_fl);
+    w->tdone = reinterpret_cast<int32_t*>(basep + o_td);
     w->perm = reinterpret_cast<int32_t*>(basep + o_perm);
     w->pmax = reinterpret_cast<int32_t*>(basep + o_pmax);
     w->hist = reinterpret_cast<int32_t*>(basep + o_hist);
@@ -2560,11 +2758,27 @@ int launch_pair(RnnArgs args, const RnnGeom& g, cudaStream_t stream) {
   if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n++ + 1], stream);
   return skb_check_launch();
 }
-template <typename XT, int ACT, int CELL = SKB_CELL_LSTM>
-int launch_pair4(RnnArgs args, const RnnGeom& g, cudaStream_t stream) {
-  auto kern = rnn_fwd_pair4_kernel<XT, ACT, CELL>;
+// SKB_RNN_FILLW=1: the pair4 kernel's fill warp writes the frozen tails (measured slower:
+// the 21st warp caps the kernel at 80 registers).
+inline bool rnn_fill_warp() {
+  static int v = -1;
+  if (v < 0) v = env_flag("SKB_RNN_FILLW", 0) ? 1 : 0;
+  return v == 1;
+}
+// SKB_RNN_XOVL=1: the pair4 kernel's x images are packed concurrently on the
+// idle SMs (pack_x_stream_kernel) instead of by a pre-pass.
+int g_overlap_off = 0;   // skb_rnn_set_overlap(0): no auxiliary grid (e.g. after a handoff timeout)
+inline bool rnn_x_overlap() {
+  static int v = -1;
+  if (v < 0) v = env_flag("SKB_RNN_XOVL", 0) ? 1 : 0;
+  return v == 1 && !g_overlap_off;
+}
+
+template <typename XT, int ACT, int CELL, int FW>
+int launch_pair4_fw(RnnArgs args, const RnnGeom& g, cudaStream_t stream) {
+  auto kern = rnn_fwd_pair4_kernel<XT, ACT, CELL, FW>;
   g_last_kernel = SKB_RNN_KERNEL_PAIR;
-  constexpr int kThreads = 20 * 32;
+  constexpr int kThreads = (20 + FW) * 32;
   const size_t smem = pair4_smem(g);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SKB_ERR_CUDA;
@@ -2591,6 +2805,11 @@ int launch_pair4(RnnArgs args, const RnnGeom& g, cudaStream_t stream) {
   if (cudaLaunchKernelEx(&cfg, kern, args) != cudaSuccess) return SKB_ERR_CUDA;
   if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n++ + 1], stream);
   return skb_check_launch();
+}
+template <typename XT, int ACT, int CELL = SKB_CELL_LSTM>
+int launch_pair4(RnnArgs args, const RnnGeom& g, cudaStream_t stream) {
+  return args.fill_inkernel || !rnn_fill_warp() ? launch_pair4_fw<XT, ACT, CELL, 0>(args, g, stream)
+                                                : launch_pair4_fw<XT, ACT, CELL, 1>(args, g, stream);
 }
 
 
@@ -2644,9 +2863,93 @@ int launch_main(const RnnArgs& args, const RnnGeom& g, cudaStream_t stream) {
   return rnn_ew() == 8 ? launch_main_ew<CELL, XT, 8>(args, g, stream) : launch_main_ew<CELL, XT, 16>(args, g, stream);
 }
 
+// SKB_RNN_FOVL=1: the pair4 kernel's frozen tails are written concurrently by
+// the auxiliary grid on the idle SMs instead of by a pass after the kernel.
+inline bool rnn_fill_overlap() {
+  static int v = -1;
+  if (v < 0) v = env_flag("SKB_RNN_FOVL", 0) ? 1 : 0;
+  return v == 1 && !g_overlap_off;
+}
+
+// Force-load the auxiliary kernel before the recurrent kernel is queued: with CUDA's lazy
+// module loading, loading a function while a kernel that waits on it is running stalls
+// until that kernel ends (here: until its handoff waits time out).
+int preload_aux(int nq, size_t smem) {
+  static bool done[5] = {false, false, false, false, false};
+  if (nq < 1 || nq > 4) return SKB_ERR_INVALID;
+  if (!done[nq]) {
+    cudaFuncAttributes fa;
+    const void* f = nq == 1 ? (const void*)rnn_aux_kernel<1> : nq == 2 ? (const void*)rnn_aux_kernel<2>
+                                                                      : (const void*)rnn_aux_kernel<4>;
+    if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return SKB_ERR_CUDA;
+    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * (512 * 2 + 16)) != cudaSuccess)
+      return SKB_ERR_CUDA;
+    done[nq] = true;
+  }
+  (void)smem;
+  return SKB_OK;
+}
+
+// Clusters the pair4 kernel launches with for `ntiles` tiles (as launch_pair4_fw computes it).
+template <int FW>
+int pair4_clusters(const RnnGeom& g, int ntiles) {
+  auto kern = rnn_fwd_pair4_kernel<float, 1, SKB_CELL_LSTM, FW>;
+  const size_t smem = pair4_smem(g);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3((20 + FW) * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(g.C);
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) return 0;
+  return max(1, min(min(max_clusters, (ntiles + 3) / 4), max_clusters_bound(g) - 1));
+}
+
+// Side streams of the concurrent-packer launch: the recurrent kernel on the
+// highest-priority stream (its clusters are placed before the packer's CTAs), the
+// packer on a lowest-priority one; fork/join through events on the caller's stream.
+struct OverlapStreams {
+  cudaStream_t hi = nullptr, pack = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_hi = nullptr, ev_pack = nullptr;
+  bool ok = false;
+};
+OverlapStreams g_ovl[16];
+
+OverlapStreams* overlap_streams() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  OverlapStreams& o = g_ovl[dev];
+  if (!o.ok) {
+    int least = 0, greatest = 0;
+    if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return nullptr;
+    if (cudaStreamCreateWithPriority(&o.hi, cudaStreamNonBlocking, greatest) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&o.pack, cudaStreamNonBlocking, least) != cudaSuccess ||
+        cudaEventCreateWithFlags(&o.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&o.ev_hi, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&o.ev_pack, cudaEventDisableTiming) != cudaSuccess)
+      return nullptr;
+    o.ok = true;
+  }
+  return &o;
+}
+
+int g_last_overlap = 0;
+
 }  // namespace
 
 extern "C" int skb_rnn_last_kernel(void) { return g_last_kernel; }
+extern "C" int skb_rnn_last_overlap(void) { return g_last_overlap; }
+extern "C" int skb_rnn_set_overlap(int enable) {
+  g_overlap_off = enable ? 0 : 1;
+  return SKB_OK;
+}
 extern "C" int skb_rnn_last_clusters(void) { return g_last_clusters; }
 
 extern "C" int skb_profile_begin(int max_launches) {
@@ -2773,8 +3076,31 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   Workspace w;
   ws_layout(g, reinterpret_cast<uint8_t*>(workspace_dev), &w);
   const int ntiles = n_tiles64(g);
-  SchedArgs sa = {len_dev, w.perm, w.pmax, w.hist, w.base, w.cursor, max_len_dev, err_dev,
-                  g.R, g.Bp, g.P, g.T, ntiles * kNT};
+  // The four-lane pair kernel reads 32-row half images, packed by a pre-pass; its frozen
+  // tails are filled by a pass after it.  Measured alternatives (each slower on the B200,
+  // profiles/r02_c1_overlap.md): SKB_RNN_XOVL=1 / SKB_RNN_FOVL=1 pack / fill concurrently
+  // on the idle SMs (the auxiliary grid); SKB_RNN_FILLW=1 fill warp in the kernel;
+  // SKB_RNN_INFILL=1 fill from the epilogue.
+  const bool pair4 = kernel_choice(g, c0_dev != nullptr) == SKB_RNN_KERNEL_PAIR;
+  const bool infill = pair4 && env_flag("SKB_RNN_INFILL", 0);
+  const bool fillw = pair4 && !infill && rnn_fill_warp();
+  const bool rows_ok = !x_f64 && g.F == g.Kx && (reinterpret_cast<uintptr_t>(x_dev) & 15) == 0 &&
+                       (g.F == 128 || g.F == 256 || g.F == 512) && !getenv("SKB_PACK_X_LEGACY");
+  bool xovl = pair4 && rows_ok && rnn_x_overlap();
+  bool fovl = pair4 && !infill && !fillw && rnn_fill_overlap();
+  OverlapStreams* ovs = nullptr;
+  int idle = 0;
+  if (xovl || fovl) {   // only with enough idle SMs for the auxiliary grid (the kernel waits on it)
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ncl = fillw ? pair4_clusters<1>(g, ntiles) : pair4_clusters<0>(g, ntiles);
+    idle = sms - ncl * g.C;
+    if (ncl > 0 && idle >= 16) ovs = overlap_streams();
+  }
+  if (!ovs) xovl = fovl = false;
+  g_last_overlap = (xovl ? 1 : 0) | (fovl ? 2 : 0);
+  SchedArgs sa = {len_dev, w.perm, w.pmax, w.hist, w.base, w.cursor, max_len_dev, err_dev, w.xflag, w.tdone,
+                  g.R, g.Bp, g.P, g.T, ntiles * kNT, xovl ? ntiles * g.T : 0, fovl ? ntiles : 0};
   const int blocks = min(1184, max(1, (max(g.R, g.P) + 255) / 256));
   sched_init<<<blocks, 256, 0, st>>>(sa);
   sched_hist<<<blocks, 256, 0, st>>>(sa);
@@ -2789,15 +3115,12 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
   a.out = out_dev; a.hT = hT_dev ? hT_dev : w.hT; a.cT = cT_dev; a.err = err_dev; a.x_f64 = x_f64;
   a.hscratch = w.hscratch;
   a.ximg = w.ximg;
-  // the four-lane pair kernel reads 32-row half images; it can write the frozen tails
-  // itself (SKB_RNN_INFILL=1)
-  const bool pair4 = kernel_choice(g, c0_dev != nullptr) == SKB_RNN_KERNEL_PAIR;
-  a.fill_inkernel = pair4 && env_flag("SKB_RNN_INFILL", 0);
-  {
+  a.fill_inkernel = infill ? 1 : 0;
+  a.R = g.R; a.T = g.T; a.F = g.F; a.H = g.H; a.Kx = g.Kx; a.Kh = g.Kh; a.K = g.K; a.U = g.U;
+  a.C = g.C; a.Bp = g.Bp; a.ntiles = ntiles;
+  if (!xovl) {   // pre-pass packer
     const dim3 pg(ntiles, g.T);
     const int halves = pair4 ? 1 : 0;
-    const bool rows_ok = !x_f64 && g.F == g.Kx && (reinterpret_cast<uintptr_t>(x_dev) & 15) == 0 &&
-                         (g.F == 128 || g.F == 256 || g.F == 512) && !getenv("SKB_PACK_X_LEGACY");
     if (x_f64)
       pack_x_kernel<double><<<pg, 256, 0, st>>>((const double*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
                                                   err_dev, ntiles, g.T, g.F, g.Kx, g.Bp, halves);
@@ -2818,18 +3141,45 @@ extern "C" int skb_rnn_forward(const skb_rnn_shape* shape, const void* packed_de
     } else
       pack_x_kernel<float><<<pg, 256, 0, st>>>((const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg,
                                                  err_dev, ntiles, g.T, g.F, g.Kx, g.Bp, halves);
+    if (int e = skb_check_launch()) return e;
   }
-  a.R = g.R; a.T = g.T; a.F = g.F; a.H = g.H; a.Kx = g.Kx; a.Kh = g.Kh; a.K = g.K; a.U = g.U;
-  a.C = g.C; a.Bp = g.Bp; a.ntiles = ntiles;
-  int rc;
-  if (g.cell == SKB_CELL_LSTM)
-    rc = x_f64 ? launch_main<SKB_CELL_LSTM, double>(a, g, st) : launch_main<SKB_CELL_LSTM, float>(a, g, st);
-  else if (g.cell == SKB_CELL_GRU)
-    rc = x_f64 ? launch_main<SKB_CELL_GRU, double>(a, g, st) : launch_main<SKB_CELL_GRU, float>(a, g, st);
-  else
-    rc = x_f64 ? launch_main<SKB_CELL_RNN_TANH, double>(a, g, st) : launch_main<SKB_CELL_RNN_TANH, float>(a, g, st);
-  if (rc) return rc;
-  if (!a.fill_inkernel)
+  auto launch_rec = [&](cudaStream_t rs) {
+    if (g.cell == SKB_CELL_LSTM)
+      return x_f64 ? launch_main<SKB_CELL_LSTM, double>(a, g, rs) : launch_main<SKB_CELL_LSTM, float>(a, g, rs);
+    if (g.cell == SKB_CELL_GRU)
+      return x_f64 ? launch_main<SKB_CELL_GRU, double>(a, g, rs) : launch_main<SKB_CELL_GRU, float>(a, g, rs);
+    return x_f64 ? launch_main<SKB_CELL_RNN_TANH, double>(a, g, rs) : launch_main<SKB_CELL_RNN_TANH, float>(a, g, rs);
+  };
+  if (ovs) {
+    // fork: the recurrent kernel (high priority, placed first) and the auxiliary grid
+    // (low priority, on the idle SMs); join on the caller's stream
+    const int nq = xovl ? g.F / 128 : 1;
+    const size_t sm = xovl ? (size_t)kNT * (g.F * 2 + 16) : 0;
+    if (int e = preload_aux(nq, sm)) return e;
+    a.xflag = xovl ? w.xflag : nullptr;
+    a.tdone = fovl ? w.tdone : nullptr;
+    cudaEventRecord(ovs->ev_fork, st);
+    cudaStreamWaitEvent(ovs->hi, ovs->ev_fork, 0);
+    cudaStreamWaitEvent(ovs->pack, ovs->ev_fork, 0);
+    int rc = launch_rec(ovs->hi);
+    if (rc == SKB_OK) {
+      AuxArgs x = {(const float*)x_dev, w.perm, len_dev, w.pmax, w.ximg, err_dev, xovl ? w.xflag : nullptr, a.tdone, out_dev, a.hT,
+                   ntiles, g.T, g.H, g.Bp, 4 * g_last_clusters, g.C};
+      const int grid = 2 * idle;
+      if (nq == 1) rnn_aux_kernel<1><<<grid, 256, sm, ovs->pack>>>(x);
+      else if (nq == 2) rnn_aux_kernel<2><<<grid, 256, sm, ovs->pack>>>(x);
+      else rnn_aux_kernel<4><<<grid, 256, sm, ovs->pack>>>(x);
+      rc = skb_check_launch();
+    }
+    cudaEventRecord(ovs->ev_hi, ovs->hi);
+    cudaEventRecord(ovs->ev_pack, ovs->pack);
+    cudaStreamWaitEvent(st, ovs->ev_hi, 0);
+    cudaStreamWaitEvent(st, ovs->ev_pack, 0);
+    if (rc) return rc;
+  } else if (int rc = launch_rec(st)) {
+    return rc;
+  }
+  if (!fillw && !infill && !fovl)
     rnn_fill_frozen_kernel<<<(g.R + 7) / 8, 256, 0, st>>>(out_dev, a.hT, len_dev, w.pmax, g.R, g.T, g.H, g.Bp);
   return skb_check_launch();
 }

@@ -79,6 +79,7 @@ STATUS_TO_CAUSE = {
     15: ASSERTION_FAILED,
 }
 SKB_ERR_FP16_RANGE = 20
+SKB_ERR_HANDOFF = 21   # internal: a concurrent-kernel handoff timed out (never expected)
 
 
 class IntegerOverflow(SkbError):

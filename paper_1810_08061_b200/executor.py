@@ -618,6 +618,12 @@ def _execute_many(graph, feeds_list, check, stream, return_exceptions, host_outp
     if T > 0:
         exe.run(x, h0, c0, lens, out, hT, cT, stream=stream)
         status = exe.err.to("cpu")
+        if int(status[0]) == E.SKB_ERR_HANDOFF:
+            # the concurrent auxiliary grid did not get SMs next to the recurrent kernel:
+            # stop using it in this process and run the launch sequence instead
+            exe.lib.skb_rnn_set_overlap(0)
+            exe.run(x, h0, c0, lens, out, hT, cT, stream=stream)
+            status = exe.err.to("cpu")
         max_len = exe.max_len.to("cpu").numpy()
     else:
         status = torch.zeros(4, dtype=torch.int32)
@@ -781,6 +787,8 @@ TIER_PRECISION = {"f16": "fp16 tensor-core operands, fp32 accumulate/state (boun
 def _assemble(prog, out, hT, cT, max_len, status, Bsz, T, P, return_exceptions, tier="f16"):
     if status is not None and int(status[0]) == E.SKB_ERR_FP16_RANGE:
         raise PrecisionRangeError("an input exceeds the fp16 range (|x| > 65504) of the tensor-core path")
+    if status is not None and int(status[0]) == E.SKB_ERR_HANDOFF:
+        raise E.DeviceError("recurrent kernel: the x-image handoff from the concurrent packer timed out")
     results = []
     for p in range(P):
         m = int(max_len[p])

@@ -160,7 +160,8 @@ def test_pipelined_host_to_host_matches_device_path(c1_graph):
         assert np.array_equal(a.outputs[0].array, b.outputs[0].array)
 
 
-@pytest.mark.parametrize("variant", ["SKB_RNN_EW=8", "SKB_RNN_PP=1", "SKB_RNN_DL=0", "SKB_RNN_ACT=0"])
+@pytest.mark.parametrize("variant", ["SKB_RNN_EW=8", "SKB_RNN_PP=1", "SKB_RNN_DL=0", "SKB_RNN_ACT=0",
+                                     "SKB_RNN_FILLW=1", "SKB_RNN_XOVL=1", "SKB_RNN_FOVL=1", "SKB_RNN_INFILL=1"])
 def test_kernel_variants_bit_identical_to_default(c1_graph, variant):
     """The alternative C1 kernel layouts (8-warp epilogue; ping-pong halves)
     produce results identical to the default kernel (same arithmetic per
@@ -174,7 +175,8 @@ def test_kernel_variants_bit_identical_to_default(c1_graph, variant):
             "from oracle.fixtures import load_graph_fixture;"
             "from paper_1810_08061_b200 import execute_many;"
             "g, _ = load_graph_fixture('graph_lstm_c1');"
-            "r = execute_many(g, _c1_problems(6, seed=9));"
+            "r = execute_many(g, [dict(f, input_data=f['input_data'].astype(np.float32)) "
+            "                     for f in _c1_problems(6, seed=9)]);"
             "np.save(sys.argv[1], np.concatenate([x.outputs[0].array.reshape(-1) for x in r]))")
     import os
     import tempfile
