@@ -362,6 +362,22 @@ skb_status skb_diag_cluster_exchange(int cluster, int slice_bytes, int rounds,
                                      long long* cycles_dev, int* errors_dev, void* gscratch_dev,
                                      void* stream);
 
+
+/* ---------------------------------------------------------------------------
+ * skb's own tcgen05 GEMM engine (csrc/gemm.cuh): C[M,N] (+)= op(A) op(B), fp32 out.
+ *   elem 0: bf16 operands (kind::f16), 1: fp32 operands on tf32 tensor cores (K-major
+ *   operands only: a_mn = b_mn = 0, else SKB_ERR_UNSUPPORTED)
+ *   A: [M,K] row-major (a_mn = 0) or [K,M] row-major (a_mn = 1), leading dim lda
+ *   B: [N,K] row-major (b_mn = 0) or [K,N] row-major (b_mn = 1), leading dim ldb
+ *   beta 0/1 (accumulate into C), bn tile width 64/128/256 (0 = auto),
+ *   ksplit > 1: deterministic split-K through workspace (skb_gemm_workspace_bytes).
+ * Operand rows must be 16-byte aligned; N % 16 == 0.  Replaces the cuBLAS calls the
+ * reference-free configs used in round 1 (C2 training GEMMs). */
+int64_t skb_gemm_workspace_bytes(int M, int N, int ksplit);
+skb_status skb_gemm(int elem, int a_mn, int b_mn, int M, int N, int K, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, float* C, int64_t ldc, int beta, int bn, int ksplit,
+                    void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -430,8 +430,24 @@ int g_train_mode = 0;
 
 }  // namespace
 
+extern "C" int64_t skb_train_tc_workspace_bytes(const skb_train_shape* d);
+extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, const float* y, const int64_t* lens,
+                                    const float* h0, const float* c0, const float* params, float* grads, float* loss,
+                                    int n, void* workspace, void* stream);
+
+namespace {
+// math == 2 (bf16): the tensor-core path of train_tc.cu (skb's own tcgen05 GEMMs with the
+// cell fused into their epilogues); SKB_TRAIN_CUBLAS=1 keeps the round-1 cuBLAS bf16 path.
+bool use_tc(const skb_train_shape* d) {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("SKB_TRAIN_CUBLAS"); v = (e && atoi(e) == 1) ? 0 : 1; }
+  return v == 1 && d->math == 2 && d->input % 8 == 0 && d->hidden % 32 == 0;
+}
+}  // namespace
+
 extern "C" int64_t skb_train_workspace_bytes(const skb_train_shape* d) {
   if (!d) return -1;
+  if (use_tc(d)) return skb_train_tc_workspace_bytes(d);
   size_t total = 0;
   layout(d->rows, d->time, d->input, d->hidden, d->math == 2, nullptr, nullptr, &total);
   return (int64_t)total;
@@ -445,10 +461,23 @@ extern "C" skb_status skb_lstm_train_step(const skb_train_shape* d, const float*
   if (!d || d->rows < 1 || d->time < 1 || d->input < 1 || d->hidden < 1 || max_len < 0 || max_len > d->time)
     return SKB_ERR_INVALID;
   cudaStream_t cs = (cudaStream_t)stream;
+  const bool tc = use_tc(d);
   TrainBufs w;
   layout(d->rows, d->time, d->input, d->hidden, d->math == 2, (uint8_t*)workspace, &w, nullptr);
-  cublasHandle_t hb = skb::blas_handle(cs);
-  if (!hb) return SKB_ERR_CUDA;
+  cublasHandle_t hb = tc ? nullptr : skb::blas_handle(cs);
+  if (!tc && !hb) return SKB_ERR_CUDA;
+  auto enq = [&](cudaStream_t s) -> bool {
+    if (tc) {
+      if (max_len == 0) {   // no step: zero loss and gradients
+        cudaMemsetAsync(loss, 0, sizeof(float), s);
+        cudaMemsetAsync(grads, 0, sizeof(float) * ((size_t)d->input * 4 * d->hidden + (size_t)d->hidden * 4 * d->hidden +
+                                                  4 * (size_t)d->hidden), s);
+        return cudaPeekAtLastError() == cudaSuccess;
+      }
+      return skb_train_tc_enqueue(d, x, y, lens, h0, c0, params, grads, loss, max_len, workspace, s) == SKB_OK;
+    }
+    return enqueue(hb, s, *d, w, x, y, lens, h0, c0, params, grads, loss, max_len);
+  };
   const void* key[9] = {x, y, lens, h0, c0, params, grads, loss, workspace};
   cudaGraphExec_t exec = nullptr;
   for (int i = 0; i < g_ntg; ++i)
@@ -460,14 +489,14 @@ extern "C" skb_status skb_lstm_train_step(const skb_train_shape* d, const float*
     bool ok = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed) == cudaSuccess;
     if (ok) {
-      cublasSetStream(hb, cap);
-      const bool enq = enqueue(hb, cap, *d, w, x, y, lens, h0, c0, params, grads, loss, max_len);
-      ok = cudaStreamEndCapture(cap, &g) == cudaSuccess && enq;
+      if (hb) cublasSetStream(hb, cap);
+      const bool e = enq(cap);
+      ok = cudaStreamEndCapture(cap, &g) == cudaSuccess && e;
     }
     if (ok) ok = cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
     if (g) cudaGraphDestroy(g);
     if (cap) cudaStreamDestroy(cap);
-    cublasSetStream(hb, cs);
+    if (hb) cublasSetStream(hb, cs);
     cudaGetLastError();
     if (!ok) exec = nullptr;
     if (exec) {
@@ -486,7 +515,7 @@ extern "C" skb_status skb_lstm_train_step(const skb_train_shape* d, const float*
   g_train_mode = exec ? 1 : 0;
   if (exec) {
     if (cudaGraphLaunch(exec, cs) != cudaSuccess) return SKB_ERR_CUDA;
-  } else if (!enqueue(hb, cs, *d, w, x, y, lens, h0, c0, params, grads, loss, max_len)) {
+  } else if (!enq(cs)) {
     return SKB_ERR_CUDA;
   }
   return skb_check_launch();

@@ -1,0 +1,452 @@
+// train_tc.cu — the C2 training step (dynamic-length LSTM, BPTT) on skb's own tcgen05
+// GEMM engine (gemm.cuh): bf16 operands, fp32 accumulation in TMEM, the LSTM cell
+// fused into the GEMM epilogues.  No cuBLAS.  Replaces the staged BPTT program
+// oracle/programs/lstm_bptt.msl (the reference cannot differentiate a While,
+// graph/grad.py:159-161); same arithmetic as the fp32 path of train.cu.
+//
+// Layouts (per GPU shard of B rows; time-major, so a step's rows are one contiguous block):
+//   XH  [T, B, KX] bf16, KX = F + 16 + H: row (t, b) = [x_t | 1 | 0 x 15 | h_{t-1}].
+//       The ones column folds the bias into the gate GEMM and makes the bias gradient a
+//       row of the weight-gradient GEMM; h_{t-1} is written by the epilogue of step t-1.
+//   WU  [4H, KX] bf16, gate-interleaved rows n = 4j + g (g = i, f, g, o):
+//       [W[:, gH+j] | b[gH+j] | 0 | U[:, gH+j]]  -> one N-tile holds all four gates of
+//       its units, so the cell runs in the epilogue of the tile that produced them.
+//   Ut  [H, 4H] bf16, Ut[k][4j+g] = U[k][gH+j]  (the B operand of dh = dG U^T).
+//   Rec [T, B, H] x 8 fp16: i, f, g, o, c_{t-1}, tanh(c_t) of each live (t, b, j).
+//   dG  [T, B, 4H] bf16 gate gradients (interleaved), zero for t >= len.
+//   hcur, ccur, dhc, dc [B, H] fp32: running state and the BPTT carries.
+// Forward (one persistent launch over t = 0 .. n-1, grid barrier between steps):
+//     D = XH[t] WU^T (K = KX)    -> EpiFwd: gates, c, h, Rec, loss partial <h_t, y_t>
+//                                   (live rows), h_t -> XH[t+1]
+// Backward (one persistent launch over t = n-1 .. 0):
+//     D = dG[t+1] Ut^T (K = 4H)  -> EpiBwd: dh = D + carry + y/B, cell backward -> dG[t],
+//                                   dc, frozen-row carries
+// (gemm_steps_kernel: the epilogue operands of each tile are TMA-prefetched into shared
+// memory while its MMAs run.)
+// Then one GEMM over every (b, t):  P = XH^T dG  (M = KX, N = 4H, K = B T)
+//                         -> dW (rows < F), db (row F), dU (rows >= F + 16), un-interleaved.
+#include <cuda_fp16.h>
+#include <math.h>
+#include <string.h>
+
+#include "gemm.cuh"
+#include "skb_internal.h"
+
+namespace skb {
+namespace train_tc {
+
+using gemm::kBF16;
+
+struct Bufs {
+  __nv_bfloat16 *XH, *WU, *Ut, *dG;
+  __half* Rec;
+  float *hcur, *ccur, *dhc, *dc;
+  double* lpart;   // [T][fwd tiles][epilogue warps]
+  double* lsum;    // [T] per-step loss sums
+  int* sync;       // [2] grid-barrier counters of the forward / backward launches
+};
+
+inline int kx_of(int F, int H) { return F + 16 + H; }
+inline size_t al(size_t b) { return (b + 255) & ~size_t(255); }
+constexpr int kFwdBN = 128;
+constexpr int kFwdEW = 4;                    // epilogue warps per TMEM lane quarter (forward)
+constexpr int kFwdSlots = 4 * kFwdEW;        // loss partials per forward tile
+
+inline int fwd_tiles(int B, int H) { return ((B + 127) / 128) * (4 * H / kFwdBN); }
+
+size_t layout(int B, int T, int F, int H, uint8_t* base, Bufs* w) {
+  const size_t KX = kx_of(F, H), G = 4ull * H;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { uint8_t* p = base ? base + off : nullptr; off += al(bytes); return p; };
+  Bufs s;
+  s.XH = (__nv_bfloat16*)take(2ull * B * T * KX);
+  s.WU = (__nv_bfloat16*)take(2ull * G * KX);
+  s.Ut = (__nv_bfloat16*)take(2ull * H * G);
+  s.dG = (__nv_bfloat16*)take(2ull * B * T * G);
+  s.Rec = (__half*)take(16ull * B * T * H);
+  s.hcur = (float*)take(4ull * B * H);
+  s.ccur = (float*)take(4ull * B * H);
+  s.dhc = (float*)take(4ull * B * H);
+  s.dc = (float*)take(4ull * B * H);
+  s.lpart = (double*)take(8ull * T * fwd_tiles(B, H) * kFwdSlots);
+  s.lsum = (double*)take(8ull * T);
+  s.sync = (int*)take(8);
+  if (w) *w = s;
+  return off;
+}
+
+// Gate activations on the MUFU pipe: tanh.approx (|rel err| < 6e-4, inside the bf16
+// operand path's bound) and sigmoid(x) = tanh(x/2)/2 + 1/2.
+SKB_DEV float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+SKB_DEV float sigf(float x) { return fmaf(0.5f, tanh_fast(0.5f * x), 0.5f); }
+SKB_DEV uint32_t pack_bf2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+SKB_DEV uint32_t pack_h2(float a, float b) {
+  __half2 v = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+SKB_DEV float2 unpack_h2(uint32_t u) {
+  __half2 v = *reinterpret_cast<__half2*>(&u);
+  return __half22float2(v);
+}
+
+// ------------------------------------------------------------------ operand preparation
+// XH rows: [bf16(x) | 1 | 0 | h part: bf16(h0) at t = 0, else 0 (rewritten by the forward)]
+__global__ void prep_xh(const float* __restrict__ x, const float* __restrict__ h0, __nv_bfloat16* __restrict__ XH,
+                        int B, int T, int F, int H) {
+  const int KX = F + 16 + H, KX2 = KX / 2;
+  const long long pairs = (long long)B * T * KX2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / KX2;   // time-major row t B + b
+    const int c = (int)(i % KX2) * 2;
+    const int t = (int)(row / B), b = (int)(row % B);
+    float v0, v1;
+    if (c < F) {
+      const float2 xv = *reinterpret_cast<const float2*>(x + ((long long)b * T + t) * F + c);
+      v0 = xv.x; v1 = xv.y;
+    } else if (c < F + 16) {
+      v0 = c == F ? 1.f : 0.f;
+      v1 = 0.f;
+    } else if (t == 0 && h0) {
+      const int k = c - F - 16;
+      v0 = h0[(long long)b * H + k];
+      v1 = h0[(long long)b * H + k + 1];
+    } else {
+      v0 = v1 = 0.f;
+    }
+    *reinterpret_cast<uint32_t*>(XH + row * KX + c) = pack_bf2(v0, v1);
+  }
+}
+
+// WU [4H, KX] (interleaved rows) and Ut [H, 4H] from the fp32 parameters W [F, 4H],
+// U [H, 4H], b [4H]; one thread per output pair.
+__global__ void prep_weights(const float* __restrict__ W, const float* __restrict__ U, const float* __restrict__ bias,
+                             __nv_bfloat16* __restrict__ WU, __nv_bfloat16* __restrict__ Ut, int F, int H) {
+  const int G = 4 * H, KX = F + 16 + H;
+  const long long n1 = (long long)G * KX / 2, n2 = (long long)H * G / 2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n1 + n2; i += (long long)gridDim.x * blockDim.x) {
+    if (i < n1) {
+      const int n = (int)(i / (KX / 2)), c = (int)(i % (KX / 2)) * 2;
+      const int col = (n & 3) * H + (n >> 2);   // source column g H + j
+      float v[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k = c + e;
+        v[e] = k < F ? W[(long long)k * G + col] : k == F ? bias[col] : k < F + 16 ? 0.f : U[(long long)(k - F - 16) * G + col];
+      }
+      *reinterpret_cast<uint32_t*>(WU + (long long)n * KX + c) = pack_bf2(v[0], v[1]);
+    } else {
+      const long long ii = i - n1;
+      const int k = (int)(ii / (G / 2)), n = (int)(ii % (G / 2)) * 2;
+      const float a = U[(long long)k * G + (n & 3) * H + (n >> 2)];
+      const float b = U[(long long)k * G + ((n + 1) & 3) * H + ((n + 1) >> 2)];
+      *reinterpret_cast<uint32_t*>(Ut + (long long)k * G + n) = pack_bf2(a, b);
+    }
+  }
+}
+
+__global__ void init_state(const float* __restrict__ h0, const float* __restrict__ c0, Bufs w, int B, int H) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)B * H;
+       i += (long long)gridDim.x * blockDim.x) {
+    w.hcur[i] = h0 ? h0[i] : 0.f;
+    w.ccur[i] = c0 ? c0[i] : 0.f;
+    w.dhc[i] = 0.f;
+    w.dc[i] = 0.f;
+  }
+}
+
+// loss = inv_b * sum of the partials: stage 1 one block per step (fixed order within the
+// block), stage 2 the step sums in order (deterministic).
+__global__ void loss_step_sums(const double* __restrict__ part, int per_step, double* __restrict__ sums) {
+  __shared__ double red[256];
+  double s = 0.0;
+  const double* p = part + (long long)blockIdx.x * per_step;
+  for (int i = threadIdx.x; i < per_step; i += blockDim.x) s += p[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sums[blockIdx.x] = red[0];
+}
+__global__ void loss_final_sum(const double* __restrict__ sums, int n, float inv_b, float* loss) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += sums[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = (float)(red[0] * inv_b);
+}
+
+// ------------------------------------------------------------------ fused epilogues
+// Each step kernel's TMA producer loads the tile's epilogue operands (state, carries,
+// y_t, cell records) into shared memory while the MMAs run (kOpBytes); the epilogue
+// reads them conflict-free from the 128-byte-swizzled boxes and writes its results.
+constexpr uint32_t kBox = 128 * 128;   // one [128 rows][128 B] operand box
+
+// Forward cell of step t = st: 16 accumulator columns = 4 units x (i, f, g, o); tile = 32 units.
+struct EpiFwd {
+  static constexpr uint32_t kOpBytes = 3 * kBox;   // c_{t-1}, h_{t-1}, y_t: [128 rows][32 units] fp32
+  struct State { double lacc; bool live; };
+  CUtensorMap mC, mH, mY;   // mY: y [B][T][H] as a 3-D map {H, T, B}
+  const int64_t* lens;
+  float *hcur, *ccur;
+  __nv_bfloat16* XH;
+  __half* Rec;
+  double* lpart;
+  int T, F, H, B, tiles_n, tiles;
+  int diag;   // SKB_TC_DIAG (timing experiments only): bit 0 skip the cell
+  SKB_DEV int a_coord(int st) const { return st; }
+  SKB_DEV bool k_empty(int) const { return false; }
+  SKB_DEV void prefetch(uint8_t* sop, int st, int tm, int tn, uint64_t* bar) const {
+    gemm::tma_load_2d(sop, &mC, tn * 32, tm * 128, bar);
+    gemm::tma_load_2d(sop + kBox, &mH, tn * 32, tm * 128, bar);
+    gemm::tma_load_3d(sop + 2 * kBox, &mY, tn * 32, st, tm * 128, bar);
+  }
+  SKB_DEV void begin_tile(State& es, int st, int, int, int m) const {
+    es.lacc = 0.0;
+    es.live = m < B && st < lens[m];
+  }
+  SKB_DEV void chunk(State& es, const uint8_t* sop, int t, int r, int m, int n0, int c, const float (&v)[16],
+                     bool row_ok) const {
+    if (!row_ok || (diag & 1)) return;
+    const int j0 = n0 >> 2;
+    const long long s = (long long)m * H + j0;
+    const float4 cp4 = *reinterpret_cast<const float4*>(gemm::sw128_at(sop, r, c >> 4));
+    const float4 hp4 = *reinterpret_cast<const float4*>(gemm::sw128_at(sop + kBox, r, c >> 4));
+    const float cp[4] = {cp4.x, cp4.y, cp4.z, cp4.w}, hp[4] = {hp4.x, hp4.y, hp4.z, hp4.w};
+    float cn[4], hn[4];
+    uint4 rec[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float ig = sigf(v[4 * u]), fg = sigf(v[4 * u + 1]), gg = tanh_fast(v[4 * u + 2]), og = sigf(v[4 * u + 3]);
+      const float c2 = fg * cp[u] + ig * gg;
+      const float tc = tanh_fast(c2);
+      const float h2 = og * tc;
+      cn[u] = es.live ? c2 : cp[u];
+      hn[u] = es.live ? h2 : hp[u];
+      rec[u] = make_uint4(pack_h2(ig, fg), pack_h2(gg, og), pack_h2(cp[u], tc), 0u);
+    }
+    *reinterpret_cast<float4*>(ccur + s) = make_float4(cn[0], cn[1], cn[2], cn[3]);
+    *reinterpret_cast<float4*>(hcur + s) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+    if (t + 1 < T) {
+      const int KX = F + 16 + H;
+      *reinterpret_cast<uint2*>(XH + ((long long)(t + 1) * B + m) * KX + F + 16 + j0) =
+          make_uint2(pack_bf2(hn[0], hn[1]), pack_bf2(hn[2], hn[3]));
+    }
+    if (es.live) {
+      uint4* rp = reinterpret_cast<uint4*>(Rec + (((long long)t * B + m) * H + j0) * 8);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) __stcs(rp + u, rec[u]);   // streamed: read once, in the backward
+      const float4 yv = *reinterpret_cast<const float4*>(gemm::sw128_at(sop + 2 * kBox, r, c >> 4));
+      es.lacc += (double)hn[0] * yv.x + (double)hn[1] * yv.y + (double)hn[2] * yv.z + (double)hn[3] * yv.w;
+    }
+  }
+  SKB_DEV void end_tile(State& es, int t, int tm, int tn, int slot, int lane) const {
+    double sum = es.lacc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) lpart[((long long)t * tiles + tm * tiles_n + tn) * kFwdSlots + slot] = sum;
+  }
+};
+
+// Backward cell of step t = n-1-st: 16 accumulator columns = dh of 16 consecutive units;
+// tile = 32 units.  Operands: dh carry, dc carry, y_t (fp32 boxes) and the cell records
+// (four [128 rows][8 units x 16 B] boxes).
+struct EpiBwd {
+  static constexpr uint32_t kOpBytes = 7 * kBox;
+  struct State { bool live; };
+  CUtensorMap mDh, mDc, mY, mRec;   // mY {H, T, B}, mRec {8H, B, T} (3-D)
+  const int64_t* lens;
+  float *dhc, *dc;
+  __nv_bfloat16* dG;
+  int n, T, H, B;
+  float inv_b;
+  int diag;
+  SKB_DEV int a_coord(int st) const { return n - st; }          // dG[t + 1]
+  SKB_DEV bool k_empty(int st) const { return st == 0; }        // t = n-1: no dG_{t+1}
+  SKB_DEV void prefetch(uint8_t* sop, int st, int tm, int tn, uint64_t* bar) const {
+    const int t = n - 1 - st;
+    gemm::tma_load_2d(sop, &mDh, tn * 32, tm * 128, bar);
+    gemm::tma_load_2d(sop + kBox, &mDc, tn * 32, tm * 128, bar);
+    gemm::tma_load_3d(sop + 2 * kBox, &mY, tn * 32, t, tm * 128, bar);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) gemm::tma_load_3d(sop + (3 + b) * kBox, &mRec, (tn * 32 + 8 * b) * 8, tm * 128, t, bar);
+  }
+  SKB_DEV void begin_tile(State& es, int st, int, int, int m) const { es.live = m < B && n - 1 - st < lens[m]; }
+  SKB_DEV void chunk(State& es, const uint8_t* sop, int st, int r, int m, int k0, int c, const float (&v)[16],
+                     bool row_ok) const {
+    if (!row_ok || (diag & 1)) return;
+    const int t = n - 1 - st;
+    const long long s = (long long)m * H + k0;
+    uint2* g = reinterpret_cast<uint2*>(dG + ((long long)t * B + m) * 4 * H + 4 * k0);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {   // four units per pass
+      const int c16 = (c >> 2) + q4, uu = c + 4 * q4;   // fp32 chunk, first unit (tile-relative)
+      const float4 c4 = *reinterpret_cast<const float4*>(gemm::sw128_at(sop, r, c16));
+      float dh[4] = {v[4 * q4] + c4.x, v[4 * q4 + 1] + c4.y, v[4 * q4 + 2] + c4.z, v[4 * q4 + 3] + c4.w};
+      if (!es.live) {
+        *reinterpret_cast<float4*>(dhc + s + 4 * q4) = make_float4(dh[0], dh[1], dh[2], dh[3]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) g[4 * q4 + u] = make_uint2(0u, 0u);
+        continue;
+      }
+      const float4 yv = *reinterpret_cast<const float4*>(gemm::sw128_at(sop + 2 * kBox, r, c16));
+      dh[0] += yv.x * inv_b; dh[1] += yv.y * inv_b; dh[2] += yv.z * inv_b; dh[3] += yv.w * inv_b;
+      const float4 dc4 = *reinterpret_cast<const float4*>(gemm::sw128_at(sop + kBox, r, c16));
+      const float dcv[4] = {dc4.x, dc4.y, dc4.z, dc4.w};
+      float dco[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int un = uu + u;
+        const uint4 rr = *reinterpret_cast<const uint4*>(gemm::sw128_at(sop + (3 + (un >> 3)) * kBox, r, un & 7));
+        const float2 a = unpack_h2(rr.x), b = unpack_h2(rr.y), cc = unpack_h2(rr.z);
+        const float ig = a.x, fg = a.y, gg = b.x, og = b.y, cp = cc.x, tc = cc.y;
+        const float dcn = dcv[u] + dh[u] * og * (1.f - tc * tc);
+        const float di = dcn * gg * ig * (1.f - ig);
+        const float df = dcn * cp * fg * (1.f - fg);
+        const float dg = dcn * ig * (1.f - gg * gg);
+        const float dO = dh[u] * tc * og * (1.f - og);
+        g[4 * q4 + u] = make_uint2(pack_bf2(di, df), pack_bf2(dg, dO));
+        dco[u] = dcn * fg;
+      }
+      *reinterpret_cast<float4*>(dc + s + 4 * q4) = make_float4(dco[0], dco[1], dco[2], dco[3]);
+      *reinterpret_cast<float4*>(dhc + s + 4 * q4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  SKB_DEV void end_tile(State&, int, int, int, int, int) const {}
+};
+
+// Weight gradients from P = XH^T dG (rows m of KX, interleaved columns n = 4j + g).
+struct EpiGrad {
+  static constexpr uint32_t kOpBytes = 0;
+  struct State {};
+  float *dW, *dU, *db;
+  int F, H;
+  SKB_DEV bool ops_on() const { return false; }
+  SKB_DEV void prefetch(uint8_t*, int, int, uint64_t*) const {}
+  SKB_DEV void begin_tile(State&, int, int, int, int) const {}
+  SKB_DEV void chunk(State&, const uint8_t*, int, int m, int n0, int, int, const float (&v)[16], bool row_ok) const {
+    if (!row_ok || (m > F && m < F + 16)) return;
+    const int G = 4 * H, j0 = n0 >> 2;
+    float* dst = m < F ? dW + (long long)m * G : m == F ? db : dU + (long long)(m - F - 16) * G;
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      *reinterpret_cast<float4*>(dst + g * H + j0) = make_float4(v[g], v[4 + g], v[8 + g], v[12 + g]);
+  }
+  SKB_DEV void end_tile(State&, int, int, int, int, int) const {}
+};
+
+int diag() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("SKB_TC_DIAG"); v = e ? atoi(e) : 0; }
+  return v;
+}
+
+// SKB_TRAIN_PDL=0 disables programmatic dependent launch of the step kernels.
+bool pdl() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("SKB_TRAIN_PDL"); v = (e && atoi(e) == 0) ? 0 : 1; }
+  return v == 1;
+}
+
+}  // namespace train_tc
+}  // namespace skb
+
+using namespace skb::train_tc;
+
+// Workspace of the tensor-core path (math == 2).
+extern "C" int64_t skb_train_tc_workspace_bytes(const skb_train_shape* d) {
+  if (!d) return -1;
+  return (int64_t)layout(d->rows, d->time, d->input, d->hidden, nullptr, nullptr);
+}
+
+// Enqueue one training step (forward + BPTT + gradients) on `cs`; the caller captures
+// it into a CUDA graph.  Returns false on a launch/encode failure.
+extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, const float* y, const int64_t* lens,
+                                    const float* h0, const float* c0, const float* params, float* grads, float* loss,
+                                    int n, void* workspace, void* stream) {
+  namespace gm = skb::gemm;
+  const int B = d->rows, T = d->time, F = d->input, H = d->hidden, G = 4 * H, KX = kx_of(F, H);
+  if ((F % 8) || (H % 16) || G % kFwdBN) return SKB_ERR_UNSUPPORTED;
+  cudaStream_t cs = (cudaStream_t)stream;
+  Bufs w;
+  layout(B, T, F, H, (uint8_t*)workspace, &w);
+  const float* W = params;
+  const float* U = params + (size_t)F * G;
+  const float* bias = U + (size_t)H * G;
+  float* dW = grads;
+  float* dU = grads + (size_t)F * G;
+  float* db = dU + (size_t)H * G;
+  const int blocks = gm::num_sms() * 8;
+  prep_xh<<<blocks, 256, 0, cs>>>(x, h0, w.XH, B, T, F, H);
+  prep_weights<<<blocks, 256, 0, cs>>>(W, U, bias, w.WU, w.Ut, F, H);
+  init_state<<<blocks, 256, 0, cs>>>(h0, c0, w, B, H);
+  if (cudaPeekAtLastError() != cudaSuccess) return SKB_ERR_CUDA;
+
+  // forward: one persistent launch; B operand WU (K-major), A operand XH[t] (3-D map)
+  using GF = gm::Geo<kBF16, kFwdBN>;
+  CUtensorMap mWU, mUt, mXH, mdG, mY, mRec, mC, mH, mDh, mDc;
+  const int tiles_n = G / kFwdBN;
+  if (!gm::encode_2d(&mWU, kBF16, w.WU, KX, G, KX, GF::BK, kFwdBN) ||
+      !gm::encode_3d(&mXH, kBF16, w.XH, KX, B, T, KX, (uint64_t)B * KX, GF::BK, GF::BM, 1) ||
+      !gm::encode_3d(&mY, gm::kTF32, y, H, T, B, H, (uint64_t)T * H, 32, 1, 128) ||
+      !gm::encode_2d(&mC, gm::kTF32, w.ccur, H, B, H, 32, 128) || !gm::encode_2d(&mH, gm::kTF32, w.hcur, H, B, H, 32, 128) ||
+      !gm::encode_2d(&mDh, gm::kTF32, w.dhc, H, B, H, 32, 128) || !gm::encode_2d(&mDc, gm::kTF32, w.dc, H, B, H, 32, 128) ||
+      !gm::encode_2d(&mUt, kBF16, w.Ut, G, H, G, 64, 32) ||
+      !gm::encode_3d(&mdG, kBF16, w.dG, G, B, T, G, (uint64_t)B * G, 64, 128, 1) ||
+      !gm::encode_3d(&mRec, kBF16, w.Rec, (uint64_t)H * 8, B, T, (uint64_t)H * 8, (uint64_t)B * H * 8, 64, 128, 1))
+    return SKB_ERR_INVALID;
+  cudaMemsetAsync(w.sync, 0, 8, cs);
+  {
+    EpiFwd e;
+    e.mC = mC; e.mH = mH; e.mY = mY;
+    e.lens = lens; e.hcur = w.hcur; e.ccur = w.ccur; e.XH = w.XH; e.Rec = w.Rec; e.lpart = w.lpart;
+    e.T = T; e.F = F; e.H = H; e.B = B; e.tiles_n = tiles_n; e.tiles = fwd_tiles(B, H); e.diag = diag();
+    gm::StepShape sh{B, G, KX, n, w.sync};
+    if (int rc = gm::launch_steps<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXH, mWU, sh, e, cs))
+      return rc == 3 ? SKB_ERR_UNSUPPORTED : SKB_ERR_CUDA;
+  }
+  loss_step_sums<<<n, 256, 0, cs>>>(w.lpart, fwd_tiles(B, H) * kFwdSlots, w.lsum);
+  loss_final_sum<<<1, 256, 0, cs>>>(w.lsum, n, d->inv_batch, loss);
+
+  // backward: one persistent launch; dh = dG[t+1] Ut^T, 32-unit tiles
+  {
+    EpiBwd e;
+    e.mDh = mDh; e.mDc = mDc; e.mY = mY; e.mRec = mRec;
+    e.lens = lens; e.dhc = w.dhc; e.dc = w.dc; e.dG = w.dG;
+    e.n = n; e.T = T; e.H = H; e.B = B; e.inv_b = d->inv_batch; e.diag = diag();
+    gm::StepShape sh{B, H, G, n, w.sync + 1};
+    if (int rc = gm::launch_steps<kBF16, 32, EpiBwd, 2>(mdG, mUt, sh, e, cs))
+      return rc == 3 ? SKB_ERR_UNSUPPORTED : SKB_ERR_CUDA;
+  }
+  // dG rows t >= n take no part in the step: zero for the weight-gradient GEMM (its K
+  // runs over every (t, b)); XH's h part of rows t > n is zero from prep_xh
+  if (n < T) cudaMemsetAsync(w.dG + (size_t)n * B * G, 0, 2ull * (T - n) * B * G, cs);
+
+  // weight gradients over every (t, b): P = XH^T dG  (A: XH as [K = T B, M = KX], MN-major;
+  // B: dG as [K = B T, N = 4H], MN-major)
+  {
+    using GG = gm::Geo<kBF16, 256>;
+    CUtensorMap mX, mD;
+    const uint64_t rows = (uint64_t)B * T;
+    if (!gm::encode_2d(&mX, kBF16, w.XH, KX, rows, KX, GG::MNB, GG::BK)) return SKB_ERR_INVALID;
+    if (!gm::encode_2d(&mD, kBF16, w.dG, G, rows, G, GG::MNB, GG::BK)) return SKB_ERR_INVALID;
+    EpiGrad e;
+    e.dW = dW; e.dU = dU; e.db = db; e.F = F; e.H = H;
+    gm::Shape sh{KX, G, (int)rows, 1, 0};
+    if (gm::launch<kBF16, 256, true, true>(mX, mD, sh, e, cs)) return SKB_ERR_CUDA;
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? SKB_OK : SKB_ERR_CUDA;
+}

@@ -107,6 +107,10 @@ SIGNATURES = {
     "skb_rnn_last_clusters": (ctypes.c_int, []),
     "skb_rnn_last_overlap": (ctypes.c_int, []),
     "skb_rnn_set_overlap": (ctypes.c_int, [ctypes.c_int]),
+    "skb_gemm_workspace_bytes": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "skb_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                _VP, ctypes.c_int64, _VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int,
+                                ctypes.c_int, ctypes.c_int, _VP, _VP]),
     "skb_diag_umma_pair": (ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP]),
     "skb_diag_cluster_exchange": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _VP, _VP, _VP, _VP]),
 }

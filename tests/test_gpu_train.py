@@ -49,6 +49,32 @@ def test_train_step_matches_oracle(B, T, F, H, math, tol, graph):
         assert np.max(np.abs(got - ref)) <= tol * max(1.0, np.max(np.abs(ref))), np.max(np.abs(got - ref))
 
 
+def test_c2_configured_shape_against_oracle():
+    """The benchmarked C2 shape (hidden 1024, input 1024, max_len 512, lengths U{1..512},
+    the bench's bf16 tensor-core path: skb's tcgen05 GEMMs with fused cells), batch
+    reduced to 8 rows so the float64 oracle finishes in seconds.  The measured error is
+    written to gpurun_out/c2_err.json; bound: 6e-2 of the largest gradient entry."""
+    import json
+    import os
+    B, T, F, H = 8, 512, 1024, 1024
+    x, y, h0, c0, _, W, U, b = _problem(B, T, F, H, 77)
+    lens = np.random.default_rng(78).integers(1, T + 1, B)
+    lens[0] = T   # the full trip count
+    loss_ref, dW, dU, db = bptt.forward_backward(x, h0, c0, lens, y, W, U, b, 1.0 / B)
+    tr = LstmTrainer(F, H, B, T, global_batch=B, lr=0.0, math="bf16", graph=True,
+                     params=np.concatenate([W.reshape(-1), U.reshape(-1), b]))
+    loss = tr.forward_backward(_dev(x), _dev(y), _dev(lens, torch.int64), _dev(h0), _dev(c0))
+    gW, gU, gb = (t.cpu().numpy().astype(np.float64) for t in tr.views(tr.grads))
+    errs = {"loss": abs(float(loss.item()) - loss_ref) / max(1.0, abs(loss_ref))}
+    for name, got, ref in (("dW", gW, dW), ("dU", gU, dU), ("db", gb, db)):
+        errs[name] = float(np.max(np.abs(got - ref)) / max(1.0, np.max(np.abs(ref))))
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/c2_err.json", "w") as f:
+        json.dump({"shape": {"B": B, "T": T, "F": F, "H": H}, "math": "bf16", "lib_path": "tcgen05 (train_tc.cu)",
+                   "metric": "max|gpu-ref| / max(1, max|ref|)", "errors": errs, "bound": 6e-2}, f)
+    assert all(e <= 6e-2 for e in errs.values()), errs
+
+
 def test_sgd_step_and_replay():
     B, T, F, H = 8, 9, 6, 16
     x, y, h0, c0, lens, W, U, b = _problem(B, T, F, H, 5)
