@@ -79,6 +79,25 @@ def test_beam_search_matches_oracle(S, V, E, H, K, T, eos, seed, eb):
     assert np.allclose(s_got, s_ref, rtol=1e-4, atol=1e-4)
 
 
+def test_full_size_beam8_matches_oracle():
+    """BASELINE C3 shape (beam 8, vocab 32k, H=E=512; 16 sentences, 12 steps, EOS-biased so
+    beams finish at steps 1..12) against the float64 oracle, fp32 GEMMs: tokens, lengths
+    and the trip count exact, scores within 1e-4.  Margin audit: the oracle's smallest
+    K-th-choice score gap over all steps must exceed 20x the fp32 score error (~1e-5), so
+    no near-tie can legitimately flip a choice (measured 4.5e-4 for this seed)."""
+    S, V, E, H, K, T, eos = 16, 32000, 512, 512, 8, 12, 2
+    h0, c0, emb, w = _lstm_problem(S, V, E, H, 9, eos, 4.0)
+    ref = obeam.decode("lstm", h0, emb, w, K, eos, T, c0=c0)
+    assert min(ref["margins"]) >= 2e-4, ref["margins"]
+    got = decode("lstm", h0, emb, w, K, eos, T, c0=c0, math="fp32")
+    steps = ref["steps"]
+    assert got["steps"] == steps
+    assert np.array_equal(got["tokens"].cpu().numpy()[:, :, :steps + 1], ref["tokens"][:, :, :steps + 1])
+    assert np.array_equal(got["lengths"].cpu().numpy(), ref["lengths"])
+    s_got, s_ref = got["scores"].cpu().numpy().astype(np.float64), ref["scores"]
+    assert np.allclose(s_got, s_ref, rtol=1e-4, atol=1e-4), np.max(np.abs(s_got - s_ref))
+
+
 def test_full_size_beam8_properties():
     """BASELINE C3 shape (beam 8, vocab 32k, H=512) on TF32 tensor cores."""
     S, V, E, H, K, T = 16, 32000, 512, 512, 8, 12
