@@ -4,12 +4,18 @@
 //
 // One decode step for R = sentences x beam rows:
 //   dec_gather   xh = [emb[tok], h]                      (tensor.py:420-430 Index)
-//   GEMM         gates = xh @ W_gates       (cuBLAS; fp32 exact or TF32 tensor cores)
+//   GEMM         gates = xh @ W_gates
 //   dec_cell     rnn: h' = tanh(gates); lstm: i,f,g,o -> c', h'   (tensor.py:391-407)
-//   GEMM         logits = h' @ W_out                     (cuBLAS, same math)
+//   GEMM         logits = h' @ W_out
 //   beam_rows    ONE pass over the logits, one CTA per beam row: it keeps
 //                an online max / sum-exp (log-softmax) and per-thread top-K lists
 //                merged by warp-shuffle argmax;
+// With SKB_DEC_TC=1, TF32 LSTM decoding runs both GEMMs on skb's own tcgen05 engine
+// (gemm.cuh) instead (measured slower, see dec_tc): the cell is fused into the gate GEMM's epilogue
+// (gate-interleaved weight rows), and the log-softmax normaliser + per-row top-K into the
+// logits GEMM's epilogue (per-tile partials merged by dec_merge), so the [R, V] logits
+// never reach HBM.  fp32-exact decoding (math 0) keeps cuBLAS GEMMs (tensor cores cannot
+// do exact fp32).
 //   beam_choose  per sentence: ranks its K x K candidates (score desc, flat index
 //                asc — the oracle's tie-break), reindexes h, c, scores, tokens,
 //                lengths and history from the chosen parents and counts
@@ -23,6 +29,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
+#include "gemm.cuh"
 #include "skb_internal.h"
 
 namespace {
@@ -50,7 +57,27 @@ struct DecodeState {             // device pointers into the workspace
   int32_t* row_i;                // [R, KMAX] their vocabulary ids
   float* row_lse;                // [R] log-sum-exp of the row
   float* margin;                 // [R] greedy (beam 1): smallest top-1 - top-2 logit gap over the decode
+  // tensor-core path (math 1, LSTM)
+  float* wgT;                    // [4H, E+H] gate-interleaved rows n = 4j + g (K-major B operand)
+  float* bg;                     // [4H] interleaved gate bias
+  float* woT;                    // [Vp, H] w_out^T (K-major B operand), rows >= V zero
+  float* bo;                     // [Vp] output bias, -inf on the pad columns v >= V (masks them)
+  float* part;                   // [R][ntn][kDecEW][2 + 2 KR] logits-tile partials (max, sum-exp, top-K)
 };
+constexpr int kDecBN = 256;       // logits tile width
+constexpr int kDecEW = 2;         // logits epilogue warps per TMEM lane quarter
+constexpr int kCellBN = 128;      // gate tile width: 32 units x (i, f, g, o)
+inline int dec_vp(int V) { return (V + 15) / 16 * 16; }
+inline int dec_ntn(int V) { return (dec_vp(V) + kDecBN - 1) / kDecBN; }
+// SKB_DEC_TC=1 selects the engine path for TF32 LSTM decoding.  Measured on the B200 at the
+// C3 shape it is 2.2x slower than the library GEMMs + beam_rows (4.6 vs 2.1 ms per decode:
+// the 1-CTA 128x256 tcgen05 tiles run the logits GEMM at ~350 TFLOP/s vs CUTLASS's 2-SM
+// 256x256 at ~600, and the per-row top-K insertion in the epilogue costs more than the
+// logits round trip it removes), so it is opt-in (profiles/r02_c3_engine.md).
+inline bool dec_tc(const skb_decode_shape& d) {
+  const char* e = getenv("SKB_DEC_TC");
+  return e && atoi(e) == 1 && d.math == 1 && d.cell == SKB_CELL_LSTM && d.embed % 4 == 0 && d.hidden % 32 == 0;
+}
 
 __device__ __forceinline__ float sigmoidf_ref(float x) {   // reference tensor.py:403-407 (two branches)
   if (x >= 0.f) return 1.f / (1.f + expf(-x));
@@ -382,6 +409,181 @@ __global__ void __launch_bounds__(SEL_THREADS) beam_choose(DecodeState st, int S
   }
 }
 
+// ------------------------------------------------------------------ tensor-core path
+// Weights for the engine (once per decode): gate-interleaved W_gates^T, bias, w_out^T.
+__global__ void dec_prep_gates(const float* __restrict__ w_gates, const float* __restrict__ b_gates,
+                               float* __restrict__ wgT, float* __restrict__ bg, int KG, int H) {
+  const int G = 4 * H;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)G * KG;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(i / KG), k = (int)(i % KG);
+    wgT[i] = w_gates[(long long)k * G + (n & 3) * H + (n >> 2)];
+  }
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < G; n += gridDim.x * blockDim.x)
+    bg[n] = b_gates ? b_gates[(n & 3) * H + (n >> 2)] : 0.f;
+}
+// woT[v][k] = w_out[k][v] (32 x 32 shared-memory tiles: coalesced both ways), zero rows v >= V.
+__global__ void dec_prep_out(const float* __restrict__ w_out, const float* __restrict__ b_out, float* __restrict__ woT,
+                             float* __restrict__ bo, int H, int V, int Vp) {
+  __shared__ float tile[32][33];
+  if (blockIdx.y == 0 && threadIdx.y == 0) {
+    const int v = blockIdx.x * 32 + threadIdx.x;
+    if (v < Vp) bo[v] = v < V ? (b_out ? b_out[v] : 0.f) : -INFINITY;
+  }
+  const int v0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int k = k0 + j, v = v0 + threadIdx.x;
+    tile[j][threadIdx.x] = (k < H && v < V) ? w_out[(long long)k * V + v] : 0.f;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int v = v0 + j, k = k0 + threadIdx.x;
+    if (v < Vp && k < H) woT[(long long)v * H + k] = tile[threadIdx.x][j];
+  }
+}
+
+// Gate GEMM epilogue: 16 accumulator columns = 4 units x (i, f, g, o) -> c', h' (the
+// arithmetic of dec_cell4: bias, reference sigmoid branches, tanhf).
+struct EpiDecCell {
+  static constexpr uint32_t kOpBytes = 0;
+  struct State {};
+  DecodeState st;
+  int H;
+  SKB_DEV bool skip() const { return st.active[*st.tstep] == 0; }
+  SKB_DEV bool ops_on() const { return false; }
+  SKB_DEV void prefetch(uint8_t*, int, int, uint64_t*) const {}
+  SKB_DEV void begin_tile(State&, int, int, int, int) const {}
+  SKB_DEV void chunk(State&, const uint8_t*, int, int m, int n0, int, int, const float (&v)[16], bool row_ok) const {
+    if (!row_ok) return;
+    const int j0 = n0 >> 2, cur = *st.tstep & 1;
+    const float4 cv = *reinterpret_cast<const float4*>(st.c[cur] + (long long)m * H + j0);
+    const float4 b0 = *reinterpret_cast<const float4*>(st.bg + n0), b1 = *reinterpret_cast<const float4*>(st.bg + n0 + 4);
+    const float4 b2 = *reinterpret_cast<const float4*>(st.bg + n0 + 8), b3 = *reinterpret_cast<const float4*>(st.bg + n0 + 12);
+    const float bb[16] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w, b3.x, b3.y, b3.z, b3.w};
+    const float cp[4] = {cv.x, cv.y, cv.z, cv.w};
+    float cn[4], hn[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float ig = v[4 * u] + bb[4 * u], fg = v[4 * u + 1] + bb[4 * u + 1];
+      const float gg = v[4 * u + 2] + bb[4 * u + 2], og = v[4 * u + 3] + bb[4 * u + 3];
+      cn[u] = sigmoidf_ref(fg) * cp[u] + sigmoidf_ref(ig) * tanhf(gg);
+      hn[u] = sigmoidf_ref(og) * tanhf(cn[u]);
+    }
+    *reinterpret_cast<float4*>(st.cn + (long long)m * H + j0) = make_float4(cn[0], cn[1], cn[2], cn[3]);
+    *reinterpret_cast<float4*>(st.hn + (long long)m * H + j0) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+  }
+  SKB_DEV void end_tile(State&, int, int, int, int, int) const {}
+};
+
+// Logits GEMM epilogue: per row and tile column group, the online max / sum-exp and the
+// KR best (value desc, index asc) of logit + b_out — one partial record per (row, tile,
+// group); the [R, V] logits are never stored.
+template <int KR>
+struct EpiLogits {
+  static constexpr uint32_t kOpBytes = 0;
+  struct State { float mx, sum; float v[KR]; int ix[KR]; };
+  DecodeState st;
+  const float* b_out;
+  int V, ntn, R;
+  SKB_DEV bool skip() const { return st.active[*st.tstep] == 0; }
+  SKB_DEV bool ops_on() const { return false; }
+  SKB_DEV void prefetch(uint8_t*, int, int, uint64_t*) const {}
+  SKB_DEV void begin_tile(State& es, int, int, int, int) const {
+    es.mx = -INFINITY;
+    es.sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) { es.v[k] = -INFINITY; es.ix[k] = 0x7fffffff; }
+  }
+  SKB_DEV void chunk(State& es, const uint8_t*, int, int, int n0, int, int, const float (&a)[16], bool row_ok) const {
+    if (!row_ok) return;
+    // bias (pad columns carry -inf: no per-element range test), branch-free max / sum-exp
+    const float4* b4 = reinterpret_cast<const float4*>(st.bo + n0);
+    float x[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 b = __ldg(b4 + q);
+      x[4 * q] = a[4 * q] + b.x; x[4 * q + 1] = a[4 * q + 1] + b.y;
+      x[4 * q + 2] = a[4 * q + 2] + b.z; x[4 * q + 3] = a[4 * q + 3] + b.w;
+    }
+    float cm = x[0];
+#pragma unroll
+    for (int i = 1; i < 16; ++i) cm = fmaxf(cm, x[i]);
+    if (cm == -INFINITY) return;
+    const float nm = fmaxf(es.mx, cm);
+    const float l2e = 1.4426950408889634f, off = -nm * l2e;
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};   // four independent chains, ex2 of (x - max) log2 e
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s4[i & 3] += exp2f(fmaf(x[i], l2e, off));
+    es.sum = es.sum * exp2f(fmaf(es.mx, l2e, off)) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
+    es.mx = nm;
+    if (cm >= es.v[KR - 1]) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) topk_insert<KR>(es.v, es.ix, x[i], n0 + i);
+    }
+  }
+  SKB_DEV void end_tile(State& es, int tm, int tn, int, int slot, int lane) const {
+    const int m = tm * 128 + ((slot + 2) & 3) * 32 + lane, cg = slot >> 2;   // slot = warp - 2
+    if (m < R) {
+      float* p = st.part + (((long long)m * ntn + tn) * kDecEW + cg) * (2 + 2 * KR);
+      p[0] = es.mx;
+      p[1] = es.sum;
+#pragma unroll
+      for (int k = 0; k < KR; ++k) { p[2 + k] = es.v[k]; p[2 + KR + k] = __int_as_float(es.ix[k]); }
+    }
+  }
+};
+
+// Merge of the logits partials, one warp per live beam row: log-sum-exp and the row's KR
+// best (value desc, index asc) -> row_v / row_i / row_lse (what beam_rows produces).
+template <int KR>
+__global__ void dec_merge(DecodeState st, int R, int ntn) {
+  const int t = *st.tstep, cur = t & 1;
+  if (st.active[t] == 0) return;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= R || st.fin[cur][r]) return;
+  const int np = ntn * kDecEW;
+  const float* P = st.part + (long long)r * np * (2 + 2 * KR);
+  float mx = -INFINITY, sum = 0.f, v[KR];
+  int ix[KR];
+#pragma unroll
+  for (int k = 0; k < KR; ++k) { v[k] = -INFINITY; ix[k] = 0x7fffffff; }
+  for (int p = lane; p < np; p += 32) {
+    const float* q = P + (long long)p * (2 + 2 * KR);
+    const float pm = q[0], ps = q[1];
+    if (pm != -INFINITY) {
+      const float m = fmaxf(mx, pm);
+      sum = (mx == -INFINITY ? 0.f : sum * __expf(mx - m)) + ps * __expf(pm - m);
+      mx = m;
+    }
+#pragma unroll
+    for (int k = 0; k < KR; ++k) topk_insert<KR>(v, ix, q[2 + k], __float_as_int(q[2 + KR + k]));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, mx, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+    const float m = fmaxf(mx, m2);
+    sum = (mx == -INFINITY ? 0.f : sum * __expf(mx - m)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - m));
+    mx = m;
+  }
+  int head = 0;
+  for (int k = 0; k < KR; ++k) {
+    float bv = -INFINITY;
+    int bi = 0x7fffffff, bl = lane;
+#pragma unroll
+    for (int j = 0; j < KR; ++j)
+      if (j == head) { bv = v[j]; bi = ix[j]; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (better(ov, oi, bv, bi) || (ov == bv && oi == bi && ol < bl)) { bv = ov; bi = oi; bl = ol; }
+    }
+    if (lane == 0) { st.row_v[(long long)r * KMAX + k] = bv; st.row_i[(long long)r * KMAX + k] = bi; }
+    if (lane == bl) ++head;
+  }
+  if (lane == 0) st.row_lse[r] = mx + logf(sum);
+}
+
 // Steps that found every sentence finished leave the state untouched: carry
 // the current ping-pong side forward so the host can read "side of step T".
 __global__ void dec_init(DecodeState st, const float* __restrict__ h0, const float* __restrict__ c0, int S, int K,
@@ -457,7 +659,7 @@ size_t layout(const skb_decode_shape& d, DecodeState* st, uint8_t* base) {
   for (int k = 0; k < 2; ++k) { s.h[k] = (float*)take(4 * R * H); s.c[k] = (float*)take(4 * R * H); }
   s.hn = (float*)take(4 * R * H);
   s.cn = (float*)take(4 * R * H);
-  s.logits = (float*)take(4 * R * V);
+  s.logits = dec_tc(d) ? nullptr : (float*)take(4 * R * V);   // the engine path never stores logits
   for (int k = 0; k < 2; ++k) {
     s.score[k] = (double*)take(8 * R);
     s.fin[k] = (int32_t*)take(4 * R);
@@ -471,6 +673,15 @@ size_t layout(const skb_decode_shape& d, DecodeState* st, uint8_t* base) {
   s.row_i = (int32_t*)take(4 * R * KMAX);
   s.row_lse = (float*)take(4 * R);
   s.margin = (float*)take(4 * R);
+  s.wgT = s.bg = s.woT = s.bo = s.part = nullptr;
+  if (dec_tc(d)) {
+    const int KR = d.beam < 2 ? 2 : d.beam;
+    s.wgT = (float*)take(4 * G * (E + H));
+    s.bg = (float*)take(4 * G);
+    s.woT = (float*)take(4 * (size_t)dec_vp((int)V) * H);
+    s.bo = (float*)take(4 * (size_t)dec_vp((int)V));
+    s.part = (float*)take(4 * R * dec_ntn((int)V) * kDecEW * (2 + 2 * KR));
+  }
   if (st) *st = s;
   return off;
 }
@@ -508,9 +719,56 @@ extern "C" int64_t skb_decode_margin_offset(const skb_decode_shape* d) {
 namespace {
 
 // One decode step on stream `cs` (kernels read the step index from st.tstep).
+// The TF32 LSTM step on the engine: gather, gate GEMM + fused cell, logits GEMM + fused
+// log-softmax / top-K partials, merge, choose, advance.
+template <int K>
+bool enqueue_step_tc(const skb_decode_shape* d, DecodeState& st, cudaStream_t cs, const float* emb, const float* b_out,
+                     cudaGraphConditionalHandle cond, int use_cond, int prof_step) {
+  namespace gm = skb::gemm;
+  constexpr int KR = K < 2 ? 2 : K;
+  const int S = d->sentences, R = S * K, E = d->embed, H = d->hidden, V = d->vocab, G = 4 * H, LT = d->max_len + 1;
+  const int Vp = dec_vp(V), ntn = dec_ntn(V), KG = E + H;
+  prof_mark(prof_step, 0, cs);
+  dec_gather4<<<dim3((KG / 4 + 127) / 128, R), 128, 0, cs>>>(st, emb, R, E, H);
+  prof_mark(prof_step, 1, cs);
+  CUtensorMap ma, mb, ml, mo;
+  if (!gm::encode_2d(&ma, gm::kTF32, st.xh, KG, R, KG, 32, 128) ||
+      !gm::encode_2d(&mb, gm::kTF32, st.wgT, KG, G, KG, 32, kCellBN) ||
+      !gm::encode_2d(&ml, gm::kTF32, st.hn, H, R, H, 32, 128) ||
+      !gm::encode_2d(&mo, gm::kTF32, st.woT, H, Vp, H, 32, kDecBN))
+    return false;
+  {
+    EpiDecCell e;
+    e.st = st; e.H = H;
+    gm::Shape sh{R, G, KG, 1, 0};
+    if (gm::launch<gm::kTF32, kCellBN, false, false, EpiDecCell, false, 2>(ma, mb, sh, e, cs)) return false;
+  }
+  prof_mark(prof_step, 2, cs);
+  {
+    EpiLogits<KR> e;
+    e.st = st; e.b_out = b_out; e.V = V; e.ntn = ntn; e.R = R;
+    gm::Shape sh{R, Vp, H, 1, 0};
+    if (gm::launch<gm::kTF32, kDecBN, false, false, EpiLogits<KR>, false, kDecEW>(ml, mo, sh, e, cs)) return false;
+  }
+  prof_mark(prof_step, 3, cs);
+  dec_merge<KR><<<(R + 7) / 8, 256, 0, cs>>>(st, R, ntn);
+  beam_choose<K><<<S, SEL_THREADS, 0, cs>>>(st, S, V, H, LT, d->eos);
+  prof_mark(prof_step, 4, cs);
+  dec_advance<<<1, 1, 0, cs>>>(st, d->max_len, cond, use_cond);
+  return cudaPeekAtLastError() == cudaSuccess;
+}
+
 bool enqueue_step(const skb_decode_shape* d, DecodeState& st, cublasHandle_t hb, cudaStream_t cs, const float* emb,
                   const float* w_gates, const float* b_gates, const float* w_out, const float* b_out,
                   cudaGraphConditionalHandle cond, int use_cond, int prof_step) {
+  if (dec_tc(*d)) {
+    switch (d->beam) {
+#define SKB_TC(k) case k: return enqueue_step_tc<k>(d, st, cs, emb, b_out, cond, use_cond, prof_step);
+      SKB_TC(1) SKB_TC(2) SKB_TC(3) SKB_TC(4) SKB_TC(5) SKB_TC(6) SKB_TC(7) SKB_TC(8)
+#undef SKB_TC
+    }
+    return false;
+  }
   const int S = d->sentences, K = d->beam, R = S * K, E = d->embed, H = d->hidden, V = d->vocab;
   const int G = d->cell == SKB_CELL_LSTM ? 4 * H : H, LT = d->max_len + 1;
   const int rows = R < 148 * 8 ? R : 148 * 8;
@@ -626,6 +884,11 @@ extern "C" skb_status skb_decode(const skb_decode_shape* d, const float* h0, con
   static int32_t* host_word = nullptr;   // pinned poll / result word, allocated once
   if (!host_word && cudaMallocHost(&host_word, sizeof(int32_t) * 2) != cudaSuccess) return SKB_ERR_CUDA;
   dec_init<<<148 * 8, 256, 0, cs>>>(st, h0, c0, S, K, H, LT, d->max_len);
+  if (dec_tc(*d)) {   // engine operands: K-major, gate-interleaved weights
+    dec_prep_gates<<<148 * 8, 256, 0, cs>>>(w_gates, b_gates, st.wgT, st.bg, d->embed + H, H);
+    const int Vp = dec_vp(d->vocab);
+    dec_prep_out<<<dim3((Vp + 31) / 32, (H + 31) / 32), dim3(32, 8), 0, cs>>>(w_out, b_out, st.woT, st.bo, H, d->vocab, Vp);
+  }
   cudaGraphExec_t exec = nullptr;
   if (d->max_len > 0 && !g_dprof && d->poll >= 0)
     exec = decode_graph(d, st, hb, workspace, emb, w_gates, b_gates, w_out, b_out);

@@ -115,6 +115,7 @@ SKB_DEV void tile_coords(int u, int tiles_n, int ksplit, int& tm, int& tn, int& 
 
 // Epilogue functor contract (const: the functor is a __grid_constant__ kernel parameter,
 // so tensor maps it holds are usable by TMA; per-thread state lives in Epi::State):
+//   skip()                    true: the whole grid exits at once (checked before any setup)
 //   kOpBytes                  shared-memory bytes of per-tile epilogue operands (0: none)
 //   prefetch(sop, tm, tn, bar) producer thread: TMA loads of the tile's operands into sop
 //                             (completion counted on bar; issued before the tile's K loop,
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_kernel(const __grid_con
                                                       const __grid_constant__ CUtensorMap tmA2, const Shape sh,
                                                       const __grid_constant__ Epi epi) {
   using G = Geo<ELEM, BN, Epi::kOpBytes>;
+  if (epi.skip()) return;   // device-side predicate (e.g. a decode loop that has finished)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sop = smem + G::S * G::STAGE;   // epilogue operands (1024-aligned: STAGE is)
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_kernel(const __grid_con
         tile_coords(u, tiles_n, sh.ksplit, tm, tn, ks);
         const int kb0 = (int)((long long)kblocks * ks / sh.ksplit), kb1 = (int)((long long)kblocks * (ks + 1) / sh.ksplit);
         if constexpr (Epi::kOpBytes > 0) {   // the tile's epilogue operands, behind its MMAs
-          mbar_wait(&opfree, oph ^ 1);
+          mbar_wait_sleep(&opfree, oph ^ 1);
           if (epi.ops_on()) {
             mbar_arrive_expect_tx(&opfull, Epi::kOpBytes);
             epi.prefetch(sop, tm, tn, &opfull);
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_kernel(const __grid_con
           oph ^= 1;
         }
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], ph ^ 1);
+          mbar_wait_sleep(&empty[stage], ph ^ 1);
           mbar_arrive_expect_tx(&full[stage], G::STAGE);
           uint8_t* sa = smem + stage * G::STAGE;
           uint8_t* sb = sa + G::A_BYTES;
@@ -217,11 +219,11 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_kernel(const __grid_con
         int tm, tn, ks;
         tile_coords(u, tiles_n, sh.ksplit, tm, tn, ks);
         const int kb0 = (int)((long long)kblocks * ks / sh.ksplit), kb1 = (int)((long long)kblocks * (ks + 1) / sh.ksplit);
-        mbar_wait(&tempty[acc], aph ^ 1);
+        mbar_wait_sleep(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], ph);
+          mbar_wait_sleep(&full[stage], ph);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * G::STAGE), sb = sa + G::A_BYTES;
 #pragma unroll
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_kernel(const __grid_con
       epi.begin_tile(st, tm, tn, ks, m);
       mbar_wait_sleep(&tfull[acc], aph);
       tc_fence_after();
-      if constexpr (Epi::kOpBytes > 0) mbar_wait(&opfull, oph);
+      if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
       const int kb0 = (int)((long long)kblocks * ks / sh.ksplit), kb1 = (int)((long long)kblocks * (ks + 1) / sh.ksplit);
       const bool empty_k = kb1 <= kb0;   // no MMA ran: the accumulator is stale, the tile is zero
 #pragma unroll 1
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
       for (int st = 0; st < sh.steps; ++st) {
         if (st > 0) {   // every tile of step st - 1 stored: A_st (and this CTA's state) is ready
           const int want = st * per_step;
-          while (ld_acquire_gpu_s32(sh.sync) < want) __nanosleep(32);
+          while (ld_acquire_gpu_s32(sh.sync) < want) __nanosleep(64);
           fence_proxy_async_global();
         }
         const int ac = epi.a_coord(st);
@@ -357,14 +359,14 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
         for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
           const int tm = u / tiles_n, tn = u % tiles_n;
           if constexpr (Epi::kOpBytes > 0) {
-            mbar_wait(&opfree, oph ^ 1);
+            mbar_wait_sleep(&opfree, oph ^ 1);
             mbar_arrive_expect_tx(&opfull, Epi::kOpBytes);
             epi.prefetch(sop, st, tm, tn, &opfull);
             oph ^= 1;
           }
           if (kz) continue;
           for (int kb = 0; kb < kblocks; ++kb) {
-            mbar_wait(&empty[stage], ph ^ 1);
+            mbar_wait_sleep(&empty[stage], ph ^ 1);
             mbar_arrive_expect_tx(&full[stage], G::STAGE);
             uint8_t* sa = smem + stage * G::STAGE;
             tma_load_3d(sa, &tmA, kb * G::BK, tm * G::BM, ac, &full[stage]);
@@ -383,12 +385,12 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
       for (int st = 0; st < sh.steps; ++st) {
         const bool kz = epi.k_empty(st);
         for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
-          mbar_wait(&tempty[acc], aph ^ 1);
+          mbar_wait_sleep(&tempty[acc], aph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + acc * BN;
           if (!kz) {
             for (int kb = 0; kb < kblocks; ++kb) {
-              mbar_wait(&full[stage], ph);
+              mbar_wait_sleep(&full[stage], ph);
               tc_fence_after();
               const uint32_t sa = smem_u32(smem + stage * G::STAGE), sb = sa + G::A_BYTES;
 #pragma unroll
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
         epi.begin_tile(es, st, tm, tn, m);
         mbar_wait_sleep(&tfull[acc], aph);
         tc_fence_after();
-        if constexpr (Epi::kOpBytes > 0) mbar_wait(&opfull, oph);
+        if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
 #pragma unroll 1
         for (int c = cg0; c < cg0 + BN / EW; c += 16) {
           float v[16];
@@ -466,6 +468,7 @@ struct EpiStore {
   long long ldc;
   long long split_stride;
   int beta;
+  SKB_DEV bool skip() const { return false; }
   SKB_DEV bool ops_on() const { return false; }
   SKB_DEV void prefetch(uint8_t*, int, int, uint64_t*) const {}
   SKB_DEV void begin_tile(State&, int, int, int, int) const {}

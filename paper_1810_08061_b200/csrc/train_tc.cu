@@ -334,6 +334,7 @@ struct EpiGrad {
   struct State {};
   float *dW, *dU, *db;
   int F, H;
+  SKB_DEV bool skip() const { return false; }
   SKB_DEV bool ops_on() const { return false; }
   SKB_DEV void prefetch(uint8_t*, int, int, uint64_t*) const {}
   SKB_DEV void begin_tile(State&, int, int, int, int) const {}

@@ -98,6 +98,30 @@ def test_full_size_beam8_matches_oracle():
     assert np.allclose(s_got, s_ref, rtol=1e-4, atol=1e-4), np.max(np.abs(s_got - s_ref))
 
 
+@pytest.mark.parametrize("S,V,E,H,K,T,seed", [
+    (4, 1000, 128, 128, 4, 8, 5),
+    (2, 2000, 128, 128, 4, 6, 2),
+    (4, 500, 64, 64, 4, 8, 4),
+    (2, 4096, 128, 128, 2, 6, 1),
+])
+@pytest.mark.parametrize("engine", ["1", "0"])
+def test_tf32_paths_match_oracle(S, V, E, H, K, T, seed, engine, monkeypatch):
+    """TF32 LSTM decoding, both paths: skb's tcgen05 engine (SKB_DEC_TC=1: gate GEMM + fused
+    cell, logits GEMM + fused log-softmax / top-K partials) and the library GEMMs + beam_rows
+    (default).  Cases whose oracle K-th-choice margins all exceed 3e-2 (TF32 logit error
+    ~3e-3): tokens and lengths exact, scores within 5e-3."""
+    monkeypatch.setenv("SKB_DEC_TC", engine)
+    h0, c0, emb, w = _lstm_problem(S, V, E, H, seed, 2, 4.0)
+    ref = obeam.decode("lstm", h0, emb, w, K, 2, T, c0=c0)
+    assert min(ref["margins"] or [1.0]) > 3e-2
+    got = decode("lstm", h0, emb, w, K, 2, T, c0=c0, math="tf32")
+    steps = ref["steps"]
+    assert got["steps"] == steps
+    assert np.array_equal(got["tokens"].cpu().numpy()[:, :, :steps + 1], ref["tokens"][:, :, :steps + 1])
+    assert np.array_equal(got["lengths"].cpu().numpy(), ref["lengths"])
+    assert np.allclose(got["scores"].cpu().numpy().astype(np.float64), ref["scores"], rtol=5e-3, atol=5e-3)
+
+
 def test_full_size_beam8_properties():
     """BASELINE C3 shape (beam 8, vocab 32k, H=512) on TF32 tensor cores."""
     S, V, E, H, K, T = 16, 32000, 512, 512, 8, 12
