@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_kernel(const __grid_con
 // epilogue warp publishes its tile with a fence + gpu-scope release add on `sync`; the
 // producer acquires the count, orders its bulk reads after it with a proxy fence.
 // Epi contract as above plus a_coord(s), k_empty(s) (no MMA at step s: D = 0) and the
-// step index in begin_tile / chunk / end_tile / prefetch.
+// step index in begin_tile / chunk / end_tile / prefetch.  prefetch(st) may only read
+// inputs and state written by this CTA's own epilogue (it is issued before the barrier).
 SKB_DEV void tma_load_3d(void* smem_dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                :: "r"(smem_u32(smem_dst)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
@@ -308,15 +309,26 @@ SKB_DEV int ld_acquire_gpu_s32(const int* p) {
 struct StepShape {
   int M, N, K;
   int steps;
-  int* sync;    // zeroed before the launch
+  int* sync;      // zeroed before the launch
+  float* xbuf;    // KS = 2: [tiles][2 halves][128 rows][BN / 2] fp32 partial-sum exchange (L2)
+  int* xflag;     // KS = 2: [tiles][2] publication counters, zeroed before the launch
 };
 
-template <int ELEM, int BN, class Epi, int EW>
+// KS = 2: every output tile is computed by two CTAs, each over half of K (fewer, wider
+// tiles for the same CTA count: the activations / weights are re-read by fewer tiles).
+// The partial sums are exchanged through L2: each CTA publishes the half of its
+// accumulator columns that its partner finishes, and runs the epilogue on the other
+// half (the epilogue functor sees tiles of BN / 2 columns, tile index 2 tn + ks).
+// Step st + 1 arms its first stages with the weight (B) k-blocks before the grid
+// barrier; the activation (A) halves follow once the barrier is passed.
+template <int ELEM, int BN, class Epi, int EW, int KS = 1>
 __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                      const __grid_constant__ CUtensorMap tmB,
                                                                      const StepShape sh,
                                                                      const __grid_constant__ Epi epi) {
   using G = Geo<ELEM, BN, Epi::kOpBytes>;
+  constexpr int BNE = BN / KS;   // epilogue columns per CTA
+  static_assert((BNE / EW) % 16 == 0, "epilogue column groups are multiples of 16");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sop = smem + G::S * G::STAGE;
@@ -325,8 +337,8 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_n = (sh.N + BN - 1) / BN;
   const int kblocks = (sh.K + G::BK - 1) / G::BK;
-  const int ntiles = ((sh.M + G::BM - 1) / G::BM) * tiles_n;
-  const int per_step = ntiles * 4 * EW;   // barrier arrivals per step (every epilogue warp of every tile)
+  const int nunits = ((sh.M + G::BM - 1) / G::BM) * tiles_n * KS;
+  const int per_step = nunits * 4 * EW;   // barrier arrivals per step (every epilogue warp of every unit)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < G::S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -349,23 +361,46 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
       int stage = 0;
       uint32_t ph = 0, oph = 0;
       for (int st = 0; st < sh.steps; ++st) {
-        if (st > 0) {   // every tile of step st - 1 stored: A_st (and this CTA's state) is ready
-          const int want = st * per_step;
-          while (ld_acquire_gpu_s32(sh.sync) < want) __nanosleep(64);
-          fence_proxy_async_global();
-        }
         const int ac = epi.a_coord(st);
         const bool kz = epi.k_empty(st);
-        for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
-          const int tm = u / tiles_n, tn = u % tiles_n;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+          const int t = u / KS, ks = u % KS, tm = t / tiles_n, tn = t % tiles_n;
+          const int kb0 = kblocks * ks / KS, kb1 = kblocks * (ks + 1) / KS;
+          const bool first = u == (int)blockIdx.x;
+          // weights first: they do not depend on step st - 1
+          int npre = 0;
+          const int s0 = stage;
+          if (st > 0 && first && !kz) {
+            npre = min(G::S, kb1 - kb0);
+            for (int i = 0; i < npre; ++i) {
+              mbar_wait_sleep(&empty[stage], ph ^ 1);
+              mbar_arrive_expect_tx(&full[stage], G::STAGE);
+              tma_load_2d(smem + stage * G::STAGE + G::A_BYTES, &tmB, (kb0 + i) * G::BK, tn * BN, &full[stage]);
+              if (++stage == G::S) { stage = 0; ph ^= 1; }
+            }
+          }
           if constexpr (Epi::kOpBytes > 0) {
+            // the epilogue operands depend only on this CTA's own previous epilogue (its state
+            // slice; opfree is arrived after its stores) and on inputs: no grid barrier needed
             mbar_wait_sleep(&opfree, oph ^ 1);
+            fence_proxy_async_global();
             mbar_arrive_expect_tx(&opfull, Epi::kOpBytes);
-            epi.prefetch(sop, st, tm, tn, &opfull);
+            epi.prefetch(sop, st, tm, tn * KS + ks, &opfull);
             oph ^= 1;
           }
+          if (st > 0 && first) {   // every unit of step st - 1 stored: A_st is ready
+            const int want = st * per_step;
+            while (ld_acquire_gpu_s32(sh.sync) < want) __nanosleep(64);
+            fence_proxy_async_global();
+          }
           if (kz) continue;
-          for (int kb = 0; kb < kblocks; ++kb) {
+          for (int kb = kb0; kb < kb1; ++kb) {
+            const int i = kb - kb0;
+            if (i < npre) {   // stage armed before the barrier: only its A half is missing
+              const int sidx = (s0 + i) % G::S;
+              tma_load_3d(smem + sidx * G::STAGE, &tmA, kb * G::BK, tm * G::BM, ac, &full[sidx]);
+              continue;
+            }
             mbar_wait_sleep(&empty[stage], ph ^ 1);
             mbar_arrive_expect_tx(&full[stage], G::STAGE);
             uint8_t* sa = smem + stage * G::STAGE;
@@ -384,19 +419,21 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
       uint32_t ph = 0, aph = 0;
       for (int st = 0; st < sh.steps; ++st) {
         const bool kz = epi.k_empty(st);
-        for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+          const int ks = u % KS;
+          const int kb0 = kblocks * ks / KS, kb1 = kblocks * (ks + 1) / KS;
           mbar_wait_sleep(&tempty[acc], aph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + acc * BN;
           if (!kz) {
-            for (int kb = 0; kb < kblocks; ++kb) {
+            for (int kb = kb0; kb < kb1; ++kb) {
               mbar_wait_sleep(&full[stage], ph);
               tc_fence_after();
               const uint32_t sa = smem_u32(smem + stage * G::STAGE), sb = sa + G::A_BYTES;
 #pragma unroll
               for (int k = 0; k < G::BK / G::UK; ++k)
                 umma_ss<ELEM>(d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), id,
-                              (kb > 0 || k > 0) ? 1u : 0u);
+                              (kb > kb0 || k > 0) ? 1u : 0u);
               umma_commit(&empty[stage]);
               if (++stage == G::S) { stage = 0; ph ^= 1; }
             }
@@ -408,30 +445,59 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
     }
   } else {
     // ===================== epilogue warps
-    static_assert((BN / EW) % 16 == 0, "epilogue column groups are multiples of 16");
-    const int q = warp & 3, r = q * 32 + lane, cg0 = ((warp - 2) >> 2) * (BN / EW);
+    const int q = warp & 3, r = q * 32 + lane, cg0 = ((warp - 2) >> 2) * (BNE / EW);
     int acc = 0;
     uint32_t aph = 0, oph = 0;
     for (int st = 0; st < sh.steps; ++st) {
       const bool kz = epi.k_empty(st);
-      for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
-        const int tm = u / tiles_n, tn = u % tiles_n;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int t = u / KS, ks = u % KS, tm = t / tiles_n, tn = t % tiles_n, tv = tn * KS + ks;
         const int m = tm * G::BM + r;
         typename Epi::State es;
-        epi.begin_tile(es, st, tm, tn, m);
+        epi.begin_tile(es, st, tm, tv, m);
         mbar_wait_sleep(&tfull[acc], aph);
         tc_fence_after();
+        const uint32_t dacc = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
+        if constexpr (KS == 2) {   // publish the partner's half of the partial sums
+          if (!kz) {   // (a step without MMAs still counts: the counters advance every step)
+            float* xo = sh.xbuf + (((long long)t * 2 + (ks ^ 1)) * 128 + r) * BNE;
+#pragma unroll 1
+            for (int c = cg0; c < cg0 + BNE / EW; c += 16) {
+              float v[16];
+              tmem_ld16(dacc + (ks ^ 1) * BNE + c, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 16; i += 4)
+                __stcg(reinterpret_cast<float4*>(xo + c + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+            }
+            __threadfence();
+          }
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(sh.xflag + t * 2 + ks), "r"(1) : "memory");
+            const int want = (st + 1) * 4 * EW;
+            while (ld_acquire_gpu_s32(sh.xflag + t * 2 + (ks ^ 1)) < want) __nanosleep(32);
+          }
+          __syncwarp();
+        }
         if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
 #pragma unroll 1
-        for (int c = cg0; c < cg0 + BN / EW; c += 16) {
+        for (int c = cg0; c < cg0 + BNE / EW; c += 16) {
           float v[16];
-          tmem_ld16(tmem + acc * BN + c + ((uint32_t)(q * 32) << 16), v);
+          tmem_ld16(dacc + ks * BNE + c, v);
           tmem_ld_wait();
           if (kz) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          } else if constexpr (KS == 2) {
+            const float* xi = sh.xbuf + (((long long)t * 2 + ks) * 128 + r) * BNE + c;
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              const float4 p = __ldcg(reinterpret_cast<const float4*>(xi + i));
+              v[i] += p.x; v[i + 1] += p.y; v[i + 2] += p.z; v[i + 3] += p.w;
+            }
           }
-          const int n0 = tn * BN + c;
+          const int n0 = tn * BN + ks * BNE + c;
           if (n0 < sh.N) epi.chunk(es, sop, st, r, m, n0, c, v, m < sh.M);
         }
         tc_fence_before();
@@ -441,7 +507,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
           if constexpr (Epi::kOpBytes > 0) mbar_arrive(&opfree);
         }
         oph ^= 1;
-        epi.end_tile(es, st, tm, tn, warp - 2, lane);
+        epi.end_tile(es, st, tm, tv, warp - 2, lane);
         // publish this warp's stores of step st (the next step's A operand / state)
         __threadfence();
         __syncwarp();
@@ -553,24 +619,25 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Shape& sh, const 
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, ta2 ? *ta2 : ta, sh, epi) == cudaSuccess ? 0 : 2;
 }
 
-// Cooperative launch of gemm_steps_kernel: one CTA per tile, all resident.
-template <int ELEM, int BN, class Epi, int EW>
+// Cooperative launch of gemm_steps_kernel: one CTA per unit (tile x K half), all resident.
+template <int ELEM, int BN, class Epi, int EW, int KS = 1>
 int launch_steps(const CUtensorMap& ta, const CUtensorMap& tb, const StepShape& sh, const Epi& epi, cudaStream_t st) {
   using G = Geo<ELEM, BN, Epi::kOpBytes>;
-  auto kern = gemm_steps_kernel<ELEM, BN, Epi, EW>;
+  auto kern = gemm_steps_kernel<ELEM, BN, Epi, EW, KS>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess)
       return 2;
     attr = true;
   }
-  const int ntiles = ((sh.M + G::BM - 1) / G::BM) * ((sh.N + BN - 1) / BN);
-  if (ntiles > num_sms()) return 3;   // one resident CTA per tile
+  const int nunits = ((sh.M + G::BM - 1) / G::BM) * ((sh.N + BN - 1) / BN) * KS;
+  if (nunits > num_sms()) return 3;   // one resident CTA per unit
+  if (KS == 2 && (!sh.xbuf || !sh.xflag)) return 3;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute lattr[1];
   lattr[0].id = cudaLaunchAttributeCooperative;
   lattr[0].val.cooperative = 1;
-  cfg.gridDim = dim3(ntiles);
+  cfg.gridDim = dim3(nunits);
   cfg.blockDim = dim3(64 + 128 * EW);
   cfg.dynamicSmemBytes = G::SMEM;
   cfg.stream = st;

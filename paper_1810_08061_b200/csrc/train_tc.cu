@@ -44,6 +44,8 @@ struct Bufs {
   double* lpart;   // [T][fwd tiles][epilogue warps]
   double* lsum;    // [T] per-step loss sums
   int* sync;       // [2] grid-barrier counters of the forward / backward launches
+  float* xbuf;     // split-K partial-sum exchange of the step kernels (KS = 2)
+  int* xflag;      // [2][tiles][2] its publication counters (forward, backward)
 };
 
 inline int kx_of(int F, int H) { return F + 16 + H; }
@@ -71,6 +73,8 @@ size_t layout(int B, int T, int F, int H, uint8_t* base, Bufs* w) {
   s.lpart = (double*)take(8ull * T * fwd_tiles(B, H) * kFwdSlots);
   s.lsum = (double*)take(8ull * T);
   s.sync = (int*)take(8);
+  s.xbuf = (float*)take(4ull * ((B + 127) / 128) * (G / 256 + 1) * 2 * 128 * 128);
+  s.xflag = (int*)take(4ull * 2 * ((B + 127) / 128) * (G / 64 + 1) * 2);
   if (w) *w = s;
   return off;
 }
@@ -100,27 +104,31 @@ SKB_DEV float2 unpack_h2(uint32_t u) {
 // XH rows: [bf16(x) | 1 | 0 | h part: bf16(h0) at t = 0, else 0 (rewritten by the forward)]
 __global__ void prep_xh(const float* __restrict__ x, const float* __restrict__ h0, __nv_bfloat16* __restrict__ XH,
                         int B, int T, int F, int H) {
-  const int KX = F + 16 + H, KX2 = KX / 2;
-  const long long pairs = (long long)B * T * KX2;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += (long long)gridDim.x * blockDim.x) {
-    const long long row = i / KX2;   // time-major row t B + b
-    const int c = (int)(i % KX2) * 2;
+  // eight columns per thread (F % 8 == 0: a group never straddles the x / ones / h parts),
+  // two 16-byte loads of x, one 16-byte store of XH
+  const int KX = F + 16 + H, KX8 = KX / 8;
+  const long long groups = (long long)B * T * KX8;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < groups; i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / KX8;   // time-major row t B + b
+    const int c = (int)(i % KX8) * 8;
     const int t = (int)(row / B), b = (int)(row % B);
-    float v0, v1;
+    float v[8];
     if (c < F) {
-      const float2 xv = *reinterpret_cast<const float2*>(x + ((long long)b * T + t) * F + c);
-      v0 = xv.x; v1 = xv.y;
+      const float4* xp = reinterpret_cast<const float4*>(x + ((long long)b * T + t) * F + c);
+      const float4 a = __ldcs(xp), e = __ldcs(xp + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = e.x; v[5] = e.y; v[6] = e.z; v[7] = e.w;
     } else if (c < F + 16) {
-      v0 = c == F ? 1.f : 0.f;
-      v1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = (c + k == F) ? 1.f : 0.f;
     } else if (t == 0 && h0) {
-      const int k = c - F - 16;
-      v0 = h0[(long long)b * H + k];
-      v1 = h0[(long long)b * H + k + 1];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = h0[(long long)b * H + c - F - 16 + k];
     } else {
-      v0 = v1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = 0.f;
     }
-    *reinterpret_cast<uint32_t*>(XH + row * KX + c) = pack_bf2(v0, v1);
+    *reinterpret_cast<uint4*>(XH + row * KX + c) =
+        make_uint4(pack_bf2(v[0], v[1]), pack_bf2(v[2], v[3]), pack_bf2(v[4], v[5]), pack_bf2(v[6], v[7]));
   }
 }
 
@@ -349,6 +357,20 @@ struct EpiGrad {
   SKB_DEV void end_tile(State&, int, int, int, int, int) const {}
 };
 
+// Split-K mode of the step kernels (SKB_TC_FWD_KS / SKB_TC_BWD_KS = 1 or 2).  Forward
+// default 1: 256-column split-K tiles measured slower (30.1 vs 27.6 ms per C2 step: only 3
+// pipeline stages fit beside the epilogue operands).
+int fwd_ks() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("SKB_TC_FWD_KS"); v = e ? atoi(e) : 1; }
+  return v;
+}
+int bwd_ks() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("SKB_TC_BWD_KS"); v = e ? atoi(e) : 2; }
+  return v;
+}
+
 int diag() {
   static int v = -1;
   if (v < 0) { const char* e = getenv("SKB_TC_DIAG"); v = e ? atoi(e) : 0; }
@@ -409,28 +431,45 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
       !gm::encode_3d(&mdG, kBF16, w.dG, G, B, T, G, (uint64_t)B * G, 64, 128, 1) ||
       !gm::encode_3d(&mRec, kBF16, w.Rec, (uint64_t)H * 8, B, T, (uint64_t)H * 8, (uint64_t)B * H * 8, 64, 128, 1))
     return SKB_ERR_INVALID;
+  const int tm_ = (B + 127) / 128;
+  const size_t nflag = (size_t)tm_ * (G / 64 + 1) * 2;
   cudaMemsetAsync(w.sync, 0, 8, cs);
+  cudaMemsetAsync(w.xflag, 0, 4 * 2 * nflag, cs);
   {
     EpiFwd e;
     e.mC = mC; e.mH = mH; e.mY = mY;
     e.lens = lens; e.hcur = w.hcur; e.ccur = w.ccur; e.XH = w.XH; e.Rec = w.Rec; e.lpart = w.lpart;
     e.T = T; e.F = F; e.H = H; e.B = B; e.tiles_n = tiles_n; e.tiles = fwd_tiles(B, H); e.diag = diag();
-    gm::StepShape sh{B, G, KX, n, w.sync};
-    if (int rc = gm::launch_steps<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXH, mWU, sh, e, cs))
-      return rc == 3 ? SKB_ERR_UNSUPPORTED : SKB_ERR_CUDA;
+    gm::StepShape sh{B, G, KX, n, w.sync, w.xbuf, w.xflag};
+    int rc;
+    if (fwd_ks() == 2 && (G % 256) == 0) {   // 256-column tiles, each computed by two CTAs over K halves
+      CUtensorMap mWU2;
+      if (!gm::encode_2d(&mWU2, kBF16, w.WU, KX, G, KX, GF::BK, 256)) return SKB_ERR_INVALID;
+      rc = gm::launch_steps<kBF16, 256, EpiFwd, kFwdEW, 2>(mXH, mWU2, sh, e, cs);
+    } else {
+      rc = gm::launch_steps<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXH, mWU, sh, e, cs);
+    }
+    if (rc) return rc == 3 ? SKB_ERR_UNSUPPORTED : SKB_ERR_CUDA;
   }
   loss_step_sums<<<n, 256, 0, cs>>>(w.lpart, fwd_tiles(B, H) * kFwdSlots, w.lsum);
   loss_final_sum<<<1, 256, 0, cs>>>(w.lsum, n, d->inv_batch, loss);
 
-  // backward: one persistent launch; dh = dG[t+1] Ut^T, 32-unit tiles
+  // backward: one persistent launch; dh = dG[t+1] Ut^T
   {
     EpiBwd e;
     e.mDh = mDh; e.mDc = mDc; e.mY = mY; e.mRec = mRec;
     e.lens = lens; e.dhc = w.dhc; e.dc = w.dc; e.dG = w.dG;
     e.n = n; e.T = T; e.H = H; e.B = B; e.inv_b = d->inv_batch; e.diag = diag();
-    gm::StepShape sh{B, H, G, n, w.sync + 1};
-    if (int rc = gm::launch_steps<kBF16, 32, EpiBwd, 2>(mdG, mUt, sh, e, cs))
-      return rc == 3 ? SKB_ERR_UNSUPPORTED : SKB_ERR_CUDA;
+    gm::StepShape sh{B, H, G, n, w.sync + 1, w.xbuf, w.xflag + nflag};
+    int rc;
+    if (bwd_ks() == 2 && (H % 64) == 0) {   // 64-unit tiles, each computed by two CTAs over K halves
+      CUtensorMap mUt2;
+      if (!gm::encode_2d(&mUt2, kBF16, w.Ut, G, H, G, 64, 64)) return SKB_ERR_INVALID;
+      rc = gm::launch_steps<kBF16, 64, EpiBwd, 2, 2>(mdG, mUt2, sh, e, cs);
+    } else {
+      rc = gm::launch_steps<kBF16, 32, EpiBwd, 2>(mdG, mUt, sh, e, cs);
+    }
+    if (rc) return rc == 3 ? SKB_ERR_UNSUPPORTED : SKB_ERR_CUDA;
   }
   // dG rows t >= n take no part in the step: zero for the weight-gradient GEMM (its K
   // runs over every (t, b)); XH's h part of rows t > n is zero from prep_xh
