@@ -18,10 +18,11 @@ tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 CONFIGS = [("c1", "C1 dynamic-length LSTM inference (headline)"), ("c2", "C2 LSTM training step"),
            ("c3", "C3 beam-search decoder"), ("c4", "C4 L-BFGS (vector-stream tier)"),
            ("c5", "C5 TreeLSTM"), ("c5m", "C5 MAML")]
-CAPTURES = [("rnn_fwd_kernel", "prof_rnn.ncu-rep", "C1: bench.py (default)"),
+CAPTURES = [("rnn_fwd_pair4_kernel", "prof_rnn.ncu-rep", "C1: bench.py --steps 1 --warmup 1 (launch 2)"),
+            ("gemm_steps_kernel<EpiBwd>", "prof_c2bwd.ncu-rep", "C2: bench.py --config c2, backward persistent step kernel"),
+            ("gemm_steps_kernel<EpiFwd>", "prof_c2fwd.ncu-rep", "C2: bench.py --config c2, forward persistent step kernel"),
             ("stream_kernel", "prof_stream.ncu-rep", "C4 tier: axpy probe n=1e7 x 20 (tools/stream_micro_one.py)"),
             ("beam_rows", "prof_beam_rows.ncu-rep", "C3: bench.py --config c3"),
-            ("lstm_bwd_cell", "prof_train_cell.ncu-rep", "C2: bench.py --config c2"),
             ("tree_cell", "prof_tree_cell.ncu-rep", "C5: bench.py --config c5"),
             ("maml_task_kernel", "prof_maml.ncu-rep", "C5 MAML: bench.py --config c5m")]
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -115,8 +116,17 @@ def main():
         md.append("")
     with open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w") as f:
         f.write("\n".join(md) + "\n")
-    with open(os.path.join(PROF, "ncu_summary.json"), "w") as f:
-        json.dump(summary, f, indent=1)
+    path = os.path.join(PROF, "ncu_summary.json")
+    old = json.load(open(path)) if os.path.exists(path) else {}
+    commit = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True,
+                            cwd=REPO).stdout.strip()
+    for k, v in summary.items():
+        v["commit"] = commit
+        if k == "rnn_fwd_pair4_kernel":
+            v["problems"] = 1152
+        old[k] = v
+    with open(path, "w") as f:
+        json.dump(old, f, indent=1)
     print("\n".join(md))
 
 
