@@ -378,6 +378,15 @@ skb_status skb_gemm(int elem, int a_mn, int b_mn, int M, int N, int K, const voi
                     const void* B, int64_t ldb, float* C, int64_t ldc, int beta, int bn, int ksplit,
                     void* workspace, void* stream);
 
+
+/* Host-to-device copy of the valid prefix of each row of a [rows, T, step] PINNED host
+ * array: row r moves min(max(lens[r], 0), T) * step_bytes bytes, read by a device-pull
+ * gather kernel on `stream` (lens_dev: the device copy of the row lengths).  Used by the
+ * host-to-host C1 pipeline: the padded timesteps of a dynamic-length batch are never read
+ * by the kernels.  SKB_ERR_INVALID for pageable memory (the caller copies the block). */
+int skb_h2d_rows(void* dst_dev, const void* src_host, int64_t row_bytes, const int64_t* lens_dev,
+                 int64_t rows, int64_t step_bytes, int T, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,9 +74,14 @@ inline int dec_ntn(int V) { return (dec_vp(V) + kDecBN - 1) / kDecBN; }
 // the 1-CTA 128x256 tcgen05 tiles run the logits GEMM at ~350 TFLOP/s vs CUTLASS's 2-SM
 // 256x256 at ~600, and the per-row top-K insertion in the epilogue costs more than the
 // logits round trip it removes), so it is opt-in (profiles/r02_c3_engine.md).
+// The workspace holds the engine path's buffers whenever the shape is eligible, so the
+// layout (sized once per Decoder) does not depend on the environment at call time.
+inline bool dec_tc_shape(const skb_decode_shape& d) {
+  return d.math == 1 && d.cell == SKB_CELL_LSTM && d.embed % 4 == 0 && d.hidden % 32 == 0;
+}
 inline bool dec_tc(const skb_decode_shape& d) {
   const char* e = getenv("SKB_DEC_TC");
-  return e && atoi(e) == 1 && d.math == 1 && d.cell == SKB_CELL_LSTM && d.embed % 4 == 0 && d.hidden % 32 == 0;
+  return e && atoi(e) == 1 && dec_tc_shape(d);
 }
 
 __device__ __forceinline__ float sigmoidf_ref(float x) {   // reference tensor.py:403-407 (two branches)
@@ -659,7 +664,7 @@ size_t layout(const skb_decode_shape& d, DecodeState* st, uint8_t* base) {
   for (int k = 0; k < 2; ++k) { s.h[k] = (float*)take(4 * R * H); s.c[k] = (float*)take(4 * R * H); }
   s.hn = (float*)take(4 * R * H);
   s.cn = (float*)take(4 * R * H);
-  s.logits = dec_tc(d) ? nullptr : (float*)take(4 * R * V);   // the engine path never stores logits
+  s.logits = (float*)take(4 * R * V);
   for (int k = 0; k < 2; ++k) {
     s.score[k] = (double*)take(8 * R);
     s.fin[k] = (int32_t*)take(4 * R);
@@ -674,7 +679,7 @@ size_t layout(const skb_decode_shape& d, DecodeState* st, uint8_t* base) {
   s.row_lse = (float*)take(4 * R);
   s.margin = (float*)take(4 * R);
   s.wgT = s.bg = s.woT = s.bo = s.part = nullptr;
-  if (dec_tc(d)) {
+  if (dec_tc_shape(d)) {
     const int KR = d.beam < 2 ? 2 : d.beam;
     s.wgT = (float*)take(4 * G * (E + H));
     s.bg = (float*)take(4 * G);
@@ -807,6 +812,7 @@ bool enqueue_step(const skb_decode_shape* d, DecodeState& st, cublasHandle_t hb,
 struct GraphEntry {
   skb_decode_shape d;
   const void* ptrs[6];
+  int tc;   // captured on the engine path (SKB_DEC_TC) or the library path
   cudaGraphExec_t exec;
 };
 constexpr int kGraphCache = 16;
@@ -817,9 +823,10 @@ cudaGraphExec_t decode_graph(const skb_decode_shape* d, DecodeState& st, cublasH
                              const float* emb, const float* w_gates, const float* b_gates, const float* w_out,
                              const float* b_out) {
   const void* key[6] = {ws, emb, w_gates, b_gates, w_out, b_out};
+  const int tc = dec_tc(*d) ? 1 : 0;
   for (int i = 0; i < g_ngraphs; ++i) {
     GraphEntry& e = g_graphs[i];
-    if (memcmp(&e.d, d, sizeof(*d)) == 0 && memcmp(e.ptrs, key, sizeof(key)) == 0) return e.exec;
+    if (memcmp(&e.d, d, sizeof(*d)) == 0 && memcmp(e.ptrs, key, sizeof(key)) == 0 && e.tc == tc) return e.exec;
   }
   cudaGraph_t g = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -858,6 +865,7 @@ cudaGraphExec_t decode_graph(const skb_decode_shape* d, DecodeState& st, cublasH
   GraphEntry& e = g_graphs[g_ngraphs++];
   e.d = *d;
   memcpy(e.ptrs, key, sizeof(key));
+  e.tc = tc;
   e.exec = exec;
   return exec;
 }

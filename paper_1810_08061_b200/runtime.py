@@ -108,6 +108,7 @@ SIGNATURES = {
     "skb_rnn_last_overlap": (ctypes.c_int, []),
     "skb_rnn_set_overlap": (ctypes.c_int, [ctypes.c_int]),
     "skb_gemm_workspace_bytes": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "skb_h2d_rows": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _VP]),
     "skb_gemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 _VP, ctypes.c_int64, _VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int,
                                 ctypes.c_int, ctypes.c_int, _VP, _VP]),
