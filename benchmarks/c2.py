@@ -85,8 +85,10 @@ def run(args, rank, world, local_rank, clocks_cls):
         dist.all_reduce(n_t, op=dist.ReduceOp.MAX)
     n = int(n_t.item())
     tr = LstmTrainer(F, H, ROWS, T, global_batch=ROWS * world, lr=0.01, math="bf16", seed=7, device=dev)
+    # the While trip count of each step is decided on the device (no host round trip);
+    # n (host) only sizes the FLOP count of the roofline below
     for _ in range(args.warmup):
-        tr.step(x, y, lens, max_len=n)
+        tr.step(x, y, lens)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -101,7 +103,7 @@ def run(args, rank, world, local_rank, clocks_cls):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        tr.forward_backward(x, y, lens, max_len=n)
+        tr.forward_backward(x, y, lens)
         b.record(stream)
         tr.sync.reduce_(tr.grads)   # NCCL allreduce behind the libskb C ABI (skb_comm_allreduce)
         from paper_1810_08061_b200 import runtime as rt
@@ -155,7 +157,7 @@ def run(args, rank, world, local_rank, clocks_cls):
         for k in range(count):
             j = k & 1
             comp.wait_event(ready)
-            loss = tr.step(*bufs[j], max_len=n)
+            loss = tr.step(*bufs[j])
             done[j] = torch.cuda.Event()
             done[j].record(comp)
             if k + 1 < count:

@@ -238,6 +238,9 @@ skb_status skb_lstm_train_step(const skb_train_shape* shape, const float* x_dev,
                                const int64_t* lens_dev, const float* h0_dev, const float* c0_dev,
                                const float* params_dev, float* grads_dev, float* loss_dev, int max_len,
                                void* workspace_dev, void* stream);
+/* 1 if skb_lstm_train_step runs on skb's tcgen05 engine for this shape (bf16 math); then
+ * max_len = -1 lets the device determine the While trip count (reduce_max of the lengths). */
+int skb_train_uses_engine(const skb_train_shape* shape);
 int skb_train_last_mode(void);   /* 1 = the last step replayed a CUDA graph */
 skb_status skb_sgd_update(float* params_dev, const float* grads_dev, int64_t n, float lr, void* stream);
 

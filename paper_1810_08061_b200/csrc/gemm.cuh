@@ -309,6 +309,7 @@ SKB_DEV int ld_acquire_gpu_s32(const int* p) {
 struct StepShape {
   int M, N, K;
   int steps;
+  const int* steps_dev;   // non-null: the step count is read from device memory (a device-side trip count)
   int* sync;      // zeroed before the launch
   float* xbuf;    // KS = 2: [tiles][2 halves][128 rows][BN / 2] fp32 partial-sum exchange (L2)
   int* xflag;     // KS = 2: [tiles][2] publication counters, zeroed before the launch
@@ -339,6 +340,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
   const int kblocks = (sh.K + G::BK - 1) / G::BK;
   const int nunits = ((sh.M + G::BM - 1) / G::BM) * tiles_n * KS;
   const int per_step = nunits * 4 * EW;   // barrier arrivals per step (every epilogue warp of every unit)
+  const int steps = sh.steps_dev ? *sh.steps_dev : sh.steps;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < G::S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -360,7 +362,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
     if (lane == 0) {
       int stage = 0;
       uint32_t ph = 0, oph = 0;
-      for (int st = 0; st < sh.steps; ++st) {
+      for (int st = 0; st < steps; ++st) {
         const int ac = epi.a_coord(st);
         const bool kz = epi.k_empty(st);
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
       constexpr uint32_t id = idesc(ELEM, G::BM, BN, false, false);
       int stage = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
-      for (int st = 0; st < sh.steps; ++st) {
+      for (int st = 0; st < steps; ++st) {
         const bool kz = epi.k_empty(st);
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
           const int ks = u % KS;
@@ -448,7 +450,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
     const int q = warp & 3, r = q * 32 + lane, cg0 = ((warp - 2) >> 2) * (BNE / EW);
     int acc = 0;
     uint32_t aph = 0, oph = 0;
-    for (int st = 0; st < sh.steps; ++st) {
+    for (int st = 0; st < steps; ++st) {
       const bool kz = epi.k_empty(st);
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int t = u / KS, ks = u % KS, tm = t / tiles_n, tn = t % tiles_n, tv = tn * KS + ks;

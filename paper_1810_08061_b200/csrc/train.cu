@@ -455,11 +455,18 @@ extern "C" int64_t skb_train_workspace_bytes(const skb_train_shape* d) {
 
 extern "C" int skb_train_last_mode(void) { return g_train_mode; }
 
+// 1: skb_lstm_train_step runs on the tcgen05 engine for this shape (and accepts max_len = -1,
+// the While trip count determined on the device: no host round trip per step).
+extern "C" int skb_train_uses_engine(const skb_train_shape* d) { return d && use_tc(d) ? 1 : 0; }
+
 extern "C" skb_status skb_lstm_train_step(const skb_train_shape* d, const float* x, const float* y,
                                           const int64_t* lens, const float* h0, const float* c0, const float* params,
                                           float* grads, float* loss, int max_len, void* workspace, void* stream) {
-  if (!d || d->rows < 1 || d->time < 1 || d->input < 1 || d->hidden < 1 || max_len < 0 || max_len > d->time)
+  // max_len < 0: the trip count is determined on the device (engine path only)
+  if (!d || d->rows < 1 || d->time < 1 || d->input < 1 || d->hidden < 1 || max_len > d->time ||
+      (max_len < 0 && !use_tc(d)))
     return SKB_ERR_INVALID;
+  if (max_len < 0) max_len = -1;
   cudaStream_t cs = (cudaStream_t)stream;
   const bool tc = use_tc(d);
   TrainBufs w;

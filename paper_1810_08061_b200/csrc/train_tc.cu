@@ -43,7 +43,7 @@ struct Bufs {
   float *hcur, *ccur, *dhc, *dc;
   double* lpart;   // [T][fwd tiles][epilogue warps]
   double* lsum;    // [T] per-step loss sums
-  int* sync;       // [2] grid-barrier counters of the forward / backward launches
+  int* sync;       // [2] grid-barrier counters of the forward / backward launches, [2] the trip count
   float* xbuf;     // split-K partial-sum exchange of the step kernels (KS = 2)
   int* xflag;      // [2][tiles][2] its publication counters (forward, backward)
 };
@@ -72,7 +72,7 @@ size_t layout(int B, int T, int F, int H, uint8_t* base, Bufs* w) {
   s.dc = (float*)take(4ull * B * H);
   s.lpart = (double*)take(8ull * T * fwd_tiles(B, H) * kFwdSlots);
   s.lsum = (double*)take(8ull * T);
-  s.sync = (int*)take(8);
+  s.sync = (int*)take(16);
   s.xbuf = (float*)take(4ull * ((B + 127) / 128) * (G / 256 + 1) * 2 * 128 * 128);
   s.xflag = (int*)take(4ull * 2 * ((B + 127) / 128) * (G / 64 + 1) * 2);
   if (w) *w = s;
@@ -169,10 +169,40 @@ __global__ void init_state(const float* __restrict__ h0, const float* __restrict
   }
 }
 
+// The While trip count n = clamp(reduce_max(lens), 0, T) on the device (given >= 0: that
+// value), so a training step makes no host round trip.  One block.
+__global__ void trip_count(const int64_t* __restrict__ lens, int B, int T, int given, int* __restrict__ n_out) {
+  __shared__ int red[256];
+  long long m = 0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) m = lens[b] > m ? lens[b] : m;
+  red[threadIdx.x] = (int)(m > T ? T : m);
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] = max(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_out = given >= 0 ? min(given, T) : red[0];
+}
+
+// dG rows t >= n take no part in the step: zero them for the weight-gradient GEMM (its K runs
+// over every (t, b)); XH's h part of rows t > n is zero from prep_xh.
+__global__ void zero_dg_tail(__nv_bfloat16* __restrict__ dG, const int* __restrict__ n_dev, int B, int T, int G) {
+  const int n = *n_dev;
+  const long long begin = (long long)n * B * G / 8, end = (long long)T * B * G / 8;
+  uint4* p = reinterpret_cast<uint4*>(dG);
+  for (long long i = begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < end; i += (long long)gridDim.x * blockDim.x)
+    p[i] = make_uint4(0, 0, 0, 0);
+}
+
 // loss = inv_b * sum of the partials: stage 1 one block per step (fixed order within the
 // block), stage 2 the step sums in order (deterministic).
-__global__ void loss_step_sums(const double* __restrict__ part, int per_step, double* __restrict__ sums) {
+__global__ void loss_step_sums(const double* __restrict__ part, int per_step, const int* __restrict__ n_dev,
+                               double* __restrict__ sums) {
   __shared__ double red[256];
+  if ((int)blockIdx.x >= *n_dev) {   // steps past the trip count contribute nothing
+    if (threadIdx.x == 0) sums[blockIdx.x] = 0.0;
+    return;
+  }
   double s = 0.0;
   const double* p = part + (long long)blockIdx.x * per_step;
   for (int i = threadIdx.x; i < per_step; i += blockDim.x) s += p[i];
@@ -279,24 +309,25 @@ struct EpiBwd {
   const int64_t* lens;
   float *dhc, *dc;
   __nv_bfloat16* dG;
-  int n, T, H, B;
+  const int* n_dev;   // the trip count (device-determined: reduce_max of the lengths)
+  int T, H, B;
   float inv_b;
   int diag;
-  SKB_DEV int a_coord(int st) const { return n - st; }          // dG[t + 1]
+  SKB_DEV int a_coord(int st) const { return *n_dev - st; }     // dG[t + 1]
   SKB_DEV bool k_empty(int st) const { return st == 0; }        // t = n-1: no dG_{t+1}
   SKB_DEV void prefetch(uint8_t* sop, int st, int tm, int tn, uint64_t* bar) const {
-    const int t = n - 1 - st;
+    const int t = *n_dev - 1 - st;
     gemm::tma_load_2d(sop, &mDh, tn * 32, tm * 128, bar);
     gemm::tma_load_2d(sop + kBox, &mDc, tn * 32, tm * 128, bar);
     gemm::tma_load_3d(sop + 2 * kBox, &mY, tn * 32, t, tm * 128, bar);
 #pragma unroll
     for (int b = 0; b < 4; ++b) gemm::tma_load_3d(sop + (3 + b) * kBox, &mRec, (tn * 32 + 8 * b) * 8, tm * 128, t, bar);
   }
-  SKB_DEV void begin_tile(State& es, int st, int, int, int m) const { es.live = m < B && n - 1 - st < lens[m]; }
+  SKB_DEV void begin_tile(State& es, int st, int, int, int m) const { es.live = m < B && *n_dev - 1 - st < lens[m]; }
   SKB_DEV void chunk(State& es, const uint8_t* sop, int st, int r, int m, int k0, int c, const float (&v)[16],
                      bool row_ok) const {
     if (!row_ok || (diag & 1)) return;
-    const int t = n - 1 - st;
+    const int t = *n_dev - 1 - st;
     const long long s = (long long)m * H + k0;
     uint2* g = reinterpret_cast<uint2*>(dG + ((long long)t * B + m) * 4 * H + 4 * k0);
 #pragma unroll
@@ -435,12 +466,14 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
   const size_t nflag = (size_t)tm_ * (G / 64 + 1) * 2;
   cudaMemsetAsync(w.sync, 0, 8, cs);
   cudaMemsetAsync(w.xflag, 0, 4 * 2 * nflag, cs);
+  int* n_dev = w.sync + 2;
+  trip_count<<<1, 256, 0, cs>>>(lens, B, T, n, n_dev);
   {
     EpiFwd e;
     e.mC = mC; e.mH = mH; e.mY = mY;
     e.lens = lens; e.hcur = w.hcur; e.ccur = w.ccur; e.XH = w.XH; e.Rec = w.Rec; e.lpart = w.lpart;
     e.T = T; e.F = F; e.H = H; e.B = B; e.tiles_n = tiles_n; e.tiles = fwd_tiles(B, H); e.diag = diag();
-    gm::StepShape sh{B, G, KX, n, w.sync, w.xbuf, w.xflag};
+    gm::StepShape sh{B, G, KX, 0, n_dev, w.sync, w.xbuf, w.xflag};
     int rc;
     if (fwd_ks() == 2 && (G % 256) == 0) {   // 256-column tiles, each computed by two CTAs over K halves
       CUtensorMap mWU2;
@@ -451,16 +484,16 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     }
     if (rc) return rc == 3 ? SKB_ERR_UNSUPPORTED : SKB_ERR_CUDA;
   }
-  loss_step_sums<<<n, 256, 0, cs>>>(w.lpart, fwd_tiles(B, H) * kFwdSlots, w.lsum);
-  loss_final_sum<<<1, 256, 0, cs>>>(w.lsum, n, d->inv_batch, loss);
+  loss_step_sums<<<T, 256, 0, cs>>>(w.lpart, fwd_tiles(B, H) * kFwdSlots, n_dev, w.lsum);
+  loss_final_sum<<<1, 256, 0, cs>>>(w.lsum, T, d->inv_batch, loss);
 
   // backward: one persistent launch; dh = dG[t+1] Ut^T
   {
     EpiBwd e;
     e.mDh = mDh; e.mDc = mDc; e.mY = mY; e.mRec = mRec;
     e.lens = lens; e.dhc = w.dhc; e.dc = w.dc; e.dG = w.dG;
-    e.n = n; e.T = T; e.H = H; e.B = B; e.inv_b = d->inv_batch; e.diag = diag();
-    gm::StepShape sh{B, H, G, n, w.sync + 1, w.xbuf, w.xflag + nflag};
+    e.n_dev = n_dev; e.T = T; e.H = H; e.B = B; e.inv_b = d->inv_batch; e.diag = diag();
+    gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, w.xbuf, w.xflag + nflag};
     int rc;
     if (bwd_ks() == 2 && (H % 64) == 0) {   // 64-unit tiles, each computed by two CTAs over K halves
       CUtensorMap mUt2;
@@ -471,9 +504,7 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     }
     if (rc) return rc == 3 ? SKB_ERR_UNSUPPORTED : SKB_ERR_CUDA;
   }
-  // dG rows t >= n take no part in the step: zero for the weight-gradient GEMM (its K
-  // runs over every (t, b)); XH's h part of rows t > n is zero from prep_xh
-  if (n < T) cudaMemsetAsync(w.dG + (size_t)n * B * G, 0, 2ull * (T - n) * B * G, cs);
+  zero_dg_tail<<<blocks, 256, 0, cs>>>(w.dG, n_dev, B, T, G);
 
   // weight gradients over every (t, b): P = XH^T dG  (A: XH as [K = T B, M = KX], MN-major;
   // B: dG as [K = B T, N = 4H], MN-major)

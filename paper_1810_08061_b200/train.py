@@ -57,9 +57,12 @@ class LstmTrainer:
     def forward_backward(self, x, y, lens, h0=None, c0=None, max_len=None, stream=None):
         """Loss (device scalar) and this shard's gradients in self.grads."""
         from . import runtime as rt
-        if max_len is None:
-            max_len = int(lens.max().item()) if lens.numel() else 0   # the While trip count
-        max_len = max(0, min(int(max_len), self.time))
+        if max_len is None:   # the While trip count: on the device when the engine runs the step
+            if self.lib.skb_train_uses_engine(ctypes.byref(self.shape)):
+                max_len = -1
+            else:
+                max_len = int(lens.max().item()) if lens.numel() else 0
+        max_len = -1 if max_len == -1 else max(0, min(int(max_len), self.time))
         p = rt.ptr
         rt.check(self.lib.skb_lstm_train_step(ctypes.byref(self.shape), p(x), p(y), p(lens),
                                               p(h0) if h0 is not None else None, p(c0) if c0 is not None else None,
