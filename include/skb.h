@@ -372,7 +372,8 @@ skb_status skb_diag_cluster_exchange(int cluster, int slice_bytes, int rounds,
  *   operands only: a_mn = b_mn = 0, else SKB_ERR_UNSUPPORTED)
  *   A: [M,K] row-major (a_mn = 0) or [K,M] row-major (a_mn = 1), leading dim lda
  *   B: [N,K] row-major (b_mn = 0) or [K,N] row-major (b_mn = 1), leading dim ldb
- *   beta 0/1 (accumulate into C), bn tile width 64/128/256 (0 = auto),
+ *   beta 0/1 (accumulate into C), bn tile width 64/128/256 (0 = auto; -128 / -256: CTA-pair
+ *   cta_group::2 tiles of 256 x |bn|, the two CTAs of a cluster sharing the B tile),
  *   ksplit > 1: deterministic split-K through workspace (skb_gemm_workspace_bytes).
  * Operand rows must be 16-byte aligned; N % 16 == 0.  Replaces the cuBLAS calls the
  * reference-free configs used in round 1 (C2 training GEMMs). */

@@ -103,6 +103,28 @@ int run_store(const Problem& p, float* C, long long ldc, int beta, int ksplit, f
   return SKB_OK;
 }
 
+template <int ELEM, int BN, bool AMN, bool BMN>
+int run_pair(const Problem& p, float* C, long long ldc, int beta, cudaStream_t st) {
+  using G = Geo<ELEM, BN / 2>;
+  CUtensorMap ta, tb;
+  const bool oka = p.a_mn ? encode_2d(&ta, ELEM, p.A, p.M, p.K, p.lda, G::MNB, G::BK)
+                          : encode_2d(&ta, ELEM, p.A, p.K, p.M, p.lda, G::BK, G::BM);
+  const bool okb = p.b_mn ? encode_2d(&tb, ELEM, p.B, p.N, p.K, p.ldb, G::MNB, G::BK)
+                          : encode_2d(&tb, ELEM, p.B, p.K, p.N, p.ldb, G::BK, BN / 2);
+  if (!oka || !okb) return SKB_ERR_INVALID;
+  Shape sh{p.M, p.N, p.K, 1, 0};
+  EpiStore e{C, ldc, 0, beta};
+  return launch_pair<ELEM, BN, AMN, BMN>(ta, tb, sh, e, st) ? SKB_ERR_CUDA : SKB_OK;
+}
+
+template <int ELEM, int BN>
+int run_pair_majors(const Problem& p, float* C, long long ldc, int beta, cudaStream_t st) {
+  if (!p.a_mn && !p.b_mn) return run_pair<ELEM, BN, false, false>(p, C, ldc, beta, st);
+  if (!p.a_mn && p.b_mn) return run_pair<ELEM, BN, false, true>(p, C, ldc, beta, st);
+  if (p.a_mn && !p.b_mn) return run_pair<ELEM, BN, true, false>(p, C, ldc, beta, st);
+  return run_pair<ELEM, BN, true, true>(p, C, ldc, beta, st);
+}
+
 template <int ELEM, int BN>
 int run_majors(const Problem& p, float* C, long long ldc, int beta, int ksplit, float* ws, cudaStream_t st) {
   if (!p.a_mn && !p.b_mn) return run_store<ELEM, BN, false, false>(p, C, ldc, beta, ksplit, ws, st);
@@ -129,9 +151,19 @@ extern "C" skb_status skb_gemm(int elem, int a_mn, int b_mn, int M, int N, int K
   if (elem == kTF32 && (a_mn || b_mn)) return SKB_ERR_UNSUPPORTED;   // kind::tf32: K-major operands only
   if (ksplit < 1) ksplit = 1;
   if (ksplit > 1 && !workspace) return SKB_ERR_INVALID;
-  if (bn == 0) bn = N >= 256 ? 256 : 128;
   Problem p{elem, a_mn != 0, b_mn != 0, A, lda, B, ldb, M, N, K};
   cudaStream_t st = (cudaStream_t)stream;
+  if (bn < 0) {   // CTA-pair (cta_group::2) tiles of 256 x |bn|
+    if (ksplit > 1 || (bn != -256 && bn != -128)) return SKB_ERR_INVALID;
+    int rc;
+    if (elem == kBF16)
+      rc = bn == -256 ? run_pair_majors<kBF16, 256>(p, C, ldc, beta, st) : run_pair_majors<kBF16, 128>(p, C, ldc, beta, st);
+    else
+      rc = bn == -256 ? run_pair<kTF32, 256, false, false>(p, C, ldc, beta, st)
+                      : run_pair<kTF32, 128, false, false>(p, C, ldc, beta, st);
+    return rc == SKB_OK ? (skb_status)skb_check_launch() : (skb_status)rc;
+  }
+  if (bn == 0) bn = N >= 256 ? 256 : 128;
   float* ws = (float*)workspace;
   int rc;
   if (elem == kBF16)

@@ -283,6 +283,177 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_kernel(const __grid_con
   if (warp == 1) tmem_dealloc<G::TMEM_COLS>(tmem);
 }
 
+// ---------------------------------------------------------------- CTA-pair kernel
+// cta_group::2 tiles of 256 x BN: a cluster of two CTAs (a TPC pair); each CTA stages its own
+// 128 rows of A and half of B's BN rows (the pair's tensor cores read B from both CTAs' shared
+// memory), so per-CTA operand traffic drops from (16 KB + BN x 128 B) to (16 KB + BN x 64 B) per
+// k-block.  Both CTAs' TMA loads complete on the LEADER's full barrier (the .cta_group::2 form
+// of cp.async.bulk.tensor); the leader's single thread issues tcgen05.mma.cta_group::2 (M = 256)
+// and commits, multicast, to both CTAs' empty / TMEM-full barriers; each CTA's epilogue reads
+// its own 128 TMEM lanes and both arrive on the leader's TMEM-empty barrier.
+SKB_DEV void tma_load_2d_pair(void* smem_dst, const CUtensorMap* tm, int c0, int c1, uint32_t leader_bar) {
+  asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%2, %3}], [%4];"
+               :: "r"(smem_u32(smem_dst)), "l"(tm), "r"(c0), "r"(c1), "r"(leader_bar) : "memory");
+}
+SKB_DEV void tma_load_3d_pair(void* smem_dst, const CUtensorMap* tm, int c0, int c1, int c2, uint32_t leader_bar) {
+  asm volatile("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%2, %3, %4}], [%5];"
+               :: "r"(smem_u32(smem_dst)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar) : "memory");
+}
+template <int ELEM>
+SKB_DEV void umma_ss_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t id, uint32_t accumulate) {
+  if constexpr (ELEM == kBF16) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                 :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(id), "r"(accumulate) : "memory");
+  } else {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                 :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(id), "r"(accumulate) : "memory");
+  }
+}
+SKB_DEV void umma_commit_pair(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               :: "r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+
+template <int ELEM, int BN, bool AMN, bool BMN, class Epi, int EW = 1>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Shape sh,
+                     const __grid_constant__ Epi epi) {
+  using G = Geo<ELEM, BN / 2, Epi::kOpBytes>;   // per-CTA stage: A 128 rows + B BN / 2 rows
+  static_assert(Epi::kOpBytes == 0, "pair kernel: epilogue operands not supported");
+  static_assert((BN / EW) % 16 == 0, "epilogue column groups are multiples of 16");
+  constexpr uint32_t TMEM_COLS = BN * 2 <= 256 ? 256 : 512;   // two BN-column accumulators
+  if (epi.skip()) return;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[G::S], empty[G::S], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pairs_m = (sh.M + 255) / 256, tiles_n = (sh.N + BN - 1) / BN;
+  const int kblocks = (sh.K + G::BK - 1) / G::BK;
+  const int units = pairs_m * tiles_n;
+  const int npairs = gridDim.x / 2, pair = blockIdx.x / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < G::S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * 4 * EW); }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tmem_alloc_pair<TMEM_COLS>(&tmem_s);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();   // both CTAs' barriers and TMEM ready before any cross-CTA traffic
+  tc_fence_after();
+  const uint32_t tmem = tmem_s;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs; completion on the leader's barrier)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int u = pair; u < units; u += npairs) {
+        const int tm = u / tiles_n, tn = u % tiles_n;
+        const int row0 = tm * 256 + (int)rank * 128, col0 = tn * BN + (int)rank * (BN / 2);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait_sleep(&empty[stage], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE);
+          const uint32_t lbar = mapa(smem_u32(&full[stage]), 0);
+          uint8_t* sa = smem + stage * G::STAGE;
+          uint8_t* sb = sa + G::A_BYTES;
+          const int k0 = kb * G::BK;
+          if constexpr (!AMN) {
+            tma_load_2d_pair(sa, &tmA, k0, row0, lbar);
+          } else {
+#pragma unroll
+            for (int h = 0; h < G::BM / G::MNB; ++h)
+              tma_load_2d_pair(sa + h * (G::BK * 128), &tmA, row0 + h * G::MNB, k0, lbar);
+          }
+          if constexpr (!BMN) {
+            tma_load_2d_pair(sb, &tmB, k0, col0, lbar);
+          } else {
+#pragma unroll
+            for (int h = 0; h < (BN / 2) / G::MNB; ++h)
+              tma_load_2d_pair(sb + h * (G::BK * 128), &tmB, col0 + h * G::MNB, k0, lbar);
+          }
+          if (++stage == G::S) { stage = 0; ph ^= 1; }
+        }
+      }
+      // drain: every slot's last commit has arrived here before the CTA may exit
+      for (int i = 0; i < G::S; ++i) {
+        mbar_wait_sleep(&empty[stage], ph ^ 1);
+        if (++stage == G::S) { stage = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA, one thread)
+    if (leader && lane == 0) {
+      constexpr uint32_t id = idesc(ELEM, 256, BN, AMN, BMN);
+      constexpr uint32_t a_step = AMN ? G::UK * 128 : 32, b_step = BMN ? G::UK * 128 : 32;
+      constexpr uint32_t a_lbo = AMN ? G::BK * 128 : 16, b_lbo = BMN ? G::BK * 128 : 16;
+      int stage = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int u = pair; u < units; u += npairs) {
+        mbar_wait_sleep(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait_sleep(&full[stage], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * G::STAGE), sb = sa + G::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < G::BK / G::UK; ++k)
+            umma_ss_pair<ELEM>(d, sdesc_sw128(sa + k * a_step, a_lbo, 1024), sdesc_sw128(sb + k * b_step, b_lbo, 1024),
+                               id, (kb > 0 || k > 0) ? 1u : 0u);
+          umma_commit_pair(&empty[stage]);   // frees the slot in both CTAs
+          if (++stage == G::S) { stage = 0; ph ^= 1; }
+        }
+        umma_commit_pair(&tfull[acc]);       // accumulator complete, in both CTAs
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else {
+    // ===================== epilogue warps (each CTA: its 128 rows)
+    const int q = warp & 3, r = q * 32 + lane, cg0 = ((warp - 2) >> 2) * (BN / EW);
+    const uint32_t ltempty0 = mapa(smem_u32(&tempty[0]), 0), ltempty1 = mapa(smem_u32(&tempty[1]), 0);
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int u = pair; u < units; u += npairs) {
+      const int tm = u / tiles_n, tn = u % tiles_n;
+      const int m = tm * 256 + (int)rank * 128 + r;
+      typename Epi::State st;
+      epi.begin_tile(st, 2 * tm + (int)rank, tn, 0, m);
+      mbar_wait_sleep(&tfull[acc], aph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = cg0; c < cg0 + BN / EW; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + acc * BN + c + ((uint32_t)(q * 32) << 16), v);
+        tmem_ld_wait();
+        const int n0 = tn * BN + c;
+        if (n0 < sh.N) epi.chunk(st, nullptr, r, m, n0, c, 0, v, m < sh.M);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_remote_arrive(acc ? ltempty1 : ltempty0);
+      epi.end_tile(st, 2 * tm + (int)rank, tn, 0, warp - 2, lane);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();   // no CTA leaves while its peer may still signal its barriers
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair<TMEM_COLS>(tmem);
+}
+
 // ---------------------------------------------------------------- persistent step kernel
 // A recurrence of `steps` dependent GEMMs D_s = A_s · B^T with the same B (weights) and
 // tiling every step (BPTT, the forward While): one launch, one CTA per tile (all
@@ -526,6 +697,188 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
   if (warp == 1) tmem_dealloc<G::TMEM_COLS>(tmem);
 }
 
+// CTA-pair form of gemm_steps_kernel (KS = 1): each cluster of two CTAs computes a 256 x BN
+// tile of every step with cta_group::2 MMAs (the B = weights tile is split between the two
+// CTAs: half the per-CTA weight traffic); the epilogue functor sees the CTA's own 128-row
+// tile (tile row 2 tm + rank).  Cooperative launch with static cluster dims.
+template <int ELEM, int BN, class Epi, int EW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
+    gemm_steps_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const StepShape sh, const __grid_constant__ Epi epi) {
+  using G = Geo<ELEM, BN / 2, Epi::kOpBytes>;
+  static_assert((BN / EW) % 16 == 0, "epilogue column groups are multiples of 16");
+  constexpr uint32_t TMEM_COLS = BN * 2 <= 256 ? 256 : 512;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sop = smem + G::S * G::STAGE;
+  __shared__ uint64_t full[G::S], empty[G::S], tfull[2], tempty[2], opfull, opfree;
+  __shared__ uint32_t tmem_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int tiles_n = (sh.N + BN - 1) / BN;
+  const int kblocks = (sh.K + G::BK - 1) / G::BK;
+  const int units = ((sh.M + 255) / 256) * tiles_n;          // pair tiles
+  const int npairs = gridDim.x / 2, pair = blockIdx.x / 2;
+  const int per_step = 2 * units * 4 * EW;
+  const int steps = sh.steps_dev ? *sh.steps_dev : sh.steps;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < G::S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * 4 * EW); }
+    mbar_init(&opfull, 1);
+    mbar_init(&opfree, 4 * EW);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tmem_alloc_pair<TMEM_COLS>(&tmem_s);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = tmem_s;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs; completion on the leader's barrier)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0, oph = 0;
+      for (int st = 0; st < steps; ++st) {
+        const int ac = epi.a_coord(st);
+        const bool kz = epi.k_empty(st);
+        for (int u = pair; u < units; u += npairs) {
+          const int tm2 = u / tiles_n, tn = u % tiles_n, tmv = 2 * tm2 + (int)rank;
+          const int row0 = tmv * 128, col0 = tn * BN + (int)rank * (BN / 2);
+          const bool first = u == pair;
+          int npre = 0;
+          const int s0 = stage;
+          if (st > 0 && first && !kz) {   // weights first (independent of step st - 1)
+            npre = min(G::S, kblocks);
+            for (int i = 0; i < npre; ++i) {
+              mbar_wait_sleep(&empty[stage], ph ^ 1);
+              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE);
+              tma_load_2d_pair(smem + stage * G::STAGE + G::A_BYTES, &tmB, i * G::BK, col0,
+                               mapa(smem_u32(&full[stage]), 0));
+              if (++stage == G::S) { stage = 0; ph ^= 1; }
+            }
+          }
+          if constexpr (Epi::kOpBytes > 0) {   // CTA-local operands of this CTA's 128 rows
+            mbar_wait_sleep(&opfree, oph ^ 1);
+            fence_proxy_async_global();
+            mbar_arrive_expect_tx(&opfull, Epi::kOpBytes);
+            epi.prefetch(sop, st, tmv, tn, &opfull);
+            oph ^= 1;
+          }
+          if (st > 0 && first) {
+            const int want = st * per_step;
+            while (ld_acquire_gpu_s32(sh.sync) < want) __nanosleep(64);
+            fence_proxy_async_global();
+          }
+          if (kz) continue;
+          for (int kb = 0; kb < kblocks; ++kb) {
+            if (kb < npre) {
+              const int sidx = (s0 + kb) % G::S;
+              tma_load_3d_pair(smem + sidx * G::STAGE, &tmA, kb * G::BK, row0, ac, mapa(smem_u32(&full[sidx]), 0));
+              continue;
+            }
+            mbar_wait_sleep(&empty[stage], ph ^ 1);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE);
+            const uint32_t lbar = mapa(smem_u32(&full[stage]), 0);
+            uint8_t* sa = smem + stage * G::STAGE;
+            tma_load_3d_pair(sa, &tmA, kb * G::BK, row0, ac, lbar);
+            tma_load_2d_pair(sa + G::A_BYTES, &tmB, kb * G::BK, col0, lbar);
+            if (++stage == G::S) { stage = 0; ph ^= 1; }
+          }
+        }
+      }
+      for (int i = 0; i < G::S; ++i) {   // drain the last commits before the CTA may exit
+        mbar_wait_sleep(&empty[stage], ph ^ 1);
+        if (++stage == G::S) { stage = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA, one thread)
+    if (leader && lane == 0) {
+      constexpr uint32_t id = idesc(ELEM, 256, BN, false, false);
+      int stage = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int st = 0; st < steps; ++st) {
+        const bool kz = epi.k_empty(st);
+        for (int u = pair; u < units; u += npairs) {
+          mbar_wait_sleep(&tempty[acc], aph ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + acc * BN;
+          if (!kz) {
+            for (int kb = 0; kb < kblocks; ++kb) {
+              mbar_wait_sleep(&full[stage], ph);
+              tc_fence_after();
+              const uint32_t sa = smem_u32(smem + stage * G::STAGE), sb = sa + G::A_BYTES;
+#pragma unroll
+              for (int k = 0; k < G::BK / G::UK; ++k)
+                umma_ss_pair<ELEM>(d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), id,
+                                   (kb > 0 || k > 0) ? 1u : 0u);
+              umma_commit_pair(&empty[stage]);
+              if (++stage == G::S) { stage = 0; ph ^= 1; }
+            }
+          }
+          umma_commit_pair(&tfull[acc]);
+          if (++acc == 2) { acc = 0; aph ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue warps (each CTA: its 128 rows)
+    const int q = warp & 3, r = q * 32 + lane, cg0 = ((warp - 2) >> 2) * (BN / EW);
+    const uint32_t ltempty0 = mapa(smem_u32(&tempty[0]), 0), ltempty1 = mapa(smem_u32(&tempty[1]), 0);
+    int acc = 0;
+    uint32_t aph = 0, oph = 0;
+    for (int st = 0; st < steps; ++st) {
+      const bool kz = epi.k_empty(st);
+      for (int u = pair; u < units; u += npairs) {
+        const int tm2 = u / tiles_n, tn = u % tiles_n, tmv = 2 * tm2 + (int)rank;
+        const int m = tmv * 128 + r;
+        typename Epi::State es;
+        epi.begin_tile(es, st, tmv, tn, m);
+        mbar_wait_sleep(&tfull[acc], aph);
+        tc_fence_after();
+        if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
+#pragma unroll 1
+        for (int c = cg0; c < cg0 + BN / EW; c += 16) {
+          float v[16];
+          tmem_ld16(tmem + acc * BN + c + ((uint32_t)(q * 32) << 16), v);
+          tmem_ld_wait();
+          if (kz) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          }
+          const int n0 = tn * BN + c;
+          if (n0 < sh.N) epi.chunk(es, sop, st, r, m, n0, c, v, m < sh.M);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_remote_arrive(acc ? ltempty1 : ltempty0);
+          if constexpr (Epi::kOpBytes > 0) mbar_arrive(&opfree);
+        }
+        oph ^= 1;
+        epi.end_tile(es, st, tmv, tn, warp - 2, lane);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(sh.sync), "r"(1) : "memory");
+        }
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair<TMEM_COLS>(tmem);
+}
+
 // ---------------------------------------------------------------- epilogues
 // C[m, n] (+)= D, fp32, row-major with ldc; with ksplit > 1 each split writes its own
 // partial plane C + ks * split_stride (reduced by reduce_splits).
@@ -619,6 +972,52 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Shape& sh, const 
   cfg.attrs = lattr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, ta2 ? *ta2 : ta, sh, epi) == cudaSuccess ? 0 : 2;
+}
+
+// Persistent CTA-pair GEMM: pairs over (256-row, BN-column) tiles.
+template <int ELEM, int BN, bool AMN, bool BMN, class Epi, int EW = 1>
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const Shape& sh, const Epi& epi, cudaStream_t st) {
+  using G = Geo<ELEM, BN / 2, Epi::kOpBytes>;
+  auto kern = gemm_pair_kernel<ELEM, BN, AMN, BMN, Epi, EW>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess)
+      return 2;
+    attr = true;
+  }
+  const int units = ((sh.M + 255) / 256) * ((sh.N + BN - 1) / BN);
+  int pairs = num_sms() / 2;
+  if (units < pairs) pairs = units;
+  if (pairs < 1) return 0;
+  kern<<<2 * pairs, 64 + 128 * EW, G::SMEM, st>>>(ta, tb, sh, epi);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
+}
+
+// Cooperative launch of gemm_steps_pair_kernel: one CTA pair per 256-row tile, all resident.
+template <int ELEM, int BN, class Epi, int EW>
+int launch_steps_pair(const CUtensorMap& ta, const CUtensorMap& tb, const StepShape& sh, const Epi& epi,
+                      cudaStream_t st) {
+  using G = Geo<ELEM, BN / 2, Epi::kOpBytes>;
+  auto kern = gemm_steps_pair_kernel<ELEM, BN, Epi, EW>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess)
+      return 2;
+    attr = true;
+  }
+  const int units = ((sh.M + 255) / 256) * ((sh.N + BN - 1) / BN);
+  if (2 * units > num_sms()) return 3;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute lattr[1];
+  lattr[0].id = cudaLaunchAttributeCooperative;
+  lattr[0].val.cooperative = 1;
+  cfg.gridDim = dim3(2 * units);
+  cfg.blockDim = dim3(64 + 128 * EW);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cfg.stream = st;
+  cfg.attrs = lattr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, sh, epi) == cudaSuccess ? 0 : 2;
 }
 
 // Cooperative launch of gemm_steps_kernel: one CTA per unit (tile x K half), all resident.

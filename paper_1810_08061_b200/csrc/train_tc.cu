@@ -402,6 +402,18 @@ int bwd_ks() {
   return v;
 }
 
+int pair_fwd() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("SKB_TC_PAIR_FWD"); v = (e && atoi(e) == 0) ? 0 : 1; }
+  return v;
+}
+
+int pair_grad() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("SKB_TC_PAIR"); v = (e && atoi(e) == 0) ? 0 : 1; }
+  return v;
+}
+
 int diag() {
   static int v = -1;
   if (v < 0) { const char* e = getenv("SKB_TC_DIAG"); v = e ? atoi(e) : 0; }
@@ -479,6 +491,12 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
       CUtensorMap mWU2;
       if (!gm::encode_2d(&mWU2, kBF16, w.WU, KX, G, KX, GF::BK, 256)) return SKB_ERR_INVALID;
       rc = gm::launch_steps<kBF16, 256, EpiFwd, kFwdEW, 2>(mXH, mWU2, sh, e, cs);
+    } else if (pair_fwd() && (B % 256) == 0) {   // CTA pairs: 256-row tiles sharing the weight tile
+      CUtensorMap mWUp, mXHp;
+      if (!gm::encode_2d(&mWUp, kBF16, w.WU, KX, G, KX, GF::BK, kFwdBN / 2) ||
+          !gm::encode_3d(&mXHp, kBF16, w.XH, KX, B, T, KX, (uint64_t)B * KX, GF::BK, GF::BM, 1))
+        return SKB_ERR_INVALID;
+      rc = gm::launch_steps_pair<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXHp, mWUp, sh, e, cs);
     } else {
       rc = gm::launch_steps<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXH, mWU, sh, e, cs);
     }
@@ -517,7 +535,10 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     EpiGrad e;
     e.dW = dW; e.dU = dU; e.db = db; e.F = F; e.H = H;
     gm::Shape sh{KX, G, (int)rows, 1, 0};
-    if (gm::launch<kBF16, 256, true, true>(mX, mD, sh, e, cs)) return SKB_ERR_CUDA;
+    // CTA-pair 256 x 256 tiles (cta_group::2; SKB_TC_PAIR=0: 1-CTA 128 x 256)
+    const int rc = pair_grad() ? gm::launch_pair<kBF16, 256, true, true>(mX, mD, sh, e, cs)
+                               : gm::launch<kBF16, 256, true, true>(mX, mD, sh, e, cs);
+    if (rc) return SKB_ERR_CUDA;
   }
   return cudaPeekAtLastError() == cudaSuccess ? SKB_OK : SKB_ERR_CUDA;
 }

@@ -65,3 +65,15 @@ def test_split_k_is_deterministic():
 def test_large_bf16():
     got, ref = _gemm(0, 0, 0, 4096, 4096, 1024, seed=11)
     assert (got - ref).abs().max().item() <= 1e-5 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("elem", [0, 1])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("bn", [-128, -256])
+def test_cta_pair_tiles(elem, a_mn, b_mn, bn):
+    """cta_group::2 tiles (M = 256 across a CTA pair, B split between the two CTAs)."""
+    if elem == 1 and (a_mn or b_mn):
+        pytest.skip("kind::tf32 takes K-major operands only")
+    got, ref = _gemm(elem, a_mn, b_mn, 560, 272 if bn == -128 else 512, 200, bn=bn, beta=1, seed=3 - bn)
+    scale = ref.abs().max().item()
+    assert (got - ref).abs().max().item() <= (1e-5 if elem == 0 else 3e-3) * scale

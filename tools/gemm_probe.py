@@ -58,3 +58,6 @@ run("C2 dW = X^T dG", 0, 1, 1, 1024, 4096, 262144, bn=256)
 run("C2 dW ks8", 0, 1, 1, 1024, 4096, 262144, bn=256, ksplit=8)
 run("tf32 square", 1, 0, 0, 8192, 8192, 4096)
 run("C3 logits tf32", 1, 0, 0, 1024, 32000, 512, bn=128)
+run("square bf16 pair", 0, 0, 0, 8192, 8192, 8192, bn=-256)
+run("C2 dW pair", 0, 1, 1, 1024, 4096, 262144, bn=-256)
+run("C3 logits tf32 pair", 1, 0, 0, 1024, 32000, 512, bn=-256)
