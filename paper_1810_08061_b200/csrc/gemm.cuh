@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
   const int tiles_n = (sh.N + BN - 1) / BN;
   const int kblocks = (sh.K + G::BK - 1) / G::BK;
   const int nunits = ((sh.M + G::BM - 1) / G::BM) * tiles_n * KS;
-  const int per_step = nunits * 4 * EW;   // barrier arrivals per step (every epilogue warp of every unit)
+  const int per_step = nunits;   // barrier arrivals per step: one per unit (CTA tile)
   const int steps = sh.steps_dev ? *sh.steps_dev : sh.steps;
 
   if (threadIdx.x == 0) {
@@ -681,10 +681,11 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
         }
         oph ^= 1;
         epi.end_tile(es, st, tm, tv, warp - 2, lane);
-        // publish this warp's stores of step st (the next step's A operand / state)
+        // publish this CTA's stores of step st (the next step's A operand / state): one
+        // arrival per CTA after the epilogue warps' named barrier
         __threadfence();
-        __syncwarp();
-        if (lane == 0) {
+        named_bar_sync(1, 128 * EW);
+        if (warp == 2 && lane == 0) {
           asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(sh.sync), "r"(1) : "memory");
         }
         if (++acc == 2) { acc = 0; aph ^= 1; }
@@ -720,7 +721,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
   const int kblocks = (sh.K + G::BK - 1) / G::BK;
   const int units = ((sh.M + 255) / 256) * tiles_n;          // pair tiles
   const int npairs = gridDim.x / 2, pair = blockIdx.x / 2;
-  const int per_step = 2 * units * 4 * EW;
+  const int per_step = 2 * units;   // one arrival per CTA per step
   const int steps = sh.steps_dev ? *sh.steps_dev : sh.steps;
 
   if (threadIdx.x == 0) {
@@ -864,8 +865,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
         oph ^= 1;
         epi.end_tile(es, st, tmv, tn, warp - 2, lane);
         __threadfence();
-        __syncwarp();
-        if (lane == 0) {
+        named_bar_sync(1, 128 * EW);
+        if (warp == 2 && lane == 0) {
           asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(sh.sync), "r"(1) : "memory");
         }
         if (++acc == 2) { acc = 0; aph ^= 1; }
