@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_kernel(const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&tempty[acc]);
+        mbar_arrive_relaxed(&tempty[acc]);   // TMEM drained: nothing to publish
         if constexpr (Epi::kOpBytes > 0) mbar_arrive(&opfree);
       }
       oph ^= 1;
@@ -442,7 +442,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_remote_arrive(acc ? ltempty1 : ltempty0);
+      if (lane == 0) mbar_remote_arrive_relaxed(acc ? ltempty1 : ltempty0);
       epi.end_tile(st, 2 * tm + (int)rank, tn, 0, warp - 2, lane);
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
@@ -484,7 +484,15 @@ struct StepShape {
   int* sync;      // zeroed before the launch
   float* xbuf;    // KS = 2: [tiles][2 halves][128 rows][BN / 2] fp32 partial-sum exchange (L2)
   int* xflag;     // KS = 2: [tiles][2] publication counters, zeroed before the launch
+  long long* trace;   // optional: per-step globaltimer stamps of CTA 0 ([steps][8]), else null
 };
+SKB_DEV void step_trace(const StepShape& sh, int st, int slot) {
+  if (sh.trace && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    sh.trace[(long long)st * 8 + slot] = (long long)t;
+  }
+}
 
 // KS = 2: every output tile is computed by two CTAs, each over half of K (fewer, wider
 // tiles for the same CTA count: the activations / weights are re-read by fewer tiles).
@@ -643,7 +651,6 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
               for (int i = 0; i < 16; i += 4)
                 __stcg(reinterpret_cast<float4*>(xo + c + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
             }
-            __threadfence();
           }
           __syncwarp();
           if (lane == 0) {
@@ -676,14 +683,15 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&tempty[acc]);
+          mbar_arrive_relaxed(&tempty[acc]);   // TMEM drained: nothing to publish
           if constexpr (Epi::kOpBytes > 0) mbar_arrive(&opfree);
         }
         oph ^= 1;
         epi.end_tile(es, st, tm, tv, warp - 2, lane);
         // publish this CTA's stores of step st (the next step's A operand / state): one
         // arrival per CTA after the epilogue warps' named barrier
-        __threadfence();
+        // (no per-thread __threadfence: it is fence.sc.gpu + an L1 invalidate; the named barrier
+        // orders every epilogue thread's stores before the single gpu-scope release below)
         named_bar_sync(1, 128 * EW);
         if (warp == 2 && lane == 0) {
           asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(sh.sync), "r"(1) : "memory");
@@ -752,6 +760,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
           const int tm2 = u / tiles_n, tn = u % tiles_n, tmv = 2 * tm2 + (int)rank;
           const int row0 = tmv * 128, col0 = tn * BN + (int)rank * (BN / 2);
           const bool first = u == pair;
+          if (first) step_trace(sh, st, 0);
           int npre = 0;
           const int s0 = stage;
           if (st > 0 && first && !kz) {   // weights first (independent of step st - 1)
@@ -776,6 +785,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
             while (ld_acquire_gpu_s32(sh.sync) < want) __nanosleep(64);
             fence_proxy_async_global();
           }
+          if (first) step_trace(sh, st, 1);
           if (kz) continue;
           for (int kb = 0; kb < kblocks; ++kb) {
             if (kb < npre) {
@@ -813,6 +823,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
           if (!kz) {
             for (int kb = 0; kb < kblocks; ++kb) {
               mbar_wait_sleep(&full[stage], ph);
+              if (kb == 0) step_trace(sh, st, 2);
               tc_fence_after();
               const uint32_t sa = smem_u32(smem + stage * G::STAGE), sb = sa + G::A_BYTES;
 #pragma unroll
@@ -823,6 +834,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
               if (++stage == G::S) { stage = 0; ph ^= 1; }
             }
           }
+          step_trace(sh, st, 3);
           umma_commit_pair(&tfull[acc]);
           if (++acc == 2) { acc = 0; aph ^= 1; }
         }
@@ -842,8 +854,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
         typename Epi::State es;
         epi.begin_tile(es, st, tmv, tn, m);
         mbar_wait_sleep(&tfull[acc], aph);
+        if (warp == 2 && lane == 0) step_trace(sh, st, 4);
         tc_fence_after();
         if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
+        if (warp == 2 && lane == 0) step_trace(sh, st, 5);
 #pragma unroll 1
         for (int c = cg0; c < cg0 + BN / EW; c += 16) {
           float v[16];
@@ -859,15 +873,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_remote_arrive(acc ? ltempty1 : ltempty0);
+          mbar_remote_arrive_relaxed(acc ? ltempty1 : ltempty0);
           if constexpr (Epi::kOpBytes > 0) mbar_arrive(&opfree);
         }
         oph ^= 1;
         epi.end_tile(es, st, tmv, tn, warp - 2, lane);
-        __threadfence();
+        if (warp == 2 && lane == 0) step_trace(sh, st, 6);
+        // (no per-thread __threadfence: it is fence.sc.gpu + an L1 invalidate; the named barrier
+        // orders every epilogue thread's stores before the single gpu-scope release below)
         named_bar_sync(1, 128 * EW);
         if (warp == 2 && lane == 0) {
           asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(sh.sync), "r"(1) : "memory");
+          step_trace(sh, st, 7);
         }
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }

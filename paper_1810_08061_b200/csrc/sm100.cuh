@@ -46,6 +46,12 @@ SKB_DEV void fence_mbar_init() {
 SKB_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }
+// A pure "done" signal (no memory to publish, e.g. TMEM drained after tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync): no release fence, so it never waits on the thread's
+// outstanding global stores.
+SKB_DEV void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
 SKB_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                :: "r"(smem_u32(bar)), "r"(bytes) : "memory");

@@ -402,6 +402,22 @@ int bwd_ks() {
   return v;
 }
 
+// SKB_TC_TRACE=1: per-step globaltimer stamps of the forward step kernel's CTA 0
+// (tools/trace_c2.py reads them through skb_train_tc_trace).
+long long* g_trace = nullptr;
+int g_trace_cap = 0;
+long long* trace_buf(int T) {
+  static int on = -1;
+  if (on < 0) { const char* e = getenv("SKB_TC_TRACE"); on = (e && atoi(e) == 1) ? 1 : 0; }
+  if (!on) return nullptr;
+  if (T > g_trace_cap) {
+    if (g_trace) cudaFree(g_trace);
+    if (cudaMalloc(&g_trace, sizeof(long long) * 8 * T) != cudaSuccess) { g_trace = nullptr; g_trace_cap = 0; return nullptr; }
+    g_trace_cap = T;
+  }
+  return g_trace;
+}
+
 int pair_fwd() {
   static int v = -1;
   if (v < 0) { const char* e = getenv("SKB_TC_PAIR_FWD"); v = (e && atoi(e) == 0) ? 0 : 1; }
@@ -485,7 +501,7 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     e.mC = mC; e.mH = mH; e.mY = mY;
     e.lens = lens; e.hcur = w.hcur; e.ccur = w.ccur; e.XH = w.XH; e.Rec = w.Rec; e.lpart = w.lpart;
     e.T = T; e.F = F; e.H = H; e.B = B; e.tiles_n = tiles_n; e.tiles = fwd_tiles(B, H); e.diag = diag();
-    gm::StepShape sh{B, G, KX, 0, n_dev, w.sync, w.xbuf, w.xflag};
+    gm::StepShape sh{B, G, KX, 0, n_dev, w.sync, w.xbuf, w.xflag, trace_buf(T)};
     int rc;
     if (fwd_ks() == 2 && (G % 256) == 0) {   // 256-column tiles, each computed by two CTAs over K halves
       CUtensorMap mWU2;
@@ -511,7 +527,7 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     e.mDh = mDh; e.mDc = mDc; e.mY = mY; e.mRec = mRec;
     e.lens = lens; e.dhc = w.dhc; e.dc = w.dc; e.dG = w.dG;
     e.n_dev = n_dev; e.T = T; e.H = H; e.B = B; e.inv_b = d->inv_batch; e.diag = diag();
-    gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, w.xbuf, w.xflag + nflag};
+    gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, w.xbuf, w.xflag + nflag, nullptr};
     int rc;
     if (bwd_ks() == 2 && (H % 64) == 0) {   // 64-unit tiles, each computed by two CTAs over K halves
       CUtensorMap mUt2;
@@ -541,4 +557,9 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     if (rc) return SKB_ERR_CUDA;
   }
   return cudaPeekAtLastError() == cudaSuccess ? SKB_OK : SKB_ERR_CUDA;
+}
+
+extern "C" int skb_train_tc_trace(long long* host_out, int steps) {
+  if (!g_trace || steps > g_trace_cap) return -1;
+  return cudaMemcpy(host_out, g_trace, sizeof(long long) * 8 * steps, cudaMemcpyDeviceToHost) == cudaSuccess ? steps : -1;
 }
