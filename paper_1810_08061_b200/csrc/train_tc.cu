@@ -12,9 +12,12 @@
 //       [W[:, gH+j] | b[gH+j] | 0 | U[:, gH+j]]  -> one N-tile holds all four gates of
 //       its units, so the cell runs in the epilogue of the tile that produced them.
 //   Ut  [H, 4H] bf16, Ut[k][4j+g] = U[k][gH+j]  (the B operand of dh = dG U^T).
-//   Rec [T, B, H] x 8 fp16: i, f, g, o, c_{t-1}, tanh(c_t) of each live (t, b, j).
+//   Rec [T, B/128, H, 128] x 8 fp16 (tile-major: for one unit the 128 rows of a row tile are
+//       contiguous, so the epilogue's stores coalesce and a tile's records are one bulk copy):
+//       i, f, g, o, c_{t-1}, tanh(c_t) of each live (t, b, j).
 //   dG  [T, B, 4H] bf16 gate gradients (interleaved), zero for t >= len.
-//   hcur, ccur, dhc, dc [B, H] fp32: running state and the BPTT carries.
+//   hcur, ccur, dhc, dc [B/128, H, 128] fp32 (tile-major likewise): running state and the
+//       BPTT carries.
 // Forward (one persistent launch over t = 0 .. n-1, grid barrier between steps):
 //     D = XH[t] WU^T (K = KX)    -> EpiFwd: gates, c, h, Rec, loss partial <h_t, y_t>
 //                                   (live rows), h_t -> XH[t+1]
@@ -65,11 +68,12 @@ size_t layout(int B, int T, int F, int H, uint8_t* base, Bufs* w) {
   s.WU = (__nv_bfloat16*)take(2ull * G * KX);
   s.Ut = (__nv_bfloat16*)take(2ull * H * G);
   s.dG = (__nv_bfloat16*)take(2ull * B * T * G);
-  s.Rec = (__half*)take(16ull * B * T * H);
-  s.hcur = (float*)take(4ull * B * H);
-  s.ccur = (float*)take(4ull * B * H);
-  s.dhc = (float*)take(4ull * B * H);
-  s.dc = (float*)take(4ull * B * H);
+  const size_t Bp = (size_t)(B + 127) / 128 * 128;   // rows padded to whole 128-row tiles
+  s.Rec = (__half*)take(16ull * Bp * T * H);
+  s.hcur = (float*)take(4ull * Bp * H);
+  s.ccur = (float*)take(4ull * Bp * H);
+  s.dhc = (float*)take(4ull * Bp * H);
+  s.dc = (float*)take(4ull * Bp * H);
   s.lpart = (double*)take(8ull * T * fwd_tiles(B, H) * kFwdSlots);
   s.lsum = (double*)take(8ull * T);
   s.sync = (int*)take(16);
@@ -159,13 +163,21 @@ __global__ void prep_weights(const float* __restrict__ W, const float* __restric
   }
 }
 
+// Tile-major index of (row m, unit j) in a [B/128, H, 128] state array.
+__host__ __device__ __forceinline__ long long tmi(int m, int j, int H) {
+  return ((long long)(m >> 7) * H + j) * 128 + (m & 127);
+}
+
 __global__ void init_state(const float* __restrict__ h0, const float* __restrict__ c0, Bufs w, int B, int H) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)B * H;
+  const int Bp = (B + 127) / 128 * 128;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)Bp * H;
        i += (long long)gridDim.x * blockDim.x) {
-    w.hcur[i] = h0 ? h0[i] : 0.f;
-    w.ccur[i] = c0 ? c0[i] : 0.f;
-    w.dhc[i] = 0.f;
-    w.dc[i] = 0.f;
+    const int m = (int)(i / H), j = (int)(i % H);
+    const long long d = tmi(m, j, H);
+    w.hcur[d] = (m < B && h0) ? h0[(long long)m * H + j] : 0.f;
+    w.ccur[d] = (m < B && c0) ? c0[(long long)m * H + j] : 0.f;
+    w.dhc[d] = 0.f;
+    w.dc[d] = 0.f;
   }
 }
 
@@ -237,7 +249,7 @@ constexpr uint32_t kBox = 128 * 128;   // one [128 rows][128 B] operand box
 struct EpiFwd {
   static constexpr uint32_t kOpBytes = 3 * kBox;   // c_{t-1}, h_{t-1}, y_t: [128 rows][32 units] fp32
   struct State { double lacc; bool live; };
-  CUtensorMap mC, mH, mY;   // mY: y [B][T][H] as a 3-D map {H, T, B}
+  CUtensorMap mY;   // y [B][T][H] as a 3-D map {H, T, B}
   const int64_t* lens;
   float *hcur, *ccur;
   __nv_bfloat16* XH;
@@ -248,8 +260,9 @@ struct EpiFwd {
   SKB_DEV int a_coord(int st) const { return st; }
   SKB_DEV bool k_empty(int) const { return false; }
   SKB_DEV void prefetch(uint8_t* sop, int st, int tm, int tn, uint64_t* bar) const {
-    gemm::tma_load_2d(sop, &mC, tn * 32, tm * 128, bar);
-    gemm::tma_load_2d(sop + kBox, &mH, tn * 32, tm * 128, bar);
+    // the tile's c / h state: one contiguous [32 units][128 rows] block each (tile-major)
+    bulk_g2s(sop, ccur + tmi(tm * 128, tn * 32, H), kBox, bar);
+    bulk_g2s(sop + kBox, hcur + tmi(tm * 128, tn * 32, H), kBox, bar);
     gemm::tma_load_3d(sop + 2 * kBox, &mY, tn * 32, st, tm * 128, bar);
   }
   SKB_DEV void begin_tile(State& es, int st, int, int, int m) const {
@@ -259,11 +272,10 @@ struct EpiFwd {
   SKB_DEV void chunk(State& es, const uint8_t* sop, int t, int r, int m, int n0, int c, const float (&v)[16],
                      bool row_ok) const {
     if (!row_ok || (diag & 1)) return;
-    const int j0 = n0 >> 2;
-    const long long s = (long long)m * H + j0;
-    const float4 cp4 = *reinterpret_cast<const float4*>(gemm::sw128_at(sop, r, c >> 4));
-    const float4 hp4 = *reinterpret_cast<const float4*>(gemm::sw128_at(sop + kBox, r, c >> 4));
-    const float cp[4] = {cp4.x, cp4.y, cp4.z, cp4.w}, hp[4] = {hp4.x, hp4.y, hp4.z, hp4.w};
+    const int j0 = n0 >> 2, ul = c >> 2;   // first unit (global / tile-relative)
+    const float* sc = reinterpret_cast<const float*>(sop) + ul * 128 + r;
+    const float* sh = reinterpret_cast<const float*>(sop + kBox) + ul * 128 + r;
+    const float cp[4] = {sc[0], sc[128], sc[256], sc[384]}, hp[4] = {sh[0], sh[128], sh[256], sh[384]};
     float cn[4], hn[4];
     uint4 rec[4];
 #pragma unroll
@@ -276,17 +288,24 @@ struct EpiFwd {
       hn[u] = es.live ? h2 : hp[u];
       rec[u] = make_uint4(pack_h2(ig, fg), pack_h2(gg, og), pack_h2(cp[u], tc), 0u);
     }
-    *reinterpret_cast<float4*>(ccur + s) = make_float4(cn[0], cn[1], cn[2], cn[3]);
-    *reinterpret_cast<float4*>(hcur + s) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+    if (diag & 4) return;   // timing experiment: no stores
+    const long long s0 = tmi(m, j0, H);   // unit j0 + u at s0 + 128 u: coalesced across the warp's rows
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      ccur[s0 + 128 * u] = cn[u];
+      hcur[s0 + 128 * u] = hn[u];
+    }
     if (t + 1 < T) {
       const int KX = F + 16 + H;
       *reinterpret_cast<uint2*>(XH + ((long long)(t + 1) * B + m) * KX + F + 16 + j0) =
           make_uint2(pack_bf2(hn[0], hn[1]), pack_bf2(hn[2], hn[3]));
     }
     if (es.live) {
-      uint4* rp = reinterpret_cast<uint4*>(Rec + (((long long)t * B + m) * H + j0) * 8);
+      uint4* rp = reinterpret_cast<uint4*>(Rec) + (long long)t * ((B + 127) / 128) * 128 * H + s0;
+      if (!(diag & 8)) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) __stcs(rp + u, rec[u]);   // streamed: read once, in the backward
+        for (int u = 0; u < 4; ++u) __stcs(rp + 128 * u, rec[u]);   // streamed: read once, in the backward
+      }
       const float4 yv = *reinterpret_cast<const float4*>(gemm::sw128_at(sop + 2 * kBox, r, c >> 4));
       es.lacc += (double)hn[0] * yv.x + (double)hn[1] * yv.y + (double)hn[2] * yv.z + (double)hn[3] * yv.w;
     }
@@ -305,7 +324,8 @@ struct EpiFwd {
 struct EpiBwd {
   static constexpr uint32_t kOpBytes = 7 * kBox;
   struct State { bool live; };
-  CUtensorMap mDh, mDc, mY, mRec;   // mY {H, T, B}, mRec {8H, B, T} (3-D)
+  CUtensorMap mY;   // y as a 3-D map {H, T, B}
+  const __half* Rec;
   const int64_t* lens;
   float *dhc, *dc;
   __nv_bfloat16* dG;
@@ -317,42 +337,47 @@ struct EpiBwd {
   SKB_DEV bool k_empty(int st) const { return st == 0; }        // t = n-1: no dG_{t+1}
   SKB_DEV void prefetch(uint8_t* sop, int st, int tm, int tn, uint64_t* bar) const {
     const int t = *n_dev - 1 - st;
-    gemm::tma_load_2d(sop, &mDh, tn * 32, tm * 128, bar);
-    gemm::tma_load_2d(sop + kBox, &mDc, tn * 32, tm * 128, bar);
+    const long long s0 = tmi(tm * 128, tn * 32, H);   // the tile's 32 units x 128 rows, contiguous
+    bulk_g2s(sop, dhc + s0, kBox, bar);
+    bulk_g2s(sop + kBox, dc + s0, kBox, bar);
     gemm::tma_load_3d(sop + 2 * kBox, &mY, tn * 32, t, tm * 128, bar);
-#pragma unroll
-    for (int b = 0; b < 4; ++b) gemm::tma_load_3d(sop + (3 + b) * kBox, &mRec, (tn * 32 + 8 * b) * 8, tm * 128, t, bar);
+    bulk_g2s(sop + 3 * kBox, reinterpret_cast<const uint4*>(Rec) + (long long)t * ((B + 127) / 128) * 128 * H + s0,
+             4 * kBox, bar);
   }
   SKB_DEV void begin_tile(State& es, int st, int, int, int m) const { es.live = m < B && *n_dev - 1 - st < lens[m]; }
   SKB_DEV void chunk(State& es, const uint8_t* sop, int st, int r, int m, int k0, int c, const float (&v)[16],
                      bool row_ok) const {
     if (!row_ok || (diag & 1)) return;
     const int t = *n_dev - 1 - st;
-    const long long s = (long long)m * H + k0;
+    const long long s0 = tmi(m, k0, H);   // unit k0 + i at s0 + 128 i
     uint2* g = reinterpret_cast<uint2*>(dG + ((long long)t * B + m) * 4 * H + 4 * k0);
+    const float* sdh = reinterpret_cast<const float*>(sop) + c * 128 + r;
+    const float* sdc = reinterpret_cast<const float*>(sop + kBox) + c * 128 + r;
+    const uint4* srec = reinterpret_cast<const uint4*>(sop + 3 * kBox) + c * 128 + r;
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {   // four units per pass
-      const int c16 = (c >> 2) + q4, uu = c + 4 * q4;   // fp32 chunk, first unit (tile-relative)
-      const float4 c4 = *reinterpret_cast<const float4*>(gemm::sw128_at(sop, r, c16));
-      float dh[4] = {v[4 * q4] + c4.x, v[4 * q4 + 1] + c4.y, v[4 * q4 + 2] + c4.z, v[4 * q4 + 3] + c4.w};
-      if (!es.live) {
-        *reinterpret_cast<float4*>(dhc + s + 4 * q4) = make_float4(dh[0], dh[1], dh[2], dh[3]);
+      const int c16 = (c >> 2) + q4;   // y chunk (swizzled TMA box)
+      float dh[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) g[4 * q4 + u] = make_uint2(0u, 0u);
+      for (int u = 0; u < 4; ++u) dh[u] = v[4 * q4 + u] + sdh[(4 * q4 + u) * 128];
+      if (!es.live) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          dhc[s0 + 128 * (4 * q4 + u)] = dh[u];
+          g[4 * q4 + u] = make_uint2(0u, 0u);
+        }
         continue;
       }
       const float4 yv = *reinterpret_cast<const float4*>(gemm::sw128_at(sop + 2 * kBox, r, c16));
       dh[0] += yv.x * inv_b; dh[1] += yv.y * inv_b; dh[2] += yv.z * inv_b; dh[3] += yv.w * inv_b;
-      const float4 dc4 = *reinterpret_cast<const float4*>(gemm::sw128_at(sop + kBox, r, c16));
-      const float dcv[4] = {dc4.x, dc4.y, dc4.z, dc4.w};
       float dco[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int un = uu + u;
-        const uint4 rr = *reinterpret_cast<const uint4*>(gemm::sw128_at(sop + (3 + (un >> 3)) * kBox, r, un & 7));
+        const float dcv_u = sdc[(4 * q4 + u) * 128];
+        const uint4 rr = srec[(4 * q4 + u) * 128];
         const float2 a = unpack_h2(rr.x), b = unpack_h2(rr.y), cc = unpack_h2(rr.z);
         const float ig = a.x, fg = a.y, gg = b.x, og = b.y, cp = cc.x, tc = cc.y;
-        const float dcn = dcv[u] + dh[u] * og * (1.f - tc * tc);
+        const float dcn = dcv_u + dh[u] * og * (1.f - tc * tc);
         const float di = dcn * gg * ig * (1.f - ig);
         const float df = dcn * cp * fg * (1.f - fg);
         const float dg = dcn * ig * (1.f - gg * gg);
@@ -360,8 +385,11 @@ struct EpiBwd {
         g[4 * q4 + u] = make_uint2(pack_bf2(di, df), pack_bf2(dg, dO));
         dco[u] = dcn * fg;
       }
-      *reinterpret_cast<float4*>(dc + s + 4 * q4) = make_float4(dco[0], dco[1], dco[2], dco[3]);
-      *reinterpret_cast<float4*>(dhc + s + 4 * q4) = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        dc[s0 + 128 * (4 * q4 + u)] = dco[u];
+        dhc[s0 + 128 * (4 * q4 + u)] = 0.f;
+      }
     }
   }
   SKB_DEV void end_tile(State&, int, int, int, int, int) const {}
@@ -479,16 +507,13 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
 
   // forward: one persistent launch; B operand WU (K-major), A operand XH[t] (3-D map)
   using GF = gm::Geo<kBF16, kFwdBN>;
-  CUtensorMap mWU, mUt, mXH, mdG, mY, mRec, mC, mH, mDh, mDc;
+  CUtensorMap mWU, mUt, mXH, mdG, mY;
   const int tiles_n = G / kFwdBN;
   if (!gm::encode_2d(&mWU, kBF16, w.WU, KX, G, KX, GF::BK, kFwdBN) ||
       !gm::encode_3d(&mXH, kBF16, w.XH, KX, B, T, KX, (uint64_t)B * KX, GF::BK, GF::BM, 1) ||
       !gm::encode_3d(&mY, gm::kTF32, y, H, T, B, H, (uint64_t)T * H, 32, 1, 128) ||
-      !gm::encode_2d(&mC, gm::kTF32, w.ccur, H, B, H, 32, 128) || !gm::encode_2d(&mH, gm::kTF32, w.hcur, H, B, H, 32, 128) ||
-      !gm::encode_2d(&mDh, gm::kTF32, w.dhc, H, B, H, 32, 128) || !gm::encode_2d(&mDc, gm::kTF32, w.dc, H, B, H, 32, 128) ||
       !gm::encode_2d(&mUt, kBF16, w.Ut, G, H, G, 64, 32) ||
-      !gm::encode_3d(&mdG, kBF16, w.dG, G, B, T, G, (uint64_t)B * G, 64, 128, 1) ||
-      !gm::encode_3d(&mRec, kBF16, w.Rec, (uint64_t)H * 8, B, T, (uint64_t)H * 8, (uint64_t)B * H * 8, 64, 128, 1))
+      !gm::encode_3d(&mdG, kBF16, w.dG, G, B, T, G, (uint64_t)B * G, 64, 128, 1))
     return SKB_ERR_INVALID;
   const int tm_ = (B + 127) / 128;
   const size_t nflag = (size_t)tm_ * (G / 64 + 1) * 2;
@@ -498,7 +523,7 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
   trip_count<<<1, 256, 0, cs>>>(lens, B, T, n, n_dev);
   {
     EpiFwd e;
-    e.mC = mC; e.mH = mH; e.mY = mY;
+    e.mY = mY;
     e.lens = lens; e.hcur = w.hcur; e.ccur = w.ccur; e.XH = w.XH; e.Rec = w.Rec; e.lpart = w.lpart;
     e.T = T; e.F = F; e.H = H; e.B = B; e.tiles_n = tiles_n; e.tiles = fwd_tiles(B, H); e.diag = diag();
     gm::StepShape sh{B, G, KX, 0, n_dev, w.sync, w.xbuf, w.xflag, trace_buf(T)};
@@ -524,7 +549,7 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
   // backward: one persistent launch; dh = dG[t+1] Ut^T
   {
     EpiBwd e;
-    e.mDh = mDh; e.mDc = mDc; e.mY = mY; e.mRec = mRec;
+    e.mY = mY; e.Rec = w.Rec;
     e.lens = lens; e.dhc = w.dhc; e.dc = w.dc; e.dG = w.dG;
     e.n_dev = n_dev; e.T = T; e.H = H; e.B = B; e.inv_b = d->inv_batch; e.diag = diag();
     gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, w.xbuf, w.xflag + nflag, nullptr};
