@@ -241,10 +241,10 @@ skb_status skb_lstm_train_step(const skb_train_shape* shape, const float* x_dev,
 /* 1 if skb_lstm_train_step runs on skb's tcgen05 engine for this shape (bf16 math); then
  * max_len = -1 lets the device determine the While trip count (reduce_max of the lengths). */
 int skb_train_uses_engine(const skb_train_shape* shape);
-/* Debug: with SKB_TC_TRACE=1, copy the last forward step kernel's per-step globaltimer stamps
- * of CTA 0 ([steps][8] int64: step start, barrier passed, first stage, last MMA, TMEM full,
- * operands, epilogue done, published) to host_out; returns steps or -1. */
-int skb_train_tc_trace(long long* host_out, int steps);
+/* Debug: with SKB_TC_TRACE=1, copy the last forward (which = 0) or backward (1) step kernel's
+ * per-step globaltimer stamps of CTA 0 ([steps][8] int64: step start, barrier passed, first
+ * stage, last MMA, TMEM full, operands, epilogue done, published); returns steps or -1. */
+int skb_train_tc_trace(long long* host_out, int steps, int which);
 int skb_train_last_mode(void);   /* 1 = the last step replayed a CUDA graph */
 skb_status skb_sgd_update(float* params_dev, const float* grads_dev, int64_t n, float lr, void* stream);
 

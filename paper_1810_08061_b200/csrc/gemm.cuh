@@ -548,6 +548,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
           const int t = u / KS, ks = u % KS, tm = t / tiles_n, tn = t % tiles_n;
           const int kb0 = kblocks * ks / KS, kb1 = kblocks * (ks + 1) / KS;
           const bool first = u == (int)blockIdx.x;
+          if (first) step_trace(sh, st, 0);
           // weights first: they do not depend on step st - 1
           int npre = 0;
           const int s0 = stage;
@@ -574,6 +575,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
             while (ld_acquire_gpu_s32(sh.sync) < want) __nanosleep(64);
             fence_proxy_async_global();
           }
+          if (first) step_trace(sh, st, 1);
           if (kz) continue;
           for (int kb = kb0; kb < kb1; ++kb) {
             const int i = kb - kb0;
@@ -609,6 +611,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
           if (!kz) {
             for (int kb = kb0; kb < kb1; ++kb) {
               mbar_wait_sleep(&full[stage], ph);
+              if (kb == kb0) step_trace(sh, st, 2);
               tc_fence_after();
               const uint32_t sa = smem_u32(smem + stage * G::STAGE), sb = sa + G::A_BYTES;
 #pragma unroll
@@ -619,6 +622,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
               if (++stage == G::S) { stage = 0; ph ^= 1; }
             }
           }
+          step_trace(sh, st, 3);
           umma_commit(&tfull[acc]);
           if (++acc == 2) { acc = 0; aph ^= 1; }
         }
@@ -637,6 +641,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
         typename Epi::State es;
         epi.begin_tile(es, st, tm, tv, m);
         mbar_wait_sleep(&tfull[acc], aph);
+        if (warp == 2 && lane == 0) step_trace(sh, st, 4);
         tc_fence_after();
         const uint32_t dacc = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
         if constexpr (KS == 2) {   // publish the partner's half of the partial sums
@@ -661,6 +666,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
           __syncwarp();
         }
         if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
+        if (warp == 2 && lane == 0) step_trace(sh, st, 5);
 #pragma unroll 1
         for (int c = cg0; c < cg0 + BNE / EW; c += 16) {
           float v[16];
@@ -688,6 +694,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
         }
         oph ^= 1;
         epi.end_tile(es, st, tm, tv, warp - 2, lane);
+        if (warp == 2 && lane == 0) step_trace(sh, st, 6);
         // publish this CTA's stores of step st (the next step's A operand / state): one
         // arrival per CTA after the epilogue warps' named barrier
         // (no per-thread __threadfence: it is fence.sc.gpu + an L1 invalidate; the named barrier
@@ -695,6 +702,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
         named_bar_sync(1, 128 * EW);
         if (warp == 2 && lane == 0) {
           asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(sh.sync), "r"(1) : "memory");
+          step_trace(sh, st, 7);
         }
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }

@@ -345,15 +345,16 @@ struct EpiBwd {
              4 * kBox, bar);
   }
   SKB_DEV void begin_tile(State& es, int st, int, int, int m) const { es.live = m < B && *n_dev - 1 - st < lens[m]; }
+  // Warp-collective (every lane of the warp calls it; rows past B compute but store nothing).
   SKB_DEV void chunk(State& es, const uint8_t* sop, int st, int r, int m, int k0, int c, const float (&v)[16],
                      bool row_ok) const {
-    if (!row_ok || (diag & 1)) return;
+    if (diag & 1) return;
     const int t = *n_dev - 1 - st;
     const long long s0 = tmi(m, k0, H);   // unit k0 + i at s0 + 128 i
-    uint2* g = reinterpret_cast<uint2*>(dG + ((long long)t * B + m) * 4 * H + 4 * k0);
     const float* sdh = reinterpret_cast<const float*>(sop) + c * 128 + r;
     const float* sdc = reinterpret_cast<const float*>(sop + kBox) + c * 128 + r;
     const uint4* srec = reinterpret_cast<const uint4*>(sop + 3 * kBox) + c * 128 + r;
+    uint2 res[16];   // the 16 units' four gate gradients (bf16)
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {   // four units per pass
       const int c16 = (c >> 2) + q4;   // y chunk (swizzled TMA box)
@@ -363,8 +364,8 @@ struct EpiBwd {
       if (!es.live) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          dhc[s0 + 128 * (4 * q4 + u)] = dh[u];
-          g[4 * q4 + u] = make_uint2(0u, 0u);
+          if (row_ok) dhc[s0 + 128 * (4 * q4 + u)] = dh[u];
+          res[4 * q4 + u] = make_uint2(0u, 0u);
         }
         continue;
       }
@@ -382,15 +383,39 @@ struct EpiBwd {
         const float df = dcn * cp * fg * (1.f - fg);
         const float dg = dcn * ig * (1.f - gg * gg);
         const float dO = dh[u] * tc * og * (1.f - og);
-        g[4 * q4 + u] = make_uint2(pack_bf2(di, df), pack_bf2(dg, dO));
+        res[4 * q4 + u] = make_uint2(pack_bf2(di, df), pack_bf2(dg, dO));
         dco[u] = dcn * fg;
       }
+      if (row_ok) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        dc[s0 + 128 * (4 * q4 + u)] = dco[u];
-        dhc[s0 + 128 * (4 * q4 + u)] = 0.f;
+        for (int u = 0; u < 4; ++u) {
+          dc[s0 + 128 * (4 * q4 + u)] = dco[u];
+          dhc[s0 + 128 * (4 * q4 + u)] = 0.f;
+        }
       }
     }
+    // dG rows through shared memory: the warp's 32 rows x 16 units x 8 B (4 KB) are staged in
+    // the cell-record segments it has finished reading (units c..c+7 of its rows), 16-byte pairs
+    // XOR-swizzled by row, then written as whole 128-byte row segments (4 rows per instruction
+    // instead of 32 scattered 8-byte stores).
+    const int lane = r & 31, wq = r >> 5;
+    uint8_t* stg = const_cast<uint8_t*>(sop) + 3 * kBox + ((long long)c * 128 + wq * 32) * 16;   // unit c's segment
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+      *reinterpret_cast<uint4*>(stg + (lane >> 2) * 2048 + (lane & 3) * 128 + ((p ^ (lane & 7)) << 4)) =
+          make_uint4(res[2 * p].x, res[2 * p].y, res[2 * p + 1].x, res[2 * p + 1].y);
+    __syncwarp();
+    const int m0 = m - lane;   // the warp's first row
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int rho = 4 * k + (lane >> 3), p = lane & 7;
+      const uint4 val = *reinterpret_cast<const uint4*>(stg + k * 2048 + (rho & 3) * 128 + ((p ^ (rho & 7)) << 4));
+      if (m0 + rho < B)
+        *reinterpret_cast<uint4*>(dG + ((long long)t * B + m0 + rho) * 4 * H + 4 * k0 + 8 * p) = val;
+    }
+    fence_proxy_async_smem();   // the next step's TMA operand loads overwrite the staging area
+    __syncwarp();
   }
   SKB_DEV void end_tile(State&, int, int, int, int, int) const {}
 };
@@ -440,7 +465,7 @@ long long* trace_buf(int T) {
   if (!on) return nullptr;
   if (T > g_trace_cap) {
     if (g_trace) cudaFree(g_trace);
-    if (cudaMalloc(&g_trace, sizeof(long long) * 8 * T) != cudaSuccess) { g_trace = nullptr; g_trace_cap = 0; return nullptr; }
+    if (cudaMalloc(&g_trace, sizeof(long long) * 16 * T) != cudaSuccess) { g_trace = nullptr; g_trace_cap = 0; return nullptr; }
     g_trace_cap = T;
   }
   return g_trace;
@@ -552,7 +577,8 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     e.mY = mY; e.Rec = w.Rec;
     e.lens = lens; e.dhc = w.dhc; e.dc = w.dc; e.dG = w.dG;
     e.n_dev = n_dev; e.T = T; e.H = H; e.B = B; e.inv_b = d->inv_batch; e.diag = diag();
-    gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, w.xbuf, w.xflag + nflag, nullptr};
+    long long* tb = trace_buf(T) ? g_trace + 8ll * g_trace_cap : nullptr;   // second half of the trace
+    gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, w.xbuf, w.xflag + nflag, tb};
     int rc;
     if (bwd_ks() == 2 && (H % 64) == 0) {   // 64-unit tiles, each computed by two CTAs over K halves
       CUtensorMap mUt2;
@@ -584,7 +610,9 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
   return cudaPeekAtLastError() == cudaSuccess ? SKB_OK : SKB_ERR_CUDA;
 }
 
-extern "C" int skb_train_tc_trace(long long* host_out, int steps) {
-  if (!g_trace || steps > g_trace_cap) return -1;
-  return cudaMemcpy(host_out, g_trace, sizeof(long long) * 8 * steps, cudaMemcpyDeviceToHost) == cudaSuccess ? steps : -1;
+// which = 0: forward kernel, 1: backward kernel
+extern "C" int skb_train_tc_trace(long long* host_out, int steps, int which) {
+  if (!g_trace || steps > g_trace_cap || which < 0 || which > 1) return -1;
+  return cudaMemcpy(host_out, g_trace + (which ? 8ll * g_trace_cap : 0), sizeof(long long) * 8 * steps,
+                    cudaMemcpyDeviceToHost) == cudaSuccess ? steps : -1;
 }

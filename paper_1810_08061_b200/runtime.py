@@ -86,7 +86,7 @@ SIGNATURES = {
     "skb_lstm_train_step": (ctypes.c_int, [ctypes.POINTER(TrainShape)] + [_VP] * 8 + [ctypes.c_int, _VP, _VP]),
     "skb_train_last_mode": (ctypes.c_int, []),
     "skb_train_uses_engine": (ctypes.c_int, [_VP]),
-    "skb_train_tc_trace": (ctypes.c_int, [_VP, ctypes.c_int]),
+    "skb_train_tc_trace": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int]),
     "skb_sgd_update": (ctypes.c_int, [_VP, _VP, ctypes.c_int64, ctypes.c_float, _VP]),
     "skb_maml_workspace_bytes": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int]),
     "skb_maml_meta_grad": (ctypes.c_int, [ctypes.c_int] * 3 + [_VP] * 5 + [ctypes.c_float, _VP, _VP, _VP, _VP]),

@@ -21,14 +21,15 @@ tr = LstmTrainer(F, H, ROWS, T, global_batch=ROWS, lr=0.0, math="bf16", seed=1, 
 for _ in range(2):
     tr.forward_backward(x, y, lens)
 torch.cuda.synchronize()
-buf = np.zeros((T, 8), dtype=np.int64)
-n = tr.lib.skb_train_tc_trace(ctypes.c_void_p(buf.ctypes.data), T)
-assert n == T, n
 names = ["start", "barrier passed", "first stage full", "last MMA issued", "TMEM full (epi)",
          "operands ready", "epilogue done", "published"]
-d = np.diff(buf[16:T - 16], axis=1) / 1e3
-print("per-step phase durations (us), CTA 0, steps 16..T-16, mean / median:")
-for i in range(7):
-    print(f"  {names[i]:>18s} -> {names[i + 1]:<18s} {d[:, i].mean():7.2f} {np.median(d[:, i]):7.2f}")
-step = np.diff(buf[16:T - 16, 0]) / 1e3
-print(f"  step period {step.mean():.2f} us; published -> next start {np.mean(buf[17:T - 15, 0] - buf[16:T - 16, 7]) / 1e3:.2f} us")
+for which, title in ((0, "forward"), (1, "backward")):
+    buf = np.zeros((T, 8), dtype=np.int64)
+    n = tr.lib.skb_train_tc_trace(ctypes.c_void_p(buf.ctypes.data), T, which)
+    assert n == T, n
+    d = np.diff(buf[16:T - 16], axis=1) / 1e3
+    print(f"{title} step kernel: per-step phase durations (us), CTA 0, steps 16..T-16, mean / median:")
+    for i in range(7):
+        print(f"  {names[i]:>18s} -> {names[i + 1]:<18s} {d[:, i].mean():7.2f} {np.median(d[:, i]):7.2f}")
+    step = np.abs(np.diff(buf[16:T - 16, 1])) / 1e3
+    print(f"  step period {step.mean():.2f} us")
