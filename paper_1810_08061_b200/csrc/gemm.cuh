@@ -77,7 +77,7 @@ SKB_DEV void umma_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t i
 }
 
 // ---------------------------------------------------------------- geometry
-template <int ELEM, int BN, uint32_t OPB = 0>
+template <int ELEM, int BN, uint32_t OPB = 0, int BUDGET_KB = 212>
 struct Geo {
   static constexpr int EB = ELEM == kBF16 ? 2 : 4;      // bytes per element
   static constexpr int BM = 128;
@@ -87,7 +87,7 @@ struct Geo {
   static constexpr int A_BYTES = BM * BK * EB;          // 16 KB
   static constexpr int B_BYTES = BN * BK * EB;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int S = ((212 * 1024 - (int)OPB) / STAGE) > 8 ? 8 : ((212 * 1024 - (int)OPB) / STAGE);
+  static constexpr int S = ((BUDGET_KB * 1024 - (int)OPB) / STAGE) > 8 ? 8 : ((BUDGET_KB * 1024 - (int)OPB) / STAGE);
   static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                       : 2 * BN <= 256 ? 256 : 512;
   static constexpr size_t SMEM = (size_t)S * STAGE + OPB + 1024;
@@ -501,19 +501,27 @@ SKB_DEV void step_trace(const StepShape& sh, int st, int slot) {
 // half (the epilogue functor sees tiles of BN / 2 columns, tile index 2 tn + ks).
 // Step st + 1 arms its first stages with the weight (B) k-blocks before the grid
 // barrier; the activation (A) halves follow once the barrier is passed.
+// Steps-kernel geometry: behind the epilogue operands, KS = 2 keeps a [128][BN / 2] fp32
+// receive buffer for the partner's partial sums; the budget runs to the 227 KB limit.
+template <int ELEM, int BN, class Epi, int KS>
+using StepGeo = Geo<ELEM, BN, Epi::kOpBytes + (KS == 2 ? 128u * (BN / 2) * 4u : 0u), 224>;
+
 template <int ELEM, int BN, class Epi, int EW, int KS = 1>
-__global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __grid_constant__ CUtensorMap tmA,
+__global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                      const __grid_constant__ CUtensorMap tmB,
                                                                      const StepShape sh,
                                                                      const __grid_constant__ Epi epi) {
-  using G = Geo<ELEM, BN, Epi::kOpBytes>;
+  using G = StepGeo<ELEM, BN, Epi, KS>;
   constexpr int BNE = BN / KS;   // epilogue columns per CTA
   static_assert((BNE / EW) % 16 == 0, "epilogue column groups are multiples of 16");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sop = smem + G::S * G::STAGE;
-  __shared__ uint64_t full[G::S], empty[G::S], tfull[2], tempty[2], opfull, opfree;
+  __shared__ uint64_t full[G::S], empty[G::S], tfull[2], tempty[2], opfull, opfree, xfull;
   __shared__ uint32_t tmem_s;
+  // KS = 2: the partner CTA (the other K half of the tile, same cluster) writes its partial
+  // sums of this CTA's columns straight into xrecv through distributed shared memory
+  float* xrecv = reinterpret_cast<float*>(sop + Epi::kOpBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_n = (sh.N + BN - 1) / BN;
   const int kblocks = (sh.K + G::BK - 1) / G::BK;
@@ -526,6 +534,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * EW); }
     mbar_init(&opfull, 1);
     mbar_init(&opfree, 4 * EW);
+    mbar_init(&xfull, 4 * EW);
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -533,6 +542,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
   if (warp == 1) tmem_alloc<G::TMEM_COLS>(&tmem_s);
   tc_fence_before();
   __syncthreads();
+  if constexpr (KS == 2) cluster_sync();   // the partner's barriers exist before any DSMEM traffic
   tc_fence_after();
   const uint32_t tmem = tmem_s;
 
@@ -644,26 +654,26 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
         if (warp == 2 && lane == 0) step_trace(sh, st, 4);
         tc_fence_after();
         const uint32_t dacc = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
-        if constexpr (KS == 2) {   // publish the partner's half of the partial sums
-          if (!kz) {   // (a step without MMAs still counts: the counters advance every step)
-            float* xo = sh.xbuf + (((long long)t * 2 + (ks ^ 1)) * 128 + r) * BNE;
+        if constexpr (KS == 2) {   // the partner's half of the partial sums -> its xrecv (DSMEM)
+          const uint32_t peer = cluster_ctarank() ^ 1u;
+          if (!kz) {   // (a step without MMAs still signals: the barrier phases advance every step)
+            const uint32_t xr = mapa(smem_u32(xrecv), peer) + (uint32_t)(r * BNE * 4);
 #pragma unroll 1
             for (int c = cg0; c < cg0 + BNE / EW; c += 16) {
               float v[16];
               tmem_ld16(dacc + (ks ^ 1) * BNE + c, v);
               tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 16; i += 4)
-                __stcg(reinterpret_cast<float4*>(xo + c + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+              for (int i = 0; i < 16; i += 4) {   // 16-byte chunks XOR-swizzled by row: conflict-free
+                const uint32_t q = (uint32_t)((c + i) >> 2) ^ (uint32_t)(r & 7);
+                asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};"
+                             :: "r"(xr + q * 16), "f"(v[i]), "f"(v[i + 1]), "f"(v[i + 2]), "f"(v[i + 3]) : "memory");
+              }
             }
           }
           __syncwarp();
-          if (lane == 0) {
-            asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(sh.xflag + t * 2 + ks), "r"(1) : "memory");
-            const int want = (st + 1) * 4 * EW;
-            while (ld_acquire_gpu_s32(sh.xflag + t * 2 + (ks ^ 1)) < want) __nanosleep(32);
-          }
-          __syncwarp();
+          if (lane == 0) mbar_remote_arrive(mapa(smem_u32(&xfull), peer));   // release.cluster: the stores above
+          mbar_wait_cluster(&xfull, st & 1);                                 // acquire: the partner's stores
         }
         if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
         if (warp == 2 && lane == 0) step_trace(sh, st, 5);
@@ -676,10 +686,10 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
           } else if constexpr (KS == 2) {
-            const float* xi = sh.xbuf + (((long long)t * 2 + ks) * 128 + r) * BNE + c;
 #pragma unroll
             for (int i = 0; i < 16; i += 4) {
-              const float4 p = __ldcg(reinterpret_cast<const float4*>(xi + i));
+              const uint32_t q = (uint32_t)((c + i) >> 2) ^ (uint32_t)(r & 7);
+              const float4 p = *reinterpret_cast<const float4*>(xrecv + r * BNE + q * 4);
               v[i] += p.x; v[i + 1] += p.y; v[i + 2] += p.z; v[i + 3] += p.w;
             }
           }
@@ -710,6 +720,7 @@ __global__ void __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __gr
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (KS == 2) cluster_sync();   // no CTA leaves while its partner may still write to it
   tc_fence_after();
   if (warp == 1) tmem_dealloc<G::TMEM_COLS>(tmem);
 }
@@ -1049,7 +1060,7 @@ int launch_steps_pair(const CUtensorMap& ta, const CUtensorMap& tb, const StepSh
 // Cooperative launch of gemm_steps_kernel: one CTA per unit (tile x K half), all resident.
 template <int ELEM, int BN, class Epi, int EW, int KS = 1>
 int launch_steps(const CUtensorMap& ta, const CUtensorMap& tb, const StepShape& sh, const Epi& epi, cudaStream_t st) {
-  using G = Geo<ELEM, BN, Epi::kOpBytes>;
+  using G = StepGeo<ELEM, BN, Epi, KS>;
   auto kern = gemm_steps_kernel<ELEM, BN, Epi, EW, KS>;
   static bool attr = false;
   if (!attr) {
@@ -1059,7 +1070,6 @@ int launch_steps(const CUtensorMap& ta, const CUtensorMap& tb, const StepShape& 
   }
   const int nunits = ((sh.M + G::BM - 1) / G::BM) * ((sh.N + BN - 1) / BN) * KS;
   if (nunits > num_sms()) return 3;   // one resident CTA per unit
-  if (KS == 2 && (!sh.xbuf || !sh.xflag)) return 3;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute lattr[1];
   lattr[0].id = cudaLaunchAttributeCooperative;
