@@ -464,8 +464,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
 // epilogue of step s has stored (the epilogue's global writes produce A_{s+1}): each
 // epilogue warp publishes its tile with a fence + gpu-scope release add on `sync`; the
 // producer acquires the count, orders its bulk reads after it with a proxy fence.
-// Epi contract as above plus a_coord(s), k_empty(s) (no MMA at step s: D = 0) and the
-// step index in begin_tile / chunk / end_tile / prefetch.  prefetch(st) may only read
+// Epi contract as above plus a_coord(s), k_empty(s) (no MMA at step s: D = 0), k_indep(s)
+// (the leading K blocks of A_s that no earlier step writes: loaded and multiplied before the
+// barrier) and the step index in begin_tile / chunk / end_tile / prefetch.  prefetch(st) may only read
 // inputs and state written by this CTA's own epilogue (it is issued before the barrier).
 SKB_DEV void tma_load_3d(void* smem_dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
@@ -559,15 +560,28 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
           const int kb0 = kblocks * ks / KS, kb1 = kblocks * (ks + 1) / KS;
           const bool first = u == (int)blockIdx.x;
           if (first) step_trace(sh, st, 0);
-          // weights first: they do not depend on step st - 1
-          int npre = 0;
-          const int s0 = stage;
+          // before the grid barrier: the K blocks of A that do not depend on step st - 1
+          // (epi.k_indep) in full -- their MMAs run while the previous step finishes --, then
+          // the weights of the next blocks
+          int npre = 0, nind = 0;
+          int s0 = stage;
           if (st > 0 && first && !kz) {
-            npre = min(G::S, kb1 - kb0);
+            nind = max(0, min(kb1, epi.k_indep(st)) - kb0);
+            for (int i = 0; i < nind; ++i) {
+              mbar_wait_sleep(&empty[stage], ph ^ 1);
+              mbar_arrive_expect_tx(&full[stage], G::STAGE);
+              uint8_t* sa = smem + stage * G::STAGE;
+              tma_load_3d(sa, &tmA, (kb0 + i) * G::BK, tm * G::BM, ac, &full[stage]);
+              tma_load_2d(sa + G::A_BYTES, &tmB, (kb0 + i) * G::BK, tn * BN, &full[stage]);
+              if (++stage == G::S) { stage = 0; ph ^= 1; }
+            }
+            s0 = stage;
+            npre = min(G::S, kb1 - kb0 - nind);
             for (int i = 0; i < npre; ++i) {
               mbar_wait_sleep(&empty[stage], ph ^ 1);
               mbar_arrive_expect_tx(&full[stage], G::STAGE);
-              tma_load_2d(smem + stage * G::STAGE + G::A_BYTES, &tmB, (kb0 + i) * G::BK, tn * BN, &full[stage]);
+              tma_load_2d(smem + stage * G::STAGE + G::A_BYTES, &tmB, (kb0 + nind + i) * G::BK, tn * BN,
+                          &full[stage]);
               if (++stage == G::S) { stage = 0; ph ^= 1; }
             }
           }
@@ -587,8 +601,8 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
           }
           if (first) step_trace(sh, st, 1);
           if (kz) continue;
-          for (int kb = kb0; kb < kb1; ++kb) {
-            const int i = kb - kb0;
+          for (int kb = kb0 + nind; kb < kb1; ++kb) {
+            const int i = kb - kb0 - nind;
             if (i < npre) {   // stage armed before the barrier: only its A half is missing
               const int sidx = (s0 + i) % G::S;
               tma_load_3d(smem + sidx * G::STAGE, &tmA, kb * G::BK, tm * G::BM, ac, &full[sidx]);
@@ -643,12 +657,12 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
     const int q = warp & 3, r = q * 32 + lane, cg0 = ((warp - 2) >> 2) * (BNE / EW);
     int acc = 0;
     uint32_t aph = 0, oph = 0;
+    typename Epi::State es;   // lives across steps: a CTA keeps its unit, so state may ride in registers
     for (int st = 0; st < steps; ++st) {
       const bool kz = epi.k_empty(st);
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int t = u / KS, ks = u % KS, tm = t / tiles_n, tn = t % tiles_n, tv = tn * KS + ks;
         const int m = tm * G::BM + r;
-        typename Epi::State es;
         epi.begin_tile(es, st, tm, tv, m);
         mbar_wait_sleep(&tfull[acc], aph);
         if (warp == 2 && lane == 0) step_trace(sh, st, 4);
@@ -780,14 +794,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
           const int row0 = tmv * 128, col0 = tn * BN + (int)rank * (BN / 2);
           const bool first = u == pair;
           if (first) step_trace(sh, st, 0);
-          int npre = 0;
-          const int s0 = stage;
-          if (st > 0 && first && !kz) {   // weights first (independent of step st - 1)
-            npre = min(G::S, kblocks);
+          int npre = 0, nind = 0;
+          int s0 = stage;
+          if (st > 0 && first && !kz) {   // independent A blocks in full, then weights (as above)
+            nind = min(kblocks, epi.k_indep(st));
+            for (int i = 0; i < nind; ++i) {
+              mbar_wait_sleep(&empty[stage], ph ^ 1);
+              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE);
+              const uint32_t lbar = mapa(smem_u32(&full[stage]), 0);
+              uint8_t* sa = smem + stage * G::STAGE;
+              tma_load_3d_pair(sa, &tmA, i * G::BK, row0, ac, lbar);
+              tma_load_2d_pair(sa + G::A_BYTES, &tmB, i * G::BK, col0, lbar);
+              if (++stage == G::S) { stage = 0; ph ^= 1; }
+            }
+            s0 = stage;
+            npre = min(G::S, kblocks - nind);
             for (int i = 0; i < npre; ++i) {
               mbar_wait_sleep(&empty[stage], ph ^ 1);
               if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE);
-              tma_load_2d_pair(smem + stage * G::STAGE + G::A_BYTES, &tmB, i * G::BK, col0,
+              tma_load_2d_pair(smem + stage * G::STAGE + G::A_BYTES, &tmB, (nind + i) * G::BK, col0,
                                mapa(smem_u32(&full[stage]), 0));
               if (++stage == G::S) { stage = 0; ph ^= 1; }
             }
@@ -806,9 +831,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
           }
           if (first) step_trace(sh, st, 1);
           if (kz) continue;
-          for (int kb = 0; kb < kblocks; ++kb) {
-            if (kb < npre) {
-              const int sidx = (s0 + kb) % G::S;
+          for (int kb = nind; kb < kblocks; ++kb) {
+            if (kb - nind < npre) {
+              const int sidx = (s0 + kb - nind) % G::S;
               tma_load_3d_pair(smem + sidx * G::STAGE, &tmA, kb * G::BK, row0, ac, mapa(smem_u32(&full[sidx]), 0));
               continue;
             }
@@ -865,12 +890,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
     const uint32_t ltempty0 = mapa(smem_u32(&tempty[0]), 0), ltempty1 = mapa(smem_u32(&tempty[1]), 0);
     int acc = 0;
     uint32_t aph = 0, oph = 0;
+    typename Epi::State es;   // lives across steps: a pair keeps its unit, so state may ride in registers
     for (int st = 0; st < steps; ++st) {
       const bool kz = epi.k_empty(st);
       for (int u = pair; u < units; u += npairs) {
         const int tm2 = u / tiles_n, tn = u % tiles_n, tmv = 2 * tm2 + (int)rank;
         const int m = tmv * 128 + r;
-        typename Epi::State es;
         epi.begin_tile(es, st, tmv, tn, m);
         mbar_wait_sleep(&tfull[acc], aph);
         if (warp == 2 && lane == 0) step_trace(sh, st, 4);

@@ -246,9 +246,12 @@ __global__ void loss_final_sum(const double* __restrict__ sums, int n, float inv
 constexpr uint32_t kBox = 128 * 128;   // one [128 rows][128 B] operand box
 
 // Forward cell of step t = st: 16 accumulator columns = 4 units x (i, f, g, o); tile = 32 units.
+// Every step kernel keeps one tile per CTA for all steps, and each epilogue thread owns one row
+// and the same 8 units (two 16-column chunks) every step, so c and h ride in registers across
+// steps: read from ccur/hcur at step 0, written back at the row's last live step.
 struct EpiFwd {
-  static constexpr uint32_t kOpBytes = 3 * kBox;   // c_{t-1}, h_{t-1}, y_t: [128 rows][32 units] fp32
-  struct State { double lacc; bool live; };
+  static constexpr uint32_t kOpBytes = kBox;   // y_t: [128 rows][32 units] fp32
+  struct State { double lacc; bool live, last; float c0[4], c1[4], h0[4], h1[4]; };
   CUtensorMap mY;   // y [B][T][H] as a 3-D map {H, T, B}
   const int64_t* lens;
   float *hcur, *ccur;
@@ -259,23 +262,31 @@ struct EpiFwd {
   int diag;   // SKB_TC_DIAG (timing experiments only): bit 0 skip the cell
   SKB_DEV int a_coord(int st) const { return st; }
   SKB_DEV bool k_empty(int) const { return false; }
+  // XH[t]'s x part (and nothing of h_{t-1}) fills the first F / 64 K blocks
+  SKB_DEV int k_indep(int) const { return F / 64; }
   SKB_DEV void prefetch(uint8_t* sop, int st, int tm, int tn, uint64_t* bar) const {
-    // the tile's c / h state: one contiguous [32 units][128 rows] block each (tile-major)
-    bulk_g2s(sop, ccur + tmi(tm * 128, tn * 32, H), kBox, bar);
-    bulk_g2s(sop + kBox, hcur + tmi(tm * 128, tn * 32, H), kBox, bar);
-    gemm::tma_load_3d(sop + 2 * kBox, &mY, tn * 32, st, tm * 128, bar);
+    gemm::tma_load_3d(sop, &mY, tn * 32, st, tm * 128, bar);
   }
   SKB_DEV void begin_tile(State& es, int st, int, int, int m) const {
     es.lacc = 0.0;
-    es.live = m < B && st < lens[m];
+    const int len = m < B ? (int)lens[m] : 0;
+    es.live = st < len;
+    es.last = st == len - 1;
   }
   SKB_DEV void chunk(State& es, const uint8_t* sop, int t, int r, int m, int n0, int c, const float (&v)[16],
                      bool row_ok) const {
     if (!row_ok || (diag & 1)) return;
-    const int j0 = n0 >> 2, ul = c >> 2;   // first unit (global / tile-relative)
-    const float* sc = reinterpret_cast<const float*>(sop) + ul * 128 + r;
-    const float* sh = reinterpret_cast<const float*>(sop + kBox) + ul * 128 + r;
-    const float cp[4] = {sc[0], sc[128], sc[256], sc[384]}, hp[4] = {sh[0], sh[128], sh[256], sh[384]};
+    const int j0 = n0 >> 2;                 // first unit
+    const bool k1 = (c >> 4) & 1;           // which of the thread's two chunks
+    const long long s0 = tmi(m, j0, H);   // unit j0 + u at s0 + 128 u: coalesced across the warp's rows
+    float cp[4], hp[4];
+    if (t == 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { cp[u] = ccur[s0 + 128 * u]; hp[u] = hcur[s0 + 128 * u]; }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { cp[u] = k1 ? es.c1[u] : es.c0[u]; hp[u] = k1 ? es.h1[u] : es.h0[u]; }
+    }
     float cn[4], hn[4];
     uint4 rec[4];
 #pragma unroll
@@ -287,13 +298,15 @@ struct EpiFwd {
       cn[u] = es.live ? c2 : cp[u];
       hn[u] = es.live ? h2 : hp[u];
       rec[u] = make_uint4(pack_h2(ig, fg), pack_h2(gg, og), pack_h2(cp[u], tc), 0u);
+      if (k1) { es.c1[u] = cn[u]; es.h1[u] = hn[u]; } else { es.c0[u] = cn[u]; es.h0[u] = hn[u]; }
     }
     if (diag & 4) return;   // timing experiment: no stores
-    const long long s0 = tmi(m, j0, H);   // unit j0 + u at s0 + 128 u: coalesced across the warp's rows
+    if (es.last) {   // the row's final state
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      ccur[s0 + 128 * u] = cn[u];
-      hcur[s0 + 128 * u] = hn[u];
+      for (int u = 0; u < 4; ++u) {
+        ccur[s0 + 128 * u] = cn[u];
+        hcur[s0 + 128 * u] = hn[u];
+      }
     }
     if (t + 1 < T) {
       const int KX = F + 16 + H;
@@ -306,7 +319,7 @@ struct EpiFwd {
 #pragma unroll
         for (int u = 0; u < 4; ++u) __stcs(rp + 128 * u, rec[u]);   // streamed: read once, in the backward
       }
-      const float4 yv = *reinterpret_cast<const float4*>(gemm::sw128_at(sop + 2 * kBox, r, c >> 4));
+      const float4 yv = *reinterpret_cast<const float4*>(gemm::sw128_at(sop, r, c >> 4));
       es.lacc += (double)hn[0] * yv.x + (double)hn[1] * yv.y + (double)hn[2] * yv.z + (double)hn[3] * yv.w;
     }
   }
@@ -335,6 +348,7 @@ struct EpiBwd {
   int diag;
   SKB_DEV int a_coord(int st) const { return *n_dev - st; }     // dG[t + 1]
   SKB_DEV bool k_empty(int st) const { return st == 0; }        // t = n-1: no dG_{t+1}
+  SKB_DEV int k_indep(int) const { return 0; }                  // every block is dG_{t+1}
   SKB_DEV void prefetch(uint8_t* sop, int st, int tm, int tn, uint64_t* bar) const {
     const int t = *n_dev - 1 - st;
     const long long s0 = tmi(tm * 128, tn * 32, H);   // the tile's 32 units x 128 rows, contiguous
