@@ -483,8 +483,6 @@ struct StepShape {
   int steps;
   const int* steps_dev;   // non-null: the step count is read from device memory (a device-side trip count)
   int* sync;      // zeroed before the launch
-  float* xbuf;    // KS = 2: [tiles][2 halves][128 rows][BN / 2] fp32 partial-sum exchange (L2)
-  int* xflag;     // KS = 2: [tiles][2] publication counters, zeroed before the launch
   long long* trace;   // optional: per-step globaltimer stamps of CTA 0 ([steps][8]), else null
 };
 SKB_DEV void step_trace(const StepShape& sh, int st, int slot) {

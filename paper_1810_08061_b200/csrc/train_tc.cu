@@ -16,8 +16,8 @@
 //       contiguous, so the epilogue's stores coalesce and a tile's records are one bulk copy):
 //       i, f, g, o, c_{t-1}, tanh(c_t) of each live (t, b, j).
 //   dG  [T, B, 4H] bf16 gate gradients (interleaved), zero for t >= len.
-//   hcur, ccur, dhc, dc [B/128, H, 128] fp32 (tile-major likewise): running state and the
-//       BPTT carries.
+//   hcur, ccur [B/128, H, 128] fp32 (tile-major likewise): initial / final state (the running
+//       state and the BPTT carries ride in the step kernels' epilogue registers).
 // Forward (one persistent launch over t = 0 .. n-1, grid barrier between steps):
 //     D = XH[t] WU^T (K = KX)    -> EpiFwd: gates, c, h, Rec, loss partial <h_t, y_t>
 //                                   (live rows), h_t -> XH[t+1]
@@ -43,12 +43,10 @@ using gemm::kBF16;
 struct Bufs {
   __nv_bfloat16 *XH, *WU, *Ut, *dG;
   __half* Rec;
-  float *hcur, *ccur, *dhc, *dc;
+  float *hcur, *ccur;
   double* lpart;   // [T][fwd tiles][epilogue warps]
   double* lsum;    // [T] per-step loss sums
   int* sync;       // [2] grid-barrier counters of the forward / backward launches, [2] the trip count
-  float* xbuf;     // split-K partial-sum exchange of the step kernels (KS = 2)
-  int* xflag;      // [2][tiles][2] its publication counters (forward, backward)
 };
 
 inline int kx_of(int F, int H) { return F + 16 + H; }
@@ -72,13 +70,9 @@ size_t layout(int B, int T, int F, int H, uint8_t* base, Bufs* w) {
   s.Rec = (__half*)take(16ull * Bp * T * H);
   s.hcur = (float*)take(4ull * Bp * H);
   s.ccur = (float*)take(4ull * Bp * H);
-  s.dhc = (float*)take(4ull * Bp * H);
-  s.dc = (float*)take(4ull * Bp * H);
   s.lpart = (double*)take(8ull * T * fwd_tiles(B, H) * kFwdSlots);
   s.lsum = (double*)take(8ull * T);
   s.sync = (int*)take(16);
-  s.xbuf = (float*)take(4ull * ((B + 127) / 128) * (G / 256 + 1) * 2 * 128 * 128);
-  s.xflag = (int*)take(4ull * 2 * ((B + 127) / 128) * (G / 64 + 1) * 2);
   if (w) *w = s;
   return off;
 }
@@ -176,8 +170,6 @@ __global__ void init_state(const float* __restrict__ h0, const float* __restrict
     const long long d = tmi(m, j, H);
     w.hcur[d] = (m < B && h0) ? h0[(long long)m * H + j] : 0.f;
     w.ccur[d] = (m < B && c0) ? c0[(long long)m * H + j] : 0.f;
-    w.dhc[d] = 0.f;
-    w.dc[d] = 0.f;
   }
 }
 
@@ -333,14 +325,14 @@ struct EpiFwd {
 
 // Backward cell of step t = n-1-st: 16 accumulator columns = dh of 16 consecutive units;
 // tile = 32 units.  Operands: dh carry, dc carry, y_t (fp32 boxes) and the cell records
-// (four [128 rows][8 units x 16 B] boxes).
+// (four [128 rows][8 units x 16 B] boxes).  Each epilogue thread owns one row and the same 16
+// units (one chunk) every step, so the dh / dc carries ride in its registers (zero at t = n-1).
 struct EpiBwd {
-  static constexpr uint32_t kOpBytes = 7 * kBox;
-  struct State { bool live; };
+  static constexpr uint32_t kOpBytes = 5 * kBox;   // y_t, then the cell records
+  struct State { bool live; float dh[16], dc[16]; };
   CUtensorMap mY;   // y as a 3-D map {H, T, B}
   const __half* Rec;
   const int64_t* lens;
-  float *dhc, *dc;
   __nv_bfloat16* dG;
   const int* n_dev;   // the trip count (device-determined: reduce_max of the lengths)
   int T, H, B;
@@ -352,43 +344,43 @@ struct EpiBwd {
   SKB_DEV void prefetch(uint8_t* sop, int st, int tm, int tn, uint64_t* bar) const {
     const int t = *n_dev - 1 - st;
     const long long s0 = tmi(tm * 128, tn * 32, H);   // the tile's 32 units x 128 rows, contiguous
-    bulk_g2s(sop, dhc + s0, kBox, bar);
-    bulk_g2s(sop + kBox, dc + s0, kBox, bar);
-    gemm::tma_load_3d(sop + 2 * kBox, &mY, tn * 32, t, tm * 128, bar);
-    bulk_g2s(sop + 3 * kBox, reinterpret_cast<const uint4*>(Rec) + (long long)t * ((B + 127) / 128) * 128 * H + s0,
+    gemm::tma_load_3d(sop, &mY, tn * 32, t, tm * 128, bar);
+    bulk_g2s(sop + kBox, reinterpret_cast<const uint4*>(Rec) + (long long)t * ((B + 127) / 128) * 128 * H + s0,
              4 * kBox, bar);
   }
-  SKB_DEV void begin_tile(State& es, int st, int, int, int m) const { es.live = m < B && *n_dev - 1 - st < lens[m]; }
+  SKB_DEV void begin_tile(State& es, int st, int, int, int m) const {
+    es.live = m < B && *n_dev - 1 - st < lens[m];
+    if (st == 0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) { es.dh[i] = 0.f; es.dc[i] = 0.f; }
+    }
+  }
   // Warp-collective (every lane of the warp calls it; rows past B compute but store nothing).
   SKB_DEV void chunk(State& es, const uint8_t* sop, int st, int r, int m, int k0, int c, const float (&v)[16],
                      bool row_ok) const {
     if (diag & 1) return;
     const int t = *n_dev - 1 - st;
-    const long long s0 = tmi(m, k0, H);   // unit k0 + i at s0 + 128 i
-    const float* sdh = reinterpret_cast<const float*>(sop) + c * 128 + r;
-    const float* sdc = reinterpret_cast<const float*>(sop + kBox) + c * 128 + r;
-    const uint4* srec = reinterpret_cast<const uint4*>(sop + 3 * kBox) + c * 128 + r;
+    const uint4* srec = reinterpret_cast<const uint4*>(sop + kBox) + c * 128 + r;
     uint2 res[16];   // the 16 units' four gate gradients (bf16)
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {   // four units per pass
       const int c16 = (c >> 2) + q4;   // y chunk (swizzled TMA box)
       float dh[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) dh[u] = v[4 * q4 + u] + sdh[(4 * q4 + u) * 128];
-      if (!es.live) {
+      for (int u = 0; u < 4; ++u) dh[u] = v[4 * q4 + u] + es.dh[4 * q4 + u];
+      if (!es.live) {   // frozen step: dh carries on to the row's last live step
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (row_ok) dhc[s0 + 128 * (4 * q4 + u)] = dh[u];
+          es.dh[4 * q4 + u] = dh[u];
           res[4 * q4 + u] = make_uint2(0u, 0u);
         }
         continue;
       }
-      const float4 yv = *reinterpret_cast<const float4*>(gemm::sw128_at(sop + 2 * kBox, r, c16));
+      const float4 yv = *reinterpret_cast<const float4*>(gemm::sw128_at(sop, r, c16));
       dh[0] += yv.x * inv_b; dh[1] += yv.y * inv_b; dh[2] += yv.z * inv_b; dh[3] += yv.w * inv_b;
-      float dco[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float dcv_u = sdc[(4 * q4 + u) * 128];
+        const float dcv_u = es.dc[4 * q4 + u];
         const uint4 rr = srec[(4 * q4 + u) * 128];
         const float2 a = unpack_h2(rr.x), b = unpack_h2(rr.y), cc = unpack_h2(rr.z);
         const float ig = a.x, fg = a.y, gg = b.x, og = b.y, cp = cc.x, tc = cc.y;
@@ -398,14 +390,8 @@ struct EpiBwd {
         const float dg = dcn * ig * (1.f - gg * gg);
         const float dO = dh[u] * tc * og * (1.f - og);
         res[4 * q4 + u] = make_uint2(pack_bf2(di, df), pack_bf2(dg, dO));
-        dco[u] = dcn * fg;
-      }
-      if (row_ok) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          dc[s0 + 128 * (4 * q4 + u)] = dco[u];
-          dhc[s0 + 128 * (4 * q4 + u)] = 0.f;
-        }
+        es.dc[4 * q4 + u] = dcn * fg;
+        es.dh[4 * q4 + u] = 0.f;
       }
     }
     // dG rows through shared memory: the warp's 32 rows x 16 units x 8 B (4 KB) are staged in
@@ -413,7 +399,7 @@ struct EpiBwd {
     // XOR-swizzled by row, then written as whole 128-byte row segments (4 rows per instruction
     // instead of 32 scattered 8-byte stores).
     const int lane = r & 31, wq = r >> 5;
-    uint8_t* stg = const_cast<uint8_t*>(sop) + 3 * kBox + ((long long)c * 128 + wq * 32) * 16;   // unit c's segment
+    uint8_t* stg = const_cast<uint8_t*>(sop) + kBox + ((long long)c * 128 + wq * 32) * 16;   // unit c's segment
     __syncwarp();
 #pragma unroll
     for (int p = 0; p < 8; ++p)
@@ -554,10 +540,7 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
       !gm::encode_2d(&mUt, kBF16, w.Ut, G, H, G, 64, 32) ||
       !gm::encode_3d(&mdG, kBF16, w.dG, G, B, T, G, (uint64_t)B * G, 64, 128, 1))
     return SKB_ERR_INVALID;
-  const int tm_ = (B + 127) / 128;
-  const size_t nflag = (size_t)tm_ * (G / 64 + 1) * 2;
   cudaMemsetAsync(w.sync, 0, 8, cs);
-  cudaMemsetAsync(w.xflag, 0, 4 * 2 * nflag, cs);
   int* n_dev = w.sync + 2;
   trip_count<<<1, 256, 0, cs>>>(lens, B, T, n, n_dev);
   {
@@ -565,7 +548,7 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     e.mY = mY;
     e.lens = lens; e.hcur = w.hcur; e.ccur = w.ccur; e.XH = w.XH; e.Rec = w.Rec; e.lpart = w.lpart;
     e.T = T; e.F = F; e.H = H; e.B = B; e.tiles_n = tiles_n; e.tiles = fwd_tiles(B, H); e.diag = diag();
-    gm::StepShape sh{B, G, KX, 0, n_dev, w.sync, w.xbuf, w.xflag, trace_buf(T)};
+    gm::StepShape sh{B, G, KX, 0, n_dev, w.sync, trace_buf(T)};
     int rc;
     if (fwd_ks() == 2 && (G % 256) == 0) {   // 256-column tiles, each computed by two CTAs over K halves
       CUtensorMap mWU2;
@@ -589,10 +572,10 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
   {
     EpiBwd e;
     e.mY = mY; e.Rec = w.Rec;
-    e.lens = lens; e.dhc = w.dhc; e.dc = w.dc; e.dG = w.dG;
+    e.lens = lens; e.dG = w.dG;
     e.n_dev = n_dev; e.T = T; e.H = H; e.B = B; e.inv_b = d->inv_batch; e.diag = diag();
     long long* tb = trace_buf(T) ? g_trace + 8ll * g_trace_cap : nullptr;   // second half of the trace
-    gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, w.xbuf, w.xflag + nflag, tb};
+    gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, tb};
     int rc;
     if (bwd_ks() == 2 && (H % 64) == 0) {   // 64-unit tiles, each computed by two CTAs over K halves
       CUtensorMap mUt2;
