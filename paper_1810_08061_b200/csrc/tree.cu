@@ -13,12 +13,20 @@
 // Each node's h is written straight into its parent's X row (left or right
 // half), so no gather pass exists between levels.  Semantics: oracle/tree.py
 // (bit-exact with the reference interpreter in float64).
+// SKB_TREE_TC=1 (TF32, even H): each level is ONE launch of skb's tcgen05 GEMM engine (gemm.cuh)
+// with the cell fused into its epilogue (EpiTree): U is repacked gate-interleaved, three units x
+// five gates per 16 accumulator columns, so a thread holds every gate of its units and the
+// [rows, 5H] gate matrix never reaches HBM.  Parity-tested, but measured 1.9x slower on C5
+// (0.76 vs 0.40 ms per forest): the epilogue's per-row gathers of node ids and children's c
+// (thread = row) are latency-bound at one CTA per SM, where tree_cell4 runs eight CTAs per SM with
+// row-contiguous loads.  Default: cuBLAS level GEMMs + tree_cell4.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include "blas.cuh"
+#include "gemm.cuh"
 #include "skb_internal.h"
 
 namespace {
@@ -147,11 +155,85 @@ __global__ void tree_cell4(const int32_t* __restrict__ order, int row0, int nrow
   }
 }
 
+// ---------------------------------------------------------------- engine path
+// Packed U: row n' = 16 q + 5 e + g (e < 3, g < 5) holds column g H + j of U, j = 3 q + e; rows
+// 16 q + 15 and units j >= H are zero.  K-major [NP][2H] fp32 (TF32 operands).
+inline int tree_np(int H) { return ((H + 2) / 3 * 16 + 127) / 128 * 128; }
+
+__global__ void tree_pack_u(const float* __restrict__ U, int H, int NP, float* __restrict__ Up) {
+  const int K = 2 * H;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)NP * K;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int np = (int)(i / K), k = (int)(i % K);
+    const int q = np >> 4, w = np & 15, e = w / 5, g = w % 5, j = 3 * q + e;
+    Up[i] = (w < 15 && j < H) ? U[(long long)k * 5 * H + g * H + j] : 0.f;
+  }
+}
+
+// Epilogue geometry: 128-column tiles, 4 x 4 epilogue warps, so a thread owns 32 columns (two
+// chunks = 6 units) of one row; begin_tile (before the tile's accumulator is waited for) fetches
+// the row's node ids and its children's c values of those 6 units into registers.
+constexpr int kTreeBN = 128, kTreeEW = 4, kTreeUnits = 6;
+struct EpiTree {
+  static constexpr uint32_t kOpBytes = 0;
+  struct State { int n, d; float cl[kTreeUnits], cr[kTreeUnits]; };
+  const int32_t *order, *left, *right, *dest;
+  const float* bias;
+  float *h, *c, *X;
+  int H, r0, nr;
+  SKB_DEV bool skip() const { return false; }
+  SKB_DEV bool ops_on() const { return false; }
+  SKB_DEV void prefetch(uint8_t*, int, int, uint64_t*) const {}
+  SKB_DEV void begin_tile(State& s, int, int tn, int, int m) const {
+    if (m >= nr) return;
+    s.n = order[r0 + m];
+    s.d = dest[s.n];
+    const int slice = ((int)(threadIdx.x >> 5) - 2) >> 2;   // the thread's column slice (gemm_kernel)
+    const int j0 = tn * (kTreeBN / 16 * 3) + slice * kTreeUnits;
+    const float* cl = c + (long long)left[s.n] * H;
+    const float* cr = c + (long long)right[s.n] * H;
+#pragma unroll
+    for (int u = 0; u < kTreeUnits; ++u) {
+      s.cl[u] = j0 + u < H ? cl[j0 + u] : 0.f;
+      s.cr[u] = j0 + u < H ? cr[j0 + u] : 0.f;
+    }
+  }
+  SKB_DEV void chunk(State& s, const uint8_t*, int, int, int n0, int, int, const float (&v)[16], bool row_ok) const {
+    if (!row_ok) return;
+    const int n = s.n, d = s.d;
+    const bool k1 = (n0 >> 4) & 1;   // second chunk of the thread's slice
+    float* xrow = d >= 0 ? X + (long long)(d >> 1) * 2 * H + (d & 1) * H : nullptr;
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      const int j = 3 * (n0 >> 4) + e;
+      if (j >= H) break;
+      const float gi = sigmoidf_ref(v[5 * e] + bias[j]);
+      const float gfl = sigmoidf_ref(v[5 * e + 1] + bias[H + j]);
+      const float gfr = sigmoidf_ref(v[5 * e + 2] + bias[2 * H + j]);
+      const float go = sigmoidf_ref(v[5 * e + 3] + bias[3 * H + j]);
+      const float gu = tanhf(v[5 * e + 4] + bias[4 * H + j]);
+      const float cv = gi * gu + gfl * (k1 ? s.cl[3 + e] : s.cl[e]) + gfr * (k1 ? s.cr[3 + e] : s.cr[e]);
+      const float hv = go * tanhf(cv);
+      c[(long long)n * H + j] = cv;
+      h[(long long)n * H + j] = hv;
+      if (xrow) xrow[j] = hv;
+    }
+  }
+  SKB_DEV void end_tile(State&, int, int, int, int, int) const {}
+};
+
+bool tree_engine(int H, int math) {
+  static int on = -1;
+  if (on < 0) { const char* e = getenv("SKB_TREE_TC"); on = (e && atoi(e) == 1) ? 1 : 0; }
+  return on && math == 1 && (H % 2) == 0;
+}
+
 }  // namespace
 
 extern "C" int64_t skb_tree_workspace_bytes(int nnodes, int ninternal, int hidden) {
   auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
-  return al(4ll * ninternal * 2 * hidden) + al(4ll * ninternal * 5 * hidden) + 2 * al(4ll * nnodes * hidden);
+  return al(4ll * ninternal * 2 * hidden) + al(4ll * ninternal * 5 * hidden) + 2 * al(4ll * nnodes * hidden) +
+         al(4ll * tree_np(hidden) * 2 * hidden);   // the engine's packed U
 }
 
 namespace {
@@ -159,7 +241,7 @@ namespace {
 bool enqueue_forest(cublasHandle_t hb, cudaStream_t cs, int nnodes, int nleaves, int ninternal, int H, int nlevels,
                     const int32_t* leaves, const int32_t* order, const int32_t* level_off_host, const int32_t* left,
                     const int32_t* right, const int32_t* dest, const float* value, const float* wc, const float* U,
-                    const float* bias, int math, float* h, float* c, float* X, float* G) {
+                    const float* bias, int math, float* h, float* c, float* X, float* G, float* Up) {
   const int blocks = 148 * 8;
   // float4 path when H % 4 == 0 (rows of 16-byte chunks); scalar path otherwise
   const bool v4 = (H & 3) == 0 && !getenv("SKB_TREE_SCALAR");
@@ -171,6 +253,25 @@ bool enqueue_forest(cublasHandle_t hb, cudaStream_t cs, int nnodes, int nleaves,
     tree_leaves4<<<lb, blk, 0, cs>>>(leaves, nleaves, value, wc, dest, h, c, X, H);
   else
     tree_leaves<<<lb, blk, 0, cs>>>(leaves, nleaves, value, wc, dest, h, c, X, H);
+  if (tree_engine(H, math)) {
+    namespace gm = skb::gemm;
+    constexpr int BN = kTreeBN, EW = kTreeEW;
+    using GT = gm::Geo<gm::kTF32, BN>;
+    const int NP = tree_np(H);
+    tree_pack_u<<<148 * 4, 256, 0, cs>>>(U, H, NP, Up);
+    CUtensorMap tb;
+    if (!gm::encode_2d(&tb, gm::kTF32, Up, 2 * H, NP, 2 * H, GT::BK, BN)) return false;
+    for (int L = 0; L < nlevels; ++L) {
+      const int r0 = level_off_host[L], nr = level_off_host[L + 1] - r0;
+      if (nr <= 0) continue;
+      CUtensorMap ta;
+      if (!gm::encode_2d(&ta, gm::kTF32, X + (int64_t)r0 * 2 * H, 2 * H, nr, 2 * H, GT::BK, GT::BM)) return false;
+      EpiTree e{order, left, right, dest, bias, h, c, X, H, r0, nr};
+      gm::Shape sh{nr, NP, 2 * H, 1, 0};
+      if (gm::launch<gm::kTF32, BN, false, false, EpiTree, false, EW>(ta, tb, sh, e, cs)) return false;
+    }
+    return cudaPeekAtLastError() == cudaSuccess;
+  }
   for (int L = 0; L < nlevels; ++L) {
     const int r0 = level_off_host[L], nr = level_off_host[L + 1] - r0;
     if (nr <= 0) continue;
@@ -218,6 +319,7 @@ extern "C" skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int 
   float* G = (float*)(ws + al(4ll * ninternal * 2 * H));
   float* h = h_out ? h_out : (float*)(ws + al(4ll * ninternal * 2 * H) + al(4ll * ninternal * 5 * H));
   float* c = c_out ? c_out : h + (int64_t)nnodes * H;
+  float* Up = (float*)(ws + al(4ll * ninternal * 2 * H) + al(4ll * ninternal * 5 * H) + 2 * al(4ll * nnodes * H));
   cublasHandle_t hb = skb::blas_handle(cs);
   if (!hb) return SKB_ERR_CUDA;
   const void* key[13] = {leaves, order, left, right, dest, value, wc, U, bias, h, c, workspace, nullptr};
@@ -254,7 +356,7 @@ extern "C" skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int 
     if (ok) {
       cublasSetStream(hb, cap);
       const bool enq = enqueue_forest(hb, cap, nnodes, nleaves, ninternal, H, nlevels, leaves, order, level_off_host,
-                                      left, right, dest, value, wc, U, bias, math, h, c, X, G);
+                                      left, right, dest, value, wc, U, bias, math, h, c, X, G, Up);
       ok = cudaStreamEndCapture(cap, &g) == cudaSuccess && enq;
     }
     if (ok) ok = cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
@@ -283,7 +385,7 @@ extern "C" skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int 
   if (exec) {
     if (cudaGraphLaunch(exec, cs) != cudaSuccess) return SKB_ERR_CUDA;
   } else if (!enqueue_forest(hb, cs, nnodes, nleaves, ninternal, H, nlevels, leaves, order, level_off_host, left,
-                             right, dest, value, wc, U, bias, math, h, c, X, G)) {
+                             right, dest, value, wc, U, bias, math, h, c, X, G, Up)) {
     return SKB_ERR_CUDA;
   }
   return skb_check_launch();
