@@ -35,6 +35,8 @@ def _dev(a, dt=torch.float32):
     (16, 20, 32, 64, "fp32", 1e-4, False),
     (64, 33, 64, 128, "tf32", 3e-2, True),
     (64, 33, 64, 128, "bf16", 6e-2, True),
+    (256, 40, 128, 256, "bf16", 6e-2, True),   # B % 256 == 0: the CTA-pair forward step kernel
+    (512, 24, 72, 96, "bf16", 6e-2, False),    # F % 64 != 0: partial pre-barrier K blocks
 ])
 def test_train_step_matches_oracle(B, T, F, H, math, tol, graph):
     x, y, h0, c0, lens, W, U, b = _problem(B, T, F, H, B + T)
@@ -89,3 +91,33 @@ def test_sgd_step_and_replay():
     W2, U2, b2 = (v.cpu().numpy().astype(np.float64) for v in tr.views(torch.from_numpy(p1.astype(np.float32))))
     ref2 = bptt.forward_backward(x, h0, c0, lens, y, W2, U2, b2, 1.0 / B)[0]
     assert abs(l2 - ref2) < 1e-4
+
+
+@pytest.mark.parametrize("env", [{"SKB_TC_FWD_KS": "2"}, {"SKB_TC_BWD_KS": "1"}, {"SKB_TC_PAIR_FWD": "0"},
+                                 {"SKB_TC_PAIR": "0"}])
+def test_step_kernel_variants_match_oracle(env):
+    """The C2 engine's alternative step kernels (split-K forward over a CTA cluster, 1-CTA
+    backward tiles, 1-CTA forward tiles, 1-CTA gradient GEMM) against the oracle; the switches
+    are read once per process, so each runs in a child."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "from test_gpu_train import _problem, _dev\n"
+        "from oracle import bptt\n"
+        "from paper_1810_08061_b200.train import LstmTrainer\n"
+        "B, T, F, H = 256, 30, 128, 256\n"
+        "x, y, h0, c0, lens, W, U, b = _problem(B, T, F, H, 3)\n"
+        "loss_ref, dW, dU, db = bptt.forward_backward(x, h0, c0, lens, y, W, U, b, 1.0 / B)\n"
+        "tr = LstmTrainer(F, H, B, T, global_batch=B, lr=0.0, math='bf16', graph=True,\n"
+        "                 params=np.concatenate([W.reshape(-1), U.reshape(-1), b]))\n"
+        "loss = tr.forward_backward(_dev(x), _dev(y), _dev(lens, torch.int64), _dev(h0), _dev(c0))\n"
+        "assert abs(float(loss.item()) - loss_ref) <= 6e-2 * max(1.0, abs(loss_ref))\n"
+        "for got, ref in zip((t.cpu().numpy().astype(np.float64) for t in tr.views(tr.grads)), (dW, dU, db)):\n"
+        "    assert np.max(np.abs(got - ref)) <= 6e-2 * max(1.0, np.max(np.abs(ref)))\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]), **env)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
