@@ -279,13 +279,17 @@ __global__ void __launch_bounds__(TPB) maml_task_kernel(int H_, int K_, int P, c
   const int KH = K * H;
   const int PP = P + H;          // padded block (w2 rows of H + 1)
   float* th_p = sm;              // PP
-  float* th2_p = th_p + PP;      // PP adapted weights
-  float* gs_p = th2_p + PP;      // PP support gradient, then reused for H_s v
+  // gs_p: the support gradient, turned in place into the adapted weights theta' (the gradient
+  // itself is not read again), then -- once the query pass is done with theta' -- H_s v.
+  // The R-operator's R{a1} / R{a2} reuse the query pass's z / a buffers (dead by then).
+  // 3 PP + 12 KH floats: five CTAs per SM at H = 40, K = 10.
+  float* gs_p = th_p + PP;
   float* gq_p = gs_p + PP;       // PP query gradient (= v)
-  float* z1 = gq_p + PP; float* a1 = z1 + KH; float* z2 = a1 + KH; float* a2 = z2 + KH;
+  float* z1 = sm + ((3 * PP + 3) & ~3);   // activations 16-byte aligned (float4 reads)
+  float* a1 = z1 + KH; float* z2 = a1 + KH; float* a2 = z2 + KH;
   float* dz1 = a2 + KH; float* dz2 = dz1 + KH;
   float* q1 = dz2 + KH; float* qa1 = q1 + KH; float* q2 = qa1 + KH; float* qa2 = q2 + KH;
-  float* r1 = qa2 + KH; float* r2 = r1 + KH; float* rd2 = r2 + KH; float* rd1 = rd2 + KH;
+  float* r1 = q1; float* r2 = qa1; float* rd2 = qa2 + KH; float* rd1 = rd2 + KH;
   float* x = rd1 + KH; float* y = x + KMAXT; float* xqs = y + KMAXT; float* yqs = xqs + KMAXT;
   float* p = yqs + KMAXT; float* dp = p + KMAXT; float* rp = dp + KMAXT; float* rdp = rp + KMAXT;
   for (int i = threadIdx.x; i < PP; i += TPB) th_p[i] = 0.f;
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(TPB) maml_task_kernel(int H_, int K_, int P, c
     xqs[k] = xq[(long long)task * K + k]; yqs[k] = yq[(long long)task * K + k];
   }
   __syncthreads();
-  const Theta th = view(th_p, H), th2 = view(th2_p, H), gs = view(gs_p, H), gq = view(gq_p, H);
+  const Theta th = view(th_p, H), th2 = view(gs_p, H), gs = view(gs_p, H), gq = view(gq_p, H);
   const float inv_k = 1.f / (float)K;
   constexpr bool TILED = HC > 0 && KC > 0 && HC % 4 == 0 && KC % 2 == 0;
   // support pass
@@ -310,7 +314,7 @@ __global__ void __launch_bounds__(TPB) maml_task_kernel(int H_, int K_, int P, c
   __syncthreads();
   if constexpr (TILED) backward_t<HC, KC>(x, th, z1, a1, z2, a2, dp, dz1, dz2, gs);
   else backward(x, th, z1, a1, z2, a2, dp, dz1, dz2, gs, K, H);
-  for (int i = threadIdx.x; i < PP; i += TPB) th2_p[i] = th_p[i] - alpha * gs_p[i];
+  for (int i = threadIdx.x; i < PP; i += TPB) gs_p[i] = th_p[i] - alpha * gs_p[i];   // theta', in place
   __syncthreads();
   // query pass at theta'
   layer1(xqs, th2.w1, th2.b1, q1, qa1, K, H);
@@ -437,7 +441,7 @@ __global__ void maml_reduce_final(const double* __restrict__ part, int n, int P,
 
 size_t smem_for(int H, int K) {
   const int P = H * H + 4 * H + 1;
-  return sizeof(float) * (4 * (size_t)(P + H) + 14 * (size_t)K * H + 8 * KMAXT);
+  return sizeof(float) * ((3 * (size_t)(P + H) + 3) / 4 * 4 + 12 * (size_t)K * H + 8 * KMAXT);
 }
 
 }  // namespace
@@ -460,6 +464,8 @@ extern "C" skb_status skb_maml_meta_grad(int hidden, int shots, int tasks, const
   auto kern = hidden == 40 ? (shots == 10 ? maml_task_kernel<40, 10> : maml_task_kernel<40, 0>) : maml_task_kernel<0, 0>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return SKB_ERR_CUDA;
+  // all of the unified L1 / shared array as shared memory: five task CTAs per SM at H = 40
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   kern<<<tasks, TPB, sm, cs>>>(hidden, shots, P, theta, xs, ys, xq, yq, alpha, task_grad, task_loss);
   double* part = (double*)(((uintptr_t)(task_loss + tasks) + 15) & ~(uintptr_t)15);
   maml_reduce_partial<<<dim3((P + 256) / 256, kTaskChunks), 256, 0, cs>>>(task_grad, task_loss, tasks, P, part);
