@@ -493,17 +493,18 @@ SKB_DEV void step_trace(const StepShape& sh, int st, int slot) {
   }
 }
 
-// KS = 2: every output tile is computed by two CTAs, each over half of K (fewer, wider
-// tiles for the same CTA count: the activations / weights are re-read by fewer tiles).
-// The partial sums are exchanged through L2: each CTA publishes the half of its
-// accumulator columns that its partner finishes, and runs the epilogue on the other
-// half (the epilogue functor sees tiles of BN / 2 columns, tile index 2 tn + ks).
+// KS = 2 or 4: every output tile is computed by KS CTAs of one cluster, each over 1/KS of K
+// (fewer, wider tiles for the same CTA count: the activations / weights are re-read by fewer
+// tiles).  The partial sums are reduce-scattered through distributed shared memory: each CTA
+// writes every partner's BN / KS accumulator columns into that partner's receive buffer and
+// runs the epilogue on its own columns (the epilogue functor sees tiles of BN / KS columns,
+// tile index KS tn + ks).
 // Step st + 1 arms its first stages with the weight (B) k-blocks before the grid
 // barrier; the activation (A) halves follow once the barrier is passed.
-// Steps-kernel geometry: behind the epilogue operands, KS = 2 keeps a [128][BN / 2] fp32
-// receive buffer for the partner's partial sums; the budget runs to the 227 KB limit.
+// Steps-kernel geometry: behind the epilogue operands, KS > 1 keeps KS - 1 [128][BN / KS] fp32
+// receive buffers for the partners' partial sums; the budget runs to the 227 KB limit.
 template <int ELEM, int BN, class Epi, int KS>
-using StepGeo = Geo<ELEM, BN, Epi::kOpBytes + (KS == 2 ? 128u * (BN / 2) * 4u : 0u), 224>;
+using StepGeo = Geo<ELEM, BN, Epi::kOpBytes + 128u * (BN / KS) * 4u * (KS - 1), 224>;
 
 template <int ELEM, int BN, class Epi, int EW, int KS = 1>
 __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) gemm_steps_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -533,7 +534,7 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * EW); }
     mbar_init(&opfull, 1);
     mbar_init(&opfree, 4 * EW);
-    mbar_init(&xfull, 4 * EW);
+    mbar_init(&xfull, 4 * EW * (KS > 1 ? KS - 1 : 1));
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -541,7 +542,7 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
   if (warp == 1) tmem_alloc<G::TMEM_COLS>(&tmem_s);
   tc_fence_before();
   __syncthreads();
-  if constexpr (KS == 2) cluster_sync();   // the partner's barriers exist before any DSMEM traffic
+  if constexpr (KS > 1) cluster_sync();   // the partners' barriers exist before any DSMEM traffic
   tc_fence_after();
   const uint32_t tmem = tmem_s;
 
@@ -666,26 +667,31 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
         if (warp == 2 && lane == 0) step_trace(sh, st, 4);
         tc_fence_after();
         const uint32_t dacc = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
-        if constexpr (KS == 2) {   // the partner's half of the partial sums -> its xrecv (DSMEM)
-          const uint32_t peer = cluster_ctarank() ^ 1u;
+        if constexpr (KS > 1) {   // each partner's columns of the partial sums -> its xrecv (DSMEM)
+          // (partner ks ^ o files this CTA's block in slot o - 1; cluster rank = ks)
           if (!kz) {   // (a step without MMAs still signals: the barrier phases advance every step)
-            const uint32_t xr = mapa(smem_u32(xrecv), peer) + (uint32_t)(r * BNE * 4);
 #pragma unroll 1
             for (int c = cg0; c < cg0 + BNE / EW; c += 16) {
-              float v[16];
-              tmem_ld16(dacc + (ks ^ 1) * BNE + c, v);
+              float v[KS - 1][16];
+#pragma unroll
+              for (int o = 1; o < KS; ++o) tmem_ld16(dacc + (ks ^ o) * BNE + c, v[o - 1]);   // all in flight
               tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 16; i += 4) {   // 16-byte chunks XOR-swizzled by row: conflict-free
-                const uint32_t q = (uint32_t)((c + i) >> 2) ^ (uint32_t)(r & 7);
-                asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};"
-                             :: "r"(xr + q * 16), "f"(v[i]), "f"(v[i + 1]), "f"(v[i + 2]), "f"(v[i + 3]) : "memory");
+              for (int o = 1; o < KS; ++o) {
+                const uint32_t xr = mapa(smem_u32(xrecv + ((o - 1) * 128 + r) * BNE), (uint32_t)(ks ^ o));
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {   // 16-byte chunks XOR-swizzled by row: conflict-free
+                  const uint32_t q = (uint32_t)((c + i) >> 2) ^ (uint32_t)(r & 7);
+                  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};"
+                               :: "r"(xr + q * 16), "f"(v[o - 1][i]), "f"(v[o - 1][i + 1]), "f"(v[o - 1][i + 2]),
+                                  "f"(v[o - 1][i + 3]) : "memory");
+                }
               }
             }
           }
           __syncwarp();
-          if (lane == 0) mbar_remote_arrive(mapa(smem_u32(&xfull), peer));   // release.cluster: the stores above
-          mbar_wait_cluster(&xfull, st & 1);                                 // acquire: the partner's stores
+          if (lane < KS - 1) mbar_remote_arrive(mapa(smem_u32(&xfull), (uint32_t)(ks ^ (lane + 1))));   // release
+          mbar_wait_cluster(&xfull, st & 1);   // acquire: every partner's stores
         }
         if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
         if (warp == 2 && lane == 0) step_trace(sh, st, 5);
@@ -697,12 +703,15 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
           if (kz) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
-          } else if constexpr (KS == 2) {
+          } else if constexpr (KS > 1) {
 #pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-              const uint32_t q = (uint32_t)((c + i) >> 2) ^ (uint32_t)(r & 7);
-              const float4 p = *reinterpret_cast<const float4*>(xrecv + r * BNE + q * 4);
-              v[i] += p.x; v[i + 1] += p.y; v[i + 2] += p.z; v[i + 3] += p.w;
+            for (int o = 1; o < KS; ++o) {   // partners in rank order ks ^ 1, ks ^ 2, ...
+#pragma unroll
+              for (int i = 0; i < 16; i += 4) {
+                const uint32_t q = (uint32_t)((c + i) >> 2) ^ (uint32_t)(r & 7);
+                const float4 p = *reinterpret_cast<const float4*>(xrecv + ((o - 1) * 128 + r) * BNE + q * 4);
+                v[i] += p.x; v[i + 1] += p.y; v[i + 2] += p.z; v[i + 3] += p.w;
+              }
             }
           }
           const int n0 = tn * BN + ks * BNE + c;
@@ -732,7 +741,7 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (KS == 2) cluster_sync();   // no CTA leaves while its partner may still write to it
+  if constexpr (KS > 1) cluster_sync();   // no CTA leaves while a partner may still write to it
   tc_fence_after();
   if (warp == 1) tmem_dealloc<G::TMEM_COLS>(tmem);
 }

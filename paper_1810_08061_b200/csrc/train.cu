@@ -439,9 +439,18 @@ namespace {
 // math == 2 (bf16): the tensor-core path of train_tc.cu (skb's own tcgen05 GEMMs with the
 // cell fused into their epilogues); SKB_TRAIN_CUBLAS=1 keeps the round-1 cuBLAS bf16 path.
 bool use_tc(const skb_train_shape* d) {
-  static int v = -1;
-  if (v < 0) { const char* e = getenv("SKB_TRAIN_CUBLAS"); v = (e && atoi(e) == 1) ? 0 : 1; }
-  return v == 1 && d->math == 2 && d->input % 8 == 0 && d->hidden % 32 == 0;
+  static int v = -1, sms = 0;
+  if (v < 0) {
+    const char* e = getenv("SKB_TRAIN_CUBLAS");
+    v = (e && atoi(e) == 1) ? 0 : 1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+    cudaGetLastError();
+  }
+  // the persistent step kernels keep one CTA per (128-row tile, 32 hidden units) resident
+  const long long ctas = (long long)((d->rows + 127) / 128) * (d->hidden / 32);
+  return v == 1 && d->math == 2 && d->input % 8 == 0 && d->hidden % 32 == 0 && ctas <= sms;
 }
 }  // namespace
 

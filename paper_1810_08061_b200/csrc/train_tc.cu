@@ -451,7 +451,7 @@ int fwd_ks() {
 }
 int bwd_ks() {
   static int v = -1;
-  if (v < 0) { const char* e = getenv("SKB_TC_BWD_KS"); v = e ? atoi(e) : 2; }
+  if (v < 0) { const char* e = getenv("SKB_TC_BWD_KS"); v = e ? atoi(e) : 4; }
   return v;
 }
 
@@ -577,7 +577,12 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     long long* tb = trace_buf(T) ? g_trace + 8ll * g_trace_cap : nullptr;   // second half of the trace
     gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, tb};
     int rc;
-    if (bwd_ks() == 2 && (H % 64) == 0) {   // 64-unit tiles, each computed by two CTAs over K halves
+    const int ks = bwd_ks() == 4 && (H % 128) != 0 ? 2 : bwd_ks();   // (same CTA count for 4 / 2 / 1)
+    if (ks == 4) {   // 128-unit tiles, each computed by four CTAs over K quarters (a 4-CTA cluster)
+      CUtensorMap mUt4;
+      if (!gm::encode_2d(&mUt4, kBF16, w.Ut, G, H, G, 64, 128)) return SKB_ERR_INVALID;
+      rc = gm::launch_steps<kBF16, 128, EpiBwd, 2, 4>(mdG, mUt4, sh, e, cs);
+    } else if (ks == 2 && (H % 64) == 0) {   // 64-unit tiles, each computed by two CTAs over K halves
       CUtensorMap mUt2;
       if (!gm::encode_2d(&mUt2, kBF16, w.Ut, G, H, G, 64, 64)) return SKB_ERR_INVALID;
       rc = gm::launch_steps<kBF16, 64, EpiBwd, 2, 2>(mdG, mUt2, sh, e, cs);

@@ -37,6 +37,7 @@ def _dev(a, dt=torch.float32):
     (64, 33, 64, 128, "bf16", 6e-2, True),
     (256, 40, 128, 256, "bf16", 6e-2, True),   # B % 256 == 0: the CTA-pair forward step kernel
     (512, 24, 72, 96, "bf16", 6e-2, False),    # F % 64 != 0: partial pre-barrier K blocks
+    (2432, 4, 8, 256, "bf16", 6e-2, True),     # 152 step-kernel CTAs > 148 SMs: the cuBLAS bf16 path
 ])
 def test_train_step_matches_oracle(B, T, F, H, math, tol, graph):
     x, y, h0, c0, lens, W, U, b = _problem(B, T, F, H, B + T)
@@ -94,7 +95,7 @@ def test_sgd_step_and_replay():
 
 
 @pytest.mark.parametrize("env", [{"SKB_TC_FWD_KS": "2"}, {"SKB_TC_BWD_KS": "1"}, {"SKB_TC_PAIR_FWD": "0"},
-                                 {"SKB_TC_PAIR": "0"}])
+                                 {"SKB_TC_PAIR": "0"}, {"SKB_TC_BWD_KS": "2"}])
 def test_step_kernel_variants_match_oracle(env):
     """The C2 engine's alternative step kernels (split-K forward over a CTA cluster, 1-CTA
     backward tiles, 1-CTA forward tiles, 1-CTA gradient GEMM) against the oracle; the switches
