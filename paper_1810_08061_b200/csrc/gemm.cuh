@@ -313,9 +313,9 @@ SKB_DEV void umma_ss_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint3
                  :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(id), "r"(accumulate) : "memory");
   }
 }
-SKB_DEV void umma_commit_pair(uint64_t* bar) {
+SKB_DEV void umma_commit_pair(uint64_t* bar, uint16_t mask = 3) {   // mask: the pair's cluster ranks
   asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-               :: "r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
+               :: "r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 
 template <int ELEM, int BN, bool AMN, bool BMN, class Epi, int EW = 1>
@@ -746,30 +746,41 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
   if (warp == 1) tmem_dealloc<G::TMEM_COLS>(tmem);
 }
 
-// CTA-pair form of gemm_steps_kernel (KS = 1): each cluster of two CTAs computes a 256 x BN
-// tile of every step with cta_group::2 MMAs (the B = weights tile is split between the two
-// CTAs: half the per-CTA weight traffic); the epilogue functor sees the CTA's own 128-row
-// tile (tile row 2 tm + rank).  Cooperative launch with static cluster dims.
-template <int ELEM, int BN, class Epi, int EW>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
+// CTA-pair form of gemm_steps_kernel: each pair of CTAs computes a 256 x BN tile of every
+// step with cta_group::2 MMAs (the B = weights tile is split between the two CTAs: half the
+// per-CTA weight traffic); the epilogue functor sees the CTA's own 128-row tile (tile row
+// 2 tm + rank).  KS = 2: two pairs (one 4-CTA cluster) share each tile, pair ks taking the K
+// blocks ks, ks + 2, ... (so both halves hold independent and dependent blocks), and the CTAs
+// with the same rows reduce-scatter their partial sums through DSMEM (the functor then sees
+// tiles of BN / 2 columns, index 2 tn + ks).  Cooperative launch with static cluster dims.
+template <int ELEM, int BN, class Epi, int EW, int KS = 1>
+using PairGeo = Geo<ELEM, BN / 2, Epi::kOpBytes + 128u * (BN / KS) * 4u * (KS - 1), (KS > 1 ? 224 : 212)>;
+
+template <int ELEM, int BN, class Epi, int EW, int KS = 1>
+__global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
     gemm_steps_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const StepShape sh, const __grid_constant__ Epi epi) {
-  using G = Geo<ELEM, BN / 2, Epi::kOpBytes>;
-  static_assert((BN / EW) % 16 == 0, "epilogue column groups are multiples of 16");
+  using G = PairGeo<ELEM, BN, Epi, EW, KS>;
+  constexpr int BNE = BN / KS;   // epilogue columns per CTA
+  static_assert((BNE / EW) % 16 == 0, "epilogue column groups are multiples of 16");
   constexpr uint32_t TMEM_COLS = BN * 2 <= 256 ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sop = smem + G::S * G::STAGE;
-  __shared__ uint64_t full[G::S], empty[G::S], tfull[2], tempty[2], opfull, opfree;
+  float* xrecv = reinterpret_cast<float*>(sop + Epi::kOpBytes);   // KS = 2: the partner's partial sums
+  __shared__ uint64_t full[G::S], empty[G::S], tfull[2], tempty[2], opfull, opfree, xfull;
   __shared__ uint32_t tmem_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1u, base = crank & ~1u;   // rank in the pair; the pair's leader
+  const int ks = (int)(crank >> 1);                        // K share (0 when KS = 1)
   const bool leader = rank == 0;
   const int tiles_n = (sh.N + BN - 1) / BN;
   const int kblocks = (sh.K + G::BK - 1) / G::BK;
+  const int nk = (kblocks - ks + KS - 1) / KS;   // this pair's K blocks: ks, ks + KS, ...
   const int units = ((sh.M + 255) / 256) * tiles_n;          // pair tiles
-  const int npairs = gridDim.x / 2, pair = blockIdx.x / 2;
-  const int per_step = 2 * units;   // one arrival per CTA per step
+  const int nclu = gridDim.x / (2 * KS), clu = blockIdx.x / (2 * KS);
+  const int per_step = gridDim.x;   // one arrival per CTA per step
   const int steps = sh.steps_dev ? *sh.steps_dev : sh.steps;
 
   if (threadIdx.x == 0) {
@@ -777,6 +788,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * 4 * EW); }
     mbar_init(&opfull, 1);
     mbar_init(&opfree, 4 * EW);
+    mbar_init(&xfull, 4 * EW);
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -796,31 +808,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
       for (int st = 0; st < steps; ++st) {
         const int ac = epi.a_coord(st);
         const bool kz = epi.k_empty(st);
-        for (int u = pair; u < units; u += npairs) {
+        for (int u = clu; u < units; u += nclu) {
           const int tm2 = u / tiles_n, tn = u % tiles_n, tmv = 2 * tm2 + (int)rank;
           const int row0 = tmv * 128, col0 = tn * BN + (int)rank * (BN / 2);
-          const bool first = u == pair;
+          const bool first = u == clu;
           if (first) step_trace(sh, st, 0);
           int npre = 0, nind = 0;
           int s0 = stage;
           if (st > 0 && first && !kz) {   // independent A blocks in full, then weights (as above)
-            nind = min(kblocks, epi.k_indep(st));
+            const int kind = min(kblocks, epi.k_indep(st));
+            nind = kind > ks ? min(nk, (kind - ks + KS - 1) / KS) : 0;
             for (int i = 0; i < nind; ++i) {
+              const int kb = ks + KS * i;
               mbar_wait_sleep(&empty[stage], ph ^ 1);
               if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE);
-              const uint32_t lbar = mapa(smem_u32(&full[stage]), 0);
+              const uint32_t lbar = mapa(smem_u32(&full[stage]), base);
               uint8_t* sa = smem + stage * G::STAGE;
-              tma_load_3d_pair(sa, &tmA, i * G::BK, row0, ac, lbar);
-              tma_load_2d_pair(sa + G::A_BYTES, &tmB, i * G::BK, col0, lbar);
+              tma_load_3d_pair(sa, &tmA, kb * G::BK, row0, ac, lbar);
+              tma_load_2d_pair(sa + G::A_BYTES, &tmB, kb * G::BK, col0, lbar);
               if (++stage == G::S) { stage = 0; ph ^= 1; }
             }
             s0 = stage;
-            npre = min(G::S, kblocks - nind);
+            npre = min(G::S, nk - nind);
             for (int i = 0; i < npre; ++i) {
               mbar_wait_sleep(&empty[stage], ph ^ 1);
               if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE);
-              tma_load_2d_pair(smem + stage * G::STAGE + G::A_BYTES, &tmB, (nind + i) * G::BK, col0,
-                               mapa(smem_u32(&full[stage]), 0));
+              tma_load_2d_pair(smem + stage * G::STAGE + G::A_BYTES, &tmB, (ks + KS * (nind + i)) * G::BK, col0,
+                               mapa(smem_u32(&full[stage]), base));
               if (++stage == G::S) { stage = 0; ph ^= 1; }
             }
           }
@@ -828,7 +842,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
             mbar_wait_sleep(&opfree, oph ^ 1);
             fence_proxy_async_global();
             mbar_arrive_expect_tx(&opfull, Epi::kOpBytes);
-            epi.prefetch(sop, st, tmv, tn, &opfull);
+            epi.prefetch(sop, st, tmv, tn * KS + ks, &opfull);
             oph ^= 1;
           }
           if (st > 0 && first) {
@@ -838,15 +852,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
           }
           if (first) step_trace(sh, st, 1);
           if (kz) continue;
-          for (int kb = nind; kb < kblocks; ++kb) {
-            if (kb - nind < npre) {
-              const int sidx = (s0 + kb - nind) % G::S;
-              tma_load_3d_pair(smem + sidx * G::STAGE, &tmA, kb * G::BK, row0, ac, mapa(smem_u32(&full[sidx]), 0));
+          for (int i = nind; i < nk; ++i) {
+            const int kb = ks + KS * i;
+            if (i - nind < npre) {
+              const int sidx = (s0 + i - nind) % G::S;
+              tma_load_3d_pair(smem + sidx * G::STAGE, &tmA, kb * G::BK, row0, ac, mapa(smem_u32(&full[sidx]), base));
               continue;
             }
             mbar_wait_sleep(&empty[stage], ph ^ 1);
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE);
-            const uint32_t lbar = mapa(smem_u32(&full[stage]), 0);
+            const uint32_t lbar = mapa(smem_u32(&full[stage]), base);
             uint8_t* sa = smem + stage * G::STAGE;
             tma_load_3d_pair(sa, &tmA, kb * G::BK, row0, ac, lbar);
             tma_load_2d_pair(sa + G::A_BYTES, &tmB, kb * G::BK, col0, lbar);
@@ -863,62 +878,92 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
     // ===================== MMA issuer (leader CTA, one thread)
     if (leader && lane == 0) {
       constexpr uint32_t id = idesc(ELEM, 256, BN, false, false);
+      const uint16_t pmask = (uint16_t)(3u << base);   // commits reach both CTAs of this pair
       int stage = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       for (int st = 0; st < steps; ++st) {
         const bool kz = epi.k_empty(st);
-        for (int u = pair; u < units; u += npairs) {
+        for (int u = clu; u < units; u += nclu) {
           mbar_wait_sleep(&tempty[acc], aph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + acc * BN;
           if (!kz) {
-            for (int kb = 0; kb < kblocks; ++kb) {
+            for (int i = 0; i < nk; ++i) {
               mbar_wait_sleep(&full[stage], ph);
-              if (kb == 0) step_trace(sh, st, 2);
+              if (i == 0) step_trace(sh, st, 2);
               tc_fence_after();
               const uint32_t sa = smem_u32(smem + stage * G::STAGE), sb = sa + G::A_BYTES;
 #pragma unroll
               for (int k = 0; k < G::BK / G::UK; ++k)
                 umma_ss_pair<ELEM>(d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), id,
-                                   (kb > 0 || k > 0) ? 1u : 0u);
-              umma_commit_pair(&empty[stage]);
+                                   (i > 0 || k > 0) ? 1u : 0u);
+              umma_commit_pair(&empty[stage], pmask);
               if (++stage == G::S) { stage = 0; ph ^= 1; }
             }
           }
           step_trace(sh, st, 3);
-          umma_commit_pair(&tfull[acc]);
+          umma_commit_pair(&tfull[acc], pmask);
           if (++acc == 2) { acc = 0; aph ^= 1; }
         }
       }
     }
   } else {
     // ===================== epilogue warps (each CTA: its 128 rows)
-    const int q = warp & 3, r = q * 32 + lane, cg0 = ((warp - 2) >> 2) * (BN / EW);
-    const uint32_t ltempty0 = mapa(smem_u32(&tempty[0]), 0), ltempty1 = mapa(smem_u32(&tempty[1]), 0);
+    const int q = warp & 3, r = q * 32 + lane, cg0 = ((warp - 2) >> 2) * (BNE / EW);
+    const uint32_t ltempty0 = mapa(smem_u32(&tempty[0]), base), ltempty1 = mapa(smem_u32(&tempty[1]), base);
     int acc = 0;
     uint32_t aph = 0, oph = 0;
     typename Epi::State es;   // lives across steps: a pair keeps its unit, so state may ride in registers
     for (int st = 0; st < steps; ++st) {
       const bool kz = epi.k_empty(st);
-      for (int u = pair; u < units; u += npairs) {
-        const int tm2 = u / tiles_n, tn = u % tiles_n, tmv = 2 * tm2 + (int)rank;
+      for (int u = clu; u < units; u += nclu) {
+        const int tm2 = u / tiles_n, tn = u % tiles_n, tmv = 2 * tm2 + (int)rank, tv = tn * KS + ks;
         const int m = tmv * 128 + r;
-        epi.begin_tile(es, st, tmv, tn, m);
+        epi.begin_tile(es, st, tmv, tv, m);
         mbar_wait_sleep(&tfull[acc], aph);
         if (warp == 2 && lane == 0) step_trace(sh, st, 4);
         tc_fence_after();
+        const uint32_t dacc = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
+        if constexpr (KS == 2) {   // the other pair's columns of these rows -> its xrecv (DSMEM)
+          const uint32_t peer = crank ^ 2u;
+          if (!kz) {
+#pragma unroll 1
+            for (int c = cg0; c < cg0 + BNE / EW; c += 16) {
+              float v[16];
+              tmem_ld16(dacc + (ks ^ 1) * BNE + c, v);
+              tmem_ld_wait();
+              const uint32_t xr = mapa(smem_u32(xrecv + r * BNE), peer);
+#pragma unroll
+              for (int i = 0; i < 16; i += 4) {   // 16-byte chunks XOR-swizzled by row: conflict-free
+                const uint32_t qq = (uint32_t)((c + i) >> 2) ^ (uint32_t)(r & 7);
+                asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};"
+                             :: "r"(xr + qq * 16), "f"(v[i]), "f"(v[i + 1]), "f"(v[i + 2]), "f"(v[i + 3]) : "memory");
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_remote_arrive(mapa(smem_u32(&xfull), peer));   // release.cluster
+          mbar_wait_cluster(&xfull, st & 1);                                 // acquire: the partner's stores
+        }
         if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
         if (warp == 2 && lane == 0) step_trace(sh, st, 5);
 #pragma unroll 1
-        for (int c = cg0; c < cg0 + BN / EW; c += 16) {
+        for (int c = cg0; c < cg0 + BNE / EW; c += 16) {
           float v[16];
-          tmem_ld16(tmem + acc * BN + c + ((uint32_t)(q * 32) << 16), v);
+          tmem_ld16(dacc + ks * BNE + c, v);
           tmem_ld_wait();
           if (kz) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          } else if constexpr (KS == 2) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              const uint32_t qq = (uint32_t)((c + i) >> 2) ^ (uint32_t)(r & 7);
+              const float4 p = *reinterpret_cast<const float4*>(xrecv + r * BNE + qq * 4);
+              v[i] += p.x; v[i + 1] += p.y; v[i + 2] += p.z; v[i + 3] += p.w;
+            }
           }
-          const int n0 = tn * BN + c;
+          const int n0 = tn * BN + ks * BNE + c;
           if (n0 < sh.N) epi.chunk(es, sop, st, r, m, n0, c, v, m < sh.M);
         }
         tc_fence_before();
@@ -928,7 +973,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
           if constexpr (Epi::kOpBytes > 0) mbar_arrive(&opfree);
         }
         oph ^= 1;
-        epi.end_tile(es, st, tmv, tn, warp - 2, lane);
+        epi.end_tile(es, st, tmv, tv, warp - 2, lane);
         if (warp == 2 && lane == 0) step_trace(sh, st, 6);
         // (no per-thread __threadfence: it is fence.sc.gpu + an L1 invalidate; the named barrier
         // orders every epilogue thread's stores before the single gpu-scope release below)
@@ -1063,11 +1108,11 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const Shape& sh, c
 }
 
 // Cooperative launch of gemm_steps_pair_kernel: one CTA pair per 256-row tile, all resident.
-template <int ELEM, int BN, class Epi, int EW>
+template <int ELEM, int BN, class Epi, int EW, int KS = 1>
 int launch_steps_pair(const CUtensorMap& ta, const CUtensorMap& tb, const StepShape& sh, const Epi& epi,
                       cudaStream_t st) {
-  using G = Geo<ELEM, BN / 2, Epi::kOpBytes>;
-  auto kern = gemm_steps_pair_kernel<ELEM, BN, Epi, EW>;
+  using G = PairGeo<ELEM, BN, Epi, EW, KS>;
+  auto kern = gemm_steps_pair_kernel<ELEM, BN, Epi, EW, KS>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess)
@@ -1075,12 +1120,12 @@ int launch_steps_pair(const CUtensorMap& ta, const CUtensorMap& tb, const StepSh
     attr = true;
   }
   const int units = ((sh.M + 255) / 256) * ((sh.N + BN - 1) / BN);
-  if (2 * units > num_sms()) return 3;
+  if (2 * KS * units > num_sms()) return 3;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute lattr[1];
   lattr[0].id = cudaLaunchAttributeCooperative;
   lattr[0].val.cooperative = 1;
-  cfg.gridDim = dim3(2 * units);
+  cfg.gridDim = dim3(2 * KS * units);
   cfg.blockDim = dim3(64 + 128 * EW);
   cfg.dynamicSmemBytes = G::SMEM;
   cfg.stream = st;

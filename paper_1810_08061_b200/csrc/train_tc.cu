@@ -550,7 +550,14 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     e.T = T; e.F = F; e.H = H; e.B = B; e.tiles_n = tiles_n; e.tiles = fwd_tiles(B, H); e.diag = diag();
     gm::StepShape sh{B, G, KX, 0, n_dev, w.sync, trace_buf(T)};
     int rc;
-    if (fwd_ks() == 2 && (G % 256) == 0) {   // 256-column tiles, each computed by two CTAs over K halves
+    if (fwd_ks() == 2 && pair_fwd() && (B % 256) == 0 && (G % 256) == 0) {
+      // 256 x 256 tiles, each computed by two CTA pairs (a 4-CTA cluster) over alternate K blocks
+      CUtensorMap mWUp, mXHp;
+      if (!gm::encode_2d(&mWUp, kBF16, w.WU, KX, G, KX, GF::BK, 128) ||
+          !gm::encode_3d(&mXHp, kBF16, w.XH, KX, B, T, KX, (uint64_t)B * KX, GF::BK, GF::BM, 1))
+        return SKB_ERR_INVALID;
+      rc = gm::launch_steps_pair<kBF16, 256, EpiFwd, kFwdEW, 2>(mXHp, mWUp, sh, e, cs);
+    } else if (fwd_ks() == 2 && (G % 256) == 0) {   // 256-column tiles, each computed by two CTAs over K halves
       CUtensorMap mWU2;
       if (!gm::encode_2d(&mWU2, kBF16, w.WU, KX, G, KX, GF::BK, 256)) return SKB_ERR_INVALID;
       rc = gm::launch_steps<kBF16, 256, EpiFwd, kFwdEW, 2>(mXH, mWU2, sh, e, cs);
