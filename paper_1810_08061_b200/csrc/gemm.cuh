@@ -1107,6 +1107,24 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const Shape& sh, c
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 2;
 }
 
+// Clusters of `kern` (launch shape `cfg`) that can be resident at once: the persistent step
+// kernels need every cluster co-resident (cached per kernel; INT_MAX if the query fails).
+template <class K>
+int resident_clusters(K kern, const cudaLaunchConfig_t& cfg) {
+  static const void* key[16];   // per kernel (instantiations of one signature share K)
+  static int val[16], cnt = 0;
+  for (int i = 0; i < cnt; ++i)
+    if (key[i] == (const void*)kern) return val[i];
+  cudaLaunchConfig_t q = cfg;
+  q.attrs = nullptr;
+  q.numAttrs = 0;
+  int c = 0;
+  const int n = cudaOccupancyMaxActiveClusters(&c, (void*)kern, &q) == cudaSuccess ? c : 0x7fffffff;
+  cudaGetLastError();
+  if (cnt < 16) { key[cnt] = (const void*)kern; val[cnt] = n; ++cnt; }
+  return n;
+}
+
 // Cooperative launch of gemm_steps_pair_kernel: one CTA pair per 256-row tile, all resident.
 template <int ELEM, int BN, class Epi, int EW, int KS = 1>
 int launch_steps_pair(const CUtensorMap& ta, const CUtensorMap& tb, const StepShape& sh, const Epi& epi,
@@ -1131,6 +1149,7 @@ int launch_steps_pair(const CUtensorMap& ta, const CUtensorMap& tb, const StepSh
   cfg.stream = st;
   cfg.attrs = lattr;
   cfg.numAttrs = 1;
+  if (units > resident_clusters(kern, cfg)) return 3;   // not all clusters co-resident
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, sh, epi) == cudaSuccess ? 0 : 2;
 }
 
@@ -1157,6 +1176,7 @@ int launch_steps(const CUtensorMap& ta, const CUtensorMap& tb, const StepShape& 
   cfg.stream = st;
   cfg.attrs = lattr;
   cfg.numAttrs = 1;
+  if (nunits / KS > resident_clusters(kern, cfg)) return 3;   // not all clusters co-resident
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, sh, epi) == cudaSuccess ? 0 : 2;
 }
 

@@ -567,6 +567,7 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
           !gm::encode_3d(&mXHp, kBF16, w.XH, KX, B, T, KX, (uint64_t)B * KX, GF::BK, GF::BM, 1))
         return SKB_ERR_INVALID;
       rc = gm::launch_steps_pair<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXHp, mWUp, sh, e, cs);
+      if (rc == 3) rc = gm::launch_steps<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXH, mWU, sh, e, cs);   // pairs not all resident
     } else {
       rc = gm::launch_steps<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXH, mWU, sh, e, cs);
     }
@@ -584,18 +585,21 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     long long* tb = trace_buf(T) ? g_trace + 8ll * g_trace_cap : nullptr;   // second half of the trace
     gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, tb};
     int rc;
-    const int ks = bwd_ks() == 4 && (H % 128) != 0 ? 2 : bwd_ks();   // (same CTA count for 4 / 2 / 1)
+    // (same CTA count for 4 / 2 / 1; a split whose clusters cannot all be resident falls back)
+    int ks = bwd_ks() == 4 && (H % 128) != 0 ? 2 : bwd_ks();
+    rc = 3;
     if (ks == 4) {   // 128-unit tiles, each computed by four CTAs over K quarters (a 4-CTA cluster)
       CUtensorMap mUt4;
       if (!gm::encode_2d(&mUt4, kBF16, w.Ut, G, H, G, 64, 128)) return SKB_ERR_INVALID;
       rc = gm::launch_steps<kBF16, 128, EpiBwd, 2, 4>(mdG, mUt4, sh, e, cs);
-    } else if (ks == 2 && (H % 64) == 0) {   // 64-unit tiles, each computed by two CTAs over K halves
+      if (rc == 3) ks = 2;
+    }
+    if (rc == 3 && ks == 2 && (H % 64) == 0) {   // 64-unit tiles, each computed by two CTAs over K halves
       CUtensorMap mUt2;
       if (!gm::encode_2d(&mUt2, kBF16, w.Ut, G, H, G, 64, 64)) return SKB_ERR_INVALID;
       rc = gm::launch_steps<kBF16, 64, EpiBwd, 2, 2>(mdG, mUt2, sh, e, cs);
-    } else {
-      rc = gm::launch_steps<kBF16, 32, EpiBwd, 2>(mdG, mUt, sh, e, cs);
     }
+    if (rc == 3) rc = gm::launch_steps<kBF16, 32, EpiBwd, 2>(mdG, mUt, sh, e, cs);
     if (rc) return rc == 3 ? SKB_ERR_UNSUPPORTED : SKB_ERR_CUDA;
   }
   zero_dg_tail<<<blocks, 256, 0, cs>>>(w.dG, n_dev, B, T, G);
