@@ -206,6 +206,11 @@ int skb_tree_last_mode(void);   /* 1 = the last skb_tree_lstm replayed a capture
  * Returns the maximum height, or -1 for a node with exactly one child. */
 int skb_tree_schedule(int64_t nnodes, const int64_t* left, const int64_t* right, int32_t* height,
                       int32_t* order, int32_t* level_off, int32_t* leaves, int32_t* dest);
+/* Forest form: concatenated trees with tree-local child indices; writes global int32 child ids.
+ * Replaces the per-tree recursion of the reference's Tree values (graph/execute.py:136-146). */
+int skb_forest_schedule(int64_t ntrees, const int64_t* sizes, const int64_t* left, const int64_t* right,
+                        int32_t* left_out, int32_t* right_out, int32_t* height, int32_t* order,
+                        int32_t* level_off, int32_t* leaves, int32_t* dest);
 skb_status skb_tree_lstm(int nnodes, int nleaves, int ninternal, int hidden, int nlevels, const int32_t* leaves_dev,
                          const int32_t* order_dev, const int32_t* level_off_host, const int32_t* left_dev,
                          const int32_t* right_dev, const int32_t* dest_dev, const float* value_dev,

@@ -434,3 +434,61 @@ extern "C" int skb_tree_schedule(int64_t n, const int64_t* left, const int64_t* 
   free(cnt);
   return maxh;
 }
+
+// Forest form of skb_tree_schedule: the trees' node arrays concatenated, child indices LOCAL to
+// each tree (pre-order, -1 for none, `sizes[t]` nodes each).  Two passes instead of five and no
+// separate global-index pass: heights (per tree, reverse pre-order) with the global int32 child
+// ids and per-height counts, then one forward pass that places every internal node in its
+// level (order), lists the leaves and writes each child's destination row/side at its parent
+// (children follow their parent in pre-order).  Returns max_height, or -1 for a node with one
+// child or a child index outside its tree / not after its parent.
+extern "C" int skb_forest_schedule(int64_t ntrees, const int64_t* sizes, const int64_t* left, const int64_t* right,
+                                   int32_t* left_out, int32_t* right_out, int32_t* height, int32_t* order,
+                                   int32_t* level_off, int32_t* leaves, int32_t* dest) {
+  int64_t cap = 64;
+  int64_t* cnt = (int64_t*)calloc((size_t)cap, sizeof(int64_t));
+  if (!cnt) return -1;
+  int maxh = 0;
+  int64_t b = 0;
+  for (int64_t t = 0; t < ntrees; ++t) {
+    const int64_t sz = sizes[t];
+    if (sz < 1) { free(cnt); return -1; }
+    dest[b] = -1;   // the tree's root
+    for (int64_t k = sz - 1; k >= 0; --k) {
+      const int64_t i = b + k, l = left[i], r = right[i];
+      if ((l < 0) != (r < 0)) { free(cnt); return -1; }
+      if (l < 0) { height[i] = 0; left_out[i] = right_out[i] = -1; continue; }
+      if (l <= k || r <= k || l >= sz || r >= sz) { free(cnt); return -1; }
+      const int32_t gl = (int32_t)(b + l), gr = (int32_t)(b + r);
+      const int h = 1 + (height[gl] > height[gr] ? height[gl] : height[gr]);
+      height[i] = h;
+      left_out[i] = gl;
+      right_out[i] = gr;
+      if (h >= cap) {
+        const int64_t nc = 2 * h;
+        int64_t* g = (int64_t*)realloc(cnt, (size_t)nc * sizeof(int64_t));
+        if (!g) { free(cnt); return -1; }
+        memset(g + cap, 0, (size_t)(nc - cap) * sizeof(int64_t));
+        cnt = g;
+        cap = nc;
+      }
+      ++cnt[h];
+      if (h > maxh) maxh = h;
+    }
+    b += sz;
+  }
+  const int64_t n = b;
+  int64_t acc = 0;
+  for (int h = 1; h <= maxh; ++h) { level_off[h - 1] = (int32_t)acc; acc += cnt[h]; cnt[h] = level_off[h - 1]; }
+  level_off[maxh] = (int32_t)acc;
+  int64_t nleaf = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (left_out[i] < 0) { leaves[nleaf++] = (int32_t)i; continue; }
+    const int32_t p = (int32_t)cnt[height[i]]++;
+    order[p] = (int32_t)i;
+    dest[left_out[i]] = 2 * p;
+    dest[right_out[i]] = 2 * p + 1;
+  }
+  free(cnt);
+  return maxh;
+}

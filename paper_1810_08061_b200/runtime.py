@@ -81,6 +81,7 @@ SIGNATURES = {
     "skb_tree_workspace_bytes": (ctypes.c_int64, [ctypes.c_int] * 3),
     "skb_tree_last_mode": (ctypes.c_int, []),
     "skb_tree_schedule": (ctypes.c_int, [ctypes.c_int64] + [_VP] * 7),
+    "skb_forest_schedule": (ctypes.c_int, [ctypes.c_int64] + [_VP] * 10),
     "skb_tree_lstm": (ctypes.c_int, [ctypes.c_int] * 5 + [_VP] * 10 + [ctypes.c_int, _VP, _VP, _VP, _VP]),
     "skb_train_workspace_bytes": (ctypes.c_int64, [ctypes.POINTER(TrainShape)]),
     "skb_lstm_train_step": (ctypes.c_int, [ctypes.POINTER(TrainShape)] + [_VP] * 8 + [ctypes.c_int, _VP, _VP]),

@@ -41,35 +41,33 @@ def _flatten_tree(t):
 
 class Forest:
     """Host schedule of a batch of binary trees (leaves: both children empty);
-    the O(nodes) scheduling pass is native (skb_tree_schedule in csrc/tree.cu)."""
+    the O(nodes) scheduling pass is native (skb_forest_schedule in csrc/tree.cu)."""
 
     def __init__(self, trees):
         flat = [t if isinstance(t, tuple) else _flatten_tree(t) for t in trees]
-        sizes = np.fromiter((len(f[0]) for f in flat), dtype=np.int64, count=len(flat))
+        vals, lefts, rights = (list(x) for x in zip(*flat)) if flat else ([], [], [])
+        sizes = np.fromiter(map(len, vals), dtype=np.int64, count=len(vals))
         bases = np.concatenate([[0], np.cumsum(sizes)[:-1]]) if len(flat) else np.zeros(0, np.int64)
-        shift = np.repeat(bases, sizes)   # every node's tree offset, one vectorised pass
         # (np.concatenate converts array-likes itself; one dtype cast per field)
-        self.value = np.concatenate([f[0] for f in flat]).astype(np.float64, copy=False)
-        left = np.concatenate([f[1] for f in flat]).astype(np.int64, copy=False)
-        right = np.concatenate([f[2] for f in flat]).astype(np.int64, copy=False)
-        self.left = np.where(left >= 0, left + shift, -1)
-        self.right = np.where(right >= 0, right + shift, -1)
+        self.value = np.concatenate(vals).astype(np.float64, copy=False) if flat else np.zeros(0)
+        left = np.ascontiguousarray(np.concatenate(lefts) if flat else np.zeros(0), dtype=np.int64)
+        right = np.ascontiguousarray(np.concatenate(rights) if flat else np.zeros(0), dtype=np.int64)
         self.roots = bases.astype(np.int64)
         n = len(self.value)
         from . import runtime as rt
         lib = rt.host_lib()   # the scheduler is host code
+        self.left = np.empty(n, dtype=np.int32)    # global child ids (-1: none)
+        self.right = np.empty(n, dtype=np.int32)
         self.height = np.empty(n, dtype=np.int32)
         order = np.empty(n, dtype=np.int32)
         level_off = np.empty(n + 1, dtype=np.int32)
         leaves = np.empty(n, dtype=np.int32)
         self.dest = np.empty(n, dtype=np.int32)
         c = lambda a: a.ctypes.data_as(ctypes.c_void_p)
-        self.left = np.ascontiguousarray(self.left, dtype=np.int64)
-        self.right = np.ascontiguousarray(self.right, dtype=np.int64)
-        maxh = lib.skb_tree_schedule(n, c(self.left), c(self.right), c(self.height), c(order), c(level_off),
-                                     c(leaves), c(self.dest))
+        maxh = lib.skb_forest_schedule(len(flat), c(sizes), c(left), c(right), c(self.left), c(self.right),
+                                       c(self.height), c(order), c(level_off), c(leaves), c(self.dest))
         if maxh < 0:
-            raise ValueError("TreeLSTM trees must be full binary trees (0 or 2 children)")
+            raise ValueError("TreeLSTM trees must be full binary trees (0 or 2 children, listed in pre-order)")
         self.nlevels = int(maxh)
         self.level_off = level_off[:maxh + 1].copy()
         ninternal = int(self.level_off[-1]) if maxh > 0 else 0
