@@ -215,6 +215,10 @@ __global__ void __launch_bounds__(ROW_THREADS) beam_rows(DecodeState st, int V, 
   int li = 0x7fffffff;
   float thr = -INFINITY;
   int thr_i = 0x7fffffff;
+  // floor: a value with at least K elements >= it already seen (the K-th largest lane maximum of
+  // the warp's first chunk), so while the list still holds -inf entries the threshold does not
+  // drop below it and the first chunk offers a handful of candidates instead of all of them
+  float fl = -INFINITY;
   auto offer = [&](float x, int v) {
     unsigned m = __ballot_sync(0xffffffffu, better(x, v, thr, thr_i));
     while (m) {
@@ -231,6 +235,7 @@ __global__ void __launch_bounds__(ROW_THREADS) beam_rows(DecodeState st, int V, 
       else if (lane > pos && lane < K) { lv = uv; li = ui; }
       thr = __shfl_sync(0xffffffffu, lv, K - 1);
       thr_i = __shfl_sync(0xffffffffu, li, K - 1);
+      if (fl > thr) { thr = fl; thr_i = 0x7fffffff; }
     }
   };
   // Chunks of 4*U values per lane: one max per chunk rescales the running sum
@@ -265,6 +270,19 @@ __global__ void __launch_bounds__(ROW_THREADS) beam_rows(DecodeState st, int V, 
     if (cm != -INFINITY) {
 #pragma unroll
       for (int e = 0; e < 4 * U; ++e) sum += __expf(x[e] - mx);
+    }
+    if (thr == -INFINITY && fl == -INFINITY) {   // warp-uniform: the first chunk with values
+      float c = cm, m = -INFINITY;
+#pragma unroll 1
+      for (int k = 0; k < K; ++k) {   // K-th largest of the lanes' chunk maxima
+        m = c;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const unsigned b = __ballot_sync(0xffffffffu, c == m);
+        if (lane == __ffs(b) - 1) c = -INFINITY;
+      }
+      fl = m;
+      if (fl > thr) { thr = fl; thr_i = 0x7fffffff; }
     }
     if (__any_sync(0xffffffffu, cm >= thr && cm != -INFINITY)) {
 #pragma unroll
