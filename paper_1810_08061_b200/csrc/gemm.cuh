@@ -483,10 +483,11 @@ struct StepShape {
   int steps;
   const int* steps_dev;   // non-null: the step count is read from device memory (a device-side trip count)
   int* sync;      // zeroed before the launch
-  long long* trace;   // optional: per-step globaltimer stamps of CTA 0 ([steps][8]), else null
+  long long* trace;   // optional: per-step globaltimer stamps of CTA trace_cta ([steps][8]), else null
+  int trace_cta;
 };
 SKB_DEV void step_trace(const StepShape& sh, int st, int slot) {
-  if (sh.trace && blockIdx.x == 0) {
+  if (sh.trace && (int)blockIdx.x == sh.trace_cta) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     sh.trace[(long long)st * 8 + slot] = (long long)t;
@@ -534,7 +535,7 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * EW); }
     mbar_init(&opfull, 1);
     mbar_init(&opfree, 4 * EW);
-    mbar_init(&xfull, 4 * EW * (KS > 1 ? KS - 1 : 1));
+    mbar_init(&xfull, 1);   // KS > 1: one local expect_tx arrival per step; partners' st.async complete_tx
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -668,8 +669,12 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
         tc_fence_after();
         const uint32_t dacc = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
         if constexpr (KS > 1) {   // each partner's columns of the partial sums -> its xrecv (DSMEM)
-          // (partner ks ^ o files this CTA's block in slot o - 1; cluster rank = ks)
-          if (!kz) {   // (a step without MMAs still signals: the barrier phases advance every step)
+          // (partner ks ^ o files this CTA's block in slot o - 1; cluster rank = ks).  st.async:
+          // each 16-byte store completes its bytes on the receiver's xfull, whose one local
+          // arrival per step announces the bytes to expect -- no release fence, no arrivals
+          if (warp == 2 && lane == 0)
+            mbar_arrive_expect_tx(&xfull, kz ? 0u : (uint32_t)((KS - 1) * 128 * BNE * 4));
+          if (!kz) {   // (a step without MMAs still completes the phase: expect 0 bytes)
 #pragma unroll 1
             for (int c = cg0; c < cg0 + BNE / EW; c += 16) {
               float v[KS - 1][16];
@@ -678,20 +683,20 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
               tmem_ld_wait();
 #pragma unroll
               for (int o = 1; o < KS; ++o) {
-                const uint32_t xr = mapa(smem_u32(xrecv + ((o - 1) * 128 + r) * BNE), (uint32_t)(ks ^ o));
+                const uint32_t peer = (uint32_t)(ks ^ o);
+                const uint32_t xr = mapa(smem_u32(xrecv + ((o - 1) * 128 + r) * BNE), peer);
+                const uint32_t xb = mapa(smem_u32(&xfull), peer);
 #pragma unroll
                 for (int i = 0; i < 16; i += 4) {   // 16-byte chunks XOR-swizzled by row: conflict-free
                   const uint32_t q = (uint32_t)((c + i) >> 2) ^ (uint32_t)(r & 7);
-                  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};"
+                  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
                                :: "r"(xr + q * 16), "f"(v[o - 1][i]), "f"(v[o - 1][i + 1]), "f"(v[o - 1][i + 2]),
-                                  "f"(v[o - 1][i + 3]) : "memory");
+                                  "f"(v[o - 1][i + 3]), "r"(xb) : "memory");
                 }
               }
             }
           }
-          __syncwarp();
-          if (lane < KS - 1) mbar_remote_arrive(mapa(smem_u32(&xfull), (uint32_t)(ks ^ (lane + 1))));   // release
-          mbar_wait_cluster(&xfull, st & 1);   // acquire: every partner's stores
+          mbar_wait_cluster(&xfull, st & 1);   // every partner's bytes landed
         }
         if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
         if (warp == 2 && lane == 0) step_trace(sh, st, 5);

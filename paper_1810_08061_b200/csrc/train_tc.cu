@@ -584,6 +584,7 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
     e.n_dev = n_dev; e.T = T; e.H = H; e.B = B; e.inv_b = d->inv_batch; e.diag = diag();
     long long* tb = trace_buf(T) ? g_trace + 8ll * g_trace_cap : nullptr;   // second half of the trace
     gm::StepShape sh{B, H, G, 0, n_dev, w.sync + 1, tb};
+    { const char* v = getenv("SKB_TC_TRACE_CTA"); sh.trace_cta = v ? atoi(v) : 0; }
     int rc;
     // (same CTA count for 4 / 2 / 1; a split whose clusters cannot all be resident falls back)
     int ks = bwd_ks() == 4 && (H % 128) != 0 ? 2 : bwd_ks();
