@@ -793,7 +793,7 @@ __global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * 4 * EW); }
     mbar_init(&opfull, 1);
     mbar_init(&opfree, 4 * EW);
-    mbar_init(&xfull, 4 * EW);
+    mbar_init(&xfull, 1);   // KS = 2: one local expect_tx arrival per step; the partner's st.async bytes
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -929,26 +929,26 @@ __global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 
         if (warp == 2 && lane == 0) step_trace(sh, st, 4);
         tc_fence_after();
         const uint32_t dacc = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
-        if constexpr (KS == 2) {   // the other pair's columns of these rows -> its xrecv (DSMEM)
+        if constexpr (KS == 2) {   // the other pair's columns of these rows -> its xrecv (DSMEM, st.async)
           const uint32_t peer = crank ^ 2u;
+          if (warp == 2 && lane == 0) mbar_arrive_expect_tx(&xfull, kz ? 0u : (uint32_t)(128 * BNE * 4));
           if (!kz) {
+            const uint32_t xr = mapa(smem_u32(xrecv + r * BNE), peer), xb = mapa(smem_u32(&xfull), peer);
 #pragma unroll 1
             for (int c = cg0; c < cg0 + BNE / EW; c += 16) {
               float v[16];
               tmem_ld16(dacc + (ks ^ 1) * BNE + c, v);
               tmem_ld_wait();
-              const uint32_t xr = mapa(smem_u32(xrecv + r * BNE), peer);
 #pragma unroll
               for (int i = 0; i < 16; i += 4) {   // 16-byte chunks XOR-swizzled by row: conflict-free
                 const uint32_t qq = (uint32_t)((c + i) >> 2) ^ (uint32_t)(r & 7);
-                asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};"
-                             :: "r"(xr + qq * 16), "f"(v[i]), "f"(v[i + 1]), "f"(v[i + 2]), "f"(v[i + 3]) : "memory");
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+                             :: "r"(xr + qq * 16), "f"(v[i]), "f"(v[i + 1]), "f"(v[i + 2]), "f"(v[i + 3]), "r"(xb)
+                             : "memory");
               }
             }
           }
-          __syncwarp();
-          if (lane == 0) mbar_remote_arrive(mapa(smem_u32(&xfull), peer));   // release.cluster
-          mbar_wait_cluster(&xfull, st & 1);                                 // acquire: the partner's stores
+          mbar_wait_cluster(&xfull, st & 1);   // the partner's bytes landed
         }
         if constexpr (Epi::kOpBytes > 0) mbar_wait_sleep(&opfull, oph);
         if (warp == 2 && lane == 0) step_trace(sh, st, 5);
