@@ -301,6 +301,15 @@ SKB_DEV void tma_load_3d_pair(void* smem_dst, const CUtensorMap* tm, int c0, int
                " [%0], [%1, {%2, %3, %4}], [%5];"
                :: "r"(smem_u32(smem_dst)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar) : "memory");
 }
+// Multicast form: the box lands at the same offset in every CTA of `mask`; each destination's
+// bytes complete on its own pair leader's barrier (the .cta_group::2 signalling rule).
+SKB_DEV void tma_load_3d_pair_mc(void* smem_dst, const CUtensorMap* tm, int c0, int c1, int c2, uint32_t leader_bar,
+                                 uint16_t mask) {
+  asm volatile("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+               ".multicast::cluster [%0], [%1, {%2, %3, %4}], [%5], %6;"
+               :: "r"(smem_u32(smem_dst)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar), "h"(mask)
+               : "memory");
+}
 template <int ELEM>
 SKB_DEV void umma_ss_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t id, uint32_t accumulate) {
   if constexpr (ELEM == kBF16) {
@@ -761,11 +770,12 @@ __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1) g
 template <int ELEM, int BN, class Epi, int EW, int KS = 1>
 using PairGeo = Geo<ELEM, BN / 2, Epi::kOpBytes + 128u * (BN / KS) * 4u * (KS - 1), (KS > 1 ? 224 : 212)>;
 
-template <int ELEM, int BN, class Epi, int EW, int KS = 1>
-__global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
+template <int ELEM, int BN, class Epi, int EW, int KS = 1, int MC = 1>
+__global__ void __cluster_dims__(2 * KS * MC, 1, 1) __launch_bounds__(64 + 128 * EW, 1)
     gemm_steps_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const StepShape sh, const __grid_constant__ Epi epi) {
   using G = PairGeo<ELEM, BN, Epi, EW, KS>;
+  static_assert(KS == 1 || MC == 1, "split-K and A multicast are separate variants");
   constexpr int BNE = BN / KS;   // epilogue columns per CTA
   static_assert((BNE / EW) % 16 == 0, "epilogue column groups are multiples of 16");
   constexpr uint32_t TMEM_COLS = BN * 2 <= 256 ? 256 : 512;
@@ -778,18 +788,24 @@ __global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
   const uint32_t rank = crank & 1u, base = crank & ~1u;   // rank in the pair; the pair's leader
-  const int ks = (int)(crank >> 1);                        // K share (0 when KS = 1)
+  const int ks = KS > 1 ? (int)(crank >> 1) : 0;          // K share (0 when KS = 1)
+  // MC = 2: two pairs (a 4-CTA cluster) on adjacent column tiles of the same rows; each CTA
+  // loads half of its A box's rows and multicasts it to the CTA with the same rows in the
+  // other pair, so every stage slot is refilled only after both pairs consumed it
+  const int mcg = MC > 1 ? (int)(crank >> 1) : 0;
+  const uint16_t amask = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));
   const bool leader = rank == 0;
   const int tiles_n = (sh.N + BN - 1) / BN;
   const int kblocks = (sh.K + G::BK - 1) / G::BK;
   const int nk = (kblocks - ks + KS - 1) / KS;   // this pair's K blocks: ks, ks + KS, ...
-  const int units = ((sh.M + 255) / 256) * tiles_n;          // pair tiles
-  const int nclu = gridDim.x / (2 * KS), clu = blockIdx.x / (2 * KS);
+  const int tiles_c = tiles_n / MC;                            // column tiles per cluster
+  const int units = ((sh.M + 255) / 256) * tiles_c;          // cluster tiles
+  const int nclu = gridDim.x / (2 * KS * MC), clu = blockIdx.x / (2 * KS * MC);
   const int per_step = gridDim.x;   // one arrival per CTA per step
   const int steps = sh.steps_dev ? *sh.steps_dev : sh.steps;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < G::S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < G::S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MC); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * 4 * EW); }
     mbar_init(&opfull, 1);
     mbar_init(&opfree, 4 * EW);
@@ -814,9 +830,17 @@ __global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 
         const int ac = epi.a_coord(st);
         const bool kz = epi.k_empty(st);
         for (int u = clu; u < units; u += nclu) {
-          const int tm2 = u / tiles_n, tn = u % tiles_n, tmv = 2 * tm2 + (int)rank;
+          const int tm2 = u / tiles_c, tn = (u % tiles_c) * MC + mcg, tmv = 2 * tm2 + (int)rank;
           const int row0 = tmv * 128, col0 = tn * BN + (int)rank * (BN / 2);
           const bool first = u == clu;
+          // A of K block kb into stage slot sa (completion on lbar): MC = 2 loads half the rows
+          // and multicasts them to the same-rows CTA of the other pair
+          auto load_a = [&](uint8_t* sa, int kb, uint32_t lbar) {
+            if constexpr (MC > 1)
+              tma_load_3d_pair_mc(sa + mcg * 64 * 128, &tmA, kb * G::BK, row0 + mcg * 64, ac, lbar, amask);
+            else
+              tma_load_3d_pair(sa, &tmA, kb * G::BK, row0, ac, lbar);
+          };
           if (first) step_trace(sh, st, 0);
           int npre = 0, nind = 0;
           int s0 = stage;
@@ -829,7 +853,7 @@ __global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 
               if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE);
               const uint32_t lbar = mapa(smem_u32(&full[stage]), base);
               uint8_t* sa = smem + stage * G::STAGE;
-              tma_load_3d_pair(sa, &tmA, kb * G::BK, row0, ac, lbar);
+              load_a(sa, kb, lbar);
               tma_load_2d_pair(sa + G::A_BYTES, &tmB, kb * G::BK, col0, lbar);
               if (++stage == G::S) { stage = 0; ph ^= 1; }
             }
@@ -861,14 +885,14 @@ __global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 
             const int kb = ks + KS * i;
             if (i - nind < npre) {
               const int sidx = (s0 + i - nind) % G::S;
-              tma_load_3d_pair(smem + sidx * G::STAGE, &tmA, kb * G::BK, row0, ac, mapa(smem_u32(&full[sidx]), base));
+              load_a(smem + sidx * G::STAGE, kb, mapa(smem_u32(&full[sidx]), base));
               continue;
             }
             mbar_wait_sleep(&empty[stage], ph ^ 1);
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE);
             const uint32_t lbar = mapa(smem_u32(&full[stage]), base);
             uint8_t* sa = smem + stage * G::STAGE;
-            tma_load_3d_pair(sa, &tmA, kb * G::BK, row0, ac, lbar);
+            load_a(sa, kb, lbar);
             tma_load_2d_pair(sa + G::A_BYTES, &tmB, kb * G::BK, col0, lbar);
             if (++stage == G::S) { stage = 0; ph ^= 1; }
           }
@@ -884,6 +908,7 @@ __global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 
     if (leader && lane == 0) {
       constexpr uint32_t id = idesc(ELEM, 256, BN, false, false);
       const uint16_t pmask = (uint16_t)(3u << base);   // commits reach both CTAs of this pair
+      const uint16_t emask = MC > 1 ? (uint16_t)0xF : pmask;   // MC = 2: stage slots are shared by both pairs
       int stage = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       for (int st = 0; st < steps; ++st) {
@@ -902,7 +927,7 @@ __global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 
               for (int k = 0; k < G::BK / G::UK; ++k)
                 umma_ss_pair<ELEM>(d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), id,
                                    (i > 0 || k > 0) ? 1u : 0u);
-              umma_commit_pair(&empty[stage], pmask);
+              umma_commit_pair(&empty[stage], emask);
               if (++stage == G::S) { stage = 0; ph ^= 1; }
             }
           }
@@ -922,7 +947,7 @@ __global__ void __cluster_dims__(2 * KS, 1, 1) __launch_bounds__(64 + 128 * EW, 
     for (int st = 0; st < steps; ++st) {
       const bool kz = epi.k_empty(st);
       for (int u = clu; u < units; u += nclu) {
-        const int tm2 = u / tiles_n, tn = u % tiles_n, tmv = 2 * tm2 + (int)rank, tv = tn * KS + ks;
+        const int tm2 = u / tiles_c, tn = (u % tiles_c) * MC + mcg, tmv = 2 * tm2 + (int)rank, tv = tn * KS + ks;
         const int m = tmv * 128 + r;
         epi.begin_tile(es, st, tmv, tv, m);
         mbar_wait_sleep(&tfull[acc], aph);
@@ -1131,11 +1156,12 @@ int resident_clusters(K kern, const cudaLaunchConfig_t& cfg) {
 }
 
 // Cooperative launch of gemm_steps_pair_kernel: one CTA pair per 256-row tile, all resident.
-template <int ELEM, int BN, class Epi, int EW, int KS = 1>
+template <int ELEM, int BN, class Epi, int EW, int KS = 1, int MC = 1>
 int launch_steps_pair(const CUtensorMap& ta, const CUtensorMap& tb, const StepShape& sh, const Epi& epi,
                       cudaStream_t st) {
   using G = PairGeo<ELEM, BN, Epi, EW, KS>;
-  auto kern = gemm_steps_pair_kernel<ELEM, BN, Epi, EW, KS>;
+  auto kern = gemm_steps_pair_kernel<ELEM, BN, Epi, EW, KS, MC>;
+  if (((sh.N + BN - 1) / BN) % MC) return 3;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess)
@@ -1143,7 +1169,7 @@ int launch_steps_pair(const CUtensorMap& ta, const CUtensorMap& tb, const StepSh
     attr = true;
   }
   const int units = ((sh.M + 255) / 256) * ((sh.N + BN - 1) / BN);
-  if (2 * KS * units > num_sms()) return 3;
+  if (2 * KS * units > num_sms()) return 3;   // (units: pair tiles; MC pairs per cluster)
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute lattr[1];
   lattr[0].id = cudaLaunchAttributeCooperative;
@@ -1154,7 +1180,7 @@ int launch_steps_pair(const CUtensorMap& ta, const CUtensorMap& tb, const StepSh
   cfg.stream = st;
   cfg.attrs = lattr;
   cfg.numAttrs = 1;
-  if (units > resident_clusters(kern, cfg)) return 3;   // not all clusters co-resident
+  if (units / MC > resident_clusters(kern, cfg)) return 3;   // not all clusters co-resident
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, sh, epi) == cudaSuccess ? 0 : 2;
 }
 

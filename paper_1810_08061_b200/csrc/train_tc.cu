@@ -471,6 +471,11 @@ long long* trace_buf(int T) {
   return g_trace;
 }
 
+int fwd_mc() {   // SKB_TC_FWD_MC=1: forward A boxes multicast across two CTA pairs
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("SKB_TC_FWD_MC"); v = (e && atoi(e) == 1) ? 1 : 0; }
+  return v;
+}
 int pair_fwd() {
   static int v = -1;
   if (v < 0) { const char* e = getenv("SKB_TC_PAIR_FWD"); v = (e && atoi(e) == 0) ? 0 : 1; }
@@ -566,7 +571,13 @@ extern "C" int skb_train_tc_enqueue(const skb_train_shape* d, const float* x, co
       if (!gm::encode_2d(&mWUp, kBF16, w.WU, KX, G, KX, GF::BK, kFwdBN / 2) ||
           !gm::encode_3d(&mXHp, kBF16, w.XH, KX, B, T, KX, (uint64_t)B * KX, GF::BK, GF::BM, 1))
         return SKB_ERR_INVALID;
-      rc = gm::launch_steps_pair<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXHp, mWUp, sh, e, cs);
+      rc = 3;
+      if (fwd_mc()) {   // two pairs per cluster sharing each A box by multicast
+        CUtensorMap mXHh;
+        if (!gm::encode_3d(&mXHh, kBF16, w.XH, KX, B, T, KX, (uint64_t)B * KX, GF::BK, 64, 1)) return SKB_ERR_INVALID;
+        rc = gm::launch_steps_pair<kBF16, kFwdBN, EpiFwd, kFwdEW, 1, 2>(mXHh, mWUp, sh, e, cs);
+      }
+      if (rc == 3) rc = gm::launch_steps_pair<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXHp, mWUp, sh, e, cs);
       if (rc == 3) rc = gm::launch_steps<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXH, mWU, sh, e, cs);   // pairs not all resident
     } else {
       rc = gm::launch_steps<kBF16, kFwdBN, EpiFwd, kFwdEW>(mXH, mWU, sh, e, cs);

@@ -95,7 +95,7 @@ def test_sgd_step_and_replay():
 
 
 @pytest.mark.parametrize("env", [{"SKB_TC_FWD_KS": "2"}, {"SKB_TC_BWD_KS": "1"}, {"SKB_TC_PAIR_FWD": "0"},
-                                 {"SKB_TC_PAIR": "0"}, {"SKB_TC_BWD_KS": "2"}])
+                                 {"SKB_TC_PAIR": "0"}, {"SKB_TC_BWD_KS": "2"}, {"SKB_TC_FWD_MC": "1"}])
 def test_step_kernel_variants_match_oracle(env):
     """The C2 engine's alternative step kernels (split-K forward over a CTA cluster, 1-CTA
     backward tiles, 1-CTA forward tiles, 1-CTA gradient GEMM) against the oracle; the switches
